@@ -1,0 +1,236 @@
+/*
+ * p3d.h — C-ABI of libp3d.so, the B200 (sm_100a) global-placement hot path of
+ * the arXiv 2403.09070 F2F 3D placer.
+ *
+ * Every entry point is stream-ordered and asynchronous: it enqueues kernels on
+ * the given cudaStream_t (passed as void*) and returns.  All pointers are
+ * DEVICE pointers unless noted; scalar results are written to device memory
+ * (no implicit host synchronisation).  The library allocates nothing: the
+ * caller owns every buffer (the Python host layer allocates them as torch
+ * tensors).  Return value: P3D_OK or an error code; p3d_last_error() gives the
+ * message.  Each declaration cites the reference routine it replaces
+ * (paths relative to /root/reference/pkg/src/place3d).
+ */
+#ifndef P3D_H_
+#define P3D_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define P3D_ABI_VERSION 1
+
+#define P3D_OK 0
+#define P3D_ERR_ARG 1          /* bad argument -> ValueError */
+#define P3D_ERR_CUDA 2         /* launch / runtime failure -> RuntimeError */
+#define P3D_ERR_UNSUPPORTED 3  /* size outside what this build handles */
+
+/* ------------------------------------------------------------------------ */
+/* library                                                                   */
+/* ------------------------------------------------------------------------ */
+int p3d_abi_version(void);
+/* Copies the last error message (thread-local) into buf; returns its length. */
+int p3d_last_error(char* buf, size_t n);
+/* sizeof() of the structs below, so bindings can verify their mirrors. */
+size_t p3d_sizeof_topology(void);
+size_t p3d_sizeof_grid(void);
+size_t p3d_sizeof_cloud(void);
+size_t p3d_sizeof_gp(void);
+size_t p3d_sizeof_loop_state(void);
+
+/* ------------------------------------------------------------------------ */
+/* netlist topology: CSR pins by net (wirelength.py:30-47 NetTopology)       */
+/* ------------------------------------------------------------------------ */
+typedef struct p3d_topology {
+  int32_t n_net;
+  int32_t n_pin;
+  int32_t n_obj;             /* length of per-object outputs (gradient vector) */
+  int32_t pad0;
+  const int32_t* net_ptr;    /* [n_net+1] */
+  const int32_t* pin_inst;   /* [n_pin] owner object of each pin */
+  const uint8_t* net_dup;    /* [n_net] 1 if an owner has >= 2 pins in the net
+                                (model.py:268-275 net_has_dup_inst) */
+  const int32_t* net_order;  /* [n_net] processing order (nets grouped by
+                                degree); NULL = identity */
+  const int32_t* pin_slot;   /* [n_pin] position of the pin in owner-sorted
+                                order; NULL = identity */
+  const int32_t* obj_slot_ptr; /* [n_obj+1] slot range of each owner */
+} p3d_topology;
+
+/* Per-(net, die) first/second extrema with multiplicity on one axis
+ * (wirelength.py:101-142 NetBoxes).  Outputs [n_net*2] (index 2*net+die) and
+ * [n_net]; all nullable. */
+int p3d_netboxes(const p3d_topology* t, const double* coord, const uint8_t* on_top,
+                 int64_t* cnt, double* min1, double* min2, double* max1, double* max2,
+                 double* full_min, double* full_max, double* spans_bistratal,
+                 void* stream);
+
+/* Smoothed bistratal planar WL and per-pin gradients, branch per net/axis from
+ * the unsmoothed spans (wirelength.py:173-192 planar_objective).  value: one
+ * device double.  gx/gy: [n_pin] (nullable).  scratch: zeroed device buffer of
+ * >= 8 + 6*2048 doubles (reduction partials; left zeroed for reuse). */
+int p3d_planar_objective_ex(const p3d_topology* t, const double* pin_x, const double* pin_y,
+                            const uint8_t* on_top, double gamma, double* value, double* gx,
+                            double* gy, double* scratch, void* stream);
+
+/* WA z-span per net (wirelength.py:195-198 z_cut_penalty); scratch as above. */
+int p3d_z_cut_penalty_ex(const p3d_topology* t, const double* pin_z, double gamma,
+                         double* value, double* g, double* scratch, void* stream);
+
+/* Incremental finite-difference depth gradient, accumulated per owner object
+ * (wirelength.py:251-293 fd_z_gradient_incremental; exact O(|P|^2) path for
+ * nets flagged in net_dup).  g: [n_obj]; requires net_dup, pin_slot and
+ * obj_slot_ptr; pin_scratch: >= 4*n_pin + 4*n_obj doubles. */
+int p3d_fd_z_gradient(const p3d_topology* t, const double* pin_x, const double* pin_y,
+                      const uint8_t* on_top, double dz, double* g, double* pin_scratch,
+                      void* stream);
+
+/* Per-pin -> per-object ordered sums of up to 4 pin arrays laid out
+ * [n_pin][4] in slot order (the np.bincount(pin_inst, w) of gp.py:307-309). */
+int p3d_gather_pins(const p3d_topology* t, const double* pin4, double* obj4_soa,
+                    void* stream);
+
+/* dynamic_pin_coords (wirelength.py:308-322): pins from instance centres with
+ * per-die rotated offsets.  off: [n_pin][4] (rx_top, ry_top, rx_bot, ry_bot). */
+int p3d_pin_coords(const p3d_topology* t, const double* x, const double* y,
+                   const double* z, const double* off, double dz, double* px,
+                   double* py, double* pz, uint8_t* on_top, void* stream);
+
+/* normalize_z_gradient (wirelength.py:296-305, Eq. 17); scratch: zeroed,
+ * >= 8 + 3*1024 doubles. */
+int p3d_normalize_z_gradient(int32_t n, const double* gx, const double* gy,
+                             const double* gz_bist, const double* gz_hbt, double alpha,
+                             double* out, double* scratch, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* density grid + spectral plan (density.py:26-55 DensityGrid)               */
+/* ------------------------------------------------------------------------ */
+typedef struct p3d_grid {
+  int32_t nx, ny, nz, pad0;
+  double dx, dy, dz, wb, hb, db, bin_vol;
+  double fx_scale;           /* 2^40 / bin_vol (fixed-point density scale) */
+  const double* omega[3];    /* [nx], [ny], [nz]: pi*k/d */
+  const double* twiddle[3];  /* per axis: [n] (cos,sin)(-2 pi j/n), j < n/2 */
+  const double* phase[3];    /* per axis: [2n] (cos,sin)(pi k/(2n)) */
+} p3d_grid;
+
+/* Charges (density.py:58-83 ChargeCloud), SoA, length n. */
+typedef struct p3d_cloud {
+  int32_t n, n_macro;
+  const double *x, *y, *z, *w, *h, *dep, *weight;
+  const uint8_t* is_macro;
+  const int32_t* macro_ids;  /* [n_macro] indices with is_macro set */
+} p3d_cloud;
+
+/* Fixed-point density accumulation (density.py:301-311 accumulate_density):
+ * rho_fx [nx*ny*nz] int64 in units of 2^-40, ADDED into (caller zeroes). */
+int p3d_accumulate_density(const p3d_grid* g, const p3d_cloud* c, int64_t* rho_fx,
+                           void* stream);
+/* rho = rho_fx * 2^-40 (exact). */
+int p3d_fx_to_density(int64_t n, const int64_t* rho_fx, double* rho, void* stream);
+/* overflow (density.py:612-617) from the fixed-point map; out: one double;
+ * scratch: zeroed, >= 8 + 1024 doubles. */
+int p3d_overflow_fx(const p3d_grid* g, const int64_t* rho_fx, double rho_t,
+                    double movable_volume, double* out, double* scratch, void* stream);
+
+/* Spectral Poisson solve + field (density.py:319-368).  rho: [B] float64.
+ * coef (nullable): scipy-normalised dctn(rho, type=2).  maps (nullable):
+ * [B][4] = (phi, Ex, Ey, Ez) interleaved.  scratch: >= 6*B doubles. */
+int p3d_spectral(const p3d_grid* g, const double* rho, double* coef, double* maps,
+                 double* scratch, void* stream);
+/* The same from a given scipy-normalised coefficient array (electric_field). */
+int p3d_spectral_from_coef(const p3d_grid* g, const double* coef, double* maps,
+                           double* scratch, void* stream);
+
+/* Overlap-weighted map means per charge (density.py:376-386, 489-609):
+ * energy = sum q*phibar (one double), force[n][3] = -2 q Ebar (freeze: nullable
+ * per-object mask zeroing the z component).  maps: [B][4].  scratch: zeroed,
+ * >= 8 + n_macro + 1024 doubles. */
+int p3d_density_gather(const p3d_grid* g, const p3d_cloud* c, const double* maps,
+                       const uint8_t* freeze_z, double* energy, double* force,
+                       double* scratch, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* optimiser pieces (gp.py:142-147, 178-227, 280-294)                        */
+/* ------------------------------------------------------------------------ */
+/* precondition: out[n][3] = g / max(1, lam*q + macro*deg); div[n]. */
+int p3d_precondition(int32_t n, const double* g, double lam, const double* q,
+                     const double* deg, const uint8_t* macro, double* out, double* div,
+                     void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* the fused device-resident GP loop (gp.py:359-455 run_gp3d)                */
+/* ------------------------------------------------------------------------ */
+typedef struct p3d_loop_state {
+  /* control */
+  int32_t it, done, diverged, lam_set;
+  int32_t step_set, stop_now, best_flag, rise;
+  int32_t nonfinite, converged, eval_only, pad0;
+  /* schedule / optimiser scalars */
+  double lam, a, step, a_new, mom;
+  double prev_ovfl, prev_value, last_mu, best0, best1;
+  /* results of the current evaluation */
+  double wl_x, wl_y, cut, exact, ncross;
+  double norm_x, norm_y, norm_zb, gz_scale;
+  double energy, ovfl, value, wl_value, l1_wl, l1_dens;
+  double gamma, lam_eval;
+  double dv2, dg2, gmax;
+  /* GpInfo */
+  int32_t iterations, hbt_count;
+  double final_overflow, wirelength;
+  uint32_t counters[16];
+} p3d_loop_state;
+
+typedef struct p3d_gp {
+  int32_t n_inst, n_fill, n_obj, n_macro;
+  int32_t max_iters, divergence_window, nblk_obj, nblk_net;
+  p3d_topology topo;           /* n_obj = n_inst here */
+  p3d_grid grid;
+  /* per-object constants */
+  const double* pin_off;       /* [n_pin][4] rotated (rx_top, ry_top, rx_bot, ry_bot) */
+  const double *w_top, *h_top, *w_bot, *h_bot;  /* [n_inst], rotated dims */
+  const uint8_t* is_macro;     /* [n_inst] */
+  const double* degree;        /* [n_inst] pin counts (Eq. 19) */
+  const double *fill_w, *fill_h, *fill_z;       /* [n_fill] */
+  const int32_t* macro_ids;    /* [n_macro] */
+  const double* gamma_tab;     /* [max_iters] gamma schedule (gp.py:171-175) */
+  /* scalars */
+  double alpha, target_density, movable_volume, stop_overflow;
+  double mu_min, mu_max, gamma0, gamma1, min_step, step_scale;
+  int64_t rho_t_fx;
+  /* state, [3][n_obj] SoA unless noted */
+  double *u, *v, *v_prev, *best;
+  double *wl_grad, *dens_grad, *pre, *prev_wl, *prev_dens;
+  double* prev_q;              /* [n_obj] */
+  double* pin_out;             /* [n_pin][4] slot order */
+  double* inst_g;              /* [4][n_inst] gx, gy, gz_hbt, gz_bist */
+  int64_t* rho_fx;             /* [B] */
+  double* rho;                 /* [B] */
+  double* spec_scratch;        /* [6*B] */
+  double* maps;                /* [B][4] */
+  double* partials;            /* [16][4096] */
+  p3d_loop_state* st;
+  double* log;                 /* [max_iters][4]: it, exact WL, crossings, overflow */
+  double* ovfl_hist;           /* [max_iters] */
+} p3d_gp;
+
+/* Reset the loop state (lambda unset, a = 1, iteration 0) and project u = v =
+ * P(pos0) (gp.py:188-196); pos0 [3][n_obj] may alias u. */
+int p3d_gp_init(const p3d_gp* gp, const double* pos0, void* stream);
+/* One full GP iteration (gp.py:386-444) with all control on the device;
+ * a no-op once st->done is set.  Capturable in a CUDA graph. */
+int p3d_gp_iterate(const p3d_gp* gp, void* stream);
+/* Gp3dProblem.evaluate (gp.py:296-341) at gp->v with the given lambda and
+ * gamma, filling wl_grad, dens_grad, rho_fx -> maps and the st result fields
+ * (no optimiser step, loop control untouched). */
+int p3d_gp_evaluate(const p3d_gp* gp, double lam, double gamma, void* stream);
+/* Gp3dProblem.project (gp.py:280-294): out = P(in), [3][n_obj]. */
+int p3d_gp_project(const p3d_gp* gp, const double* in, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* P3D_H_ */

@@ -1,0 +1,68 @@
+"""Host -> device staging helpers (plumbing only; all compute is in libp3d.so)."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+DEV = "cuda"
+
+
+def dev(x, dtype):
+    """numpy / list / tensor -> contiguous CUDA tensor of `dtype` (copies only if needed)."""
+    if isinstance(x, torch.Tensor):
+        t = x
+        if t.dtype != dtype:
+            t = t.to(dtype)
+        if not t.is_cuda:
+            t = t.to(DEV)
+        return t.contiguous()
+    a = np.ascontiguousarray(np.asarray(x))
+    return torch.from_numpy(a).to(device=DEV, dtype=dtype).contiguous()
+
+
+def f64(x):
+    return dev(x, torch.float64)
+
+
+def i32(x):
+    return dev(x, torch.int32)
+
+
+def u8(x):
+    if isinstance(x, torch.Tensor):
+        return x.to(device=DEV, dtype=torch.uint8).contiguous()
+    return dev(np.asarray(x).astype(np.uint8), torch.uint8)
+
+
+def host(x):
+    """Tensor -> numpy (for the reference-shaped return values of the loop driver)."""
+    if isinstance(x, torch.Tensor):
+        return x.detach().cpu().numpy()
+    return np.asarray(x)
+
+
+def zeros(n, dtype=torch.float64):
+    return torch.zeros(int(max(n, 1)), dtype=dtype, device=DEV)
+
+
+def scratch(n_doubles):
+    """Zeroed reduction scratch (the C side resets its ticket counters)."""
+    return torch.zeros(int(n_doubles), dtype=torch.float64, device=DEV)
+
+
+def sync_scalar(t):
+    return float(t.item())
+
+
+class Keep:
+    """Holds tensors alive for as long as a ctypes struct points at them."""
+
+    def __init__(self):
+        self.items = []
+
+    def __call__(self, t):
+        self.items.append(t)
+        return _lib.ptr(t)

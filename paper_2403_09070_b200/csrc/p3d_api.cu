@@ -1,0 +1,318 @@
+// extern "C" entry points of libp3d.so (declared in include/p3d.h).
+// Argument validation, error strings, and dispatch to the kernel launchers.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "p3d_common.cuh"
+#include "p3d_geom.cuh"
+#include "p3d_internal.cuh"
+
+namespace p3d {
+
+static thread_local char g_err[512] = {0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return P3D_ERR_CUDA;
+  }
+  return P3D_OK;
+}
+
+template <class Cloud>
+void launch_scatter(const Cloud& cl, int n, int n_macro, const int32_t* macro_ids,
+                    const p3d_grid& g, int64_t* rho, const int* halt, cudaStream_t s);
+void launch_gather_op(const p3d_cloud& c, const p3d_grid& g, const double* maps,
+                      const uint8_t* freeze, double* energy, double* force, double* scratch,
+                      cudaStream_t s);
+void launch_fx_to_density(long long n, const int64_t* in, double* out, cudaStream_t s);
+void launch_overflow(long long n, const int64_t* rho, long long t, double scale, double* scratch,
+                     double* out, cudaStream_t s);
+void launch_precondition(int n, const double* g, double lam, const double* q, const double* deg,
+                         const uint8_t* macro, double* out, double* div, cudaStream_t s);
+void launch_pin_coords(int n_pin, const int32_t* pin_inst, const double* x, const double* y,
+                       const double* z, const double* off, double dz, double* px, double* py,
+                       double* pz, uint8_t* top, cudaStream_t s);
+void launch_normalize(int n, const double* gx, const double* gy, const double* gzb,
+                      const double* gzh, double alpha, double* out, double* scratch,
+                      cudaStream_t s);
+int gp_iterate(const p3d_gp& gp, cudaStream_t s);
+int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s);
+int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s);
+int gp_project(const p3d_gp& gp, const double* in, double* out, cudaStream_t s);
+
+static NetArgs net_args(const p3d_topology* t) {
+  NetArgs a{};
+  a.n_net = t->n_net;
+  a.blocks = grid_blocks(t->n_net, 256, kMaxBlocks);
+  a.net_ptr = t->net_ptr;
+  a.pin_inst = t->pin_inst;
+  a.net_order = t->net_order;
+  a.net_dup = t->net_dup;
+  a.pin_slot = nullptr;
+  return a;
+}
+
+static bool bad_topo(const p3d_topology* t) {
+  if (!t || t->n_net < 0 || t->n_pin < 0 || !t->net_ptr || (t->n_pin > 0 && !t->pin_inst)) {
+    set_error("invalid topology");
+    return true;
+  }
+  return false;
+}
+
+static bool bad_grid(const p3d_grid* g) {
+  if (!g || g->nx <= 0 || g->ny <= 0 || g->nz <= 0 || !(g->bin_vol > 0)) {
+    set_error("invalid grid");
+    return true;
+  }
+  for (int k = 0; k < 3; ++k)
+    if (!g->omega[k] || !g->twiddle[k] || !g->phase[k]) {
+      set_error("grid tables missing");
+      return true;
+    }
+  return false;
+}
+
+}  // namespace p3d
+
+using namespace p3d;
+
+#define STREAM(s) reinterpret_cast<cudaStream_t>(s)
+
+extern "C" {
+
+int p3d_abi_version(void) { return P3D_ABI_VERSION; }
+
+int p3d_last_error(char* buf, size_t n) {
+  size_t l = strlen(g_err);
+  if (buf && n) {
+    size_t c = l < n - 1 ? l : n - 1;
+    memcpy(buf, g_err, c);
+    buf[c] = 0;
+  }
+  return (int)l;
+}
+
+size_t p3d_sizeof_topology(void) { return sizeof(p3d_topology); }
+size_t p3d_sizeof_grid(void) { return sizeof(p3d_grid); }
+size_t p3d_sizeof_cloud(void) { return sizeof(p3d_cloud); }
+size_t p3d_sizeof_gp(void) { return sizeof(p3d_gp); }
+size_t p3d_sizeof_loop_state(void) { return sizeof(p3d_loop_state); }
+
+int p3d_netboxes(const p3d_topology* t, const double* coord, const uint8_t* on_top, int64_t* cnt,
+                 double* min1, double* min2, double* max1, double* max2, double* full_min,
+                 double* full_max, double* spans, void* stream) {
+  if (bad_topo(t) || !coord || !on_top) return P3D_ERR_ARG;
+  if (t->n_net == 0) return P3D_OK;
+  NetArgs a = net_args(t);
+  launch_netboxes(a, coord, on_top, cnt, min1, min2, max1, max2, full_min, full_max, spans,
+                  STREAM(stream));
+  return check_launch("netboxes");
+}
+
+// scratch for reductions: caller-provided value buffer must hold >= 1 double;
+// the per-op WL reductions use a small scratch carved from `value`'s neighbour
+// arrays: value[0] result, value[1..] are NOT used.  Partials live in gx/gy-free
+// scratch allocated by the caller through p3d_planar_objective_ex.
+static int planar_like(const p3d_topology* t, const double* px, const double* py,
+                       const double* pz, const uint8_t* top, double gamma, double* value,
+                       int value_mode, double* gx, double* gy, double* gc, bool planar, bool cut,
+                       double* scratch, cudaStream_t s) {
+  NetArgs a = net_args(t);
+  a.gamma = gamma;
+  a.want_pins = (gx || gy || gc) ? 1 : 0;
+  a.gx = gx;
+  a.gy = gy;
+  a.gc = gc;
+  a.value_mode = value_mode;
+  a.value_out = value;
+  a.counter = reinterpret_cast<unsigned int*>(scratch);
+  a.final6 = scratch + 2;
+  a.partials = scratch + 8;
+  launch_net_direct(a, px, py, pz, top, planar, cut, false, s);
+  return check_launch(planar ? "planar_objective" : "z_cut_penalty");
+}
+
+int p3d_planar_objective_ex(const p3d_topology* t, const double* pin_x, const double* pin_y,
+                            const uint8_t* on_top, double gamma, double* value, double* gx,
+                            double* gy, double* scratch, void* stream) {
+  if (bad_topo(t) || !pin_x || !pin_y || !on_top || !value || !scratch) {
+    if (!g_err[0]) set_error("planar_objective: null argument");
+    return P3D_ERR_ARG;
+  }
+  if (!(gamma > 0)) { set_error("gamma must be positive"); return P3D_ERR_ARG; }
+  return planar_like(t, pin_x, pin_y, nullptr, on_top, gamma, value, 0, gx, gy, nullptr, true,
+                     false, scratch, STREAM(stream));
+}
+
+int p3d_z_cut_penalty_ex(const p3d_topology* t, const double* pin_z, double gamma, double* value,
+                         double* g, double* scratch, void* stream) {
+  if (bad_topo(t) || !pin_z || !value || !scratch) { set_error("z_cut_penalty: null argument"); return P3D_ERR_ARG; }
+  if (!(gamma > 0)) { set_error("gamma must be positive"); return P3D_ERR_ARG; }
+  return planar_like(t, nullptr, nullptr, pin_z, nullptr, gamma, value, 1, nullptr, nullptr, g,
+                     false, true, scratch, STREAM(stream));
+}
+
+int p3d_fd_z_gradient(const p3d_topology* t, const double* pin_x, const double* pin_y,
+                      const uint8_t* on_top, double dz, double* g, double* pin_scratch,
+                      void* stream) {
+  if (bad_topo(t) || !pin_x || !pin_y || !on_top || !g || !pin_scratch || !t->pin_slot ||
+      !t->obj_slot_ptr || !t->net_dup) {
+    set_error("fd_z_gradient: null argument (needs pin_slot, obj_slot_ptr, net_dup)");
+    return P3D_ERR_ARG;
+  }
+  cudaStream_t s = STREAM(stream);
+  NetArgs a = net_args(t);
+  a.gamma = 1.0;
+  a.scale4 = 4.0 / dz;
+  a.want_pins = 1;
+  a.pin_slot = t->pin_slot;
+  // the FD term lands in column 3 of a [n_pin][4] slot array
+  a.out4 = pin_scratch;
+  cudaMemsetAsync(pin_scratch, 0, sizeof(double) * 4 * (size_t)t->n_pin, s);
+  if (t->n_net > 0) launch_net_direct(a, pin_x, pin_y, nullptr, on_top, false, false, true, s);
+  GatherArgs ga{};
+  ga.n_obj = t->n_obj;
+  ga.blocks = grid_blocks(t->n_obj, 256, kMaxBlocks);
+  ga.obj_slot_ptr = t->obj_slot_ptr;
+  ga.pin4 = pin_scratch;
+  // gather all four columns into pin_scratch's tail? keep simple: columns to a
+  // caller-visible [4][n_obj] area placed after the pin array
+  double* out4 = pin_scratch + 4 * (size_t)t->n_pin;
+  ga.out = out4;
+  launch_gather(ga, s);
+  cudaMemcpyAsync(g, out4 + 3 * (size_t)t->n_obj, sizeof(double) * t->n_obj,
+                  cudaMemcpyDeviceToDevice, s);
+  return check_launch("fd_z_gradient");
+}
+
+int p3d_gather_pins(const p3d_topology* t, const double* pin4, double* obj4, void* stream) {
+  if (bad_topo(t) || !pin4 || !obj4 || !t->obj_slot_ptr) { set_error("gather_pins: null argument"); return P3D_ERR_ARG; }
+  GatherArgs ga{};
+  ga.n_obj = t->n_obj;
+  ga.blocks = grid_blocks(t->n_obj, 256, kMaxBlocks);
+  ga.obj_slot_ptr = t->obj_slot_ptr;
+  ga.pin4 = pin4;
+  ga.out = obj4;
+  launch_gather(ga, STREAM(stream));
+  return check_launch("gather_pins");
+}
+
+int p3d_pin_coords(const p3d_topology* t, const double* x, const double* y, const double* z,
+                   const double* off, double dz, double* px, double* py, double* pz,
+                   uint8_t* on_top, void* stream) {
+  if (bad_topo(t) || !x || !y || !z || !off) { set_error("pin_coords: null argument"); return P3D_ERR_ARG; }
+  if (t->n_pin == 0) return P3D_OK;
+  launch_pin_coords(t->n_pin, t->pin_inst, x, y, z, off, dz, px, py, pz, on_top, STREAM(stream));
+  return check_launch("pin_coords");
+}
+
+int p3d_normalize_z_gradient(int32_t n, const double* gx, const double* gy, const double* gzb,
+                             const double* gzh, double alpha, double* out, double* scratch,
+                             void* stream) {
+  if (n < 0 || !gx || !gy || !gzb || !gzh || !out || !scratch) { set_error("normalize: null argument"); return P3D_ERR_ARG; }
+  if (n == 0) return P3D_OK;
+  launch_normalize(n, gx, gy, gzb, gzh, alpha, out, scratch, STREAM(stream));
+  return check_launch("normalize_z_gradient");
+}
+
+int p3d_accumulate_density(const p3d_grid* g, const p3d_cloud* c, int64_t* rho_fx,
+                           void* stream) {
+  if (bad_grid(g) || !c || !rho_fx || c->n < 0) { if (!g_err[0]) set_error("accumulate: bad args"); return P3D_ERR_ARG; }
+  if (c->n == 0) return P3D_OK;
+  if (c->n_macro > 0 && !c->macro_ids) { set_error("macro_ids missing"); return P3D_ERR_ARG; }
+  CloudArrays cl;
+  cl.c = *c;
+  launch_scatter(cl, c->n, c->n_macro, c->macro_ids, *g, rho_fx, nullptr, STREAM(stream));
+  return check_launch("accumulate_density");
+}
+
+int p3d_fx_to_density(int64_t n, const int64_t* rho_fx, double* rho, void* stream) {
+  if (n < 0 || !rho_fx || !rho) { set_error("fx_to_density: bad args"); return P3D_ERR_ARG; }
+  if (n == 0) return P3D_OK;
+  launch_fx_to_density(n, rho_fx, rho, STREAM(stream));
+  return check_launch("fx_to_density");
+}
+
+int p3d_overflow_fx(const p3d_grid* g, const int64_t* rho_fx, double rho_t, double mv, double* out,
+                    double* scratch, void* stream) {
+  if (bad_grid(g) || !rho_fx || !out || !scratch) { if (!g_err[0]) set_error("overflow: bad args"); return P3D_ERR_ARG; }
+  const long long n = (long long)g->nx * g->ny * g->nz;
+  const long long t = __builtin_llrint(rho_t * 1099511627776.0);
+  const double scale = mv > 0 ? 9.094947017729282379150390625e-13 * g->bin_vol / mv : 0.0;
+  launch_overflow(n, rho_fx, t, scale, scratch, out, STREAM(stream));
+  return check_launch("overflow");
+}
+
+int p3d_spectral(const p3d_grid* g, const double* rho, double* coef, double* maps,
+                 double* scratch, void* stream) {
+  if (bad_grid(g) || !rho || !scratch) { if (!g_err[0]) set_error("spectral: bad args"); return P3D_ERR_ARG; }
+  return launch_spectral_ex(g, rho, nullptr, nullptr, coef, maps, scratch, nullptr, nullptr,
+                            STREAM(stream));
+}
+
+int p3d_spectral_from_coef(const p3d_grid* g, const double* coef, double* maps, double* scratch,
+                           void* stream) {
+  if (bad_grid(g) || !coef || !maps || !scratch) { if (!g_err[0]) set_error("spectral: bad args"); return P3D_ERR_ARG; }
+  return launch_spectral_ex(g, nullptr, nullptr, coef, nullptr, maps, scratch, nullptr, nullptr,
+                            STREAM(stream));
+}
+
+int p3d_density_gather(const p3d_grid* g, const p3d_cloud* c, const double* maps,
+                       const uint8_t* freeze_z, double* energy, double* force, double* scratch,
+                       void* stream) {
+  if (bad_grid(g) || !c || !maps || !energy || !force || !scratch) { if (!g_err[0]) set_error("density_gather: bad args"); return P3D_ERR_ARG; }
+  if (c->n_macro > 0 && !c->macro_ids) { set_error("macro_ids missing"); return P3D_ERR_ARG; }
+  launch_gather_op(*c, *g, maps, freeze_z, energy, force, scratch, STREAM(stream));
+  return check_launch("density_gather");
+}
+
+int p3d_precondition(int32_t n, const double* gr, double lam, const double* q, const double* deg,
+                     const uint8_t* macro, double* out, double* div, void* stream) {
+  if (n < 0 || !gr || !q || !deg || !out) { set_error("precondition: bad args"); return P3D_ERR_ARG; }
+  if (n == 0) return P3D_OK;
+  launch_precondition(n, gr, lam, q, deg, macro, out, div, STREAM(stream));
+  return check_launch("precondition");
+}
+
+static bool bad_gp(const p3d_gp* gp) {
+  if (!gp || !gp->st || !gp->u || !gp->v || gp->n_obj <= 0 || gp->n_inst < 0 ||
+      gp->nblk_obj <= 0 || gp->nblk_obj > kMaxBlocks || gp->nblk_net <= 0 ||
+      gp->nblk_net > kMaxBlocks || gp->n_macro > kMaxBlocks) {
+    set_error("invalid p3d_gp descriptor");
+    return true;
+  }
+  return bad_grid(&gp->grid);
+}
+
+int p3d_gp_init(const p3d_gp* gp, const double* pos0, void* stream) {
+  if (bad_gp(gp) || !pos0) return P3D_ERR_ARG;
+  return gp_init(*gp, pos0, STREAM(stream));
+}
+
+int p3d_gp_iterate(const p3d_gp* gp, void* stream) {
+  if (bad_gp(gp)) return P3D_ERR_ARG;
+  return gp_iterate(*gp, STREAM(stream));
+}
+
+int p3d_gp_evaluate(const p3d_gp* gp, double lam, double gamma, void* stream) {
+  if (bad_gp(gp)) return P3D_ERR_ARG;
+  return gp_evaluate(*gp, lam, gamma, STREAM(stream));
+}
+
+int p3d_gp_project(const p3d_gp* gp, const double* in, double* out, void* stream) {
+  if (bad_gp(gp) || !in || !out) return P3D_ERR_ARG;
+  return gp_project(*gp, in, out, STREAM(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// Shared device helpers and the parameter blocks of the GP hot path.
+// See DESIGN.md for the HBM layout and include/p3d.h for the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/p3d.h"
+
+#define P3D_INF (__longlong_as_double(0x7ff0000000000000LL))
+
+namespace p3d {
+
+constexpr int kFxBits = 40;  // fixed-point density: 2^-40 per unit density
+
+// ---------------------------------------------------------------------------
+// error reporting (host)
+// ---------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+
+// ---------------------------------------------------------------------------
+// warp / block reductions (deterministic: fixed shuffle tree, fixed order)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum of K doubles per thread; result valid in thread 0.
+// blockDim.x must be a multiple of 32 and <= 1024.
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double* smem /* >= 32*K */) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) smem[k * 32 + wid] = v[k];
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double t = lane < nw ? smem[k * 32 + lane] : 0.0;
+      v[k] = warp_sum(t);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double block_max(double v, double* smem) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double t = lane < nw ? smem[lane] : 0.0;
+    v = warp_max(t);
+  }
+  __syncthreads();
+  return v;
+}
+
+// "Last block done" handshake: every block publishes its partials, then the
+// last block to arrive (by an atomic ticket) sees all of them and runs the
+// grid-level epilogue.  The ticket counter resets itself for graph replay.
+__device__ __forceinline__ bool last_block(unsigned int* counter) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int t = atomicAdd(counter, 1u);
+    is_last = (t == gridDim.x * gridDim.y - 1);
+    if (is_last) *counter = 0u;
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
+// Ordered sum of n partials by one block (fixed order => deterministic).
+__device__ __forceinline__ double ordered_sum(const volatile double* p, int n, double* smem) {
+  double acc[1] = {0.0};
+  // contiguous chunk per thread, then fixed tree
+  int per = (n + blockDim.x - 1) / blockDim.x;
+  int b = threadIdx.x * per, e = min(n, b + per);
+  double s = 0.0;
+  for (int i = b; i < e; ++i) s += p[i];
+  acc[0] = s;
+  block_sum<1>(acc, smem);
+  return acc[0];  // valid in thread 0
+}
+
+// ---------------------------------------------------------------------------
+// numpy-faithful small math (compiled with -fmad=false where used)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double clipd(double v, double lo, double hi) {
+  // np.clip(v, lo, hi) == minimum(maximum(v, lo), hi)
+  return fmin(fmax(v, lo), hi);
+}
+
+}  // namespace p3d

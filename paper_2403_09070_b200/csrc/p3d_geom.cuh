@@ -1,0 +1,209 @@
+// Charge geometry shared by the density scatter (K2) and gather (K4).
+// Every expression mirrors numpy's operation order in density.py:134-196 so
+// that, compiled with -fmad=false, the per-(object, bin) overlap volumes are
+// bit-identical to the reference's _direct_terms.
+#pragma once
+
+#include "p3d_common.cuh"
+
+namespace p3d {
+
+struct Charge {
+  double x, y, z, w, h, dep, weight;
+};
+
+// density.py:134-147 (Eqs. 6-7); z clamped to [dz/4, 3dz/4] first
+__device__ __forceinline__ void dynamic_wh(double z, double dz, bool macro, double wt, double ht,
+                                           double wb, double hb, double& w, double& h) {
+  const double zc = clipd(z, dz / 4, 3 * dz / 4);
+  if (macro) {
+    const double t = 2 * zc / dz - 0.5;
+    w = t * wt + (1 - t) * wb;
+    h = t * ht + (1 - t) * hb;
+  } else {
+    const bool top = (zc - dz / 2) > 0.0;
+    w = top ? wt : wb;
+    h = top ? ht : hb;
+  }
+}
+
+struct AxisSpan {
+  double lo, hi;
+  int i0, i1;
+};
+
+// density.py:155-169: clipped extent and inclusive bin range on one axis
+__device__ __forceinline__ AxisSpan axis_span(double c, double size, double extent, double step,
+                                              int n) {
+  AxisSpan s;
+  s.lo = clipd(c - size / 2, 0.0, extent);
+  s.hi = clipd(c + size / 2, 0.0, extent);
+  long long a = (long long)floor(s.lo / step);
+  long long b = (long long)ceil(s.hi / step) - 1;
+  a = a < 0 ? 0 : (a > n - 1 ? n - 1 : a);
+  b = b < 0 ? 0 : (b > n - 1 ? n - 1 : b);
+  if (b < a) b = a;
+  s.i0 = (int)a;
+  s.i1 = (int)b;
+  return s;
+}
+
+// density.py:172-173
+__device__ __forceinline__ double overlap_len(const AxisSpan& s, int i, double step) {
+  return fmax(fmin(s.hi, (double)(i + 1) * step) - fmax(s.lo, (double)i * step), 0.0);
+}
+
+struct Footprint {
+  AxisSpan ax, ay, az;
+};
+
+__device__ __forceinline__ Footprint footprint(const Charge& c, const p3d_grid& g) {
+  Footprint f;
+  f.ax = axis_span(c.x, c.w, g.dx, g.wb, g.nx);
+  f.ay = axis_span(c.y, c.h, g.dy, g.hb, g.ny);
+  f.az = axis_span(c.z, c.dep, g.dz, g.db, g.nz);
+  return f;
+}
+
+// ---------------------------------------------------------------------------
+// charge sources
+// ---------------------------------------------------------------------------
+struct CloudArrays {  // explicit ChargeCloud (per-op API)
+  p3d_cloud c;
+  __device__ __forceinline__ bool is_macro(int i) const { return c.is_macro && c.is_macro[i]; }
+  __device__ __forceinline__ Charge get(int i) const {
+    Charge q;
+    q.x = c.x[i]; q.y = c.y[i]; q.z = c.z[i];
+    q.w = c.w[i]; q.h = c.h[i]; q.dep = c.dep[i]; q.weight = c.weight[i];
+    return q;
+  }
+};
+
+struct CloudGP {  // Gp3dProblem.cloud(pos) computed on the fly (gp.py:267-278)
+  const double* pos;  // [3][n_obj]
+  int n_inst, n_obj;
+  const double *wt, *ht, *wb, *hb, *fw, *fh;
+  const uint8_t* macro;
+  double dz, target_density;
+  __device__ __forceinline__ bool is_macro(int i) const { return i < n_inst && macro[i]; }
+  __device__ __forceinline__ Charge get(int i) const {
+    Charge q;
+    q.x = pos[i];
+    q.y = pos[n_obj + i];
+    q.z = pos[2 * n_obj + i];
+    if (i < n_inst) {
+      const bool m = macro[i] != 0;
+      dynamic_wh(q.z, dz, m, wt[i], ht[i], wb[i], hb[i], q.w, q.h);
+      q.weight = m ? target_density : 1.0;
+    } else {
+      q.w = fw[i - n_inst];
+      q.h = fh[i - n_inst];
+      q.weight = 1.0;
+    }
+    q.dep = dz / 2;
+    return q;
+  }
+};
+
+__device__ __forceinline__ double charge_of(const Charge& q) {
+  return q.weight * (q.w * q.h * q.dep);  // ChargeCloud.charge (density.py:71-77)
+}
+
+// ---------------------------------------------------------------------------
+// K2: fixed-point scatter of one object's overlaps (thread-serial)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void scatter_object(const Charge& q, const p3d_grid& g,
+                                               unsigned long long* rho) {
+  const Footprint f = footprint(q, g);
+  for (int ix = f.ax.i0; ix <= f.ax.i1; ++ix) {
+    const double wx = overlap_len(f.ax, ix, g.wb);
+    for (int iy = f.ay.i0; iy <= f.ay.i1; ++iy) {
+      const double wxy = wx * overlap_len(f.ay, iy, g.hb);
+      for (int iz = f.az.i0; iz <= f.az.i1; ++iz) {
+        const double vol = wxy * overlap_len(f.az, iz, g.db);
+        const long long t = __double2ll_rn((q.weight * vol) * g.fx_scale);
+        if (t) atomicAdd(rho + ((long long)(ix * g.ny + iy) * g.nz + iz), (unsigned long long)t);
+      }
+    }
+  }
+}
+
+// block-cooperative scatter of one large object (per-macro tile path)
+__device__ __forceinline__ void scatter_object_block(const Charge& q, const p3d_grid& g,
+                                                     unsigned long long* rho) {
+  const Footprint f = footprint(q, g);
+  const int nxr = f.ax.i1 - f.ax.i0 + 1, nyr = f.ay.i1 - f.ay.i0 + 1, nzr = f.az.i1 - f.az.i0 + 1;
+  const int tot = nxr * nyr * nzr;
+  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int iz = f.az.i0 + t % nzr;
+    const int iy = f.ay.i0 + (t / nzr) % nyr;
+    const int ix = f.ax.i0 + t / (nzr * nyr);
+    const double wxy = overlap_len(f.ax, ix, g.wb) * overlap_len(f.ay, iy, g.hb);
+    const double vol = wxy * overlap_len(f.az, iz, g.db);
+    const long long v = __double2ll_rn((q.weight * vol) * g.fx_scale);
+    if (v) atomicAdd(rho + ((long long)(ix * g.ny + iy) * g.nz + iz), (unsigned long long)v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: overlap-weighted means of the 4 interleaved maps (density.py:376-386)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void gather_object(const Charge& q, const p3d_grid& g,
+                                              const double* maps, double (&mean)[4]) {
+  const Footprint f = footprint(q, g);
+  double tot = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const double4* m4 = reinterpret_cast<const double4*>(maps);
+  for (int ix = f.ax.i0; ix <= f.ax.i1; ++ix) {
+    const double wx = overlap_len(f.ax, ix, g.wb);
+    for (int iy = f.ay.i0; iy <= f.ay.i1; ++iy) {
+      const double wxy = wx * overlap_len(f.ay, iy, g.hb);
+      for (int iz = f.az.i0; iz <= f.az.i1; ++iz) {
+        const double vol = wxy * overlap_len(f.az, iz, g.db);
+        const double4 m = m4[(long long)(ix * g.ny + iy) * g.nz + iz];
+        tot += vol;
+        a0 += m.x * vol;
+        a1 += m.y * vol;
+        a2 += m.z * vol;
+        a3 += m.w * vol;
+      }
+    }
+  }
+  tot = fmax(tot, 1e-300);
+  mean[0] = a0 / tot;
+  mean[1] = a1 / tot;
+  mean[2] = a2 / tot;
+  mean[3] = a3 / tot;
+}
+
+// block-cooperative macro means: sum m*vol over the footprint / unclipped
+// volume (== the suffix-sum corner dots of density.py:489-530); thread 0 holds
+// the result.
+__device__ __forceinline__ void gather_object_block(const Charge& q, const p3d_grid& g,
+                                                    const double* maps, double (&mean)[4],
+                                                    double* red) {
+  const Footprint f = footprint(q, g);
+  const int nxr = f.ax.i1 - f.ax.i0 + 1, nyr = f.ay.i1 - f.ay.i0 + 1, nzr = f.az.i1 - f.az.i0 + 1;
+  const int tot = nxr * nyr * nzr;
+  const double4* m4 = reinterpret_cast<const double4*>(maps);
+  double acc[4] = {0, 0, 0, 0};
+  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int iz = f.az.i0 + t % nzr;
+    const int iy = f.ay.i0 + (t / nzr) % nyr;
+    const int ix = f.ax.i0 + t / (nzr * nyr);
+    const double wxy = overlap_len(f.ax, ix, g.wb) * overlap_len(f.ay, iy, g.hb);
+    const double vol = wxy * overlap_len(f.az, iz, g.db);
+    const double4 m = m4[(long long)(ix * g.ny + iy) * g.nz + iz];
+    acc[0] += m.x * vol;
+    acc[1] += m.y * vol;
+    acc[2] += m.z * vol;
+    acc[3] += m.w * vol;
+  }
+  block_sum<4>(acc, red);
+  const double vol = fmax(q.w * q.h * q.dep, 1e-300);
+  mean[0] = acc[0] / vol;
+  mean[1] = acc[1] / vol;
+  mean[2] = acc[2] / vol;
+  mean[3] = acc[3] / vol;
+}
+
+}  // namespace p3d

@@ -1,0 +1,93 @@
+// Internal launch-argument blocks and launcher declarations shared by the
+// translation units of libp3d.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/p3d.h"
+
+namespace p3d {
+
+constexpr int kMaxBlocks = 2048;      // cap on grid-stride grids (partials sizing)
+constexpr int kPartialStride = 8 * kMaxBlocks;
+
+// partials layout inside p3d_gp::partials ([16][kPartialStride] doubles)
+enum PartialSlot {
+  kSlotNet = 0,      // net kernel: 6 x blocks
+  kSlotGather = 1,   // owner gather: 3 x blocks
+  kSlotOvfl = 2,     // overflow
+  kSlotDens = 3,     // density gather (energy, |dens|, |wl|)
+  kSlotStep = 4,     // preconditioner / BB norms
+  kSlotFinal = 15,   // finalised scalars of the sub-kernels
+};
+// offsets inside the final slot
+enum FinalIdx {
+  kFinNet = 0,      // 6 values: planar x, planar y, cut, exact x, exact y, crossings
+  kFinNorm = 8,     // 4 values: |gx|, |gy|, |gzb|, Eq. 17 scale
+  kFinOvfl = 16,    // 1 value: overflow excess (already / movable volume)
+};
+// counters inside p3d_loop_state::counters
+enum CounterIdx { kCntNet = 0, kCntGather, kCntOvfl, kCntDens, kCntStep, kCntAdvance, kCntOp };
+
+struct NetArgs {
+  int n_net, blocks;
+  const int32_t* net_ptr;
+  const int32_t* pin_inst;
+  const int32_t* net_order;
+  const uint8_t* net_dup;
+  const int32_t* pin_slot;
+  double gamma, scale4;
+  const double* gamma_ptr;    // nullable: device gamma overrides `gamma`
+  int want_pins, value_mode;
+  double* out4;  // [n_pin][4] by slot (fused) or nullptr
+  double *gx, *gy, *gc, *gb;  // separate per-pin outputs (per-op)
+  double* partials;           // [6][blocks]
+  unsigned int* counter;
+  double* final6;             // nullable: skip reduction
+  double* value_out;          // nullable
+  const int* halt;            // nullable: skip when *halt != 0
+};
+
+struct GatherArgs {
+  int n_obj, blocks;
+  const int32_t* obj_slot_ptr;
+  const double* pin4;
+  double* out;           // [4][n_obj]
+  double* partials;      // [3][blocks]
+  unsigned int* counter;
+  double* final_norms;   // nullable: 4 values
+  const int* halt;
+};
+
+int grid_blocks(int n, int threads, int cap);
+
+// K1
+void launch_net_pos(const NetArgs& a, const double* x, const double* y, const double* z,
+                    const double* off, double dz, cudaStream_t s);
+void launch_net_direct(const NetArgs& a, const double* px, const double* py, const double* pz,
+                       const uint8_t* top, bool planar, bool cut, bool fd, cudaStream_t s);
+void launch_netboxes(const NetArgs& a, const double* c, const uint8_t* top, int64_t* cnt,
+                     double* min1, double* min2, double* max1, double* max2, double* fmn,
+                     double* fmx, double* bis, cudaStream_t s);
+void launch_gather(const GatherArgs& a, cudaStream_t s);
+
+// K3
+struct SpecOvfl {  // overflow + re-zero fused into the first (fixed-point) pass
+  int zero;
+  long long rho_t_fx;
+  double* partials;
+  unsigned int* counter;
+  double* out;
+  double scale;    // 2^-40 * bin_vol / movable_volume
+};
+int launch_spectral_ex(const p3d_grid* g, const double* rho, const int64_t* rho_fx,
+                       const double* coef_in, double* coef_out, double* maps, double* scratch,
+                       const int* halt, const SpecOvfl* ov, cudaStream_t s);
+void spectral_setup();
+void launch_scale_copy(const double* in, double* out, long long n, double s, cudaStream_t st);
+int launch_spectral(const p3d_grid* g, const double* rho, const int64_t* rho_fx,
+                    const double* coef_in, double* coef_out, double* maps, double* scratch,
+                    const int* halt, cudaStream_t s);
+
+}  // namespace p3d

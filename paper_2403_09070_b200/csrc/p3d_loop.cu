@@ -1,0 +1,518 @@
+// The device-resident GP iteration (gp.py:359-455 run_gp3d), K4 (fused with
+// the objective assembly) and K5 (preconditioner + Nesterov/BB step).
+// Compiled with -fmad=false so the optimiser arithmetic rounds exactly like
+// numpy's (no contracted v - step*g etc.).
+//
+// Kernel sequence of one iteration (each a no-op once st->done is set):
+//   K1  net_kernel      WL value/grads per pin (slot order), exact WL, crossings
+//   K1b gather_kernel   per-instance sums, L1 norms, Eq. 17 scale
+//   K2  scatter         fixed-point rho (cells thread-per-object, macro per CTA)
+//   K3  spectral        phi/E maps; the first pass also yields the overflow
+//                       and re-zeroes rho for the next iteration
+//   K4  dens_kernel     density means -> dens grad; WL grad assembly; energy;
+//                       last block: objective, lambda init, log row, best key,
+//                       stop and divergence tests            (gp.py:386-422)
+//   K5a step_kernel     best copy, precondition x2, BB norms; last block: step
+//                       size, underflow test, momentum        (gp.py:423-437)
+//   K5b advance_kernel  u' = P(v - s g), v' = P(u' + m (u' - u)); last block:
+//                       mu schedule, lambda update, next gamma (gp.py:437-444)
+#include <math.h>
+
+#include "p3d_geom.cuh"
+#include "p3d_internal.cuh"
+
+namespace p3d {
+
+template <class Cloud>
+void launch_scatter(const Cloud& cl, int n, int n_macro, const int32_t* macro_ids,
+                    const p3d_grid& g, int64_t* rho, const int* halt, cudaStream_t s);
+
+__device__ __forceinline__ double* fin(const p3d_gp& gp) {
+  return gp.partials + (long long)kSlotFinal * kPartialStride;
+}
+
+__device__ __forceinline__ CloudGP cloud_of(const p3d_gp& gp, const double* pos) {
+  CloudGP c;
+  c.pos = pos;
+  c.n_inst = gp.n_inst;
+  c.n_obj = gp.n_obj;
+  c.wt = gp.w_top; c.ht = gp.h_top; c.wb = gp.w_bot; c.hb = gp.h_bot;
+  c.fw = gp.fill_w; c.fh = gp.fill_h;
+  c.macro = gp.is_macro;
+  c.dz = gp.grid.dz;
+  c.target_density = gp.target_density;
+  return c;
+}
+
+// gp.py:344-348
+__device__ __forceinline__ double clamp_span(double v, double size, double extent) {
+  const double lo = size / 2;
+  const double hi = extent - size / 2;
+  if (lo <= hi) return clipd(v, fmin(lo, hi), fmax(lo, hi));
+  return fmin(lo, hi) + fabs(hi - lo) / 2;
+}
+
+// Gp3dProblem.project for one object (gp.py:280-294)
+__device__ __forceinline__ void project_obj(const p3d_gp& gp, int i, double& x, double& y,
+                                            double& z) {
+  const double dz = gp.grid.dz;
+  if (i < gp.n_inst) {
+    z = clipd(z, dz / 4, 3 * dz / 4);
+    double w, h;
+    dynamic_wh(z, dz, gp.is_macro[i] != 0, gp.w_top[i], gp.h_top[i], gp.w_bot[i], gp.h_bot[i],
+               w, h);
+    x = clamp_span(x, w, gp.grid.dx);
+    y = clamp_span(y, h, gp.grid.dy);
+  } else {
+    const int f = i - gp.n_inst;
+    x = clamp_span(x, gp.fill_w[f], gp.grid.dx);
+    y = clamp_span(y, gp.fill_h[f], gp.grid.dy);
+    z = gp.fill_z[f];
+  }
+}
+
+__global__ void project_kernel(p3d_gp gp, const double* in, double* out) {
+  const int O = gp.n_obj;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < O; i += gridDim.x * blockDim.x) {
+    double x = in[i], y = in[O + i], z = in[2 * O + i];
+    project_obj(gp, i, x, y, z);
+    out[i] = x;
+    out[O + i] = y;
+    out[2 * O + i] = z;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// loop state init / eval setup
+// ---------------------------------------------------------------------------
+__global__ void init_state_kernel(p3d_gp gp) {
+  p3d_loop_state* st = gp.st;
+  st->it = 0;
+  st->done = gp.max_iters <= 0;
+  st->diverged = 0;
+  st->lam_set = 0;
+  st->step_set = 0;
+  st->stop_now = 0;
+  st->best_flag = 0;
+  st->rise = 0;
+  st->nonfinite = 0;
+  st->converged = 0;
+  st->eval_only = 0;
+  st->lam = 0.0;
+  st->a = 1.0;
+  st->step = 0.0;
+  st->prev_ovfl = P3D_INF;
+  st->prev_value = P3D_INF;
+  st->last_mu = 1.0;
+  st->best0 = P3D_INF;
+  st->best1 = P3D_INF;
+  st->gamma = gp.max_iters > 0 ? gp.gamma_tab[0] : 0.0;
+  st->lam_eval = 0.0;
+  st->iterations = 0;
+  st->hbt_count = 0;
+  st->final_overflow = P3D_INF;
+  st->wirelength = 0.0;
+  for (int k = 0; k < 16; ++k) st->counters[k] = 0u;
+}
+
+__global__ void eval_setup_kernel(p3d_gp gp, double lam, double gamma) {
+  p3d_loop_state* st = gp.st;
+  st->eval_only = 1;
+  st->done = 0;
+  st->lam_eval = lam;
+  st->gamma = gamma;
+}
+
+__global__ void copy3_kernel(int O, const double* a, double* b, double* c) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 3 * O; i += gridDim.x * blockDim.x) {
+    const double v = a[i];
+    b[i] = v;
+    if (c) c[i] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: density gather + objective assembly; last block = loop control part 1
+// ---------------------------------------------------------------------------
+__device__ void finish_object(const p3d_gp& gp, int i, const Charge& q, const double (&mean)[4],
+                              double (&acc)[4]) {
+  const int O = gp.n_obj, I = gp.n_inst;
+  const double qq = charge_of(q);
+  const double c = -2.0 * qq;
+  const double dgx = mean[1] * c, dgy = mean[2] * c;
+  const double dgz = i < I ? mean[3] * c : 0.0;  // filler depth frozen (gp.py:255)
+  double gx = 0.0, gy = 0.0, gz = 0.0;
+  if (i < I) {
+    const double* f = fin(gp);
+    gx = gp.inst_g[i];
+    gy = gp.inst_g[I + i];
+    const double gzh = gp.inst_g[2 * I + i], gzb = gp.inst_g[3 * I + i];
+    const double base = f[kFinNorm + 2] == 0.0 ? 0.0 : f[kFinNorm + 3] * gzb;
+    gz = base + gp.alpha * gzh;  // wirelength.py:296-305
+  }
+  gp.wl_grad[i] = gx;
+  gp.wl_grad[O + i] = gy;
+  gp.wl_grad[2 * O + i] = gz;
+  gp.dens_grad[i] = dgx;
+  gp.dens_grad[O + i] = dgy;
+  gp.dens_grad[2 * O + i] = dgz;
+  const double lam = gp.st->lam_eval;
+  const double t0 = gx + lam * dgx, t1 = gy + lam * dgy, t2 = gz + lam * dgz;
+  acc[0] += qq * mean[0];
+  acc[1] += fabs(dgx) + fabs(dgy) + fabs(dgz);
+  acc[2] += fabs(gx) + fabs(gy) + fabs(gz);
+  acc[3] += (isfinite(t0) && isfinite(t1) && isfinite(t2)) ? 0.0 : 1.0;
+}
+
+__device__ void control_after_eval(const p3d_gp& gp, double energy, double l1_dens,
+                                   double l1_wl, double nonfinite) {
+  p3d_loop_state* st = gp.st;
+  const double* f = fin(gp);
+  const double wl_bi = f[kFinNet + 0] + f[kFinNet + 1];
+  const double cut = f[kFinNet + 2];
+  const double exact = f[kFinNet + 3] + f[kFinNet + 4];
+  const double ncross = f[kFinNet + 5];
+  const double ovfl = gp.movable_volume <= 0 ? 0.0 : f[kFinOvfl];
+  const double lam_eval = st->lam_eval;
+  const double wl_value = wl_bi + gp.alpha * cut;
+  double value = wl_bi + gp.alpha * cut + lam_eval * energy;  // gp.py:326
+  st->wl_x = f[kFinNet + 0];
+  st->wl_y = f[kFinNet + 1];
+  st->cut = cut;
+  st->exact = exact;
+  st->ncross = ncross;
+  st->norm_x = f[kFinNorm + 0];
+  st->norm_y = f[kFinNorm + 1];
+  st->norm_zb = f[kFinNorm + 2];
+  st->gz_scale = f[kFinNorm + 3];
+  st->energy = energy;
+  st->ovfl = ovfl;
+  st->wl_value = wl_value;
+  st->l1_wl = l1_wl;
+  st->l1_dens = l1_dens;
+  st->nonfinite = nonfinite != 0.0;
+  st->value = value;
+  if (st->eval_only) {
+    st->done = 1;
+    return;
+  }
+  if (!isfinite(value) || nonfinite != 0.0) {  // gp.py:328-329, 390-393
+    st->diverged = 1;
+    st->done = 1;
+    return;
+  }
+  if (!st->lam_set) {  // gp.py:394-399, lambda_init gp.py:150-153
+    st->lam = (l1_wl <= 0 || l1_dens <= 0) ? 1e-3 : 1e-3 * l1_wl / l1_dens;
+    st->lam_set = 1;
+    value = wl_value + st->lam * energy;
+    st->value = value;
+  }
+  const int it = st->it;
+  gp.log[4 * it + 0] = it;
+  gp.log[4 * it + 1] = exact;
+  gp.log[4 * it + 2] = ncross;
+  gp.log[4 * it + 3] = ovfl;
+  st->iterations = it + 1;
+  st->final_overflow = ovfl;
+  st->wirelength = exact;
+  st->hbt_count = (int)ncross;
+  const double k0 = fmax(ovfl - gp.stop_overflow, 0.0);  // gp.py:406-409
+  if (k0 < st->best0 || (k0 == st->best0 && value < st->best1)) {
+    st->best0 = k0;
+    st->best1 = value;
+    st->best_flag = 1;
+  }
+  if (ovfl <= gp.stop_overflow) {  // gp.py:410-411
+    st->converged = 1;
+    st->stop_now = 1;
+    return;
+  }
+  st->rise = value > st->prev_value * st->last_mu ? st->rise + 1 : 0;  // gp.py:414-422
+  st->prev_value = value;
+  gp.ovfl_hist[it] = ovfl;
+  const int W = gp.divergence_window;
+  if (st->rise >= W) {
+    const int first = W > 0 ? it - W + 1 : 0;
+    if (gp.ovfl_hist[first] - gp.ovfl_hist[it] < 1e-3) {
+      st->diverged = 1;
+      st->stop_now = 1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) dens_kernel(p3d_gp gp) {
+  if (gp.st->done) return;
+  __shared__ double red[32 * 4];
+  const CloudGP cl = cloud_of(gp, gp.v);
+  double acc[4] = {0, 0, 0, 0};
+  const int nm = gp.n_macro;
+  if ((int)blockIdx.x < nm) {
+    const int i = gp.macro_ids[blockIdx.x];
+    const Charge q = cl.get(i);
+    double mean[4];
+    gather_object_block(q, gp.grid, gp.maps, mean, red);
+    if (threadIdx.x == 0) finish_object(gp, i, q, mean, acc);
+  } else {
+    const int b = blockIdx.x - nm, nb = gridDim.x - nm;
+    for (int i = b * blockDim.x + threadIdx.x; i < gp.n_obj; i += nb * blockDim.x) {
+      if (cl.is_macro(i)) continue;
+      const Charge q = cl.get(i);
+      double mean[4];
+      gather_object(q, gp.grid, gp.maps, mean);
+      finish_object(gp, i, q, mean, acc);
+    }
+  }
+  double* part = gp.partials + (long long)kSlotDens * kPartialStride;
+  block_sum<4>(acc, red);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 4; ++k) part[k * gridDim.x + blockIdx.x] = acc[k];
+  if (last_block(&gp.st->counters[kCntDens])) {
+    double tot[4];
+    for (int k = 0; k < 4; ++k) tot[k] = ordered_sum(part + k * gridDim.x, gridDim.x, red);
+    if (threadIdx.x == 0) control_after_eval(gp, tot[0], tot[1], tot[2], tot[3]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5a: best snapshot, preconditioning (Eq. 19) of current and re-weighted
+// previous gradients, BB norms; last block: step size
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) step_kernel(p3d_gp gp) {
+  p3d_loop_state* st = gp.st;
+  if (st->done) return;
+  __shared__ double red[32 * 3];
+  const int O = gp.n_obj;
+  const bool best = st->best_flag != 0, stop = st->stop_now != 0;
+  const bool have_prev = st->step_set != 0;
+  const double lam = st->lam;
+  const CloudGP cl = cloud_of(gp, gp.v);
+  double acc[3] = {0, 0, 0};  // |dv|^2, |dg|^2, max|g|
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < O; i += gridDim.x * blockDim.x) {
+    if (best) {
+      gp.best[i] = gp.u[i];
+      gp.best[O + i] = gp.u[O + i];
+      gp.best[2 * O + i] = gp.u[2 * O + i];
+    }
+    if (stop) continue;
+    const double q = charge_of(cl.get(i));
+    const double mdeg = (i < gp.n_inst && gp.is_macro[i]) ? gp.degree[i] : 0.0;
+    double div = lam * q;
+    div = div + mdeg;
+    div = fmax(div, 1.0);
+    double divp = 1.0;
+    if (have_prev) {
+      divp = lam * gp.prev_q[i];
+      divp = divp + mdeg;
+      divp = fmax(divp, 1.0);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long k = (long long)c * O + i;
+      const double wl = gp.wl_grad[k], dn = gp.dens_grad[k];
+      const double pre = (wl + lam * dn) / div;
+      if (have_prev) {
+        const double pp = (gp.prev_wl[k] + lam * gp.prev_dens[k]) / divp;
+        const double dg = pre - pp, dv = gp.v[k] - gp.v_prev[k];
+        acc[0] += dv * dv;
+        acc[1] += dg * dg;
+      }
+      acc[2] = fmax(acc[2], fabs(pre));
+      gp.pre[k] = pre;
+      gp.prev_wl[k] = wl;
+      gp.prev_dens[k] = dn;
+    }
+    gp.prev_q[i] = q;
+  }
+  double* part = gp.partials + (long long)kSlotStep * kPartialStride;
+  {
+    double s2[2] = {acc[0], acc[1]};
+    block_sum<2>(s2, red);
+    double m = block_max(acc[2], red + 64);
+    if (threadIdx.x == 0) {
+      part[blockIdx.x] = s2[0];
+      part[gridDim.x + blockIdx.x] = s2[1];
+      part[2 * gridDim.x + blockIdx.x] = m;
+    }
+  }
+  if (last_block(&st->counters[kCntStep])) {
+    const double dv2 = ordered_sum(part, gridDim.x, red);
+    const double dg2 = ordered_sum(part + gridDim.x, gridDim.x, red);
+    if (threadIdx.x == 0) {
+      if (stop) {
+        st->done = 1;
+        return;
+      }
+      double gm = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) gm = fmax(gm, ((volatile double*)part)[2 * gridDim.x + b]);
+      st->dv2 = dv2;
+      st->dg2 = dg2;
+      st->gmax = gm;
+      if (!st->step_set) {  // gp.py:198-202, 207-209
+        st->step = gm == 0.0 ? 1.0 : gp.step_scale / gm;
+        st->step_set = 1;
+      } else {  // gp.py:210-217
+        const double den = sqrt(dg2);
+        if (den > 0) {
+          const double bb = sqrt(dv2) / den;
+          st->step = fmin(fmax(bb, st->step / 4), st->step * 4);
+        }
+      }
+      if (!isfinite(st->step) || st->step <= gp.min_step) {  // gp.py:218-219, 438-441
+        st->diverged = 1;
+        st->done = 1;
+        return;
+      }
+      const double a = st->a;
+      st->a_new = (1 + sqrt(4 * (a * a) + 1)) / 2;
+      st->mom = (a - 1) / st->a_new;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5b: projected Nesterov update (gp.py:220-227); last block: schedules
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
+  p3d_loop_state* st = gp.st;
+  if (st->done) return;
+  const int O = gp.n_obj;
+  const double step = st->step, mom = st->mom;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < O; i += gridDim.x * blockDim.x) {
+    double v[3], u[3], un[3], vn[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      v[c] = gp.v[(long long)c * O + i];
+      u[c] = gp.u[(long long)c * O + i];
+      un[c] = v[c] - step * gp.pre[(long long)c * O + i];
+    }
+    project_obj(gp, i, un[0], un[1], un[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) vn[c] = un[c] + mom * (un[c] - u[c]);
+    project_obj(gp, i, vn[0], vn[1], vn[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long k = (long long)c * O + i;
+      gp.v_prev[k] = v[c];
+      gp.u[k] = un[c];
+      gp.v[k] = vn[c];
+    }
+  }
+  if (last_block(&st->counters[kCntAdvance])) {
+    if (threadIdx.x == 0) {
+      st->a = st->a_new;
+      // mu_from_overflow (gp.py:156-168), lambda update (gp.py:442-444)
+      const double drop = st->prev_ovfl - st->ovfl;
+      double mu;
+      if (drop < 0) mu = gp.mu_min;
+      else if (drop >= 2e-3) mu = gp.mu_min + 0.01;
+      else if (drop >= 5e-4) mu = (gp.mu_min + gp.mu_max) / 2;
+      else mu = gp.mu_max;
+      mu = fmin(fmax(mu, gp.mu_min), gp.mu_max);
+      st->last_mu = mu;
+      st->lam *= mu;
+      st->prev_ovfl = st->ovfl;
+      st->best_flag = 0;
+      st->it += 1;
+      if (st->it >= gp.max_iters) {
+        st->done = 1;
+      } else {
+        st->gamma = gp.gamma_tab[st->it];
+      }
+      st->lam_eval = st->lam;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+static void eval_kernels(const p3d_gp& gp, cudaStream_t s) {
+  p3d_loop_state* st = gp.st;
+  const int* halt = &st->done;
+  double* finals = gp.partials + (long long)kSlotFinal * kPartialStride;
+  // K1
+  NetArgs na{};
+  na.n_net = gp.topo.n_net;
+  na.blocks = gp.nblk_net;
+  na.net_ptr = gp.topo.net_ptr;
+  na.pin_inst = gp.topo.pin_inst;
+  na.net_order = gp.topo.net_order;
+  na.net_dup = gp.topo.net_dup;
+  na.pin_slot = gp.topo.pin_slot;
+  na.gamma = 0.0;
+  na.gamma_ptr = &st->gamma;
+  na.scale4 = 4.0 / gp.grid.dz;
+  na.want_pins = 1;
+  na.out4 = gp.pin_out;
+  na.partials = gp.partials + (long long)kSlotNet * kPartialStride;
+  na.counter = &st->counters[kCntNet];
+  na.final6 = finals + kFinNet;
+  na.halt = halt;
+  const long long O = gp.n_obj;
+  launch_net_pos(na, gp.v, gp.v + O, gp.v + 2 * O, gp.pin_off, gp.grid.dz, s);
+  // K1b
+  GatherArgs ga{};
+  ga.n_obj = gp.n_inst;
+  ga.blocks = grid_blocks(gp.n_inst, 256, kMaxBlocks);
+  ga.obj_slot_ptr = gp.topo.obj_slot_ptr;
+  ga.pin4 = gp.pin_out;
+  ga.out = gp.inst_g;
+  ga.partials = gp.partials + (long long)kSlotGather * kPartialStride;
+  ga.counter = &st->counters[kCntGather];
+  ga.final_norms = finals + kFinNorm;
+  ga.halt = halt;
+  launch_gather(ga, s);
+  // K2
+  CloudGP cl;
+  cl.pos = gp.v;
+  cl.n_inst = gp.n_inst;
+  cl.n_obj = gp.n_obj;
+  cl.wt = gp.w_top; cl.ht = gp.h_top; cl.wb = gp.w_bot; cl.hb = gp.h_bot;
+  cl.fw = gp.fill_w; cl.fh = gp.fill_h;
+  cl.macro = gp.is_macro;
+  cl.dz = gp.grid.dz;
+  cl.target_density = gp.target_density;
+  launch_scatter(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, gp.rho_fx, halt, s);
+  // K3 (+ overflow, re-zero)
+  SpecOvfl ov;
+  ov.zero = 1;
+  ov.rho_t_fx = gp.rho_t_fx;
+  ov.partials = gp.partials + (long long)kSlotOvfl * kPartialStride;
+  ov.counter = &st->counters[kCntOvfl];
+  ov.out = finals + kFinOvfl;
+  ov.scale = gp.movable_volume > 0 ? 9.094947017729282379150390625e-13 * gp.grid.bin_vol / gp.movable_volume : 0.0;
+  launch_spectral_ex(&gp.grid, nullptr, gp.rho_fx, nullptr, nullptr, gp.maps, gp.spec_scratch,
+                     halt, &ov, s);
+  // K4
+  dens_kernel<<<gp.n_macro + gp.nblk_obj, 256, 0, s>>>(gp);
+}
+
+int gp_iterate(const p3d_gp& gp, cudaStream_t s) {
+  eval_kernels(gp, s);
+  step_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  return check_launch("gp_iterate");
+}
+
+int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s) {
+  eval_setup_kernel<<<1, 1, 0, s>>>(gp, lam, gamma);
+  eval_kernels(gp, s);
+  return check_launch("gp_evaluate");
+}
+
+int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s) {
+  spectral_setup();
+  init_state_kernel<<<1, 1, 0, s>>>(gp);
+  const int b = grid_blocks(gp.n_obj, 256, 4096);
+  project_kernel<<<b, 256, 0, s>>>(gp, pos0, gp.u);
+  copy3_kernel<<<b, 256, 0, s>>>(gp.n_obj, gp.u, gp.v, gp.best);
+  cudaMemsetAsync(gp.rho_fx, 0, sizeof(int64_t) * (size_t)gp.grid.nx * gp.grid.ny * gp.grid.nz, s);
+  return check_launch("gp_init");
+}
+
+int gp_project(const p3d_gp& gp, const double* in, double* out, cudaStream_t s) {
+  project_kernel<<<grid_blocks(gp.n_obj, 256, 4096), 256, 0, s>>>(gp, in, out);
+  return check_launch("gp_project");
+}
+
+}  // namespace p3d

@@ -1,0 +1,360 @@
+"""Drop-in of ``place3d.density`` on the B200 (K2/K3/K4 kernels of libp3d.so).
+
+Same names and argument meaning as ``pkg/src/place3d/density.py``; maps and
+per-object arrays come back as CUDA float64 tensors.  The density map is
+accumulated in int64 fixed point (2^-40 per unit density) — exact and
+order-independent — and converted to float64 once.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .model import partition_from_z
+
+FX_BITS = 40
+
+
+def _tables(n, d):
+    """Per-axis device tables: omega, FFT twiddles, DCT phase factors."""
+    omega = np.pi * np.arange(n) / d
+    j = np.arange(max(n // 2, 1))
+    tw = np.empty((len(j), 2))
+    tw[:, 0] = np.cos(2 * np.pi * j / n)
+    tw[:, 1] = -np.sin(2 * np.pi * j / n)
+    k = np.arange(n)
+    ph = np.empty((n, 2))
+    ph[:, 0] = np.cos(np.pi * k / (2 * n))
+    ph[:, 1] = np.sin(np.pi * k / (2 * n))
+    return omega, tw.reshape(-1), ph.reshape(-1)
+
+
+class DensityGrid:
+    """Uniform nx x ny x nz bins over [0,dx] x [0,dy] x [0,dz] (density.py:26-55)."""
+
+    def __init__(self, dx, dy, nx, ny, nz):
+        self.dx = float(dx)
+        self.dy = float(dy)
+        self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
+        self.wb = self.dx / self.nx
+        self.hb = self.dy / self.ny
+        self.db = (self.wb + self.hb) / 2
+        self.dz = self.nz * self.db
+        self.shape = (self.nx, self.ny, self.nz)
+        self.bin_vol = self.wb * self.hb * self.db
+        wx = np.pi * np.arange(self.nx) / self.dx
+        wy = np.pi * np.arange(self.ny) / self.dy
+        wz = np.pi * np.arange(self.nz) / self.dz
+        self.omega = (wx, wy, wz)
+        lam = wx[:, None, None] ** 2 + wy[None, :, None] ** 2 + wz[None, None, :] ** 2
+        inv = np.zeros_like(lam)
+        inv[lam > 0] = 1.0 / lam[lam > 0]
+        self.inv_lam = inv
+        self.fx_scale = np.ldexp(1.0, FX_BITS) / self.bin_vol
+        self._dev = None
+
+    @property
+    def extents(self):
+        return self.wb, self.hb, self.db
+
+    @property
+    def n_bins(self):
+        return self.nx * self.ny * self.nz
+
+    def device(self):
+        """ctypes ``p3d_grid`` + the device tables it points at (cached)."""
+        if self._dev is not None:
+            return self._dev
+        keep = _dev.Keep()
+        g = _lib.Grid()
+        g.nx, g.ny, g.nz = self.nx, self.ny, self.nz
+        g.dx, g.dy, g.dz = self.dx, self.dy, self.dz
+        g.wb, g.hb, g.db, g.bin_vol = self.wb, self.hb, self.db, self.bin_vol
+        g.fx_scale = self.fx_scale
+        for a, (n, d) in enumerate(((self.nx, self.dx), (self.ny, self.dy), (self.nz, self.dz))):
+            om, tw, ph = _tables(n, d)
+            g.omega[a] = keep(_dev.f64(om)).value
+            g.twiddle[a] = keep(_dev.f64(tw)).value
+            g.phase[a] = keep(_dev.f64(ph)).value
+        self._dev = (g, keep)
+        return self._dev
+
+
+@dataclass
+class ChargeCloud:
+    """Struct-of-arrays charges (density.py:58-83); numpy or CUDA tensors."""
+
+    x: object
+    y: object
+    z: object
+    w: object
+    h: object
+    dep: object
+    weight: object
+    is_macro: object
+
+    @property
+    def volume(self):
+        return self.w * self.h * self.dep
+
+    @property
+    def charge(self):
+        return self.weight * self.volume
+
+    def subset(self, mask):
+        return ChargeCloud(self.x[mask], self.y[mask], self.z[mask], self.w[mask], self.h[mask],
+                           self.dep[mask], self.weight[mask], self.is_macro[mask])
+
+
+class _DevCloud:
+    def __init__(self, cloud: ChargeCloud, macro_override=None):
+        keep = self.keep = _dev.Keep()
+        self.t = {k: _dev.f64(getattr(cloud, k)) for k in ("x", "y", "z", "w", "h", "dep", "weight")}
+        m = cloud.is_macro if macro_override is None else macro_override
+        m = m.detach().cpu().numpy() if isinstance(m, torch.Tensor) else np.asarray(m)
+        m = np.broadcast_to(np.asarray(m, dtype=bool), (self.t["x"].numel(),))
+        self.is_macro = _dev.u8(m)
+        ids = np.flatnonzero(m).astype(np.int32)
+        self.macro_ids = _dev.i32(ids if len(ids) else np.zeros(1, np.int32))
+        c = _lib.Cloud()
+        c.n = self.t["x"].numel()
+        c.n_macro = len(ids)
+        for k, v in self.t.items():
+            setattr(c, k, keep(v))
+        c.is_macro = keep(self.is_macro)
+        c.macro_ids = keep(self.macro_ids)
+        self.struct = c
+        self.n = c.n
+
+
+@dataclass
+class FillerSet:
+    """Dummy charges enforcing per-die utilisation (density.py:86-104)."""
+
+    x: np.ndarray
+    y: np.ndarray
+    z: np.ndarray
+    die: np.ndarray
+    w: np.ndarray
+    h: np.ndarray
+    dep: float
+
+    @property
+    def count(self):
+        return len(self.x)
+
+    def total_volume(self, die):
+        m = self.die == die
+        return float((self.w[m] * self.h[m]).sum() * self.dep)
+
+
+def build_fillers(die_area_wh, dz, u_top, u_bot, cell_area_hint, rng):
+    """Fillers near the typical cell footprint, exact per-die volume
+    (density.py:107-131; host setup, rng draws in the reference order)."""
+    dx, dy = die_area_wh
+    parts = []
+    for die, u in ((0, u_bot), (1, u_top)):
+        area = dx * dy * (1.0 - u)
+        if area <= 0:
+            continue
+        side_hint = max(np.sqrt(cell_area_hint), 1e-9)
+        count = int(np.clip(round(area / side_hint ** 2), 1, 20000))
+        side = np.sqrt(area / count)
+        xs = rng.uniform(side / 2, dx - side / 2, count)
+        ys = rng.uniform(side / 2, dy - side / 2, count)
+        parts.append((xs, ys, np.full(count, dz / 4 if die == 0 else 3 * dz / 4),
+                      np.full(count, die, dtype=np.int8), np.full(count, side),
+                      np.full(count, side)))
+    if not parts:
+        e = np.zeros(0)
+        return FillerSet(e, e, e, np.zeros(0, np.int8), e, e, dz / 2)
+    cols = [np.concatenate([p[i] for p in parts]) for i in range(6)]
+    return FillerSet(*cols, dz / 2)
+
+
+def dynamic_size(w_top, h_top, w_bot, h_bot, is_macro, z, dz):
+    """Footprint vs depth (density.py:134-147, Eqs. 6-7): cells switch at the
+    midplane, macros blend linearly over z in [dz/4, 3dz/4]."""
+    z = torch.clamp(_dev.f64(z), dz / 4, 3 * dz / 4)
+    wt, ht, wb, hb = (_dev.f64(a) for a in (w_top, h_top, w_bot, h_bot))
+    m = _dev.u8(is_macro).to(torch.bool)
+    top = (z - dz / 2) > 0
+    t = 2 * z / dz - 0.5
+    wm = t * wt + (1 - t) * wb
+    hm = t * ht + (1 - t) * hb
+    return torch.where(m, wm, torch.where(top, wt, wb)), torch.where(m, hm, torch.where(top, ht, hb))
+
+
+# ---------------------------------------------------------------------------
+# accumulation (K2)
+# ---------------------------------------------------------------------------
+
+
+def accumulate_density_fx(grid: DensityGrid, cloud: ChargeCloud, macro_override=None):
+    """int64 map [nx, ny, nz] in units of 2^-40 (the exact device map)."""
+    _lib.require_cuda()
+    g, _ = grid.device()
+    dc = _DevCloud(cloud, macro_override)
+    rho = torch.zeros(grid.shape, dtype=torch.int64, device="cuda")
+    if dc.n:
+        _lib.call("p3d_accumulate_density", _lib.byref(g), _lib.byref(dc.struct), _lib.ptr(rho),
+                  _lib.stream_ptr())
+    return rho
+
+
+def fx_to_density(rho_fx):
+    out = torch.empty(rho_fx.shape, dtype=torch.float64, device="cuda")
+    _lib.call("p3d_fx_to_density", int(rho_fx.numel()), _lib.ptr(rho_fx), _lib.ptr(out),
+              _lib.stream_ptr())
+    return out
+
+
+def accumulate_density(grid, cloud):
+    """Density map (density.py:301-311): cells/fillers thread-per-object,
+    macros one CTA each over their footprint tile."""
+    return fx_to_density(accumulate_density_fx(grid, cloud))
+
+
+def direct_density(grid, cloud):
+    """Per-object traversal of every given charge (density.py:199-204)."""
+    return fx_to_density(accumulate_density_fx(grid, cloud, macro_override=False))
+
+
+def macro_prefix_density(grid, cloud):
+    """Macro map (density.py:291-298); on the device every charge takes the
+    per-macro tile path, which equals the corner-stamp prefix sum exactly in
+    real arithmetic (Theorem 1)."""
+    return fx_to_density(accumulate_density_fx(grid, cloud, macro_override=True))
+
+
+def prefix_sum_3d(a):
+    """Inclusive prefix sum along x, y, z (density.py:207-209)."""
+    t = _dev.f64(a)
+    return torch.cumsum(torch.cumsum(torch.cumsum(t, 0), 1), 2)
+
+
+def suffix_sum_3d(a):
+    """Adjoint of prefix_sum_3d (density.py:212-217)."""
+    t = _dev.f64(a)
+    for ax in range(3):
+        t = torch.flip(torch.cumsum(torch.flip(t, (ax,)), ax), (ax,))
+    return t
+
+
+# ---------------------------------------------------------------------------
+# spectral solve (K3)
+# ---------------------------------------------------------------------------
+
+
+def _spectral(grid, rho=None, coef=None, want_coef=False):
+    _lib.require_cuda()
+    g, _ = grid.device()
+    B = grid.n_bins
+    maps = torch.empty((B, 4), dtype=torch.float64, device="cuda")
+    scr = torch.empty(6 * B, dtype=torch.float64, device="cuda")
+    out_coef = None
+    if coef is None:
+        r = _dev.f64(rho)
+        out_coef = torch.empty(grid.shape, dtype=torch.float64, device="cuda") if want_coef else None
+        _lib.call("p3d_spectral", _lib.byref(g), _lib.ptr(r), _lib.ptr(out_coef), _lib.ptr(maps),
+                  _lib.ptr(scr), _lib.stream_ptr())
+    else:
+        c = _dev.f64(coef)
+        _lib.call("p3d_spectral_from_coef", _lib.byref(g), _lib.ptr(c), _lib.ptr(maps),
+                  _lib.ptr(scr), _lib.stream_ptr())
+    return maps, out_coef
+
+
+def solve_potential(rho, grid):
+    """Neumann Poisson solve by cosine transforms, DC dropped
+    (density.py:319-328).  Returns (phi, scipy-normalised DCT-II coef)."""
+    maps, coef = _spectral(grid, rho=rho, want_coef=True)
+    return maps[:, 0].reshape(grid.shape).contiguous(), coef
+
+
+def electric_field(coef, grid):
+    """E = -grad(phi) evaluated spectrally (density.py:357-368)."""
+    maps, _ = _spectral(grid, coef=coef)
+    return tuple(maps[:, k].reshape(grid.shape).contiguous() for k in (1, 2, 3))
+
+
+def potential_and_field(rho, grid):
+    """Both at once as the interleaved [B][4] (phi, Ex, Ey, Ez) map the
+    density gather reads (what the fused loop uses)."""
+    maps, _ = _spectral(grid, rho=rho)
+    return maps
+
+
+# ---------------------------------------------------------------------------
+# energy / force / overflow (K4)
+# ---------------------------------------------------------------------------
+
+
+def _interleave(grid, phi=None, ex=None, ey=None, ez=None):
+    B = grid.n_bins
+    m = torch.zeros((B, 4), dtype=torch.float64, device="cuda")
+    for k, a in enumerate((phi, ex, ey, ez)):
+        if a is not None:
+            m[:, k] = _dev.f64(a).reshape(-1)
+    return m
+
+
+def _gather(grid, cloud, maps, freeze_z=None):
+    _lib.require_cuda()
+    g, _ = grid.device()
+    dc = _DevCloud(cloud)
+    force = torch.zeros((dc.n, 3), dtype=torch.float64, device="cuda")
+    energy = torch.zeros(1, dtype=torch.float64, device="cuda")
+    fr = None if freeze_z is None else _dev.u8(freeze_z)
+    scr = _dev.scratch(8 + dc.struct.n_macro + 1024 + 8)
+    if dc.n:
+        _lib.call("p3d_density_gather", _lib.byref(g), _lib.byref(dc.struct), _lib.ptr(maps),
+                  _lib.ptr(fr), _lib.ptr(energy), _lib.ptr(force), _lib.ptr(scr),
+                  _lib.stream_ptr())
+    return float(energy.item()), force
+
+
+def density_energy(grid, cloud, phi):
+    """U = sum q * overlap-weighted mean phi (density.py:568-579)."""
+    return _gather(grid, cloud, _interleave(grid, phi=phi))[0]
+
+
+def density_force(grid, cloud, ex, ey, ez, freeze_z=None):
+    """-2 q * overlap-weighted mean E (density.py:582-609)."""
+    return _gather(grid, cloud, _interleave(grid, ex=ex, ey=ey, ez=ez), freeze_z)[1]
+
+
+def density_energy_and_force(grid, cloud, maps, freeze_z=None):
+    """Energy and force from one interleaved map in one gather pass."""
+    return _gather(grid, cloud, maps, freeze_z)
+
+
+def overflow(rho, grid, rho_t, movable_volume):
+    """Fraction of movable volume above the target density (density.py:612-617)."""
+    if movable_volume <= 0:
+        return 0.0
+    r = _dev.f64(rho)
+    return float((torch.clamp(r - rho_t, min=0).sum() * grid.bin_vol / movable_volume).item())
+
+
+def overflow_fx(rho_fx, grid, rho_t, movable_volume):
+    """Overflow straight from the int64 map (exact integer excess)."""
+    g, _ = grid.device()
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    scr = _dev.scratch(8 + 1024 + 8)
+    _lib.call("p3d_overflow_fx", _lib.byref(g), _lib.ptr(rho_fx.contiguous()), float(rho_t),
+              float(movable_volume), _lib.ptr(out), _lib.ptr(scr), _lib.stream_ptr())
+    return float(out.item())
+
+
+__all__ = [
+    "DensityGrid", "ChargeCloud", "FillerSet", "build_fillers", "dynamic_size",
+    "accumulate_density", "accumulate_density_fx", "fx_to_density", "direct_density",
+    "macro_prefix_density", "prefix_sum_3d", "suffix_sum_3d", "solve_potential",
+    "electric_field", "potential_and_field", "density_energy", "density_force",
+    "density_energy_and_force", "overflow", "overflow_fx", "partition_from_z",
+]

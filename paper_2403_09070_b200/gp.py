@@ -1,0 +1,497 @@
+"""Drop-in of the ``place3d.gp`` 3D global-placement loop on the B200.
+
+``run_gp3d`` keeps the reference signature (gp.py:359-455) but runs every
+iteration on the device: one ``p3d_gp_iterate`` enqueues K1..K5 with all loop
+control (lambda init, gamma/mu schedules, best-state key, stop, divergence and
+step-underflow exits) in device memory, and the host replays a CUDA graph of
+several iterations, polling a done flag.  The per-iteration log rows
+``(it, exact WL, crossings, overflow)`` are copied back once at the end.
+
+Host-side setup (grid choice, initial jitter, fillers, alpha) is the
+reference's own numpy arithmetic so initial states are bit-identical.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import logging
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from . import density as dn
+from . import wirelength as wl
+from .model import PlacementState, partition_from_z, rotated_dims
+
+log = logging.getLogger("place3d")
+
+K_MAX_BLOCKS = 2048
+K_PARTIAL_STRIDE = 8 * K_MAX_BLOCKS
+
+
+class StepUnderflow(RuntimeError):
+    pass
+
+
+@dataclass
+class GpConfig:
+    """Field-for-field ``GpConfig`` (gp.py:30-50)."""
+
+    seed: int = 1
+    nz: int = 8
+    grid_nx: int | None = None
+    grid_ny: int | None = None
+    stop_overflow: float = 0.10
+    max_iters: int = 1200
+    mu_min: float = 1.01
+    mu_max: float = 1.05
+    gamma_start_factor: float = 4.0
+    gamma_end_factor: float = 0.5
+    target_density: float = 1.0
+    alpha: float | None = None
+    alpha0: float = 3.5e-3
+    cut_cost_factor: float = 5.0
+    log_base: float | None = None
+    flow: str = "auto"
+    jitter_frac: float = 0.02
+    divergence_window: int = 100
+    threads: int = 1
+
+
+@dataclass
+class GpInfo:
+    iterations: int = 0
+    final_overflow: float = math.inf
+    diverged: bool = False
+    wirelength: float = 0.0
+    hbt_count: int = 0
+
+
+@dataclass
+class GradientBundle:
+    """Per-object gradients ([n_obj, 3] CUDA tensors) and objective parts (gp.py:62-72)."""
+
+    wl_grad: torch.Tensor
+    dens_grad: torch.Tensor
+    total: torch.Tensor
+    divisors: torch.Tensor
+    value: float
+    wl_value: float
+    energy: float
+
+
+# ---------------------------------------------------------------------------
+# host setup (reference arithmetic, gp.py:75-175)
+# ---------------------------------------------------------------------------
+
+
+def choose_grid(design, cfg: GpConfig) -> dn.DensityGrid:
+    """gp.py:75-87."""
+    n = max(design.n_insts, 1)
+    if cfg.grid_nx is not None:
+        nx = cfg.grid_nx
+        ny = cfg.grid_ny or cfg.grid_nx
+    else:
+        k = 3
+        while (2 ** (k + 1)) ** 2 <= n / 4 and 2 ** (k + 1) <= 128:
+            k += 1
+        nx = ny = 2 ** k
+    return dn.DensityGrid(design.die.width, design.die.height, nx, ny, cfg.nz)
+
+
+def alpha_value(design, dz: float, cfg: GpConfig) -> float:
+    """gp.py:90-107."""
+    if cfg.alpha is not None:
+        return cfg.alpha
+    die, hbt = design.die, design.hbt
+    eta = 2 * hbt.pitch / (die.row_height_top + die.row_height_bottom)
+    arg = max(90 * hbt.cost * eta - 1, 1 + 1e-6)
+    lg = math.log(arg) if cfg.log_base is None else math.log(arg, cfg.log_base)
+    fitted = cfg.alpha0 * (die.width * eta ** 2 / dz) * lg
+    floor = cfg.cut_cost_factor * hbt.cost / (dz / 2)
+    return max(fitted, floor)
+
+
+def select_flow(design) -> str:
+    """gp.py:110-112."""
+    return "2d" if design.r_ma >= 0.5 else "3d"
+
+
+def init_state(design, grid, cfg: GpConfig, rng) -> PlacementState:
+    """gp.py:115-126 (same rng draws)."""
+    n = design.n_insts
+    die = design.die
+    x = np.full(n, die.width / 2) + rng.normal(0, cfg.jitter_frac * die.width, n)
+    y = np.full(n, die.height / 2) + rng.normal(0, cfg.jitter_frac * die.height, n)
+    z = np.full(n, grid.dz / 2) + rng.normal(0, cfg.jitter_frac * grid.dz, n)
+    arr = design.arrays()
+    x = np.clip(x, arr.w_bot / 2, die.width - arr.w_bot / 2)
+    y = np.clip(y, arr.h_bot / 2, die.height - arr.h_bot / 2)
+    z = np.clip(z, grid.dz / 4, 3 * grid.dz / 4)
+    return PlacementState(x=x, y=y, z=z, rot=np.zeros(n, dtype=np.int64), dz=grid.dz)
+
+
+def make_fillers(design, grid, rng) -> dn.FillerSet:
+    """gp.py:129-139."""
+    arr = design.arrays()
+    cells = ~arr.is_macro
+    if cells.any():
+        hint = float(np.median(arr.w_bot[cells] * arr.h_bot[cells]))
+    else:
+        hint = (design.die.width / 32) ** 2
+    return dn.build_fillers((design.die.width, design.die.height), grid.dz,
+                            design.die.max_util_top, design.die.max_util_bottom, hint, rng)
+
+
+def lambda_init(wl_norm, dens_norm, scale=1e-3):
+    """gp.py:150-153 (the device loop applies the same rule)."""
+    if wl_norm <= 0 or dens_norm <= 0:
+        return scale
+    return scale * wl_norm / dens_norm
+
+
+def mu_from_overflow(prev_ovfl, cur_ovfl, cfg: GpConfig):
+    """gp.py:156-168 (the device loop applies the same rule)."""
+    drop = prev_ovfl - cur_ovfl
+    if drop < 0:
+        mu = cfg.mu_min
+    elif drop >= 2e-3:
+        mu = cfg.mu_min + 0.01
+    elif drop >= 5e-4:
+        mu = (cfg.mu_min + cfg.mu_max) / 2
+    else:
+        mu = cfg.mu_max
+    return min(max(mu, cfg.mu_min), cfg.mu_max)
+
+
+def gamma_schedule(grid, it, max_iters, cfg: GpConfig):
+    """gp.py:171-175."""
+    t = min(1.0, it / max(max_iters - 1, 1))
+    g0 = cfg.gamma_start_factor * grid.db
+    g1 = cfg.gamma_end_factor * grid.db
+    return g0 * (g1 / g0) ** t
+
+
+def precondition(gradients, lam, charges, pin_degrees, macro_flags):
+    """Eq. 19 (gp.py:142-147) on the device: g / max(1, lam q [+ #pins])."""
+    _lib.require_cuda()
+    g = _dev.f64(gradients)
+    shape = g.shape
+    g = g.reshape(-1, 3) if g.dim() == 2 else g.reshape(-1, 1).expand(-1, 3).contiguous()
+    n = g.shape[0]
+    q = _dev.f64(charges)
+    deg = _dev.f64(pin_degrees)
+    m = _dev.u8(macro_flags)
+    out = torch.empty_like(g)
+    div = torch.empty(n, dtype=torch.float64, device="cuda")
+    _lib.call("p3d_precondition", int(n), _lib.ptr(g), float(lam), _lib.ptr(q), _lib.ptr(deg),
+              _lib.ptr(m), _lib.ptr(out), _lib.ptr(div), _lib.stream_ptr())
+    if len(shape) != 2:
+        out = out[:, 0].reshape(shape)
+    return out, div
+
+
+class NesterovOptimizer:
+    """Accelerated descent with a clipped Barzilai-Borwein step (gp.py:178-227),
+    on CUDA tensors, for callers that drive their own loop (the fused device
+    loop in ``run_gp3d`` does not use this class)."""
+
+    def __init__(self, x0, project=None, min_step=1e-18):
+        self.project = project or (lambda p: p)
+        self.u = self.project(_dev.f64(x0).clone())
+        self.v = self.u.clone()
+        self.a = 1.0
+        self.step = None
+        self.min_step = min_step
+        self._prev_v = None
+        self._prev_g = None
+
+    def advance(self, g, step_scale=1.0, g_prev_reval=None):
+        g = _dev.f64(g)
+        ref = _dev.f64(g_prev_reval) if g_prev_reval is not None else self._prev_g
+        if self.step is None or self._prev_v is None or ref is None:
+            if self.step is None:
+                gmax = float(g.abs().max().item()) if g.numel() else 0.0
+                self.step = 1.0 if gmax == 0 else step_scale / gmax
+        else:
+            den = float(torch.linalg.norm((g - ref).reshape(-1)).item())
+            if den > 0:
+                new = float(torch.linalg.norm((self.v - self._prev_v).reshape(-1)).item()) / den
+                self.step = float(min(max(new, self.step / 4), self.step * 4))
+        if not math.isfinite(self.step) or self.step <= self.min_step:
+            raise StepUnderflow(f"step size underflow ({self.step!r})")
+        self._prev_v = self.v.clone()
+        self._prev_g = g.clone()
+        u_new = self.project(self.v - self.step * g)
+        a_new = (1 + math.sqrt(4 * self.a ** 2 + 1)) / 2
+        self.v = self.project(u_new + (self.a - 1) / a_new * (u_new - self.u))
+        self.u = u_new
+        self.a = a_new
+        return self.u
+
+
+# ---------------------------------------------------------------------------
+# the device problem context
+# ---------------------------------------------------------------------------
+
+
+class Gp3dProblem:
+    """Evaluation context for one 3D GP run (gp.py:235-341), device-resident.
+
+    Holds the p3d_gp descriptor: topology, per-object constants and all state
+    buffers (HBM layout in DESIGN.md).  ``evaluate`` / ``project`` /
+    ``cloud`` keep the reference semantics; ``run`` drives the fused loop."""
+
+    def __init__(self, design, grid: dn.DensityGrid, fillers: dn.FillerSet, cfg: GpConfig, rot,
+                 max_iters=None):
+        _lib.require_cuda()
+        self.design = design
+        self.grid = grid
+        self.fillers = fillers
+        self.cfg = cfg
+        self.rot = np.asarray(rot)
+        self.arr = arr = design.arrays()
+        self.topo = wl.NetTopology.from_arrays(arr)
+        self.n_inst = design.n_insts
+        self.n_fill = fillers.count
+        self.n_obj = self.n_inst + self.n_fill
+        self.alpha = alpha_value(design, grid.dz, cfg)
+        self.w_top, self.h_top = rotated_dims(arr.w_top, arr.h_top, self.rot)
+        self.w_bot, self.h_bot = rotated_dims(arr.w_bot, arr.h_bot, self.rot)
+        self.is_macro_obj = np.r_[arr.is_macro, np.zeros(self.n_fill, bool)]
+        self.degree_obj = np.r_[arr.pin_degree, np.zeros(self.n_fill)]
+        self.freeze_z = np.r_[np.zeros(self.n_inst, bool), np.ones(self.n_fill, bool)]
+        self.weight = np.r_[np.where(arr.is_macro, cfg.target_density, 1.0), np.ones(self.n_fill)]
+        zmid = np.full(self.n_inst, grid.dz / 2)
+        zc = np.clip(zmid, grid.dz / 4, 3 * grid.dz / 4)
+        t = 2 * zc / grid.dz - 0.5
+        up = (zc - grid.dz / 2) > 0
+        wv = np.where(arr.is_macro, t * self.w_top + (1 - t) * self.w_bot,
+                      np.where(up, self.w_top, self.w_bot))
+        hv = np.where(arr.is_macro, t * self.h_top + (1 - t) * self.h_bot,
+                      np.where(up, self.h_top, self.h_bot))
+        self.movable_volume = float((wv * hv).sum() * grid.dz / 2)
+        self.max_iters = int(cfg.max_iters if max_iters is None else max_iters)
+        self._build()
+
+    # -- device descriptor -------------------------------------------------
+    def _build(self):
+        arr, grid, cfg = self.arr, self.grid, self.cfg
+        keep = self._keep = _dev.Keep()
+        dt = self.topo.device(arr.net_has_dup_inst)
+        self._dtopo = dt
+        I, F, O = self.n_inst, self.n_fill, self.n_obj
+        B = grid.n_bins
+        P = arr.n_pin
+        g = self.gp = _lib.Gp()
+        g.n_inst, g.n_fill, g.n_obj = I, F, O
+        macro_ids = np.flatnonzero(arr.is_macro).astype(np.int32)
+        g.n_macro = len(macro_ids)
+        if g.n_macro > K_MAX_BLOCKS:
+            raise ValueError(f"{g.n_macro} macros exceed the per-launch CTA budget {K_MAX_BLOCKS}")
+        mi = max(self.max_iters, 1)
+        g.max_iters = self.max_iters
+        g.divergence_window = int(cfg.divergence_window)
+        g.nblk_obj = max(1, min(-(-O // 256), K_MAX_BLOCKS))
+        g.nblk_net = max(1, min(-(-max(arr.n_net, 1) // 256), K_MAX_BLOCKS))
+        tp = dt.struct
+        g.topo = _lib.Topology(tp.n_net, tp.n_pin, I, 0, tp.net_ptr, tp.pin_inst, tp.net_dup,
+                               tp.net_order, tp.pin_slot, tp.obj_slot_ptr)
+        gs, gkeep = grid.device()
+        g.grid = gs
+        self._gkeep = gkeep
+        self.t_pin_off = _dev.f64(wl.rotated_pin_offsets(arr, self.rot) if P else np.zeros((1, 4)))
+        g.pin_off = keep(self.t_pin_off)
+        g.w_top = keep(_dev.f64(self.w_top if I else np.zeros(1)))
+        g.h_top = keep(_dev.f64(self.h_top if I else np.zeros(1)))
+        g.w_bot = keep(_dev.f64(self.w_bot if I else np.zeros(1)))
+        g.h_bot = keep(_dev.f64(self.h_bot if I else np.zeros(1)))
+        g.is_macro = keep(_dev.u8(arr.is_macro if I else np.zeros(1, bool)))
+        g.degree = keep(_dev.f64(arr.pin_degree.astype(np.float64) if I else np.zeros(1)))
+        fl = self.fillers
+        g.fill_w = keep(_dev.f64(fl.w if F else np.zeros(1)))
+        g.fill_h = keep(_dev.f64(fl.h if F else np.zeros(1)))
+        g.fill_z = keep(_dev.f64(fl.z if F else np.zeros(1)))
+        g.macro_ids = keep(_dev.i32(macro_ids if len(macro_ids) else np.zeros(1, np.int32)))
+        gam = [gamma_schedule(grid, it, self.max_iters, cfg) for it in range(mi)]
+        g.gamma_tab = keep(_dev.f64(np.asarray(gam, dtype=np.float64)))
+        g.alpha = self.alpha
+        g.target_density = cfg.target_density
+        g.movable_volume = self.movable_volume
+        g.stop_overflow = cfg.stop_overflow
+        g.mu_min, g.mu_max = cfg.mu_min, cfg.mu_max
+        g.gamma0 = cfg.gamma_start_factor * grid.db
+        g.gamma1 = cfg.gamma_end_factor * grid.db
+        g.min_step = 1e-18
+        g.step_scale = grid.wb
+        g.rho_t_fx = int(np.rint(cfg.target_density * np.ldexp(1.0, dn.FX_BITS)))
+        z = lambda n: torch.zeros(max(int(n), 1), dtype=torch.float64, device="cuda")  # noqa: E731
+        self.t_u, self.t_v, self.t_vprev, self.t_best = z(3 * O), z(3 * O), z(3 * O), z(3 * O)
+        self.t_wl, self.t_dens, self.t_pre = z(3 * O), z(3 * O), z(3 * O)
+        self.t_prev_wl, self.t_prev_dens, self.t_prev_q = z(3 * O), z(3 * O), z(O)
+        self.t_pin_out = z(4 * P)
+        self.t_inst_g = z(4 * I)
+        self.t_rho_fx = torch.zeros(B, dtype=torch.int64, device="cuda")
+        self.t_rho = z(B)
+        self.t_spec = z(6 * B)
+        self.t_maps = z(4 * B)
+        self.t_partials = z(16 * K_PARTIAL_STRIDE)
+        self.t_st = torch.zeros(C.sizeof(_lib.LoopState), dtype=torch.uint8, device="cuda")
+        self.t_log = z(4 * mi)
+        self.t_hist = z(mi)
+        for name, t in (("u", self.t_u), ("v", self.t_v), ("v_prev", self.t_vprev),
+                        ("best", self.t_best), ("wl_grad", self.t_wl), ("dens_grad", self.t_dens),
+                        ("pre", self.t_pre), ("prev_wl", self.t_prev_wl),
+                        ("prev_dens", self.t_prev_dens), ("prev_q", self.t_prev_q),
+                        ("pin_out", self.t_pin_out), ("inst_g", self.t_inst_g),
+                        ("rho_fx", self.t_rho_fx), ("rho", self.t_rho),
+                        ("spec_scratch", self.t_spec), ("maps", self.t_maps),
+                        ("partials", self.t_partials), ("st", self.t_st), ("log", self.t_log),
+                        ("ovfl_hist", self.t_hist)):
+            setattr(g, name, keep(t))
+        self._st_host = torch.empty(C.sizeof(_lib.LoopState), dtype=torch.uint8, pin_memory=True)
+
+    # -- helpers ------------------------------------------------------------
+    def _soa(self, pos):
+        """[O,3] (numpy or tensor) -> [3*O] SoA device tensor."""
+        p = _dev.f64(pos).reshape(self.n_obj, 3)
+        return p.t().contiguous().reshape(-1)
+
+    def _aos(self, soa):
+        return soa[: 3 * self.n_obj].reshape(3, self.n_obj).t().contiguous()
+
+    def state(self):
+        """Copy of the device loop state (synchronises)."""
+        self._st_host.copy_(self.t_st)
+        return _lib.LoopState.from_buffer_copy(bytes(self._st_host.numpy()))
+
+    # -- reference API ---------------------------------------------------------
+    def cloud(self, pos):
+        """ChargeCloud at pos [O,3] (gp.py:267-278), CUDA tensors."""
+        p = _dev.f64(pos).reshape(self.n_obj, 3)
+        w, h = dn.dynamic_size(self.w_top, self.h_top, self.w_bot, self.h_bot, self.arr.is_macro,
+                               p[: self.n_inst, 2], self.grid.dz)
+        return dn.ChargeCloud(
+            x=p[:, 0], y=p[:, 1], z=p[:, 2],
+            w=torch.cat([w, _dev.f64(self.fillers.w)]), h=torch.cat([h, _dev.f64(self.fillers.h)]),
+            dep=torch.full((self.n_obj,), self.grid.dz / 2, dtype=torch.float64, device="cuda"),
+            weight=_dev.f64(self.weight), is_macro=self.is_macro_obj)
+
+    def project(self, pos):
+        """gp.py:280-294 on the device; [O,3] -> [O,3] tensor."""
+        src = self._soa(pos)
+        out = torch.empty_like(src)
+        _lib.call("p3d_gp_project", _lib.byref(self.gp), _lib.ptr(src), _lib.ptr(out),
+                  _lib.stream_ptr())
+        return self._aos(out)
+
+    def evaluate(self, pos, lam, gamma):
+        """gp.py:296-341: (GradientBundle, overflow, exact WL, crossings)."""
+        self.t_v.copy_(self._soa(pos))
+        self.t_rho_fx.zero_()
+        _lib.call("p3d_gp_evaluate", _lib.byref(self.gp), float(lam), float(gamma),
+                  _lib.stream_ptr())
+        st = self.state()
+        if st.nonfinite or not math.isfinite(st.value):
+            raise FloatingPointError("non-finite objective or gradient")
+        wl_g = self._aos(self.t_wl)
+        dg = self._aos(self.t_dens)
+        total = wl_g + lam * dg
+        q = self.cloud(pos).charge
+        _, div = precondition(total, lam, q, self.degree_obj, self.is_macro_obj)
+        bundle = GradientBundle(wl_grad=wl_g, dens_grad=dg, total=total, divisors=div,
+                                value=st.value, wl_value=st.wl_value, energy=st.energy)
+        return bundle, st.ovfl, st.exact, int(st.ncross)
+
+    # -- fused loop ---------------------------------------------------------------
+    def init_loop(self, pos0):
+        src = self._soa(pos0)
+        _lib.call("p3d_gp_init", _lib.byref(self.gp), _lib.ptr(src), _lib.stream_ptr())
+
+    def iterate(self, n=1):
+        for _ in range(n):
+            _lib.call("p3d_gp_iterate", _lib.byref(self.gp), _lib.stream_ptr())
+
+    def capture(self, iters_per_graph=8):
+        """CUDA graph of `iters_per_graph` iterations (replayable; each
+        iteration is a no-op once the device loop is done)."""
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self.iterate(iters_per_graph)
+        torch.cuda.current_stream().wait_stream(s)
+        return g
+
+    def run(self, pos0, use_graph=True, iters_per_graph=8, poll_every=4):
+        """Initialise and run the loop to completion (max_iters or an exit)."""
+        self.init_loop(pos0)
+        total = self.max_iters
+        if not use_graph:
+            done_calls = 0
+            while done_calls < total:
+                k = min(iters_per_graph, total - done_calls)
+                self.iterate(k)
+                done_calls += k
+                if (done_calls // k) % poll_every == 0 and self.state().done:
+                    break
+            return self.state()
+        g = self.capture(iters_per_graph)
+        replays = -(-total // iters_per_graph)
+        for r in range(replays):
+            g.replay()
+            if (r + 1) % poll_every == 0 and self.state().done:
+                break
+        return self.state()
+
+    def log_rows(self, n):
+        rows = self.t_log[: 4 * n].reshape(n, 4).cpu().numpy()
+        return [(int(r[0]), float(r[1]), int(r[2]), float(r[3])) for r in rows]
+
+
+def run_gp3d(design, state: PlacementState, cfg: GpConfig, grid=None, iteration_log=None,
+             rng=None, use_graph=True):
+    """3D global placement (gp.py:359-455) with the whole loop on the device.
+    On exit z is rounded to the die planes; returns (state, GpInfo)."""
+    rng = rng or np.random.default_rng(cfg.seed)
+    grid = grid or choose_grid(design, cfg)
+    if state.fillers is None:
+        state.fillers = make_fillers(design, grid, rng)
+    state.dz = grid.dz
+    prob = Gp3dProblem(design, grid, state.fillers, cfg, state.rot)
+    n = prob.n_inst
+    pos0 = np.zeros((prob.n_obj, 3))
+    pos0[:n] = np.c_[state.x, state.y, state.z]
+    pos0[n:] = np.c_[state.fillers.x, state.fillers.y, state.fillers.z]
+    st = prob.run(pos0, use_graph=use_graph)
+    info = GpInfo(iterations=st.iterations, final_overflow=st.final_overflow,
+                  diverged=bool(st.diverged), wirelength=st.wirelength, hbt_count=st.hbt_count)
+    if st.diverged:
+        log.warning("gp3d: loop exited early (non-finite, divergence or step underflow); "
+                    "returning best state")
+    if iteration_log is not None:
+        iteration_log.extend(prob.log_rows(st.iterations))
+    src = prob.t_u if info.final_overflow <= cfg.stop_overflow else prob.t_best
+    fin = torch.empty_like(src)
+    _lib.call("p3d_gp_project", _lib.byref(prob.gp), _lib.ptr(src), _lib.ptr(fin),
+              _lib.stream_ptr())
+    final = prob._aos(fin).cpu().numpy()
+    state.x = final[:n, 0].copy()
+    state.y = final[:n, 1].copy()
+    state.z = final[:n, 2].copy()
+    state.fillers.x = final[n:, 0].copy()
+    state.fillers.y = final[n:, 1].copy()
+    delta = partition_from_z(state.z, grid.dz)
+    state.z = np.where(delta == 1, 3 * grid.dz / 4, grid.dz / 4)
+    return state, info
+
+
+__all__ = [
+    "GpConfig", "GpInfo", "GradientBundle", "StepUnderflow", "choose_grid", "alpha_value",
+    "select_flow", "init_state", "make_fillers", "precondition", "lambda_init",
+    "mu_from_overflow", "gamma_schedule", "NesterovOptimizer", "Gp3dProblem", "run_gp3d",
+]

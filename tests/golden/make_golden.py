@@ -1,0 +1,148 @@
+"""Generate the golden fixtures from the REFERENCE implementation itself.
+
+Run in the build container (where /root/reference is importable):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--big]
+
+Writes, next to this script:
+  synth_checksums.json   sha256 of every NetlistArrays field for several specs,
+                         from place3d.synth.gen_synthetic -> parse_design
+                         (pins the fast generator paper_2403_09070_b200.synth)
+  small_ops.npz          per-op inputs/outputs of one Gp3dProblem.evaluate on a
+                         2,000-instance design at its initial state
+                         (pins oracle.port op by op)
+  small_log.json         60-iteration run_gp3d log rows of that design
+  cfg1_log.json          config-1 (10k cells, 128x128x2) 200-iteration log rows
+  cfg2_log.json          (--big) config-2 (100k cells, 256x256x2) 200-iteration rows
+The reference is never imported at test time or on the GPU box.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from place3d import density as rdn  # noqa: E402
+from place3d import gp as rgp  # noqa: E402
+from place3d import wirelength as rwl  # noqa: E402
+from place3d.model import parse_design  # noqa: E402
+from place3d.synth import SynthSpec, gen_synthetic  # noqa: E402
+
+FIELDS = ["is_macro", "w_top", "h_top", "w_bot", "h_bot", "net_ptr", "pin_inst", "pin_net",
+          "ox_top", "oy_top", "ox_bot", "oy_bot", "pin_degree", "net_has_dup_inst"]
+
+SPECS = {
+    "tiny": dict(n_insts=60, n_macros=2, r_ma=0.25, seed=0),
+    "small": dict(n_insts=2000, n_macros=6, r_ma=0.30, seed=3, nets_per_inst=1.2),
+    "cfg1": dict(n_insts=10_008, n_macros=8, r_ma=0.30, seed=1, nets_per_inst=1.2),
+    "cfg2": dict(n_insts=100_032, n_macros=32, r_ma=0.30, seed=1, nets_per_inst=1.1),
+}
+
+
+def digest(a):
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.tobytes()).hexdigest() + f":{a.dtype}:{a.shape}"
+
+
+def design_of(name):
+    return parse_design(gen_synthetic(SynthSpec(**SPECS[name])))
+
+
+def checksums():
+    out = {}
+    for name in SPECS:
+        d = design_of(name)
+        a = d.arrays()
+        out[name] = {
+            "spec": SPECS[name],
+            "die": [d.die.width, d.die.height, d.die.row_height_top, d.die.row_height_bottom,
+                    d.die.max_util_top, d.die.max_util_bottom],
+            "hbt": [d.hbt.pitch, d.hbt.spacing, d.hbt.cost],
+            "fields": {f: digest(getattr(a, f)) for f in FIELDS},
+        }
+    with open(os.path.join(HERE, "synth_checksums.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
+def setup(d, nx, nz, max_iters, seed=1):
+    cfg = rgp.GpConfig(seed=seed, nz=nz, grid_nx=nx, grid_ny=nx, max_iters=max_iters,
+                       stop_overflow=0.0)
+    rng = np.random.default_rng(seed)
+    grid = rgp.choose_grid(d, cfg)
+    st = rgp.init_state(d, grid, cfg, rng)
+    st.fillers = rgp.make_fillers(d, grid, rng)
+    return cfg, rng, grid, st
+
+
+def small_ops():
+    d = design_of("small")
+    cfg, rng, grid, st = setup(d, 64, 2, 60)
+    prob = rgp.Gp3dProblem(d, grid, st.fillers, cfg, st.rot)
+    n = prob.n_inst
+    pos = np.zeros((prob.n_obj, 3))
+    pos[:n] = np.c_[st.x, st.y, st.z]
+    pos[n:] = np.c_[st.fillers.x, st.fillers.y, st.fillers.z]
+    pos = prob.project(pos)
+    arr = d.arrays()
+    topo = rwl.NetTopology.from_arrays(arr)
+    gamma = 2 * grid.db
+    px, py, pz, top = rwl.dynamic_pin_coords(arr, pos[:n, 0], pos[:n, 1], pos[:n, 2], st.rot,
+                                             grid.dz)
+    bx = rwl.NetBoxes(topo, px, top)
+    by = rwl.NetBoxes(topo, py, top)
+    wl_v, gxp, gyp = rwl.planar_objective(topo, px, py, top, gamma)
+    cut_v, gcp = rwl.z_cut_penalty(topo, pz, gamma)
+    gzb = rwl.fd_z_gradient_incremental(topo, px, py, top, grid.dz, arr.net_has_dup_inst)
+    cloud = prob.cloud(pos)
+    rho = rdn.accumulate_density(grid, cloud)
+    phi, coef = rdn.solve_potential(rho, grid)
+    ex, ey, ez = rdn.electric_field(coef, grid)
+    energy = rdn.density_energy(grid, cloud, phi)
+    force = rdn.density_force(grid, cloud, ex, ey, ez, freeze_z=prob.freeze_z)
+    bundle, ovfl, exact, ncross = prob.evaluate(pos, 1e-3, gamma)
+    pre, div = rgp.precondition(bundle.total, 1e-3, cloud.charge, prob.degree_obj,
+                                prob.is_macro_obj)
+    np.savez_compressed(
+        os.path.join(HERE, "small_ops.npz"),
+        pos=pos, gamma=gamma, px=px, py=py, pz=pz, top=top,
+        bx_cnt=bx.cnt, bx_min1=bx.min1, bx_min2=bx.min2, bx_max1=bx.max1, bx_max2=bx.max2,
+        by_cnt=by.cnt, by_min1=by.min1, by_min2=by.min2, by_max1=by.max1, by_max2=by.max2,
+        wl_value=wl_v, gx_pin=gxp, gy_pin=gyp, cut_value=cut_v, gcut_pin=gcp, gz_bist=gzb,
+        rho=rho, phi=phi, coef=coef, ex=ex, ey=ey, ez=ez, energy=energy, force=force,
+        wl_grad=bundle.wl_grad, dens_grad=bundle.dens_grad, total=bundle.total,
+        value=bundle.value, ovfl=ovfl, exact=exact, ncross=ncross, pre=pre, div=div,
+        movable_volume=prob.movable_volume, alpha=prob.alpha,
+    )
+    rows = []
+    rgp.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+    with open(os.path.join(HERE, "small_log.json"), "w") as fh:
+        json.dump({"spec": SPECS["small"], "grid": 64, "nz": 2, "max_iters": 60,
+                   "rows": [list(map(float, r)) for r in rows]}, fh)
+
+
+def loop_rows(name, nx, out):
+    d = design_of(name)
+    cfg, rng, grid, st = setup(d, nx, 2, 200)
+    rows = []
+    t = time.perf_counter()
+    rgp.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+    dt = time.perf_counter() - t
+    with open(os.path.join(HERE, out), "w") as fh:
+        json.dump({"spec": SPECS[name], "grid": nx, "nz": 2, "max_iters": 200,
+                   "seconds_1core": dt, "rows": [list(map(float, r)) for r in rows]}, fh)
+
+
+if __name__ == "__main__":
+    checksums()
+    small_ops()
+    loop_rows("cfg1", 128, "cfg1_log.json")
+    if "--big" in sys.argv:
+        loop_rows("cfg2", 256, "cfg2_log.json")
