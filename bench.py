@@ -1,0 +1,344 @@
+"""GP inner-loop benchmark (BASELINE.json metric: GP iterations/sec at 800k
+cells; % of HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+
+One step = one full global-placement iteration (gp.py:386-444: WL + density +
+field + preconditioner + Nesterov/BB step) on the synthetic config-3 design
+(800,064 instances, 850k nets, 512x512x2 bins).  Under
+torchrun every rank runs an independent placement replica (seed 1 + rank):
+weak scaling, no data-path collective; the timed region is bracketed by
+barriers and the max over ranks is reported.  Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    1: "cfg1: synthetic 2-die F2F, 10,008 cells (8 macros), 12,010 nets, 128x128x2 bins",
+    2: "cfg2: synthetic 100,032 cells (32 macros), 110k nets, 256x256x2 bins",
+    3: "cfg3: synthetic ICCAD-2023-case4-scale, 800,064 cells (64 macros), 850k nets, 512x512x2 bins",
+}
+METRIC = "GP iterations/sec at 800k cells (WL+density+field+step); % HBM roofline"
+
+
+def rank_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def setup_design(config, rank):
+    from paper_2403_09070_b200.synth import CONFIGS, cached_synth, SynthSpec
+
+    c = CONFIGS[config]
+    spec = c["spec"]
+    if rank:
+        spec = SynthSpec(**{**spec.__dict__, "seed": spec.seed + rank})
+    return cached_synth(spec), c["grid"], spec
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def algorithmic_bytes(design, n_fill, grid_bins):
+    """compulsory bytes per iteration per kernel family."""
+    a = design.arrays()
+    N, P, I, F, B = a.n_net, a.n_pin, a.n_inst, n_fill, grid_bins
+    O = I + F
+    return {
+        "K1": 4 * N + 20 * P + 40 * I,
+        "K2": 24 * O + 16 * I + 8 * F + 8 * B,
+        "K3": 24 * B,
+        "K4": 36 * O + 16 * I + 8 * F + 16 * B,
+        "K5": 152 * O + 60 * I + 8 * F,
+    }
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_baseline(design, grid_n, spec, seconds=20.0, max_iters=200):
+    """Oracle port (numpy, 1 core) on the same workload: bounded sample of
+    whole GP iterations (setup excluded)."""
+    from oracle import port as P
+
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    cfg = P.Cfg(seed=spec.seed, nz=2, grid_nx=grid_n, grid_ny=grid_n, max_iters=max_iters,
+                stop_overflow=0.0)
+    rng = np.random.default_rng(spec.seed)
+    g = P.grid_for(design, cfg)
+    x, y, z, rot = P.start_state(design, g, cfg, rng)
+    fill = P.fillers_for(design, g, rng)
+    prob = P.Problem(design, g, fill, cfg, rot)
+    n = prob.n_inst
+    pos0 = np.zeros((prob.n_obj, 3))
+    pos0[:n] = np.c_[x, y, z]
+    pos0[n:] = np.c_[fill.x, fill.y, fill.z]
+    opt = P.Nesterov(pos0, project=prob.project)
+    it, t0, lam = 0, time.perf_counter(), None
+    # same per-iteration body as oracle.port.run_loop, timed iteration by iteration
+    prev_raw, prev_ovfl = None, float("inf")
+    while True:
+        gamma = P.gamma_at(g.db, it, cfg.max_iters, cfg)
+        ev, ovfl, exact, nc = prob.evaluate(opt.v, lam or 0.0, gamma)
+        if lam is None:
+            lam = P.lam0(np.abs(ev.wl_grad).sum(), np.abs(ev.dens_grad).sum())
+            ev.total = ev.wl_grad + lam * ev.dens_grad
+        q = prob.cloud(opt.v).charge
+        pre, _ = P.precond(ev.total, lam, q, prob.degree_obj, prob.is_macro_obj)
+        pp = None
+        if prev_raw is not None:
+            pp, _ = P.precond(prev_raw[0] + lam * prev_raw[1], lam, prev_raw[2], prob.degree_obj,
+                              prob.is_macro_obj)
+        prev_raw = (ev.wl_grad, ev.dens_grad, q)
+        opt.advance(pre, step_scale=g.wb, g_prev_reval=pp)
+        lam *= P.mu_of(prev_ovfl, ovfl, cfg)
+        prev_ovfl = ovfl
+        it += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or it >= max_iters:
+            break
+    return it / el, it, el
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU implementation of the path (oracle port of the
+    reference numpy code; the Python reference itself cannot travel to the GPU
+    box) on rank 0's host cores."""
+    if rank != 0:
+        return
+    design, grid_n, spec = setup_design(args.config, 0)
+    budget = min(60.0, 6.0 * (args.steps + args.warmup))
+    rate, iters, el = cpu_baseline(design, grid_n, spec, seconds=budget)
+    ncpu = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "it/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / rate,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOADS[args.config], "grid": [grid_n] * 2 + [2],
+                                        "max_iters_schedule": 200},
+        "cpu_baseline": {"value": rate, "unit": "it/s", "cores": 1, "kind": "port",
+                         "sample": f"{iters} GP iterations from the initial state ({el:.1f} s), "
+                                   f"numpy single-threaded, host has {ncpu} cpus"},
+        "e2e": {"value": rate, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = rank_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2403_09070_b200 import _lib
+    from paper_2403_09070_b200 import gp as G
+
+    design, grid_n, spec = setup_design(args.config, rank)
+    W, K = max(args.warmup, 3), args.steps
+    max_iters = max(200, W + 2 * K + 2)
+    cfg = G.GpConfig(seed=spec.seed, nz=2, grid_nx=grid_n, grid_ny=grid_n, max_iters=max_iters,
+                     stop_overflow=0.0)
+    rng = np.random.default_rng(spec.seed)
+    grid = G.choose_grid(design, cfg)
+    st = G.init_state(design, grid, cfg, rng)
+    st.fillers = G.make_fillers(design, grid, rng)
+    prob = G.Gp3dProblem(design, grid, st.fillers, cfg, st.rot)
+    n = prob.n_inst
+    pos0 = np.zeros((prob.n_obj, 3))
+    pos0[:n] = np.c_[st.x, st.y, st.z]
+    pos0[n:] = np.c_[st.fillers.x, st.fillers.y, st.fillers.z]
+    stream = torch.cuda.current_stream()
+
+    # ---- device-resident timed region: graph replays of one iteration
+    prob.init_loop(pos0)
+    graph = prob.capture(1)
+    for _ in range(W):
+        graph.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(K):
+            graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    s = prob.state()
+    assert not s.done and s.it == W + K, f"loop ended early (it={s.it}, done={s.done})"
+
+    # ---- per-stage attribution (same state continues; events between stages)
+    stage = np.zeros(7)
+    buf = (C.c_float * 7)()
+    for _ in range(K):
+        _lib.call("p3d_gp_iterate_profiled", _lib.byref(prob.gp), _lib.stream_ptr(), buf)
+        stage += np.frombuffer(buf, dtype=np.float32)
+    stage /= K
+    kpi = _lib.load().p3d_gp_kernels_per_iteration(_lib.byref(prob.gp))
+
+    # ---- end to end through the public API: pinned host state in, K steps with
+    # the per-iteration log row read back every step, final positions out
+    host_pos = torch.from_numpy(pos0).pin_memory()
+    host_row = torch.empty(4, dtype=torch.float64).pin_memory()
+    host_out = torch.empty((prob.n_obj, 3), dtype=torch.float64).pin_memory()
+    dev_pos = torch.empty((prob.n_obj, 3), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    dev_pos.copy_(host_pos, non_blocking=True)
+    prob.init_loop(dev_pos)
+    for k in range(K):
+        graph.replay()
+        host_row.copy_(prob.t_log[4 * k: 4 * k + 4], non_blocking=True)
+    host_out.copy_(prob._aos(prob.t_u), non_blocking=True)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    if world > 1:
+        dist.barrier()
+
+    # max over ranks
+    t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, e2e_ms = float(t[0]), float(t[1])
+    if rank != 0:
+        dist.destroy_process_group() if world > 1 else None
+        return
+    it_s = world * K / (ms / 1000.0)
+    e2e_it_s = world * K / (e2e_ms / 1000.0)
+
+    # roofline of the dominant kernel family (SURVEY 8d algorithmic bytes)
+    q = algorithmic_bytes(design, prob.n_fill, grid.n_bins)
+    fam_ms = {"K1": stage[0] + stage[1], "K2": stage[2], "K3": stage[3], "K4": stage[4],
+              "K5": stage[5] + stage[6]}
+    dom = max(fam_ms, key=fam_ms.get)
+    peak, peak_kind = load_peaks()
+    achieved = q[dom] / (fam_ms[dom] / 1000.0) / 1e9
+    per_family = {k: {"ms": round(float(v), 4), "alg_MB": round(q[k] / 1e6, 2),
+                      "GBs": round(q[k] / (v / 1000.0) / 1e9, 1) if v > 0 else None}
+                  for k, v in fam_ms.items()}
+    ws_mb = (sum(t.numel() * t.element_size() for t in prob._keep.items) +
+             sum(t.numel() * t.element_size() for t in prob._dtopo.keep.items)) / 1e6
+
+    line = {
+        "metric": METRIC, "value": it_s, "unit": "it/s", "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (paper_2403_09070_b200.synth == place3d.synth.gen_synthetic, seed 1+rank)",
+        "config": {"workload": WORKLOADS[args.config], "n_inst": n, "n_fill": prob.n_fill,
+                   "n_net": design.n_nets, "n_pin": design.arrays().n_pin,
+                   "grid": [grid.nx, grid.ny, grid.nz], "max_iters_schedule": max_iters,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single",
+                   "l2": f"no flush: iteration working set {ws_mb:.0f} MB > 126 MB L2"},
+        "e2e": {"value": e2e_it_s, "unit": "it/s",
+                "h2d_bytes_per_step": int(host_pos.numel() * 8 / K),
+                "d2h_bytes_per_step": int(32 + host_out.numel() * 8 / K)},
+        "gpu_launches": int(kpi * K),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "peak_kind": peak_kind, "per_family": per_family},
+        "clocks": clocks.summary(),
+        "final_row": list(prob.log_rows(W + K)[-1]),
+    }
+    if not args.no_cpu_baseline:
+        rate, iters, el = cpu_baseline(design, grid_n, spec, seconds=args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": "it/s", "cores": 1, "kind": "port",
+                                "sample": f"{iters} GP iterations of the same workload from the "
+                                          f"initial state ({el:.1f} s), oracle.port numpy, 1 thread"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

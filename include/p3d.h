@@ -227,6 +227,13 @@ int p3d_gp_iterate(const p3d_gp* gp, void* stream);
  * gamma, filling wl_grad, dens_grad, rho_fx -> maps and the st result fields
  * (no optimiser step, loop control untouched). */
 int p3d_gp_evaluate(const p3d_gp* gp, double lam, double gamma, void* stream);
+/* p3d_gp_iterate with a CUDA event between the stages K1 (net), K1b (owner
+ * gather), K2 (scatter), K3 (spectral), K4 (density gather + assembly),
+ * K5a (precondition/BB), K5b (advance); stage_ms: HOST float[7].  Blocks until
+ * the iteration finishes.  Not capturable (benchmark attribution only). */
+int p3d_gp_iterate_profiled(const p3d_gp* gp, void* stream, float* stage_ms);
+/* Number of kernels one p3d_gp_iterate enqueues (>0), or -1 on bad input. */
+int p3d_gp_kernels_per_iteration(const p3d_gp* gp);
 /* Gp3dProblem.project (gp.py:280-294): out = P(in), [3][n_obj]. */
 int p3d_gp_project(const p3d_gp* gp, const double* in, double* out, void* stream);
 

@@ -371,7 +371,7 @@ def _stamp_iter(grid, xs, ys, zs):
             for bz in (0, 1):
                 gk, gz = k0 + bz, (fz if bz else 1.0 - fz)
                 ok = oky & (gk >= 0) & (gk < grid.nz)
-                yield gi, gj, gk, gx * gy * gz, ok
+                yield gi, gj, gk, (gx, gy, gz), ok
 
 
 def macro_rho(grid, cl):
@@ -384,9 +384,9 @@ def macro_rho(grid, cl):
     zs = np.concatenate([c[2] for c in cs])
     ws = np.concatenate([np.full(len(cl.x), c[3]) * cl.weight for c in cs])
     a = np.zeros(grid.shape)
-    for gi, gj, gk, g, ok in _stamp_iter(grid, xs, ys, zs):
+    for gi, gj, gk, (gx, gy, gz), ok in _stamp_iter(grid, xs, ys, zs):
         if ok.any():
-            np.add.at(a, (gi[ok], gj[ok], gk[ok]), (ws * g)[ok])
+            np.add.at(a, (gi[ok], gj[ok], gk[ok]), (ws * gx * gy * gz)[ok])
     return np.cumsum(np.cumsum(np.cumsum(a, axis=0), axis=1), axis=2)
 
 
@@ -434,7 +434,7 @@ def _sin_series(c, axis):
     return sfft.dst(d, type=3, axis=axis)
 
 
-def field(coef, grid):
+def efield(coef, grid):
     """density.py:357-368: E = -grad(phi), evaluated from true cosine-series
     coefficients a = coef / N with every index-0 plane halved."""
     a = coef / (grid.nx * grid.ny * grid.nz)
@@ -480,10 +480,10 @@ def macro_means(grid, cl, smap):
     acc = np.zeros(len(cl.x))
     for xs, ys, zs, sign in _corners(grid, cl):
         dot = np.zeros(len(xs))
-        for gi, gj, gk, g, ok in _stamp_iter(grid, xs, ys, zs):
+        for gi, gj, gk, (gx, gy, gz), ok in _stamp_iter(grid, xs, ys, zs):
             if ok.any():
                 part = np.zeros(len(xs))
-                part[ok] = smap[gi[ok], gj[ok], gk[ok]] * g[ok]
+                part[ok] = smap[gi[ok], gj[ok], gk[ok]] * (gx * gy * gz)[ok]
                 dot += part
         acc += sign * dot
     return acc * grid.bin_vol / np.maximum(cl.volume, 1e-300)
@@ -766,7 +766,7 @@ class Problem:
         cl = self.cloud(pos)
         rho = rho_map(g, cl)
         phi, coef = potential(rho, g)
-        ex, ey, ez = field(coef, g)
+        ex, ey, ez = efield(coef, g)
         en = energy(g, cl, phi)
         dg = force(g, cl, ex, ey, ez, freeze_z=self.freeze_z)
         value = wl_bi + self.alpha * cut + lam * en

@@ -95,6 +95,8 @@ _SIGS = {
     "p3d_gp_iterate": (I32, [P, P]),
     "p3d_gp_evaluate": (I32, [P, D, D, P]),
     "p3d_gp_project": (I32, [P, P, P, P]),
+    "p3d_gp_iterate_profiled": (I32, [P, P, P]),
+    "p3d_gp_kernels_per_iteration": (I32, [P]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -49,6 +49,8 @@ int gp_iterate(const p3d_gp& gp, cudaStream_t s);
 int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s);
 int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s);
 int gp_project(const p3d_gp& gp, const double* in, double* out, cudaStream_t s);
+int gp_iterate_profiled(const p3d_gp& gp, cudaStream_t s, float* ms);
+int gp_kernels_per_iteration(const p3d_gp& gp);
 
 static NetArgs net_args(const p3d_topology* t) {
   NetArgs a{};
@@ -303,6 +305,16 @@ int p3d_gp_init(const p3d_gp* gp, const double* pos0, void* stream) {
 int p3d_gp_iterate(const p3d_gp* gp, void* stream) {
   if (bad_gp(gp)) return P3D_ERR_ARG;
   return gp_iterate(*gp, STREAM(stream));
+}
+
+int p3d_gp_iterate_profiled(const p3d_gp* gp, void* stream, float* stage_ms) {
+  if (bad_gp(gp) || !stage_ms) return P3D_ERR_ARG;
+  return gp_iterate_profiled(*gp, STREAM(stream), stage_ms);
+}
+
+int p3d_gp_kernels_per_iteration(const p3d_gp* gp) {
+  if (bad_gp(gp)) return -1;
+  return gp_kernels_per_iteration(*gp);
 }
 
 int p3d_gp_evaluate(const p3d_gp* gp, double lam, double gamma, void* stream) {

@@ -426,7 +426,9 @@ __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
-static void eval_kernels(const p3d_gp& gp, cudaStream_t s) {
+static void eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = nullptr) {
+  auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], s); };
+  mark(0);
   p3d_loop_state* st = gp.st;
   const int* halt = &st->done;
   double* finals = gp.partials + (long long)kSlotFinal * kPartialStride;
@@ -450,6 +452,7 @@ static void eval_kernels(const p3d_gp& gp, cudaStream_t s) {
   na.halt = halt;
   const long long O = gp.n_obj;
   launch_net_pos(na, gp.v, gp.v + O, gp.v + 2 * O, gp.pin_off, gp.grid.dz, s);
+  mark(1);
   // K1b
   GatherArgs ga{};
   ga.n_obj = gp.n_inst;
@@ -462,6 +465,7 @@ static void eval_kernels(const p3d_gp& gp, cudaStream_t s) {
   ga.final_norms = finals + kFinNorm;
   ga.halt = halt;
   launch_gather(ga, s);
+  mark(2);
   // K2
   CloudGP cl;
   cl.pos = gp.v;
@@ -473,6 +477,7 @@ static void eval_kernels(const p3d_gp& gp, cudaStream_t s) {
   cl.dz = gp.grid.dz;
   cl.target_density = gp.target_density;
   launch_scatter(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, gp.rho_fx, halt, s);
+  mark(3);
   // K3 (+ overflow, re-zero)
   SpecOvfl ov;
   ov.zero = 1;
@@ -483,8 +488,10 @@ static void eval_kernels(const p3d_gp& gp, cudaStream_t s) {
   ov.scale = gp.movable_volume > 0 ? 9.094947017729282379150390625e-13 * gp.grid.bin_vol / gp.movable_volume : 0.0;
   launch_spectral_ex(&gp.grid, nullptr, gp.rho_fx, nullptr, nullptr, gp.maps, gp.spec_scratch,
                      halt, &ov, s);
+  mark(4);
   // K4
   dens_kernel<<<gp.n_macro + gp.nblk_obj, 256, 0, s>>>(gp);
+  mark(5);
 }
 
 int gp_iterate(const p3d_gp& gp, cudaStream_t s) {
@@ -492,6 +499,28 @@ int gp_iterate(const p3d_gp& gp, cudaStream_t s) {
   step_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
   advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
   return check_launch("gp_iterate");
+}
+
+// Same launches with an event between stages (host-synchronising; used by the
+// benchmark to attribute iteration time to K1..K5, never inside a graph).
+int gp_iterate_profiled(const p3d_gp& gp, cudaStream_t s, float* ms) {
+  static cudaEvent_t ev[8] = {nullptr};
+  if (!ev[0])
+    for (int k = 0; k < 8; ++k) cudaEventCreate(&ev[k]);
+  eval_kernels(gp, s, ev);
+  step_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  cudaEventRecord(ev[6], s);
+  advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  cudaEventRecord(ev[7], s);
+  cudaEventSynchronize(ev[7]);
+  for (int k = 0; k < 7; ++k) cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]);
+  return check_launch("gp_iterate_profiled");
+}
+
+// kernels enqueued by one gp_iterate (for the benchmark's launch count)
+int gp_kernels_per_iteration(const p3d_gp& gp) {
+  return 1 /*net*/ + 1 /*gather*/ + 1 + (gp.n_macro > 0) /*scatter*/ + 6 /*spectral*/ +
+         1 /*dens*/ + 2 /*step, advance*/;
 }
 
 int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s) {

@@ -1,0 +1,342 @@
+"""Per-operator parity of the CUDA path (through the C-ABI) against the
+reference's own outputs (tests/golden/small_ops.npz, produced by place3d) and
+the CPU oracle on seeded inputs.
+
+Tolerances: the kernels compute in float64, so WL/density values and
+gradients are compared at 1e-9 relative (north_star asks 1e-5 for fp32);
+box extrema, the finite-difference depth gradient, spans and crossing counts
+are compared bit-exactly; the fixed-point density map bit-exactly against
+oracle.fixed.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import fixed as FX
+from oracle import port as P
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    b = np.asarray(b)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def cpu(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def small():
+    from paper_2403_09070_b200.synth import SynthSpec, synth_arrays
+
+    g = dict(np.load(os.path.join(GOLD, "small_ops.npz")))
+    design = synth_arrays(SynthSpec(n_insts=2000, n_macros=6, r_ma=0.30, seed=3,
+                                    nets_per_inst=1.2))
+    return design, g
+
+
+# ---------------------------------------------------------------------------
+# K1 wirelength
+# ---------------------------------------------------------------------------
+
+
+def test_pin_coords_exact(small):
+    from paper_2403_09070_b200 import wirelength as wl
+
+    d, g = small
+    n = d.n_insts
+    pos = g["pos"]
+    grid = P.Grid(d.die.width, d.die.height, 64, 64, 2)
+    px, py, pz, top = wl.dynamic_pin_coords(d.arrays(), pos[:n, 0], pos[:n, 1], pos[:n, 2],
+                                            np.zeros(n, np.int64), grid.dz)
+    assert np.array_equal(cpu(px), g["px"]) and np.array_equal(cpu(py), g["py"])
+    assert np.array_equal(cpu(pz), g["pz"]) and np.array_equal(cpu(top), g["top"])
+
+
+def test_netboxes_exact(small):
+    from paper_2403_09070_b200 import wirelength as wl
+
+    d, g = small
+    topo = wl.NetTopology.from_arrays(d.arrays())
+    for ax in ("x", "y"):
+        b = wl.NetBoxes(topo, g["p" + ax], g["top"])
+        for f in ("cnt", "min1", "min2", "max1", "max2"):
+            assert np.array_equal(cpu(getattr(b, f)), g[f"b{ax}_{f}"]), (ax, f)
+
+
+def test_planar_objective(small):
+    from paper_2403_09070_b200 import wirelength as wl
+
+    d, g = small
+    topo = wl.NetTopology.from_arrays(d.arrays())
+    v, gx, gy = wl.planar_objective(topo, g["px"], g["py"], g["top"], float(g["gamma"]))
+    assert abs(v - float(g["wl_value"])) <= 1e-12 * abs(float(g["wl_value"]))
+    assert rel(gx, g["gx_pin"]) < 1e-12 and rel(gy, g["gy_pin"]) < 1e-12
+
+
+def test_z_cut_penalty(small):
+    from paper_2403_09070_b200 import wirelength as wl
+
+    d, g = small
+    topo = wl.NetTopology.from_arrays(d.arrays())
+    v, gc = wl.z_cut_penalty(topo, g["pz"], float(g["gamma"]))
+    assert abs(v - float(g["cut_value"])) <= 1e-12 * abs(float(g["cut_value"]))
+    assert rel(gc, g["gcut_pin"]) < 1e-12
+
+
+def test_fd_z_gradient_exact(small):
+    from paper_2403_09070_b200 import wirelength as wl
+
+    d, g = small
+    a = d.arrays()
+    topo = wl.NetTopology.from_arrays(a)
+    grid = P.Grid(d.die.width, d.die.height, 64, 64, 2)
+    gz = wl.fd_z_gradient_incremental(topo, g["px"], g["py"], g["top"], grid.dz,
+                                      a.net_has_dup_inst)
+    assert np.array_equal(cpu(gz), g["gz_bist"])
+
+
+def _make_topo(sizes):
+    from paper_2403_09070_b200 import wirelength as wl
+
+    ptr = np.zeros(len(sizes) + 1, dtype=np.int64)
+    np.cumsum(sizes, out=ptr[1:])
+    n = int(ptr[-1])
+    return wl.NetTopology(ptr, np.repeat(np.arange(len(sizes)), sizes), np.arange(n), n)
+
+
+def _random_net(rng, n, span=100):
+    base = rng.integers(0, span, n).astype(float)
+    if n >= 2 and rng.random() < 0.4:
+        base[rng.integers(0, n)] = base.max()
+    top = rng.random(n) < rng.uniform(0.1, 0.9)
+    return base, top
+
+
+def test_incremental_equals_naive_random():
+    """test_wirelength.py:241-261 on the device: 1,000 random integer nets."""
+    from paper_2403_09070_b200 import wirelength as wl
+
+    rng = np.random.default_rng(6)
+    sizes = [int(rng.integers(1, 10)) for _ in range(1000)]
+    topo = _make_topo(sizes)
+    x = np.zeros(topo.n_pin)
+    y = np.zeros(topo.n_pin)
+    top = np.zeros(topo.n_pin, bool)
+    p = 0
+    for s in sizes:
+        cx, ct = _random_net(rng, s)
+        cy, _ = _random_net(rng, s)
+        x[p:p + s], y[p:p + s], top[p:p + s] = cx, cy, ct
+        p += s
+    naive = wl.fd_z_gradient_naive(topo, x, y, top, 4.0)
+    inc = wl.fd_z_gradient_incremental(topo, x, y, top, 4.0)
+    ref = P.fd_depth_grad_naive(topo.net_ptr, topo.pin_inst, topo.n_obj, x, y, top, 4.0)
+    assert np.array_equal(cpu(naive), cpu(inc))
+    assert np.array_equal(cpu(inc), ref)
+
+
+def test_repeated_instance_and_tie():
+    """test_wirelength.py:264-286."""
+    from paper_2403_09070_b200 import wirelength as wl
+
+    topo = wl.NetTopology(np.array([0, 3]), np.zeros(3, np.int64), np.array([0, 0, 1]), 2)
+    x, y, t = np.array([0.0, 4.0, 2.0]), np.zeros(3), np.array([True, True, False])
+    assert np.array_equal(cpu(wl.fd_z_gradient_naive(topo, x, y, t, 4.0)),
+                          cpu(wl.fd_z_gradient_incremental(topo, x, y, t, 4.0)))
+    topo = _make_topo([3])
+    x, t = np.array([0.0, 5.0, 5.0]), np.array([True, True, True])
+    assert np.array_equal(cpu(wl.fd_z_gradient_naive(topo, x, y, t, 4.0)),
+                          cpu(wl.fd_z_gradient_incremental(topo, x, y, t, 4.0)))
+    # spec example (test_wirelength.py:213-220)
+    topo = _make_topo([4])
+    g = wl.fd_z_gradient_naive(topo, np.array([0.0, 1.0, 2.0, 3.0]), np.zeros(4),
+                               np.array([True, False, True, False]), 4.0)
+    assert cpu(g)[2] == pytest.approx(1.0)
+
+
+def test_known_answers():
+    from paper_2403_09070_b200 import wirelength as wl
+
+    val, _ = wl.wa_smooth([0.0, 10.0], 1.0)
+    assert val == pytest.approx(9.999092042625951, rel=1e-12)  # test_wirelength.py:29-32
+    assert wl.bistratal_axis([0, 1, 2, 3], [True, False, True, False]) == 4  # :129-131
+    assert wl.bistratal_axis([0, 1, 2, 3], [True, True, False, False]) == 3
+    out = wl.normalize_z_gradient(np.array([2.0, 0.0]), np.array([0.0, 2.0]),
+                                  np.array([1.0, 1.0]), np.zeros(2), 0.0)
+    assert np.allclose(cpu(out), [1.0, 1.0])  # :309-314
+    out = wl.normalize_z_gradient(np.array([1.0, 2.0]), np.array([0.5, 0.5]), np.zeros(2),
+                                  np.array([3.0, -1.0]), 0.5)
+    assert np.allclose(cpu(out), [1.5, -0.5])  # :292-299
+
+
+def test_wa_gradient_vs_oracle_random():
+    from paper_2403_09070_b200 import wirelength as wl
+
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        n = int(rng.integers(1, 9))
+        v = rng.uniform(0, 50, n)
+        gamma = rng.uniform(0.5, 5.0)
+        val, g = wl.wa_smooth(v, gamma)
+        rv, rg = P.wa_one(v, gamma)
+        assert val == pytest.approx(rv, rel=1e-12, abs=1e-12)
+        assert np.allclose(cpu(g), rg, rtol=1e-12, atol=1e-14)
+
+
+# ---------------------------------------------------------------------------
+# K2/K3/K4 density
+# ---------------------------------------------------------------------------
+
+
+def _small_cloud(small):
+    d, g = small
+    from paper_2403_09070_b200 import gp as G
+
+    cfg = G.GpConfig(seed=1, nz=2, grid_nx=64, grid_ny=64, max_iters=60, stop_overflow=0.0)
+    rng = np.random.default_rng(1)
+    grid = G.choose_grid(d, cfg)
+    st = G.init_state(d, grid, cfg, rng)
+    fill = G.make_fillers(d, grid, rng)
+    og = P.Grid(d.die.width, d.die.height, 64, 64, 2)
+    ofill = P.Fill(fill.x, fill.y, fill.z, fill.die, fill.w, fill.h, fill.dep)
+    oprob = P.Problem(d, og, ofill, P.Cfg(nz=2, grid_nx=64, max_iters=60, stop_overflow=0.0),
+                      st.rot)
+    return grid, og, oprob.cloud(g["pos"]), oprob, fill, st
+
+
+def test_density_fixed_point_bit_exact(small):
+    from paper_2403_09070_b200 import density as dn
+
+    grid, og, cl, *_ = _small_cloud(small)
+    got = dn.accumulate_density_fx(grid, dn.ChargeCloud(cl.x, cl.y, cl.z, cl.w, cl.h, cl.dep,
+                                                        cl.weight, cl.is_macro))
+    want = FX.fixed_rho(og, cl)
+    assert np.array_equal(cpu(got), want)
+
+
+def test_density_vs_reference(small):
+    from paper_2403_09070_b200 import density as dn
+
+    d, g = small
+    grid, og, cl, *_ = _small_cloud(small)
+    rho = dn.accumulate_density(grid, dn.ChargeCloud(cl.x, cl.y, cl.z, cl.w, cl.h, cl.dep,
+                                                     cl.weight, cl.is_macro))
+    assert np.abs(cpu(rho) - g["rho"]).max() < 1e-9  # brute_density tolerance (test_density.py:120)
+
+
+def test_spectral_vs_reference(small):
+    from paper_2403_09070_b200 import density as dn
+
+    d, g = small
+    grid = dn.DensityGrid(d.die.width, d.die.height, 64, 64, 2)
+    phi, coef = dn.solve_potential(g["rho"], grid)
+    assert rel(coef, g["coef"]) < 1e-12
+    assert rel(phi, g["phi"]) < 1e-10
+    ex, ey, ez = dn.electric_field(g["coef"], grid)
+    for a, k in ((ex, "ex"), (ey, "ey"), (ez, "ez")):
+        assert rel(a, g[k]) < 1e-10, k
+
+
+@pytest.mark.parametrize("shape", [(8, 8, 8), (16, 12, 4), (12, 10, 6), (5, 7, 3), (128, 64, 2)])
+def test_spectral_vs_scipy_shapes(shape):
+    """FFT path (powers of two) and direct path (others) against scipy.fft."""
+    from paper_2403_09070_b200 import density as dn
+
+    nx, ny, nz = shape
+    rng = np.random.default_rng(nx * 100 + ny)
+    grid = dn.DensityGrid(17.0, 13.0, nx, ny, nz)
+    og = P.Grid(17.0, 13.0, nx, ny, nz)
+    rho = rng.uniform(0, 2, (nx, ny, nz))
+    phi, coef = dn.solve_potential(rho, grid)
+    rphi, rcoef = P.potential(rho, og)
+    assert rel(coef, rcoef) < 1e-12 and rel(phi, rphi) < 1e-10
+    e = dn.electric_field(rcoef, grid)
+    re = P.efield(rcoef, og)
+    for a, b in zip(e, re):
+        assert rel(a, b) < 1e-10
+
+
+def test_eigenfunction_and_uniform():
+    """test_density.py:254-294 restated on the device."""
+    from paper_2403_09070_b200 import density as dn
+
+    grid = dn.DensityGrid(8, 8, 8, 8, 8)
+    phi, coef = dn.solve_potential(np.full(grid.shape, 0.7), grid)
+    assert float(phi.abs().max()) < 1e-12
+    grid = dn.DensityGrid(10.0, 10.0, 16, 16, 8)
+    xs = (np.arange(16) + 0.5) * grid.wb
+    X = np.broadcast_to(xs[:, None, None], grid.shape)
+    w1 = grid.omega[0][1]
+    phi, coef = dn.solve_potential(np.cos(w1 * X), grid)
+    ex, ey, ez = dn.electric_field(coef, grid)
+    assert np.abs(cpu(ex) - np.sin(w1 * X) / w1).max() < 1e-9
+    assert float(ey.abs().max()) < 1e-9 and float(ez.abs().max()) < 1e-9
+
+
+def test_energy_force_vs_reference(small):
+    from paper_2403_09070_b200 import density as dn
+
+    d, g = small
+    grid, og, cl, oprob, fill, st = _small_cloud(small)
+    c = dn.ChargeCloud(cl.x, cl.y, cl.z, cl.w, cl.h, cl.dep, cl.weight, cl.is_macro)
+    e = dn.density_energy(grid, c, g["phi"])
+    assert e == pytest.approx(float(g["energy"]), rel=1e-10)
+    f = dn.density_force(grid, c, g["ex"], g["ey"], g["ez"], freeze_z=oprob.freeze_z)
+    assert rel(f, g["force"]) < 1e-10
+
+
+def test_overflow_fixed_point(small):
+    from paper_2403_09070_b200 import density as dn
+
+    d, g = small
+    grid, og, cl, oprob, *_ = _small_cloud(small)
+    acc = FX.fixed_rho(og, cl)
+    import torch
+
+    got = dn.overflow_fx(torch.from_numpy(acc).cuda(), grid, 1.0, oprob.movable_volume)
+    assert got == pytest.approx(float(g["ovfl"]), rel=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# GP problem: evaluate / project / precondition
+# ---------------------------------------------------------------------------
+
+
+def test_evaluate_vs_reference(small):
+    from paper_2403_09070_b200 import gp as G
+
+    d, g = small
+    grid, og, cl, oprob, fill, st = _small_cloud(small)
+    cfg = G.GpConfig(seed=1, nz=2, grid_nx=64, grid_ny=64, max_iters=60, stop_overflow=0.0)
+    prob = G.Gp3dProblem(d, grid, fill, cfg, st.rot)
+    assert prob.movable_volume == float(g["movable_volume"]) and prob.alpha == float(g["alpha"])
+    b, ov, ex, nc = prob.evaluate(g["pos"], 1e-3, float(g["gamma"]))
+    assert nc == int(g["ncross"]) and ex == float(g["exact"])
+    assert ov == pytest.approx(float(g["ovfl"]), rel=1e-12)
+    assert b.value == pytest.approx(float(g["value"]), rel=1e-12)
+    assert rel(b.wl_grad, g["wl_grad"]) < 1e-12
+    assert rel(b.dens_grad, g["dens_grad"]) < 1e-9
+    assert rel(b.total, g["total"]) < 1e-9
+    pre, div = G.precondition(b.total, 1e-3, prob.cloud(g["pos"]).charge, prob.degree_obj,
+                              prob.is_macro_obj)
+    assert rel(pre, g["pre"]) < 1e-9 and rel(div, g["div"]) < 1e-14
+    assert np.array_equal(cpu(prob.project(g["pos"])), oprob.project(g["pos"]))
+
+
+def test_precondition_examples():
+    """test_gp.py:13-26."""
+    from paper_2403_09070_b200 import gp as G
+
+    out, div = G.precondition(np.ones((3, 3)), 1.0, np.array([0.3, 0.3, 7.0]),
+                              np.array([5.0, 2.0, 3.0]), np.array([True, False, False]))
+    d = cpu(div)
+    assert d[0] == pytest.approx(5.3) and d[1] == 1.0 and d[2] == pytest.approx(7.0)
+    assert np.allclose(cpu(out)[0], 1 / 5.3) and np.allclose(cpu(out)[2], 1 / 7.0)
