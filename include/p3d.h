@@ -187,7 +187,15 @@ typedef struct p3d_loop_state {
 typedef struct p3d_gp {
   int32_t n_inst, n_fill, n_obj, n_macro;
   int32_t max_iters, divergence_window, nblk_obj, nblk_net;
+  int32_t wl_f32;              /* 1: WA sums in fp32 on anchored differences */
+  int32_t pad1;
   p3d_topology topo;           /* n_obj = n_inst here */
+  /* degree-bucketed, transposed pin layout of the fused K1 (built by the host) */
+  const int32_t *f_net_base, *f_net_deg, *f_net_stride;  /* [n_net] */
+  const uint8_t* f_net_dup;                             /* [n_net] */
+  const int32_t* f_pin_inst;                            /* [n_pin] */
+  const float* f_pin_off;                               /* [n_pin][4] */
+  const int32_t* f_pin_slot;                            /* [n_pin] */
   p3d_grid grid;
   /* per-object constants */
   const double* pin_off;       /* [n_pin][4] rotated (rx_top, ry_top, rx_bot, ry_bot) */
@@ -205,7 +213,10 @@ typedef struct p3d_gp {
   double *u, *v, *v_prev, *best;
   double *wl_grad, *dens_grad, *pre, *prev_wl, *prev_dens;
   double* prev_q;              /* [n_obj] */
-  double* pin_out;             /* [n_pin][4] slot order */
+  double* pin_out;             /* [n_pin][4] slot order (exact mode) */
+  float* pin_out_f;            /* [n_pin][4] slot order (gx, gy, g_cut, 0) */
+  double* pin_out_fd;          /* [n_pin] slot order FD depth term */
+  double* pos4;                /* [n_inst][4] AoS copy of v (x, y, z, 0) */
   double* inst_g;              /* [4][n_inst] gx, gy, gz_hbt, gz_bist */
   int64_t* rho_fx;             /* [B] */
   double* rho;                 /* [B] */

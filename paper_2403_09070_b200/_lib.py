@@ -56,7 +56,9 @@ class LoopState(C.Structure):
 class Gp(C.Structure):
     _fields_ = [("n_inst", I32), ("n_fill", I32), ("n_obj", I32), ("n_macro", I32),
                 ("max_iters", I32), ("divergence_window", I32), ("nblk_obj", I32),
-                ("nblk_net", I32), ("topo", Topology), ("grid", Grid),
+                ("nblk_net", I32), ("wl_f32", I32), ("pad1", I32), ("topo", Topology),
+                ("f_net_base", P), ("f_net_deg", P), ("f_net_stride", P), ("f_net_dup", P),
+                ("f_pin_inst", P), ("f_pin_off", P), ("f_pin_slot", P), ("grid", Grid),
                 ("pin_off", P), ("w_top", P), ("h_top", P), ("w_bot", P), ("h_bot", P),
                 ("is_macro", P), ("degree", P), ("fill_w", P), ("fill_h", P), ("fill_z", P),
                 ("macro_ids", P), ("gamma_tab", P),
@@ -65,7 +67,7 @@ class Gp(C.Structure):
                 ("gamma1", D), ("min_step", D), ("step_scale", D), ("rho_t_fx", I64),
                 ("u", P), ("v", P), ("v_prev", P), ("best", P), ("wl_grad", P),
                 ("dens_grad", P), ("pre", P), ("prev_wl", P), ("prev_dens", P), ("prev_q", P),
-                ("pin_out", P), ("inst_g", P), ("rho_fx", P), ("rho", P), ("spec_scratch", P),
+                ("pin_out", P), ("pin_out_f", P), ("pin_out_fd", P), ("pos4", P), ("inst_g", P), ("rho_fx", P), ("rho", P), ("spec_scratch", P),
                 ("maps", P), ("partials", P), ("st", P), ("log", P), ("ovfl_hist", P)]
 
 

@@ -60,6 +60,44 @@ struct GatherArgs {
   const int* halt;
 };
 
+// K1 fused-loop variant (p3d_wl_fused.cu): degree-bucketed transposed pins
+struct FusedNetArgs {
+  int n_net, blocks;
+  const int32_t* net_base;    // [n_net] first pin index of the net (permuted order)
+  const int32_t* net_deg;     // [n_net]
+  const int32_t* net_stride;  // [n_net] distance between consecutive pins of a net
+  const uint8_t* net_dup;     // [n_net] permuted dup flags
+  const int32_t* pin_inst;    // [n_pin] permuted
+  const float4* off;          // [n_pin] permuted (rx_top, ry_top, rx_bot, ry_bot)
+  const int32_t* slot;        // [n_pin] owner-sorted slot of each permuted pin
+  const double4* pos4;        // [n_inst] AoS centres
+  double dz2, gamma, scale4;
+  const double* gamma_ptr;
+  float4* out_f;              // [n_pin] (gx, gy, g_cut, 0) by slot
+  double* out_fd;             // [n_pin] FD depth term by slot
+  double* out_d;              // nullable: [n_pin][4] float64 outputs by slot (exact mode)
+  double* partials;
+  unsigned int* counter;
+  double* final6;
+  const int* halt;
+};
+
+struct FusedGatherArgs {
+  int n_obj, blocks;
+  const int32_t* obj_slot_ptr;
+  const float4* in_f;
+  const double* in_fd;
+  const double* in_d;         // nullable: exact-mode double4 slots
+  double* out;                // [4][n_obj]
+  double* partials;
+  unsigned int* counter;
+  double* final_norms;
+  const int* halt;
+};
+
+void launch_fused_net(const FusedNetArgs& a, bool f32, cudaStream_t s);
+void launch_fused_gather(const FusedGatherArgs& a, cudaStream_t s);
+
 int grid_blocks(int n, int threads, int cap);
 
 // K1

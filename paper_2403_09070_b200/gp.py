@@ -238,6 +238,45 @@ class NesterovOptimizer:
 # ---------------------------------------------------------------------------
 
 
+def fused_pin_layout(net_ptr, pin_inst, pin_slot, off4, dup):
+    """Host build of the fused-K1 pin layout: nets grouped by degree, each
+    degree bucket stored transposed ([pin k][net j]) so a warp's pin loads
+    coalesce.  Returns per-permuted-net (base, degree, stride, dup) and the
+    permuted per-pin (owner, offsets, slot)."""
+    net_ptr = np.asarray(net_ptr, dtype=np.int64)
+    deg = np.diff(net_ptr)
+    n_net = len(deg)
+    order = np.argsort(deg, kind="stable")
+    dsorted = deg[order]
+    base = np.zeros(n_net, dtype=np.int64)
+    stride = np.ones(n_net, dtype=np.int64)
+    dest = np.empty(len(pin_inst), dtype=np.int64)
+    pos = 0
+    bounds = np.flatnonzero(np.r_[True, dsorted[1:] != dsorted[:-1], True])
+    for b0, b1 in zip(bounds[:-1], bounds[1:]):
+        D = int(dsorted[b0])
+        nb = b1 - b0
+        nets = order[b0:b1]
+        j = np.arange(nb)
+        base[b0:b1] = pos + j
+        stride[b0:b1] = nb
+        if D:
+            k = np.arange(D)
+            src = net_ptr[nets][:, None] + k[None, :]
+            dest[src.reshape(-1)] = (pos + k[None, :] * nb + j[:, None]).reshape(-1)
+        pos += nb * D
+    f_inst = np.empty_like(pin_inst)
+    f_inst[dest] = pin_inst
+    f_off = np.empty((len(pin_inst), 4), dtype=np.float32)
+    off32 = off4.astype(np.float32)
+    if not np.array_equal(off32.astype(np.float64), off4):
+        raise ValueError("pin offsets are not exactly representable in float32")
+    f_off[dest] = off32
+    f_slot = np.empty_like(pin_slot)
+    f_slot[dest] = pin_slot
+    return base, dsorted, stride, np.asarray(dup, bool)[order], f_inst, f_off, f_slot
+
+
 class Gp3dProblem:
     """Evaluation context for one 3D GP run (gp.py:235-341), device-resident.
 
@@ -246,8 +285,15 @@ class Gp3dProblem:
     ``cloud`` keep the reference semantics; ``run`` drives the fused loop."""
 
     def __init__(self, design, grid: dn.DensityGrid, fillers: dn.FillerSet, cfg: GpConfig, rot,
-                 max_iters=None):
+                 max_iters=None, precision=None):
+        """precision: "fp32" (default; WA sums in float32 on anchor-relative
+        differences, SURVEY App. B plan) or "fp64" (numpy-order float64)."""
         _lib.require_cuda()
+        import os
+
+        self.precision = precision or os.environ.get("P3D_WL_PRECISION", "fp32")
+        if self.precision not in ("fp32", "fp64"):
+            raise ValueError("precision must be 'fp32' or 'fp64'")
         self.design = design
         self.grid = grid
         self.fillers = fillers
@@ -300,6 +346,19 @@ class Gp3dProblem:
         tp = dt.struct
         g.topo = _lib.Topology(tp.n_net, tp.n_pin, I, 0, tp.net_ptr, tp.pin_inst, tp.net_dup,
                                tp.net_order, tp.pin_slot, tp.obj_slot_ptr)
+        g.wl_f32 = 1 if self.precision == "fp32" else 0
+        off4 = wl.rotated_pin_offsets(arr, self.rot) if P else np.zeros((0, 4))
+        slot = dt.pin_slot.cpu().numpy().astype(np.int64) if P else np.zeros(0, np.int64)
+        fb, fd, fs, fdup, finst, foff, fslot = fused_pin_layout(
+            arr.net_ptr, arr.pin_inst, slot, off4, arr.net_has_dup_inst)
+        one = lambda a, dt_: a if len(a) else np.zeros(1, dt_)  # noqa: E731
+        g.f_net_base = keep(_dev.i32(one(fb, np.int64)))
+        g.f_net_deg = keep(_dev.i32(one(fd, np.int64)))
+        g.f_net_stride = keep(_dev.i32(one(fs, np.int64)))
+        g.f_net_dup = keep(_dev.u8(one(fdup, bool)))
+        g.f_pin_inst = keep(_dev.i32(one(finst, np.int64)))
+        g.f_pin_off = keep(_dev.dev(one(foff.reshape(-1), np.float32), torch.float32))
+        g.f_pin_slot = keep(_dev.i32(one(fslot, np.int64)))
         gs, gkeep = grid.device()
         g.grid = gs
         self._gkeep = gkeep
@@ -333,6 +392,9 @@ class Gp3dProblem:
         self.t_wl, self.t_dens, self.t_pre = z(3 * O), z(3 * O), z(3 * O)
         self.t_prev_wl, self.t_prev_dens, self.t_prev_q = z(3 * O), z(3 * O), z(O)
         self.t_pin_out = z(4 * P)
+        self.t_pin_out_f = torch.zeros(max(4 * P, 4), dtype=torch.float32, device="cuda")
+        self.t_pin_out_fd = z(P)
+        self.t_pos4 = z(4 * I)
         self.t_inst_g = z(4 * I)
         self.t_rho_fx = torch.zeros(B, dtype=torch.int64, device="cuda")
         self.t_rho = z(B)
@@ -346,7 +408,9 @@ class Gp3dProblem:
                         ("best", self.t_best), ("wl_grad", self.t_wl), ("dens_grad", self.t_dens),
                         ("pre", self.t_pre), ("prev_wl", self.t_prev_wl),
                         ("prev_dens", self.t_prev_dens), ("prev_q", self.t_prev_q),
-                        ("pin_out", self.t_pin_out), ("inst_g", self.t_inst_g),
+                        ("pin_out", self.t_pin_out), ("pin_out_f", self.t_pin_out_f),
+                        ("pin_out_fd", self.t_pin_out_fd), ("pos4", self.t_pos4),
+                        ("inst_g", self.t_inst_g),
                         ("rho_fx", self.t_rho_fx), ("rho", self.t_rho),
                         ("spec_scratch", self.t_spec), ("maps", self.t_maps),
                         ("partials", self.t_partials), ("st", self.t_st), ("log", self.t_log),
@@ -454,7 +518,7 @@ class Gp3dProblem:
 
 
 def run_gp3d(design, state: PlacementState, cfg: GpConfig, grid=None, iteration_log=None,
-             rng=None, use_graph=True):
+             rng=None, use_graph=True, precision=None):
     """3D global placement (gp.py:359-455) with the whole loop on the device.
     On exit z is rounded to the die planes; returns (state, GpInfo)."""
     rng = rng or np.random.default_rng(cfg.seed)
@@ -462,7 +526,7 @@ def run_gp3d(design, state: PlacementState, cfg: GpConfig, grid=None, iteration_
     if state.fillers is None:
         state.fillers = make_fillers(design, grid, rng)
     state.dz = grid.dz
-    prob = Gp3dProblem(design, grid, state.fillers, cfg, state.rot)
+    prob = Gp3dProblem(design, grid, state.fillers, cfg, state.rot, precision=precision)
     n = prob.n_inst
     pos0 = np.zeros((prob.n_obj, 3))
     pos0[:n] = np.c_[state.x, state.y, state.z]

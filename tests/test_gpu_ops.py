@@ -310,21 +310,26 @@ def test_overflow_fixed_point(small):
 # ---------------------------------------------------------------------------
 
 
-def test_evaluate_vs_reference(small):
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-12), ("fp32", 1e-5)])
+def test_evaluate_vs_reference(small, precision, tol):
+    """Gp3dProblem.evaluate: fp64 WA at 1e-12, fp32 WA at the north_star's 1e-5."""
     from paper_2403_09070_b200 import gp as G
 
     d, g = small
     grid, og, cl, oprob, fill, st = _small_cloud(small)
     cfg = G.GpConfig(seed=1, nz=2, grid_nx=64, grid_ny=64, max_iters=60, stop_overflow=0.0)
-    prob = G.Gp3dProblem(d, grid, fill, cfg, st.rot)
+    prob = G.Gp3dProblem(d, grid, fill, cfg, st.rot, precision=precision)
     assert prob.movable_volume == float(g["movable_volume"]) and prob.alpha == float(g["alpha"])
     b, ov, ex, nc = prob.evaluate(g["pos"], 1e-3, float(g["gamma"]))
-    assert nc == int(g["ncross"]) and ex == float(g["exact"])
+    assert nc == int(g["ncross"]) and ex == float(g["exact"])  # exact in both modes
     assert ov == pytest.approx(float(g["ovfl"]), rel=1e-12)
-    assert b.value == pytest.approx(float(g["value"]), rel=1e-12)
-    assert rel(b.wl_grad, g["wl_grad"]) < 1e-12
+    assert b.value == pytest.approx(float(g["value"]), rel=tol)
+    w, wr = cpu(b.wl_grad), g["wl_grad"]
+    assert rel(w[:, :2], wr[:, :2]) < tol
+    # the FD depth term inside gz is exact; the Eq. 17 scale carries the planar L1 norms
+    assert rel(w[:, 2], wr[:, 2]) < tol
     assert rel(b.dens_grad, g["dens_grad"]) < 1e-9
-    assert rel(b.total, g["total"]) < 1e-9
+    assert rel(b.total, g["total"]) < max(tol, 1e-9)
     pre, div = G.precondition(b.total, 1e-3, prob.cloud(g["pos"]).charge, prob.degree_obj,
                               prob.is_macro_obj)
     assert rel(pre, g["pre"]) < 1e-9 and rel(div, g["div"]) < 1e-14
