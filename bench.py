@@ -18,7 +18,6 @@ import ctypes as C
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -52,52 +51,49 @@ def setup_design(config, rank):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled through NVML every 2 ms while the
+    timed region runs (nvidia-smi's 100 ms floor is longer than the region)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index):
         self.index = index
         self.rows = []
-        self.proc = None
+        self.stop = threading.Event()
+        self.err = None
+
+    def _run(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            get_r = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self.stop.is_set():
+                self.rows.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM), int(get_r(h))))
+                time.sleep(0.002)
+        except Exception as e:  # pragma: no cover - reported in the JSON line
+            self.err = repr(e)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        time.sleep(0.01)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 6:
-                self.rows.append(parts)
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        self.t.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err}
+        reasons = sorted({name for _, r in self.rows for bit, name in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": reasons,
                 "samples": len(self.rows)}
 
 
@@ -128,9 +124,15 @@ def load_peaks():
 def cpu_baseline(design, grid_n, spec, seconds=20.0, max_iters=200):
     """Oracle port (numpy, 1 core) on the same workload: bounded sample of
     whole GP iterations (setup excluded)."""
+    from threadpoolctl import threadpool_limits
+
     from oracle import port as P
 
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    with threadpool_limits(limits=1):
+        return _cpu_baseline(P, design, grid_n, spec, seconds, max_iters)
+
+
+def _cpu_baseline(P, design, grid_n, spec, seconds, max_iters):
     cfg = P.Cfg(seed=spec.seed, nz=2, grid_nx=grid_n, grid_ny=grid_n, max_iters=max_iters,
                 stop_overflow=0.0)
     rng = np.random.default_rng(spec.seed)
@@ -202,6 +204,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+                    help="WA arithmetic: fp64 numpy-order (default) or fp32 anchored")
     args = ap.parse_args()
     rank, world, local = rank_env()
     if args.impl == "reference":
@@ -225,7 +229,7 @@ def main():
     grid = G.choose_grid(design, cfg)
     st = G.init_state(design, grid, cfg, rng)
     st.fillers = G.make_fillers(design, grid, rng)
-    prob = G.Gp3dProblem(design, grid, st.fillers, cfg, st.rot)
+    prob = G.Gp3dProblem(design, grid, st.fillers, cfg, st.rot, precision=args.precision)
     n = prob.n_inst
     pos0 = np.zeros((prob.n_obj, 3))
     pos0[:n] = np.c_[st.x, st.y, st.z]
@@ -313,12 +317,13 @@ def main():
     line = {
         "metric": METRIC, "value": it_s, "unit": "it/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64",
+        "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f64+f32(WA)",
         "data": "synthetic (paper_2403_09070_b200.synth == place3d.synth.gen_synthetic, seed 1+rank)",
         "config": {"workload": WORKLOADS[args.config], "n_inst": n, "n_fill": prob.n_fill,
                    "n_net": design.n_nets, "n_pin": design.arrays().n_pin,
                    "grid": [grid.nx, grid.ny, grid.nz], "max_iters_schedule": max_iters,
                    "parallelism": f"replicas x{world}" if world > 1 else "single",
+                   "wl_precision": args.precision,
                    "l2": f"no flush: iteration working set {ws_mb:.0f} MB > 126 MB L2"},
         "e2e": {"value": e2e_it_s, "unit": "it/s",
                 "h2d_bytes_per_step": int(host_pos.numel() * 8 / K),

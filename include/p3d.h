@@ -191,11 +191,16 @@ typedef struct p3d_gp {
   int32_t pad1;
   p3d_topology topo;           /* n_obj = n_inst here */
   /* degree-bucketed, transposed pin layout of the fused K1 (built by the host) */
-  const int32_t *f_net_base, *f_net_deg, *f_net_stride;  /* [n_net] */
+  int32_t f_n_tasks, f_n_generic;
+  const int32_t* f_generic_nets; /* [f_n_generic] permuted indices of nets with degree
+                                    outside [2, 6] (per-thread generic path) */
+  const int32_t* f_tasks;      /* [f_n_tasks][4] warp tasks (pin base, bucket size, j0, deg) */
+  const int32_t* f_task_t0;    /* [f_n_tasks] permuted index of the bucket's first net */
+  const int32_t *f_net_base, *f_net_deg, *f_net_stride;  /* [n_net] permuted nets */
   const uint8_t* f_net_dup;                             /* [n_net] */
-  const int32_t* f_pin_inst;                            /* [n_pin] */
+  const int32_t* f_pin_inst;                            /* [n_pin] permuted pins */
   const float* f_pin_off;                               /* [n_pin][4] */
-  const int32_t* f_pin_slot;                            /* [n_pin] */
+  const int32_t* f_obj_pins;   /* [n_pin] permuted pin index of each owner-sorted slot */
   p3d_grid grid;
   /* per-object constants */
   const double* pin_off;       /* [n_pin][4] rotated (rx_top, ry_top, rx_bot, ry_bot) */

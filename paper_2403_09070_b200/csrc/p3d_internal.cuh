@@ -19,6 +19,7 @@ enum PartialSlot {
   kSlotOvfl = 2,     // overflow
   kSlotDens = 3,     // density gather (energy, |dens|, |wl|)
   kSlotStep = 4,     // preconditioner / BB norms
+  kSlotGeneric = 5,  // generic (high-degree) nets
   kSlotFinal = 15,   // finalised scalars of the sub-kernels
 };
 // offsets inside the final slot
@@ -26,9 +27,10 @@ enum FinalIdx {
   kFinNet = 0,      // 6 values: planar x, planar y, cut, exact x, exact y, crossings
   kFinNorm = 8,     // 4 values: |gx|, |gy|, |gzb|, Eq. 17 scale
   kFinOvfl = 16,    // 1 value: overflow excess (already / movable volume)
+  kFinGeneric = 24, // 6 values: generic-net totals
 };
 // counters inside p3d_loop_state::counters
-enum CounterIdx { kCntNet = 0, kCntGather, kCntOvfl, kCntDens, kCntStep, kCntAdvance, kCntOp };
+enum CounterIdx { kCntNet = 0, kCntGather, kCntOvfl, kCntDens, kCntStep, kCntAdvance, kCntOp, kCntGeneric };
 
 struct NetArgs {
   int n_net, blocks;
@@ -63,19 +65,27 @@ struct GatherArgs {
 // K1 fused-loop variant (p3d_wl_fused.cu): degree-bucketed transposed pins
 struct FusedNetArgs {
   int n_net, blocks;
+  int n_tasks;                // warp tasks
+  const int4* tasks;          // (pin base, bucket size, first net in bucket, degree | 0 = generic)
+  const int32_t* task_t0;     // permuted index of the bucket's first net
+  int n_generic;              // nets of degree outside [2, 6]
+  const int32_t* generic_nets;  // their permuted indices
+  double* gpartials;
+  unsigned int* gcounter;
+  double* generic6;           // their 6 totals (read by the staged kernel's epilogue)
   const int32_t* net_base;    // [n_net] first pin index of the net (permuted order)
   const int32_t* net_deg;     // [n_net]
   const int32_t* net_stride;  // [n_net] distance between consecutive pins of a net
   const uint8_t* net_dup;     // [n_net] permuted dup flags
   const int32_t* pin_inst;    // [n_pin] permuted
   const float4* off;          // [n_pin] permuted (rx_top, ry_top, rx_bot, ry_bot)
-  const int32_t* slot;        // [n_pin] owner-sorted slot of each permuted pin
+  const int32_t* slot;        // unused (kept for layout stability)
   const double4* pos4;        // [n_inst] AoS centres
   double dz2, gamma, scale4;
   const double* gamma_ptr;
-  float4* out_f;              // [n_pin] (gx, gy, g_cut, 0) by slot
-  double* out_fd;             // [n_pin] FD depth term by slot
-  double* out_d;              // nullable: [n_pin][4] float64 outputs by slot (exact mode)
+  float4* out_f;              // [n_pin] (gx, gy, g_cut, FD) in permuted pin order (fp32 mode)
+  double* out_fd;             // unused
+  double* out_d;              // nullable: [n_pin][4] float64 records, permuted order (fp64 mode)
   double* partials;
   unsigned int* counter;
   double* final6;
@@ -85,6 +95,7 @@ struct FusedNetArgs {
 struct FusedGatherArgs {
   int n_obj, blocks;
   const int32_t* obj_slot_ptr;
+  const int32_t* obj_pins;    // [n_pin] permuted pin index of each owner slot
   const float4* in_f;
   const double* in_fd;
   const double* in_d;         // nullable: exact-mode double4 slots
@@ -96,6 +107,7 @@ struct FusedGatherArgs {
 };
 
 void launch_fused_net(const FusedNetArgs& a, bool f32, cudaStream_t s);
+void fused_net_setup();
 void launch_fused_gather(const FusedGatherArgs& a, cudaStream_t s);
 
 int grid_blocks(int n, int threads, int cap);

@@ -443,6 +443,14 @@ static void eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = nul
   // K1 (degree-bucketed, register-resident nets) + K1b owner gather
   FusedNetArgs na{};
   na.n_net = gp.topo.n_net;
+  na.n_tasks = gp.f_n_tasks;
+  na.tasks = reinterpret_cast<const int4*>(gp.f_tasks);
+  na.task_t0 = gp.f_task_t0;
+  na.n_generic = gp.f_n_generic;
+  na.generic_nets = gp.f_generic_nets;
+  na.gpartials = gp.partials + (long long)kSlotGeneric * kPartialStride;
+  na.gcounter = &st->counters[kCntGeneric];
+  na.generic6 = finals + kFinGeneric;
   na.blocks = gp.nblk_net;
   na.net_base = gp.f_net_base;
   na.net_deg = gp.f_net_deg;
@@ -450,7 +458,6 @@ static void eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = nul
   na.net_dup = gp.f_net_dup;
   na.pin_inst = gp.f_pin_inst;
   na.off = reinterpret_cast<const float4*>(gp.f_pin_off);
-  na.slot = gp.f_pin_slot;
   na.pos4 = reinterpret_cast<const double4*>(gp.pos4);
   na.dz2 = gp.grid.dz / 2;
   na.gamma_ptr = &st->gamma;
@@ -468,6 +475,7 @@ static void eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = nul
   ga.n_obj = gp.n_inst;
   ga.blocks = grid_blocks(gp.n_inst, 256, kMaxBlocks);
   ga.obj_slot_ptr = gp.topo.obj_slot_ptr;
+  ga.obj_pins = gp.f_obj_pins;
   ga.in_f = reinterpret_cast<const float4*>(gp.pin_out_f);
   ga.in_fd = gp.pin_out_fd;
   ga.in_d = gp.wl_f32 ? nullptr : gp.pin_out;
@@ -531,7 +539,7 @@ int gp_iterate_profiled(const p3d_gp& gp, cudaStream_t s, float* ms) {
 
 // kernels enqueued by one gp_iterate (for the benchmark's launch count)
 int gp_kernels_per_iteration(const p3d_gp& gp) {
-  return (gp.topo.n_net > 0) /*net*/ + (gp.n_inst > 0) /*gather*/ + 1 + (gp.n_macro > 0) /*scatter*/ + 6 /*spectral*/ +
+  return (gp.topo.n_net > 0) + (gp.f_n_generic > 0) /*net*/ + (gp.n_inst > 0) /*gather*/ + 1 + (gp.n_macro > 0) /*scatter*/ + 6 /*spectral*/ +
          1 /*dens*/ + 2 /*step, advance*/;
 }
 
@@ -545,6 +553,7 @@ int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s) {
 
 int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s) {
   spectral_setup();
+  fused_net_setup();
   init_state_kernel<<<1, 1, 0, s>>>(gp);
   const int b = grid_blocks(gp.n_obj, 256, 4096);
   project_kernel<<<b, 256, 0, s>>>(gp, pos0, gp.u);

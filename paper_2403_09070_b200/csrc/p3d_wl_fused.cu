@@ -1,20 +1,22 @@
 // K1 (fused-loop variant) — the same math as p3d_wl.cu's net_kernel, laid out
-// for bandwidth:
-//   * nets are processed grouped by degree; for degree D <= 8 the pins of a
-//     bucket are stored transposed ([k][net]) so every pin load of a warp is
-//     one coalesced transaction, and the whole net lives in registers
-//     (template on D: no local memory, no divergence inside a bucket);
-//   * instance centres are gathered from an AoS double4 copy (one 32-byte
-//     sector per pin, L2-resident) written by the optimiser step;
-//   * pin offsets are float4 (integers / half-integers are exact in fp32);
-//   * extrema, spans, crossings and the finite-difference depth term stay in
-//     float64 (bit-exact); the weighted-average exponential sums run either in
-//     float64 with numpy's operation order (WA_F64) or in float32 on
-//     anchor-relative differences (WA_F32: value = (max-min) + fp32 residual;
-//     the SURVEY Appendix-B precision plan, within 3e-7 of the fp64
-//     trajectory).
-// Per-pin outputs: gx, gy, g_cut (float32 or float64) and the FD term (float64)
-// at the pin's owner-sorted slot; per-net scalars reduced deterministically.
+// for bandwidth and latency:
+//   * nets are grouped by degree; each degree bucket stores its pins
+//     transposed ([pin k][net j]) so a warp that owns 32 nets of one bucket
+//     loads pin k of all 32 nets in one coalesced transaction;
+//   * a warp first STAGES its 32*D pins (owner gather from the AoS double4
+//     copy of the instance centres — one 32-byte sector per pin, L2-resident —
+//     plus float4 offsets) into per-lane shared-memory columns, with all D
+//     gathers of a lane independent (memory-level parallelism), then each lane
+//     evaluates its own net from shared memory (no register spills, no local
+//     memory);
+//   * per-pin results (gx, gy, g_cut, FD term) are written as one record per
+//     pin in the same coalesced order; the owner gather reads them through an
+//     owner-sorted index list (deterministic per-object sums);
+//   * extrema, spans, crossings and the finite-difference depth term are
+//     float64 and bit-exact; the weighted-average exponential sums run in
+//     float64 with numpy's operation order (default) or, opt-in, float32 on
+//     anchor-relative differences (SURVEY App. B plan).
+// Nets with degree outside [2, kMaxStagedDeg] take a per-thread generic path.
 #include "p3d_common.cuh"
 #include "p3d_internal.cuh"
 
@@ -159,10 +161,9 @@ __device__ __noinline__ double forced_ext(const FusedNetArgs& a, int base, int d
 
 __device__ __forceinline__ void store_pin(const FusedNetArgs& a, int idx, double gx, double gy,
                                           double gc, double gb) {
-  const int s = a.slot[idx];
-  a.out_f[s] = make_float4((float)gx, (float)gy, (float)gc, 0.f);
-  a.out_fd[s] = gb;
-  if (a.out_d) reinterpret_cast<double4*>(a.out_d)[s] = make_double4(gx, gy, gc, gb);
+  // one record per pin in the coalesced (degree-bucketed) pin order
+  if (a.out_d) reinterpret_cast<double4*>(a.out_d)[idx] = make_double4(gx, gy, gc, gb);
+  else a.out_f[idx] = make_float4((float)gx, (float)gy, (float)gc, (float)gb);
 }
 
 // Dup-owner exact path (wirelength.py:280-292): value for the first pin of
@@ -175,108 +176,6 @@ __device__ __noinline__ double dup_fd(const FusedNetArgs& a, int base, int deg, 
   const double up = forced_ext(a, base, deg, stride, w, 1, 0) + forced_ext(a, base, deg, stride, w, 1, 1);
   const double dn = forced_ext(a, base, deg, stride, w, 0, 0) + forced_ext(a, base, deg, stride, w, 0, 1);
   return a.scale4 * (up - dn);
-}
-
-// One planar axis of a register-resident net: boxes, branch, WA sums of the
-// chosen branch, per-pin gradients, FD extent deltas (accumulated into dw).
-template <int D, bool F32>
-__device__ __forceinline__ void axis_phase(const double (&c)[D], int topm, typename WaSel<F32>::R ig,
-                                           double& val, double& exact, bool& crossing,
-                                           typename WaSel<F32>::R (&g)[D], double (&dw)[D]) {
-  using W = typename WaSel<F32>::W;
-  using R = typename WaSel<F32>::R;
-  Box2 bx;
-  bx.init();
-#pragma unroll
-  for (int k = 0; k < D; ++k) bx.add(c[k], (topm >> k) & 1);
-  const double full = bx.full(), part = bx.t.span() + bx.b.span();
-  const double ex = fmax(full, part);
-  const bool split = part > full;  // ties resolve to the full box (wirelength.py:186)
-  exact = ex;
-  crossing = bx.b.cnt > 0 && bx.t.cnt > 0;
-  const double fh = bx.fmx(), fl = bx.fmn();
-  W w0, w1;
-  w0.init();
-  w1.init();
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    R ep, em;
-    const int tp = (topm >> k) & 1;
-    if (!split) w0.add(c[k], fh, fl, ig, ep, em);
-    else if (tp) w1.add(c[k], bx.t.hi1, bx.t.lo1, ig, ep, em);
-    else w0.add(c[k], bx.b.hi1, bx.b.lo1, ig, ep, em);
-  }
-  val = split ? (w0.value(bx.b.hi1, bx.b.lo1) + w1.value(bx.t.hi1, bx.t.lo1)) : w0.value(fh, fl);
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const int tp = (topm >> k) & 1;
-    R ep, em;
-    W tmp;
-    tmp.init();
-    if (!split) {
-      tmp.add(c[k], fh, fl, ig, ep, em);
-      g[k] = w0.grad(c[k], fh, fl, ig, ep, em);
-    } else if (tp) {
-      tmp.add(c[k], bx.t.hi1, bx.t.lo1, ig, ep, em);
-      g[k] = w1.grad(c[k], bx.t.hi1, bx.t.lo1, ig, ep, em);
-    } else {
-      tmp.add(c[k], bx.b.hi1, bx.b.lo1, ig, ep, em);
-      g[k] = w0.grad(c[k], bx.b.hi1, bx.b.lo1, ig, ep, em);
-    }
-    dw[k] += bx.flip(c[k], tp, ex);
-  }
-}
-
-// Register-resident net of compile-time degree D (axis by axis).
-template <int D, bool F32>
-__device__ __forceinline__ void process_net(const FusedNetArgs& a, int t, double (&acc)[6]) {
-  using W = typename WaSel<F32>::W;
-  using R = typename WaSel<F32>::R;
-  const int base = a.net_base[t];
-  const int stride = a.net_stride[t];
-  double px[D], py[D], pz[D], dw[D];
-  R gx[D], gy[D];
-  int topm = 0;
-  double zhi = -P3D_INF, zlo = P3D_INF;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    int tp;
-    load_pin(a, base + k * stride, px[k], py[k], pz[k], tp);
-    topm |= tp << k;
-    zhi = fmax(zhi, pz[k]);
-    zlo = fmin(zlo, pz[k]);
-    dw[k] = 0.0;
-  }
-  const R ig = F32 ? (R)(1.0 / a.gamma) : (R)a.gamma;  // f32: multiply; f64: divide like numpy
-  double v, ex;
-  bool cross;
-  axis_phase<D, F32>(px, topm, ig, v, ex, cross, gx, dw);
-  acc[0] += v;
-  acc[3] += ex;
-  acc[5] += cross ? 1.0 : 0.0;
-  axis_phase<D, F32>(py, topm, ig, v, ex, cross, gy, dw);
-  acc[1] += v;
-  acc[4] += ex;
-  W wz;
-  wz.init();
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    R ep, em;
-    wz.add(pz[k], zhi, zlo, ig, ep, em);
-  }
-  acc[2] += wz.value(zhi, zlo);
-  const bool dup = a.net_dup[t] != 0;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    R ep, em;
-    W tmp;
-    tmp.init();
-    tmp.add(pz[k], zhi, zlo, ig, ep, em);
-    const double gc = (double)wz.grad(pz[k], zhi, zlo, ig, ep, em);
-    const int tp = (topm >> k) & 1;
-    const double gb = dup ? dup_fd(a, base, D, stride, k) : (tp ? -dw[k] : dw[k]) * a.scale4;
-    store_pin(a, base + k * stride, gx[k], gy[k], gc, gb);
-  }
 }
 
 // Any degree: three passes re-loading the pins (large nets; rare).
@@ -353,21 +252,135 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
   }
 }
 
+constexpr int kMaxStagedDeg = 6;
+constexpr int kWarpsPerBlock = 4;
+
+// per-lane shared-memory columns of one warp (index [k][lane])
 template <bool F32>
-__global__ void __launch_bounds__(256, F32 ? 2 : 1) fused_net_kernel(FusedNetArgs a) {
+struct WarpCols {
+  using R = typename WaSel<F32>::R;
+  double px[kMaxStagedDeg][32], py[kMaxStagedDeg][32], pz[kMaxStagedDeg][32];
+  double dw[kMaxStagedDeg][32];
+  R ep[kMaxStagedDeg][32], em[kMaxStagedDeg][32], gx[kMaxStagedDeg][32], gy[kMaxStagedDeg][32];
+};
+
+// One planar axis of a staged net: boxes, branch, WA sums of the chosen
+// branch, per-pin gradients, FD extent deltas (accumulated into dw).
+template <int D, bool F32>
+__device__ __forceinline__ void staged_axis(const double (&c)[kMaxStagedDeg][32], WarpCols<F32>& sm,
+                                            int lane, int topm, typename WaSel<F32>::R ig,
+                                            double& val, double& exact, bool& crossing,
+                                            typename WaSel<F32>::R (&g)[kMaxStagedDeg][32]) {
+  using W = typename WaSel<F32>::W;
+  Box2 bx;
+  bx.init();
+#pragma unroll
+  for (int k = 0; k < D; ++k) bx.add(c[k][lane], (topm >> k) & 1);
+  const double full = bx.full(), part = bx.t.span() + bx.b.span();
+  const double ex = fmax(full, part);
+  const bool split = part > full;  // ties resolve to the full box (wirelength.py:186)
+  exact = ex;
+  crossing = bx.b.cnt > 0 && bx.t.cnt > 0;
+  const double fh = bx.fmx(), fl = bx.fmn();
+  W w0, w1;
+  w0.init();
+  w1.init();
+#pragma unroll 1
+  for (int k = 0; k < D; ++k) {
+    const int tp = (topm >> k) & 1;
+    const double v = c[k][lane];
+    if (!split) w0.add(v, fh, fl, ig, sm.ep[k][lane], sm.em[k][lane]);
+    else if (tp) w1.add(v, bx.t.hi1, bx.t.lo1, ig, sm.ep[k][lane], sm.em[k][lane]);
+    else w0.add(v, bx.b.hi1, bx.b.lo1, ig, sm.ep[k][lane], sm.em[k][lane]);
+  }
+  val = split ? (w0.value(bx.b.hi1, bx.b.lo1) + w1.value(bx.t.hi1, bx.t.lo1)) : w0.value(fh, fl);
+#pragma unroll 1
+  for (int k = 0; k < D; ++k) {
+    const int tp = (topm >> k) & 1;
+    const double v = c[k][lane];
+    if (!split) g[k][lane] = w0.grad(v, fh, fl, ig, sm.ep[k][lane], sm.em[k][lane]);
+    else if (tp) g[k][lane] = w1.grad(v, bx.t.hi1, bx.t.lo1, ig, sm.ep[k][lane], sm.em[k][lane]);
+    else g[k][lane] = w0.grad(v, bx.b.hi1, bx.b.lo1, ig, sm.ep[k][lane], sm.em[k][lane]);
+    sm.dw[k][lane] += bx.flip(v, tp, ex);
+  }
+}
+
+// 32 nets of degree D owned by one warp: stage, then one net per lane.
+template <int D, bool F32>
+__device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk, int t0,
+                                            WarpCols<F32>& sm, int lane, double (&acc)[6]) {
+  using W = typename WaSel<F32>::W;
+  using R = typename WaSel<F32>::R;
+  const int nb = tk.y, j = tk.z + lane;
+  if (j >= nb || a.net_dup[t0 + j]) return;  // duplicate-owner nets: generic kernel
+  const int pin0 = tk.x + j;
+  int topm = 0;
+  double zhi = -P3D_INF, zlo = P3D_INF;
+  // stage: D independent owner gathers per lane
+  int inst[D];
+  float4 off[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    inst[k] = a.pin_inst[pin0 + k * nb];
+    off[k] = a.off[pin0 + k * nb];
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const double4 p = a.pos4[inst[k]];
+    const int tp = (p.z - a.dz2) > 0.0;
+    topm |= tp << k;
+    sm.px[k][lane] = p.x + (double)(tp ? off[k].x : off[k].z);
+    sm.py[k][lane] = p.y + (double)(tp ? off[k].y : off[k].w);
+    sm.pz[k][lane] = p.z;
+    zhi = fmax(zhi, p.z);
+    zlo = fmin(zlo, p.z);
+  }
+  const R ig = F32 ? (R)(1.0 / a.gamma) : (R)a.gamma;  // f32: multiply; f64: divide like numpy
+#pragma unroll
+  for (int k = 0; k < D; ++k) sm.dw[k][lane] = 0.0;
+  double v, ex;
+  bool cross;
+  staged_axis<D, F32>(sm.px, sm, lane, topm, ig, v, ex, cross, sm.gx);
+  acc[0] += v;
+  acc[3] += ex;
+  acc[5] += cross ? 1.0 : 0.0;
+  staged_axis<D, F32>(sm.py, sm, lane, topm, ig, v, ex, cross, sm.gy);
+  acc[1] += v;
+  acc[4] += ex;
+  W wz;
+  wz.init();
+#pragma unroll 1
+  for (int k = 0; k < D; ++k) wz.add(sm.pz[k][lane], zhi, zlo, ig, sm.ep[k][lane], sm.em[k][lane]);
+  acc[2] += wz.value(zhi, zlo);
+#pragma unroll 1
+  for (int k = 0; k < D; ++k) {
+    const double gc = (double)wz.grad(sm.pz[k][lane], zhi, zlo, ig, sm.ep[k][lane], sm.em[k][lane]);
+    const int tp = (topm >> k) & 1;
+    const double dwk = sm.dw[k][lane];
+    const double gb = (tp ? -dwk : dwk) * a.scale4;
+    store_pin(a, pin0 + k * nb, (double)sm.gx[k][lane], (double)sm.gy[k][lane], gc, gb);
+  }
+}
+
+template <bool F32>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) fused_net_kernel(FusedNetArgs a) {
   if (a.halt && *a.halt) return;
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ double red[32 * 6];
   if (a.gamma_ptr) a.gamma = *a.gamma_ptr;
   double acc[6] = {0, 0, 0, 0, 0, 0};
-  const int stride = gridDim.x * blockDim.x;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < a.n_net; t += stride) {
-    switch (a.net_deg[t]) {
-      case 2: process_net<2, F32>(a, t, acc); break;
-      case 3: process_net<3, F32>(a, t, acc); break;
-      case 4: process_net<4, F32>(a, t, acc); break;
-      case 5: process_net<5, F32>(a, t, acc); break;
-      case 6: process_net<6, F32>(a, t, acc); break;
-      default: process_net_generic<F32>(a, t, acc); break;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  WarpCols<F32>& sm = reinterpret_cast<WarpCols<F32>*>(dyn_smem)[wib];
+  for (int w = blockIdx.x * kWarpsPerBlock + wib; w < a.n_tasks; w += gridDim.x * kWarpsPerBlock) {
+    const int4 tk = a.tasks[w];
+    const int t0 = a.task_t0[w];
+    switch (tk.w) {
+      case 2: staged_task<2, F32>(a, tk, t0, sm, lane, acc); break;
+      case 3: staged_task<3, F32>(a, tk, t0, sm, lane, acc); break;
+      case 4: staged_task<4, F32>(a, tk, t0, sm, lane, acc); break;
+      case 5: staged_task<5, F32>(a, tk, t0, sm, lane, acc); break;
+      case 6: staged_task<6, F32>(a, tk, t0, sm, lane, acc); break;
+      default: break;  // generic nets run in generic_net_kernel
     }
   }
   block_sum<6>(acc, red);
@@ -375,8 +388,30 @@ __global__ void __launch_bounds__(256, F32 ? 2 : 1) fused_net_kernel(FusedNetArg
     for (int q = 0; q < 6; ++q) a.partials[q * gridDim.x + blockIdx.x] = acc[q];
   if (last_block(a.counter)) {
     for (int q = 0; q < 6; ++q) {
-      const double s = ordered_sum(a.partials + q * gridDim.x, gridDim.x, red);
-      if (threadIdx.x == 0) a.final6[q] = s;
+      const double v = ordered_sum(a.partials + q * gridDim.x, gridDim.x, red);
+      if (threadIdx.x == 0) a.final6[q] = a.n_generic ? v + a.generic6[q] : v;
+    }
+  }
+}
+
+// Nets of degree outside [2, kMaxStagedDeg] (none in the synthetic designs):
+// thread per net, pins re-loaded per pass; totals in generic6 (added by the
+// staged kernel's epilogue, so the reduction order stays fixed).
+template <bool F32>
+__global__ void __launch_bounds__(256) generic_net_kernel(FusedNetArgs a) {
+  if (a.halt && *a.halt) return;
+  __shared__ double red[32 * 6];
+  if (a.gamma_ptr) a.gamma = *a.gamma_ptr;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < a.n_generic; g += gridDim.x * blockDim.x)
+    process_net_generic<F32>(a, a.generic_nets[g], acc);
+  block_sum<6>(acc, red);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 6; ++q) a.gpartials[q * gridDim.x + blockIdx.x] = acc[q];
+  if (last_block(a.gcounter)) {
+    for (int q = 0; q < 6; ++q) {
+      const double v = ordered_sum(a.gpartials + q * gridDim.x, gridDim.x, red);
+      if (threadIdx.x == 0) a.generic6[q] = v;
     }
   }
 }
@@ -393,14 +428,13 @@ __global__ void __launch_bounds__(256) fused_gather_kernel(FusedGatherArgs a) {
     if (a.in_d) {
       const double4* in = reinterpret_cast<const double4*>(a.in_d);
       for (int s = b; s < e; ++s) {
-        const double4 r = in[s];
+        const double4 r = in[a.obj_pins[s]];
         s0 += r.x; s1 += r.y; s2 += r.z; s3 += r.w;
       }
     } else {
       for (int s = b; s < e; ++s) {
-        const float4 r = a.in_f[s];
-        s0 += (double)r.x; s1 += (double)r.y; s2 += (double)r.z;
-        s3 += a.in_fd[s];
+        const float4 r = a.in_f[a.obj_pins[s]];
+        s0 += (double)r.x; s1 += (double)r.y; s2 += (double)r.z; s3 += (double)r.w;
       }
     }
     a.out[i] = s0;
@@ -428,9 +462,26 @@ __global__ void __launch_bounds__(256) fused_gather_kernel(FusedGatherArgs a) {
 
 }  // namespace
 
+void fused_net_setup() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(fused_net_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(kWarpsPerBlock * sizeof(WarpCols<true>)));
+  cudaFuncSetAttribute(fused_net_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(kWarpsPerBlock * sizeof(WarpCols<false>)));
+  done = true;
+}
+
 void launch_fused_net(const FusedNetArgs& a, bool f32, cudaStream_t s) {
-  if (f32) fused_net_kernel<true><<<a.blocks, 256, 0, s>>>(a);
-  else fused_net_kernel<false><<<a.blocks, 256, 0, s>>>(a);
+  if (a.n_generic > 0) {
+    const int gb = grid_blocks(a.n_generic, 256, kMaxBlocks);
+    if (f32) generic_net_kernel<true><<<gb, 256, 0, s>>>(a);
+    else generic_net_kernel<false><<<gb, 256, 0, s>>>(a);
+  }
+  if (f32)
+    fused_net_kernel<true><<<a.blocks, 32 * kWarpsPerBlock, kWarpsPerBlock * sizeof(WarpCols<true>), s>>>(a);
+  else
+    fused_net_kernel<false><<<a.blocks, 32 * kWarpsPerBlock, kWarpsPerBlock * sizeof(WarpCols<false>), s>>>(a);
 }
 
 void launch_fused_gather(const FusedGatherArgs& a, cudaStream_t s) {

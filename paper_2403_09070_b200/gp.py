@@ -238,11 +238,16 @@ class NesterovOptimizer:
 # ---------------------------------------------------------------------------
 
 
-def fused_pin_layout(net_ptr, pin_inst, pin_slot, off4, dup):
-    """Host build of the fused-K1 pin layout: nets grouped by degree, each
-    degree bucket stored transposed ([pin k][net j]) so a warp's pin loads
-    coalesce.  Returns per-permuted-net (base, degree, stride, dup) and the
-    permuted per-pin (owner, offsets, slot)."""
+MAX_STAGED_DEG = 6  # kMaxStagedDeg in p3d_wl_fused.cu
+
+
+def fused_pin_layout(net_ptr, pin_inst, off4, dup):
+    """Host build of the fused-K1 layout.  Nets are grouped by degree and each
+    degree bucket is stored transposed ([pin k][net j]) so a warp owning 32
+    nets of a bucket loads pin k of all of them in one transaction.  Returns a
+    dict of device-ready arrays: warp tasks, per-permuted-net (base, degree,
+    stride, dup), permuted per-pin (owner, float32 offsets) and, per original
+    pin, its permuted index."""
     net_ptr = np.asarray(net_ptr, dtype=np.int64)
     deg = np.diff(net_ptr)
     n_net = len(deg)
@@ -251,11 +256,12 @@ def fused_pin_layout(net_ptr, pin_inst, pin_slot, off4, dup):
     base = np.zeros(n_net, dtype=np.int64)
     stride = np.ones(n_net, dtype=np.int64)
     dest = np.empty(len(pin_inst), dtype=np.int64)
+    tasks, t0s, generic = [], [], []
     pos = 0
-    bounds = np.flatnonzero(np.r_[True, dsorted[1:] != dsorted[:-1], True])
+    bounds = np.flatnonzero(np.r_[True, dsorted[1:] != dsorted[:-1], True]) if n_net else [0]
     for b0, b1 in zip(bounds[:-1], bounds[1:]):
         D = int(dsorted[b0])
-        nb = b1 - b0
+        nb = int(b1 - b0)
         nets = order[b0:b1]
         j = np.arange(nb)
         base[b0:b1] = pos + j
@@ -264,17 +270,36 @@ def fused_pin_layout(net_ptr, pin_inst, pin_slot, off4, dup):
             k = np.arange(D)
             src = net_ptr[nets][:, None] + k[None, :]
             dest[src.reshape(-1)] = (pos + k[None, :] * nb + j[:, None]).reshape(-1)
+        if 2 <= D <= MAX_STAGED_DEG:
+            for j0 in range(0, nb, 32):
+                tasks.append((pos, nb, j0, D))
+                t0s.append(int(b0))
+        else:
+            generic.extend(range(int(b0), int(b1)))
         pos += nb * D
-    f_inst = np.empty_like(pin_inst)
-    f_inst[dest] = pin_inst
-    f_off = np.empty((len(pin_inst), 4), dtype=np.float32)
+    off4 = np.asarray(off4, dtype=np.float64)
     off32 = off4.astype(np.float32)
     if not np.array_equal(off32.astype(np.float64), off4):
         raise ValueError("pin offsets are not exactly representable in float32")
+    f_inst = np.empty_like(pin_inst)
+    f_inst[dest] = pin_inst
+    f_off = np.empty((len(pin_inst), 4), dtype=np.float32)
     f_off[dest] = off32
-    f_slot = np.empty_like(pin_slot)
-    f_slot[dest] = pin_slot
-    return base, dsorted, stride, np.asarray(dup, bool)[order], f_inst, f_off, f_slot
+    # owner-sorted slots (stable: original pin order within an owner, like bincount)
+    slot_order = np.argsort(pin_inst, kind="stable")
+    return dict(tasks=np.asarray(tasks, dtype=np.int64).reshape(-1, 4),
+                task_t0=np.asarray(t0s, dtype=np.int64), net_base=base, net_deg=dsorted,
+                net_stride=stride, net_dup=np.asarray(dup, bool)[order], pin_inst=f_inst,
+                pin_off=f_off, obj_pins=dest[slot_order], dest=dest,
+                generic=np.asarray(generic, dtype=np.int64))
+
+
+def _with_dup_nets(layout):
+    """Duplicate-owner nets (exact O(|P|^2) FD path) run in the generic kernel."""
+    dup_t = np.flatnonzero(layout["net_dup"])
+    staged = ~np.isin(dup_t, layout["generic"])
+    layout["generic"] = np.sort(np.r_[layout["generic"], dup_t[staged]]).astype(np.int64)
+    return layout
 
 
 class Gp3dProblem:
@@ -286,12 +311,13 @@ class Gp3dProblem:
 
     def __init__(self, design, grid: dn.DensityGrid, fillers: dn.FillerSet, cfg: GpConfig, rot,
                  max_iters=None, precision=None):
-        """precision: "fp32" (default; WA sums in float32 on anchor-relative
-        differences, SURVEY App. B plan) or "fp64" (numpy-order float64)."""
+        """precision: "fp64" (default; WA sums in float64 with numpy's
+        operation order) or "fp32" (WA sums in float32 on anchor-relative
+        differences, the SURVEY App. B plan; faster, ~1e-7 relative)."""
         _lib.require_cuda()
         import os
 
-        self.precision = precision or os.environ.get("P3D_WL_PRECISION", "fp32")
+        self.precision = precision or os.environ.get("P3D_WL_PRECISION", "fp64")
         if self.precision not in ("fp32", "fp64"):
             raise ValueError("precision must be 'fp32' or 'fp64'")
         self.design = design
@@ -348,17 +374,22 @@ class Gp3dProblem:
                                tp.net_order, tp.pin_slot, tp.obj_slot_ptr)
         g.wl_f32 = 1 if self.precision == "fp32" else 0
         off4 = wl.rotated_pin_offsets(arr, self.rot) if P else np.zeros((0, 4))
-        slot = dt.pin_slot.cpu().numpy().astype(np.int64) if P else np.zeros(0, np.int64)
-        fb, fd, fs, fdup, finst, foff, fslot = fused_pin_layout(
-            arr.net_ptr, arr.pin_inst, slot, off4, arr.net_has_dup_inst)
+        L = self.layout = _with_dup_nets(
+            fused_pin_layout(arr.net_ptr, arr.pin_inst, off4, arr.net_has_dup_inst))
         one = lambda a, dt_: a if len(a) else np.zeros(1, dt_)  # noqa: E731
-        g.f_net_base = keep(_dev.i32(one(fb, np.int64)))
-        g.f_net_deg = keep(_dev.i32(one(fd, np.int64)))
-        g.f_net_stride = keep(_dev.i32(one(fs, np.int64)))
-        g.f_net_dup = keep(_dev.u8(one(fdup, bool)))
-        g.f_pin_inst = keep(_dev.i32(one(finst, np.int64)))
-        g.f_pin_off = keep(_dev.dev(one(foff.reshape(-1), np.float32), torch.float32))
-        g.f_pin_slot = keep(_dev.i32(one(fslot, np.int64)))
+        g.f_n_tasks = len(L["tasks"])
+        g.f_n_generic = len(L["generic"])
+        g.f_generic_nets = keep(_dev.i32(one(L["generic"], np.int64)))
+        g.f_tasks = keep(_dev.i32(one(L["tasks"].reshape(-1), np.int64)))
+        g.f_task_t0 = keep(_dev.i32(one(L["task_t0"], np.int64)))
+        g.f_net_base = keep(_dev.i32(one(L["net_base"], np.int64)))
+        g.f_net_deg = keep(_dev.i32(one(L["net_deg"], np.int64)))
+        g.f_net_stride = keep(_dev.i32(one(L["net_stride"], np.int64)))
+        g.f_net_dup = keep(_dev.u8(one(L["net_dup"], bool)))
+        g.f_pin_inst = keep(_dev.i32(one(L["pin_inst"], np.int64)))
+        g.f_pin_off = keep(_dev.dev(one(L["pin_off"].reshape(-1), np.float32), torch.float32))
+        g.f_obj_pins = keep(_dev.i32(one(L["obj_pins"], np.int64)))
+        g.nblk_net = max(1, min(-(-g.f_n_tasks // 4), K_MAX_BLOCKS))
         gs, gkeep = grid.device()
         g.grid = gs
         self._gkeep = gkeep
