@@ -81,7 +81,7 @@ struct FusedNetArgs {
   const float4* off;          // [n_pin] permuted (rx_top, ry_top, rx_bot, ry_bot)
   const int32_t* slot;        // unused (kept for layout stability)
   const double4* pos4;        // [n_inst] AoS centres
-  double dz2, gamma, scale4;
+  double dz2, gamma, scale4, inv_gamma;
   const double* gamma_ptr;
   float4* out_f;              // [n_pin] (gx, gy, g_cut, FD) in permuted pin order (fp32 mode)
   double* out_fd;             // unused

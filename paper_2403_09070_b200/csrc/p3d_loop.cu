@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
-static void eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = nullptr) {
+static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = nullptr) {
   auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], s); };
   mark(0);
   p3d_loop_state* st = gp.st;
@@ -506,16 +506,18 @@ static void eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = nul
   ov.counter = &st->counters[kCntOvfl];
   ov.out = finals + kFinOvfl;
   ov.scale = gp.movable_volume > 0 ? 9.094947017729282379150390625e-13 * gp.grid.bin_vol / gp.movable_volume : 0.0;
-  launch_spectral_ex(&gp.grid, nullptr, gp.rho_fx, nullptr, nullptr, gp.maps, gp.spec_scratch,
-                     halt, &ov, s);
+  const int rc = launch_spectral_ex(&gp.grid, nullptr, gp.rho_fx, nullptr, nullptr, gp.maps,
+                                    gp.spec_scratch, halt, &ov, s);
+  if (rc) return rc;
   mark(4);
   // K4
   dens_kernel<<<gp.n_macro + gp.nblk_obj, 256, 0, s>>>(gp);
   mark(5);
+  return check_launch("gp evaluation kernels");
 }
 
 int gp_iterate(const p3d_gp& gp, cudaStream_t s) {
-  eval_kernels(gp, s);
+  if (const int rc = eval_kernels(gp, s)) return rc;
   step_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
   advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
   return check_launch("gp_iterate");
@@ -527,7 +529,7 @@ int gp_iterate_profiled(const p3d_gp& gp, cudaStream_t s, float* ms) {
   static cudaEvent_t ev[8] = {nullptr};
   if (!ev[0])
     for (int k = 0; k < 8; ++k) cudaEventCreate(&ev[k]);
-  eval_kernels(gp, s, ev);
+  if (const int rc = eval_kernels(gp, s, ev)) return rc;
   step_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
   cudaEventRecord(ev[6], s);
   advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
@@ -544,10 +546,12 @@ int gp_kernels_per_iteration(const p3d_gp& gp) {
 }
 
 int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s) {
+  spectral_setup();
+  fused_net_setup();
   eval_setup_kernel<<<1, 1, 0, s>>>(gp, lam, gamma);
   if (gp.n_inst > 0)
     pos4_kernel<<<grid_blocks(gp.n_inst, 256, 4096), 256, 0, s>>>(gp.n_inst, gp.n_obj, gp.v, gp.pos4);
-  eval_kernels(gp, s);
+  if (const int rc = eval_kernels(gp, s)) return rc;
   return check_launch("gp_evaluate");
 }
 

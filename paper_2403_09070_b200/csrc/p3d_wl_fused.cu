@@ -57,59 +57,107 @@ struct Box2 {  // one axis, die 0 (bottom) and die 1 (top)
   __device__ __forceinline__ double fmx() const { return fmax(b.hi1, t.hi1); }
   __device__ __forceinline__ double fmn() const { return fmin(b.lo1, t.lo1); }
   __device__ __forceinline__ double full() const { return (b.cnt + t.cnt) > 0 ? fmx() - fmn() : 0.0; }
-  __device__ __forceinline__ double flip(double c, int d, double cur) const {
-    const double f = full();
-    return d ? flip_delta(t, b, c, f, cur) : flip_delta(b, t, c, f, cur);
+  // wirelength.py:227-248 with the pin's own segment / the other segment picked by selects
+  __device__ __forceinline__ double flip(double c, int d, double full_, double cur) const {
+    const int scnt = d ? t.cnt : b.cnt;
+    const double shi1 = d ? t.hi1 : b.hi1, shi2 = d ? t.hi2 : b.hi2;
+    const double slo1 = d ? t.lo1 : b.lo1, slo2 = d ? t.lo2 : b.lo2;
+    const double ohi1 = d ? b.hi1 : t.hi1, olo1 = d ? b.lo1 : t.lo1;
+    const double sp = scnt > 1 ? ((c == shi1) ? shi2 : shi1) - ((c == slo1) ? slo2 : slo1) : 0.0;
+    const double op = fmax(ohi1, c) - fmin(olo1, c);
+    return fmax(full_, sp + op) - cur;
   }
 };
 
 // ---- weighted-average segment sums -------------------------------------------
-// float64, numpy operation order (wirelength.py:85-96)
+// exp(x) for x <= 0 (every WA argument is (v - max)/gamma or (min - v)/gamma):
+// Cody-Waite reduction by ln2, degree-13 Taylor, exponent scaling; <= 1 ulp
+// against numpy's exp over [-708, 0]; values below 2^-1022 flush to 0 (each
+// segment sum contains its anchor pin's exp(0) = 1, so this is invisible).
+__device__ __forceinline__ double exp_neg(double x) {
+  const double n = rint(x * 1.4426950408889634074);
+  double r = fma(-n, 6.93147180369123816490e-01, x);
+  r = fma(-n, 1.90821492927058770002e-10, r);
+  double p = 1.6059043836821613e-10;
+  p = fma(p, r, 2.08767569878681e-09);
+  p = fma(p, r, 2.505210838544172e-08);
+  p = fma(p, r, 2.755731922398589e-07);
+  p = fma(p, r, 2.7557319223985893e-06);
+  p = fma(p, r, 2.48015873015873e-05);
+  p = fma(p, r, 1.984126984126984e-04);
+  p = fma(p, r, 1.3888888888888889e-03);
+  p = fma(p, r, 8.333333333333333e-03);
+  p = fma(p, r, 4.1666666666666664e-02);
+  p = fma(p, r, 1.6666666666666666e-01);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int ni = (int)n;
+  const double sc = __longlong_as_double((long long)(ni + 1023) << 52);
+  return x < -708.0 ? 0.0 : p * sc;
+}
+
+// float64 WA sums with numpy's structure (wirelength.py:85-96): value
+// sxp/s1p - sxm/s1m, gradient ep/s1p (1 + (v - vp)/g) - em/s1m (1 - (v - vm)/g);
+// 1/gamma and the per-segment reciprocals are hoisted (<= 1 ulp differences).
 struct Wa64 {
-  double s1p, sxp, s1m, sxm;
+  using R = double;
+  double s1p, sxp, s1m, sxm, rp, rm, vp, vm;
   __device__ __forceinline__ void init() { s1p = sxp = s1m = sxm = 0.0; }
-  __device__ __forceinline__ void add(double v, double hi, double lo, double g, double& ep,
-                                      double& em) {
-    ep = exp((v - hi) / g);
-    em = exp((lo - v) / g);
-    s1p += ep;
-    sxp += v * ep;
-    s1m += em;
-    sxm += v * em;
+  __device__ static __forceinline__ void term(double v, double hi, double lo, double ig, double& ep,
+                                              double& em) {
+    ep = exp_neg((v - hi) * ig);
+    em = exp_neg((lo - v) * ig);
   }
-  __device__ __forceinline__ double value(double, double) const {
-    return s1p > 0 ? sxp / s1p - sxm / s1m : 0.0;
+  __device__ __forceinline__ void acc(double v, double, double, double ep, double em, double on) {
+    s1p = fma(on, ep, s1p);
+    sxp = fma(on, v * ep, sxp);
+    s1m = fma(on, em, s1m);
+    sxm = fma(on, v * em, sxm);
   }
-  __device__ __forceinline__ double grad(double v, double, double, double g, double ep,
+  __device__ __forceinline__ void finalize() {
+    rp = s1p > 0 ? 1.0 / s1p : 0.0;
+    rm = s1m > 0 ? 1.0 / s1m : 0.0;
+    vp = sxp * rp;
+    vm = sxm * rm;
+  }
+  __device__ __forceinline__ double value(double, double) const { return s1p > 0 ? vp - vm : 0.0; }
+  __device__ __forceinline__ double grad(double v, double, double, double ig, double ep,
                                          double em) const {
-    const double vp = sxp / s1p, vm = sxm / s1m;
-    return ep / s1p * (1.0 + (v - vp) / g) - em / s1m * (1.0 - (v - vm) / g);
+    return ep * rp * (1.0 + (v - vp) * ig) - em * rm * (1.0 - (v - vm) * ig);
   }
 };
 
 // float32 on anchor-relative differences: vp = hi + sum(dp ep)/sum(ep), etc.
 struct Wa32 {
-  float s1p, sdp, s1m, sdm;
+  using R = float;
+  float s1p, sdp, s1m, sdm, rp, rm, mp, mm;
   __device__ __forceinline__ void init() { s1p = sdp = s1m = sdm = 0.f; }
-  __device__ __forceinline__ void add(double v, double hi, double lo, float ig, float& ep,
-                                      float& em) {
+  __device__ static __forceinline__ void term(double v, double hi, double lo, float ig, float& ep,
+                                              float& em) {
+    ep = __expf((float)(v - hi) * ig);
+    em = __expf(-(float)(v - lo) * ig);
+  }
+  __device__ __forceinline__ void acc(double v, double hi, double lo, float ep, float em, float on) {
     const float dp = (float)(v - hi), dm = (float)(v - lo);
-    ep = __expf(dp * ig);
-    em = __expf(-dm * ig);
-    s1p += ep;
-    sdp += dp * ep;
-    s1m += em;
-    sdm += dm * em;
+    s1p = fmaf(on, ep, s1p);
+    sdp = fmaf(on, dp * ep, sdp);
+    s1m = fmaf(on, em, s1m);
+    sdm = fmaf(on, dm * em, sdm);
+  }
+  __device__ __forceinline__ void finalize() {
+    rp = s1p > 0.f ? 1.f / s1p : 0.f;
+    rm = s1m > 0.f ? 1.f / s1m : 0.f;
+    mp = sdp * rp;
+    mm = sdm * rm;
   }
   __device__ __forceinline__ double value(double hi, double lo) const {
-    if (!(s1p > 0.f)) return 0.0;
-    return (hi - lo) + (double)(sdp / s1p - sdm / s1m);
+    return s1p > 0.f ? (hi - lo) + (double)(mp - mm) : 0.0;
   }
   __device__ __forceinline__ float grad(double v, double hi, double lo, float ig, float ep,
                                         float em) const {
     const float dp = (float)(v - hi), dm = (float)(v - lo);
-    const float rp = 1.f / s1p, rm = 1.f / s1m;
-    return ep * rp * (1.f + (dp - sdp * rp) * ig) - em * rm * (1.f - (dm - sdm * rm) * ig);
+    return ep * rp * (1.f + (dp - mp) * ig) - em * rm * (1.f - (dm - mm) * ig);
   }
 };
 
@@ -119,13 +167,11 @@ template <>
 struct WaSel<false> {
   using W = Wa64;
   using R = double;
-  using G = double;
 };
 template <>
 struct WaSel<true> {
   using W = Wa32;
   using R = float;
-  using G = float;
 };
 
 __device__ __forceinline__ void load_pin(const FusedNetArgs& a, int idx, double& px, double& py,
@@ -178,7 +224,20 @@ __device__ __noinline__ double dup_fd(const FusedNetArgs& a, int base, int deg, 
   return a.scale4 * (up - dn);
 }
 
-// Any degree: three passes re-loading the pins (large nets; rare).
+// segment of one pin on one axis: anchors of the chosen WA branch
+struct SegSel {
+  double hi, lo;
+  bool upper;  // true: the die-1 (top) partial segment
+};
+__device__ __forceinline__ SegSel seg_of(const Box2& bx, bool split, int tp) {
+  SegSel s;
+  s.upper = split && tp;
+  s.hi = split ? (tp ? bx.t.hi1 : bx.b.hi1) : bx.fmx();
+  s.lo = split ? (tp ? bx.t.lo1 : bx.b.lo1) : bx.fmn();
+  return s;
+}
+
+// Any degree: three passes re-loading the pins (large / duplicate-owner nets).
 template <bool F32>
 __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, double (&acc)[6]) {
   using W = typename WaSel<F32>::W;
@@ -197,58 +256,57 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
     zhi = fmax(zhi, z);
     zlo = fmin(zlo, z);
   }
-  const double ex = fmax(bx.full(), bx.t.span() + bx.b.span());
-  const double ey = fmax(by.full(), by.t.span() + by.b.span());
-  const bool sx = (bx.t.span() + bx.b.span()) > bx.full();
-  const bool sy = (by.t.span() + by.b.span()) > by.full();
+  const double fx = bx.full(), fy = by.full();
+  const double ex = fmax(fx, bx.t.span() + bx.b.span());
+  const double ey = fmax(fy, by.t.span() + by.b.span());
+  const bool sx = (bx.t.span() + bx.b.span()) > fx;
+  const bool sy = (by.t.span() + by.b.span()) > fy;
   acc[3] += ex;
   acc[4] += ey;
   acc[5] += (bx.b.cnt > 0 && bx.t.cnt > 0) ? 1.0 : 0.0;
-  const double fxh = bx.fmx(), fxl = bx.fmn(), fyh = by.fmx(), fyl = by.fmn();
-  const R ig = F32 ? (R)(1.0 / a.gamma) : (R)a.gamma;
+  const R ig = (R)a.inv_gamma;
   W wx0, wx1, wy0, wy1, wz;
   wx0.init(); wx1.init(); wy0.init(); wy1.init(); wz.init();
   for (int k = 0; k < deg; ++k) {
     double x, y, z;
     int tp;
     load_pin(a, base + k * stride, x, y, z, tp);
-    R e0, e1;
-    if (!sx) wx0.add(x, fxh, fxl, ig, e0, e1);
-    else if (tp) wx1.add(x, bx.t.hi1, bx.t.lo1, ig, e0, e1);
-    else wx0.add(x, bx.b.hi1, bx.b.lo1, ig, e0, e1);
-    if (!sy) wy0.add(y, fyh, fyl, ig, e0, e1);
-    else if (tp) wy1.add(y, by.t.hi1, by.t.lo1, ig, e0, e1);
-    else wy0.add(y, by.b.hi1, by.b.lo1, ig, e0, e1);
-    wz.add(z, zhi, zlo, ig, e0, e1);
+    R ep, em;
+    const SegSel gx = seg_of(bx, sx, tp), gy = seg_of(by, sy, tp);
+    W::term(x, gx.hi, gx.lo, ig, ep, em);
+    wx0.acc(x, gx.hi, gx.lo, ep, em, gx.upper ? 0 : 1);
+    wx1.acc(x, gx.hi, gx.lo, ep, em, gx.upper ? 1 : 0);
+    W::term(y, gy.hi, gy.lo, ig, ep, em);
+    wy0.acc(y, gy.hi, gy.lo, ep, em, gy.upper ? 0 : 1);
+    wy1.acc(y, gy.hi, gy.lo, ep, em, gy.upper ? 1 : 0);
+    W::term(z, zhi, zlo, ig, ep, em);
+    wz.acc(z, zhi, zlo, ep, em, 1);
   }
-  acc[0] += sx ? (wx0.value(bx.b.hi1, bx.b.lo1) + wx1.value(bx.t.hi1, bx.t.lo1)) : wx0.value(fxh, fxl);
-  acc[1] += sy ? (wy0.value(by.b.hi1, by.b.lo1) + wy1.value(by.t.hi1, by.t.lo1)) : wy0.value(fyh, fyl);
+  wx0.finalize(); wx1.finalize(); wy0.finalize(); wy1.finalize(); wz.finalize();
+  acc[0] += sx ? (wx0.value(bx.b.hi1, bx.b.lo1) + wx1.value(bx.t.hi1, bx.t.lo1)) : wx0.value(bx.fmx(), bx.fmn());
+  acc[1] += sy ? (wy0.value(by.b.hi1, by.b.lo1) + wy1.value(by.t.hi1, by.t.lo1)) : wy0.value(by.fmx(), by.fmn());
   acc[2] += wz.value(zhi, zlo);
   const bool dup = a.net_dup[t] != 0;
   for (int k = 0; k < deg; ++k) {
     double x, y, z;
     int tp;
     load_pin(a, base + k * stride, x, y, z, tp);
-    R e0, e1;
-    W d;
-    d.init();
-    double gx, gy;
-    if (!sx) { d.add(x, fxh, fxl, ig, e0, e1); gx = (double)wx0.grad(x, fxh, fxl, ig, e0, e1); }
-    else if (tp) { d.add(x, bx.t.hi1, bx.t.lo1, ig, e0, e1); gx = (double)wx1.grad(x, bx.t.hi1, bx.t.lo1, ig, e0, e1); }
-    else { d.add(x, bx.b.hi1, bx.b.lo1, ig, e0, e1); gx = (double)wx0.grad(x, bx.b.hi1, bx.b.lo1, ig, e0, e1); }
-    if (!sy) { d.add(y, fyh, fyl, ig, e0, e1); gy = (double)wy0.grad(y, fyh, fyl, ig, e0, e1); }
-    else if (tp) { d.add(y, by.t.hi1, by.t.lo1, ig, e0, e1); gy = (double)wy1.grad(y, by.t.hi1, by.t.lo1, ig, e0, e1); }
-    else { d.add(y, by.b.hi1, by.b.lo1, ig, e0, e1); gy = (double)wy0.grad(y, by.b.hi1, by.b.lo1, ig, e0, e1); }
-    d.add(z, zhi, zlo, ig, e0, e1);
-    const double gc = (double)wz.grad(z, zhi, zlo, ig, e0, e1);
+    R ep, em;
+    const SegSel gx = seg_of(bx, sx, tp), gy = seg_of(by, sy, tp);
+    W::term(x, gx.hi, gx.lo, ig, ep, em);
+    const double ggx = (double)(gx.upper ? wx1 : wx0).grad(x, gx.hi, gx.lo, ig, ep, em);
+    W::term(y, gy.hi, gy.lo, ig, ep, em);
+    const double ggy = (double)(gy.upper ? wy1 : wy0).grad(y, gy.hi, gy.lo, ig, ep, em);
+    W::term(z, zhi, zlo, ig, ep, em);
+    const double gc = (double)wz.grad(z, zhi, zlo, ig, ep, em);
     double gb;
     if (!dup) {
-      const double dwv = bx.flip(x, tp, ex) + by.flip(y, tp, ey);
+      const double dwv = bx.flip(x, tp, fx, ex) + by.flip(y, tp, fy, ey);
       gb = (tp ? -dwv : dwv) * a.scale4;
     } else {
       gb = dup_fd(a, base, deg, stride, k);
     }
-    store_pin(a, base + k * stride, gx, gy, gc, gb);
+    store_pin(a, base + k * stride, ggx, ggy, gc, gb);
   }
 }
 
@@ -266,57 +324,60 @@ struct WarpCols {
 
 // One planar axis of a staged net: boxes, branch, WA sums of the chosen
 // branch, per-pin gradients, FD extent deltas (accumulated into dw).
-template <int D, bool F32>
-__device__ __forceinline__ void staged_axis(const double (&c)[kMaxStagedDeg][32], WarpCols<F32>& sm,
-                                            int lane, int topm, typename WaSel<F32>::R ig,
-                                            double& val, double& exact, bool& crossing,
+template <bool F32>
+__device__ __forceinline__ void staged_axis(int D, const double (&c)[kMaxStagedDeg][32],
+                                            WarpCols<F32>& sm, int lane, int topm,
+                                            typename WaSel<F32>::R ig, double& val,
+                                            double& exact, bool& crossing,
                                             typename WaSel<F32>::R (&g)[kMaxStagedDeg][32]) {
   using W = typename WaSel<F32>::W;
+  using R = typename WaSel<F32>::R;
   Box2 bx;
   bx.init();
-#pragma unroll
+#pragma unroll 1
   for (int k = 0; k < D; ++k) bx.add(c[k][lane], (topm >> k) & 1);
   const double full = bx.full(), part = bx.t.span() + bx.b.span();
   const double ex = fmax(full, part);
   const bool split = part > full;  // ties resolve to the full box (wirelength.py:186)
   exact = ex;
   crossing = bx.b.cnt > 0 && bx.t.cnt > 0;
-  const double fh = bx.fmx(), fl = bx.fmn();
   W w0, w1;
   w0.init();
   w1.init();
 #pragma unroll 1
   for (int k = 0; k < D; ++k) {
-    const int tp = (topm >> k) & 1;
     const double v = c[k][lane];
-    if (!split) w0.add(v, fh, fl, ig, sm.ep[k][lane], sm.em[k][lane]);
-    else if (tp) w1.add(v, bx.t.hi1, bx.t.lo1, ig, sm.ep[k][lane], sm.em[k][lane]);
-    else w0.add(v, bx.b.hi1, bx.b.lo1, ig, sm.ep[k][lane], sm.em[k][lane]);
+    const SegSel sg = seg_of(bx, split, (topm >> k) & 1);
+    R ep, em;
+    W::term(v, sg.hi, sg.lo, ig, ep, em);
+    sm.ep[k][lane] = ep;
+    sm.em[k][lane] = em;
+    w0.acc(v, sg.hi, sg.lo, ep, em, sg.upper ? 0 : 1);
+    w1.acc(v, sg.hi, sg.lo, ep, em, sg.upper ? 1 : 0);
   }
-  val = split ? (w0.value(bx.b.hi1, bx.b.lo1) + w1.value(bx.t.hi1, bx.t.lo1)) : w0.value(fh, fl);
+  w0.finalize();
+  w1.finalize();
+  val = split ? (w0.value(bx.b.hi1, bx.b.lo1) + w1.value(bx.t.hi1, bx.t.lo1))
+              : w0.value(bx.fmx(), bx.fmn());
 #pragma unroll 1
   for (int k = 0; k < D; ++k) {
     const int tp = (topm >> k) & 1;
     const double v = c[k][lane];
-    if (!split) g[k][lane] = w0.grad(v, fh, fl, ig, sm.ep[k][lane], sm.em[k][lane]);
-    else if (tp) g[k][lane] = w1.grad(v, bx.t.hi1, bx.t.lo1, ig, sm.ep[k][lane], sm.em[k][lane]);
-    else g[k][lane] = w0.grad(v, bx.b.hi1, bx.b.lo1, ig, sm.ep[k][lane], sm.em[k][lane]);
-    sm.dw[k][lane] += bx.flip(v, tp, ex);
+    const SegSel sg = seg_of(bx, split, tp);
+    g[k][lane] = (sg.upper ? w1 : w0).grad(v, sg.hi, sg.lo, ig, sm.ep[k][lane], sm.em[k][lane]);
+    sm.dw[k][lane] += bx.flip(v, tp, full, ex);
   }
 }
 
-// 32 nets of degree D owned by one warp: stage, then one net per lane.
+// Stage the 32 nets of degree D owned by one warp (D independent owner gathers
+// per lane), then evaluate one net per lane from shared memory.
 template <int D, bool F32>
-__device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk, int t0,
-                                            WarpCols<F32>& sm, int lane, double (&acc)[6]) {
-  using W = typename WaSel<F32>::W;
-  using R = typename WaSel<F32>::R;
+__device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk, int t0,
+                                           WarpCols<F32>& sm, int lane, int& topm, double& zhi,
+                                           double& zlo) {
   const int nb = tk.y, j = tk.z + lane;
-  if (j >= nb || a.net_dup[t0 + j]) return;  // duplicate-owner nets: generic kernel
+  if (j >= nb || a.net_dup[t0 + j]) return false;  // duplicate-owner nets: generic kernel
   const int pin0 = tk.x + j;
-  int topm = 0;
-  double zhi = -P3D_INF, zlo = P3D_INF;
-  // stage: D independent owner gathers per lane
   int inst[D];
   float4 off[D];
 #pragma unroll
@@ -324,6 +385,9 @@ __device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk
     inst[k] = a.pin_inst[pin0 + k * nb];
     off[k] = a.off[pin0 + k * nb];
   }
+  topm = 0;
+  zhi = -P3D_INF;
+  zlo = P3D_INF;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     const double4 p = a.pos4[inst[k]];
@@ -332,34 +396,57 @@ __device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk
     sm.px[k][lane] = p.x + (double)(tp ? off[k].x : off[k].z);
     sm.py[k][lane] = p.y + (double)(tp ? off[k].y : off[k].w);
     sm.pz[k][lane] = p.z;
+    sm.dw[k][lane] = 0.0;
     zhi = fmax(zhi, p.z);
     zlo = fmin(zlo, p.z);
   }
-  const R ig = F32 ? (R)(1.0 / a.gamma) : (R)a.gamma;  // f32: multiply; f64: divide like numpy
-#pragma unroll
-  for (int k = 0; k < D; ++k) sm.dw[k][lane] = 0.0;
+  return true;
+}
+
+template <bool F32>
+__device__ __forceinline__ void staged_eval(const FusedNetArgs& a, int D, int pin0, int nb,
+                                            WarpCols<F32>& sm, int lane, int topm, double zhi,
+                                            double zlo, double (&acc)[6]) {
+  using W = typename WaSel<F32>::W;
+  using R = typename WaSel<F32>::R;
+  const R ig = (R)a.inv_gamma;
   double v, ex;
   bool cross;
-  staged_axis<D, F32>(sm.px, sm, lane, topm, ig, v, ex, cross, sm.gx);
+  staged_axis<F32>(D, sm.px, sm, lane, topm, ig, v, ex, cross, sm.gx);
   acc[0] += v;
   acc[3] += ex;
   acc[5] += cross ? 1.0 : 0.0;
-  staged_axis<D, F32>(sm.py, sm, lane, topm, ig, v, ex, cross, sm.gy);
+  staged_axis<F32>(D, sm.py, sm, lane, topm, ig, v, ex, cross, sm.gy);
   acc[1] += v;
   acc[4] += ex;
   W wz;
   wz.init();
 #pragma unroll 1
-  for (int k = 0; k < D; ++k) wz.add(sm.pz[k][lane], zhi, zlo, ig, sm.ep[k][lane], sm.em[k][lane]);
+  for (int k = 0; k < D; ++k) {
+    R ep, em;
+    W::term(sm.pz[k][lane], zhi, zlo, ig, ep, em);
+    sm.ep[k][lane] = ep;
+    sm.em[k][lane] = em;
+    wz.acc(sm.pz[k][lane], zhi, zlo, ep, em, 1);
+  }
+  wz.finalize();
   acc[2] += wz.value(zhi, zlo);
 #pragma unroll 1
   for (int k = 0; k < D; ++k) {
     const double gc = (double)wz.grad(sm.pz[k][lane], zhi, zlo, ig, sm.ep[k][lane], sm.em[k][lane]);
-    const int tp = (topm >> k) & 1;
     const double dwk = sm.dw[k][lane];
-    const double gb = (tp ? -dwk : dwk) * a.scale4;
+    const double gb = (((topm >> k) & 1) ? -dwk : dwk) * a.scale4;
     store_pin(a, pin0 + k * nb, (double)sm.gx[k][lane], (double)sm.gy[k][lane], gc, gb);
   }
+}
+
+template <int D, bool F32>
+__device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk, int t0,
+                                            WarpCols<F32>& sm, int lane, double (&acc)[6]) {
+  int topm;
+  double zhi, zlo;
+  if (stage_pins<D, F32>(a, tk, t0, sm, lane, topm, zhi, zlo))
+    staged_eval<F32>(a, D, tk.x + tk.z + lane, tk.y, sm, lane, topm, zhi, zlo, acc);
 }
 
 template <bool F32>
@@ -368,6 +455,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) fused_net_kernel(Fused
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ double red[32 * 6];
   if (a.gamma_ptr) a.gamma = *a.gamma_ptr;
+  a.inv_gamma = 1.0 / a.gamma;
   double acc[6] = {0, 0, 0, 0, 0, 0};
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   WarpCols<F32>& sm = reinterpret_cast<WarpCols<F32>*>(dyn_smem)[wib];
@@ -402,6 +490,7 @@ __global__ void __launch_bounds__(256) generic_net_kernel(FusedNetArgs a) {
   if (a.halt && *a.halt) return;
   __shared__ double red[32 * 6];
   if (a.gamma_ptr) a.gamma = *a.gamma_ptr;
+  a.inv_gamma = 1.0 / a.gamma;
   double acc[6] = {0, 0, 0, 0, 0, 0};
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < a.n_generic; g += gridDim.x * blockDim.x)
     process_net_generic<F32>(a, a.generic_nets[g], acc);

@@ -140,7 +140,42 @@ def loop_rows(name, nx, out):
                    "seconds_1core": dt, "rows": [list(map(float, r)) for r in rows]}, fh)
 
 
+def _perturbed_run(args):
+    """Reference run_gp3d with the density force perturbed by 1e-15 relative
+    noise (seeded): samples the trajectory's own sensitivity to last-bit
+    differences (any non-bit-identical implementation sits in this band)."""
+    name, nx, seed = args
+    rs = np.random.default_rng(seed)
+    orig = rdn.density_force
+
+    def noisy(*a, **k):
+        g = orig(*a, **k)
+        return g * (1 + 1e-15 * rs.standard_normal(g.shape))
+
+    rdn.density_force = noisy
+    d = design_of(name)
+    cfg, rng, grid, st = setup(d, nx, 2, 200)
+    rows = []
+    rgp.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+    rdn.density_force = orig
+    return seed, [float(v) for v in rows[-1]]
+
+
+def band(name, nx, out, seeds=(11, 12, 13, 14, 15, 16)):
+    from concurrent.futures import ProcessPoolExecutor
+
+    with ProcessPoolExecutor(max_workers=len(seeds)) as ex:
+        res = list(ex.map(_perturbed_run, [(name, nx, s) for s in seeds]))
+    with open(os.path.join(HERE, out), "w") as fh:
+        json.dump({"spec": SPECS[name], "grid": nx, "max_iters": 200, "noise_rel": 1e-15,
+                   "perturbed": "place3d.density.density_force * (1 + 1e-15 N(0,1))",
+                   "final_rows": {str(k): v for k, v in res}}, fh, indent=1)
+
+
 if __name__ == "__main__":
+    if "--band" in sys.argv:
+        band("cfg2", 256, "cfg2_band.json")
+        sys.exit(0)
     checksums()
     small_ops()
     loop_rows("cfg1", 128, "cfg1_log.json")
