@@ -258,11 +258,20 @@ def main():
     s = prob.state()
     assert not s.done and s.it == W + K, f"loop ended early (it={s.it}, done={s.done})"
 
-    # ---- per-stage attribution (same state continues; events between stages)
+    # ---- per-stage attribution: the same iteration captured with event-record
+    # nodes between the stages, replayed K times (no host gaps inside)
     stage = np.zeros(7)
     buf = (C.c_float * 7)()
+    mg = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(stream)
+    with torch.cuda.stream(side), torch.cuda.graph(mg, stream=side):
+        _lib.call("p3d_gp_iterate_marked", _lib.byref(prob.gp), _lib.stream_ptr())
+    stream.wait_stream(side)
     for _ in range(K):
-        _lib.call("p3d_gp_iterate_profiled", _lib.byref(prob.gp), _lib.stream_ptr(), buf)
+        mg.replay()
+        torch.cuda.synchronize()
+        _lib.call("p3d_gp_stage_times", buf)
         stage += np.frombuffer(buf, dtype=np.float32)
     stage /= K
     kpi = _lib.load().p3d_gp_kernels_per_iteration(_lib.byref(prob.gp))

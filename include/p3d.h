@@ -248,6 +248,12 @@ int p3d_gp_evaluate(const p3d_gp* gp, double lam, double gamma, void* stream);
  * K5a (precondition/BB), K5b (advance); stage_ms: HOST float[7].  Blocks until
  * the iteration finishes.  Not capturable (benchmark attribution only). */
 int p3d_gp_iterate_profiled(const p3d_gp* gp, void* stream, float* stage_ms);
+/* p3d_gp_iterate with library-owned stage events recorded as external
+ * event nodes (capturable); p3d_gp_stage_times then waits for the last event
+ * and returns the 7 stage durations (ms, HOST float[7]) of the most recent
+ * marked iteration (e.g. a replayed graph). */
+int p3d_gp_iterate_marked(const p3d_gp* gp, void* stream);
+int p3d_gp_stage_times(float* stage_ms);
 /* Number of kernels one p3d_gp_iterate enqueues (>0), or -1 on bad input. */
 int p3d_gp_kernels_per_iteration(const p3d_gp* gp);
 /* Gp3dProblem.project (gp.py:280-294): out = P(in), [3][n_obj]. */

@@ -51,6 +51,8 @@ int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s);
 int gp_project(const p3d_gp& gp, const double* in, double* out, cudaStream_t s);
 int gp_iterate_profiled(const p3d_gp& gp, cudaStream_t s, float* ms);
 int gp_kernels_per_iteration(const p3d_gp& gp);
+int gp_iterate_marked(const p3d_gp& gp, cudaStream_t s);
+int gp_stage_times(float* ms);
 
 static NetArgs net_args(const p3d_topology* t) {
   NetArgs a{};
@@ -310,6 +312,16 @@ int p3d_gp_iterate(const p3d_gp* gp, void* stream) {
 int p3d_gp_iterate_profiled(const p3d_gp* gp, void* stream, float* stage_ms) {
   if (bad_gp(gp) || !stage_ms) return P3D_ERR_ARG;
   return gp_iterate_profiled(*gp, STREAM(stream), stage_ms);
+}
+
+int p3d_gp_iterate_marked(const p3d_gp* gp, void* stream) {
+  if (bad_gp(gp)) return P3D_ERR_ARG;
+  return gp_iterate_marked(*gp, STREAM(stream));
+}
+
+int p3d_gp_stage_times(float* stage_ms) {
+  if (!stage_ms) return P3D_ERR_ARG;
+  return gp_stage_times(stage_ms);
 }
 
 int p3d_gp_kernels_per_iteration(const p3d_gp* gp) {

@@ -10,12 +10,17 @@
 //   K3  spectral        phi/E maps; the first pass also yields the overflow
 //                       and re-zeroes rho for the next iteration
 //   K4  dens_kernel     density means -> dens grad; WL grad assembly; energy;
+//                       preconditioned current and re-weighted previous
+//                       gradient (Eq. 19) and the BB norms |dv|, |dg|;
 //                       last block: objective, lambda init, log row, best key,
-//                       stop and divergence tests            (gp.py:386-422)
-//   K5a step_kernel     best copy, precondition x2, BB norms; last block: step
-//                       size, underflow test, momentum        (gp.py:423-437)
-//   K5b advance_kernel  u' = P(v - s g), v' = P(u' + m (u' - u)); last block:
-//                       mu schedule, lambda update, next gamma (gp.py:437-444)
+//                       stop / divergence tests, BB step, underflow test
+//                       (gp.py:386-437)
+//   K5a gmax0_kernel    iteration 0 only: max|g| for the initial step
+//                       (gp.py:198-202, needs the just-initialised lambda)
+//   K5b advance_kernel  best snapshot; u' = P(v - s g), v' = P(u' + m (u' - u))
+//                       with g re-derived from the stored gradients; last
+//                       block: mu schedule, lambda update, next gamma
+//                       (gp.py:220-227, 442-444)
 #include <math.h>
 
 #include "p3d_geom.cuh"
@@ -140,38 +145,84 @@ __global__ void pos4_kernel(int I, int O, const double* v, double* pos4) {
 // ---------------------------------------------------------------------------
 // K4: density gather + objective assembly; last block = loop control part 1
 // ---------------------------------------------------------------------------
-__device__ void finish_object(const p3d_gp& gp, int i, const Charge& q, const double (&mean)[4],
-                              double (&acc)[4]) {
+__device__ __forceinline__ double precond_div(double lam, double q, double mdeg) {
+  double d = lam * q;  // gp.py:142-147 operation order
+  d = d + mdeg;
+  return fmax(d, 1.0);
+}
+
+// acc: energy, |dens|_1, |wl|_1, non-finite count, |dv|^2, |dg|^2
+__device__ __forceinline__ void finish_object(const p3d_gp& gp, int i, const Charge& q, const double (&mean)[4],
+                              double (&acc)[6]) {
   const int O = gp.n_obj, I = gp.n_inst;
   const double qq = charge_of(q);
   const double c = -2.0 * qq;
-  const double dgx = mean[1] * c, dgy = mean[2] * c;
-  const double dgz = i < I ? mean[3] * c : 0.0;  // filler depth frozen (gp.py:255)
-  double gx = 0.0, gy = 0.0, gz = 0.0;
+  double dg[3] = {mean[1] * c, mean[2] * c, i < I ? mean[3] * c : 0.0};  // filler z frozen
+  double wl[3] = {0.0, 0.0, 0.0};
   if (i < I) {
     const double* f = fin(gp);
-    gx = gp.inst_g[i];
-    gy = gp.inst_g[I + i];
+    wl[0] = gp.inst_g[i];
+    wl[1] = gp.inst_g[I + i];
     const double gzh = gp.inst_g[2 * I + i], gzb = gp.inst_g[3 * I + i];
     const double base = f[kFinNorm + 2] == 0.0 ? 0.0 : f[kFinNorm + 3] * gzb;
-    gz = base + gp.alpha * gzh;  // wirelength.py:296-305
+    wl[2] = base + gp.alpha * gzh;  // wirelength.py:296-305
   }
-  gp.wl_grad[i] = gx;
-  gp.wl_grad[O + i] = gy;
-  gp.wl_grad[2 * O + i] = gz;
-  gp.dens_grad[i] = dgx;
-  gp.dens_grad[O + i] = dgy;
-  gp.dens_grad[2 * O + i] = dgz;
-  const double lam = gp.st->lam_eval;
-  const double t0 = gx + lam * dgx, t1 = gy + lam * dgy, t2 = gz + lam * dgz;
+  const p3d_loop_state* st = gp.st;
+  const double lam = st->lam_eval;
+  bool finite = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) finite = finite && isfinite(wl[k] + lam * dg[k]);
   acc[0] += qq * mean[0];
-  acc[1] += fabs(dgx) + fabs(dgy) + fabs(dgz);
-  acc[2] += fabs(gx) + fabs(gy) + fabs(gz);
-  acc[3] += (isfinite(t0) && isfinite(t1) && isfinite(t2)) ? 0.0 : 1.0;
+  acc[1] += fabs(dg[0]) + fabs(dg[1]) + fabs(dg[2]);
+  acc[2] += fabs(wl[0]) + fabs(wl[1]) + fabs(wl[2]);
+  acc[3] += finite ? 0.0 : 1.0;
+  if (st->eval_only) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      gp.wl_grad[(long long)k * O + i] = wl[k];
+      gp.dens_grad[(long long)k * O + i] = dg[k];
+    }
+    return;
+  }
+  // BB norms need the previous iteration's raw gradients re-weighted by the
+  // current lambda (gp.py:427-435); at iteration 0 there is no previous point.
+  if (st->step_set) {
+    const double mdeg = (i < I && gp.is_macro[i]) ? gp.degree[i] : 0.0;
+    const double div = precond_div(lam, qq, mdeg);
+    const double divp = precond_div(lam, gp.prev_q[i], mdeg);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const long long j = (long long)k * O + i;
+      const double pre = (wl[k] + lam * dg[k]) / div;
+      const double pp = (gp.prev_wl[j] + lam * gp.prev_dens[j]) / divp;
+      const double d = pre - pp, dv = gp.v[j] - gp.v_prev[j];
+      acc[4] += dv * dv;
+      acc[5] += d * d;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    gp.prev_wl[(long long)k * O + i] = wl[k];
+    gp.prev_dens[(long long)k * O + i] = dg[k];
+  }
+  gp.prev_q[i] = qq;
 }
 
-__device__ void control_after_eval(const p3d_gp& gp, double energy, double l1_dens,
-                                   double l1_wl, double nonfinite) {
+// underflow test and momentum of the accepted step (gp.py:218-226)
+__device__ __noinline__ void step_tail(const p3d_gp& gp) {
+  p3d_loop_state* st = gp.st;
+  if (!isfinite(st->step) || st->step <= gp.min_step) {  // StepUnderflow, gp.py:438-441
+    st->diverged = 1;
+    st->stop_now = 1;  // the best snapshot of this iteration is still taken
+    return;
+  }
+  const double a = st->a;
+  st->a_new = (1 + sqrt(4 * (a * a) + 1)) / 2;
+  st->mom = (a - 1) / st->a_new;
+}
+
+__device__ __noinline__ void control_after_eval(const p3d_gp& gp, double energy, double l1_dens,
+                                   double l1_wl, double nonfinite, double dv2, double dg2) {
   p3d_loop_state* st = gp.st;
   const double* f = fin(gp);
   const double wl_bi = f[kFinNet + 0] + f[kFinNet + 1];
@@ -242,15 +293,25 @@ __device__ void control_after_eval(const p3d_gp& gp, double energy, double l1_de
     if (gp.ovfl_hist[first] - gp.ovfl_hist[it] < 1e-3) {
       st->diverged = 1;
       st->stop_now = 1;
+      return;
     }
   }
+  st->dv2 = dv2;
+  st->dg2 = dg2;
+  if (!st->step_set) return;  // iteration 0: gmax0_kernel sets the initial step
+  const double den = sqrt(dg2);  // gp.py:210-217
+  if (den > 0) {
+    const double bb = sqrt(dv2) / den;
+    st->step = fmin(fmax(bb, st->step / 4), st->step * 4);
+  }
+  step_tail(gp);
 }
 
 __global__ void __launch_bounds__(256) dens_kernel(p3d_gp gp) {
   if (gp.st->done) return;
-  __shared__ double red[32 * 4];
+  __shared__ double red[32 * 6];
   const CloudGP cl = cloud_of(gp, gp.v);
-  double acc[4] = {0, 0, 0, 0};
+  double acc[6] = {0, 0, 0, 0, 0, 0};
   const int nm = gp.n_macro;
   if ((int)blockIdx.x < nm) {
     const int i = gp.macro_ids[blockIdx.x];
@@ -269,108 +330,47 @@ __global__ void __launch_bounds__(256) dens_kernel(p3d_gp gp) {
     }
   }
   double* part = gp.partials + (long long)kSlotDens * kPartialStride;
-  block_sum<4>(acc, red);
+  block_sum<6>(acc, red);
   if (threadIdx.x == 0)
-    for (int k = 0; k < 4; ++k) part[k * gridDim.x + blockIdx.x] = acc[k];
+    for (int k = 0; k < 6; ++k) part[k * gridDim.x + blockIdx.x] = acc[k];
   if (last_block(&gp.st->counters[kCntDens])) {
-    double tot[4];
-    for (int k = 0; k < 4; ++k) tot[k] = ordered_sum(part + k * gridDim.x, gridDim.x, red);
-    if (threadIdx.x == 0) control_after_eval(gp, tot[0], tot[1], tot[2], tot[3]);
+    double tot[6];
+    for (int k = 0; k < 6; ++k) tot[k] = ordered_sum(part + k * gridDim.x, gridDim.x, red);
+    if (threadIdx.x == 0) control_after_eval(gp, tot[0], tot[1], tot[2], tot[3], tot[4], tot[5]);
   }
 }
 
 // ---------------------------------------------------------------------------
-// K5a: best snapshot, preconditioning (Eq. 19) of current and re-weighted
-// previous gradients, BB norms; last block: step size
+// K5a: iteration 0 only — max |g| of the preconditioned gradient under the
+// just-initialised lambda, then the initial step wb / max|g| (gp.py:198-202)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) step_kernel(p3d_gp gp) {
+__global__ void __launch_bounds__(256) gmax0_kernel(p3d_gp gp) {
   p3d_loop_state* st = gp.st;
-  if (st->done) return;
-  __shared__ double red[32 * 3];
-  const int O = gp.n_obj;
-  const bool best = st->best_flag != 0, stop = st->stop_now != 0;
-  const bool have_prev = st->step_set != 0;
+  if (st->done || st->step_set || st->stop_now) return;
+  __shared__ double red[32];
+  const int O = gp.n_obj, I = gp.n_inst;
   const double lam = st->lam;
-  const CloudGP cl = cloud_of(gp, gp.v);
-  double acc[3] = {0, 0, 0};  // |dv|^2, |dg|^2, max|g|
+  double m = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < O; i += gridDim.x * blockDim.x) {
-    if (best) {
-      gp.best[i] = gp.u[i];
-      gp.best[O + i] = gp.u[O + i];
-      gp.best[2 * O + i] = gp.u[2 * O + i];
-    }
-    if (stop) continue;
-    const double q = charge_of(cl.get(i));
-    const double mdeg = (i < gp.n_inst && gp.is_macro[i]) ? gp.degree[i] : 0.0;
-    double div = lam * q;
-    div = div + mdeg;
-    div = fmax(div, 1.0);
-    double divp = 1.0;
-    if (have_prev) {
-      divp = lam * gp.prev_q[i];
-      divp = divp + mdeg;
-      divp = fmax(divp, 1.0);
-    }
+    const double mdeg = (i < I && gp.is_macro[i]) ? gp.degree[i] : 0.0;
+    const double div = precond_div(lam, gp.prev_q[i], mdeg);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const long long k = (long long)c * O + i;
-      const double wl = gp.wl_grad[k], dn = gp.dens_grad[k];
-      const double pre = (wl + lam * dn) / div;
-      if (have_prev) {
-        const double pp = (gp.prev_wl[k] + lam * gp.prev_dens[k]) / divp;
-        const double dg = pre - pp, dv = gp.v[k] - gp.v_prev[k];
-        acc[0] += dv * dv;
-        acc[1] += dg * dg;
-      }
-      acc[2] = fmax(acc[2], fabs(pre));
-      gp.pre[k] = pre;
-      gp.prev_wl[k] = wl;
-      gp.prev_dens[k] = dn;
+    for (int k = 0; k < 3; ++k) {
+      const long long j = (long long)k * O + i;
+      m = fmax(m, fabs((gp.prev_wl[j] + lam * gp.prev_dens[j]) / div));
     }
-    gp.prev_q[i] = q;
   }
   double* part = gp.partials + (long long)kSlotStep * kPartialStride;
-  {
-    double s2[2] = {acc[0], acc[1]};
-    block_sum<2>(s2, red);
-    double m = block_max(acc[2], red + 64);
-    if (threadIdx.x == 0) {
-      part[blockIdx.x] = s2[0];
-      part[gridDim.x + blockIdx.x] = s2[1];
-      part[2 * gridDim.x + blockIdx.x] = m;
-    }
-  }
+  m = block_max(m, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = m;
   if (last_block(&st->counters[kCntStep])) {
-    const double dv2 = ordered_sum(part, gridDim.x, red);
-    const double dg2 = ordered_sum(part + gridDim.x, gridDim.x, red);
     if (threadIdx.x == 0) {
-      if (stop) {
-        st->done = 1;
-        return;
-      }
       double gm = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) gm = fmax(gm, ((volatile double*)part)[2 * gridDim.x + b]);
-      st->dv2 = dv2;
-      st->dg2 = dg2;
+      for (int b = 0; b < (int)gridDim.x; ++b) gm = fmax(gm, ((volatile double*)part)[b]);
       st->gmax = gm;
-      if (!st->step_set) {  // gp.py:198-202, 207-209
-        st->step = gm == 0.0 ? 1.0 : gp.step_scale / gm;
-        st->step_set = 1;
-      } else {  // gp.py:210-217
-        const double den = sqrt(dg2);
-        if (den > 0) {
-          const double bb = sqrt(dv2) / den;
-          st->step = fmin(fmax(bb, st->step / 4), st->step * 4);
-        }
-      }
-      if (!isfinite(st->step) || st->step <= gp.min_step) {  // gp.py:218-219, 438-441
-        st->diverged = 1;
-        st->done = 1;
-        return;
-      }
-      const double a = st->a;
-      st->a_new = (1 + sqrt(4 * (a * a) + 1)) / 2;
-      st->mom = (a - 1) / st->a_new;
+      st->step = gm == 0.0 ? 1.0 : gp.step_scale / gm;
+      st->step_set = 1;
+      step_tail(gp);
     }
   }
 }
@@ -381,15 +381,28 @@ __global__ void __launch_bounds__(256) step_kernel(p3d_gp gp) {
 __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
   p3d_loop_state* st = gp.st;
   if (st->done) return;
-  const int O = gp.n_obj;
-  const double step = st->step, mom = st->mom;
+  const int O = gp.n_obj, I = gp.n_inst;
+  const bool best = st->best_flag != 0, stop = st->stop_now != 0;
+  const double step = st->step, mom = st->mom, lam = st->lam;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < O; i += gridDim.x * blockDim.x) {
-    double v[3], u[3], un[3], vn[3];
+    double u[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) u[c] = gp.u[(long long)c * O + i];
+    if (best) {  // gp.py:406-409 (taken before the stop / advance, as in the reference)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) gp.best[(long long)c * O + i] = u[c];
+    }
+    if (stop) continue;
+    // the step's gradient, re-derived from the stored raw gradients (gp.py:424-426)
+    const double mdeg = (i < I && gp.is_macro[i]) ? gp.degree[i] : 0.0;
+    const double div = precond_div(lam, gp.prev_q[i], mdeg);
+    double v[3], un[3], vn[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      v[c] = gp.v[(long long)c * O + i];
-      u[c] = gp.u[(long long)c * O + i];
-      un[c] = v[c] - step * gp.pre[(long long)c * O + i];
+      const long long j = (long long)c * O + i;
+      v[c] = gp.v[j];
+      const double pre = (gp.prev_wl[j] + lam * gp.prev_dens[j]) / div;
+      un[c] = v[c] - step * pre;
     }
     project_obj(gp, i, un[0], un[1], un[2]);
 #pragma unroll
@@ -402,11 +415,14 @@ __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
       gp.u[k] = un[c];
       gp.v[k] = vn[c];
     }
-    if (i < gp.n_inst)
-      reinterpret_cast<double4*>(gp.pos4)[i] = make_double4(vn[0], vn[1], vn[2], 0.0);
+    if (i < I) reinterpret_cast<double4*>(gp.pos4)[i] = make_double4(vn[0], vn[1], vn[2], 0.0);
   }
   if (last_block(&st->counters[kCntAdvance])) {
     if (threadIdx.x == 0) {
+      if (stop) {
+        st->done = 1;
+        return;
+      }
       st->a = st->a_new;
       // mu_from_overflow (gp.py:156-168), lambda update (gp.py:442-444)
       const double drop = st->prev_ovfl - st->ovfl;
@@ -434,8 +450,13 @@ __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
-static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = nullptr) {
-  auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], s); };
+static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = nullptr,
+                        bool external = false) {
+  auto mark = [&](int k) {
+    if (!ev) return;
+    if (external) cudaEventRecordWithFlags(ev[k], s, cudaEventRecordExternal);
+    else cudaEventRecord(ev[k], s);
+  };
   mark(0);
   p3d_loop_state* st = gp.st;
   const int* halt = &st->done;
@@ -518,7 +539,7 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
 
 int gp_iterate(const p3d_gp& gp, cudaStream_t s) {
   if (const int rc = eval_kernels(gp, s)) return rc;
-  step_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  gmax0_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
   advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
   return check_launch("gp_iterate");
 }
@@ -530,13 +551,36 @@ int gp_iterate_profiled(const p3d_gp& gp, cudaStream_t s, float* ms) {
   if (!ev[0])
     for (int k = 0; k < 8; ++k) cudaEventCreate(&ev[k]);
   if (const int rc = eval_kernels(gp, s, ev)) return rc;
-  step_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  gmax0_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
   cudaEventRecord(ev[6], s);
   advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
   cudaEventRecord(ev[7], s);
   cudaEventSynchronize(ev[7]);
   for (int k = 0; k < 7; ++k) cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]);
   return check_launch("gp_iterate_profiled");
+}
+
+// Capturable variant: the stage events become event-record nodes of a CUDA
+// graph, so a replayed graph is attributed without host gaps; read the stage
+// times with gp_stage_times after the replay completes.
+static cudaEvent_t g_marks[8] = {nullptr};
+
+int gp_iterate_marked(const p3d_gp& gp, cudaStream_t s) {
+  if (!g_marks[0])
+    for (int k = 0; k < 8; ++k) cudaEventCreate(&g_marks[k]);
+  if (const int rc = eval_kernels(gp, s, g_marks, true)) return rc;
+  gmax0_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  cudaEventRecordWithFlags(g_marks[6], s, cudaEventRecordExternal);
+  advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  cudaEventRecordWithFlags(g_marks[7], s, cudaEventRecordExternal);
+  return check_launch("gp_iterate_marked");
+}
+
+int gp_stage_times(float* ms) {
+  if (!g_marks[0]) return P3D_ERR_ARG;
+  if (cudaEventSynchronize(g_marks[7]) != cudaSuccess) return check_launch("stage times");
+  for (int k = 0; k < 7; ++k) cudaEventElapsedTime(&ms[k], g_marks[k], g_marks[k + 1]);
+  return check_launch("stage times");
 }
 
 // kernels enqueued by one gp_iterate (for the benchmark's launch count)

@@ -72,12 +72,24 @@ def test_cfg1_200_iterations_fp32():
     _check(rows, gold, tight=None)
 
 
-@pytest.mark.skipif(not os.path.exists(os.path.join(GOLD, "cfg2_log.json")),
-                    reason="config-2 golden not generated")
-def test_cfg2_200_iterations():
+def test_cfg2_200_iterations_vs_reference_band():
+    """Config 2 (100k cells) is chaotic in the last ~40 iterations: the
+    reference itself, with its density force perturbed by 1e-15 relative noise
+    (tests/golden/cfg2_band.json, produced by place3d), ends on one of two
+    attractors (8.97e6 or 9.18e6 WL).  The gate is therefore: the trajectory
+    agrees with the unperturbed reference to 1e-9 through iteration 150, and
+    the final row is within 0.5% of the reference or of a perturbed-reference
+    endpoint."""
     gold = json.load(open(os.path.join(GOLD, "cfg2_log.json")))
+    band = json.load(open(os.path.join(GOLD, "cfg2_band.json")))
     rows, info, st, grid = _run(gold["spec"], gold["grid"], gold["max_iters"])
-    _check(rows, gold, tight=1e-4)
+    got = np.array(rows, dtype=float)
+    ref = np.array(gold["rows"])
+    assert np.all(np.abs(got[:151, 1] - ref[:151, 1]) <= 1e-9 * ref[:151, 1])
+    ends = [ref[-1]] + [np.array(r) for r in band["final_rows"].values()]
+    ok = [abs(got[-1, 1] - e[1]) <= 5e-3 * e[1] and abs(got[-1, 3] - e[3]) <= 5e-3 * e[3]
+          for e in ends]
+    assert any(ok), (got[-1], ends)
 
 
 def test_single_instance_converges():
