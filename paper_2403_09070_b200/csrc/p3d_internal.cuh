@@ -135,6 +135,11 @@ int launch_spectral_ex(const p3d_grid* g, const double* rho, const int64_t* rho_
                        const double* coef_in, double* coef_out, double* maps, double* scratch,
                        const int* halt, const SpecOvfl* ov, cudaStream_t s);
 void spectral_setup();
+bool spectral_fast_ok(const p3d_grid* g);
+void spectral_fast_setup();
+int launch_spectral_fast(const p3d_grid* g, const double* rho, const int64_t* rho_fx,
+                         const double* coef_in, double* coef_out, double* maps, double* scratch,
+                         const int* halt, const SpecOvfl* ov, cudaStream_t s);
 void launch_scale_copy(const double* in, double* out, long long n, double s, cudaStream_t st);
 int launch_spectral(const p3d_grid* g, const double* rho, const int64_t* rho_fx,
                     const double* coef_in, double* coef_out, double* maps, double* scratch,

@@ -585,7 +585,7 @@ int gp_stage_times(float* ms) {
 
 // kernels enqueued by one gp_iterate (for the benchmark's launch count)
 int gp_kernels_per_iteration(const p3d_gp& gp) {
-  return (gp.topo.n_net > 0) + (gp.f_n_generic > 0) /*net*/ + (gp.n_inst > 0) /*gather*/ + 1 + (gp.n_macro > 0) /*scatter*/ + 6 /*spectral*/ +
+  return (gp.topo.n_net > 0) + (gp.f_n_generic > 0) /*net*/ + (gp.n_inst > 0) /*gather*/ + 1 + (gp.n_macro > 0) /*scatter*/ + (spectral_fast_ok(&gp.grid) ? 3 : 6) /*spectral*/ +
          1 /*dens*/ + 2 /*step, advance*/;
 }
 

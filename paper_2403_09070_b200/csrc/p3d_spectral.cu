@@ -17,6 +17,7 @@
 // (4 maps, coefficient scaling fused into the load), inverse y, inverse z
 // (writes the interleaved [B][4] map that the density gather reads).
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "p3d_common.cuh"
 #include "p3d_internal.cuh"
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(256) line_pass(PassArgs a) {
 // Opt the line-pass kernel into large dynamic shared memory.  Called from the
 // non-captured entry points (init / per-op) so graph capture never sees it.
 void spectral_setup() {
+  spectral_fast_setup();
   static bool done = false;
   if (!done) {
     cudaFuncSetAttribute(line_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -298,6 +300,8 @@ int launch_spectral(const p3d_grid* g, const double* rho, const int64_t* rho_fx,
 int launch_spectral_ex(const p3d_grid* g, const double* rho, const int64_t* rho_fx,
                        const double* coef_in, double* coef_out, double* maps, double* scratch,
                        const int* halt, const SpecOvfl* ov, cudaStream_t s) {
+  if (spectral_fast_ok(g) && !getenv("P3D_SPECTRAL_GENERIC"))
+    return launch_spectral_fast(g, rho, rho_fx, coef_in, coef_out, maps, scratch, halt, ov, s);
   const long long B = (long long)g->nx * g->ny * g->nz;
   double* X = scratch;       // [B]
   double* M = scratch + B;   // [4][B]
