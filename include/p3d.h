@@ -224,6 +224,9 @@ typedef struct p3d_gp {
   double* pos4;                /* [n_inst][4] AoS copy of v (x, y, z, 0) */
   double* inst_g;              /* [4][n_inst] gx, gy, gz_hbt, gz_bist */
   int64_t* rho_fx;             /* [B] */
+  /* spatial tile sort of the objects for the privatised scatter (K2) */
+  int32_t ts_n_tiles, ts_tiles_x, ts_tiles_y, ts_pad;
+  int32_t *ts_tile_of, *ts_hist, *ts_start, *ts_cursor, *ts_order;  /* [O], [T], [T+1], [T], [O] */
   double* rho;                 /* [B] */
   double* spec_scratch;        /* [6*B] */
   double* maps;                /* [B][4] */

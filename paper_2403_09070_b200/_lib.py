@@ -68,7 +68,10 @@ class Gp(C.Structure):
                 ("gamma1", D), ("min_step", D), ("step_scale", D), ("rho_t_fx", I64),
                 ("u", P), ("v", P), ("v_prev", P), ("best", P), ("wl_grad", P),
                 ("dens_grad", P), ("pre", P), ("prev_wl", P), ("prev_dens", P), ("prev_q", P),
-                ("pin_out", P), ("pin_out_f", P), ("pin_out_fd", P), ("pos4", P), ("inst_g", P), ("rho_fx", P), ("rho", P), ("spec_scratch", P),
+                ("pin_out", P), ("pin_out_f", P), ("pin_out_fd", P), ("pos4", P), ("inst_g", P), ("rho_fx", P),
+                ("ts_n_tiles", I32), ("ts_tiles_x", I32), ("ts_tiles_y", I32), ("ts_pad", I32),
+                ("ts_tile_of", P), ("ts_hist", P), ("ts_start", P), ("ts_cursor", P),
+                ("ts_order", P), ("rho", P), ("spec_scratch", P),
                 ("maps", P), ("partials", P), ("st", P), ("log", P), ("ovfl_hist", P)]
 
 

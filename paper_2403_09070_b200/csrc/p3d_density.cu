@@ -9,6 +9,8 @@
 // K4  density_energy / density_force (density.py:568-609): thread-per-object
 //     overlap-weighted means of the interleaved (phi, Ex, Ey, Ez) map, one CTA
 //     per macro.
+#include <limits.h>
+
 #include "p3d_geom.cuh"
 #include "p3d_internal.cuh"
 
@@ -39,6 +41,193 @@ void launch_scatter(const Cloud& cl, int n, int n_macro, const int32_t* macro_id
                     const p3d_grid& g, int64_t* rho, const int* halt, cudaStream_t s) {
   unsigned long long* r = reinterpret_cast<unsigned long long*>(rho);
   if (n > 0) scatter_cells_kernel<<<grid_blocks(n, 256, 148 * 16), 256, 0, s>>>(cl, n, g, r, halt);
+  if (n_macro > 0) scatter_macros_kernel<<<n_macro, 256, 0, s>>>(cl, macro_ids, g, r, halt);
+}
+
+// ---------------------------------------------------------------------------
+// Spatially ordered, shared-memory-privatised scatter (the fused loop's K2).
+// Every iteration the non-macro objects are counting-sorted by the planar
+// tile (kTile x kTile bins) of their current centre; a CTA then takes 1024
+// consecutive objects of that order, whose footprints cover a small bounding
+// box of bins: it accumulates their int64 terms in shared memory (contention
+// moves from L2 atomics to shared-memory atomics) and flushes the box once.
+// Boxes that do not fit fall back to global atomics.  Integer sums make the
+// map independent of the (atomic, unstable) order within a tile.
+// ---------------------------------------------------------------------------
+constexpr int kTile = 16;
+constexpr int kChunk = 1024;
+constexpr int kBoxBins = 6144;  // 48 KB of int64 bins per CTA
+
+template <class Cloud>
+__global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_grid g, TileSort ts,
+                                                       const int* halt) {
+  if (halt && *halt) return;
+  extern __shared__ int sh_hist[];
+  for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x) sh_hist[t] = 0;
+  __syncthreads();
+  const double tw = g.wb * kTile, th = g.hb * kTile;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (cl.is_macro(i)) {
+      ts.tile_of[i] = -1;
+      continue;
+    }
+    const Charge q = cl.get(i);
+    int tx = (int)floor(q.x / tw), ty = (int)floor(q.y / th);
+    tx = tx < 0 ? 0 : (tx >= ts.tiles_x ? ts.tiles_x - 1 : tx);
+    ty = ty < 0 ? 0 : (ty >= ts.tiles_y ? ts.tiles_y - 1 : ty);
+    const int t = tx * ts.tiles_y + ty;
+    ts.tile_of[i] = t;
+    atomicAdd(&sh_hist[t], 1);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x)
+    if (sh_hist[t]) atomicAdd(&ts.hist[t], sh_hist[t]);
+}
+
+// exclusive scan of the tile histogram (one CTA); re-zeroes the histogram
+__global__ void __launch_bounds__(1024) tile_scan_kernel(TileSort ts, const int* halt) {
+  if (halt && *halt) return;
+  __shared__ int carry;
+  __shared__ int wsum[32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < ts.n_tiles; base += blockDim.x) {
+    const int t = base + threadIdx.x;
+    const int v = t < ts.n_tiles ? ts.hist[t] : 0;
+    int x = v;  // inclusive warp scan
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const int excl = carry + (wid ? wsum[wid - 1] : 0) + x - v;
+    if (t < ts.n_tiles) {
+      ts.start[t] = excl;
+      ts.cursor[t] = excl;
+      ts.hist[t] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ts.start[ts.n_tiles] = carry;
+}
+
+__global__ void __launch_bounds__(256) tile_place_kernel(int n, TileSort ts, const int* halt) {
+  if (halt && *halt) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int t = ts.tile_of[i];
+    if (t >= 0) ts.order[atomicAdd(&ts.cursor[t], 1)] = i;
+  }
+}
+
+template <class Cloud>
+__global__ void __launch_bounds__(256) scatter_tiled_kernel(Cloud cl, p3d_grid g, TileSort ts,
+                                                           unsigned long long* rho,
+                                                           const int* halt) {
+  if (halt && *halt) return;
+  // int64 bins as two u32 halves: 32-bit shared atomics (native ATOMS.ADD) with
+  // the carry propagated by the thread that produced it (exact)
+  extern __shared__ unsigned int sbin32[];
+  __shared__ int box[4];
+  const int total = ts.start[ts.n_tiles];
+  const int c0 = blockIdx.x * kChunk;
+  if (c0 >= total) return;
+  const int c1 = min(total, c0 + kChunk);
+  int bx0 = INT_MAX, bx1 = -1, by0 = INT_MAX, by1 = -1;
+  for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
+    const Footprint f = footprint(cl.get(ts.order[k]), g);
+    bx0 = min(bx0, f.ax.i0); bx1 = max(bx1, f.ax.i1);
+    by0 = min(by0, f.ay.i0); by1 = max(by1, f.ay.i1);
+  }
+  if (threadIdx.x == 0) { box[0] = INT_MAX; box[1] = -1; box[2] = INT_MAX; box[3] = -1; }
+  __syncthreads();
+  atomicMin(&box[0], bx0); atomicMax(&box[1], bx1);
+  atomicMin(&box[2], by0); atomicMax(&box[3], by1);
+  __syncthreads();
+  const int X0 = box[0], Y0 = box[2];
+  const int W = box[1] - X0 + 1, H = box[3] - Y0 + 1, nz = g.nz;
+  const int nbins = W * H * nz;
+  const bool local = (long long)W * H * nz <= kBoxBins;
+  unsigned int* lo32 = sbin32;
+  unsigned int* hi32 = sbin32 + kBoxBins;
+  if (local) {
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) lo32[b] = hi32[b] = 0u;
+    __syncthreads();
+  }
+  for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
+    const Charge q = cl.get(ts.order[k]);
+    const Footprint f = footprint(q, g);
+    for (int ix = f.ax.i0; ix <= f.ax.i1; ++ix) {
+      const double wx = overlap_len(f.ax, ix, g.wb);
+      for (int iy = f.ay.i0; iy <= f.ay.i1; ++iy) {
+        const double wxy = wx * overlap_len(f.ay, iy, g.hb);
+        for (int iz = f.az.i0; iz <= f.az.i1; ++iz) {
+          const double vol = wxy * overlap_len(f.az, iz, g.db);
+          const long long t = __double2ll_rn((q.weight * vol) * g.fx_scale);
+          if (!t) continue;
+          if (local) {
+            const int b = ((ix - X0) * H + (iy - Y0)) * nz + iz;
+            const unsigned int tl = (unsigned int)t, th = (unsigned int)((unsigned long long)t >> 32);
+            const unsigned int old = atomicAdd(&lo32[b], tl);
+            const unsigned int hadd = th + (old + tl < old ? 1u : 0u);
+            if (hadd) atomicAdd(&hi32[b], hadd);
+          } else {
+            atomicAdd(rho + ((long long)(ix * g.ny + iy) * nz + iz), (unsigned long long)t);
+          }
+        }
+      }
+    }
+  }
+  if (!local) return;
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
+    const unsigned long long v = ((unsigned long long)hi32[b] << 32) | lo32[b];
+    if (!v) continue;
+    const int iz = b % nz, r = b / nz, iy = r % H, ix = r / H;
+    atomicAdd(rho + ((long long)((ix + X0) * g.ny + (iy + Y0)) * nz + iz), v);
+  }
+}
+
+void tiled_scatter_setup() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(scatter_tiled_kernel<CloudGP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kBoxBins * 8);
+  cudaFuncSetAttribute(tile_hist_kernel<CloudGP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       200 * 1024);
+  done = true;
+}
+
+int tiled_scatter_tiles(const p3d_grid& g, int* tx, int* ty) {
+  *tx = (g.nx + kTile - 1) / kTile;
+  *ty = (g.ny + kTile - 1) / kTile;
+  return *tx * *ty;
+}
+
+void launch_scatter_tiled(const CloudGP& cl, int n, int n_macro, const int32_t* macro_ids,
+                          const p3d_grid& g, const TileSort& ts, int64_t* rho, const int* halt,
+                          cudaStream_t s) {
+  unsigned long long* r = reinterpret_cast<unsigned long long*>(rho);
+  const int nb = grid_blocks(n, 256, 148 * 8);
+  tile_hist_kernel<CloudGP><<<nb, 256, ts.n_tiles * sizeof(int), s>>>(cl, n, g, ts, halt);
+  tile_scan_kernel<<<1, 1024, 0, s>>>(ts, halt);
+  tile_place_kernel<<<nb, 256, 0, s>>>(n, ts, halt);
+  const int chunks = (n + kChunk - 1) / kChunk;
+  scatter_tiled_kernel<CloudGP><<<chunks, 256, kBoxBins * 8, s>>>(cl, g, ts, r, halt);
   if (n_macro > 0) scatter_macros_kernel<<<n_macro, 256, 0, s>>>(cl, macro_ids, g, r, halt);
 }
 

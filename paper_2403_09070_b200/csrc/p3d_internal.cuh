@@ -112,6 +112,22 @@ void launch_fused_gather(const FusedGatherArgs& a, cudaStream_t s);
 
 int grid_blocks(int n, int threads, int cap);
 
+// spatially ordered scatter (p3d_density.cu)
+struct TileSort {
+  int n_tiles, tiles_x, tiles_y, pad;
+  int32_t* tile_of;  // [n_obj]
+  int32_t* hist;     // [n_tiles] (kept zeroed between iterations)
+  int32_t* start;    // [n_tiles + 1]
+  int32_t* cursor;   // [n_tiles]
+  int32_t* order;    // [n_obj]
+};
+struct CloudGP;
+void tiled_scatter_setup();
+int tiled_scatter_tiles(const p3d_grid& g, int* tx, int* ty);
+void launch_scatter_tiled(const CloudGP& cl, int n, int n_macro, const int32_t* macro_ids,
+                          const p3d_grid& g, const TileSort& ts, int64_t* rho, const int* halt,
+                          cudaStream_t s);
+
 // K1
 void launch_net_pos(const NetArgs& a, const double* x, const double* y, const double* z,
                     const double* off, double dz, cudaStream_t s);

@@ -517,7 +517,20 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
   cl.macro = gp.is_macro;
   cl.dz = gp.grid.dz;
   cl.target_density = gp.target_density;
-  launch_scatter(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, gp.rho_fx, halt, s);
+  if (gp.ts_order) {
+    TileSort ts;
+    ts.n_tiles = gp.ts_n_tiles;
+    ts.tiles_x = gp.ts_tiles_x;
+    ts.tiles_y = gp.ts_tiles_y;
+    ts.tile_of = gp.ts_tile_of;
+    ts.hist = gp.ts_hist;
+    ts.start = gp.ts_start;
+    ts.cursor = gp.ts_cursor;
+    ts.order = gp.ts_order;
+    launch_scatter_tiled(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, ts, gp.rho_fx, halt, s);
+  } else {
+    launch_scatter(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, gp.rho_fx, halt, s);
+  }
   mark(3);
   // K3 (+ overflow, re-zero)
   SpecOvfl ov;
@@ -585,12 +598,13 @@ int gp_stage_times(float* ms) {
 
 // kernels enqueued by one gp_iterate (for the benchmark's launch count)
 int gp_kernels_per_iteration(const p3d_gp& gp) {
-  return (gp.topo.n_net > 0) + (gp.f_n_generic > 0) /*net*/ + (gp.n_inst > 0) /*gather*/ + 1 + (gp.n_macro > 0) /*scatter*/ + (spectral_fast_ok(&gp.grid) ? 3 : 6) /*spectral*/ +
+  return (gp.topo.n_net > 0) + (gp.f_n_generic > 0) /*net*/ + (gp.n_inst > 0) /*gather*/ + 1 + (gp.ts_order ? 3 : 0) /*tile sort*/ + (gp.n_macro > 0) /*scatter*/ + (spectral_fast_ok(&gp.grid) ? 3 : 6) /*spectral*/ +
          1 /*dens*/ + 2 /*step, advance*/;
 }
 
 int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s) {
   spectral_setup();
+  tiled_scatter_setup();
   fused_net_setup();
   eval_setup_kernel<<<1, 1, 0, s>>>(gp, lam, gamma);
   if (gp.n_inst > 0)
@@ -601,6 +615,7 @@ int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s) {
 
 int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s) {
   spectral_setup();
+  tiled_scatter_setup();
   fused_net_setup();
   init_state_kernel<<<1, 1, 0, s>>>(gp);
   const int b = grid_blocks(gp.n_obj, 256, 4096);

@@ -32,12 +32,13 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 
 // Pre-process nl real lines (element k of line l at r[l*rs + k*es]) into
-// bit-reversed complex FFT input (Makhoul).
+// bit-reversed complex FFT input (Makhoul).  N = 2^logN: all index math is
+// shifts and masks.
 __device__ __forceinline__ void pre_lines(int op, const double* r, int rs, int es, int nl, int N,
                                           int logN, const double* ph, double2* c) {
   const int shift = 32 - logN;
-  for (int t = threadIdx.x; t < nl * N; t += blockDim.x) {
-    const int l = t / N, n = t - l * N;
+  for (int t = threadIdx.x; t < (nl << logN); t += blockDim.x) {
+    const int l = t >> logN, n = t & (N - 1);
     const double* line = r + l * rs;
     double2 v;
     int pos;
@@ -59,22 +60,24 @@ __device__ __forceinline__ void pre_lines(int op, const double* r, int rs, int e
       v = make_double2(cs * A + sn * B, sn * A - cs * B);
       pos = k;
     }
-    c[l * N + (__brev(pos) >> shift)] = v;
+    c[(l << logN) + (__brev(pos) >> shift)] = v;
   }
 }
 
-// in-place radix-2 DIT over nl lines (bit-reversed input, natural output)
-__device__ __forceinline__ void fft_lines(double2* c, int nl, int N, const double* tw, bool inv) {
-  const double sgn = inv ? -1.0 : 1.0;
-  const int half_n = N >> 1;
-  for (int len = 2; len <= N; len <<= 1) {
-    const int half = len >> 1, tstep = N / len;
-    for (int t = threadIdx.x; t < nl * half_n; t += blockDim.x) {
-      const int l = t / half_n, b = t - l * half_n;
-      const int grp = b / half, j = b - grp * half;
-      const int i0 = grp * len + j, i1 = i0 + half;
-      const double2 w = make_double2(tw[2 * j * tstep], sgn * tw[2 * j * tstep + 1]);
-      double2* buf = c + l * N;
+// in-place radix-2 DIT over nl lines (bit-reversed input, natural output);
+// twiddles staged in shared memory by the caller (tw: N/2 complex)
+__device__ __forceinline__ void fft_lines(double2* c, int nl, int N, int logN, const double2* tw,
+                                          bool inv) {
+  const int lhalf = logN - 1;
+  for (int s = 0; s < logN; ++s) {
+    const int half = 1 << s;
+    for (int t = threadIdx.x; t < (nl << lhalf); t += blockDim.x) {
+      const int l = t >> lhalf, b = t & ((1 << lhalf) - 1);
+      const int j = b & (half - 1);
+      const int i0 = ((b >> s) << (s + 1)) + j, i1 = i0 + half;
+      double2 w = tw[j << (lhalf - s)];
+      if (inv) w.y = -w.y;
+      double2* buf = c + (l << logN);
       const double2 x0 = buf[i0], x1 = cmul(w, buf[i1]);
       buf[i0] = make_double2(x0.x + x1.x, x0.y + x1.y);
       buf[i1] = make_double2(x0.x - x1.x, x0.y - x1.y);
@@ -84,11 +87,11 @@ __device__ __forceinline__ void fft_lines(double2* c, int nl, int N, const doubl
 }
 
 // Post-process FFT output into real lines (element m at r[l*rs + m*es]).
-__device__ __forceinline__ void post_lines(int op, const double2* c, int nl, int N,
+__device__ __forceinline__ void post_lines(int op, const double2* c, int nl, int N, int logN,
                                            const double* ph, double* r, int rs, int es) {
-  for (int t = threadIdx.x; t < nl * N; t += blockDim.x) {
-    const int l = t / N, m = t - l * N;
-    const double2* buf = c + l * N;
+  for (int t = threadIdx.x; t < (nl << logN); t += blockDim.x) {
+    const int l = t >> logN, m = t & (N - 1);
+    const double2* buf = c + (l << logN);
     double y;
     if (op == T_DCT2) {
       y = ph[2 * m] * buf[m].x + ph[2 * m + 1] * buf[m].y;
@@ -101,8 +104,28 @@ __device__ __forceinline__ void post_lines(int op, const double2* c, int nl, int
   }
 }
 
-// direct transform along z of every row of a slab [ny][nz] held in smem
+__device__ __forceinline__ void stage_twiddles(const double* tw, int N, double2* smem_tw) {
+  for (int j = threadIdx.x; j < (N >> 1); j += blockDim.x)
+    smem_tw[j] = make_double2(tw[2 * j], tw[2 * j + 1]);
+}
+
+// direct transform along z of every row of a slab [ny][nz] held in smem;
+// nz == 2 (every BASELINE config) is a closed-form butterfly
 __device__ __forceinline__ void z_direct(int op, double* slab, int ny, int nz, double* tmp) {
+  if (nz == 2) {
+    const double r2 = 0.70710678118654752440;  // cos(pi/4) = sin(pi/4)
+    for (int iy = threadIdx.x; iy < ny; iy += blockDim.x) {
+      const double x0 = slab[2 * iy], x1 = slab[2 * iy + 1];
+      double y0, y1;
+      if (op == T_DCT2) { y0 = x0 + x1; y1 = (x0 - x1) * r2; }
+      else if (op == T_COS) { y0 = x0 + x1 * r2; y1 = x0 - x1 * r2; }
+      else { y0 = x1 * r2; y1 = x1 * r2; }
+      slab[2 * iy] = y0;
+      slab[2 * iy + 1] = y1;
+    }
+    __syncthreads();
+    return;
+  }
   const int mod = 4 * nz;
   for (int t = threadIdx.x; t < ny * nz; t += blockDim.x) {
     const int iy = t / nz, m = t - iy * nz;
@@ -153,6 +176,8 @@ __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
   double* slab = sm;                                   // [S]
   double* tmp = sm + S;                                // [S]
   double2* cb = reinterpret_cast<double2*>(sm + 2 * S);  // [S] complex
+  double2* tw = reinterpret_cast<double2*>(sm + 4 * S);  // [ny/2]
+  stage_twiddles(a.twy, ny, tw);
   const long long base = (long long)blockIdx.x * S;
   long long excess = 0;
   for (int t = threadIdx.x; t < S; t += blockDim.x) {
@@ -173,8 +198,8 @@ __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
   // y lines: line iz, element iy at slab[iy*nz + iz]
   pre_lines(T_DCT2, slab, 1, nz, nz, ny, a.logy, a.phy, cb);
   __syncthreads();
-  fft_lines(cb, nz, ny, a.twy, false);
-  post_lines(T_DCT2, cb, nz, ny, a.phy, slab, 1, nz);
+  fft_lines(cb, nz, ny, a.logy, tw, false);
+  post_lines(T_DCT2, cb, nz, ny, a.logy, a.phy, slab, 1, nz);
   __syncthreads();
   for (int t = threadIdx.x; t < S; t += blockDim.x) a.X[base + t] = slab[t];
   if (a.ovfl_out) {
@@ -219,6 +244,8 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
   double* X = sm;                                           // [C][nx]
   double* R = sm + C * nx;                                  // [C][nx]
   double2* cb = reinterpret_cast<double2*>(sm + 2 * C * nx);  // [C][nx]
+  double2* tw = reinterpret_cast<double2*>(sm + 4 * C * nx);  // [nx/2]
+  stage_twiddles(a.twx, nx, tw);
   const double* src = a.coef_in ? a.coef_in : a.X;
   for (int t = threadIdx.x; t < C * nx; t += blockDim.x) {
     const int ix = t / C, c = t - ix * C;  // consecutive threads: consecutive columns
@@ -228,8 +255,8 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
   if (!a.coef_in) {
     pre_lines(T_DCT2, X, nx, 1, C, nx, a.logx, a.phx, cb);
     __syncthreads();
-    fft_lines(cb, C, nx, a.twx, false);
-    post_lines(T_DCT2, cb, C, nx, a.phx, X, nx, 1);
+    fft_lines(cb, C, nx, a.logx, tw, false);
+    post_lines(T_DCT2, cb, C, nx, a.logx, a.phx, X, nx, 1);
     __syncthreads();
     if (a.coef_out)
       for (int t = threadIdx.x; t < C * nx; t += blockDim.x) {
@@ -240,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
   if (!a.maps) return;
   for (int map = 0; map < 4; ++map) {
     for (int t = threadIdx.x; t < C * nx; t += blockDim.x) {
-      const int c = t / nx, ix = t - c * nx;
+      const int c = t >> a.logx, ix = t & (nx - 1);
       const int col = c0 + c, k = col / a.nz, l = col - k * a.nz;
       R[t] = X[t] * coef_factor(a, ix, k, l, map);
     }
@@ -248,8 +275,8 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
     const int op = map == 1 ? T_SIN : T_COS;
     pre_lines(op, R, nx, 1, C, nx, a.logx, a.phx, cb);
     __syncthreads();
-    fft_lines(cb, C, nx, a.twx, true);
-    post_lines(op, cb, C, nx, a.phx, R, nx, 1);
+    fft_lines(cb, C, nx, a.logx, tw, true);
+    post_lines(op, cb, C, nx, a.logx, a.phx, R, nx, 1);
     __syncthreads();
     double* out = a.M + (long long)map * nx * S;
     for (int t = threadIdx.x; t < C * nx; t += blockDim.x) {
@@ -268,6 +295,8 @@ __global__ void __launch_bounds__(kThreads) spec_inv_yz(FastArgs a) {
   double* slab = sm;
   double* tmp = sm + S;
   double2* cb = reinterpret_cast<double2*>(sm + 2 * S);
+  double2* tw = reinterpret_cast<double2*>(sm + 4 * S);
+  stage_twiddles(a.twy, ny, tw);
   const long long base = (long long)blockIdx.x * S;
   const long long B = (long long)a.nx * S;
   for (int map = 0; map < 4; ++map) {
@@ -277,8 +306,8 @@ __global__ void __launch_bounds__(kThreads) spec_inv_yz(FastArgs a) {
     const int opy = map == 2 ? T_SIN : T_COS, opz = map == 3 ? T_SIN : T_COS;
     pre_lines(opy, slab, 1, nz, nz, ny, a.logy, a.phy, cb);
     __syncthreads();
-    fft_lines(cb, nz, ny, a.twy, true);
-    post_lines(opy, cb, nz, ny, a.phy, slab, 1, nz);
+    fft_lines(cb, nz, ny, a.logy, tw, true);
+    post_lines(opy, cb, nz, ny, a.logy, a.phy, slab, 1, nz);
     __syncthreads();
     z_direct(opz, slab, ny, nz, tmp);
     for (int t = threadIdx.x; t < S; t += blockDim.x) a.maps[(base + t) * 4 + map] = slab[t];
@@ -297,8 +326,8 @@ int ilog2_pow2(int n) {
 bool spectral_fast_ok(const p3d_grid* g) {
   const int lx = ilog2_pow2(g->nx), ly = ilog2_pow2(g->ny);
   return lx >= 3 && ly >= 3 && g->nz >= 1 && g->nz <= kMaxNz &&
-         (size_t)g->ny * g->nz * 4 * sizeof(double) <= 200 * 1024 &&
-         (size_t)kColTile * g->nx * 4 * sizeof(double) <= 200 * 1024 &&
+         ((size_t)g->ny * g->nz * 4 + g->ny) * sizeof(double) <= 200 * 1024 &&
+         ((size_t)kColTile * g->nx * 4 + g->nx) * sizeof(double) <= 200 * 1024 &&
          (g->ny * g->nz) % kColTile == 0;
 }
 
@@ -340,9 +369,9 @@ int launch_spectral_fast(const p3d_grid* g, const double* rho, const int64_t* rh
     a.ovfl_out = ov->out;
     a.ovfl_scale = ov->scale;
   }
-  const size_t smA = (size_t)S * 4 * sizeof(double);
+  const size_t smA = ((size_t)S * 4 + g->ny) * sizeof(double);
   if (!coef_in) spec_fwd_yz<<<g->nx, kThreads, smA, s>>>(a);
-  const size_t smB = (size_t)kColTile * g->nx * 4 * sizeof(double);
+  const size_t smB = ((size_t)kColTile * g->nx * 4 + g->nx) * sizeof(double);
   spec_x<<<(int)(S / kColTile), kThreads, smB, s>>>(a);
   if (maps) spec_inv_yz<<<g->nx, kThreads, smA, s>>>(a);
   return check_launch("spectral (fast path)");

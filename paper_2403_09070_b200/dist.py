@@ -1,0 +1,53 @@
+"""Multi-GPU plumbing for the GP loop (one process per GPU, torch.distributed).
+
+Round 1 runs independent replicas per rank (config-5 style); the sharded
+config-4 path partitions objects and nets into contiguous slabs and combines
+the density map with an all-reduce.  Because rho is int64 fixed point
+(2^-40 per unit density) the all-reduced map is bit-identical to the
+single-GPU map for any number of ranks and any reduction order — the property
+``tests/test_dist.py`` checks with the gloo backend on CPU.
+"""
+
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+
+def rank_world():
+    """(rank, world, local_rank) from the torchrun environment."""
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def shard_range(n, rank, world):
+    """Contiguous slab [lo, hi) of n units owned by `rank` (sizes differ by <= 1)."""
+    q, r = divmod(int(n), int(world))
+    lo = rank * q + min(rank, r)
+    return lo, lo + q + (1 if rank < r else 0)
+
+
+def replica_seed(base_seed, rank):
+    """Seed of the independent placement a rank runs in replica mode."""
+    return int(base_seed) + int(rank)
+
+
+def allreduce_rho_fx(rho_fx: torch.Tensor) -> torch.Tensor:
+    """Sum the per-rank int64 fixed-point density maps in place (exact)."""
+    if rho_fx.dtype != torch.int64:
+        raise TypeError("the density map must be int64 fixed point")
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(rho_fx, op=dist.ReduceOp.SUM)
+    return rho_fx
+
+
+def max_over_ranks(values):
+    """Element-wise max of a list of floats over all ranks (timings)."""
+    t = torch.tensor(list(values), dtype=torch.float64,
+                     device="cuda" if dist.is_initialized() and
+                     dist.get_backend() == "nccl" else "cpu")
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.cpu()]

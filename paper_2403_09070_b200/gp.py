@@ -429,6 +429,13 @@ class Gp3dProblem:
         self.t_inst_g = z(4 * I)
         self.t_rho_fx = torch.zeros(B, dtype=torch.int64, device="cuda")
         self.t_rho = z(B)
+        tx, ty = -(-grid.nx // 16), -(-grid.ny // 16)  # kTile in p3d_density.cu
+        nt = tx * ty
+        i32z = lambda n: torch.zeros(max(int(n), 1), dtype=torch.int32, device="cuda")  # noqa: E731
+        self.t_ts = [i32z(O), i32z(nt), i32z(nt + 1), i32z(nt), i32z(O)]
+        g.ts_n_tiles, g.ts_tiles_x, g.ts_tiles_y = nt, tx, ty
+        for name, t in zip(("ts_tile_of", "ts_hist", "ts_start", "ts_cursor", "ts_order"), self.t_ts):
+            setattr(g, name, keep(t))
         self.t_spec = z(6 * B)
         self.t_maps = z(4 * B)
         self.t_partials = z(16 * K_PARTIAL_STRIDE)

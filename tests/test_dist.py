@@ -1,0 +1,73 @@
+"""Host-side multi-process logic with the gloo backend (world_size 2, CPU).
+
+* slab partitioning covers every unit exactly once;
+* per-rank fixed-point density maps of disjoint object slabs, all-reduced,
+  equal the single-process map bit for bit (the property that makes the
+  config-4 sharded path exact for any GPU count);
+* the max-over-ranks timing reduction used by bench.py.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2403_09070_b200.dist import (allreduce_rho_fx, max_over_ranks, replica_seed,
+                                        shard_range)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import fixed as FX
+        from oracle import port as P
+
+        rng = np.random.default_rng(3)
+        grid = P.Grid(40.0, 30.0, 16, 12, 2)
+        n = 500
+        w = rng.uniform(0.5, 4, n)
+        h = rng.uniform(0.5, 4, n)
+        cl = P.Cloud(rng.uniform(0, 40, n), rng.uniform(0, 30, n),
+                     rng.uniform(grid.dz / 4, 3 * grid.dz / 4, n), w, h,
+                     np.full(n, grid.dz / 2), np.ones(n), rng.random(n) < 0.05)
+        lo, hi = shard_range(n, rank, world)
+        part = torch.from_numpy(FX.fixed_rho(grid, cl.take(np.arange(lo, hi))).reshape(-1).copy())
+        allreduce_rho_fx(part)
+        full = FX.fixed_rho(grid, cl).reshape(-1)
+        ok = bool(np.array_equal(part.numpy(), full))
+        mx = max_over_ranks([1.0 + rank, 5.0 - rank])
+        out[rank] = (ok, mx)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_range_covers():
+    for n in (0, 1, 7, 100, 101):
+        for world in (1, 2, 3, 8):
+            got = [shard_range(n, r, world) for r in range(world)]
+            assert got[0][0] == 0 and got[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
+            assert max(h - l for l, h in got) - min(h - l for l, h in got) <= 1
+    assert replica_seed(1, 3) == 4
+
+
+def test_gloo_world2_fixed_point_allreduce_exact():
+    world = 2
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    assert all(res[r][0] for r in range(world))
+    assert all(res[r][1] == [2.0, 5.0] for r in range(world))
