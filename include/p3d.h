@@ -227,6 +227,7 @@ typedef struct p3d_gp {
   /* spatial tile sort of the objects for the privatised scatter (K2) */
   int32_t ts_n_tiles, ts_tiles_x, ts_tiles_y, ts_pad;
   int32_t *ts_tile_of, *ts_hist, *ts_start, *ts_cursor, *ts_order;  /* [O], [T], [T+1], [T], [O] */
+  double* ts_rec;              /* [O][6] charge records (x, y, z, w, h, weight) in tile order */
   double* rho;                 /* [B] */
   double* spec_scratch;        /* [6*B] */
   double* maps;                /* [B][4] */

@@ -71,7 +71,7 @@ class Gp(C.Structure):
                 ("pin_out", P), ("pin_out_f", P), ("pin_out_fd", P), ("pos4", P), ("inst_g", P), ("rho_fx", P),
                 ("ts_n_tiles", I32), ("ts_tiles_x", I32), ("ts_tiles_y", I32), ("ts_pad", I32),
                 ("ts_tile_of", P), ("ts_hist", P), ("ts_start", P), ("ts_cursor", P),
-                ("ts_order", P), ("rho", P), ("spec_scratch", P),
+                ("ts_order", P), ("ts_rec", P), ("rho", P), ("spec_scratch", P),
                 ("maps", P), ("partials", P), ("st", P), ("log", P), ("ovfl_hist", P)]
 
 

@@ -126,16 +126,55 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(TileSort ts, const int*
   if (threadIdx.x == 0) ts.start[ts.n_tiles] = carry;
 }
 
-__global__ void __launch_bounds__(256) tile_place_kernel(int n, TileSort ts, const int* halt) {
+// Stable-per-block placement: each CTA ranks its objects per tile in shared
+// memory, reserves one range per (CTA, tile) with a single global atomic, and
+// writes each object's charge record (x, y, z, w, h, weight) at its slot, so
+// the scatter reads its chunk contiguously.
+constexpr int kPlacePerThread = 8;
+
+template <class Cloud>
+__global__ void __launch_bounds__(256) tile_place_kernel(Cloud cl, int n, TileSort ts,
+                                                        const int* halt) {
   if (halt && *halt) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int t = ts.tile_of[i];
-    if (t >= 0) ts.order[atomicAdd(&ts.cursor[t], 1)] = i;
+  extern __shared__ int sh[];
+  int* cnt = sh;                  // [n_tiles]
+  int* base = sh + ts.n_tiles;    // [n_tiles]
+  for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x) cnt[t] = 0;
+  __syncthreads();
+  const int i0 = blockIdx.x * blockDim.x * kPlacePerThread + threadIdx.x;
+  int tile[kPlacePerThread], rank[kPlacePerThread];
+#pragma unroll
+  for (int k = 0; k < kPlacePerThread; ++k) {
+    const int i = i0 + k * blockDim.x;
+    tile[k] = i < n ? ts.tile_of[i] : -1;
+    rank[k] = tile[k] >= 0 ? atomicAdd(&cnt[tile[k]], 1) : 0;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x)
+    base[t] = cnt[t] ? atomicAdd(&ts.cursor[t], cnt[t]) : 0;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kPlacePerThread; ++k) {
+    if (tile[k] < 0) continue;
+    const int i = i0 + k * blockDim.x;
+    const int pos = base[tile[k]] + rank[k];
+    const Charge q = cl.get(i);
+    double2* r = reinterpret_cast<double2*>(ts.rec) + 3 * (long long)pos;
+    r[0] = make_double2(q.x, q.y);
+    r[1] = make_double2(q.z, q.w);
+    r[2] = make_double2(q.h, q.weight);
   }
 }
 
-template <class Cloud>
-__global__ void __launch_bounds__(256) scatter_tiled_kernel(Cloud cl, p3d_grid g, TileSort ts,
+__device__ __forceinline__ Charge rec_charge(const TileSort& ts, int pos, double dep) {
+  const double2* r = reinterpret_cast<const double2*>(ts.rec) + 3 * (long long)pos;
+  const double2 a = r[0], b = r[1], c = r[2];
+  Charge q;
+  q.x = a.x; q.y = a.y; q.z = b.x; q.w = b.y; q.h = c.x; q.weight = c.y; q.dep = dep;
+  return q;
+}
+
+__global__ void __launch_bounds__(256) scatter_tiled_kernel(p3d_grid g, TileSort ts,
                                                            unsigned long long* rho,
                                                            const int* halt) {
   if (halt && *halt) return;
@@ -147,9 +186,10 @@ __global__ void __launch_bounds__(256) scatter_tiled_kernel(Cloud cl, p3d_grid g
   const int c0 = blockIdx.x * kChunk;
   if (c0 >= total) return;
   const int c1 = min(total, c0 + kChunk);
+  const double dep = g.dz / 2;
   int bx0 = INT_MAX, bx1 = -1, by0 = INT_MAX, by1 = -1;
   for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
-    const Footprint f = footprint(cl.get(ts.order[k]), g);
+    const Footprint f = footprint(rec_charge(ts, k, dep), g);
     bx0 = min(bx0, f.ax.i0); bx1 = max(bx1, f.ax.i1);
     by0 = min(by0, f.ay.i0); by1 = max(by1, f.ay.i1);
   }
@@ -169,7 +209,7 @@ __global__ void __launch_bounds__(256) scatter_tiled_kernel(Cloud cl, p3d_grid g
     __syncthreads();
   }
   for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
-    const Charge q = cl.get(ts.order[k]);
+    const Charge q = rec_charge(ts, k, dep);
     const Footprint f = footprint(q, g);
     for (int ix = f.ax.i0; ix <= f.ax.i1; ++ix) {
       const double wx = overlap_len(f.ax, ix, g.wb);
@@ -205,8 +245,10 @@ __global__ void __launch_bounds__(256) scatter_tiled_kernel(Cloud cl, p3d_grid g
 void tiled_scatter_setup() {
   static bool done = false;
   if (done) return;
-  cudaFuncSetAttribute(scatter_tiled_kernel<CloudGP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(scatter_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kBoxBins * 8);
+  cudaFuncSetAttribute(tile_place_kernel<CloudGP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       200 * 1024);
   cudaFuncSetAttribute(tile_hist_kernel<CloudGP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        200 * 1024);
   done = true;
@@ -225,9 +267,10 @@ void launch_scatter_tiled(const CloudGP& cl, int n, int n_macro, const int32_t* 
   const int nb = grid_blocks(n, 256, 148 * 8);
   tile_hist_kernel<CloudGP><<<nb, 256, ts.n_tiles * sizeof(int), s>>>(cl, n, g, ts, halt);
   tile_scan_kernel<<<1, 1024, 0, s>>>(ts, halt);
-  tile_place_kernel<<<nb, 256, 0, s>>>(n, ts, halt);
+  const int np = (n + 256 * kPlacePerThread - 1) / (256 * kPlacePerThread);
+  tile_place_kernel<CloudGP><<<np, 256, 2 * ts.n_tiles * sizeof(int), s>>>(cl, n, ts, halt);
   const int chunks = (n + kChunk - 1) / kChunk;
-  scatter_tiled_kernel<CloudGP><<<chunks, 256, kBoxBins * 8, s>>>(cl, g, ts, r, halt);
+  scatter_tiled_kernel<<<chunks, 256, kBoxBins * 8, s>>>(g, ts, r, halt);
   if (n_macro > 0) scatter_macros_kernel<<<n_macro, 256, 0, s>>>(cl, macro_ids, g, r, halt);
 }
 

@@ -119,7 +119,8 @@ struct TileSort {
   int32_t* hist;     // [n_tiles] (kept zeroed between iterations)
   int32_t* start;    // [n_tiles + 1]
   int32_t* cursor;   // [n_tiles]
-  int32_t* order;    // [n_obj]
+  int32_t* order;    // [n_obj] (unused by the record path; kept for debugging)
+  double* rec;       // [n_obj][6] charge records in tile order
 };
 struct CloudGP;
 void tiled_scatter_setup();

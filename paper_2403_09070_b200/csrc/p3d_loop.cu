@@ -209,7 +209,7 @@ __device__ __forceinline__ void finish_object(const p3d_gp& gp, int i, const Cha
 }
 
 // underflow test and momentum of the accepted step (gp.py:218-226)
-__device__ __noinline__ void step_tail(const p3d_gp& gp) {
+__device__ __forceinline__ void step_tail(const p3d_gp& gp) {
   p3d_loop_state* st = gp.st;
   if (!isfinite(st->step) || st->step <= gp.min_step) {  // StepUnderflow, gp.py:438-441
     st->diverged = 1;
@@ -221,7 +221,7 @@ __device__ __noinline__ void step_tail(const p3d_gp& gp) {
   st->mom = (a - 1) / st->a_new;
 }
 
-__device__ __noinline__ void control_after_eval(const p3d_gp& gp, double energy, double l1_dens,
+__device__ __forceinline__ void control_after_eval(const p3d_gp& gp, double energy, double l1_dens,
                                    double l1_wl, double nonfinite, double dv2, double dg2) {
   p3d_loop_state* st = gp.st;
   const double* f = fin(gp);
@@ -307,7 +307,7 @@ __device__ __noinline__ void control_after_eval(const p3d_gp& gp, double energy,
   step_tail(gp);
 }
 
-__global__ void __launch_bounds__(256) dens_kernel(p3d_gp gp) {
+__global__ void __launch_bounds__(256, 3) dens_kernel(p3d_gp gp) {
   if (gp.st->done) return;
   __shared__ double red[32 * 6];
   const CloudGP cl = cloud_of(gp, gp.v);
@@ -527,6 +527,7 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
     ts.start = gp.ts_start;
     ts.cursor = gp.ts_cursor;
     ts.order = gp.ts_order;
+    ts.rec = gp.ts_rec;
     launch_scatter_tiled(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, ts, gp.rho_fx, halt, s);
   } else {
     launch_scatter(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, gp.rho_fx, halt, s);

@@ -70,31 +70,43 @@ struct Box2 {  // one axis, die 0 (bottom) and die 1 (top)
 };
 
 // ---- weighted-average segment sums -------------------------------------------
-// exp(x) for x <= 0 (every WA argument is (v - max)/gamma or (min - v)/gamma):
-// Cody-Waite reduction by ln2, degree-13 Taylor, exponent scaling; <= 1 ulp
-// against numpy's exp over [-708, 0]; values below 2^-1022 flush to 0 (each
-// segment sum contains its anchor pin's exp(0) = 1, so this is invisible).
+// exp(x) for x <= 0 (every WA argument is (v - max)/gamma or (min - v)/gamma).
+// x = (64 m + k) ln2/64 + r with |r| <= ln2/128: exp(x) = 2^m T[k] (1 + q(r)),
+// T[k] = 2^(k/64) (64-entry table), q a degree-6 Taylor polynomial evaluated
+// with short dependency chains (Estrin) — this kernel is latency-bound at the
+// occupancy its shared-memory columns allow.  <= 2 ulp against numpy's exp
+// over [-708, 0]; results below 2^-1022 flush to 0 (each segment sum holds its
+// anchor pin's exp(0) = 1, so this is invisible).
+__device__ const double kExp2Tab[64] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
+    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
+    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
+    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
+    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
+    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
+    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
+    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+
 __device__ __forceinline__ double exp_neg(double x) {
-  const double n = rint(x * 1.4426950408889634074);
-  double r = fma(-n, 6.93147180369123816490e-01, x);
-  r = fma(-n, 1.90821492927058770002e-10, r);
-  double p = 1.6059043836821613e-10;
-  p = fma(p, r, 2.08767569878681e-09);
-  p = fma(p, r, 2.505210838544172e-08);
-  p = fma(p, r, 2.755731922398589e-07);
-  p = fma(p, r, 2.7557319223985893e-06);
-  p = fma(p, r, 2.48015873015873e-05);
-  p = fma(p, r, 1.984126984126984e-04);
-  p = fma(p, r, 1.3888888888888889e-03);
-  p = fma(p, r, 8.333333333333333e-03);
-  p = fma(p, r, 4.1666666666666664e-02);
-  p = fma(p, r, 1.6666666666666666e-01);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+  const double n = rint(x * 92.332482616893656877);  // 64 / ln 2
+  const double r = fma(-n, 2.572804622327669e-14, fma(-n, 0.010830424696223417, x));
   const int ni = (int)n;
-  const double sc = __longlong_as_double((long long)(ni + 1023) << 52);
-  return x < -708.0 ? 0.0 : p * sc;
+  const double r2 = r * r;
+  const double a = fma(r, 1.6666666666666666e-01, 0.5);            // 1/2 + r/6
+  const double b = fma(r, 8.333333333333333e-03, 4.1666666666666664e-02);  // 1/24 + r/120
+  const double c = fma(r2, 1.3888888888888889e-03, b);             // + r^2/720
+  const double q = fma(r2, fma(r2, c, a), r);                      // r + r^2 a + r^4 c
+  const double t = __ldg(&kExp2Tab[ni & 63]);
+  const double sc = __longlong_as_double((long long)((ni >> 6) + 1023) << 52);
+  return x < -708.0 ? 0.0 : fma(t, q, t) * sc;
 }
 
 // float64 WA sums with numpy's structure (wirelength.py:85-96): value
@@ -317,10 +329,17 @@ constexpr int kWarpsPerBlock = 4;
 template <bool F32>
 struct WarpCols {
   using R = typename WaSel<F32>::R;
-  double px[kMaxStagedDeg][32], py[kMaxStagedDeg][32], pz[kMaxStagedDeg][32];
-  double dw[kMaxStagedDeg][32];
-  R ep[kMaxStagedDeg][32], em[kMaxStagedDeg][32], gx[kMaxStagedDeg][32], gy[kMaxStagedDeg][32];
+  double px[kMaxStagedDeg][32], py[kMaxStagedDeg][32];
+  double pz[kMaxStagedDeg][32];  // z for the cut phase, then reused as the FD accumulator
+  R ep[kMaxStagedDeg][32], em[kMaxStagedDeg][32];
 };
+
+// one component of a pin's output record (written piecewise by the phases;
+// the L2 merges the partial sectors of a record before write-back)
+__device__ __forceinline__ void store_comp(const FusedNetArgs& a, int idx, int comp, double v) {
+  if (a.out_d) a.out_d[4 * (long long)idx + comp] = v;
+  else reinterpret_cast<float*>(a.out_f)[4 * (long long)idx + comp] = (float)v;
+}
 
 // One planar axis of a staged net: boxes, branch, WA sums of the chosen
 // branch, per-pin gradients, FD extent deltas (accumulated into dw).
@@ -328,8 +347,8 @@ template <bool F32>
 __device__ __forceinline__ void staged_axis(int D, const double (&c)[kMaxStagedDeg][32],
                                             WarpCols<F32>& sm, int lane, int topm,
                                             typename WaSel<F32>::R ig, double& val,
-                                            double& exact, bool& crossing,
-                                            typename WaSel<F32>::R (&g)[kMaxStagedDeg][32]) {
+                                            double& exact, bool& crossing, const FusedNetArgs& a,
+                                            int pin0, int nb, int comp) {
   using W = typename WaSel<F32>::W;
   using R = typename WaSel<F32>::R;
   Box2 bx;
@@ -364,8 +383,9 @@ __device__ __forceinline__ void staged_axis(int D, const double (&c)[kMaxStagedD
     const int tp = (topm >> k) & 1;
     const double v = c[k][lane];
     const SegSel sg = seg_of(bx, split, tp);
-    g[k][lane] = (sg.upper ? w1 : w0).grad(v, sg.hi, sg.lo, ig, sm.ep[k][lane], sm.em[k][lane]);
-    sm.dw[k][lane] += bx.flip(v, tp, full, ex);
+    store_comp(a, pin0 + k * nb, comp,
+               (double)(sg.upper ? w1 : w0).grad(v, sg.hi, sg.lo, ig, sm.ep[k][lane], sm.em[k][lane]));
+    sm.pz[k][lane] += bx.flip(v, tp, full, ex);  // pz holds the FD accumulator by now
   }
 }
 
@@ -396,7 +416,6 @@ __device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk,
     sm.px[k][lane] = p.x + (double)(tp ? off[k].x : off[k].z);
     sm.py[k][lane] = p.y + (double)(tp ? off[k].y : off[k].w);
     sm.pz[k][lane] = p.z;
-    sm.dw[k][lane] = 0.0;
     zhi = fmax(zhi, p.z);
     zlo = fmin(zlo, p.z);
   }
@@ -410,15 +429,7 @@ __device__ __forceinline__ void staged_eval(const FusedNetArgs& a, int D, int pi
   using W = typename WaSel<F32>::W;
   using R = typename WaSel<F32>::R;
   const R ig = (R)a.inv_gamma;
-  double v, ex;
-  bool cross;
-  staged_axis<F32>(D, sm.px, sm, lane, topm, ig, v, ex, cross, sm.gx);
-  acc[0] += v;
-  acc[3] += ex;
-  acc[5] += cross ? 1.0 : 0.0;
-  staged_axis<F32>(D, sm.py, sm, lane, topm, ig, v, ex, cross, sm.gy);
-  acc[1] += v;
-  acc[4] += ex;
+  // z-cut phase first: its column is then recycled as the FD accumulator
   W wz;
   wz.init();
 #pragma unroll 1
@@ -433,10 +444,23 @@ __device__ __forceinline__ void staged_eval(const FusedNetArgs& a, int D, int pi
   acc[2] += wz.value(zhi, zlo);
 #pragma unroll 1
   for (int k = 0; k < D; ++k) {
-    const double gc = (double)wz.grad(sm.pz[k][lane], zhi, zlo, ig, sm.ep[k][lane], sm.em[k][lane]);
-    const double dwk = sm.dw[k][lane];
-    const double gb = (((topm >> k) & 1) ? -dwk : dwk) * a.scale4;
-    store_pin(a, pin0 + k * nb, (double)sm.gx[k][lane], (double)sm.gy[k][lane], gc, gb);
+    store_comp(a, pin0 + k * nb, 2,
+               (double)wz.grad(sm.pz[k][lane], zhi, zlo, ig, sm.ep[k][lane], sm.em[k][lane]));
+    sm.pz[k][lane] = 0.0;
+  }
+  double v, ex;
+  bool cross;
+  staged_axis<F32>(D, sm.px, sm, lane, topm, ig, v, ex, cross, a, pin0, nb, 0);
+  acc[0] += v;
+  acc[3] += ex;
+  acc[5] += cross ? 1.0 : 0.0;
+  staged_axis<F32>(D, sm.py, sm, lane, topm, ig, v, ex, cross, a, pin0, nb, 1);
+  acc[1] += v;
+  acc[4] += ex;
+#pragma unroll 1
+  for (int k = 0; k < D; ++k) {
+    const double dwk = sm.pz[k][lane];
+    store_comp(a, pin0 + k * nb, 3, (((topm >> k) & 1) ? -dwk : dwk) * a.scale4);
   }
 }
 
@@ -450,7 +474,7 @@ __device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk
 }
 
 template <bool F32>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) fused_net_kernel(FusedNetArgs a) {
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) fused_net_kernel(FusedNetArgs a) {
   if (a.halt && *a.halt) return;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ double red[32 * 6];

@@ -436,6 +436,8 @@ class Gp3dProblem:
         g.ts_n_tiles, g.ts_tiles_x, g.ts_tiles_y = nt, tx, ty
         for name, t in zip(("ts_tile_of", "ts_hist", "ts_start", "ts_cursor", "ts_order"), self.t_ts):
             setattr(g, name, keep(t))
+        self.t_ts_rec = z(6 * O)
+        g.ts_rec = keep(self.t_ts_rec)
         self.t_spec = z(6 * B)
         self.t_maps = z(4 * B)
         self.t_partials = z(16 * K_PARTIAL_STRIDE)
