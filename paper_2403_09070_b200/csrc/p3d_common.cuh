@@ -105,6 +105,29 @@ __device__ __forceinline__ double ordered_sum(const volatile double* p, int n, d
   return acc[0];  // valid in thread 0
 }
 
+// Sum of n int64 partials by the whole block (integer: order-independent);
+// result valid in thread 0.
+__device__ __forceinline__ long long block_sum_ll_partials(const volatile long long* p, int n) {
+  __shared__ long long ws[32];
+  long long s = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += p[i];
+  s = warp_sum_ll(s);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  long long t = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+  return t;
+}
+
+// Max of n double partials by the whole block; result valid in thread 0.
+__device__ __forceinline__ double block_max_partials(const volatile double* p, int n, double* smem) {
+  double m = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, p[i]);
+  return block_max(m, smem);
+}
+
 // ---------------------------------------------------------------------------
 // numpy-faithful small math (compiled with -fmad=false where used)
 // ---------------------------------------------------------------------------

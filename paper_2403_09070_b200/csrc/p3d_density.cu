@@ -372,11 +372,8 @@ __global__ void overflow_kernel(long long n, const int64_t* rho, long long t, do
     partials[blockIdx.x] = b;
   }
   if (last_block(counter)) {
-    if (threadIdx.x == 0) {
-      long long s = 0;
-      for (int i = 0; i < (int)gridDim.x; ++i) s += ((volatile long long*)partials)[i];
-      *out = (double)s * scale;
-    }
+    const long long s = block_sum_ll_partials((volatile long long*)partials, gridDim.x);
+    if (threadIdx.x == 0) *out = (double)s * scale;
   }
 }
 

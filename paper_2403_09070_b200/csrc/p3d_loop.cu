@@ -364,9 +364,8 @@ __global__ void __launch_bounds__(256) gmax0_kernel(p3d_gp gp) {
   m = block_max(m, red);
   if (threadIdx.x == 0) part[blockIdx.x] = m;
   if (last_block(&st->counters[kCntStep])) {
+    const double gm = block_max_partials((volatile double*)part, gridDim.x, red);
     if (threadIdx.x == 0) {
-      double gm = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) gm = fmax(gm, ((volatile double*)part)[b]);
       st->gmax = gm;
       st->step = gm == 0.0 ? 1.0 : gp.step_scale / gm;
       st->step_set = 1;

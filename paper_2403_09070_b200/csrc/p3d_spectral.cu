@@ -222,12 +222,9 @@ __global__ void __launch_bounds__(256) line_pass(PassArgs a) {
       reinterpret_cast<long long*>(a.partials)[blockIdx.x] = b;
     }
     if (last_block(a.counter)) {
-      if (threadIdx.x == 0) {
-        long long s = 0;
-        const volatile long long* p = reinterpret_cast<const volatile long long*>(a.partials);
-        for (int i = 0; i < (int)gridDim.x; ++i) s += p[i];
-        *a.ovfl_out = (double)s * a.ovfl_scale;
-      }
+      const long long s = block_sum_ll_partials(
+          reinterpret_cast<const volatile long long*>(a.partials), gridDim.x);
+      if (threadIdx.x == 0) *a.ovfl_out = (double)s * a.ovfl_scale;
     }
   }
 }

@@ -22,7 +22,6 @@ namespace p3d {
 namespace {
 
 constexpr int kMaxNz = 16;
-constexpr int kColTile = 4;  // columns per CTA in kernel B
 constexpr int kThreads = 256;
 
 enum { T_DCT2 = 0, T_COS = 1, T_SIN = 2 };
@@ -213,12 +212,9 @@ __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
       reinterpret_cast<long long*>(a.partials)[blockIdx.x] = b;
     }
     if (last_block(a.counter)) {
-      if (threadIdx.x == 0) {
-        long long s = 0;
-        const volatile long long* p = reinterpret_cast<const volatile long long*>(a.partials);
-        for (int i = 0; i < (int)gridDim.x; ++i) s += p[i];
-        *a.ovfl_out = (double)s * a.ovfl_scale;
-      }
+      const long long s = block_sum_ll_partials(
+          reinterpret_cast<const volatile long long*>(a.partials), gridDim.x);
+      if (threadIdx.x == 0) *a.ovfl_out = (double)s * a.ovfl_scale;
     }
   }
 }
@@ -235,16 +231,20 @@ __device__ __forceinline__ double coef_factor(const FastArgs& a, int j, int k, i
   return s * a.in_scale;
 }
 
-// ---- B: x-lines of a C-column tile: DCT-II, then 4x (scale, inverse along x)
+// ---- B: x-lines of a C-column tile: DCT-II, then the 4 outputs' coefficient
+// scaling + inverse transforms batched into one FFT pass of 4C lines.  Output
+// M is interleaved [B][4] so kernel C reads whole slabs of all four maps.
+__device__ __forceinline__ int col_tile(int nx) { return nx >= 1024 ? 1 : 1024 / nx; }
+
 __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
   if (a.halt && *a.halt) return;
   extern __shared__ double sm[];
-  const int nx = a.nx, S = a.ny * a.nz, C = kColTile;
+  const int nx = a.nx, S = a.ny * a.nz, C = col_tile(nx), lg = a.logx;
   const int c0 = blockIdx.x * C;
-  double* X = sm;                                           // [C][nx]
-  double* R = sm + C * nx;                                  // [C][nx]
-  double2* cb = reinterpret_cast<double2*>(sm + 2 * C * nx);  // [C][nx]
-  double2* tw = reinterpret_cast<double2*>(sm + 4 * C * nx);  // [nx/2]
+  double* X = sm;                                              // [C][nx]
+  double* R = X + C * nx;                                      // [4C][nx]
+  double2* cb = reinterpret_cast<double2*>(R + 4 * C * nx);    // [4C][nx]
+  double2* tw = cb + 4 * C * nx;                               // [nx/2]
   stage_twiddles(a.twx, nx, tw);
   const double* src = a.coef_in ? a.coef_in : a.X;
   for (int t = threadIdx.x; t < C * nx; t += blockDim.x) {
@@ -253,10 +253,10 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
   }
   __syncthreads();
   if (!a.coef_in) {
-    pre_lines(T_DCT2, X, nx, 1, C, nx, a.logx, a.phx, cb);
+    pre_lines(T_DCT2, X, nx, 1, C, nx, lg, a.phx, cb);
     __syncthreads();
-    fft_lines(cb, C, nx, a.logx, tw, false);
-    post_lines(T_DCT2, cb, C, nx, a.logx, a.phx, X, nx, 1);
+    fft_lines(cb, C, nx, lg, tw, false);
+    post_lines(T_DCT2, cb, C, nx, lg, a.phx, X, nx, 1);
     __syncthreads();
     if (a.coef_out)
       for (int t = threadIdx.x; t < C * nx; t += blockDim.x) {
@@ -265,54 +265,92 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
       }
   }
   if (!a.maps) return;
-  for (int map = 0; map < 4; ++map) {
-    for (int t = threadIdx.x; t < C * nx; t += blockDim.x) {
-      const int c = t >> a.logx, ix = t & (nx - 1);
-      const int col = c0 + c, k = col / a.nz, l = col - k * a.nz;
-      R[t] = X[t] * coef_factor(a, ix, k, l, map);
+  // line L = map * C + c: scaled coefficients -> bit-reversed Makhoul input
+  const int shift = 32 - lg;
+  for (int t = threadIdx.x; t < (4 * C) << lg; t += blockDim.x) {
+    const int L = t >> lg, k = t & (nx - 1);
+    const int map = L / C, c = L - map * C;
+    const int col = c0 + c, ky = col / a.nz, kz = col - ky * a.nz;
+    const double* line = X + c * nx;
+    const int kn = (nx - k) & (nx - 1);
+    const double fk = coef_factor(a, k, ky, kz, map), fn = coef_factor(a, kn, ky, kz, map);
+    double ck, cn;
+    if (map != 1) {  // cosine series along x (phi, Ey, Ez)
+      ck = line[k] * fk;
+      cn = k ? line[kn] * fn : 0.0;
+    } else {  // sine series along x (Ex)
+      ck = k ? line[kn] * fn : 0.0;
+      cn = k ? line[k] * fk : 0.0;
     }
-    __syncthreads();
-    const int op = map == 1 ? T_SIN : T_COS;
-    pre_lines(op, R, nx, 1, C, nx, a.logx, a.phx, cb);
-    __syncthreads();
-    fft_lines(cb, C, nx, a.logx, tw, true);
-    post_lines(op, cb, C, nx, a.logx, a.phx, R, nx, 1);
-    __syncthreads();
-    double* out = a.M + (long long)map * nx * S;
-    for (int t = threadIdx.x; t < C * nx; t += blockDim.x) {
-      const int ix = t / C, c = t - ix * C;
-      out[(long long)ix * S + c0 + c] = R[c * nx + ix];
-    }
-    __syncthreads();
+    const double A = (k ? 0.5 : 1.0) * ck, B = 0.5 * cn;
+    const double cs = a.phx[2 * k], sn = a.phx[2 * k + 1];
+    cb[(L << lg) + (__brev(k) >> shift)] = make_double2(cs * A + sn * B, sn * A - cs * B);
+  }
+  __syncthreads();
+  fft_lines(cb, 4 * C, nx, lg, tw, true);
+  for (int t = threadIdx.x; t < (4 * C) << lg; t += blockDim.x) {
+    const int L = t >> lg, m = t & (nx - 1);
+    const int idx = (m & 1) ? nx - 1 - (m >> 1) : (m >> 1);
+    double y = cb[(L << lg) + idx].x;
+    if (L / C == 1 && (m & 1)) y = -y;
+    R[t] = y;
+  }
+  __syncthreads();
+  // interleaved write: for each row ix, C columns x 4 maps are contiguous
+  for (int t = threadIdx.x; t < 4 * C * nx; t += blockDim.x) {
+    const int ix = t / (4 * C), r = t - ix * 4 * C, c = r >> 2, map = r & 3;
+    a.M[((long long)ix * S + c0 + c) * 4 + map] = R[((map * C + c) << lg) + ix];
   }
 }
 
-// ---- C: inverse along y then z for the 4 maps of one x-slab -> [B][4]
+// ---- C: inverse along y then z for the 4 maps of one x-slab -> [B][4];
+// the 4*nz y-lines of the slab are one FFT batch
 __global__ void __launch_bounds__(kThreads) spec_inv_yz(FastArgs a) {
   if (a.halt && *a.halt) return;
   extern __shared__ double sm[];
-  const int ny = a.ny, nz = a.nz, S = ny * nz;
-  double* slab = sm;
-  double* tmp = sm + S;
-  double2* cb = reinterpret_cast<double2*>(sm + 2 * S);
-  double2* tw = reinterpret_cast<double2*>(sm + 4 * S);
+  const int ny = a.ny, nz = a.nz, S = ny * nz, lg = a.logy;
+  double* slab = sm;                                          // [4][S]
+  double* tmp = slab + 4 * S;                                 // [S]
+  double2* cb = reinterpret_cast<double2*>(tmp + S);          // [4 nz][ny]
+  double2* tw = cb + 4 * S;                                   // [ny/2]
   stage_twiddles(a.twy, ny, tw);
   const long long base = (long long)blockIdx.x * S;
-  const long long B = (long long)a.nx * S;
-  for (int map = 0; map < 4; ++map) {
-    const double* in = a.M + map * B + base;
-    for (int t = threadIdx.x; t < S; t += blockDim.x) slab[t] = in[t];
-    __syncthreads();
-    const int opy = map == 2 ? T_SIN : T_COS, opz = map == 3 ? T_SIN : T_COS;
-    pre_lines(opy, slab, 1, nz, nz, ny, a.logy, a.phy, cb);
-    __syncthreads();
-    fft_lines(cb, nz, ny, a.logy, tw, true);
-    post_lines(opy, cb, nz, ny, a.logy, a.phy, slab, 1, nz);
-    __syncthreads();
-    z_direct(opz, slab, ny, nz, tmp);
-    for (int t = threadIdx.x; t < S; t += blockDim.x) a.maps[(base + t) * 4 + map] = slab[t];
-    __syncthreads();
+  for (int t = threadIdx.x; t < 4 * S; t += blockDim.x)  // contiguous interleaved slab
+    slab[(t & 3) * S + (t >> 2)] = a.M[base * 4 + t];
+  __syncthreads();
+  // pre: line L = map * nz + iz, element iy at slab[map][iy*nz + iz]
+  const int shift = 32 - lg;
+  for (int t = threadIdx.x; t < (4 * nz) << lg; t += blockDim.x) {
+    const int L = t >> lg, k = t & (ny - 1);
+    const int map = L / nz, iz = L - map * nz;
+    const double* line = slab + map * S + iz;
+    const int kn = (ny - k) & (ny - 1);
+    double ck, cn;
+    if (map != 2) {  // cosine series along y (phi, Ex, Ez)
+      ck = line[k * nz];
+      cn = k ? line[kn * nz] : 0.0;
+    } else {  // sine series along y (Ey)
+      ck = k ? line[kn * nz] : 0.0;
+      cn = k ? line[k * nz] : 0.0;
+    }
+    const double A = (k ? 0.5 : 1.0) * ck, B = 0.5 * cn;
+    const double cs = a.phy[2 * k], sn = a.phy[2 * k + 1];
+    cb[(L << lg) + (__brev(k) >> shift)] = make_double2(cs * A + sn * B, sn * A - cs * B);
   }
+  __syncthreads();
+  fft_lines(cb, 4 * nz, ny, lg, tw, true);
+  for (int t = threadIdx.x; t < (4 * nz) << lg; t += blockDim.x) {
+    const int L = t >> lg, m = t & (ny - 1);
+    const int map = L / nz, iz = L - map * nz;
+    const int idx = (m & 1) ? ny - 1 - (m >> 1) : (m >> 1);
+    double y = cb[(L << lg) + idx].x;
+    if (map == 2 && (m & 1)) y = -y;
+    slab[map * S + m * nz + iz] = y;
+  }
+  __syncthreads();
+  for (int map = 0; map < 4; ++map) z_direct(map == 3 ? T_SIN : T_COS, slab + map * S, ny, nz, tmp);
+  for (int t = threadIdx.x; t < 4 * S; t += blockDim.x)
+    a.maps[base * 4 + t] = slab[(t & 3) * S + (t >> 2)];
 }
 
 int ilog2_pow2(int n) {
@@ -323,20 +361,30 @@ int ilog2_pow2(int n) {
 
 }  // namespace
 
+constexpr size_t kSmemMax = 227 * 1024;
+size_t smem_a(const p3d_grid* g) { return ((size_t)g->ny * g->nz * 4 + g->ny) * sizeof(double); }
+size_t smem_b(const p3d_grid* g) {
+  const size_t C = g->nx >= 1024 ? 1 : 1024 / g->nx;
+  return (C * g->nx * (1 + 4 + 8) + g->nx) * sizeof(double);
+}
+size_t smem_c(const p3d_grid* g) {
+  const size_t S = (size_t)g->ny * g->nz;
+  return (4 * S + S + 8 * S + g->ny) * sizeof(double);
+}
+
 bool spectral_fast_ok(const p3d_grid* g) {
   const int lx = ilog2_pow2(g->nx), ly = ilog2_pow2(g->ny);
   return lx >= 3 && ly >= 3 && g->nz >= 1 && g->nz <= kMaxNz &&
-         ((size_t)g->ny * g->nz * 4 + g->ny) * sizeof(double) <= 200 * 1024 &&
-         ((size_t)kColTile * g->nx * 4 + g->nx) * sizeof(double) <= 200 * 1024 &&
-         (g->ny * g->nz) % kColTile == 0;
+         smem_a(g) <= kSmemMax && smem_b(g) <= kSmemMax && smem_c(g) <= kSmemMax &&
+         g->nx <= 4096 && (g->ny * g->nz) % (g->nx >= 1024 ? 1 : 1024 / g->nx) == 0;
 }
 
 void spectral_fast_setup() {
   static bool done = false;
   if (done) return;
-  cudaFuncSetAttribute(spec_fwd_yz, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(spec_x, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(spec_inv_yz, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(spec_fwd_yz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+  cudaFuncSetAttribute(spec_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+  cudaFuncSetAttribute(spec_inv_yz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
   done = true;
 }
 
@@ -369,11 +417,10 @@ int launch_spectral_fast(const p3d_grid* g, const double* rho, const int64_t* rh
     a.ovfl_out = ov->out;
     a.ovfl_scale = ov->scale;
   }
-  const size_t smA = ((size_t)S * 4 + g->ny) * sizeof(double);
-  if (!coef_in) spec_fwd_yz<<<g->nx, kThreads, smA, s>>>(a);
-  const size_t smB = ((size_t)kColTile * g->nx * 4 + g->nx) * sizeof(double);
-  spec_x<<<(int)(S / kColTile), kThreads, smB, s>>>(a);
-  if (maps) spec_inv_yz<<<g->nx, kThreads, smA, s>>>(a);
+  if (!coef_in) spec_fwd_yz<<<g->nx, kThreads, smem_a(g), s>>>(a);
+  const int C = g->nx >= 1024 ? 1 : 1024 / g->nx;
+  spec_x<<<(int)(S / C), kThreads, smem_b(g), s>>>(a);
+  if (maps) spec_inv_yz<<<g->nx, kThreads, smem_c(g), s>>>(a);
   return check_launch("spectral (fast path)");
 }
 
