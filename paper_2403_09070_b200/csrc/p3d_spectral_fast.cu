@@ -375,7 +375,7 @@ int ilog2_pow2(int n) {
   return (1 << l) == n ? l : -1;
 }
 
-constexpr size_t kSmemMax = 227 * 1024;
+constexpr size_t kSmemMax = 220 * 1024;  // opt-in limit is 227 KB minus static smem
 size_t smem_a(const p3d_grid* g) {
   const size_t S = (size_t)g->ny * g->nz;
   return (2 * S + 4 * S + g->ny) * sizeof(double);
@@ -397,9 +397,13 @@ bool spectral_fast_ok(const p3d_grid* g) {
 void spectral_fast_setup() {
   static bool done = false;
   if (done) return;
-  cudaFuncSetAttribute(spec_fwd_yz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
-  cudaFuncSetAttribute(spec_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
-  cudaFuncSetAttribute(spec_inv_yz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+  if (cudaFuncSetAttribute(spec_fwd_yz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax) ||
+      cudaFuncSetAttribute(spec_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax) ||
+      cudaFuncSetAttribute(spec_inv_yz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax)) {
+    set_error("spectral: cannot opt into %zu bytes of shared memory", kSmemMax);
+    cudaGetLastError();
+    return;
+  }
   done = true;
 }
 

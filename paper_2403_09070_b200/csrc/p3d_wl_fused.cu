@@ -112,6 +112,16 @@ __device__ __forceinline__ double exp_neg(double x) {
 // float64 WA sums with numpy's structure (wirelength.py:85-96): value
 // sxp/s1p - sxm/s1m, gradient ep/s1p (1 + (v - vp)/g) - em/s1m (1 - (v - vm)/g);
 // 1/gamma and the per-segment reciprocals are hoisted (<= 1 ulp differences).
+template <class R>
+struct GradK {  // per-segment constants of the per-pin WA gradient
+  R rp, rm;
+  double vp, vm;
+  // ep/s1p (1 + (v - vp)/g) - em/s1m (1 - (v - vm)/g)  (wirelength.py:94-96)
+  __device__ __forceinline__ R grad(double v, R ig, R ep, R em) const {
+    return ep * rp * ((R)1 + (R)(v - vp) * ig) - em * rm * ((R)1 - (R)(v - vm) * ig);
+  }
+};
+
 struct Wa64 {
   using R = double;
   double s1p, sxp, s1m, sxm, rp, rm, vp, vm;
@@ -134,6 +144,7 @@ struct Wa64 {
     vm = sxm * rm;
   }
   __device__ __forceinline__ double value(double, double) const { return s1p > 0 ? vp - vm : 0.0; }
+  __device__ __forceinline__ GradK<double> gk(double, double) const { return {rp, rm, vp, vm}; }
   __device__ __forceinline__ double grad(double v, double, double, double ig, double ep,
                                          double em) const {
     return ep * rp * (1.0 + (v - vp) * ig) - em * rm * (1.0 - (v - vm) * ig);
@@ -165,6 +176,9 @@ struct Wa32 {
   }
   __device__ __forceinline__ double value(double hi, double lo) const {
     return s1p > 0.f ? (hi - lo) + (double)(mp - mm) : 0.0;
+  }
+  __device__ __forceinline__ GradK<float> gk(double hi, double lo) const {
+    return {rp, rm, hi + (double)mp, lo + (double)mm};
   }
   __device__ __forceinline__ float grad(double v, double hi, double lo, float ig, float ep,
                                         float em) const {
@@ -341,10 +355,14 @@ __device__ __forceinline__ void store_comp(const FusedNetArgs& a, int idx, int c
   else reinterpret_cast<float*>(a.out_f)[4 * (long long)idx + comp] = (float)v;
 }
 
-// One planar axis of a staged net: boxes, branch, WA sums of the chosen
-// branch, per-pin gradients, FD extent deltas (accumulated into dw).
-template <bool F32>
-__device__ __forceinline__ void staged_axis(int D, const double (&c)[kMaxStagedDeg][32],
+// One planar axis of a staged net (degree D, fully unrolled: every shared-
+// memory column offset is an immediate): boxes, branch, WA sums of the chosen
+// branch, per-pin gradients, FD extent deltas (accumulated into pz, which
+// holds the FD accumulator by this phase).  Per-pin segment choices are
+// selects of hoisted per-segment constants; the FD delta is evaluated for
+// both dies and selected.
+template <int D, bool F32>
+__device__ __forceinline__ void staged_axis(const double (&c)[kMaxStagedDeg][32],
                                             WarpCols<F32>& sm, int lane, int topm,
                                             typename WaSel<F32>::R ig, double& val,
                                             double& exact, bool& crossing, const FusedNetArgs& a,
@@ -353,39 +371,44 @@ __device__ __forceinline__ void staged_axis(int D, const double (&c)[kMaxStagedD
   using R = typename WaSel<F32>::R;
   Box2 bx;
   bx.init();
-#pragma unroll 1
+#pragma unroll
   for (int k = 0; k < D; ++k) bx.add(c[k][lane], (topm >> k) & 1);
   const double full = bx.full(), part = bx.t.span() + bx.b.span();
   const double ex = fmax(full, part);
   const bool split = part > full;  // ties resolve to the full box (wirelength.py:186)
   exact = ex;
   crossing = bx.b.cnt > 0 && bx.t.cnt > 0;
+  // segment 0: the whole net (unsplit) or die 0; segment 1: die 1 (split only)
+  const double h0 = split ? bx.b.hi1 : bx.fmx(), l0 = split ? bx.b.lo1 : bx.fmn();
+  const double h1 = bx.t.hi1, l1 = bx.t.lo1;
+  const int umask = split ? topm : 0;
   W w0, w1;
   w0.init();
   w1.init();
 #pragma unroll 1
   for (int k = 0; k < D; ++k) {
     const double v = c[k][lane];
-    const SegSel sg = seg_of(bx, split, (topm >> k) & 1);
+    const bool up = (umask >> k) & 1;
     R ep, em;
-    W::term(v, sg.hi, sg.lo, ig, ep, em);
+    W::term(v, up ? h1 : h0, up ? l1 : l0, ig, ep, em);
     sm.ep[k][lane] = ep;
     sm.em[k][lane] = em;
-    w0.acc(v, sg.hi, sg.lo, ep, em, sg.upper ? 0 : 1);
-    w1.acc(v, sg.hi, sg.lo, ep, em, sg.upper ? 1 : 0);
+    w0.acc(v, h0, l0, ep, em, up ? 0 : 1);
+    w1.acc(v, h1, l1, ep, em, up ? 1 : 0);
   }
   w0.finalize();
   w1.finalize();
-  val = split ? (w0.value(bx.b.hi1, bx.b.lo1) + w1.value(bx.t.hi1, bx.t.lo1))
-              : w0.value(bx.fmx(), bx.fmn());
+  val = split ? (w0.value(h0, l0) + w1.value(h1, l1)) : w0.value(h0, l0);
+  const GradK<R> k0 = w0.gk(h0, l0), k1 = w1.gk(h1, l1);
 #pragma unroll 1
   for (int k = 0; k < D; ++k) {
-    const int tp = (topm >> k) & 1;
     const double v = c[k][lane];
-    const SegSel sg = seg_of(bx, split, tp);
-    store_comp(a, pin0 + k * nb, comp,
-               (double)(sg.upper ? w1 : w0).grad(v, sg.hi, sg.lo, ig, sm.ep[k][lane], sm.em[k][lane]));
-    sm.pz[k][lane] += bx.flip(v, tp, full, ex);  // pz holds the FD accumulator by now
+    const bool up = (umask >> k) & 1;
+    const GradK<R> gk = {up ? k1.rp : k0.rp, up ? k1.rm : k0.rm, up ? k1.vp : k0.vp,
+                         up ? k1.vm : k0.vm};
+    store_comp(a, pin0 + k * nb, comp, (double)gk.grad(v, ig, sm.ep[k][lane], sm.em[k][lane]));
+    const double fb = flip_delta(bx.b, bx.t, v, full, ex), ft = flip_delta(bx.t, bx.b, v, full, ex);
+    sm.pz[k][lane] += ((topm >> k) & 1) ? ft : fb;
   }
 }
 
@@ -422,8 +445,8 @@ __device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk,
   return true;
 }
 
-template <bool F32>
-__device__ __forceinline__ void staged_eval(const FusedNetArgs& a, int D, int pin0, int nb,
+template <int D, bool F32>
+__device__ __forceinline__ void staged_eval(const FusedNetArgs& a, int pin0, int nb,
                                             WarpCols<F32>& sm, int lane, int topm, double zhi,
                                             double zlo, double (&acc)[6]) {
   using W = typename WaSel<F32>::W;
@@ -442,19 +465,19 @@ __device__ __forceinline__ void staged_eval(const FusedNetArgs& a, int D, int pi
   }
   wz.finalize();
   acc[2] += wz.value(zhi, zlo);
+  const GradK<R> kz = wz.gk(zhi, zlo);
 #pragma unroll 1
   for (int k = 0; k < D; ++k) {
-    store_comp(a, pin0 + k * nb, 2,
-               (double)wz.grad(sm.pz[k][lane], zhi, zlo, ig, sm.ep[k][lane], sm.em[k][lane]));
+    store_comp(a, pin0 + k * nb, 2, (double)kz.grad(sm.pz[k][lane], ig, sm.ep[k][lane], sm.em[k][lane]));
     sm.pz[k][lane] = 0.0;
   }
   double v, ex;
   bool cross;
-  staged_axis<F32>(D, sm.px, sm, lane, topm, ig, v, ex, cross, a, pin0, nb, 0);
+  staged_axis<D, F32>(sm.px, sm, lane, topm, ig, v, ex, cross, a, pin0, nb, 0);
   acc[0] += v;
   acc[3] += ex;
   acc[5] += cross ? 1.0 : 0.0;
-  staged_axis<F32>(D, sm.py, sm, lane, topm, ig, v, ex, cross, a, pin0, nb, 1);
+  staged_axis<D, F32>(sm.py, sm, lane, topm, ig, v, ex, cross, a, pin0, nb, 1);
   acc[1] += v;
   acc[4] += ex;
 #pragma unroll 1
@@ -470,7 +493,7 @@ __device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk
   int topm;
   double zhi, zlo;
   if (stage_pins<D, F32>(a, tk, t0, sm, lane, topm, zhi, zlo))
-    staged_eval<F32>(a, D, tk.x + tk.z + lane, tk.y, sm, lane, topm, zhi, zlo, acc);
+    staged_eval<D, F32>(a, tk.x + tk.z + lane, tk.y, sm, lane, topm, zhi, zlo, acc);
 }
 
 template <bool F32>
