@@ -113,7 +113,9 @@ typedef struct p3d_grid {
   double dx, dy, dz, wb, hb, db, bin_vol;
   double fx_scale;           /* 2^40 / bin_vol (fixed-point density scale) */
   const double* omega[3];    /* [nx], [ny], [nz]: pi*k/d */
-  const double* twiddle[3];  /* per axis: [n] (cos,sin)(-2 pi j/n), j < n/2 */
+  const double* twiddle[3];  /* per axis: [n] (cos,sin)(-2 pi j/n), j < n/2; then, for
+                                power-of-two n in [8,1024], the per-pass DIF table
+                                W_{8s}^{qj} [pass][q-1][j] (density._pass_twiddles) */
   const double* phase[3];    /* per axis: [2n] (cos,sin)(pi k/(2n)) */
 } p3d_grid;
 

@@ -1,20 +1,27 @@
-// K3 fast path — the spectral solve in three kernels instead of six passes,
-// for power-of-two nx, ny >= 8 and nz <= kMaxNz (every BASELINE config):
-//   A  yz-forward : one x-slab [ny][nz] (contiguous) per CTA: int64 fixed-point
+// K3 fast path — the spectral solve in three kernels for power-of-two nx, ny
+// in [8, 1024] and small nz (every BASELINE config):
+//   A  yz-forward : SA x-slabs [ny][nz] (contiguous) per CTA: int64 fixed-point
 //                   rho -> float64 (+ overflow excess, + re-zero for the next
 //                   scatter), DCT-II along z (direct, nz small) and along y;
-//   B  x          : one column x all nx rows per CTA: DCT-II along x, then the
-//                   4 outputs' coefficient scaling (1/lambda, omega) and inverse
-//                   transforms along x batched into one FFT pass (cosine series
-//                   for phi, Ey, Ez; sine series for Ex), written interleaved;
+//   B  x          : 4 adjacent (y, z) columns per CTA (one 32-byte sector per
+//                   row): DCT-II along x, the 1/lambda and omega scaling of the
+//                   four outputs, and their inverse transforms along x, written
+//                   as the interleaved [B][4] intermediate;
 //   C  yz-inverse : one x-slab of all 4 maps per CTA: inverse along y and z,
 //                   written as the interleaved [B][4] (phi, Ex, Ey, Ez) map the
 //                   density gather reads.
-// Every 1-D transform is Makhoul's N-point complex FFT reordering (see
-// p3d_spectral.cu for the math); the FFT itself is a self-sorting Stockham
-// radix-4 (+ one radix-2 stage for odd log2 N) in shared memory, ping-ponging
-// between two buffers: natural-order input and output, no bit reversal, and
-// only the first one or two stages have strided (2-4 way conflicted) stores.
+// Every 1-D real transform is Makhoul's N-point reordering onto a complex FFT,
+// with TWO real lines packed into one complex line (re/im), so a 512-point
+// line costs half a 512-point complex FFT.  The FFT is an in-place mixed-radix
+// decimation-in-frequency transform: radix-8 butterflies held in registers
+// (log8 N passes, + one radix-2/4 pass), a per-pass twiddle table laid out
+// [q][j] (lanes read consecutive entries; read-only cached, built on the host
+// with the grid), and a padded line layout (one slot per 8) so every pass is
+// bank-conflict free.  nz == 2 (every BASELINE config) fuses the z transform
+// into A's load and C's store, so neither stages a slab.  The output is
+// left in mixed-radix digit-reversed order and the post-processing reads it
+// through pos_of().  fp64 throughout (TF32 breaks trajectory parity, SURVEY
+// App. B).
 #include "p3d_common.cuh"
 #include "p3d_internal.cuh"
 
@@ -24,6 +31,8 @@ namespace {
 
 constexpr int kMaxNz = 16;
 constexpr int kThreads = 256;
+constexpr int kColsB = 2;     // columns per CTA in B
+constexpr int kFftRoundC = 4; // complex lines per round in C
 
 enum { T_DCT2 = 0, T_COS = 1, T_SIN = 2 };
 
@@ -32,147 +41,220 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-
-// e^{-2 pi i idx / N} from the half table tw[j] = e^{-2 pi i j / N}, j < N/2
-__device__ __forceinline__ double2 twiddle(const double2* tw, int idx, int N, bool inv) {
-  const int h = N >> 1;
-  double2 w = idx < h ? tw[idx] : make_double2(-tw[idx - h].x, -tw[idx - h].y);
-  if (inv) w.y = -w.y;
-  return w;
+// -i z (forward) / +i z (inverse)
+template <bool INV>
+__device__ __forceinline__ double2 rot_i(double2 z) {
+  return INV ? make_double2(-z.y, z.x) : make_double2(z.y, -z.x);
 }
 
-// Stockham autosort FFT over nl lines of N = 2^logN (line l at A + l*N).
-// Returns the buffer holding the natural-order result (A or B).
-__device__ double2* fft_stockham(double2* A, double2* B, int nl, int logN, const double2* tw,
-                                 bool inv) {
-  const int N = 1 << logN;
-  double2* in = A;
-  double2* out = B;
-  int lns = 0;  // log2 Ns
-  if (logN & 1) {  // one radix-2 stage (Ns = 1)
-    const int q = N >> 1;
-    for (int t = threadIdx.x; t < nl * q; t += blockDim.x) {
-      const int l = t >> (logN - 1), j = t & (q - 1);
-      const double2* src = in + (l << logN);
-      double2* dst = out + (l << logN);
-      const double2 v0 = src[j], v1 = src[j + q];
-      dst[2 * j] = cadd(v0, v1);
-      dst[2 * j + 1] = csub(v0, v1);
-    }
-    __syncthreads();
-    double2* tmp = in; in = out; out = tmp;
-    lns = 1;
+template <int L>
+struct Fft {
+  static constexpr int N = 1 << L;
+  static constexpr int P8 = L / 3;                 // radix-8 passes
+  static constexpr int REM = L % 3;                // last pass radix 2^REM (0: none)
+  static constexpr int LS = N + (N >> 3) + 2;      // padded line stride (complex slots)
+  __host__ __device__ static constexpr int pad(int p) { return p + (p >> 3); }
+  __host__ __device__ static constexpr int lspan(int s) { return L - 3 * (s + 1); }
+  __host__ __device__ static constexpr int tw_off(int s) {
+    int o = 0;
+    for (int i = 0; i < s; ++i) o += lspan(i) > 0 ? 7 << lspan(i) : 0;
+    return o;
   }
-  for (; lns < logN; lns += 2) {  // radix-4 stages
-    const int Ns = 1 << lns, q = N >> 2, tstride = N >> (lns + 2);
-    for (int t = threadIdx.x; t < nl * q; t += blockDim.x) {
-      const int l = t >> (logN - 2), j = t & (q - 1);
-      const double2* src = in + (l << logN);
-      double2* dst = out + (l << logN);
-      const int k = j & (Ns - 1);
-      double2 v0 = src[j], v1 = src[j + q], v2 = src[j + 2 * q], v3 = src[j + 3 * q];
-      if (k) {
-        const int e = k * tstride;  // W_{4Ns}^{r k} = W_N^{r k N/(4 Ns)}
-        v1 = cmul(v1, twiddle(tw, e, N, inv));
-        v2 = cmul(v2, twiddle(tw, 2 * e, N, inv));
-        v3 = cmul(v3, twiddle(tw, 3 * e, N, inv));
+  static constexpr int TW = tw_off(P8);            // twiddle entries (complex)
+  // frequency k -> slot after the DIF passes (mixed-radix digit reversal)
+  __device__ static __forceinline__ int pos_of(int k) {
+    int p = 0;
+#pragma unroll
+    for (int s = 0; s < P8; ++s) {
+      p += (k & 7) << lspan(s);
+      k >>= 3;
+    }
+    if (REM) p += k & ((1 << REM) - 1);
+    return p;
+  }
+};
+
+// 8-point DFT in registers; a[q] = X_q on return
+template <bool INV>
+__device__ __forceinline__ void dft8(double2 (&a)[8]) {
+  const double r2 = 0.70710678118654752440;
+  double2 b[8];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) b[m] = cadd(a[m], a[m + 4]);
+  b[4] = csub(a[0], a[4]);
+  {
+    const double2 d = csub(a[1], a[5]);  // * W8^1
+    b[5] = INV ? make_double2(r2 * (d.x - d.y), r2 * (d.x + d.y))
+               : make_double2(r2 * (d.x + d.y), r2 * (d.y - d.x));
+  }
+  b[6] = rot_i<INV>(csub(a[2], a[6]));  // * W8^2
+  {
+    const double2 d = csub(a[3], a[7]);  // * W8^3
+    b[7] = INV ? make_double2(-r2 * (d.x + d.y), r2 * (d.x - d.y))
+               : make_double2(r2 * (d.y - d.x), -r2 * (d.x + d.y));
+  }
+  double2 c[8];
+#pragma unroll
+  for (int h = 0; h < 8; h += 4) {
+    c[h + 0] = cadd(b[h + 0], b[h + 2]);
+    c[h + 2] = csub(b[h + 0], b[h + 2]);
+    c[h + 1] = cadd(b[h + 1], b[h + 3]);
+    c[h + 3] = rot_i<INV>(csub(b[h + 1], b[h + 3]));
+  }
+  // d[p] = X[bitrev3(p)]
+  a[0] = cadd(c[0], c[1]);
+  a[4] = csub(c[0], c[1]);
+  a[2] = cadd(c[2], c[3]);
+  a[6] = csub(c[2], c[3]);
+  a[1] = cadd(c[4], c[5]);
+  a[5] = csub(c[4], c[5]);
+  a[3] = cadd(c[6], c[7]);
+  a[7] = csub(c[6], c[7]);
+}
+
+// The per-pass twiddle table of one axis (density._pass_twiddles): W_{8 span}^{q j}
+// for q = 1..7, j < span, laid out [pass][q-1][j], stored after the n/2-entry
+// half table.  Read through the read-only path (<= 16 KB, L1-resident).
+__device__ __forceinline__ const double2* pass_twiddles(const double* tw, int N) {
+  return reinterpret_cast<const double2*>(tw) + (N >> 1);
+}
+
+// In-place DIF FFT of nl lines (line l at buf + l * LS); all threads take part.
+template <int L, bool INV>
+__device__ __forceinline__ void fft_lines(double2* buf, int nl, const double2* tw) {
+  using F = Fft<L>;
+#pragma unroll
+  for (int s = 0; s < F::P8; ++s) {
+    const int ls = F::lspan(s);
+    const int nb = F::N >> 3;
+    for (int t = threadIdx.x; t < nl * nb; t += blockDim.x) {
+      const int l = t >> (L - 3), u = t & (nb - 1);
+      const int j = u & ((1 << ls) - 1), b = u >> ls;
+      double2* x = buf + l * F::LS;
+      const int base = (b << (ls + 3)) + j;
+      double2 a[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) a[m] = x[F::pad(base + (m << ls))];
+      dft8<INV>(a);
+      if (ls > 0) {
+        const double2* w = tw + F::tw_off(s) + j;
+#pragma unroll
+        for (int q = 1; q < 8; ++q) {
+          double2 wq = __ldg(w + ((q - 1) << ls));
+          if (INV) wq.y = -wq.y;
+          a[q] = cmul(a[q], wq);
+        }
       }
-      const double2 a0 = cadd(v0, v2), a1 = csub(v0, v2), a2 = cadd(v1, v3);
-      const double2 d = csub(v1, v3);
-      const double2 a3 = inv ? make_double2(-d.y, d.x) : make_double2(d.y, -d.x);  // +-i d
-      const int o = ((j - k) << 2) + k;
-      dst[o] = cadd(a0, a2);
-      dst[o + Ns] = cadd(a1, a3);
-      dst[o + 2 * Ns] = csub(a0, a2);
-      dst[o + 3 * Ns] = csub(a1, a3);
+#pragma unroll
+      for (int m = 0; m < 8; ++m) x[F::pad(base + (m << ls))] = a[m];
     }
     __syncthreads();
-    double2* tmp = in; in = out; out = tmp;
   }
-  return in;
-}
-
-// Makhoul pre-processing of one element into natural-order FFT input at `pos`.
-__device__ __forceinline__ void pre_elem(int op, int n, int N, double xn, double ck, double cn,
-                                         const double* ph, double2& v, int& pos) {
-  if (op == T_DCT2) {
-    pos = (n & 1) ? N - 1 - (n >> 1) : (n >> 1);  // v[n/2] = x[n], v[N-1-(n-1)/2] = x[n]
-    v = make_double2(xn, 0.0);
-  } else {  // V_k = e^{i pi k/2N} (t_k c_k - i t_{N-k} c_{N-k}), t_0 = 1, t_k = 1/2
-    const double A = (n ? 0.5 : 1.0) * ck, B = 0.5 * cn;
-    const double cs = ph[2 * n], sn = ph[2 * n + 1];
-    v = make_double2(cs * A + sn * B, sn * A - cs * B);
-    pos = n;
-  }
-}
-
-// Pre-process nl real lines (element k of line l at r[l*rs + k*es]).
-__device__ __forceinline__ void pre_lines(int op, const double* r, int rs, int es, int nl,
-                                          int logN, const double* ph, double2* c) {
-  const int N = 1 << logN;
-  for (int t = threadIdx.x; t < (nl << logN); t += blockDim.x) {
-    const int l = t >> logN, n = t & (N - 1);
-    const double* line = r + l * rs;
-    double ck = 0.0, cn = 0.0, xn = 0.0;
-    if (op == T_DCT2) xn = line[n * es];
-    else if (op == T_COS) { ck = line[n * es]; cn = n ? line[(N - n) * es] : 0.0; }
-    else { ck = n ? line[(N - n) * es] : 0.0; cn = n ? line[n * es] : 0.0; }
-    double2 v;
-    int pos;
-    pre_elem(op, n, N, xn, ck, cn, ph, v, pos);
-    c[(l << logN) + pos] = v;
+  if (F::REM == 2) {
+    for (int t = threadIdx.x; t < nl * (F::N >> 2); t += blockDim.x) {
+      const int l = t >> (L - 2), u = t & ((F::N >> 2) - 1);
+      double2* x = buf + l * F::LS + F::pad(u << 2);  // 4 slots never straddle a pad
+      const double2 a0 = x[0], a1 = x[1], a2 = x[2], a3 = x[3];
+      const double2 b0 = cadd(a0, a2), b2 = csub(a0, a2), b1 = cadd(a1, a3);
+      const double2 b3 = rot_i<INV>(csub(a1, a3));
+      x[0] = cadd(b0, b1);
+      x[1] = cadd(b2, b3);
+      x[2] = csub(b0, b1);
+      x[3] = csub(b2, b3);
+    }
+    __syncthreads();
+  } else if (F::REM == 1) {
+    for (int t = threadIdx.x; t < nl * (F::N >> 1); t += blockDim.x) {
+      const int l = t >> (L - 1), u = t & ((F::N >> 1) - 1);
+      double2* x = buf + l * F::LS + F::pad(u << 1);
+      const double2 a0 = x[0], a1 = x[1];
+      x[0] = cadd(a0, a1);
+      x[1] = csub(a0, a1);
+    }
+    __syncthreads();
   }
 }
 
-// Post-process natural-order FFT output of one line (element m).
-__device__ __forceinline__ double post_elem(int op, const double2* buf, int m, int N,
-                                            const double* ph) {
-  if (op == T_DCT2) return ph[2 * m] * buf[m].x + ph[2 * m + 1] * buf[m].y;  // Re(e^{-i pi k/2N} V_k)
-  const int idx = (m & 1) ? N - 1 - (m >> 1) : (m >> 1);
-  const double y = buf[idx].x;
-  return (op == T_SIN && (m & 1)) ? -y : y;  // sine series: (-1)^m cosine series of c'
+// Makhoul DCT-II input slot of element n
+template <int L>
+__device__ __forceinline__ int dct_slot(int n) {
+  return (n & 1) ? (1 << L) - 1 - (n >> 1) : (n >> 1);
 }
 
-__device__ __forceinline__ void post_lines(int op, const double2* c, int nl, int logN,
-                                           const double* ph, double* r, int rs, int es) {
-  const int N = 1 << logN;
-  for (int t = threadIdx.x; t < (nl << logN); t += blockDim.x) {
-    const int l = t >> logN, m = t & (N - 1);
-    r[l * rs + m * es] = post_elem(op, c + (l << logN), m, N, ph);
-  }
+// packed DCT-II post-processing of frequency k: (X_a[k], X_b[k])
+template <int L>
+__device__ __forceinline__ double2 dct2_post(const double2* line, int k, const double* ph) {
+  using F = Fft<L>;
+  const double2 zk = line[F::pad(F::pos_of(k))];
+  const double2 zn = line[F::pad(F::pos_of((F::N - k) & (F::N - 1)))];
+  const double cs = __ldg(ph + 2 * k), sn = __ldg(ph + 2 * k + 1);
+  // V_a = (Z_k + conj Z_{N-k}) / 2, V_b = -i (Z_k - conj Z_{N-k}) / 2; X = Re(e^{-i pi k/2N} V)
+  const double ar = 0.5 * (zk.x + zn.x), ai = 0.5 * (zk.y - zn.y);
+  const double br = 0.5 * (zk.y + zn.y), bi = 0.5 * (zn.x - zk.x);
+  return make_double2(cs * ar + sn * ai, cs * br + sn * bi);
 }
 
-__device__ __forceinline__ void stage_twiddles(const double* tw, int N, double2* smem_tw) {
-  for (int j = threadIdx.x; j < (N >> 1); j += blockDim.x)
-    smem_tw[j] = make_double2(tw[2 * j], tw[2 * j + 1]);
+// inverse (cosine / sine series) pre-processing of element n of one real
+// line with coefficients c_k = get(k): V_n = e^{i pi n/2N} (t_n c'_n - i t_{N-n} c'_{N-n})
+__device__ __forceinline__ double2 inv_pre(int op, int n, int N, double cn_self, double cn_mirror,
+                                           const double* ph) {
+  // COS: c'_n = c_n; SIN: c'_n = c_{N-n} (c'_0 = 0), output sign (-1)^m in post
+  double ck, cm;
+  if (op == T_COS) { ck = cn_self; cm = n ? cn_mirror : 0.0; }
+  else { ck = n ? cn_mirror : 0.0; cm = n ? cn_self : 0.0; }
+  const double A = (n ? 0.5 : 1.0) * ck, B = 0.5 * cm;
+  const double cs = __ldg(ph + 2 * n), sn = __ldg(ph + 2 * n + 1);
+  return make_double2(cs * A + sn * B, sn * A - cs * B);
 }
 
-// direct transform along z of every row of a slab [ny][nz] held in smem;
+template <int L>
+__device__ __forceinline__ double2 inv_post(const double2* line, int m) {
+  using F = Fft<L>;
+  const int idx = (m & 1) ? F::N - 1 - (m >> 1) : (m >> 1);
+  return line[F::pad(F::pos_of(idx))];
+}
+
+// direct transform along z of every row of nsl slabs [ny][nz] held in smem;
 // nz == 2 (every BASELINE config) is a closed-form butterfly
-__device__ __forceinline__ void z_direct(int op, double* slab, int ny, int nz, double* tmp) {
-  if (nz == 2) {
-    const double r2 = 0.70710678118654752440;  // cos(pi/4) = sin(pi/4)
-    for (int iy = threadIdx.x; iy < ny; iy += blockDim.x) {
-      const double x0 = slab[2 * iy], x1 = slab[2 * iy + 1];
-      double y0, y1;
-      if (op == T_DCT2) { y0 = x0 + x1; y1 = (x0 - x1) * r2; }
-      else if (op == T_COS) { y0 = x0 + x1 * r2; y1 = x0 - x1 * r2; }
-      else { y0 = x1 * r2; y1 = x1 * r2; }
-      slab[2 * iy] = y0;
-      slab[2 * iy + 1] = y1;
+__device__ __forceinline__ void z_direct(int op, double* slab, int rows, int nz, int stride_map,
+                                         int nmaps, const int* map_op, double* tmp) {
+  if (nz == 1) {
+    for (int t = threadIdx.x; t < rows * nmaps; t += blockDim.x) {
+      const int mp = t / rows, r = t - mp * rows;
+      const int o = map_op ? map_op[mp] : op;
+      if (o == T_SIN) slab[mp * stride_map + r] = 0.0;
     }
     __syncthreads();
     return;
   }
-  const int mod = 4 * nz;
-  for (int t = threadIdx.x; t < ny * nz; t += blockDim.x) {
-    const int iy = t / nz, m = t - iy * nz;
-    const double* row = slab + iy * nz;
+  if (nz == 2) {
+    const double r2 = 0.70710678118654752440;  // cos(pi/4) = sin(pi/4)
+    for (int t = threadIdx.x; t < rows * nmaps; t += blockDim.x) {
+      const int mp = t / rows, iy = t - mp * rows;
+      const int o = map_op ? map_op[mp] : op;
+      double* p = slab + mp * stride_map + 2 * iy;
+      const double x0 = p[0], x1 = p[1];
+      double y0, y1;
+      if (o == T_DCT2) { y0 = x0 + x1; y1 = (x0 - x1) * r2; }
+      else if (o == T_COS) { y0 = x0 + x1 * r2; y1 = x0 - x1 * r2; }
+      else { y0 = x1 * r2; y1 = x1 * r2; }
+      p[0] = y0;
+      p[1] = y1;
+    }
+    __syncthreads();
+    return;
+  }
+  const int mod = 4 * nz, S = rows * nz;
+  for (int t = threadIdx.x; t < S * nmaps; t += blockDim.x) {
+    const int mp = t / S, e = t - mp * S;
+    const int iy = e / nz, m = e - iy * nz;
+    const int o = map_op ? map_op[mp] : op;
+    const double* row = slab + mp * stride_map + iy * nz;
     double s = 0.0;
     for (int n = 0; n < nz; ++n) {
-      const long long p = op == T_DCT2 ? (long long)m * (2 * n + 1) : (long long)n * (2 * m + 1);
+      const long long p = o == T_DCT2 ? (long long)m * (2 * n + 1) : (long long)n * (2 * m + 1);
       const double ang = (double)(p % mod) / (double)(2 * nz);
-      if (op == T_SIN) {
+      if (o == T_SIN) {
         if (n) s += row[n] * sinpi(ang);
       } else {
         s += row[n] * cospi(ang);
@@ -181,12 +263,15 @@ __device__ __forceinline__ void z_direct(int op, double* slab, int ny, int nz, d
     tmp[t] = s;
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < ny * nz; t += blockDim.x) slab[t] = tmp[t];
+  for (int t = threadIdx.x; t < S * nmaps; t += blockDim.x) {
+    const int mp = t / S, e = t - mp * S;
+    slab[mp * stride_map + e] = tmp[t];
+  }
   __syncthreads();
 }
 
 struct FastArgs {
-  int nx, ny, nz, logx, logy;
+  int nx, ny, nz, logx, logy, sa;
   const double *omx, *omy, *omz;
   const double *twx, *twy, *phx, *phy;
   const int64_t* rho_fx;  // A input (or rho_d)
@@ -206,165 +291,280 @@ struct FastArgs {
   const int* halt;
 };
 
-// ---- A: fixed-point rho -> X_yz (DCT-II along z, then y), overflow, re-zero
+// overflow excess of the fixed-point map: per-CTA partials + last-block total
+__device__ __forceinline__ void ovfl_epilogue(const FastArgs& a, long long excess) {
+  if (!a.ovfl_out) return;
+  long long e = warp_sum_ll(excess);
+  __shared__ long long ws[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = e;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long b = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += ws[w];
+    reinterpret_cast<long long*>(a.partials)[blockIdx.x] = b;
+  }
+  if (last_block(a.counter)) {
+    const long long sum = block_sum_ll_partials(
+        reinterpret_cast<const volatile long long*>(a.partials), gridDim.x);
+    if (threadIdx.x == 0) *a.ovfl_out = (double)sum * a.ovfl_scale;
+  }
+}
+
+// ---- A: fixed-point rho -> X_yz (DCT-II along z, then y), overflow, re-zero.
+// nz == 2: the z butterfly of row iy IS the packed complex input of element iy
+// (re: z-mode 0, im: z-mode 1), so a slab is one complex line and nothing is
+// staged; other nz stage the slab and run the direct z transform.
+template <int LY, bool NZ2>
 __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
+  using F = Fft<LY>;
   if (a.halt && *a.halt) return;
-  extern __shared__ double sm[];
-  const int ny = a.ny, nz = a.nz, S = ny * nz;
-  double* slab = sm;                                     // [S]
-  double* tmp = sm + S;                                  // [S]
-  double2* cA = reinterpret_cast<double2*>(sm + 2 * S);  // [S] complex
-  double2* cB = cA + S;                                  // [S] complex
-  double2* tw = cB + S;                                  // [ny/2]
-  stage_twiddles(a.twy, ny, tw);
-  const long long base = (long long)blockIdx.x * S;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int ny = F::N, nz = a.nz, S = ny * nz, nfs = (nz + 1) >> 1;
+  const int x0 = blockIdx.x * a.sa, nsl = min(a.sa, a.nx - x0);
+  const double2* tw = pass_twiddles(a.twy, ny);
+  double2* buf = reinterpret_cast<double2*>(smraw);  // [sa * nfs][LS]
+  const long long base = (long long)x0 * S;
+  const int nf = nsl * nfs;
   long long excess = 0;
-  for (int t = threadIdx.x; t < S; t += blockDim.x) {
-    double v;
-    if (a.rho_fx) {
-      const long long q = a.rho_fx[base + t];
-      v = (double)q * 9.094947017729282379150390625e-13;  // 2^-40, exact
-      const long long e = q - a.rho_t_fx;
-      excess += e > 0 ? e : 0;
-      if (a.zero_fx) a.zero_fx[base + t] = 0;
-    } else {
-      v = a.rho_d[base + t];
+  if (NZ2) {
+    constexpr int U = 8;  // all loads of a batch issued before its re-zero stores
+    const double r2 = 0.70710678118654752440;
+    for (int t0 = threadIdx.x; t0 < nsl * ny; t0 += U * blockDim.x) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u * blockDim.x;
+        v[u] = make_double2(0.0, 0.0);
+        if (t >= nsl * ny) continue;
+        if (a.rho_fx) {
+          const longlong2 q = reinterpret_cast<const longlong2*>(a.rho_fx + base)[t];
+          v[u] = make_double2((double)q.x * 9.094947017729282379150390625e-13,  // 2^-40, exact
+                              (double)q.y * 9.094947017729282379150390625e-13);
+          const long long e0 = q.x - a.rho_t_fx, e1 = q.y - a.rho_t_fx;
+          excess += (e0 > 0 ? e0 : 0) + (e1 > 0 ? e1 : 0);
+        } else {
+          v[u] = reinterpret_cast<const double2*>(a.rho_d + base)[t];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u * blockDim.x;
+        if (t >= nsl * ny) continue;
+        if (a.zero_fx) reinterpret_cast<longlong2*>(a.zero_fx + base)[t] = make_longlong2(0, 0);
+        const int sl = t >> LY, iy = t & (ny - 1);
+        buf[sl * F::LS + F::pad(dct_slot<LY>(iy))] =
+            make_double2(v[u].x + v[u].y, (v[u].x - v[u].y) * r2);  // DCT-II along z (nz = 2)
+      }
     }
-    slab[t] = v;
-  }
-  __syncthreads();
-  if (nz > 1) z_direct(T_DCT2, slab, ny, nz, tmp);
-  // y lines: line iz, element iy at slab[iy*nz + iz]
-  pre_lines(T_DCT2, slab, 1, nz, nz, a.logy, a.phy, cA);
-  __syncthreads();
-  const double2* res = fft_stockham(cA, cB, nz, a.logy, tw, false);
-  post_lines(T_DCT2, res, nz, a.logy, a.phy, slab, 1, nz);
-  __syncthreads();
-  for (int t = threadIdx.x; t < S; t += blockDim.x) a.X[base + t] = slab[t];
-  if (a.ovfl_out) {
-    long long e = warp_sum_ll(excess);
-    __shared__ long long ws[kThreads / 32];
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = e;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      long long b = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += ws[w];
-      reinterpret_cast<long long*>(a.partials)[blockIdx.x] = b;
+    fft_lines<LY, false>(buf, nf, tw);
+    for (int t = threadIdx.x; t < nf << LY; t += blockDim.x) {
+      const int sl = t >> LY, k = t & (ny - 1);
+      reinterpret_cast<double2*>(a.X + base)[t] = dct2_post<LY>(buf + sl * F::LS, k, a.phy);
     }
-    if (last_block(a.counter)) {
-      const long long s = block_sum_ll_partials(
-          reinterpret_cast<const volatile long long*>(a.partials), gridDim.x);
-      if (threadIdx.x == 0) *a.ovfl_out = (double)s * a.ovfl_scale;
+  } else {
+    double* stage = reinterpret_cast<double*>(buf + a.sa * nfs * F::LS);  // [sa][S]
+    for (int t = threadIdx.x; t < nsl * S; t += blockDim.x) {
+      double v;
+      if (a.rho_fx) {
+        const long long q = a.rho_fx[base + t];
+        v = (double)q * 9.094947017729282379150390625e-13;
+        const long long e = q - a.rho_t_fx;
+        excess += e > 0 ? e : 0;
+        if (a.zero_fx) a.zero_fx[base + t] = 0;
+      } else {
+        v = a.rho_d[base + t];
+      }
+      stage[t] = v;
     }
+    __syncthreads();
+    if (nz > 1) z_direct(T_DCT2, stage, nsl * ny, nz, 0, 1, nullptr, reinterpret_cast<double*>(buf));
+    // y lines: (slab s, z pair p) -> lines iz = 2p (re), 2p + 1 (im)
+    for (int t = threadIdx.x; t < nf << LY; t += blockDim.x) {
+      const int f = t >> LY, n = t & (ny - 1);
+      const int sl = f / nfs, p = f - sl * nfs;
+      const double* row = stage + sl * S + n * nz + 2 * p;
+      const double xa = row[0], xb = (2 * p + 1 < nz) ? row[1] : 0.0;
+      buf[f * F::LS + F::pad(dct_slot<LY>(n))] = make_double2(xa, xb);
+    }
+    __syncthreads();
+    fft_lines<LY, false>(buf, nf, tw);
+    for (int t = threadIdx.x; t < nf << LY; t += blockDim.x) {
+      const int f = t >> LY, k = t & (ny - 1);
+      const int sl = f / nfs, p = f - sl * nfs;
+      const double2 r = dct2_post<LY>(buf + f * F::LS, k, a.phy);
+      double* row = stage + sl * S + k * nz + 2 * p;
+      row[0] = r.x;
+      if (2 * p + 1 < nz) row[1] = r.y;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nsl * S; t += blockDim.x) a.X[base + t] = stage[t];
   }
+  ovfl_epilogue(a, excess);
 }
 
-// spectral coefficient of output map m at mode (j, k, l) (see p3d_spectral.cu)
-__device__ __forceinline__ double coef_factor(const FastArgs& a, int j, int k, int l, int map) {
-  const double ox = a.omx[j], oy = a.omy[k], oz = a.omz[l];
-  const double lam = ox * ox + oy * oy + oz * oz;
-  const double inv = lam > 0.0 ? 1.0 / lam : 0.0;
-  double s = (j ? 2.0 : 1.0) / a.nx * ((k ? 2.0 : 1.0) / a.ny) * ((l ? 2.0 : 1.0) / a.nz) * inv;
-  if (map == 1) s *= ox;
-  else if (map == 2) s *= oy;
-  else if (map == 3) s *= oz;
-  return s * a.in_scale;
-}
-
-// ---- B: one x-column per CTA: DCT-II, then the 4 outputs' coefficient
-// scaling + inverse transforms as one batched FFT of 4 lines.
+// ---- B: kColsB adjacent columns per CTA: DCT-II along x, coefficient
+// scaling, and the 4 outputs' inverse transforms along x (4 kColsB real lines
+// in 2 kColsB complex FFTs)
+template <int LX>
 __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
+  using F = Fft<LX>;
   if (a.halt && *a.halt) return;
-  extern __shared__ double sm[];
-  const int nx = a.nx, S = a.ny * a.nz, lg = a.logx;
-  const int col = blockIdx.x, ky = col / a.nz, kz = col - ky * a.nz;
-  double* X = sm;                                              // [nx]
-  double* R = X + nx;                                          // [4][nx]
-  double2* cA = reinterpret_cast<double2*>(R + 4 * nx);       // [4][nx]
-  double2* cB = cA + 4 * nx;                                   // [4][nx]
-  double2* tw = cB + 4 * nx;                                   // [nx/2]
-  stage_twiddles(a.twx, nx, tw);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  constexpr int CB = kColsB;
+  const int nx = F::N, S = a.ny * a.nz, c0 = blockIdx.x * CB;
+  const double2* tw = pass_twiddles(a.twx, nx);
+  double2* buf = reinterpret_cast<double2*>(smraw);            // [2 CB][LS]
+  double* Xs = reinterpret_cast<double*>(buf + 2 * CB * F::LS);  // [CB][nx]
+  double* om = Xs + CB * nx;                                    // [nx]
+  for (int t = threadIdx.x; t < nx; t += blockDim.x) om[t] = a.omx[t];
   const double* src = a.coef_in ? a.coef_in : a.X;
-  for (int ix = threadIdx.x; ix < nx; ix += blockDim.x) X[ix] = src[(long long)ix * S + col];
+  for (int t = threadIdx.x; t < CB * nx; t += blockDim.x) {
+    const int ix = t / CB, c = t % CB;
+    Xs[c * nx + ix] = src[(long long)ix * S + c0 + c];
+  }
   __syncthreads();
   if (!a.coef_in) {
-    pre_lines(T_DCT2, X, nx, 1, 1, lg, a.phx, cA);
+    for (int t = threadIdx.x; t < (CB / 2) * nx; t += blockDim.x) {
+      const int f = t >> LX, n = t & (nx - 1);
+      buf[f * F::LS + F::pad(dct_slot<LX>(n))] =
+          make_double2(Xs[(2 * f) * nx + n], Xs[(2 * f + 1) * nx + n]);
+    }
     __syncthreads();
-    const double2* res = fft_stockham(cA, cB, 1, lg, tw, false);
-    post_lines(T_DCT2, res, 1, lg, a.phx, X, nx, 1);
+    fft_lines<LX, false>(buf, CB / 2, tw);
+    for (int t = threadIdx.x; t < (CB / 2) * nx; t += blockDim.x) {
+      const int f = t >> LX, k = t & (nx - 1);
+      const double2 r = dct2_post<LX>(buf + f * F::LS, k, a.phx);
+      Xs[(2 * f) * nx + k] = r.x;
+      Xs[(2 * f + 1) * nx + k] = r.y;
+    }
     __syncthreads();
     if (a.coef_out)
-      for (int ix = threadIdx.x; ix < nx; ix += blockDim.x)
-        a.coef_out[(long long)ix * S + col] = 8.0 * X[ix];
+      for (int t = threadIdx.x; t < CB * nx; t += blockDim.x) {
+        const int ix = t / CB, c = t % CB;
+        a.coef_out[(long long)ix * S + c0 + c] = 8.0 * Xs[c * nx + ix];
+      }
   }
   if (!a.maps) return;
-  for (int t = threadIdx.x; t < 4 << lg; t += blockDim.x) {
-    const int map = t >> lg, k = t & (nx - 1), kn = (nx - k) & (nx - 1);
-    const double fk = coef_factor(a, k, ky, kz, map), fn = coef_factor(a, kn, ky, kz, map);
-    double ck, cn;
-    if (map != 1) { ck = X[k] * fk; cn = k ? X[kn] * fn : 0.0; }   // cosine series (phi, Ey, Ez)
-    else { ck = k ? X[kn] * fn : 0.0; cn = k ? X[k] * fk : 0.0; }  // sine series (Ex)
-    double2 v;
-    int pos;
-    pre_elem(T_COS, k, nx, 0.0, ck, cn, a.phx, v, pos);
-    cA[(map << lg) + pos] = v;
+  // A = X (w_j/nx)(w_k/ny)(w_l/nz) / lambda  (DC mode: 0)
+  for (int t = threadIdx.x; t < CB * nx; t += blockDim.x) {
+    const int c = t >> LX, j = t & (nx - 1);
+    const int col = c0 + c, ky = col / a.nz, kz = col - ky * a.nz;
+    const double ox = om[j], oy = a.omy[ky], oz = a.omz[kz];
+    const double lam = ox * ox + oy * oy + oz * oz;
+    const double inv = lam > 0.0 ? 1.0 / lam : 0.0;
+    const double sc = (j ? 2.0 : 1.0) / a.nx * ((ky ? 2.0 : 1.0) / a.ny) * ((kz ? 2.0 : 1.0) / a.nz) * inv;
+    Xs[t] *= sc * a.in_scale;
   }
   __syncthreads();
-  const double2* res = fft_stockham(cA, cB, 4, lg, tw, true);
-  for (int t = threadIdx.x; t < 4 << lg; t += blockDim.x) {
-    const int map = t >> lg, m = t & (nx - 1);
-    R[t] = post_elem(map == 1 ? T_SIN : T_COS, res + (map << lg), m, nx, a.phx);
+  // complex line f = 2c + h: h = 0 -> (phi: cos, Ex: sin of A*omega_x), h = 1 -> (Ey, Ez: cos)
+  for (int t = threadIdx.x; t < 2 * CB * nx; t += blockDim.x) {
+    const int f = t >> LX, n = t & (nx - 1), c = f >> 1, h = f & 1;
+    const int nn = (nx - n) & (nx - 1);
+    const double an = Xs[c * nx + n], am = Xs[c * nx + nn];
+    double2 va, vb;
+    if (!h) {
+      va = inv_pre(T_COS, n, nx, an, am, a.phx);
+      vb = inv_pre(T_SIN, n, nx, an * om[n], am * om[nn], a.phx);
+    } else {
+      const int col = c0 + c, ky = col / a.nz, kz = col - ky * a.nz;
+      const double my = a.omy[ky], mz = a.omz[kz];
+      va = inv_pre(T_COS, n, nx, an * my, am * my, a.phx);
+      vb = inv_pre(T_COS, n, nx, an * mz, am * mz, a.phx);
+    }
+    buf[f * F::LS + F::pad(n)] = make_double2(va.x - vb.y, va.y + vb.x);
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < 4 * nx; t += blockDim.x) {  // 32-byte record per row
-    const int ix = t >> 2, map = t & 3;
-    a.M[((long long)ix * S + col) * 4 + map] = R[(map << lg) + ix];
+  fft_lines<LX, true>(buf, 2 * CB, tw);
+  for (int t = threadIdx.x; t < 4 * CB * nx; t += blockDim.x) {  // contiguous row segments
+    const int map = t & 3, c = (t >> 2) % CB, ix = t / (4 * CB);
+    const double2 z = inv_post<LX>(buf + (2 * c + (map >> 1)) * F::LS, ix);
+    double v = (map & 1) ? z.y : z.x;
+    if (map == 1 && (ix & 1)) v = -v;  // sine series
+    a.M[((long long)ix * S + c0 + c) * 4 + map] = v;
   }
 }
 
-// ---- C: inverse along y then z for the 4 maps of one x-slab -> [B][4]
-// (two FFT batches of 2*nz lines)
+// ---- C: inverse along y then z for the 4 maps of one x-slab -> [B][4].
+// nz == 2: complex line f = map packs (iz = 0, iz = 1); the inputs are read
+// straight from the interleaved intermediate and the z transform is fused into
+// the output write.  Other nz stage the slab and loop over rounds of lines.
+template <int LY, bool NZ2>
 __global__ void __launch_bounds__(kThreads) spec_inv_yz(FastArgs a) {
+  using F = Fft<LY>;
   if (a.halt && *a.halt) return;
-  extern __shared__ double sm[];
-  const int ny = a.ny, nz = a.nz, S = ny * nz, SP = S + 1, lg = a.logy;
-  double* slab = sm;                                          // [4][S+1] (padded)
-  double* tmp = slab + 4 * SP;                                // [S]
-  double2* cA = reinterpret_cast<double2*>(tmp + S);          // [2 nz][ny]
-  double2* cB = cA + 2 * S;                                   // [2 nz][ny]
-  double2* tw = cB + 2 * S;                                   // [ny/2]
-  stage_twiddles(a.twy, ny, tw);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int ny = F::N, nz = a.nz, S = ny * nz, SP = S + 1;
+  const double2* tw = pass_twiddles(a.twy, ny);
+  double2* buf = reinterpret_cast<double2*>(smraw);  // [kFftRoundC][LS] (>= S doubles)
   const long long base = (long long)blockIdx.x * S;
+  if (NZ2) {
+    const double* Mb = a.M + base * 4;  // [iy][iz][map]
+    for (int t = threadIdx.x; t < 4 << LY; t += blockDim.x) {
+      const int f = t & 3, n = t >> 2, nn = (ny - n) & (ny - 1);
+      const int op = f == 2 ? T_SIN : T_COS;  // Ey: sine series along y
+      const double2 va = inv_pre(op, n, ny, Mb[n * 8 + f], Mb[nn * 8 + f], a.phy);
+      const double2 vb = inv_pre(op, n, ny, Mb[n * 8 + 4 + f], Mb[nn * 8 + 4 + f], a.phy);
+      buf[f * F::LS + F::pad(n)] = make_double2(va.x - vb.y, va.y + vb.x);
+    }
+    __syncthreads();
+    fft_lines<LY, true>(buf, 4, tw);
+    const double r2 = 0.70710678118654752440;
+    double* out = a.maps + base * 4;
+    for (int t = threadIdx.x; t < 4 << LY; t += blockDim.x) {
+      const int map = t & 3, m = t >> 2;
+      double2 z = inv_post<LY>(buf + map * F::LS, m);
+      if (map == 2 && (m & 1)) z = make_double2(-z.x, -z.y);
+      double y0, y1;
+      if (map == 3) { y0 = z.y * r2; y1 = y0; }  // sine series along z (Ez)
+      else { y0 = z.x + z.y * r2; y1 = z.x - z.y * r2; }
+      out[m * 8 + map] = y0;
+      out[m * 8 + 4 + map] = y1;
+    }
+    return;
+  }
+  double* slab = reinterpret_cast<double*>(buf + max(kFftRoundC * F::LS, (S + 1) / 2));  // [4][S+1]
   for (int t = threadIdx.x; t < 4 * S; t += blockDim.x)  // contiguous interleaved slab
     slab[(t & 3) * SP + (t >> 2)] = a.M[base * 4 + t];
   __syncthreads();
-  for (int half = 0; half < 2; ++half) {
-    // line L = mm * nz + iz (mm = 0, 1 -> map 2*half + mm), element iy at slab[map][iy*nz + iz]
-    for (int t = threadIdx.x; t < (2 * nz) << lg; t += blockDim.x) {
-      const int L = t >> lg, k = t & (ny - 1);
-      const int mm = L / nz, iz = L - mm * nz, map = 2 * half + mm;
-      const double* line = slab + map * SP + iz;
-      const int kn = (ny - k) & (ny - 1);
-      double ck, cn;
-      if (map != 2) { ck = line[k * nz]; cn = k ? line[kn * nz] : 0.0; }  // cosine (phi, Ex, Ez)
-      else { ck = k ? line[kn * nz] : 0.0; cn = k ? line[k * nz] : 0.0; }  // sine (Ey)
-      double2 v;
-      int pos;
-      pre_elem(T_COS, k, ny, 0.0, ck, cn, a.phy, v, pos);
-      cA[(L << lg) + pos] = v;
+  // real line L = map * nz + iz (element iy at slab[map][iy*nz + iz]); complex f = (2f, 2f+1)
+  const int nfc = 2 * nz;
+  for (int f0 = 0; f0 < nfc; f0 += kFftRoundC) {
+    const int nf = min(kFftRoundC, nfc - f0);
+    for (int t = threadIdx.x; t < nf << LY; t += blockDim.x) {
+      const int fl = t >> LY, n = t & (ny - 1), nn = (ny - n) & (ny - 1);
+      double2 v[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int Lr = 2 * (f0 + fl) + h, map = Lr / nz, iz = Lr - map * nz;
+        const double* line = slab + map * SP + iz;
+        v[h] = inv_pre(map == 2 ? T_SIN : T_COS, n, ny, line[n * nz], line[nn * nz], a.phy);
+      }
+      buf[fl * F::LS + F::pad(n)] = make_double2(v[0].x - v[1].y, v[0].y + v[1].x);
     }
     __syncthreads();
-    const double2* res = fft_stockham(cA, cB, 2 * nz, lg, tw, true);
-    for (int t = threadIdx.x; t < (2 * nz) << lg; t += blockDim.x) {
-      const int L = t >> lg, m = t & (ny - 1);
-      const int mm = L / nz, iz = L - mm * nz, map = 2 * half + mm;
-      slab[map * SP + m * nz + iz] =
-          post_elem(map == 2 ? T_SIN : T_COS, res + (L << lg), m, ny, a.phy);
+    fft_lines<LY, true>(buf, nf, tw);
+    for (int t = threadIdx.x; t < nf << LY; t += blockDim.x) {
+      const int fl = t >> LY, m = t & (ny - 1);
+      const double2 z = inv_post<LY>(buf + fl * F::LS, m);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int Lr = 2 * (f0 + fl) + h, map = Lr / nz, iz = Lr - map * nz;
+        double v = h ? z.y : z.x;
+        if (map == 2 && (m & 1)) v = -v;  // sine series along y (Ey)
+        slab[map * SP + m * nz + iz] = v;
+      }
     }
     __syncthreads();
   }
-  for (int map = 0; map < 4; ++map)
-    z_direct(map == 3 ? T_SIN : T_COS, slab + map * SP, ny, nz, tmp);
+  if (nz == 1) {
+    const int ops[4] = {T_COS, T_COS, T_COS, T_SIN};
+    z_direct(T_COS, slab, ny, nz, SP, 4, ops, nullptr);
+  } else {
+    for (int map = 0; map < 4; ++map)
+      z_direct(map == 3 ? T_SIN : T_COS, slab + map * SP, ny, nz, 0, 1, nullptr,
+               reinterpret_cast<double*>(buf));
+  }
   for (int t = threadIdx.x; t < 4 * S; t += blockDim.x)
     a.maps[base * 4 + t] = slab[(t & 3) * SP + (t >> 2)];
 }
@@ -376,32 +576,81 @@ int ilog2_pow2(int n) {
 }
 
 constexpr size_t kSmemMax = 220 * 1024;  // opt-in limit is 227 KB minus static smem
-size_t smem_a(const p3d_grid* g) {
-  const size_t S = (size_t)g->ny * g->nz;
-  return (2 * S + 4 * S + g->ny) * sizeof(double);
+
+size_t line_stride(int L) { return (size_t)(1 << L) + ((size_t)(1 << L) >> 3) + 2; }
+
+size_t smem_a(const p3d_grid* g, int sa) {
+  const int L = ilog2_pow2(g->ny);
+  const size_t S = (size_t)g->ny * g->nz, nfs = (g->nz + 1) / 2;
+  return sa * nfs * line_stride(L) * 16 + (g->nz == 2 ? 0 : sa * S * 8);
 }
-size_t smem_b(const p3d_grid* g) { return ((size_t)g->nx * (1 + 4 + 16) + g->nx) * sizeof(double); }
+size_t smem_b(const p3d_grid* g) {
+  const int L = ilog2_pow2(g->nx);
+  return 2 * kColsB * line_stride(L) * 16 + (size_t)(kColsB + 1) * g->nx * 8;
+}
 size_t smem_c(const p3d_grid* g) {
+  const int L = ilog2_pow2(g->ny);
   const size_t S = (size_t)g->ny * g->nz;
-  return (4 * (S + 1) + S + 8 * S + g->ny) * sizeof(double);
+  if (g->nz == 2) return 4 * line_stride(L) * 16;
+  const size_t bufc = kFftRoundC * line_stride(L) > (S + 1) / 2 ? kFftRoundC * line_stride(L) : (S + 1) / 2;
+  return bufc * 16 + 4 * (S + 1) * 8;
 }
+// slabs per CTA in A: at least 64 butterflies per FFT pass
+int slabs_a(const p3d_grid* g) {
+  const int nfs = (g->nz + 1) / 2;
+  int sa = 64 / (nfs * (g->ny / 8));
+  sa = sa < 1 ? 1 : (sa > g->nx ? g->nx : sa);
+  while (sa > 1 && smem_a(g, sa) > kSmemMax) --sa;
+  return sa;
+}
+int threads_a(const p3d_grid* g, int sa) {
+  int t = sa * ((g->nz + 1) / 2) * (g->ny / 8);
+  t = (t + 31) / 32 * 32;
+  return t < 64 ? 64 : (t > kThreads ? kThreads : t);
+}
+int threads_c(const p3d_grid* g) {
+  int t = (g->nz == 2 ? 4 : kFftRoundC) * (g->ny / 8);
+  t = (t + 31) / 32 * 32;
+  return t < 64 ? 64 : (t > kThreads ? kThreads : t);
+}
+
+template <int L>
+void set_smem_attrs() {
+  cudaFuncSetAttribute(spec_fwd_yz<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+  cudaFuncSetAttribute(spec_fwd_yz<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+  cudaFuncSetAttribute(spec_x<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+  cudaFuncSetAttribute(spec_inv_yz<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+  cudaFuncSetAttribute(spec_inv_yz<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+}
+
+#define P3D_SPEC_SWITCH(L, EXPR)     \
+  switch (L) {                       \
+    case 3: { constexpr int LL = 3; EXPR; } break;   \
+    case 4: { constexpr int LL = 4; EXPR; } break;   \
+    case 5: { constexpr int LL = 5; EXPR; } break;   \
+    case 6: { constexpr int LL = 6; EXPR; } break;   \
+    case 7: { constexpr int LL = 7; EXPR; } break;   \
+    case 8: { constexpr int LL = 8; EXPR; } break;   \
+    case 9: { constexpr int LL = 9; EXPR; } break;   \
+    case 10: { constexpr int LL = 10; EXPR; } break; \
+    default: break;                  \
+  }
 
 }  // namespace
 
 bool spectral_fast_ok(const p3d_grid* g) {
   const int lx = ilog2_pow2(g->nx), ly = ilog2_pow2(g->ny);
-  return lx >= 3 && ly >= 3 && g->nz >= 1 && g->nz <= kMaxNz && smem_a(g) <= kSmemMax &&
-         smem_b(g) <= kSmemMax && smem_c(g) <= kSmemMax;
+  return lx >= 3 && lx <= 10 && ly >= 3 && ly <= 10 && g->nz >= 1 && g->nz <= kMaxNz &&
+         smem_a(g, 1) <= kSmemMax && smem_b(g) <= kSmemMax && smem_c(g) <= kSmemMax;
 }
 
 void spectral_fast_setup() {
   static bool done = false;
   if (done) return;
-  if (cudaFuncSetAttribute(spec_fwd_yz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax) ||
-      cudaFuncSetAttribute(spec_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax) ||
-      cudaFuncSetAttribute(spec_inv_yz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax)) {
+  set_smem_attrs<3>(); set_smem_attrs<4>(); set_smem_attrs<5>(); set_smem_attrs<6>();
+  set_smem_attrs<7>(); set_smem_attrs<8>(); set_smem_attrs<9>(); set_smem_attrs<10>();
+  if (cudaGetLastError() != cudaSuccess) {
     set_error("spectral: cannot opt into %zu bytes of shared memory", kSmemMax);
-    cudaGetLastError();
     return;
   }
   done = true;
@@ -416,6 +665,7 @@ int launch_spectral_fast(const p3d_grid* g, const double* rho, const int64_t* rh
   a.nx = g->nx; a.ny = g->ny; a.nz = g->nz;
   a.logx = ilog2_pow2(g->nx);
   a.logy = ilog2_pow2(g->ny);
+  a.sa = slabs_a(g);
   a.omx = g->omega[0]; a.omy = g->omega[1]; a.omz = g->omega[2];
   a.twx = g->twiddle[0]; a.twy = g->twiddle[1];
   a.phx = g->phase[0]; a.phy = g->phase[1];
@@ -436,9 +686,17 @@ int launch_spectral_fast(const p3d_grid* g, const double* rho, const int64_t* rh
     a.ovfl_out = ov->out;
     a.ovfl_scale = ov->scale;
   }
-  if (!coef_in) spec_fwd_yz<<<g->nx, kThreads, smem_a(g), s>>>(a);
-  spec_x<<<(int)S, kThreads, smem_b(g), s>>>(a);
-  if (maps) spec_inv_yz<<<g->nx, kThreads, smem_c(g), s>>>(a);
+  const int ga = (g->nx + a.sa - 1) / a.sa, ta = threads_a(g, a.sa), tc = threads_c(g);
+  const bool nz2 = g->nz == 2;
+  if (!coef_in) {
+    if (nz2) P3D_SPEC_SWITCH(a.logy, (spec_fwd_yz<LL, true><<<ga, ta, smem_a(g, a.sa), s>>>(a)))
+    else P3D_SPEC_SWITCH(a.logy, (spec_fwd_yz<LL, false><<<ga, ta, smem_a(g, a.sa), s>>>(a)))
+  }
+  P3D_SPEC_SWITCH(a.logx, (spec_x<LL><<<(int)(S / kColsB), kThreads, smem_b(g), s>>>(a)));
+  if (maps) {
+    if (nz2) P3D_SPEC_SWITCH(a.logy, (spec_inv_yz<LL, true><<<g->nx, tc, smem_c(g), s>>>(a)))
+    else P3D_SPEC_SWITCH(a.logy, (spec_inv_yz<LL, false><<<g->nx, tc, smem_c(g), s>>>(a)))
+  }
   return check_launch("spectral (fast path)");
 }
 

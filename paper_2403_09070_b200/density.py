@@ -19,18 +19,40 @@ from .model import partition_from_z
 FX_BITS = 40
 
 
+def _pass_twiddles(n):
+    """Per-pass twiddles of the fast path's in-place mixed-radix DIF FFT
+    (p3d_spectral_fast.cu): for each radix-8 pass with span > 1, W_{8 span}^{q j}
+    for q = 1..7, j < span, laid out [pass][q-1][j] as (cos, sin) pairs.  Empty
+    unless n is a power of two in [8, 1024]."""
+    L = int(n).bit_length() - 1
+    if n < 8 or n > 1024 or (1 << L) != n:
+        return np.zeros(0)
+    out = []
+    for s in range(L // 3):
+        ls = L - 3 * (s + 1)
+        if ls <= 0:
+            continue
+        span = 1 << ls
+        q, j = np.meshgrid(np.arange(1, 8), np.arange(span), indexing="ij")
+        ang = -2 * np.pi * (q * j) / (8 * span)
+        out.append(np.stack([np.cos(ang), np.sin(ang)], -1).reshape(-1))
+    return np.concatenate(out) if out else np.zeros(0)
+
+
 def _tables(n, d):
-    """Per-axis device tables: omega, FFT twiddles, DCT phase factors."""
+    """Per-axis device tables: omega, FFT twiddles (the half table e^{-2 pi i j/n},
+    j < n/2, followed by the fast path's per-pass table), DCT phase factors."""
     omega = np.pi * np.arange(n) / d
     j = np.arange(max(n // 2, 1))
     tw = np.empty((len(j), 2))
     tw[:, 0] = np.cos(2 * np.pi * j / n)
     tw[:, 1] = -np.sin(2 * np.pi * j / n)
+    tw = np.concatenate([tw.reshape(-1), _pass_twiddles(n)])
     k = np.arange(n)
     ph = np.empty((n, 2))
     ph[:, 0] = np.cos(np.pi * k / (2 * n))
     ph[:, 1] = np.sin(np.pi * k / (2 * n))
-    return omega, tw.reshape(-1), ph.reshape(-1)
+    return omega, tw, ph.reshape(-1)
 
 
 class DensityGrid:

@@ -246,7 +246,8 @@ def test_spectral_vs_reference(small):
 
 
 @pytest.mark.parametrize("shape", [(8, 8, 8), (16, 12, 4), (12, 10, 6), (5, 7, 3), (128, 64, 2),
-                                   (512, 512, 2), (256, 1024, 2), (32, 16, 16)])
+                                   (512, 512, 2), (256, 1024, 2), (32, 16, 16), (1024, 256, 2),
+                                   (64, 32, 1), (64, 32, 3), (8, 1024, 2), (16, 8, 5), (1024, 1024, 2)])
 def test_spectral_vs_scipy_shapes(shape):
     """FFT path (powers of two) and direct path (others) against scipy.fft."""
     from paper_2403_09070_b200 import density as dn
