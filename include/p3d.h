@@ -202,7 +202,7 @@ typedef struct p3d_gp {
   const uint8_t* f_net_dup;                             /* [n_net] */
   const int32_t* f_pin_inst;                            /* [n_pin] permuted pins */
   const float* f_pin_off;                               /* [n_pin][4] */
-  const int32_t* f_obj_pins;   /* [n_pin] permuted pin index of each owner-sorted slot */
+  const int32_t* f_pin_slot;   /* [n_pin] owner-sorted record slot of each permuted pin */
   p3d_grid grid;
   /* per-object constants */
   const double* pin_off;       /* [n_pin][4] rotated (rx_top, ry_top, rx_bot, ry_bot) */

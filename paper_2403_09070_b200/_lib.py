@@ -13,7 +13,9 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libp3d.so")
+# P3D_LIB_VARIANT=<v> loads libp3d_<v>.so (an A/B build from build.build(variant=...))
+_VARIANT = os.environ.get("P3D_LIB_VARIANT", "")
+LIB_PATH = os.path.join(_HERE, f"libp3d_{_VARIANT}.so" if _VARIANT else "libp3d.so")
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -59,7 +61,7 @@ class Gp(C.Structure):
                 ("nblk_net", I32), ("wl_f32", I32), ("pad1", I32), ("topo", Topology),
                 ("f_n_tasks", I32), ("f_n_generic", I32), ("f_generic_nets", P), ("f_tasks", P), ("f_task_t0", P),
                 ("f_net_base", P), ("f_net_deg", P), ("f_net_stride", P), ("f_net_dup", P),
-                ("f_pin_inst", P), ("f_pin_off", P), ("f_obj_pins", P), ("grid", Grid),
+                ("f_pin_inst", P), ("f_pin_off", P), ("f_pin_slot", P), ("grid", Grid),
                 ("pin_off", P), ("w_top", P), ("h_top", P), ("w_bot", P), ("h_bot", P),
                 ("is_macro", P), ("degree", P), ("fill_w", P), ("fill_h", P), ("fill_z", P),
                 ("macro_ids", P), ("gamma_tab", P),

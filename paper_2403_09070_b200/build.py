@@ -37,8 +37,8 @@ def _headers():
     return max(os.path.getmtime(h) for h in hs)
 
 
-def _compile(src, extra):
-    obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
+def _compile(src, extra, objdir=OBJDIR):
+    obj = os.path.join(objdir, src.replace(".cu", ".o"))
     path = os.path.join(CSRC, src)
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(path), _headers()):
         return obj, None
@@ -51,21 +51,25 @@ def _compile(src, extra):
     return obj, r.stderr
 
 
-def build(verbose=False, extra=()):
-    os.makedirs(OBJDIR, exist_ok=True)
+def build(verbose=False, extra=(), variant=""):
+    """Build libp3d.so; with `variant`, an A/B copy libp3d_<variant>.so built
+    with the `extra` nvcc flags (e.g. -D switches) in its own object dir."""
+    objdir = OBJDIR + (f"_{variant}" if variant else "")
+    lib_path = LIB if not variant else os.path.join(HERE, f"libp3d_{variant}.so")
+    os.makedirs(objdir, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        results = list(ex.map(lambda s: _compile(s, list(extra)), SOURCES))
+        results = list(ex.map(lambda s: _compile(s, list(extra), objdir), SOURCES))
     objs = [o for o, _ in results]
     if verbose:
         for o, log in results:
             if log:
                 print(o, log)
-    if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [_nvcc(), *ARCH, "-shared", "-o", LIB, *objs]
+    if not os.path.exists(lib_path) or os.path.getmtime(lib_path) < max(os.path.getmtime(o) for o in objs):
+        cmd = [_nvcc(), *ARCH, "-shared", "-o", lib_path, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc link failed:\n{r.stderr}")
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":

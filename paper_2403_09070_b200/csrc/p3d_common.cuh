@@ -75,14 +75,17 @@ __device__ __forceinline__ double block_max(double v, double* smem) {
   return v;
 }
 
-// "Last block done" handshake: every block publishes its partials, then the
-// last block to arrive (by an atomic ticket) sees all of them and runs the
-// grid-level epilogue.  The ticket counter resets itself for graph replay.
+// "Last block done" handshake: every block publishes its partials (written by
+// thread 0, after the block reduction), then the last block to arrive (by an
+// atomic ticket) sees all of them and runs the grid-level epilogue.  Only
+// thread 0 fences (it wrote the partials), so the other warps of a block do
+// not wait for their own outstanding stores.  The ticket counter resets itself
+// for graph replay.
 __device__ __forceinline__ bool last_block(unsigned int* counter) {
   __shared__ bool is_last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     unsigned int t = atomicAdd(counter, 1u);
     is_last = (t == gridDim.x * gridDim.y - 1);
     if (is_last) *counter = 0u;

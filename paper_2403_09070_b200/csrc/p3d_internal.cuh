@@ -79,13 +79,13 @@ struct FusedNetArgs {
   const uint8_t* net_dup;     // [n_net] permuted dup flags
   const int32_t* pin_inst;    // [n_pin] permuted
   const float4* off;          // [n_pin] permuted (rx_top, ry_top, rx_bot, ry_bot)
-  const int32_t* slot;        // unused (kept for layout stability)
+  const int32_t* slot;        // [n_pin] owner-sorted record slot of each permuted pin
   const double4* pos4;        // [n_inst] AoS centres
   double dz2, gamma, scale4, inv_gamma;
   const double* gamma_ptr;
-  float4* out_f;              // [n_pin] (gx, gy, g_cut, FD) in permuted pin order (fp32 mode)
+  float4* out_f;              // [n_pin] (gx, gy, g_cut, FD) records by slot (fp32 mode)
   double* out_fd;             // unused
-  double* out_d;              // nullable: [n_pin][4] float64 records, permuted order (fp64 mode)
+  double* out_d;              // [n_pin][4] float64 records by slot (fp64 mode)
   double* partials;
   unsigned int* counter;
   double* final6;
@@ -95,10 +95,9 @@ struct FusedNetArgs {
 struct FusedGatherArgs {
   int n_obj, blocks;
   const int32_t* obj_slot_ptr;
-  const int32_t* obj_pins;    // [n_pin] permuted pin index of each owner slot
-  const float4* in_f;
+  const float4* in_f;         // fp32-mode records by slot
   const double* in_fd;
-  const double* in_d;         // nullable: exact-mode double4 slots
+  const double* in_d;         // nullable: fp64-mode double4 records by slot
   double* out;                // [4][n_obj]
   double* partials;
   unsigned int* counter;

@@ -477,6 +477,7 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
   na.net_stride = gp.f_net_stride;
   na.net_dup = gp.f_net_dup;
   na.pin_inst = gp.f_pin_inst;
+  na.slot = gp.f_pin_slot;
   na.off = reinterpret_cast<const float4*>(gp.f_pin_off);
   na.pos4 = reinterpret_cast<const double4*>(gp.pos4);
   na.dz2 = gp.grid.dz / 2;
@@ -495,7 +496,6 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
   ga.n_obj = gp.n_inst;
   ga.blocks = grid_blocks(gp.n_inst, 256, kMaxBlocks);
   ga.obj_slot_ptr = gp.topo.obj_slot_ptr;
-  ga.obj_pins = gp.f_obj_pins;
   ga.in_f = reinterpret_cast<const float4*>(gp.pin_out_f);
   ga.in_fd = gp.pin_out_fd;
   ga.in_d = gp.wl_f32 ? nullptr : gp.pin_out;

@@ -231,11 +231,13 @@ __device__ __noinline__ double forced_ext(const FusedNetArgs& a, int base, int d
   return fmax(full, (nt ? thi - tlo : 0.0) + (nb ? bhi - blo : 0.0));
 }
 
+// one output record per pin, written at its owner-sorted slot (the owner
+// gather then streams each object's records contiguously)
 __device__ __forceinline__ void store_pin(const FusedNetArgs& a, int idx, double gx, double gy,
                                           double gc, double gb) {
-  // one record per pin in the coalesced (degree-bucketed) pin order
-  if (a.out_d) reinterpret_cast<double4*>(a.out_d)[idx] = make_double4(gx, gy, gc, gb);
-  else a.out_f[idx] = make_float4((float)gx, (float)gy, (float)gc, (float)gb);
+  const int s = a.slot[idx];
+  if (a.out_d) reinterpret_cast<double4*>(a.out_d)[s] = make_double4(gx, gy, gc, gb);
+  else a.out_f[s] = make_float4((float)gx, (float)gy, (float)gc, (float)gb);
 }
 
 // Dup-owner exact path (wirelength.py:280-292): value for the first pin of
@@ -336,6 +338,13 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
   }
 }
 
+#ifndef P3D_K1_MINB
+#define P3D_K1_MINB 5
+#endif
+#ifndef P3D_TASK_PREFETCH
+#define P3D_TASK_PREFETCH 0
+#endif
+
 constexpr int kMaxStagedDeg = 6;
 constexpr int kWarpsPerBlock = 4;
 
@@ -345,28 +354,21 @@ struct WarpCols {
   using R = typename WaSel<F32>::R;
   double px[kMaxStagedDeg][32], py[kMaxStagedDeg][32];
   double pz[kMaxStagedDeg][32];  // z for the cut phase, then reused as the FD accumulator
+  double gc[kMaxStagedDeg][32];  // z-cut gradient
   R ep[kMaxStagedDeg][32], em[kMaxStagedDeg][32];
 };
 
-// one component of a pin's output record (written piecewise by the phases;
-// the L2 merges the partial sectors of a record before write-back)
-__device__ __forceinline__ void store_comp(const FusedNetArgs& a, int idx, int comp, double v) {
-  if (a.out_d) a.out_d[4 * (long long)idx + comp] = v;
-  else reinterpret_cast<float*>(a.out_f)[4 * (long long)idx + comp] = (float)v;
-}
-
 // One planar axis of a staged net (degree D, fully unrolled: every shared-
 // memory column offset is an immediate): boxes, branch, WA sums of the chosen
-// branch, per-pin gradients, FD extent deltas (accumulated into pz, which
-// holds the FD accumulator by this phase).  Per-pin segment choices are
-// selects of hoisted per-segment constants; the FD delta is evaluated for
-// both dies and selected.
+// branch, per-pin gradients (written over the consumed coordinate column), FD
+// extent deltas (accumulated into pz, which holds the FD accumulator by this
+// phase).  Per-pin segment choices are selects of hoisted per-segment
+// constants; the FD delta is evaluated for both dies and selected.  The
+// second segment is finalised only for split nets.
 template <int D, bool F32>
-__device__ __forceinline__ void staged_axis(const double (&c)[kMaxStagedDeg][32],
-                                            WarpCols<F32>& sm, int lane, int topm,
-                                            typename WaSel<F32>::R ig, double& val,
-                                            double& exact, bool& crossing, const FusedNetArgs& a,
-                                            int pin0, int nb, int comp) {
+__device__ __forceinline__ void staged_axis(double (&c)[kMaxStagedDeg][32], WarpCols<F32>& sm,
+                                            int lane, int topm, typename WaSel<F32>::R ig,
+                                            double& val, double& exact, bool& crossing) {
   using W = typename WaSel<F32>::W;
   using R = typename WaSel<F32>::R;
   Box2 bx;
@@ -397,18 +399,23 @@ __device__ __forceinline__ void staged_axis(const double (&c)[kMaxStagedDeg][32]
     w1.acc(v, h1, l1, ep, em, up ? 1 : 0);
   }
   w0.finalize();
-  w1.finalize();
-  val = split ? (w0.value(h0, l0) + w1.value(h1, l1)) : w0.value(h0, l0);
-  const GradK<R> k0 = w0.gk(h0, l0), k1 = w1.gk(h1, l1);
+  GradK<R> k1 = {};
+  val = w0.value(h0, l0);
+  if (split) {
+    w1.finalize();
+    val += w1.value(h1, l1);
+    k1 = w1.gk(h1, l1);
+  }
+  const GradK<R> k0 = w0.gk(h0, l0);
 #pragma unroll 1
   for (int k = 0; k < D; ++k) {
     const double v = c[k][lane];
     const bool up = (umask >> k) & 1;
     const GradK<R> gk = {up ? k1.rp : k0.rp, up ? k1.rm : k0.rm, up ? k1.vp : k0.vp,
                          up ? k1.vm : k0.vm};
-    store_comp(a, pin0 + k * nb, comp, (double)gk.grad(v, ig, sm.ep[k][lane], sm.em[k][lane]));
     const double fb = flip_delta(bx.b, bx.t, v, full, ex), ft = flip_delta(bx.t, bx.b, v, full, ex);
     sm.pz[k][lane] += ((topm >> k) & 1) ? ft : fb;
+    c[k][lane] = (double)gk.grad(v, ig, sm.ep[k][lane], sm.em[k][lane]);
   }
 }
 
@@ -468,22 +475,93 @@ __device__ __forceinline__ void staged_eval(const FusedNetArgs& a, int pin0, int
   const GradK<R> kz = wz.gk(zhi, zlo);
 #pragma unroll 1
   for (int k = 0; k < D; ++k) {
-    store_comp(a, pin0 + k * nb, 2, (double)kz.grad(sm.pz[k][lane], ig, sm.ep[k][lane], sm.em[k][lane]));
+    sm.gc[k][lane] = (double)kz.grad(sm.pz[k][lane], ig, sm.ep[k][lane], sm.em[k][lane]);
     sm.pz[k][lane] = 0.0;
   }
   double v, ex;
   bool cross;
-  staged_axis<D, F32>(sm.px, sm, lane, topm, ig, v, ex, cross, a, pin0, nb, 0);
+  staged_axis<D, F32>(sm.px, sm, lane, topm, ig, v, ex, cross);
   acc[0] += v;
   acc[3] += ex;
   acc[5] += cross ? 1.0 : 0.0;
-  staged_axis<D, F32>(sm.py, sm, lane, topm, ig, v, ex, cross, a, pin0, nb, 1);
+  staged_axis<D, F32>(sm.py, sm, lane, topm, ig, v, ex, cross);
   acc[1] += v;
   acc[4] += ex;
-#pragma unroll 1
+  int slot[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) slot[k] = a.slot[pin0 + k * nb];
+#pragma unroll
   for (int k = 0; k < D; ++k) {
     const double dwk = sm.pz[k][lane];
-    store_comp(a, pin0 + k * nb, 3, (((topm >> k) & 1) ? -dwk : dwk) * a.scale4);
+    const double gb = (((topm >> k) & 1) ? -dwk : dwk) * a.scale4;
+    if (F32)
+      a.out_f[slot[k]] = make_float4((float)sm.px[k][lane], (float)sm.py[k][lane],
+                                     (float)sm.gc[k][lane], (float)gb);
+    else
+      reinterpret_cast<double4*>(a.out_d)[slot[k]] =
+          make_double4(sm.px[k][lane], sm.py[k][lane], sm.gc[k][lane], gb);
+  }
+}
+
+// Two-pin WA on one axis (wirelength.py:76-98): the anchor pin's terms are
+// exp(0) = 1 and both non-trivial terms share the argument (lo - hi) / gamma,
+// so one exponential serves the segment.  Accumulated exactly like the staged
+// path (pin order), so the results are bit-identical to it.
+template <bool F32>
+__device__ __forceinline__ void pair_axis(double v0, double v1, typename WaSel<F32>::R ig,
+                                          double& val, double& g0, double& g1) {
+  using W = typename WaSel<F32>::W;
+  using R = typename WaSel<F32>::R;
+  const double hi = fmax(v0, v1), lo = fmin(v0, v1);
+  R e, one_p, one_m;
+  W::term(lo, hi, lo, ig, e, one_m);  // e = exp((lo - hi)/g); one_m = exp(0)
+  one_p = one_m;
+  const bool first_hi = v0 >= v1;
+  const R e0p = first_hi ? one_p : e, e1p = first_hi ? e : one_p;
+  const R e0m = first_hi ? e : one_m, e1m = first_hi ? one_m : e;
+  W w;
+  w.init();
+  w.acc(v0, hi, lo, e0p, e0m, 1);
+  w.acc(v1, hi, lo, e1p, e1m, 1);
+  w.finalize();
+  val = w.value(hi, lo);
+  g0 = (double)w.grad(v0, hi, lo, ig, e0p, e0m);
+  g1 = (double)w.grad(v1, hi, lo, ig, e1p, e1m);
+}
+
+// Degree-2 nets (about half of all nets): never split (both partial spans are
+// 0 or the full span) and the FD flip delta is exactly 0 for both pins
+// (wirelength.py:227-248), so a lane evaluates its net from registers.
+template <bool F32>
+__device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, int t0, int lane,
+                                          double (&acc)[6]) {
+  const int nb = tk.y, j = tk.z + lane;
+  if (j >= nb || a.net_dup[t0 + j]) return;  // duplicate-owner nets: generic kernel
+  const int p0 = tk.x + j, p1 = p0 + nb;
+  const int i0 = a.pin_inst[p0], i1 = a.pin_inst[p1];
+  const int s0 = a.slot[p0], s1 = a.slot[p1];
+  const float4 o0 = a.off[p0], o1 = a.off[p1];
+  const double4 q0 = a.pos4[i0], q1 = a.pos4[i1];
+  const int t0p = (q0.z - a.dz2) > 0.0, t1p = (q1.z - a.dz2) > 0.0;
+  const double x0 = q0.x + (double)(t0p ? o0.x : o0.z), y0 = q0.y + (double)(t0p ? o0.y : o0.w);
+  const double x1 = q1.x + (double)(t1p ? o1.x : o1.z), y1 = q1.y + (double)(t1p ? o1.y : o1.w);
+  const typename WaSel<F32>::R ig = (typename WaSel<F32>::R)a.inv_gamma;
+  double vx, vy, vz, gx0, gx1, gy0, gy1, gz0, gz1;
+  pair_axis<F32>(x0, x1, ig, vx, gx0, gx1);
+  pair_axis<F32>(y0, y1, ig, vy, gy0, gy1);
+  pair_axis<F32>(q0.z, q1.z, ig, vz, gz0, gz1);
+  acc[0] += vx;
+  acc[1] += vy;
+  acc[2] += vz;
+  acc[3] += fmax(x0, x1) - fmin(x0, x1);
+  acc[4] += fmax(y0, y1) - fmin(y0, y1);
+  acc[5] += (t0p != t1p) ? 1.0 : 0.0;
+  if (F32) {
+    a.out_f[s0] = make_float4((float)gx0, (float)gy0, (float)gz0, 0.f);
+    a.out_f[s1] = make_float4((float)gx1, (float)gy1, (float)gz1, 0.f);
+  } else {
+    reinterpret_cast<double4*>(a.out_d)[s0] = make_double4(gx0, gy0, gz0, 0.0);
+    reinterpret_cast<double4*>(a.out_d)[s1] = make_double4(gx1, gy1, gz1, 0.0);
   }
 }
 
@@ -497,7 +575,7 @@ __device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk
 }
 
 template <bool F32>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) fused_net_kernel(FusedNetArgs a) {
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_kernel(FusedNetArgs a) {
   if (a.halt && *a.halt) return;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ double red[32 * 6];
@@ -506,11 +584,31 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) fused_net_kernel(Fused
   double acc[6] = {0, 0, 0, 0, 0, 0};
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   WarpCols<F32>& sm = reinterpret_cast<WarpCols<F32>*>(dyn_smem)[wib];
-  for (int w = blockIdx.x * kWarpsPerBlock + wib; w < a.n_tasks; w += gridDim.x * kWarpsPerBlock) {
+  const int wstride = gridDim.x * kWarpsPerBlock;
+#if P3D_TASK_PREFETCH
+  int w = blockIdx.x * kWarpsPerBlock + wib;
+  int4 tkn = w < a.n_tasks ? a.tasks[w] : make_int4(0, 0, 0, 0);
+  int t0n = w < a.n_tasks ? a.task_t0[w] : 0;
+  for (; w < a.n_tasks; w += wstride) {
+    const int4 tk = tkn;  // the next task's descriptor is fetched before this one runs
+    const int t0 = t0n;
+    if (w + wstride < a.n_tasks) {
+      tkn = a.tasks[w + wstride];
+      t0n = a.task_t0[w + wstride];
+    }
+#else
+  for (int w = blockIdx.x * kWarpsPerBlock + wib; w < a.n_tasks; w += wstride) {
     const int4 tk = a.tasks[w];
     const int t0 = a.task_t0[w];
+#endif
+#ifdef P3D_SKIP_D2
+    if (tk.w == 2) continue;
+#endif
+#ifdef P3D_SKIP_DGE3
+    if (tk.w >= 3) continue;
+#endif
     switch (tk.w) {
-      case 2: staged_task<2, F32>(a, tk, t0, sm, lane, acc); break;
+      case 2: pair_task<F32>(a, tk, t0, lane, acc); break;
       case 3: staged_task<3, F32>(a, tk, t0, sm, lane, acc); break;
       case 4: staged_task<4, F32>(a, tk, t0, sm, lane, acc); break;
       case 5: staged_task<5, F32>(a, tk, t0, sm, lane, acc); break;
@@ -552,7 +650,8 @@ __global__ void __launch_bounds__(256) generic_net_kernel(FusedNetArgs a) {
   }
 }
 
-// owner gather of the split outputs: per object, ordered fp64 sums over slots
+// owner gather: per object, ordered fp64 sums over its contiguous slot records
+// (pin order within the owner, like bincount)
 __global__ void __launch_bounds__(256) fused_gather_kernel(FusedGatherArgs a) {
   if (a.halt && *a.halt) return;
   __shared__ double red[32 * 3];
@@ -563,13 +662,15 @@ __global__ void __launch_bounds__(256) fused_gather_kernel(FusedGatherArgs a) {
     const int b = a.obj_slot_ptr[i], e = a.obj_slot_ptr[i + 1];
     if (a.in_d) {
       const double4* in = reinterpret_cast<const double4*>(a.in_d);
+#pragma unroll 4
       for (int s = b; s < e; ++s) {
-        const double4 r = in[a.obj_pins[s]];
+        const double4 r = in[s];
         s0 += r.x; s1 += r.y; s2 += r.z; s3 += r.w;
       }
     } else {
+#pragma unroll 4
       for (int s = b; s < e; ++s) {
-        const float4 r = a.in_f[a.obj_pins[s]];
+        const float4 r = a.in_f[s];
         s0 += (double)r.x; s1 += (double)r.y; s2 += (double)r.z; s3 += (double)r.w;
       }
     }

@@ -16,6 +16,7 @@ from __future__ import annotations
 import ctypes as C
 import logging
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -246,8 +247,10 @@ def fused_pin_layout(net_ptr, pin_inst, off4, dup):
     degree bucket is stored transposed ([pin k][net j]) so a warp owning 32
     nets of a bucket loads pin k of all of them in one transaction.  Returns a
     dict of device-ready arrays: warp tasks, per-permuted-net (base, degree,
-    stride, dup), permuted per-pin (owner, float32 offsets) and, per original
-    pin, its permuted index."""
+    stride, dup), permuted per-pin (owner, float32 offsets, owner-sorted record
+    slot) and, per original pin, its permuted index.  Records are written at
+    their owner-sorted slot (stable: original pin order within an owner, like
+    bincount), so the owner gather streams them."""
     net_ptr = np.asarray(net_ptr, dtype=np.int64)
     deg = np.diff(net_ptr)
     n_net = len(deg)
@@ -287,10 +290,12 @@ def fused_pin_layout(net_ptr, pin_inst, off4, dup):
     f_off[dest] = off32
     # owner-sorted slots (stable: original pin order within an owner, like bincount)
     slot_order = np.argsort(pin_inst, kind="stable")
+    pin_slot = np.empty(len(pin_inst), dtype=np.int64)
+    pin_slot[dest[slot_order]] = np.arange(len(pin_inst))
     return dict(tasks=np.asarray(tasks, dtype=np.int64).reshape(-1, 4),
                 task_t0=np.asarray(t0s, dtype=np.int64), net_base=base, net_deg=dsorted,
                 net_stride=stride, net_dup=np.asarray(dup, bool)[order], pin_inst=f_inst,
-                pin_off=f_off, obj_pins=dest[slot_order], dest=dest,
+                pin_off=f_off, pin_slot=pin_slot, dest=dest,
                 generic=np.asarray(generic, dtype=np.int64))
 
 
@@ -388,8 +393,11 @@ class Gp3dProblem:
         g.f_net_dup = keep(_dev.u8(one(L["net_dup"], bool)))
         g.f_pin_inst = keep(_dev.i32(one(L["pin_inst"], np.int64)))
         g.f_pin_off = keep(_dev.dev(one(L["pin_off"].reshape(-1), np.float32), torch.float32))
-        g.f_obj_pins = keep(_dev.i32(one(L["obj_pins"], np.int64)))
-        g.nblk_net = max(1, min(-(-g.f_n_tasks // 4), K_MAX_BLOCKS))
+        g.f_pin_slot = keep(_dev.i32(one(L["pin_slot"], np.int64)))
+        # K1 runs one wave of persistent CTAs (5 resident 128-thread CTAs per SM)
+        n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        g.nblk_net = max(1, min(-(-g.f_n_tasks // 4), K_MAX_BLOCKS,
+                                int(os.environ.get("P3D_NBLK_NET", 5 * n_sm))))
         gs, gkeep = grid.device()
         g.grid = gs
         self._gkeep = gkeep
