@@ -180,6 +180,7 @@ typedef struct p3d_loop_state {
   double energy, ovfl, value, wl_value, l1_wl, l1_dens;
   double gamma, lam_eval;
   double dv2, dg2, gmax;
+  double dv2_next;             /* |v_new - v|^2 of the last advance (BB numerator) */
   /* GpInfo */
   int32_t iterations, hbt_count;
   double final_overflow, wirelength;
@@ -227,8 +228,10 @@ typedef struct p3d_gp {
   double* inst_g;              /* [4][n_inst] gx, gy, gz_hbt, gz_bist */
   int64_t* rho_fx;             /* [B] */
   /* spatial tile sort of the objects for the privatised scatter (K2) */
-  int32_t ts_n_tiles, ts_tiles_x, ts_tiles_y, ts_pad;
-  int32_t *ts_tile_of, *ts_hist, *ts_start, *ts_cursor, *ts_order;  /* [O], [T], [T+1], [T], [O] */
+  int32_t ts_n_tiles, ts_tiles_x, ts_tiles_y;
+  int32_t ts_margin;           /* bins an object footprint can reach past its centre tile */
+  int32_t *ts_tile_of, *ts_hist, *ts_start, *ts_cursor, *ts_order;  /* [O], [T], [T+1], [T], [O]:
+                                  ts_order = tile of each record, in tile order */
   double* ts_rec;              /* [O][6] charge records (x, y, z, w, h, weight) in tile order */
   double* rho;                 /* [B] */
   double* spec_scratch;        /* [6*B] */
@@ -262,6 +265,10 @@ int p3d_gp_iterate_marked(const p3d_gp* gp, void* stream);
 int p3d_gp_stage_times(float* stage_ms);
 /* Number of kernels one p3d_gp_iterate enqueues (>0), or -1 on bad input. */
 int p3d_gp_kernels_per_iteration(const p3d_gp* gp);
+/* The loop's K2 alone (spatially sorted, shared-memory privatised scatter;
+ * accumulate_density, density.py:301-311) at gp->v: the int64 fixed-point map
+ * is written to out [B] and gp->rho_fx is left zeroed. */
+int p3d_gp_density_fx(const p3d_gp* gp, int64_t* out, void* stream);
 /* Gp3dProblem.project (gp.py:280-294): out = P(in), [3][n_obj]. */
 int p3d_gp_project(const p3d_gp* gp, const double* in, double* out, void* stream);
 

@@ -51,7 +51,7 @@ class LoopState(C.Structure):
                 ("norm_x", D), ("norm_y", D), ("norm_zb", D), ("gz_scale", D),
                 ("energy", D), ("ovfl", D), ("value", D), ("wl_value", D), ("l1_wl", D),
                 ("l1_dens", D), ("gamma", D), ("lam_eval", D), ("dv2", D), ("dg2", D),
-                ("gmax", D), ("iterations", I32), ("hbt_count", I32),
+                ("gmax", D), ("dv2_next", D), ("iterations", I32), ("hbt_count", I32),
                 ("final_overflow", D), ("wirelength", D), ("counters", C.c_uint32 * 16)]
 
 
@@ -71,7 +71,7 @@ class Gp(C.Structure):
                 ("u", P), ("v", P), ("v_prev", P), ("best", P), ("wl_grad", P),
                 ("dens_grad", P), ("pre", P), ("prev_wl", P), ("prev_dens", P), ("prev_q", P),
                 ("pin_out", P), ("pin_out_f", P), ("pin_out_fd", P), ("pos4", P), ("inst_g", P), ("rho_fx", P),
-                ("ts_n_tiles", I32), ("ts_tiles_x", I32), ("ts_tiles_y", I32), ("ts_pad", I32),
+                ("ts_n_tiles", I32), ("ts_tiles_x", I32), ("ts_tiles_y", I32), ("ts_margin", I32),
                 ("ts_tile_of", P), ("ts_hist", P), ("ts_start", P), ("ts_cursor", P),
                 ("ts_order", P), ("ts_rec", P), ("rho", P), ("spec_scratch", P),
                 ("maps", P), ("partials", P), ("st", P), ("log", P), ("ovfl_hist", P)]
@@ -103,6 +103,7 @@ _SIGS = {
     "p3d_gp_iterate": (I32, [P, P]),
     "p3d_gp_evaluate": (I32, [P, D, D, P]),
     "p3d_gp_project": (I32, [P, P, P, P]),
+    "p3d_gp_density_fx": (I32, [P, P, P]),
     "p3d_gp_iterate_profiled": (I32, [P, P, P]),
     "p3d_gp_kernels_per_iteration": (I32, [P]),
     "p3d_gp_iterate_marked": (I32, [P, P]),

@@ -49,6 +49,7 @@ int gp_iterate(const p3d_gp& gp, cudaStream_t s);
 int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s);
 int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s);
 int gp_project(const p3d_gp& gp, const double* in, double* out, cudaStream_t s);
+int gp_density_fx(const p3d_gp& gp, int64_t* out, cudaStream_t s);
 int gp_iterate_profiled(const p3d_gp& gp, cudaStream_t s, float* ms);
 int gp_kernels_per_iteration(const p3d_gp& gp);
 int gp_iterate_marked(const p3d_gp& gp, cudaStream_t s);
@@ -332,6 +333,11 @@ int p3d_gp_kernels_per_iteration(const p3d_gp* gp) {
 int p3d_gp_evaluate(const p3d_gp* gp, double lam, double gamma, void* stream) {
   if (bad_gp(gp)) return P3D_ERR_ARG;
   return gp_evaluate(*gp, lam, gamma, STREAM(stream));
+}
+
+int p3d_gp_density_fx(const p3d_gp* gp, int64_t* out, void* stream) {
+  if (!gp || !out) { set_error("gp_density_fx: null argument"); return P3D_ERR_ARG; }
+  return gp_density_fx(*gp, out, STREAM(stream));
 }
 
 int p3d_gp_project(const p3d_gp* gp, const double* in, double* out, void* stream) {

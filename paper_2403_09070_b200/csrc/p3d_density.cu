@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(256) tile_place_kernel(Cloud cl, int n, TileSo
     const int i = i0 + k * blockDim.x;
     const int pos = base[tile[k]] + rank[k];
     const Charge q = cl.get(i);
+    ts.order[pos] = tile[k];
     double2* r = reinterpret_cast<double2*>(ts.rec) + 3 * (long long)pos;
     r[0] = make_double2(q.x, q.y);
     r[1] = make_double2(q.z, q.w);
@@ -174,12 +175,77 @@ __device__ __forceinline__ Charge rec_charge(const TileSort& ts, int pos, double
   return q;
 }
 
+// One fixed-point term into the CTA's shared-memory window (int64 bins as
+// two u32 halves: 32-bit shared atomics, native ATOMS.ADD, with the carry
+// propagated by the thread that produced it — exact), or straight to the
+// global map when it falls outside the window.
+struct SmemWindow {
+  unsigned int *lo32, *hi32;
+  int X0, Y0, W, H, nz;
+  bool local;
+};
+
+__device__ __forceinline__ void put_term(const SmemWindow& w, const p3d_grid& g,
+                                         unsigned long long* rho, long long t, int ix, int iy,
+                                         int iz) {
+  if (!t) return;
+  const int lx = ix - w.X0, ly = iy - w.Y0;
+  if (w.local && (unsigned)lx < (unsigned)w.W && (unsigned)ly < (unsigned)w.H) {
+    const int b = (lx * w.H + ly) * w.nz + iz;
+    const unsigned int tl = (unsigned int)t, th = (unsigned int)((unsigned long long)t >> 32);
+    const unsigned int old = atomicAdd(&w.lo32[b], tl);
+    const unsigned int hadd = th + (old + tl < old ? 1u : 0u);
+    if (hadd) atomicAdd(&w.hi32[b], hadd);
+  } else {
+    atomicAdd(rho + ((long long)(ix * g.ny + iy) * g.nz + iz), (unsigned long long)t);
+  }
+}
+
+// all terms of one object: per-axis overlap lengths computed once; footprints
+// of at most 3 x 3 x 2 bins fully unrolled (same terms as scatter_object)
+__device__ __forceinline__ void scatter_terms(const Charge& q, const p3d_grid& g,
+                                              const SmemWindow& w, unsigned long long* rho) {
+  const Footprint f = footprint(q, g);
+  const int nxr = f.ax.i1 - f.ax.i0 + 1, nyr = f.ay.i1 - f.ay.i0 + 1, nzr = f.az.i1 - f.az.i0 + 1;
+  if (nxr <= 3 && nyr <= 3 && nzr <= 2) {
+    double wx[3], wy[3], wz[2];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) wx[k] = k < nxr ? overlap_len(f.ax, f.ax.i0 + k, g.wb) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) wy[k] = k < nyr ? overlap_len(f.ay, f.ay.i0 + k, g.hb) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) wz[k] = k < nzr ? overlap_len(f.az, f.az.i0 + k, g.db) : 0.0;
+#pragma unroll
+    for (int x = 0; x < 3; ++x)
+#pragma unroll
+      for (int y = 0; y < 3; ++y) {
+        const double wxy = wx[x] * wy[y];
+#pragma unroll
+        for (int z = 0; z < 2; ++z)
+          if (x < nxr && y < nyr && z < nzr) {
+            const double vol = wxy * wz[z];
+            put_term(w, g, rho, __double2ll_rn((q.weight * vol) * g.fx_scale), f.ax.i0 + x,
+                     f.ay.i0 + y, f.az.i0 + z);
+          }
+      }
+    return;
+  }
+  for (int ix = f.ax.i0; ix <= f.ax.i1; ++ix) {
+    const double wx = overlap_len(f.ax, ix, g.wb);
+    for (int iy = f.ay.i0; iy <= f.ay.i1; ++iy) {
+      const double wxy = wx * overlap_len(f.ay, iy, g.hb);
+      for (int iz = f.az.i0; iz <= f.az.i1; ++iz) {
+        const double vol = wxy * overlap_len(f.az, iz, g.db);
+        put_term(w, g, rho, __double2ll_rn((q.weight * vol) * g.fx_scale), ix, iy, iz);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) scatter_tiled_kernel(p3d_grid g, TileSort ts,
                                                            unsigned long long* rho,
                                                            const int* halt) {
   if (halt && *halt) return;
-  // int64 bins as two u32 halves: 32-bit shared atomics (native ATOMS.ADD) with
-  // the carry propagated by the thread that produced it (exact)
   extern __shared__ unsigned int sbin32[];
   __shared__ int box[4];
   const int total = ts.start[ts.n_tiles];
@@ -187,58 +253,53 @@ __global__ void __launch_bounds__(256) scatter_tiled_kernel(p3d_grid g, TileSort
   if (c0 >= total) return;
   const int c1 = min(total, c0 + kChunk);
   const double dep = g.dz / 2;
-  int bx0 = INT_MAX, bx1 = -1, by0 = INT_MAX, by1 = -1;
-  for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
-    const Footprint f = footprint(rec_charge(ts, k, dep), g);
-    bx0 = min(bx0, f.ax.i0); bx1 = max(bx1, f.ax.i1);
-    by0 = min(by0, f.ay.i0); by1 = max(by1, f.ay.i1);
+  // window: the chunk's tiles (when they share one tile column) widened by the
+  // footprint margin; otherwise the bounding box of the chunk's footprints
+  const int tf = ts.order[c0], tl = ts.order[c1 - 1];
+  SmemWindow w;
+  w.nz = g.nz;
+  if (tf / ts.tiles_y == tl / ts.tiles_y) {
+    const int tx = tf / ts.tiles_y;
+    w.X0 = max(0, tx * kTile - ts.margin);
+    const int X1 = min(g.nx - 1, tx * kTile + kTile - 1 + ts.margin);
+    w.Y0 = max(0, (tf % ts.tiles_y) * kTile - ts.margin);
+    const int Y1 = min(g.ny - 1, (tl % ts.tiles_y) * kTile + kTile - 1 + ts.margin);
+    w.W = X1 - w.X0 + 1;
+    w.H = Y1 - w.Y0 + 1;
+  } else {
+    int bx0 = INT_MAX, bx1 = -1, by0 = INT_MAX, by1 = -1;
+    for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
+      const Footprint f = footprint(rec_charge(ts, k, dep), g);
+      bx0 = min(bx0, f.ax.i0); bx1 = max(bx1, f.ax.i1);
+      by0 = min(by0, f.ay.i0); by1 = max(by1, f.ay.i1);
+    }
+    if (threadIdx.x == 0) { box[0] = INT_MAX; box[1] = -1; box[2] = INT_MAX; box[3] = -1; }
+    __syncthreads();
+    atomicMin(&box[0], bx0); atomicMax(&box[1], bx1);
+    atomicMin(&box[2], by0); atomicMax(&box[3], by1);
+    __syncthreads();
+    w.X0 = box[0];
+    w.Y0 = box[2];
+    w.W = box[1] - box[0] + 1;
+    w.H = box[3] - box[2] + 1;
   }
-  if (threadIdx.x == 0) { box[0] = INT_MAX; box[1] = -1; box[2] = INT_MAX; box[3] = -1; }
-  __syncthreads();
-  atomicMin(&box[0], bx0); atomicMax(&box[1], bx1);
-  atomicMin(&box[2], by0); atomicMax(&box[3], by1);
-  __syncthreads();
-  const int X0 = box[0], Y0 = box[2];
-  const int W = box[1] - X0 + 1, H = box[3] - Y0 + 1, nz = g.nz;
-  const int nbins = W * H * nz;
-  const bool local = (long long)W * H * nz <= kBoxBins;
-  unsigned int* lo32 = sbin32;
-  unsigned int* hi32 = sbin32 + kBoxBins;
-  if (local) {
-    for (int b = threadIdx.x; b < nbins; b += blockDim.x) lo32[b] = hi32[b] = 0u;
+  const int nbins = w.W * w.H * w.nz;
+  w.local = (long long)w.W * w.H * w.nz <= kBoxBins;
+  w.lo32 = sbin32;
+  w.hi32 = sbin32 + kBoxBins;
+  if (w.local) {
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) w.lo32[b] = w.hi32[b] = 0u;
     __syncthreads();
   }
-  for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
-    const Charge q = rec_charge(ts, k, dep);
-    const Footprint f = footprint(q, g);
-    for (int ix = f.ax.i0; ix <= f.ax.i1; ++ix) {
-      const double wx = overlap_len(f.ax, ix, g.wb);
-      for (int iy = f.ay.i0; iy <= f.ay.i1; ++iy) {
-        const double wxy = wx * overlap_len(f.ay, iy, g.hb);
-        for (int iz = f.az.i0; iz <= f.az.i1; ++iz) {
-          const double vol = wxy * overlap_len(f.az, iz, g.db);
-          const long long t = __double2ll_rn((q.weight * vol) * g.fx_scale);
-          if (!t) continue;
-          if (local) {
-            const int b = ((ix - X0) * H + (iy - Y0)) * nz + iz;
-            const unsigned int tl = (unsigned int)t, th = (unsigned int)((unsigned long long)t >> 32);
-            const unsigned int old = atomicAdd(&lo32[b], tl);
-            const unsigned int hadd = th + (old + tl < old ? 1u : 0u);
-            if (hadd) atomicAdd(&hi32[b], hadd);
-          } else {
-            atomicAdd(rho + ((long long)(ix * g.ny + iy) * nz + iz), (unsigned long long)t);
-          }
-        }
-      }
-    }
-  }
-  if (!local) return;
+  for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x)
+    scatter_terms(rec_charge(ts, k, dep), g, w, rho);
+  if (!w.local) return;
   __syncthreads();
   for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
-    const unsigned long long v = ((unsigned long long)hi32[b] << 32) | lo32[b];
+    const unsigned long long v = ((unsigned long long)w.hi32[b] << 32) | w.lo32[b];
     if (!v) continue;
-    const int iz = b % nz, r = b / nz, iy = r % H, ix = r / H;
-    atomicAdd(rho + ((long long)((ix + X0) * g.ny + (iy + Y0)) * nz + iz), v);
+    const int iz = b % w.nz, r = b / w.nz, iy = r % w.H, ix = r / w.H;
+    atomicAdd(rho + ((long long)((ix + w.X0) * g.ny + (iy + w.Y0)) * g.nz + iz), v);
   }
 }
 

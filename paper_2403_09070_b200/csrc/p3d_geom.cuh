@@ -148,11 +148,8 @@ __device__ __forceinline__ void scatter_object_block(const Charge& q, const p3d_
 // ---------------------------------------------------------------------------
 // K4: overlap-weighted means of the 4 interleaved maps (density.py:376-386)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void gather_object(const Charge& q, const p3d_grid& g,
-                                              const double* maps, double (&mean)[4]) {
-  const Footprint f = footprint(q, g);
-  double tot = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  const double4* m4 = reinterpret_cast<const double4*>(maps);
+__device__ __forceinline__ void gather_generic(const Footprint& f, const p3d_grid& g,
+                                               const double4* m4, double& tot, double (&a)[4]) {
   for (int ix = f.ax.i0; ix <= f.ax.i1; ++ix) {
     const double wx = overlap_len(f.ax, ix, g.wb);
     for (int iy = f.ay.i0; iy <= f.ay.i1; ++iy) {
@@ -161,18 +158,66 @@ __device__ __forceinline__ void gather_object(const Charge& q, const p3d_grid& g
         const double vol = wxy * overlap_len(f.az, iz, g.db);
         const double4 m = m4[(long long)(ix * g.ny + iy) * g.nz + iz];
         tot += vol;
-        a0 += m.x * vol;
-        a1 += m.y * vol;
-        a2 += m.z * vol;
-        a3 += m.w * vol;
+        a[0] += m.x * vol;
+        a[1] += m.y * vol;
+        a[2] += m.z * vol;
+        a[3] += m.w * vol;
       }
     }
   }
+}
+
+// Footprints of at most MX x MY x MZ bins (every standard cell and filler of
+// the BASELINE configs): per-axis overlap lengths computed once, the bin loop
+// fully unrolled with guards so all map loads are in flight together.  Same
+// terms, same accumulation order as gather_generic.
+template <int MX, int MY, int MZ>
+__device__ __forceinline__ void gather_small(const Footprint& f, const p3d_grid& g,
+                                             const double4* m4, double& tot, double (&a)[4]) {
+  const int nxr = f.ax.i1 - f.ax.i0 + 1, nyr = f.ay.i1 - f.ay.i0 + 1, nzr = f.az.i1 - f.az.i0 + 1;
+  double wx[MX], wy[MY], wz[MZ];
+#pragma unroll
+  for (int k = 0; k < MX; ++k) wx[k] = k < nxr ? overlap_len(f.ax, f.ax.i0 + k, g.wb) : 0.0;
+#pragma unroll
+  for (int k = 0; k < MY; ++k) wy[k] = k < nyr ? overlap_len(f.ay, f.ay.i0 + k, g.hb) : 0.0;
+#pragma unroll
+  for (int k = 0; k < MZ; ++k) wz[k] = k < nzr ? overlap_len(f.az, f.az.i0 + k, g.db) : 0.0;
+  const long long b0 = (long long)(f.ax.i0 * g.ny + f.ay.i0) * g.nz + f.az.i0;
+#pragma unroll
+  for (int x = 0; x < MX; ++x) {
+#pragma unroll
+    for (int y = 0; y < MY; ++y) {
+      const double wxy = wx[x] * wy[y];
+#pragma unroll
+      for (int z = 0; z < MZ; ++z) {
+        if (x < nxr && y < nyr && z < nzr) {
+          const double vol = wxy * wz[z];
+          const double4 m = m4[b0 + ((long long)x * g.ny + y) * g.nz + z];
+          tot += vol;
+          a[0] += m.x * vol;
+          a[1] += m.y * vol;
+          a[2] += m.z * vol;
+          a[3] += m.w * vol;
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void gather_object(const Charge& q, const p3d_grid& g,
+                                              const double* maps, double (&mean)[4]) {
+  const Footprint f = footprint(q, g);
+  double tot = 0.0, a[4] = {0.0, 0.0, 0.0, 0.0};
+  const double4* m4 = reinterpret_cast<const double4*>(maps);
+  if (f.ax.i1 - f.ax.i0 < 3 && f.ay.i1 - f.ay.i0 < 3 && f.az.i1 - f.az.i0 < 2)
+    gather_small<3, 3, 2>(f, g, m4, tot, a);
+  else
+    gather_generic(f, g, m4, tot, a);
   tot = fmax(tot, 1e-300);
-  mean[0] = a0 / tot;
-  mean[1] = a1 / tot;
-  mean[2] = a2 / tot;
-  mean[3] = a3 / tot;
+  mean[0] = a[0] / tot;
+  mean[1] = a[1] / tot;
+  mean[2] = a[2] / tot;
+  mean[3] = a[3] / tot;
 }
 
 // block-cooperative macro means: sum m*vol over the footprint / unclipped

@@ -20,6 +20,7 @@ enum PartialSlot {
   kSlotDens = 3,     // density gather (energy, |dens|, |wl|)
   kSlotStep = 4,     // preconditioner / BB norms
   kSlotGeneric = 5,  // generic (high-degree) nets
+  kSlotAdv = 6,      // advance: |v_new - v|^2
   kSlotFinal = 15,   // finalised scalars of the sub-kernels
 };
 // offsets inside the final slot
@@ -113,12 +114,12 @@ int grid_blocks(int n, int threads, int cap);
 
 // spatially ordered scatter (p3d_density.cu)
 struct TileSort {
-  int n_tiles, tiles_x, tiles_y, pad;
+  int n_tiles, tiles_x, tiles_y, margin;
   int32_t* tile_of;  // [n_obj]
   int32_t* hist;     // [n_tiles] (kept zeroed between iterations)
   int32_t* start;    // [n_tiles + 1]
   int32_t* cursor;   // [n_tiles]
-  int32_t* order;    // [n_obj] (unused by the record path; kept for debugging)
+  int32_t* order;    // [n_obj] tile of each record, in tile order
   double* rec;       // [n_obj][6] charge records in tile order
 };
 struct CloudGP;

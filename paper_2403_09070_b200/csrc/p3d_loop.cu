@@ -108,6 +108,7 @@ __global__ void init_state_kernel(p3d_gp gp) {
   st->step = 0.0;
   st->prev_ovfl = P3D_INF;
   st->prev_value = P3D_INF;
+  st->dv2_next = 0.0;
   st->last_mu = 1.0;
   st->best0 = P3D_INF;
   st->best1 = P3D_INF;
@@ -151,24 +152,33 @@ __device__ __forceinline__ double precond_div(double lam, double q, double mdeg)
   return fmax(d, 1.0);
 }
 
-// acc: energy, |dens|_1, |wl|_1, non-finite count, |dv|^2, |dg|^2
-__device__ __forceinline__ void finish_object(const p3d_gp& gp, int i, const Charge& q, const double (&mean)[4],
-                              double (&acc)[6]) {
+// per-launch scalars of K4 (the loop state changes only in the last block,
+// after every object has been processed)
+struct DensScal {
+  double lam, zscale;
+  bool eval_only, bb;
+};
+
+// acc: energy, |dens|_1, |wl|_1, non-finite count, (unused), |dg|^2
+// wl4 = the object's owner sums (gx, gy, g_cut, FD), pw/pd/pq its previous raw
+// gradients and charge: loaded by the caller before the map gathers so their
+// latency overlaps them.
+__device__ __forceinline__ void finish_object(const p3d_gp& gp, int i, const Charge& q,
+                                              const double (&mean)[4], const DensScal& sc,
+                                              const double (&wl4)[4], const double (&pw)[3],
+                                              const double (&pd)[3], double pq, double mdeg,
+                                              double (&acc)[6]) {
   const int O = gp.n_obj, I = gp.n_inst;
   const double qq = charge_of(q);
   const double c = -2.0 * qq;
   double dg[3] = {mean[1] * c, mean[2] * c, i < I ? mean[3] * c : 0.0};  // filler z frozen
   double wl[3] = {0.0, 0.0, 0.0};
   if (i < I) {
-    const double* f = fin(gp);
-    wl[0] = gp.inst_g[i];
-    wl[1] = gp.inst_g[I + i];
-    const double gzh = gp.inst_g[2 * I + i], gzb = gp.inst_g[3 * I + i];
-    const double base = f[kFinNorm + 2] == 0.0 ? 0.0 : f[kFinNorm + 3] * gzb;
-    wl[2] = base + gp.alpha * gzh;  // wirelength.py:296-305
+    wl[0] = wl4[0];
+    wl[1] = wl4[1];
+    wl[2] = sc.zscale * wl4[3] + gp.alpha * wl4[2];  // wirelength.py:296-305
   }
-  const p3d_loop_state* st = gp.st;
-  const double lam = st->lam_eval;
+  const double lam = sc.lam;
   bool finite = true;
 #pragma unroll
   for (int k = 0; k < 3; ++k) finite = finite && isfinite(wl[k] + lam * dg[k]);
@@ -176,7 +186,7 @@ __device__ __forceinline__ void finish_object(const p3d_gp& gp, int i, const Cha
   acc[1] += fabs(dg[0]) + fabs(dg[1]) + fabs(dg[2]);
   acc[2] += fabs(wl[0]) + fabs(wl[1]) + fabs(wl[2]);
   acc[3] += finite ? 0.0 : 1.0;
-  if (st->eval_only) {
+  if (sc.eval_only) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       gp.wl_grad[(long long)k * O + i] = wl[k];
@@ -184,19 +194,17 @@ __device__ __forceinline__ void finish_object(const p3d_gp& gp, int i, const Cha
     }
     return;
   }
-  // BB norms need the previous iteration's raw gradients re-weighted by the
+  // BB denominator: the previous iteration's raw gradients re-weighted by the
   // current lambda (gp.py:427-435); at iteration 0 there is no previous point.
-  if (st->step_set) {
-    const double mdeg = (i < I && gp.is_macro[i]) ? gp.degree[i] : 0.0;
+  // (The numerator |v - v_prev|^2 comes from the last advance.)
+  if (sc.bb) {
     const double div = precond_div(lam, qq, mdeg);
-    const double divp = precond_div(lam, gp.prev_q[i], mdeg);
+    const double divp = precond_div(lam, pq, mdeg);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const long long j = (long long)k * O + i;
       const double pre = (wl[k] + lam * dg[k]) / div;
-      const double pp = (gp.prev_wl[j] + lam * gp.prev_dens[j]) / divp;
-      const double d = pre - pp, dv = gp.v[j] - gp.v_prev[j];
-      acc[4] += dv * dv;
+      const double pp = (pw[k] + lam * pd[k]) / divp;
+      const double d = pre - pp;
       acc[5] += d * d;
     }
   }
@@ -206,6 +214,29 @@ __device__ __forceinline__ void finish_object(const p3d_gp& gp, int i, const Cha
     gp.prev_dens[(long long)k * O + i] = dg[k];
   }
   gp.prev_q[i] = qq;
+}
+
+// the caller-side loads of finish_object's inputs
+__device__ __forceinline__ void load_object_inputs(const p3d_gp& gp, int i, const DensScal& sc,
+                                                   double (&wl4)[4], double (&pw)[3],
+                                                   double (&pd)[3], double& pq, double& mdeg) {
+  const int O = gp.n_obj, I = gp.n_inst;
+  wl4[0] = wl4[1] = wl4[2] = wl4[3] = 0.0;
+  if (i < I) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) wl4[k] = gp.inst_g[(long long)k * I + i];
+  }
+  pq = mdeg = 0.0;
+  pw[0] = pw[1] = pw[2] = pd[0] = pd[1] = pd[2] = 0.0;
+  if (sc.bb && !sc.eval_only) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      pw[k] = gp.prev_wl[(long long)k * O + i];
+      pd[k] = gp.prev_dens[(long long)k * O + i];
+    }
+    pq = gp.prev_q[i];
+    mdeg = (i < I && gp.is_macro[i]) ? gp.degree[i] : 0.0;
+  }
 }
 
 // underflow test and momentum of the accepted step (gp.py:218-226)
@@ -296,8 +327,9 @@ __device__ __forceinline__ void control_after_eval(const p3d_gp& gp, double ener
       return;
     }
   }
-  st->dv2 = dv2;
+  st->dv2 = st->dv2_next;  // |v - v_prev|^2, accumulated by the last advance
   st->dg2 = dg2;
+  dv2 = st->dv2;
   if (!st->step_set) return;  // iteration 0: gmax0_kernel sets the initial step
   const double den = sqrt(dg2);  // gp.py:210-217
   if (den > 0) {
@@ -307,9 +339,24 @@ __device__ __forceinline__ void control_after_eval(const p3d_gp& gp, double ener
   step_tail(gp);
 }
 
-__global__ void __launch_bounds__(256, 3) dens_kernel(p3d_gp gp) {
-  if (gp.st->done) return;
+#ifndef P3D_K4_PREFETCH
+#define P3D_K4_PREFETCH 0
+#endif
+#ifndef P3D_K4_MINB
+#define P3D_K4_MINB 4
+#endif
+__global__ void __launch_bounds__(256, P3D_K4_MINB) dens_kernel(p3d_gp gp) {
+  const p3d_loop_state* st = gp.st;
+  if (st->done) return;
   __shared__ double red[32 * 6];
+  DensScal sc;
+  sc.lam = st->lam_eval;
+  sc.eval_only = st->eval_only != 0;
+  sc.bb = st->step_set != 0;
+  {
+    const double* f = fin(gp);
+    sc.zscale = f[kFinNorm + 2] == 0.0 ? 0.0 : f[kFinNorm + 3];  // Eq. 17 (0 if |gz| = 0)
+  }
   const CloudGP cl = cloud_of(gp, gp.v);
   double acc[6] = {0, 0, 0, 0, 0, 0};
   const int nm = gp.n_macro;
@@ -318,15 +365,26 @@ __global__ void __launch_bounds__(256, 3) dens_kernel(p3d_gp gp) {
     const Charge q = cl.get(i);
     double mean[4];
     gather_object_block(q, gp.grid, gp.maps, mean, red);
-    if (threadIdx.x == 0) finish_object(gp, i, q, mean, acc);
+    if (threadIdx.x == 0) {
+      double wl4[4], pw[3], pd[3], pq, mdeg;
+      load_object_inputs(gp, i, sc, wl4, pw, pd, pq, mdeg);
+      finish_object(gp, i, q, mean, sc, wl4, pw, pd, pq, mdeg, acc);
+    }
   } else {
     const int b = blockIdx.x - nm, nb = gridDim.x - nm;
     for (int i = b * blockDim.x + threadIdx.x; i < gp.n_obj; i += nb * blockDim.x) {
       if (cl.is_macro(i)) continue;
+      double wl4[4], pw[3], pd[3], pq, mdeg;
+#if P3D_K4_PREFETCH
+      load_object_inputs(gp, i, sc, wl4, pw, pd, pq, mdeg);
+#endif
       const Charge q = cl.get(i);
       double mean[4];
       gather_object(q, gp.grid, gp.maps, mean);
-      finish_object(gp, i, q, mean, acc);
+#if !P3D_K4_PREFETCH
+      load_object_inputs(gp, i, sc, wl4, pw, pd, pq, mdeg);
+#endif
+      finish_object(gp, i, q, mean, sc, wl4, pw, pd, pq, mdeg, acc);
     }
   }
   double* part = gp.partials + (long long)kSlotDens * kPartialStride;
@@ -380,9 +438,11 @@ __global__ void __launch_bounds__(256) gmax0_kernel(p3d_gp gp) {
 __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
   p3d_loop_state* st = gp.st;
   if (st->done) return;
+  __shared__ double red[32];
   const int O = gp.n_obj, I = gp.n_inst;
   const bool best = st->best_flag != 0, stop = st->stop_now != 0;
   const double step = st->step, mom = st->mom, lam = st->lam;
+  double dv2[1] = {0.0};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < O; i += gridDim.x * blockDim.x) {
     double u[3];
 #pragma unroll
@@ -410,18 +470,24 @@ __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const long long k = (long long)c * O + i;
-      gp.v_prev[k] = v[c];
+      const double d = vn[c] - v[c];  // BB numerator of the next evaluation (gp.py:210)
+      dv2[0] += d * d;
       gp.u[k] = un[c];
       gp.v[k] = vn[c];
     }
     if (i < I) reinterpret_cast<double4*>(gp.pos4)[i] = make_double4(vn[0], vn[1], vn[2], 0.0);
   }
+  double* part = gp.partials + (long long)kSlotAdv * kPartialStride;
+  block_sum<1>(dv2, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = dv2[0];
   if (last_block(&st->counters[kCntAdvance])) {
+    const double tot = ordered_sum(part, gridDim.x, red);
     if (threadIdx.x == 0) {
       if (stop) {
         st->done = 1;
         return;
       }
+      st->dv2_next = tot;
       st->a = st->a_new;
       // mu_from_overflow (gp.py:156-168), lambda update (gp.py:442-444)
       const double drop = st->prev_ovfl - st->ovfl;
@@ -449,6 +515,36 @@ __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
+// K2 of the loop: spatially sorted, shared-memory privatised scatter of the
+// cells / fillers + per-macro tiles, into gp.rho_fx (int64 fixed point)
+static void scatter_k2(const p3d_gp& gp, const int* halt, cudaStream_t s) {
+  CloudGP cl;
+  cl.pos = gp.v;
+  cl.n_inst = gp.n_inst;
+  cl.n_obj = gp.n_obj;
+  cl.wt = gp.w_top; cl.ht = gp.h_top; cl.wb = gp.w_bot; cl.hb = gp.h_bot;
+  cl.fw = gp.fill_w; cl.fh = gp.fill_h;
+  cl.macro = gp.is_macro;
+  cl.dz = gp.grid.dz;
+  cl.target_density = gp.target_density;
+  if (gp.ts_order) {
+    TileSort ts;
+    ts.n_tiles = gp.ts_n_tiles;
+    ts.tiles_x = gp.ts_tiles_x;
+    ts.tiles_y = gp.ts_tiles_y;
+    ts.margin = gp.ts_margin;
+    ts.tile_of = gp.ts_tile_of;
+    ts.hist = gp.ts_hist;
+    ts.start = gp.ts_start;
+    ts.cursor = gp.ts_cursor;
+    ts.order = gp.ts_order;
+    ts.rec = gp.ts_rec;
+    launch_scatter_tiled(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, ts, gp.rho_fx, halt, s);
+  } else {
+    launch_scatter(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, gp.rho_fx, halt, s);
+  }
+}
+
 static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = nullptr,
                         bool external = false) {
   auto mark = [&](int k) {
@@ -507,30 +603,7 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
   if (gp.n_inst > 0) launch_fused_gather(ga, s);
   mark(2);
   // K2
-  CloudGP cl;
-  cl.pos = gp.v;
-  cl.n_inst = gp.n_inst;
-  cl.n_obj = gp.n_obj;
-  cl.wt = gp.w_top; cl.ht = gp.h_top; cl.wb = gp.w_bot; cl.hb = gp.h_bot;
-  cl.fw = gp.fill_w; cl.fh = gp.fill_h;
-  cl.macro = gp.is_macro;
-  cl.dz = gp.grid.dz;
-  cl.target_density = gp.target_density;
-  if (gp.ts_order) {
-    TileSort ts;
-    ts.n_tiles = gp.ts_n_tiles;
-    ts.tiles_x = gp.ts_tiles_x;
-    ts.tiles_y = gp.ts_tiles_y;
-    ts.tile_of = gp.ts_tile_of;
-    ts.hist = gp.ts_hist;
-    ts.start = gp.ts_start;
-    ts.cursor = gp.ts_cursor;
-    ts.order = gp.ts_order;
-    ts.rec = gp.ts_rec;
-    launch_scatter_tiled(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, ts, gp.rho_fx, halt, s);
-  } else {
-    launch_scatter(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, gp.rho_fx, halt, s);
-  }
+  scatter_k2(gp, halt, s);
   mark(3);
   // K3 (+ overflow, re-zero)
   SpecOvfl ov;
@@ -625,6 +698,16 @@ int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s) {
     pos4_kernel<<<grid_blocks(gp.n_inst, 256, 4096), 256, 0, s>>>(gp.n_inst, gp.n_obj, gp.v, gp.pos4);
   cudaMemsetAsync(gp.rho_fx, 0, sizeof(int64_t) * (size_t)gp.grid.nx * gp.grid.ny * gp.grid.nz, s);
   return check_launch("gp_init");
+}
+
+int gp_density_fx(const p3d_gp& gp, int64_t* out, cudaStream_t s) {
+  tiled_scatter_setup();
+  const size_t bytes = sizeof(int64_t) * (size_t)gp.grid.nx * gp.grid.ny * gp.grid.nz;
+  cudaMemsetAsync(gp.rho_fx, 0, bytes, s);
+  scatter_k2(gp, nullptr, s);
+  cudaMemcpyAsync(out, gp.rho_fx, bytes, cudaMemcpyDeviceToDevice, s);
+  cudaMemsetAsync(gp.rho_fx, 0, bytes, s);
+  return check_launch("gp_density_fx");
 }
 
 int gp_project(const p3d_gp& gp, const double* in, double* out, cudaStream_t s) {

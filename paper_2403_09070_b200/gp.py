@@ -442,6 +442,12 @@ class Gp3dProblem:
         i32z = lambda n: torch.zeros(max(int(n), 1), dtype=torch.int32, device="cuda")  # noqa: E731
         self.t_ts = [i32z(O), i32z(nt), i32z(nt + 1), i32z(nt), i32z(O)]
         g.ts_n_tiles, g.ts_tiles_x, g.ts_tiles_y = nt, tx, ty
+        # footprint reach past the centre tile, in bins (+2: centre-bin rounding)
+        cell = ~arr.is_macro
+        half = max([0.0] + [float(np.max(a[cell])) for a in (self.w_top, self.w_bot, self.h_top,
+                                                              self.h_bot) if cell.any()] +
+                   [float(np.max(a)) for a in (fl.w, fl.h) if F]) / 2
+        g.ts_margin = int(np.ceil(half / min(grid.wb, grid.hb))) + 2
         for name, t in zip(("ts_tile_of", "ts_hist", "ts_start", "ts_cursor", "ts_order"), self.t_ts):
             setattr(g, name, keep(t))
         self.t_ts_rec = z(6 * O)
@@ -517,6 +523,14 @@ class Gp3dProblem:
         bundle = GradientBundle(wl_grad=wl_g, dens_grad=dg, total=total, divisors=div,
                                 value=st.value, wl_value=st.wl_value, energy=st.energy)
         return bundle, st.ovfl, st.exact, int(st.ncross)
+
+    def density_fx(self, pos):
+        """The loop's K2 (sorted, shared-memory privatised scatter) at `pos`:
+        the int64 fixed-point map [nx, ny, nz] (2^-40 per unit density)."""
+        self.t_v.copy_(self._soa(pos))
+        out = torch.empty(self.grid.n_bins, dtype=torch.int64, device="cuda")
+        _lib.call("p3d_gp_density_fx", _lib.byref(self.gp), _lib.ptr(out), _lib.stream_ptr())
+        return out.reshape(self.grid.shape)
 
     # -- fused loop ---------------------------------------------------------------
     def init_loop(self, pos0):

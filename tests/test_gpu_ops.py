@@ -222,6 +222,24 @@ def test_density_fixed_point_bit_exact(small):
     assert np.array_equal(cpu(got), want)
 
 
+def test_loop_scatter_bit_exact(small):
+    """The fused loop's K2 (tile sort + shared-memory windows) == oracle.fixed,
+    at the golden point and at a spread-out point (windows vs bbox fallback)."""
+    from paper_2403_09070_b200 import gp as G
+
+    d, g = small
+    grid, og, cl, oprob, fill, st = _small_cloud(small)
+    cfg = G.GpConfig(seed=1, nz=2, grid_nx=64, grid_ny=64, max_iters=60, stop_overflow=0.0)
+    prob = G.Gp3dProblem(d, grid, fill, cfg, st.rot)
+    rng = np.random.default_rng(7)
+    spread = oprob.project(np.c_[rng.uniform(0, d.die.width, len(g["pos"])),
+                                 rng.uniform(0, d.die.height, len(g["pos"])), g["pos"][:, 2]])
+    for pos in (g["pos"], spread):
+        got = prob.density_fx(pos)
+        want = FX.fixed_rho(og, oprob.cloud(pos))
+        assert np.array_equal(cpu(got), want)
+
+
 def test_density_vs_reference(small):
     from paper_2403_09070_b200 import density as dn
 
