@@ -6,8 +6,10 @@ cells; % of HBM roofline).
 One step = one full global-placement iteration (gp.py:386-444: WL + density +
 field + preconditioner + Nesterov/BB step) on the synthetic config-3 design
 (800,064 instances, 850k nets, 512x512x2 bins).  Under
-torchrun every rank runs an independent placement replica (seed 1 + rank):
-weak scaling, no data-path collective; the timed region is bracketed by
+torchrun (N>1) the default mode shards ONE placement over the N ranks
+(paper_2403_09070_b200.shard: objects and nets per rank, int64 density map
+all-reduced over NCCL; strong scaling); --mode replicas runs N independent
+placements (seed 1 + rank; weak scaling).  The timed region is bracketed by
 barriers and the max over ranks is reported.  Prints ONE JSON line on rank 0.
 """
 
@@ -195,6 +197,42 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def make_problem_inputs(design, spec, grid_n, max_iters, G):
+    cfg = G.GpConfig(seed=spec.seed, nz=2, grid_nx=grid_n, grid_ny=grid_n, max_iters=max_iters,
+                     stop_overflow=0.0)
+    rng = np.random.default_rng(spec.seed)
+    grid = G.choose_grid(design, cfg)
+    st = G.init_state(design, grid, cfg, rng)
+    st.fillers = G.make_fillers(design, grid, rng)
+    n = design.n_insts
+    pos0 = np.zeros((n + st.fillers.count, 3))
+    pos0[:n] = np.c_[st.x, st.y, st.z]
+    pos0[n:] = np.c_[st.fillers.x, st.fillers.y, st.fillers.z]
+    return cfg, grid, st, pos0
+
+
+def roofline_of(design, n_fill, grid, stage_ms):
+    """Roofline of the dominant kernel family (SURVEY 8d algorithmic bytes)."""
+    q = algorithmic_bytes(design, n_fill, grid.n_bins)
+    fam_ms = {"K1": stage_ms[0] + stage_ms[1], "K2": stage_ms[2], "K3": stage_ms[3],
+              "K4": stage_ms[4], "K5": stage_ms[5] + stage_ms[6]}
+    dom = max(fam_ms, key=fam_ms.get)
+    peak, peak_kind = load_peaks()
+    achieved = q[dom] / (fam_ms[dom] / 1000.0) / 1e9
+    per_family = {k: {"ms": round(float(v), 4), "alg_MB": round(q[k] / 1e6, 2),
+                      "GBs": round(q[k] / (v / 1000.0) / 1e9, 1) if v > 0 else None}
+                  for k, v in fam_ms.items()}
+    traffic = None
+    try:  # DRAM bytes per launch of the dominant family from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(dom)
+    except (OSError, ValueError):
+        pass
+    return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+            "per_family": per_family}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -202,6 +240,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default=None, choices=["fused", "sharded", "replicas"],
+                    help="fused: one GPU, the whole iteration in one CUDA graph (N=1 default); "
+                         "sharded: ONE placement partitioned over the N ranks (N>1 default, "
+                         "strong scaling); replicas: N independent placements (weak scaling)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
@@ -210,6 +252,9 @@ def main():
     rank, world, local = rank_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    mode = args.mode or ("sharded" if world > 1 else "fused")
+    if mode == "fused" and world > 1:
+        mode = "replicas"
 
     import torch
     import torch.distributed as dist
@@ -220,61 +265,65 @@ def main():
     from paper_2403_09070_b200 import _lib
     from paper_2403_09070_b200 import gp as G
 
-    design, grid_n, spec = setup_design(args.config, rank)
+    design, grid_n, spec = setup_design(args.config, rank if mode == "replicas" else 0)
     W, K = max(args.warmup, 3), args.steps
     max_iters = max(200, W + 2 * K + 2)
-    cfg = G.GpConfig(seed=spec.seed, nz=2, grid_nx=grid_n, grid_ny=grid_n, max_iters=max_iters,
-                     stop_overflow=0.0)
-    rng = np.random.default_rng(spec.seed)
-    grid = G.choose_grid(design, cfg)
-    st = G.init_state(design, grid, cfg, rng)
-    st.fillers = G.make_fillers(design, grid, rng)
-    prob = G.Gp3dProblem(design, grid, st.fillers, cfg, st.rot, precision=args.precision)
-    n = prob.n_inst
-    pos0 = np.zeros((prob.n_obj, 3))
-    pos0[:n] = np.c_[st.x, st.y, st.z]
-    pos0[n:] = np.c_[st.fillers.x, st.fillers.y, st.fillers.z]
+    cfg, grid, st, pos0 = make_problem_inputs(design, spec, grid_n, max_iters, G)
     stream = torch.cuda.current_stream()
 
-    # ---- device-resident timed region: graph replays of one iteration
-    prob.init_loop(pos0)
-    graph = prob.capture(1)
-    for _ in range(W):
-        graph.replay()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    if mode == "sharded":
+        from paper_2403_09070_b200.shard import ShardedGp3d
+
+        runner = ShardedGp3d(design, grid, st.fillers, cfg, st.rot, precision=args.precision)
+        prob = runner.prob
+        step = runner.iterate
+        runner.init_loop(pos0)
+    else:
+        prob = G.Gp3dProblem(design, grid, st.fillers, cfg, st.rot, precision=args.precision)
+        prob.init_loop(pos0)
+        graph = prob.capture(1)
+        step = lambda n=1: [graph.replay() for _ in range(n)]  # noqa: E731
+
+    # ---- device-resident timed region
+    step(W)
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(K):
-            graph.replay()
+        step(K)
         e1.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    barrier()
     ms = e0.elapsed_time(e1)
     s = prob.state()
     assert not s.done and s.it == W + K, f"loop ended early (it={s.it}, done={s.done})"
 
-    # ---- per-stage attribution: the same iteration captured with event-record
-    # nodes between the stages, replayed K times (no host gaps inside)
+    # ---- per-stage attribution (fused: the same iteration captured with
+    # event-record nodes between the stages, replayed K times)
     stage = np.zeros(7)
-    buf = (C.c_float * 7)()
-    mg = torch.cuda.CUDAGraph()
-    side = torch.cuda.Stream()
-    side.wait_stream(stream)
-    with torch.cuda.stream(side), torch.cuda.graph(mg, stream=side):
-        _lib.call("p3d_gp_iterate_marked", _lib.byref(prob.gp), _lib.stream_ptr())
-    stream.wait_stream(side)
-    for _ in range(K):
-        mg.replay()
-        torch.cuda.synchronize()
-        _lib.call("p3d_gp_stage_times", buf)
-        stage += np.frombuffer(buf, dtype=np.float32)
-    stage /= K
-    kpi = _lib.load().p3d_gp_kernels_per_iteration(_lib.byref(prob.gp))
+    if mode != "sharded":
+        buf = (C.c_float * 7)()
+        mg = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side), torch.cuda.graph(mg, stream=side):
+            _lib.call("p3d_gp_iterate_marked", _lib.byref(prob.gp), _lib.stream_ptr())
+        stream.wait_stream(side)
+        for _ in range(K):
+            mg.replay()
+            torch.cuda.synchronize()
+            _lib.call("p3d_gp_stage_times", buf)
+            stage += np.frombuffer(buf, dtype=np.float32)
+        stage /= K
+        kpi = _lib.load().p3d_gp_kernels_per_iteration(_lib.byref(prob.gp))
+    else:
+        kpi = _lib.load().p3d_gp_kernels_per_iteration(_lib.byref(prob.gp)) + 3
 
     # ---- end to end through the public API: pinned host state in, K steps with
     # the per-iteration log row read back every step, final positions out
@@ -282,22 +331,19 @@ def main():
     host_row = torch.empty(4, dtype=torch.float64).pin_memory()
     host_out = torch.empty((prob.n_obj, 3), dtype=torch.float64).pin_memory()
     dev_pos = torch.empty((prob.n_obj, 3), dtype=torch.float64, device="cuda")
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     dev_pos.copy_(host_pos, non_blocking=True)
     prob.init_loop(dev_pos)
     for k in range(K):
-        graph.replay()
+        step(1)
         host_row.copy_(prob.t_log[4 * k: 4 * k + 4], non_blocking=True)
     host_out.copy_(prob._aos(prob.t_u), non_blocking=True)
     f1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = f0.elapsed_time(f1)
-    if world > 1:
-        dist.barrier()
+    barrier()
 
     # max over ranks
     t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
@@ -307,44 +353,37 @@ def main():
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
         return
-    it_s = world * K / (ms / 1000.0)
-    e2e_it_s = world * K / (e2e_ms / 1000.0)
-
-    # roofline of the dominant kernel family (SURVEY 8d algorithmic bytes)
-    q = algorithmic_bytes(design, prob.n_fill, grid.n_bins)
-    fam_ms = {"K1": stage[0] + stage[1], "K2": stage[2], "K3": stage[3], "K4": stage[4],
-              "K5": stage[5] + stage[6]}
-    dom = max(fam_ms, key=fam_ms.get)
-    peak, peak_kind = load_peaks()
-    achieved = q[dom] / (fam_ms[dom] / 1000.0) / 1e9
-    per_family = {k: {"ms": round(float(v), 4), "alg_MB": round(q[k] / 1e6, 2),
-                      "GBs": round(q[k] / (v / 1000.0) / 1e9, 1) if v > 0 else None}
-                  for k, v in fam_ms.items()}
+    units = world * K if mode == "replicas" else K
+    it_s = units / (ms / 1000.0)
+    e2e_it_s = units / (e2e_ms / 1000.0)
     ws_mb = (sum(t.numel() * t.element_size() for t in prob._keep.items) +
              sum(t.numel() * t.element_size() for t in prob._dtopo.keep.items)) / 1e6
-
+    parallelism = {"fused": "single", "replicas": f"replicas x{world}",
+                   "sharded": f"sharded over {world} (objects + nets per rank, int64 rho "
+                              f"all-reduce)"}[mode]
     line = {
         "metric": METRIC, "value": it_s, "unit": "it/s", "n_gpus": world, "steps": K,
-        "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+        "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+        "scaling": "weak" if mode == "replicas" else "strong",
         "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f64+f32(WA)",
-        "data": "synthetic (paper_2403_09070_b200.synth == place3d.synth.gen_synthetic, seed 1+rank)",
-        "config": {"workload": WORKLOADS[args.config], "n_inst": n, "n_fill": prob.n_fill,
-                   "n_net": design.n_nets, "n_pin": design.arrays().n_pin,
-                   "grid": [grid.nx, grid.ny, grid.nz], "max_iters_schedule": max_iters,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single",
+        "data": "synthetic (paper_2403_09070_b200.synth == place3d.synth.gen_synthetic" +
+                (", seed 1+rank)" if mode == "replicas" else ", seed 1)"),
+        "config": {"workload": WORKLOADS[args.config], "n_inst": prob.n_inst,
+                   "n_fill": prob.n_fill, "n_net": design.n_nets,
+                   "n_pin": design.arrays().n_pin, "grid": [grid.nx, grid.ny, grid.nz],
+                   "max_iters_schedule": max_iters, "parallelism": parallelism, "mode": mode,
                    "wl_precision": args.precision,
                    "l2": f"no flush: iteration working set {ws_mb:.0f} MB > 126 MB L2"},
         "e2e": {"value": e2e_it_s, "unit": "it/s",
                 "h2d_bytes_per_step": int(host_pos.numel() * 8 / K),
                 "d2h_bytes_per_step": int(32 + host_out.numel() * 8 / K)},
         "gpu_launches": int(kpi * K),
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                     "peak_kind": peak_kind, "per_family": per_family},
         "clocks": clocks.summary(),
         "final_row": list(prob.log_rows(W + K)[-1]),
     }
-    if not args.no_cpu_baseline:
+    if mode != "sharded":
+        line["roofline"] = roofline_of(design, prob.n_fill, grid, stage)
+    if not args.no_cpu_baseline and world == 1:
         rate, iters, el = cpu_baseline(design, grid_n, spec, seconds=args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "it/s", "cores": 1, "kind": "port",
                                 "sample": f"{iters} GP iterations of the same workload from the "

@@ -240,7 +240,37 @@ typedef struct p3d_gp {
   p3d_loop_state* st;
   double* log;                 /* [max_iters][4]: it, exact WL, crossings, overflow */
   double* ovfl_hist;           /* [max_iters] */
+  /* sharded loop (p3d_gp_shard_stage): this rank owns the instance
+   * range [sh_i0, sh_i1) and the filler range [sh_f0, sh_f1) (object indices)
+   * and the K1 warp tasks w with w % shard_size == shard_rank; n_macro /
+   * macro_ids then list its own macros.  shard_size = 0 selects the fused
+   * single-GPU loop (p3d_gp_iterate; sh_i0 = 0, sh_i1 = n_inst, sh_f0 = n_inst,
+   * sh_f1 = n_obj); shard_size >= 1 the staged protocol (world size). */
+  int32_t shard_rank, shard_size;
+  int32_t sh_i0, sh_i1, sh_f0, sh_f1;
+  double* shard_tot;           /* [32] per-rank totals the host all-reduces between
+                                  stages: [0,6) net totals, [8,14) density totals,
+                                  [16] max |g| (iteration 0) */
 } p3d_gp;
+
+/* Stages of one sharded GP iteration.  The host runs them in this order with
+ * the collectives in brackets (sum unless noted):
+ *   NET, GATHER, [inst_g], NORMS, SCATTER, [rho_fx (int64, exact)], SPECTRAL,
+ *   DENS, [shard_tot[0:16]], CONTROL, STEP0, [shard_tot[16], max],
+ *   STEP0_CONTROL, ADVANCE, [st->dv2_next], [all-gather of pos4 slabs]. */
+enum {
+  P3D_SH_NET = 0,
+  P3D_SH_GATHER = 1,
+  P3D_SH_NORMS = 2,
+  P3D_SH_SCATTER = 3,
+  P3D_SH_SPECTRAL = 4,
+  P3D_SH_DENS = 5,
+  P3D_SH_CONTROL = 6,
+  P3D_SH_STEP0 = 7,
+  P3D_SH_STEP0_CONTROL = 8,
+  P3D_SH_ADVANCE = 9,
+  P3D_SH_N_STAGES = 10
+};
 
 /* Reset the loop state (lambda unset, a = 1, iteration 0) and project u = v =
  * P(pos0) (gp.py:188-196); pos0 [3][n_obj] may alias u. */
@@ -269,6 +299,8 @@ int p3d_gp_kernels_per_iteration(const p3d_gp* gp);
  * accumulate_density, density.py:301-311) at gp->v: the int64 fixed-point map
  * is written to out [B] and gp->rho_fx is left zeroed. */
 int p3d_gp_density_fx(const p3d_gp* gp, int64_t* out, void* stream);
+/* One stage of a sharded GP iteration (see P3D_SH_*); a no-op once st->done. */
+int p3d_gp_shard_stage(const p3d_gp* gp, int stage, void* stream);
 /* Gp3dProblem.project (gp.py:280-294): out = P(in), [3][n_obj]. */
 int p3d_gp_project(const p3d_gp* gp, const double* in, double* out, void* stream);
 

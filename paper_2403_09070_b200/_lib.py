@@ -74,7 +74,12 @@ class Gp(C.Structure):
                 ("ts_n_tiles", I32), ("ts_tiles_x", I32), ("ts_tiles_y", I32), ("ts_margin", I32),
                 ("ts_tile_of", P), ("ts_hist", P), ("ts_start", P), ("ts_cursor", P),
                 ("ts_order", P), ("ts_rec", P), ("rho", P), ("spec_scratch", P),
-                ("maps", P), ("partials", P), ("st", P), ("log", P), ("ovfl_hist", P)]
+                ("maps", P), ("partials", P), ("st", P), ("log", P), ("ovfl_hist", P),
+                ("shard_rank", I32), ("shard_size", I32), ("sh_i0", I32), ("sh_i1", I32),
+                ("sh_f0", I32), ("sh_f1", I32), ("shard_tot", P)]
+
+SH_STAGES = ("NET", "GATHER", "NORMS", "SCATTER", "SPECTRAL", "DENS", "CONTROL", "STEP0",
+             "STEP0_CONTROL", "ADVANCE")
 
 
 _SIGS = {
@@ -104,6 +109,7 @@ _SIGS = {
     "p3d_gp_evaluate": (I32, [P, D, D, P]),
     "p3d_gp_project": (I32, [P, P, P, P]),
     "p3d_gp_density_fx": (I32, [P, P, P]),
+    "p3d_gp_shard_stage": (I32, [P, C.c_int, P]),
     "p3d_gp_iterate_profiled": (I32, [P, P, P]),
     "p3d_gp_kernels_per_iteration": (I32, [P]),
     "p3d_gp_iterate_marked": (I32, [P, P]),

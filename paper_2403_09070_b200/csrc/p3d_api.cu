@@ -50,6 +50,7 @@ int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s);
 int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s);
 int gp_project(const p3d_gp& gp, const double* in, double* out, cudaStream_t s);
 int gp_density_fx(const p3d_gp& gp, int64_t* out, cudaStream_t s);
+int gp_shard_stage(const p3d_gp& gp, int stage, cudaStream_t s);
 int gp_iterate_profiled(const p3d_gp& gp, cudaStream_t s, float* ms);
 int gp_kernels_per_iteration(const p3d_gp& gp);
 int gp_iterate_marked(const p3d_gp& gp, cudaStream_t s);
@@ -338,6 +339,12 @@ int p3d_gp_evaluate(const p3d_gp* gp, double lam, double gamma, void* stream) {
 int p3d_gp_density_fx(const p3d_gp* gp, int64_t* out, void* stream) {
   if (!gp || !out) { set_error("gp_density_fx: null argument"); return P3D_ERR_ARG; }
   return gp_density_fx(*gp, out, STREAM(stream));
+}
+
+int p3d_gp_shard_stage(const p3d_gp* gp, int stage, void* stream) {
+  if (!gp || stage < 0 || stage >= P3D_SH_N_STAGES) { set_error("gp_shard_stage: bad stage"); return P3D_ERR_ARG; }
+  if (gp->shard_size < 1 || !gp->shard_tot) { set_error("gp_shard_stage: not a sharded problem (shard_size < 1 or no shard_tot)"); return P3D_ERR_ARG; }
+  return gp_shard_stage(*gp, stage, STREAM(stream));
 }
 
 int p3d_gp_project(const p3d_gp* gp, const double* in, double* out, void* stream) {

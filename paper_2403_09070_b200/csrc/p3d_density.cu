@@ -66,9 +66,10 @@ __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_gri
   for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x) sh_hist[t] = 0;
   __syncthreads();
   const double tw = g.wb * kTile, th = g.hb * kTile;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int i = k < ts.ni ? ts.i0 + k : ts.f0 + (k - ts.ni);  // this rank's objects
     if (cl.is_macro(i)) {
-      ts.tile_of[i] = -1;
+      ts.tile_of[k] = -1;
       continue;
     }
     const Charge q = cl.get(i);
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_gri
     tx = tx < 0 ? 0 : (tx >= ts.tiles_x ? ts.tiles_x - 1 : tx);
     ty = ty < 0 ? 0 : (ty >= ts.tiles_y ? ts.tiles_y - 1 : ty);
     const int t = tx * ts.tiles_y + ty;
-    ts.tile_of[i] = t;
+    ts.tile_of[k] = t;
     atomicAdd(&sh_hist[t], 1);
   }
   __syncthreads();
@@ -156,7 +157,8 @@ __global__ void __launch_bounds__(256) tile_place_kernel(Cloud cl, int n, TileSo
 #pragma unroll
   for (int k = 0; k < kPlacePerThread; ++k) {
     if (tile[k] < 0) continue;
-    const int i = i0 + k * blockDim.x;
+    const int kl = i0 + k * blockDim.x;
+    const int i = kl < ts.ni ? ts.i0 + kl : ts.f0 + (kl - ts.ni);  // this rank's objects
     const int pos = base[tile[k]] + rank[k];
     const Charge q = cl.get(i);
     ts.order[pos] = tile[k];

@@ -67,6 +67,7 @@ struct GatherArgs {
 struct FusedNetArgs {
   int n_net, blocks;
   int n_tasks;                // warp tasks
+  int task_rank, task_size;   // this rank takes tasks w % task_size == task_rank (sharded)
   const int4* tasks;          // (pin base, bucket size, first net in bucket, degree | 0 = generic)
   const int32_t* task_t0;     // permuted index of the bucket's first net
   int n_generic;              // nets of degree outside [2, 6]
@@ -115,6 +116,7 @@ int grid_blocks(int n, int threads, int cap);
 // spatially ordered scatter (p3d_density.cu)
 struct TileSort {
   int n_tiles, tiles_x, tiles_y, margin;
+  int i0, ni, f0;    // object of local index k: k < ni ? i0 + k : f0 + (k - ni)
   int32_t* tile_of;  // [n_obj]
   int32_t* hist;     // [n_tiles] (kept zeroed between iterations)
   int32_t* start;    // [n_tiles + 1]

@@ -36,6 +36,15 @@ __device__ __forceinline__ double* fin(const p3d_gp& gp) {
   return gp.partials + (long long)kSlotFinal * kPartialStride;
 }
 
+// this rank's objects (all of them on one GPU): local index k -> object index
+__host__ __device__ __forceinline__ int own_count(const p3d_gp& gp) {
+  return (gp.sh_i1 - gp.sh_i0) + (gp.sh_f1 - gp.sh_f0);
+}
+__device__ __forceinline__ int own_obj(const p3d_gp& gp, int k) {
+  const int ni = gp.sh_i1 - gp.sh_i0;
+  return k < ni ? gp.sh_i0 + k : gp.sh_f0 + (k - ni);
+}
+
 __device__ __forceinline__ CloudGP cloud_of(const p3d_gp& gp, const double* pos) {
   CloudGP c;
   c.pos = pos;
@@ -371,8 +380,9 @@ __global__ void __launch_bounds__(256, P3D_K4_MINB) dens_kernel(p3d_gp gp) {
       finish_object(gp, i, q, mean, sc, wl4, pw, pd, pq, mdeg, acc);
     }
   } else {
-    const int b = blockIdx.x - nm, nb = gridDim.x - nm;
-    for (int i = b * blockDim.x + threadIdx.x; i < gp.n_obj; i += nb * blockDim.x) {
+    const int b = blockIdx.x - nm, nb = gridDim.x - nm, n_own = own_count(gp);
+    for (int k = b * blockDim.x + threadIdx.x; k < n_own; k += nb * blockDim.x) {
+      const int i = own_obj(gp, k);
       if (cl.is_macro(i)) continue;
       double wl4[4], pw[3], pd[3], pq, mdeg;
 #if P3D_K4_PREFETCH
@@ -394,7 +404,13 @@ __global__ void __launch_bounds__(256, P3D_K4_MINB) dens_kernel(p3d_gp gp) {
   if (last_block(&gp.st->counters[kCntDens])) {
     double tot[6];
     for (int k = 0; k < 6; ++k) tot[k] = ordered_sum(part + k * gridDim.x, gridDim.x, red);
-    if (threadIdx.x == 0) control_after_eval(gp, tot[0], tot[1], tot[2], tot[3], tot[4], tot[5]);
+    if (threadIdx.x == 0) {
+      if (gp.shard_size > 0) {  // sharded: the host all-reduces, then shard_control_kernel
+        for (int k = 0; k < 6; ++k) gp.shard_tot[8 + k] = tot[k];
+      } else {
+        control_after_eval(gp, tot[0], tot[1], tot[2], tot[3], tot[4], tot[5]);
+      }
+    }
   }
 }
 
@@ -409,7 +425,9 @@ __global__ void __launch_bounds__(256) gmax0_kernel(p3d_gp gp) {
   const int O = gp.n_obj, I = gp.n_inst;
   const double lam = st->lam;
   double m = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < O; i += gridDim.x * blockDim.x) {
+  const int n_own = own_count(gp);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_own; k += gridDim.x * blockDim.x) {
+    const int i = own_obj(gp, k);
     const double mdeg = (i < I && gp.is_macro[i]) ? gp.degree[i] : 0.0;
     const double div = precond_div(lam, gp.prev_q[i], mdeg);
 #pragma unroll
@@ -424,10 +442,14 @@ __global__ void __launch_bounds__(256) gmax0_kernel(p3d_gp gp) {
   if (last_block(&st->counters[kCntStep])) {
     const double gm = block_max_partials((volatile double*)part, gridDim.x, red);
     if (threadIdx.x == 0) {
-      st->gmax = gm;
-      st->step = gm == 0.0 ? 1.0 : gp.step_scale / gm;
-      st->step_set = 1;
-      step_tail(gp);
+      if (gp.shard_size > 0) {  // sharded: max over ranks, then step0_control_kernel
+        gp.shard_tot[16] = gm;
+      } else {
+        st->gmax = gm;
+        st->step = gm == 0.0 ? 1.0 : gp.step_scale / gm;
+        st->step_set = 1;
+        step_tail(gp);
+      }
     }
   }
 }
@@ -443,7 +465,9 @@ __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
   const bool best = st->best_flag != 0, stop = st->stop_now != 0;
   const double step = st->step, mom = st->mom, lam = st->lam;
   double dv2[1] = {0.0};
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < O; i += gridDim.x * blockDim.x) {
+  const int n_own = own_count(gp);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_own; k += gridDim.x * blockDim.x) {
+    const int i = own_obj(gp, k);
     double u[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) u[c] = gp.u[(long long)c * O + i];
@@ -469,11 +493,11 @@ __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
     project_obj(gp, i, vn[0], vn[1], vn[2]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const long long k = (long long)c * O + i;
+      const long long j = (long long)c * O + i;
       const double d = vn[c] - v[c];  // BB numerator of the next evaluation (gp.py:210)
       dv2[0] += d * d;
-      gp.u[k] = un[c];
-      gp.v[k] = vn[c];
+      gp.u[j] = un[c];
+      gp.v[j] = vn[c];
     }
     if (i < I) reinterpret_cast<double4*>(gp.pos4)[i] = make_double4(vn[0], vn[1], vn[2], 0.0);
   }
@@ -539,27 +563,27 @@ static void scatter_k2(const p3d_gp& gp, const int* halt, cudaStream_t s) {
     ts.cursor = gp.ts_cursor;
     ts.order = gp.ts_order;
     ts.rec = gp.ts_rec;
-    launch_scatter_tiled(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, ts, gp.rho_fx, halt, s);
+    ts.i0 = gp.sh_i0;
+    ts.ni = gp.sh_i1 - gp.sh_i0;
+    ts.f0 = gp.sh_f0;
+    launch_scatter_tiled(cl, own_count(gp), gp.n_macro, gp.macro_ids, gp.grid, ts, gp.rho_fx,
+                         halt, s);
   } else {
     launch_scatter(cl, gp.n_obj, gp.n_macro, gp.macro_ids, gp.grid, gp.rho_fx, halt, s);
   }
 }
 
-static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = nullptr,
-                        bool external = false) {
-  auto mark = [&](int k) {
-    if (!ev) return;
-    if (external) cudaEventRecordWithFlags(ev[k], s, cudaEventRecordExternal);
-    else cudaEventRecord(ev[k], s);
-  };
-  mark(0);
+// ---- the stages of one evaluation (shared by the fused and sharded loops)
+static void launch_k1(const p3d_gp& gp, cudaStream_t s) {
   p3d_loop_state* st = gp.st;
   const int* halt = &st->done;
   double* finals = gp.partials + (long long)kSlotFinal * kPartialStride;
-  // K1 (degree-bucketed, register-resident nets) + K1b owner gather
+  // K1 (degree-bucketed, register-resident nets)
   FusedNetArgs na{};
   na.n_net = gp.topo.n_net;
   na.n_tasks = gp.f_n_tasks;
+  na.task_rank = gp.shard_size > 0 ? gp.shard_rank : 0;  // shard_size 0: the fused loop
+  na.task_size = gp.shard_size > 0 ? gp.shard_size : 1;
   na.tasks = reinterpret_cast<const int4*>(gp.f_tasks);
   na.task_t0 = gp.f_task_t0;
   na.n_generic = gp.f_n_generic;
@@ -584,10 +608,16 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
   na.out_d = gp.wl_f32 ? nullptr : gp.pin_out;
   na.partials = gp.partials + (long long)kSlotNet * kPartialStride;
   na.counter = &st->counters[kCntNet];
-  na.final6 = finals + kFinNet;
+  na.final6 = gp.shard_size > 0 ? gp.shard_tot : finals + kFinNet;  // sharded: local totals
   na.halt = halt;
   if (na.n_net > 0) launch_fused_net(na, gp.wl_f32 != 0, s);
-  mark(1);
+}
+
+static void launch_k1b(const p3d_gp& gp, cudaStream_t s) {
+  p3d_loop_state* st = gp.st;
+  const int* halt = &st->done;
+  double* finals = gp.partials + (long long)kSlotFinal * kPartialStride;
+  // K1b owner gather (per-instance sums; L1 norms + Eq. 17 scale on one GPU)
   FusedGatherArgs ga{};
   ga.n_obj = gp.n_inst;
   ga.blocks = grid_blocks(gp.n_inst, 256, kMaxBlocks);
@@ -598,13 +628,15 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
   ga.out = gp.inst_g;
   ga.partials = gp.partials + (long long)kSlotGather * kPartialStride;
   ga.counter = &st->counters[kCntGather];
-  ga.final_norms = finals + kFinNorm;
+  ga.final_norms = gp.shard_size > 0 ? nullptr : finals + kFinNorm;  // sharded: NORMS stage
   ga.halt = halt;
   if (gp.n_inst > 0) launch_fused_gather(ga, s);
-  mark(2);
-  // K2
-  scatter_k2(gp, halt, s);
-  mark(3);
+}
+
+static int launch_k3(const p3d_gp& gp, cudaStream_t s) {
+  p3d_loop_state* st = gp.st;
+  const int* halt = &st->done;
+  double* finals = gp.partials + (long long)kSlotFinal * kPartialStride;
   // K3 (+ overflow, re-zero)
   SpecOvfl ov;
   ov.zero = 1;
@@ -616,9 +648,26 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
   const int rc = launch_spectral_ex(&gp.grid, nullptr, gp.rho_fx, nullptr, nullptr, gp.maps,
                                     gp.spec_scratch, halt, &ov, s);
   if (rc) return rc;
+  return 0;
+}
+
+static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = nullptr,
+                        bool external = false) {
+  auto mark = [&](int k) {
+    if (!ev) return;
+    if (external) cudaEventRecordWithFlags(ev[k], s, cudaEventRecordExternal);
+    else cudaEventRecord(ev[k], s);
+  };
+  mark(0);
+  launch_k1(gp, s);
+  mark(1);
+  launch_k1b(gp, s);
+  mark(2);
+  scatter_k2(gp, &gp.st->done, s);  // K2
+  mark(3);
+  if (const int rc = launch_k3(gp, s)) return rc;  // K3 (+ overflow, re-zero)
   mark(4);
-  // K4
-  dens_kernel<<<gp.n_macro + gp.nblk_obj, 256, 0, s>>>(gp);
+  dens_kernel<<<gp.n_macro + gp.nblk_obj, 256, 0, s>>>(gp);  // K4
   mark(5);
   return check_launch("gp evaluation kernels");
 }
@@ -698,6 +747,81 @@ int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s) {
     pos4_kernel<<<grid_blocks(gp.n_inst, 256, 4096), 256, 0, s>>>(gp.n_inst, gp.n_obj, gp.v, gp.pos4);
   cudaMemsetAsync(gp.rho_fx, 0, sizeof(int64_t) * (size_t)gp.grid.nx * gp.grid.ny * gp.grid.nz, s);
   return check_launch("gp_init");
+}
+
+// ---------------------------------------------------------------------------
+// sharded loop (config 4): the stages that follow a collective
+// ---------------------------------------------------------------------------
+// L1 norms of the all-reduced owner sums + the Eq. 17 scale (every rank, all
+// instances: identical on every rank)
+__global__ void __launch_bounds__(256) inst_norms_kernel(p3d_gp gp) {
+  if (gp.st->done) return;
+  __shared__ double red[32 * 3];
+  const int I = gp.n_inst;
+  double acc[3] = {0, 0, 0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < I; i += gridDim.x * blockDim.x) {
+    acc[0] += fabs(gp.inst_g[i]);
+    acc[1] += fabs(gp.inst_g[I + i]);
+    acc[2] += fabs(gp.inst_g[3 * (long long)I + i]);
+  }
+  double* part = gp.partials + (long long)kSlotGather * kPartialStride;
+  block_sum<3>(acc, red);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 3; ++q) part[q * gridDim.x + blockIdx.x] = acc[q];
+  if (last_block(&gp.st->counters[kCntGather])) {
+    double n[3];
+    for (int q = 0; q < 3; ++q) n[q] = ordered_sum(part + q * gridDim.x, gridDim.x, red);
+    if (threadIdx.x == 0) {
+      double* f = fin(gp) + kFinNorm;
+      f[0] = n[0];
+      f[1] = n[1];
+      f[2] = n[2];
+      f[3] = n[2] == 0.0 ? 0.0 : (n[0] + n[1]) / (2.0 * n[2]);  // Eq. 17
+    }
+  }
+}
+
+// loop control with the all-reduced totals (net: shard_tot[0,6), density:
+// shard_tot[8,14)); identical on every rank
+__global__ void shard_control_kernel(p3d_gp gp) {
+  if (gp.st->done) return;
+  double* f = fin(gp);
+  const double* t = gp.shard_tot;
+  for (int q = 0; q < 6; ++q) f[kFinNet + q] = t[q];
+  control_after_eval(gp, t[8], t[9], t[10], t[11], t[12], t[13]);
+}
+
+// iteration 0: the initial step from the max over ranks of |g| (gp.py:198-202)
+__global__ void step0_control_kernel(p3d_gp gp) {
+  p3d_loop_state* st = gp.st;
+  if (st->done || st->step_set || st->stop_now) return;
+  const double gm = gp.shard_tot[16];
+  st->gmax = gm;
+  st->step = gm == 0.0 ? 1.0 : gp.step_scale / gm;
+  st->step_set = 1;
+  step_tail(gp);
+}
+
+int gp_shard_stage(const p3d_gp& gp, int stage, cudaStream_t s) {
+  spectral_setup();
+  tiled_scatter_setup();
+  fused_net_setup();
+  switch (stage) {
+    case P3D_SH_NET: if (gp.topo.n_net > 0) launch_k1(gp, s); break;
+    case P3D_SH_GATHER: if (gp.n_inst > 0) launch_k1b(gp, s); break;
+    case P3D_SH_NORMS:
+      inst_norms_kernel<<<grid_blocks(gp.n_inst, 256, kMaxBlocks), 256, 0, s>>>(gp);
+      break;
+    case P3D_SH_SCATTER: scatter_k2(gp, &gp.st->done, s); break;
+    case P3D_SH_SPECTRAL: if (const int rc = launch_k3(gp, s)) return rc; break;
+    case P3D_SH_DENS: dens_kernel<<<gp.n_macro + gp.nblk_obj, 256, 0, s>>>(gp); break;
+    case P3D_SH_CONTROL: shard_control_kernel<<<1, 1, 0, s>>>(gp); break;
+    case P3D_SH_STEP0: gmax0_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp); break;
+    case P3D_SH_STEP0_CONTROL: step0_control_kernel<<<1, 1, 0, s>>>(gp); break;
+    case P3D_SH_ADVANCE: advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp); break;
+    default: return P3D_ERR_ARG;
+  }
+  return check_launch("gp_shard_stage");
 }
 
 int gp_density_fx(const p3d_gp& gp, int64_t* out, cudaStream_t s) {

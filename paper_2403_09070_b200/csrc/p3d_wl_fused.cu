@@ -341,9 +341,6 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
 #ifndef P3D_K1_MINB
 #define P3D_K1_MINB 5
 #endif
-#ifndef P3D_TASK_PREFETCH
-#define P3D_TASK_PREFETCH 0
-#endif
 
 constexpr int kMaxStagedDeg = 6;
 constexpr int kWarpsPerBlock = 4;
@@ -585,22 +582,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_ke
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   WarpCols<F32>& sm = reinterpret_cast<WarpCols<F32>*>(dyn_smem)[wib];
   const int wstride = gridDim.x * kWarpsPerBlock;
-#if P3D_TASK_PREFETCH
-  int w = blockIdx.x * kWarpsPerBlock + wib;
-  int4 tkn = w < a.n_tasks ? a.tasks[w] : make_int4(0, 0, 0, 0);
-  int t0n = w < a.n_tasks ? a.task_t0[w] : 0;
-  for (; w < a.n_tasks; w += wstride) {
-    const int4 tk = tkn;  // the next task's descriptor is fetched before this one runs
-    const int t0 = t0n;
-    if (w + wstride < a.n_tasks) {
-      tkn = a.tasks[w + wstride];
-      t0n = a.task_t0[w + wstride];
-    }
-#else
-  for (int w = blockIdx.x * kWarpsPerBlock + wib; w < a.n_tasks; w += wstride) {
+  for (int j = blockIdx.x * kWarpsPerBlock + wib;; j += wstride) {
+    const int w = a.task_rank + j * a.task_size;  // this rank's warp tasks (sharded loop)
+    if (w >= a.n_tasks) break;
     const int4 tk = a.tasks[w];
     const int t0 = a.task_t0[w];
-#endif
 #ifdef P3D_SKIP_D2
     if (tk.w == 2) continue;
 #endif
@@ -637,8 +623,11 @@ __global__ void __launch_bounds__(256) generic_net_kernel(FusedNetArgs a) {
   if (a.gamma_ptr) a.gamma = *a.gamma_ptr;
   a.inv_gamma = 1.0 / a.gamma;
   double acc[6] = {0, 0, 0, 0, 0, 0};
-  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < a.n_generic; g += gridDim.x * blockDim.x)
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x;; j += gridDim.x * blockDim.x) {
+    const int g = a.task_rank + j * a.task_size;  // this rank's generic nets (sharded loop)
+    if (g >= a.n_generic) break;
     process_net_generic<F32>(a, a.generic_nets[g], acc);
+  }
   block_sum<6>(acc, red);
   if (threadIdx.x == 0)
     for (int q = 0; q < 6; ++q) a.gpartials[q * gridDim.x + blockIdx.x] = acc[q];
@@ -685,7 +674,7 @@ __global__ void __launch_bounds__(256) fused_gather_kernel(FusedGatherArgs a) {
   block_sum<3>(acc, red);
   if (threadIdx.x == 0)
     for (int q = 0; q < 3; ++q) a.partials[q * gridDim.x + blockIdx.x] = acc[q];
-  if (last_block(a.counter)) {
+  if (a.final_norms && last_block(a.counter)) {  // sharded loop: norms after the all-reduce
     double n[3];
     for (int q = 0; q < 3; ++q) n[q] = ordered_sum(a.partials + q * gridDim.x, gridDim.x, red);
     if (threadIdx.x == 0) {

@@ -315,7 +315,7 @@ class Gp3dProblem:
     ``cloud`` keep the reference semantics; ``run`` drives the fused loop."""
 
     def __init__(self, design, grid: dn.DensityGrid, fillers: dn.FillerSet, cfg: GpConfig, rot,
-                 max_iters=None, precision=None):
+                 max_iters=None, precision=None, shard=None):
         """precision: "fp64" (default; WA sums in float64 with numpy's
         operation order) or "fp32" (WA sums in float32 on anchor-relative
         differences, the SURVEY App. B plan; faster, ~1e-7 relative)."""
@@ -352,6 +352,9 @@ class Gp3dProblem:
                       np.where(up, self.h_top, self.h_bot))
         self.movable_volume = float((wv * hv).sum() * grid.dz / 2)
         self.max_iters = int(cfg.max_iters if max_iters is None else max_iters)
+        # shard: None (fused single-GPU loop) or (rank, world) for shard.ShardedGp3d
+        self.sharded = shard is not None
+        self.shard_rank, self.shard_size = (int(shard[0]), int(shard[1])) if shard else (0, 1)
         self._build()
 
     # -- device descriptor -------------------------------------------------
@@ -366,6 +369,18 @@ class Gp3dProblem:
         g = self.gp = _lib.Gp()
         g.n_inst, g.n_fill, g.n_obj = I, F, O
         macro_ids = np.flatnonzero(arr.is_macro).astype(np.int32)
+        # this rank's objects: an instance slab of equal padded size
+        # (so the pos4 slabs all-gather with equal counts) and a filler slab
+        R, r = self.shard_size, self.shard_rank
+        self.inst_slab = -(-I // R) if I else 0
+        self.sh_i = (min(r * self.inst_slab, I), min((r + 1) * self.inst_slab, I))
+        q, rem = divmod(F, R)
+        f_lo = r * q + min(r, rem)
+        self.sh_f = (I + f_lo, I + f_lo + q + (1 if r < rem else 0))
+        g.shard_rank, g.shard_size = r, (R if self.sharded else 0)
+        g.sh_i0, g.sh_i1 = self.sh_i
+        g.sh_f0, g.sh_f1 = self.sh_f
+        macro_ids = macro_ids[(macro_ids >= self.sh_i[0]) & (macro_ids < self.sh_i[1])]
         g.n_macro = len(macro_ids)
         if g.n_macro > K_MAX_BLOCKS:
             raise ValueError(f"{g.n_macro} macros exceed the per-launch CTA budget {K_MAX_BLOCKS}")
@@ -433,7 +448,9 @@ class Gp3dProblem:
         self.t_pin_out = z(4 * P)
         self.t_pin_out_f = torch.zeros(max(4 * P, 4), dtype=torch.float32, device="cuda")
         self.t_pin_out_fd = z(P)
-        self.t_pos4 = z(4 * I)
+        self.t_pos4 = z(4 * max(I, R * self.inst_slab))
+        self.t_shard_tot = z(32)
+        g.shard_tot = keep(self.t_shard_tot)
         self.t_inst_g = z(4 * I)
         self.t_rho_fx = torch.zeros(B, dtype=torch.int64, device="cuda")
         self.t_rho = z(B)
