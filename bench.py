@@ -331,15 +331,20 @@ def main():
     host_row = torch.empty(4, dtype=torch.float64).pin_memory()
     host_out = torch.empty((prob.n_obj, 3), dtype=torch.float64).pin_memory()
     dev_pos = torch.empty((prob.n_obj, 3), dtype=torch.float64, device="cuda")
-    barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def e2e_pass(n):
+        dev_pos.copy_(host_pos, non_blocking=True)
+        prob.init_loop(dev_pos)
+        for k in range(n):
+            step(1)
+            host_row.copy_(prob.t_log[4 * k: 4 * k + 4], non_blocking=True)
+        host_out.copy_(prob._aos(prob.t_u), non_blocking=True)
+
+    e2e_pass(W)  # warm-up of the API path (first-use allocations, pinned staging)
+    barrier()
     f0.record(stream)
-    dev_pos.copy_(host_pos, non_blocking=True)
-    prob.init_loop(dev_pos)
-    for k in range(K):
-        step(1)
-        host_row.copy_(prob.t_log[4 * k: 4 * k + 4], non_blocking=True)
-    host_out.copy_(prob._aos(prob.t_u), non_blocking=True)
+    e2e_pass(K)
     f1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = f0.elapsed_time(f1)

@@ -155,6 +155,15 @@ int p3d_density_gather(const p3d_grid* g, const p3d_cloud* c, const double* maps
                        const uint8_t* freeze_z, double* energy, double* force,
                        double* scratch, void* stream);
 
+/* density_energy_and_gradient (density.py:533-565): energy = sum q*phibar and
+ * the exact gradient 2 w sum_b phi_b dvol/dc ([n][3]; cells: two face columns
+ * per axis, density.py:389-441; macros: differentiated corner stamps against
+ * the suffix-summed phi, density.py:444-502).  phi: [B]; freeze_z nullable.
+ * scratch: >= B + 8 + 1024 doubles (suffix map, reduction partials), zeroed. */
+int p3d_density_energy_gradient(const p3d_grid* g, const p3d_cloud* c, const double* phi,
+                                const uint8_t* freeze_z, double* energy, double* grad,
+                                double* scratch, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* optimiser pieces (gp.py:142-147, 178-227, 280-294)                        */
 /* ------------------------------------------------------------------------ */

@@ -517,6 +517,119 @@ def force(grid, cl, ex, ey, ez, freeze_z=None):
     return g
 
 
+def _axis_bins(lo, hi, step, n):
+    """density.py:155-159: inclusive bin range of a clipped extent."""
+    i0 = np.clip(np.floor(lo / step).astype(np.int64), 0, n - 1)
+    i1 = np.maximum(np.clip(np.ceil(hi / step).astype(np.int64) - 1, 0, n - 1), i0)
+    return i0, i1
+
+
+def _olap(lo, hi, idx, step):
+    """density.py:172-173."""
+    return np.clip(np.minimum(hi, (idx + 1) * step) - np.maximum(lo, idx * step), 0, None)
+
+
+def face_grad(grid, cl, phi):
+    """density.py:389-441 (_direct_face_grad): d/d(center) of sum_b phi_b *
+    vol(D cap b) from the two face columns of each axis; [n, 3]."""
+    n = len(cl.x)
+    xlo, xhi, ylo, yhi, zlo, zhi = _box(grid, cl)
+    flat = phi.reshape(-1)
+    out = np.zeros((n, 3))
+    bounds = ((xlo, xhi, grid.wb, grid.nx), (ylo, yhi, grid.hb, grid.ny),
+              (zlo, zhi, grid.db, grid.nz))
+    ranges = [_axis_bins(lo, hi, st, nb) for lo, hi, st, nb in bounds]
+    for axis in range(3):
+        lo, hi, step, nb = bounds[axis]
+        f_hi = np.clip(np.floor(hi / step).astype(np.int64), 0, nb - 1)  # density.py:392-394
+        f_lo = np.clip(np.floor(lo / step).astype(np.int64), 0, nb - 1)
+        o1, o2 = [a for a in (0, 1, 2) if a != axis]
+        (l1, h1, s1, _), (l2, h2, s2, _) = bounds[o1], bounds[o2]
+        (i10, i11), (i20, i21) = ranges[o1], ranges[o2]
+        acc = np.zeros(n)
+        for d1 in range(int((i11 - i10).max(initial=-1)) + 1):
+            b1 = np.minimum(i10 + d1, i11)
+            w1 = np.where(i10 + d1 <= i11, _olap(l1, h1, b1, s1), 0.0)
+            for d2 in range(int((i21 - i20).max(initial=-1)) + 1):
+                b2 = np.minimum(i20 + d2, i21)
+                w2 = np.where(i20 + d2 <= i21, _olap(l2, h2, b2, s2), 0.0)
+                w12 = w1 * w2
+                idx = [None, None, None]
+                idx[o1], idx[o2] = b1, b2
+                idx[axis] = f_hi
+                fhi = (idx[0] * grid.ny + idx[1]) * grid.nz + idx[2]
+                idx[axis] = f_lo
+                flo = (idx[0] * grid.ny + idx[1]) * grid.nz + idx[2]
+                acc += (flat[fhi] - flat[flo]) * w12
+        out[:, axis] = acc
+    return out
+
+
+def stamp_face_grad(grid, cl, sphi):
+    """density.py:444-486 (_stamp_face_grad): macro gradient from corner stamps
+    differentiated along the gradient axis, against the suffix-summed phi."""
+    n = len(cl.x)
+    out = np.zeros((n, 3))
+    steps = (grid.wb, grid.hb, grid.db)
+    nbins = (grid.nx, grid.ny, grid.nz)
+    extents = (grid.dx, grid.dy, grid.dz)
+    half = (cl.w / 2, cl.h / 2, cl.dep / 2)
+    centers = (cl.x, cl.y, cl.z)
+    for axis in range(3):
+        acc = np.zeros(n)
+        for sx in (-1.0, 1.0):
+            for sy in (-1.0, 1.0):
+                for sz in (-1.0, 1.0):
+                    sign = -sx * sy * sz
+                    sigma = (sx, sy, sz)
+                    coords = [np.clip(centers[a] + sigma[a] * half[a], 0, extents[a])
+                              for a in range(3)]
+                    stamps = []
+                    for a in range(3):
+                        base = coords[a] / steps[a]
+                        i0 = np.floor(base).astype(np.int64)
+                        frac = base - i0
+                        if a == axis:
+                            stamps.append([(i0, -1.0 / steps[a]), (i0 + 1, 1.0 / steps[a])])
+                        else:
+                            stamps.append([(i0, 1.0 - frac), (i0 + 1, frac)])
+                    for g0, v0 in stamps[0]:
+                        ok0 = (g0 >= 0) & (g0 < nbins[0])
+                        for g1, v1 in stamps[1]:
+                            ok1 = ok0 & (g1 >= 0) & (g1 < nbins[1])
+                            for g2, v2 in stamps[2]:
+                                ok = ok1 & (g2 >= 0) & (g2 < nbins[2])
+                                if not ok.any():
+                                    continue
+                                val = np.zeros(n)
+                                val[ok] = sphi[g0[ok], g1[ok], g2[ok]]
+                                acc += sign * val * (v0 * v1 * np.asarray(v2))
+        out[:, axis] = acc * grid.bin_vol
+    return out
+
+
+def energy_and_gradient(grid, cl, phi, freeze_z=None):
+    """density.py:533-565 (density_energy_and_gradient): U = sum q phibar and its
+    exact gradient 2 w sum_b phi_b dvol/dc (cells: face form; macros: stamps)."""
+    n = len(cl.x)
+    grad = np.zeros((n, 3))
+    phibar = np.zeros(n)
+    c = ~cl.is_macro
+    if c.any():
+        sub = cl.take(c)
+        phibar[c] = cell_means(grid, sub, (phi,))[0]
+        grad[c] = face_grad(grid, sub, phi) * (2.0 * sub.weight[:, None])
+    if cl.is_macro.any():
+        sub = cl.take(cl.is_macro)
+        sphi = rev_cumsum3(phi)
+        phibar[cl.is_macro] = macro_means(grid, sub, sphi)
+        grad[cl.is_macro] = stamp_face_grad(grid, sub, sphi) * (2.0 * sub.weight[:, None])
+    energy = float((cl.charge * phibar).sum())
+    if freeze_z is not None:
+        grad[freeze_z, 2] = 0.0
+    return energy, grad
+
+
 def overflow_of(rho, grid, rho_t, mv):
     """density.py:612-617."""
     if mv <= 0:

@@ -31,6 +31,9 @@ int check_launch(const char* what) {
 template <class Cloud>
 void launch_scatter(const Cloud& cl, int n, int n_macro, const int32_t* macro_ids,
                     const p3d_grid& g, int64_t* rho, const int* halt, cudaStream_t s);
+void launch_energy_grad(const p3d_cloud& c, const p3d_grid& g, const double* phi,
+                        const uint8_t* freeze, double* energy, double* grad, double* scratch,
+                        cudaStream_t s);
 void launch_gather_op(const p3d_cloud& c, const p3d_grid& g, const double* maps,
                       const uint8_t* freeze, double* energy, double* force, double* scratch,
                       cudaStream_t s);
@@ -281,6 +284,15 @@ int p3d_density_gather(const p3d_grid* g, const p3d_cloud* c, const double* maps
   if (c->n_macro > 0 && !c->macro_ids) { set_error("macro_ids missing"); return P3D_ERR_ARG; }
   launch_gather_op(*c, *g, maps, freeze_z, energy, force, scratch, STREAM(stream));
   return check_launch("density_gather");
+}
+
+int p3d_density_energy_gradient(const p3d_grid* g, const p3d_cloud* c, const double* phi,
+                                const uint8_t* freeze_z, double* energy, double* grad,
+                                double* scratch, void* stream) {
+  if (bad_grid(g) || !c || !phi || !energy || !grad || !scratch) { if (!g_err[0]) set_error("density_energy_gradient: bad args"); return P3D_ERR_ARG; }
+  if (c->n == 0) return P3D_OK;
+  launch_energy_grad(*c, *g, phi, freeze_z, energy, grad, scratch, STREAM(stream));
+  return check_launch("density_energy_gradient");
 }
 
 int p3d_precondition(int32_t n, const double* gr, double lam, const double* q, const double* deg,

@@ -403,6 +403,223 @@ void launch_gather_op(const p3d_cloud& c, const p3d_grid& g, const double* maps,
 }
 
 // ---------------------------------------------------------------------------
+// exact energy gradient (density_energy_and_gradient, density.py:389-565):
+// cells differentiate the overlap volume through the two face columns of each
+// axis, macros differentiate their corner stamps against the suffix-summed
+// potential.  Same terms, same order as the reference (compiled -fmad=false).
+// ---------------------------------------------------------------------------
+// inclusive sums toward smaller indices along one axis (density.py:212-217)
+__global__ void suffix_axis_kernel(const double* in, double* out, int nx, int ny, int nz,
+                                   int axis) {
+  const int len = axis == 0 ? nx : (axis == 1 ? ny : nz);
+  const long long stride = axis == 0 ? (long long)ny * nz : (axis == 1 ? nz : 1);
+  const long long n_lines = (long long)nx * ny * nz / len;
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < n_lines;
+       l += (long long)gridDim.x * blockDim.x) {
+    long long base;
+    if (axis == 0) base = l;
+    else if (axis == 1) base = (l / nz) * (long long)ny * nz + (l % nz);
+    else base = l * nz;
+    double s = 0.0;
+    for (int i = len - 1; i >= 0; --i) {
+      s += in[base + i * stride];
+      out[base + i * stride] = s;
+    }
+  }
+}
+
+// density.py:389-441, one cell: d/d(center) of sum_b phi_b vol(D cap b)
+__device__ __forceinline__ void cell_face_grad(const Footprint& f, const p3d_grid& g,
+                                               const double* phi, double (&out)[3]) {
+  const AxisSpan ax[3] = {f.ax, f.ay, f.az};
+  const double steps[3] = {g.wb, g.hb, g.db};
+  const int nb[3] = {g.nx, g.ny, g.nz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    long long fh = (long long)floor(ax[a].hi / steps[a]), fl = (long long)floor(ax[a].lo / steps[a]);
+    fh = fh < 0 ? 0 : (fh > nb[a] - 1 ? nb[a] - 1 : fh);
+    fl = fl < 0 ? 0 : (fl > nb[a] - 1 ? nb[a] - 1 : fl);
+    const int o1 = a == 0 ? 1 : 0, o2 = a == 2 ? 1 : 2;
+    double acc = 0.0;
+    for (int b1 = ax[o1].i0; b1 <= ax[o1].i1; ++b1) {
+      const double w1 = overlap_len(ax[o1], b1, steps[o1]);
+      for (int b2 = ax[o2].i0; b2 <= ax[o2].i1; ++b2) {
+        const double w12 = w1 * overlap_len(ax[o2], b2, steps[o2]);
+        int ih[3], il[3];
+        ih[o1] = il[o1] = b1;
+        ih[o2] = il[o2] = b2;
+        ih[a] = (int)fh;
+        il[a] = (int)fl;
+        const double ph = phi[((long long)ih[0] * g.ny + ih[1]) * g.nz + ih[2]];
+        const double pl = phi[((long long)il[0] * g.ny + il[1]) * g.nz + il[2]];
+        acc += (ph - pl) * w12;
+      }
+    }
+    out[a] = acc;
+  }
+}
+
+// one corner's trilinear stamp dotted with the suffix map (density.py:505-530);
+// axis >= 0 differentiates the stamp along that axis (density.py:466-476)
+__device__ __forceinline__ double corner_stamp(const p3d_grid& g, const double* sphi,
+                                               const double (&c)[3], int axis) {
+  const double steps[3] = {g.wb, g.hb, g.db};
+  const int nb[3] = {g.nx, g.ny, g.nz};
+  long long i0[3];
+  double v[3][2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double base = c[a] / steps[a];
+    i0[a] = (long long)floor(base);
+    const double frac = base - (double)i0[a];
+    if (a == axis) {
+      v[a][0] = -1.0 / steps[a];
+      v[a][1] = 1.0 / steps[a];
+    } else {
+      v[a][0] = 1.0 - frac;
+      v[a][1] = frac;
+    }
+  }
+  double acc = 0.0;
+  for (int b0 = 0; b0 < 2; ++b0) {
+    const long long g0 = i0[0] + b0;
+    if (g0 < 0 || g0 >= nb[0]) continue;
+    for (int b1 = 0; b1 < 2; ++b1) {
+      const long long g1 = i0[1] + b1;
+      if (g1 < 0 || g1 >= nb[1]) continue;
+      for (int b2 = 0; b2 < 2; ++b2) {
+        const long long g2 = i0[2] + b2;
+        if (g2 < 0 || g2 >= nb[2]) continue;
+        const double val = sphi[(g0 * g.ny + g1) * g.nz + g2];
+        acc += val * ((v[0][b0] * v[1][b1]) * v[2][b2]);  // density.py:527-528
+      }
+    }
+  }
+  return acc;
+}
+
+// density.py:444-486 (gradient) and 489-502 (phibar) of one macro
+__device__ __forceinline__ void macro_face_grad(const Charge& q, const p3d_grid& g,
+                                                const double* sphi, double (&grad)[3],
+                                                double& phibar) {
+  const double ext[3] = {g.dx, g.dy, g.dz};
+  const double half[3] = {q.w / 2, q.h / 2, q.dep / 2};
+  const double cen[3] = {q.x, q.y, q.z};
+  double pacc = 0.0;
+  double gacc[3] = {0.0, 0.0, 0.0};
+  for (int s = 0; s < 8; ++s) {
+    const double sg[3] = {(s & 4) ? 1.0 : -1.0, (s & 2) ? 1.0 : -1.0, (s & 1) ? 1.0 : -1.0};
+    const double sign = -sg[0] * sg[1] * sg[2];
+    double c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) c[a] = clipd(cen[a] + sg[a] * half[a], 0.0, ext[a]);
+    pacc += sign * corner_stamp(g, sphi, c, -1);
+  }
+  // the reference accumulates per axis over the 8 corners and every stamp point
+  for (int axis = 0; axis < 3; ++axis) {
+    double acc = 0.0;
+    for (int s = 0; s < 8; ++s) {
+      const double sg[3] = {(s & 4) ? 1.0 : -1.0, (s & 2) ? 1.0 : -1.0, (s & 1) ? 1.0 : -1.0};
+      const double sign = -sg[0] * sg[1] * sg[2];
+      double c[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) c[a] = clipd(cen[a] + sg[a] * half[a], 0.0, ext[a]);
+      const double steps[3] = {g.wb, g.hb, g.db};
+      const int nb[3] = {g.nx, g.ny, g.nz};
+      long long i0[3];
+      double v[3][2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double base = c[a] / steps[a];
+        i0[a] = (long long)floor(base);
+        const double frac = base - (double)i0[a];
+        if (a == axis) { v[a][0] = -1.0 / steps[a]; v[a][1] = 1.0 / steps[a]; }
+        else { v[a][0] = 1.0 - frac; v[a][1] = frac; }
+      }
+      for (int b0 = 0; b0 < 2; ++b0) {
+        const long long g0 = i0[0] + b0;
+        if (g0 < 0 || g0 >= nb[0]) continue;
+        for (int b1 = 0; b1 < 2; ++b1) {
+          const long long g1 = i0[1] + b1;
+          if (g1 < 0 || g1 >= nb[1]) continue;
+          for (int b2 = 0; b2 < 2; ++b2) {
+            const long long g2 = i0[2] + b2;
+            if (g2 < 0 || g2 >= nb[2]) continue;
+            const double val = sphi[(g0 * g.ny + g1) * g.nz + g2];
+            acc += sign * val * ((v[0][b0] * v[1][b1]) * v[2][b2]);  // density.py:484
+          }
+        }
+      }
+    }
+    gacc[axis] = acc * g.bin_vol;
+  }
+  for (int a = 0; a < 3; ++a) grad[a] = gacc[a];
+  phibar = pacc * g.bin_vol / fmax(q.w * q.h * q.dep, 1e-300);
+}
+
+__global__ void __launch_bounds__(256) energy_grad_kernel(CloudArrays cl, p3d_grid g,
+                                                         const double* phi, const double* sphi,
+                                                         const uint8_t* freeze, double* grad,
+                                                         double* partials, unsigned int* counter,
+                                                         double* energy) {
+  __shared__ double red[32];
+  double e[1] = {0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cl.c.n; i += gridDim.x * blockDim.x) {
+    const Charge q = cl.get(i);
+    double gr[3], pb;
+    if (cl.is_macro(i)) {
+      macro_face_grad(q, g, sphi, gr, pb);
+    } else {
+      const Footprint f = footprint(q, g);
+      double tot = 0.0, a = 0.0;
+      for (int ix = f.ax.i0; ix <= f.ax.i1; ++ix) {  // density.py:376-386 on phi alone
+        const double wx = overlap_len(f.ax, ix, g.wb);
+        for (int iy = f.ay.i0; iy <= f.ay.i1; ++iy) {
+          const double wxy = wx * overlap_len(f.ay, iy, g.hb);
+          for (int iz = f.az.i0; iz <= f.az.i1; ++iz) {
+            const double vol = wxy * overlap_len(f.az, iz, g.db);
+            tot += vol;
+            a += phi[((long long)ix * g.ny + iy) * g.nz + iz] * vol;
+          }
+        }
+      }
+      pb = a / fmax(tot, 1e-300);
+      cell_face_grad(f, g, phi, gr);
+    }
+    const double w2 = 2.0 * q.weight;
+    grad[3 * i + 0] = gr[0] * w2;
+    grad[3 * i + 1] = gr[1] * w2;
+    grad[3 * i + 2] = (freeze && freeze[i]) ? 0.0 : gr[2] * w2;
+    e[0] += charge_of(q) * pb;
+  }
+  block_sum<1>(e, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = e[0];
+  if (last_block(counter)) {
+    const double s = ordered_sum(partials, gridDim.x, red);
+    if (threadIdx.x == 0) *energy = s;
+  }
+}
+
+void launch_energy_grad(const p3d_cloud& c, const p3d_grid& g, const double* phi,
+                        const uint8_t* freeze, double* energy, double* grad, double* scratch,
+                        cudaStream_t s) {
+  CloudArrays cl;
+  cl.c = c;
+  const long long B = (long long)g.nx * g.ny * g.nz;
+  double* sphi = scratch;  // [B]
+  unsigned int* counter = reinterpret_cast<unsigned int*>(scratch + B);
+  double* partials = scratch + B + 8;
+  const int lb = (int)((B + 255) / 256 > 1024 ? 1024 : (B + 255) / 256);
+  if (c.n_macro > 0) {
+    suffix_axis_kernel<<<lb, 256, 0, s>>>(phi, sphi, g.nx, g.ny, g.nz, 0);
+    suffix_axis_kernel<<<lb, 256, 0, s>>>(sphi, sphi, g.nx, g.ny, g.nz, 1);
+    suffix_axis_kernel<<<lb, 256, 0, s>>>(sphi, sphi, g.nx, g.ny, g.nz, 2);
+  }
+  const int nb = grid_blocks(c.n, 256, 1024);
+  energy_grad_kernel<<<nb, 256, 0, s>>>(cl, g, phi, sphi, freeze, grad, partials, counter, energy);
+}
+
+// ---------------------------------------------------------------------------
 // small elementwise / reduction ops of the per-op API
 // ---------------------------------------------------------------------------
 __global__ void fx_to_density_kernel(long long n, const int64_t* in, double* out) {

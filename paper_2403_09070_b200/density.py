@@ -350,6 +350,26 @@ def density_force(grid, cloud, ex, ey, ez, freeze_z=None):
     return _gather(grid, cloud, _interleave(grid, ex=ex, ey=ey, ez=ez), freeze_z)[1]
 
 
+def density_energy_and_gradient(grid, cloud, phi, ex=None, ey=None, ez=None, freeze_z=None):
+    """Energy U = sum q * phibar and its EXACT gradient (density.py:533-565):
+    cells through the two face columns of each axis, macros through their
+    differentiated corner stamps against the suffix-summed potential.  The
+    field maps are accepted for interface symmetry and unused, as in the
+    reference."""
+    _lib.require_cuda()
+    g, _ = grid.device()
+    dc = _DevCloud(cloud)
+    grad = torch.zeros((dc.n, 3), dtype=torch.float64, device="cuda")
+    energy = torch.zeros(1, dtype=torch.float64, device="cuda")
+    fr = None if freeze_z is None else _dev.u8(freeze_z)
+    scr = _dev.scratch(grid.n_bins + 8 + 1024)
+    if dc.n:
+        _lib.call("p3d_density_energy_gradient", _lib.byref(g), _lib.byref(dc.struct),
+                  _lib.ptr(_dev.f64(phi).reshape(-1).contiguous()), _lib.ptr(fr),
+                  _lib.ptr(energy), _lib.ptr(grad), _lib.ptr(scr), _lib.stream_ptr())
+    return float(energy.item()), grad
+
+
 def density_energy_and_force(grid, cloud, maps, freeze_z=None):
     """Energy and force from one interleaved map in one gather pass."""
     return _gather(grid, cloud, maps, freeze_z)
@@ -378,5 +398,6 @@ __all__ = [
     "accumulate_density", "accumulate_density_fx", "fx_to_density", "direct_density",
     "macro_prefix_density", "prefix_sum_3d", "suffix_sum_3d", "solve_potential",
     "electric_field", "potential_and_field", "density_energy", "density_force",
+    "density_energy_and_gradient",
     "density_energy_and_force", "overflow", "overflow_fx", "partition_from_z",
 ]

@@ -365,3 +365,96 @@ def test_precondition_examples():
     d = cpu(div)
     assert d[0] == pytest.approx(5.3) and d[1] == 1.0 and d[2] == pytest.approx(7.0)
     assert np.allclose(cpu(out)[0], 1 / 5.3) and np.allclose(cpu(out)[2], 1 / 7.0)
+
+
+# ---------------------------------------------------------------------------
+# exact energy gradient (density_energy_and_gradient)
+# ---------------------------------------------------------------------------
+
+
+def _cloud_of(boxes, macro=None, weight=None):
+    from paper_2403_09070_b200 import density as dn
+
+    b = np.asarray(boxes, dtype=np.float64)
+    n = len(b)
+    return dn.ChargeCloud(b[:, 0].copy(), b[:, 1].copy(), b[:, 2].copy(), b[:, 3].copy(),
+                          b[:, 4].copy(), b[:, 5].copy(),
+                          np.ones(n) if weight is None else np.asarray(weight, float),
+                          np.zeros(n, bool) if macro is None else np.asarray(macro, bool))
+
+
+def _device_solve(grid, cloud):
+    from paper_2403_09070_b200 import density as dn
+
+    rho = dn.accumulate_density(grid, cloud)
+    phi, coef = dn.solve_potential(rho, grid)
+    return phi
+
+
+def test_energy_gradient_vs_reference_golden():
+    """Against the reference's own density_energy_and_gradient output
+    (tests/golden/energy_grad.npz): cells, macros, clipped boxes, frozen z."""
+    from paper_2403_09070_b200 import density as dn
+
+    g = dict(np.load(os.path.join(GOLD, "energy_grad.npz")))
+    grid = dn.DensityGrid(16.0, 12.0, 16, 12, 8)
+    cl = dn.ChargeCloud(*(g["a_" + k] for k in ("x", "y", "z", "w", "h", "dep", "weight",
+                                                "is_macro")))
+    e, grad = dn.density_energy_and_gradient(grid, cl, g["a_phi"], freeze_z=g["a_freeze"])
+    assert e == pytest.approx(float(g["a_energy"]), rel=1e-12)
+    assert rel(grad, g["a_grad"]) < 1e-13
+    assert np.all(cpu(grad)[g["a_freeze"], 2] == 0.0)
+
+
+def test_energy_gradient_symmetric_pair_and_macro_path():
+    """test_density.py:352-387 restated on the device: a mirrored pair feels
+    opposite forces; a macro's stamp-form gradient equals the cell face form."""
+    from paper_2403_09070_b200 import density as dn
+
+    grid = dn.DensityGrid(16, 16, 16, 16, 8)
+    c, a = 8.0, 1.3
+    cloud = _cloud_of([(c - a, 8, grid.dz / 2, 2, 2, grid.dz / 2),
+                       (c + a, 8, grid.dz / 2, 2, 2, grid.dz / 2)])
+    _, grad = dn.density_energy_and_gradient(grid, cloud, _device_solve(grid, cloud))
+    g = cpu(grad)
+    assert g[0, 0] == pytest.approx(-g[1, 0], rel=1e-9) and g[0, 0] > 0 > g[1, 0]
+    rng = np.random.default_rng(15)
+    grid = dn.DensityGrid(16, 12, 8, 8, 8)
+    for _ in range(10):
+        w, h = rng.uniform(2, 8), rng.uniform(2, 6)
+        box = (rng.uniform(w / 2, 16 - w / 2), rng.uniform(h / 2, 12 - h / 2),
+               rng.uniform(grid.dz / 4, 3 * grid.dz / 4), w, h, grid.dz / 2)
+        filler = (4.0, 3.0, grid.dz / 4, 1.5, 1.5, grid.dz / 2)
+        as_macro = _cloud_of([box, filler], macro=[True, False])
+        as_cell = _cloud_of([box, filler], macro=[False, False])
+        phi = _device_solve(grid, as_macro)
+        _, g1 = dn.density_energy_and_gradient(grid, as_macro, phi)
+        _, g2 = dn.density_energy_and_gradient(grid, as_cell, phi)
+        assert float((g1 - g2).abs().max()) < 1e-9
+
+
+def test_energy_gradient_matches_finite_difference():
+    """test_density.py:407-440 restated: central differences of U (each probe a
+    full device density + spectral solve) match the exact gradient."""
+    from paper_2403_09070_b200 import density as dn
+
+    rng = np.random.default_rng(17)
+    grid = dn.DensityGrid(16, 16, 16, 16, 16)
+    boxes = [(int(rng.integers(4, 12)) + rng.uniform(0.3, 0.7),
+              int(rng.integers(4, 12)) + rng.uniform(0.3, 0.7),
+              grid.dz * 0.5 + rng.uniform(-2, 2), 2.5, 2.5, grid.dz / 2) for _ in range(6)]
+    cloud = _cloud_of(boxes)
+    _, grad = dn.density_energy_and_gradient(grid, cloud, _device_solve(grid, cloud))
+    grad = cpu(grad)
+
+    def energy_at(i, axis, dx):
+        b = [list(t) for t in boxes]
+        b[i][axis] += dx
+        c = _cloud_of(b)
+        return dn.density_energy_and_gradient(grid, c, _device_solve(grid, c))[0]
+
+    h = 0.01
+    for i in range(len(boxes)):
+        for axis in (0, 1):
+            fd = (energy_at(i, axis, h) - energy_at(i, axis, -h)) / (2 * h)
+            assert grad[i, axis] == pytest.approx(fd, rel=0.02, abs=1e-9)  # test_density.py:442
