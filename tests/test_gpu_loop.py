@@ -110,3 +110,14 @@ def test_single_instance_converges():
     assert info.iterations <= 3
     assert 2 <= st.x[0] <= 62
     assert st.z[0] in (grid.dz / 4, 3 * grid.dz / 4)
+
+
+def test_run_to_run_bit_identical():
+    """Determinism claim: integer density, ordered reductions,
+    pin-ordered owner sums -> two runs give bit-identical logs and positions."""
+    spec = dict(n_insts=3000, n_macros=5, r_ma=0.3, seed=9, nets_per_inst=1.2)
+    a = _run(spec, 64, 40)
+    b = _run(spec, 64, 40)
+    assert a[0] == b[0]
+    assert np.array_equal(a[2].x, b[2].x) and np.array_equal(a[2].y, b[2].y)
+    assert np.array_equal(a[2].z, b[2].z)
