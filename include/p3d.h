@@ -200,7 +200,7 @@ typedef struct p3d_gp {
   int32_t n_inst, n_fill, n_obj, n_macro;
   int32_t max_iters, divergence_window, nblk_obj, nblk_net;
   int32_t wl_f32;              /* 1: WA sums in fp32 on anchored differences */
-  int32_t pad1;
+  int32_t nblk_dens;           /* K4 CTAs (besides one per macro) */
   p3d_topology topo;           /* n_obj = n_inst here */
   /* degree-bucketed, transposed pin layout of the fused K1 (built by the host) */
   int32_t f_n_tasks, f_n_generic;

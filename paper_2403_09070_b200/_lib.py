@@ -58,7 +58,7 @@ class LoopState(C.Structure):
 class Gp(C.Structure):
     _fields_ = [("n_inst", I32), ("n_fill", I32), ("n_obj", I32), ("n_macro", I32),
                 ("max_iters", I32), ("divergence_window", I32), ("nblk_obj", I32),
-                ("nblk_net", I32), ("wl_f32", I32), ("pad1", I32), ("topo", Topology),
+                ("nblk_net", I32), ("wl_f32", I32), ("nblk_dens", I32), ("topo", Topology),
                 ("f_n_tasks", I32), ("f_n_generic", I32), ("f_generic_nets", P), ("f_tasks", P), ("f_task_t0", P),
                 ("f_net_base", P), ("f_net_deg", P), ("f_net_stride", P), ("f_net_dup", P),
                 ("f_pin_inst", P), ("f_pin_off", P), ("f_pin_slot", P), ("grid", Grid),

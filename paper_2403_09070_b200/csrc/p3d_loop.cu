@@ -667,7 +667,7 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
   mark(3);
   if (const int rc = launch_k3(gp, s)) return rc;  // K3 (+ overflow, re-zero)
   mark(4);
-  dens_kernel<<<gp.n_macro + gp.nblk_obj, 256, 0, s>>>(gp);  // K4
+  dens_kernel<<<gp.n_macro + gp.nblk_dens, 256, 0, s>>>(gp);  // K4
   mark(5);
   return check_launch("gp evaluation kernels");
 }
@@ -814,7 +814,7 @@ int gp_shard_stage(const p3d_gp& gp, int stage, cudaStream_t s) {
       break;
     case P3D_SH_SCATTER: scatter_k2(gp, &gp.st->done, s); break;
     case P3D_SH_SPECTRAL: if (const int rc = launch_k3(gp, s)) return rc; break;
-    case P3D_SH_DENS: dens_kernel<<<gp.n_macro + gp.nblk_obj, 256, 0, s>>>(gp); break;
+    case P3D_SH_DENS: dens_kernel<<<gp.n_macro + gp.nblk_dens, 256, 0, s>>>(gp); break;
     case P3D_SH_CONTROL: shard_control_kernel<<<1, 1, 0, s>>>(gp); break;
     case P3D_SH_STEP0: gmax0_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp); break;
     case P3D_SH_STEP0_CONTROL: step0_control_kernel<<<1, 1, 0, s>>>(gp); break;

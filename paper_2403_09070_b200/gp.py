@@ -382,12 +382,18 @@ class Gp3dProblem:
         g.sh_f0, g.sh_f1 = self.sh_f
         macro_ids = macro_ids[(macro_ids >= self.sh_i[0]) & (macro_ids < self.sh_i[1])]
         g.n_macro = len(macro_ids)
-        if g.n_macro > K_MAX_BLOCKS:
+        if g.n_macro >= K_MAX_BLOCKS:
             raise ValueError(f"{g.n_macro} macros exceed the per-launch CTA budget {K_MAX_BLOCKS}")
         mi = max(self.max_iters, 1)
         g.max_iters = self.max_iters
         g.divergence_window = int(cfg.divergence_window)
-        g.nblk_obj = max(1, min(-(-O // 256), K_MAX_BLOCKS))
+        # object kernels run persistent waves of 256-thread CTAs: K5 with 8 per
+        # SM, K4 (64 registers) with the 4 per SM it can hold
+        n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        g.nblk_obj = max(1, min(-(-O // 256), K_MAX_BLOCKS,
+                                int(os.environ.get("P3D_NBLK_OBJ", 8 * n_sm))))
+        g.nblk_dens = max(1, min(-(-O // 256), K_MAX_BLOCKS - g.n_macro,
+                                 int(os.environ.get("P3D_NBLK_DENS", 4 * n_sm))))
         g.nblk_net = max(1, min(-(-max(arr.n_net, 1) // 256), K_MAX_BLOCKS))
         tp = dt.struct
         g.topo = _lib.Topology(tp.n_net, tp.n_pin, I, 0, tp.net_ptr, tp.pin_inst, tp.net_dup,
@@ -409,8 +415,7 @@ class Gp3dProblem:
         g.f_pin_inst = keep(_dev.i32(one(L["pin_inst"], np.int64)))
         g.f_pin_off = keep(_dev.dev(one(L["pin_off"].reshape(-1), np.float32), torch.float32))
         g.f_pin_slot = keep(_dev.i32(one(L["pin_slot"], np.int64)))
-        # K1 runs one wave of persistent CTAs (5 resident 128-thread CTAs per SM)
-        n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        # K1 runs one persistent wave (5 resident 128-thread CTAs per SM)
         g.nblk_net = max(1, min(-(-g.f_n_tasks // 4), K_MAX_BLOCKS,
                                 int(os.environ.get("P3D_NBLK_NET", 5 * n_sm))))
         gs, gkeep = grid.device()
