@@ -338,6 +338,16 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
   }
 }
 
+// the per-pin loops of the staged path: not unrolled by default (register
+// budget); -DP3D_K1_FULL_UNROLL unrolls them (D is a template constant)
+#ifdef P3D_K1_FULL_UNROLL
+#define P3D_K1_LOOP_UNROLL _Pragma("unroll")
+#else
+#define P3D_K1_LOOP_UNROLL _Pragma("unroll 1")
+#endif
+#ifndef P3D_K1_RTD
+#define P3D_K1_RTD 0
+#endif
 #ifndef P3D_K1_MINB
 #define P3D_K1_MINB 5
 #endif
@@ -365,13 +375,15 @@ struct WarpCols {
 template <int D, bool F32>
 __device__ __forceinline__ void staged_axis(double (&c)[kMaxStagedDeg][32], WarpCols<F32>& sm,
                                             int lane, int topm, typename WaSel<F32>::R ig,
-                                            double& val, double& exact, bool& crossing) {
+                                            double& val, double& exact, bool& crossing, int nd) {
   using W = typename WaSel<F32>::W;
   using R = typename WaSel<F32>::R;
+  const int DD = D ? D : nd;  // D = 0: runtime degree (one code path for every degree)
   Box2 bx;
   bx.init();
 #pragma unroll
-  for (int k = 0; k < D; ++k) bx.add(c[k][lane], (topm >> k) & 1);
+  for (int k = 0; k < (D ? D : kMaxStagedDeg); ++k)
+    if (k < DD) bx.add(c[k][lane], (topm >> k) & 1);
   const double full = bx.full(), part = bx.t.span() + bx.b.span();
   const double ex = fmax(full, part);
   const bool split = part > full;  // ties resolve to the full box (wirelength.py:186)
@@ -384,8 +396,8 @@ __device__ __forceinline__ void staged_axis(double (&c)[kMaxStagedDeg][32], Warp
   W w0, w1;
   w0.init();
   w1.init();
-#pragma unroll 1
-  for (int k = 0; k < D; ++k) {
+P3D_K1_LOOP_UNROLL
+  for (int k = 0; k < DD; ++k) {
     const double v = c[k][lane];
     const bool up = (umask >> k) & 1;
     R ep, em;
@@ -404,8 +416,8 @@ __device__ __forceinline__ void staged_axis(double (&c)[kMaxStagedDeg][32], Warp
     k1 = w1.gk(h1, l1);
   }
   const GradK<R> k0 = w0.gk(h0, l0);
-#pragma unroll 1
-  for (int k = 0; k < D; ++k) {
+P3D_K1_LOOP_UNROLL
+  for (int k = 0; k < DD; ++k) {
     const double v = c[k][lane];
     const bool up = (umask >> k) & 1;
     const GradK<R> gk = {up ? k1.rp : k0.rp, up ? k1.rm : k0.rm, up ? k1.vp : k0.vp,
@@ -425,10 +437,13 @@ __device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk,
   const int nb = tk.y, j = tk.z + lane;
   if (j >= nb || a.net_dup[t0 + j]) return false;  // duplicate-owner nets: generic kernel
   const int pin0 = tk.x + j;
-  int inst[D];
-  float4 off[D];
+  constexpr int KM = D ? D : kMaxStagedDeg;
+  const int DD = D ? D : tk.w;
+  int inst[KM];
+  float4 off[KM];
 #pragma unroll
-  for (int k = 0; k < D; ++k) {
+  for (int k = 0; k < KM; ++k) {
+    if (k >= DD) break;
     inst[k] = a.pin_inst[pin0 + k * nb];
     off[k] = a.off[pin0 + k * nb];
   }
@@ -436,7 +451,8 @@ __device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk,
   zhi = -P3D_INF;
   zlo = P3D_INF;
 #pragma unroll
-  for (int k = 0; k < D; ++k) {
+  for (int k = 0; k < KM; ++k) {
+    if (k >= DD) break;
     const double4 p = a.pos4[inst[k]];
     const int tp = (p.z - a.dz2) > 0.0;
     topm |= tp << k;
@@ -452,15 +468,17 @@ __device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk,
 template <int D, bool F32>
 __device__ __forceinline__ void staged_eval(const FusedNetArgs& a, int pin0, int nb,
                                             WarpCols<F32>& sm, int lane, int topm, double zhi,
-                                            double zlo, double (&acc)[6]) {
+                                            double zlo, double (&acc)[6], int nd) {
   using W = typename WaSel<F32>::W;
   using R = typename WaSel<F32>::R;
   const R ig = (R)a.inv_gamma;
+  constexpr int KM = D ? D : kMaxStagedDeg;
+  const int DD = D ? D : nd;
   // z-cut phase first: its column is then recycled as the FD accumulator
   W wz;
   wz.init();
-#pragma unroll 1
-  for (int k = 0; k < D; ++k) {
+P3D_K1_LOOP_UNROLL
+  for (int k = 0; k < DD; ++k) {
     R ep, em;
     W::term(sm.pz[k][lane], zhi, zlo, ig, ep, em);
     sm.ep[k][lane] = ep;
@@ -470,25 +488,29 @@ __device__ __forceinline__ void staged_eval(const FusedNetArgs& a, int pin0, int
   wz.finalize();
   acc[2] += wz.value(zhi, zlo);
   const GradK<R> kz = wz.gk(zhi, zlo);
-#pragma unroll 1
-  for (int k = 0; k < D; ++k) {
+P3D_K1_LOOP_UNROLL
+  for (int k = 0; k < DD; ++k) {
     sm.gc[k][lane] = (double)kz.grad(sm.pz[k][lane], ig, sm.ep[k][lane], sm.em[k][lane]);
     sm.pz[k][lane] = 0.0;
   }
   double v, ex;
   bool cross;
-  staged_axis<D, F32>(sm.px, sm, lane, topm, ig, v, ex, cross);
+  staged_axis<D, F32>(sm.px, sm, lane, topm, ig, v, ex, cross, nd);
   acc[0] += v;
   acc[3] += ex;
   acc[5] += cross ? 1.0 : 0.0;
-  staged_axis<D, F32>(sm.py, sm, lane, topm, ig, v, ex, cross);
+  staged_axis<D, F32>(sm.py, sm, lane, topm, ig, v, ex, cross, nd);
   acc[1] += v;
   acc[4] += ex;
-  int slot[D];
+  int slot[KM];
 #pragma unroll
-  for (int k = 0; k < D; ++k) slot[k] = a.slot[pin0 + k * nb];
+  for (int k = 0; k < KM; ++k) {
+    if (k >= DD) break;
+    slot[k] = a.slot[pin0 + k * nb];
+  }
 #pragma unroll
-  for (int k = 0; k < D; ++k) {
+  for (int k = 0; k < KM; ++k) {
+    if (k >= DD) break;
     const double dwk = sm.pz[k][lane];
     const double gb = (((topm >> k) & 1) ? -dwk : dwk) * a.scale4;
     if (F32)
@@ -565,10 +587,11 @@ __device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, 
 template <int D, bool F32>
 __device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk, int t0,
                                             WarpCols<F32>& sm, int lane, double (&acc)[6]) {
+  const int nd = tk.w;
   int topm;
   double zhi, zlo;
   if (stage_pins<D, F32>(a, tk, t0, sm, lane, topm, zhi, zlo))
-    staged_eval<D, F32>(a, tk.x + tk.z + lane, tk.y, sm, lane, topm, zhi, zlo, acc);
+    staged_eval<D, F32>(a, tk.x + tk.z + lane, tk.y, sm, lane, topm, zhi, zlo, acc, nd);
 }
 
 template <bool F32>
@@ -595,10 +618,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_ke
 #endif
     switch (tk.w) {
       case 2: pair_task<F32>(a, tk, t0, lane, acc); break;
+#if P3D_K1_RTD
+      case 3: case 4: case 5: case 6: staged_task<0, F32>(a, tk, t0, sm, lane, acc); break;
+#else
       case 3: staged_task<3, F32>(a, tk, t0, sm, lane, acc); break;
       case 4: staged_task<4, F32>(a, tk, t0, sm, lane, acc); break;
       case 5: staged_task<5, F32>(a, tk, t0, sm, lane, acc); break;
       case 6: staged_task<6, F32>(a, tk, t0, sm, lane, acc); break;
+#endif
       default: break;  // generic nets run in generic_net_kernel
     }
   }
