@@ -164,6 +164,19 @@ int p3d_density_energy_gradient(const p3d_grid* g, const p3d_cloud* c, const dou
                                 const uint8_t* freeze_z, double* energy, double* grad,
                                 double* scratch, void* stream);
 
+/* Multi-die 2D GP wirelength (gp.py:586-600, _segment_wa wirelength.py:76-98
+ * over the augmented pin list of gp.py:482-498): per (net, partial net)
+ * weighted-average span on x and y; value = sum of all segment values (one
+ * double); wl_grad [n_obj][2] = per-object owner sums of the per-pin
+ * gradients in pin order.  pos [2][n_obj]; net_ptr/pin_* describe the
+ * augmented CSR (pins sorted by net), pin_slot/obj_slot_ptr its owner-sorted
+ * slots.  scratch: zeroed, >= 2*n_pin + 8 + 1024 doubles. */
+int p3d_gp2d_wirelength(int32_t n_net, int32_t n_pin, int32_t n_obj, const int32_t* net_ptr,
+                        const int32_t* pin_obj, const uint8_t* pin_top, const double* pin_ox,
+                        const double* pin_oy, const int32_t* pin_slot,
+                        const int32_t* obj_slot_ptr, const double* pos, double gamma,
+                        double* value, double* wl_grad, double* scratch, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* optimiser pieces (gp.py:142-147, 178-227, 280-294)                        */
 /* ------------------------------------------------------------------------ */

@@ -1009,3 +1009,212 @@ class Cfg:
     jitter_frac: float = 0.02
     divergence_window: int = 100
     threads: int = 1
+
+
+# ==========================================================================
+# multi-die 2D GP (gp.py:463-690)
+# ==========================================================================
+
+
+def optimal_region(top_box, bot_box):
+    """wirelength.py:153-164."""
+    out = []
+    for a in (0, 2):
+        lo = max(top_box[a], bot_box[a])
+        hi = min(top_box[a + 1], bot_box[a + 1])
+        out.extend((min(lo, hi), max(lo, hi)))
+    return tuple(out)
+
+
+def hbt_centers(arr, x, y, z, rot, dz):
+    """wirelength.py:325-342 (optimal_hbt_centers): {net: (cx, cy)} per
+    crossing net, the centre of the zero-added-wirelength region."""
+    px, py, _, top = pins_at(arr, x, y, z, rot, dz)
+    bx = Boxes(arr.pin_net, arr.n_net, px, top)
+    by = Boxes(arr.pin_net, arr.n_net, py, top)
+    crossing = np.flatnonzero((bx.cnt[:, 0] > 0) & (bx.cnt[:, 1] > 0))
+    out = {}
+    for j in crossing:
+        r = optimal_region((bx.min1[j, 1], bx.max1[j, 1], by.min1[j, 1], by.max1[j, 1]),
+                           (bx.min1[j, 0], bx.max1[j, 0], by.min1[j, 0], by.max1[j, 0]))
+        out[int(j)] = ((r[0] + r[1]) / 2, (r[2] + r[3]) / 2)
+    return out
+
+
+class Gp2d:
+    """gp.py:463-528 (Gp2dProblem): three nz = 1 grids (bottom, top, terminal
+    layer), the augmented pin list in which each HBT joins both partial nets of
+    its crossing net, and pin offsets frozen at the partition."""
+
+    def __init__(self, design, cfg, delta, rot, n_grid):
+        arr = design.arrays()
+        self.arr = arr
+        self.delta = np.asarray(delta)
+        die = design.die
+        self.grids = [Grid(die.width, die.height, n_grid, n_grid, 1) for _ in range(3)]
+        pd = self.delta[arr.pin_inst]
+        mx = np.zeros(design.n_nets, dtype=np.int8)
+        mn = np.ones(design.n_nets, dtype=np.int8)
+        np.maximum.at(mx, arr.pin_net, pd)
+        np.minimum.at(mn, arr.pin_net, pd)
+        self.crossing = np.flatnonzero(mx > mn)
+        self.n_inst = design.n_insts
+        self.n_hbt = len(self.crossing)
+        self.n_core = self.n_inst + self.n_hbt
+        pin_net = np.r_[arr.pin_net, self.crossing, self.crossing]
+        pin_obj = np.r_[arr.pin_inst, self.n_inst + np.arange(self.n_hbt),
+                        self.n_inst + np.arange(self.n_hbt)]
+        top = np.r_[pd == 1, np.ones(self.n_hbt, bool), np.zeros(self.n_hbt, bool)]
+        order = np.argsort(pin_net, kind="stable")
+        self.pin_net, self.pin_obj, self.pin_top = pin_net[order], pin_obj[order], top[order]
+        cnt = np.bincount(self.pin_net, minlength=design.n_nets)
+        self.net_ptr = np.zeros(design.n_nets + 1, dtype=np.int64)
+        np.cumsum(cnt, out=self.net_ptr[1:])
+        wt, ht = turn_offsets_dims(arr.w_top, arr.h_top, rot)
+        wb, hb = turn_offsets_dims(arr.w_bot, arr.h_bot, rot)
+        self.inst_w = np.where(self.delta == 1, wt, wb)
+        self.inst_h = np.where(self.delta == 1, ht, hb)
+        self.hbt_size = design.hbt.pitch + design.hbt.spacing
+        q = np.asarray(rot)[arr.pin_inst]
+        rx_t, ry_t = turn_offsets(arr.ox_top, arr.oy_top, q)
+        rx_b, ry_b = turn_offsets(arr.ox_bot, arr.oy_bot, q)
+        it = pd == 1
+        self.pin_ox = np.r_[np.where(it, rx_t, rx_b), np.zeros(2 * self.n_hbt)][order]
+        self.pin_oy = np.r_[np.where(it, ry_t, ry_b), np.zeros(2 * self.n_hbt)][order]
+
+
+def turn_offsets_dims(w, h, q):
+    """model.py:292-295 (rotated_dims): w/h swap on odd quarter turns."""
+    odd = (np.asarray(q) % 4) % 2 == 1
+    return np.where(odd, h, w), np.where(odd, w, h)
+
+
+def gp2d_grid_n(n_insts):
+    """gp.py:536-539."""
+    n = max(n_insts, 1)
+    k = 2
+    while (2 ** (k + 1)) ** 2 <= n / 4 and 2 ** (k + 1) <= 128:
+        k += 1
+    return 2 ** k
+
+
+def gp2d_run(design, x, y, z, rot, dz, cfg, rng, log=None):
+    """gp.py:531-690 (run_gp2d_multi): returns (x, y, info, hbt_centers)."""
+    delta = (np.asarray(z) - dz / 2 > 0).astype(np.int8)
+    prob = Gp2d(design, cfg, delta, rot, gp2d_grid_n(design.n_insts))
+    die = design.die
+    grids = prob.grids
+    arr = prob.arr
+    cells = ~arr.is_macro
+    hint = float(np.median(arr.w_bot[cells] * arr.h_bot[cells])) if cells.any() \
+        else (die.width / 32) ** 2
+    fxy, fwh, flay = [], [], []
+    for layer, u in ((0, die.max_util_bottom), (1, die.max_util_top)):  # gp.py:552-562
+        area = die.width * die.height * (1 - u)
+        if area <= 0:
+            continue
+        count = int(np.clip(round(area / max(hint, 1e-9)), 1, 20000))
+        side = math.sqrt(area / count)
+        fxy.append(np.c_[rng.uniform(side / 2, die.width - side / 2, count),
+                         rng.uniform(side / 2, die.height - side / 2, count)])
+        fwh.append(np.full((count, 2), side))
+        flay.append(np.full(count, layer))
+    fx = np.concatenate(fxy) if fxy else np.zeros((0, 2))
+    fwh = np.concatenate(fwh) if fwh else np.zeros((0, 2))
+    flay = np.concatenate(flay) if flay else np.zeros(0, int)
+    n_core = prob.n_core
+    n_obj = n_core + len(fx)
+    pos = np.zeros((n_obj, 2))
+    pos[: prob.n_inst] = np.c_[x, y]
+    cen = hbt_centers(arr, x, y, z, rot, dz)
+    for t, j in enumerate(prob.crossing):
+        pos[prob.n_inst + t] = cen.get(int(j), (die.width / 2, die.height / 2))
+    pos[n_core:] = fx
+    size_w = np.r_[prob.inst_w, np.full(prob.n_hbt, prob.hbt_size), fwh[:, 0]]
+    size_h = np.r_[prob.inst_h, np.full(prob.n_hbt, prob.hbt_size), fwh[:, 1]]
+    obj_layer = np.r_[delta.astype(int), np.full(prob.n_hbt, 2), flay]
+    is_macro = np.r_[arr.is_macro, np.zeros(prob.n_hbt + len(fx), bool)]
+    degree = np.r_[arr.pin_degree, np.full(prob.n_hbt, 2.0), np.zeros(len(fx))]
+    is_filler = np.r_[np.zeros(n_core, bool), np.ones(len(fx), bool)]
+
+    def project(p):
+        out = p.copy()
+        out[:, 0] = clamp_span(out[:, 0], size_w, die.width)
+        out[:, 1] = clamp_span(out[:, 1], size_h, die.height)
+        return out
+
+    mv = [float((size_w[m] * size_h[m]).sum() * grids[l].db)
+          for l, m in enumerate([(obj_layer == l) & ~is_filler for l in range(3)])]
+    seg = prob.pin_net * 2 + prob.pin_top.astype(np.int64)
+    n_net = len(prob.net_ptr) - 1
+
+    def evaluate(p, gamma):  # gp.py:586-626
+        px = p[prob.pin_obj, 0] + prob.pin_ox
+        py = p[prob.pin_obj, 1] + prob.pin_oy
+        val = 0.0
+        gxp = np.zeros(len(px))
+        gyp = np.zeros(len(px))
+        for c, gp_ in ((px, gxp), (py, gyp)):
+            v, g = wa_segments(seg, 2 * n_net, c, gamma)
+            val += float(v.sum())
+            gp_ += g
+        wl_g = np.c_[np.bincount(prob.pin_obj, weights=gxp, minlength=n_obj),
+                     np.bincount(prob.pin_obj, weights=gyp, minlength=n_obj)]
+        dg = np.zeros((n_obj, 2))
+        ovfls = []
+        for layer in range(3):
+            m = obj_layer == layer
+            g = grids[layer]
+            if not m.any():
+                ovfls.append(0.0)
+                continue
+            k = int(m.sum())
+            cl = Cloud(p[m, 0], p[m, 1], np.full(k, g.dz / 2), size_w[m], size_h[m],
+                       np.full(k, g.dz), np.where(is_macro[m], cfg.target_density, 1.0),
+                       is_macro[m])
+            rho = rho_map(g, cl)
+            phi, coef = potential(rho, g)
+            ex, ey, _ = efield(coef, g)
+            dg[m] = force(g, cl, ex, ey, np.zeros_like(phi))[:, :2]
+            ovfls.append(overflow_of(rho, g, cfg.target_density, mv[layer]))
+        return val, wl_g, dg, ovfls
+
+    opt = Nesterov(pos, project=project)
+    info = LoopInfo()
+    lams = None
+    charges = size_w * size_h * grids[0].db
+    prev = [math.inf] * 3
+    prev_raw = None
+    for it in range(cfg.max_iters):  # gp.py:637-681
+        gamma = gamma_at(grids[0].db, it, cfg.max_iters, cfg)
+        val, wl_g, dg, ovfls = evaluate(opt.v, gamma)
+        if lams is None:
+            lams = [lam0(np.abs(wl_g[obj_layer == l]).sum(), np.abs(dg[obj_layer == l]).sum())
+                    for l in range(3)]
+        worst = max(ovfls)
+        info.iterations = it + 1
+        info.final_overflow = worst
+        if log is not None:
+            log.append((it, val, prob.n_hbt, worst))
+        if worst <= cfg.stop_overflow:
+            break
+        lam_obj = np.array([lams[l] for l in obj_layer])
+        total = wl_g + lam_obj[:, None] * dg
+        pre, _ = precond(total, 1.0, lam_obj * charges, degree, is_macro)
+        pre_prev = None
+        if prev_raw is not None:
+            pre_prev, _ = precond(prev_raw[0] + lam_obj[:, None] * prev_raw[1], 1.0,
+                                  lam_obj * charges, degree, is_macro)
+        prev_raw = (wl_g, dg)
+        try:
+            opt.advance(pre, step_scale=grids[0].wb, g_prev_reval=pre_prev)
+        except StepUnderflow:
+            info.diverged = True
+            break
+        for l in range(3):
+            lams[l] *= mu_of(prev[l], ovfls[l], cfg)
+            prev[l] = ovfls[l]
+    final = project(opt.u)
+    centers = {int(j): (float(final[prob.n_inst + t, 0]), float(final[prob.n_inst + t, 1]))
+               for t, j in enumerate(prob.crossing)}
+    return final[: prob.n_inst, 0].copy(), final[: prob.n_inst, 1].copy(), info, centers

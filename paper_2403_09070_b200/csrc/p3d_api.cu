@@ -295,6 +295,30 @@ int p3d_density_energy_gradient(const p3d_grid* g, const p3d_cloud* c, const dou
   return check_launch("density_energy_gradient");
 }
 
+int p3d_gp2d_wirelength(int32_t n_net, int32_t n_pin, int32_t n_obj, const int32_t* net_ptr,
+                        const int32_t* pin_obj, const uint8_t* pin_top, const double* pin_ox,
+                        const double* pin_oy, const int32_t* pin_slot,
+                        const int32_t* obj_slot_ptr, const double* pos, double gamma,
+                        double* value, double* wl_grad, double* scratch, void* stream) {
+  if (n_net < 0 || n_pin < 0 || n_obj < 0 || !net_ptr || !pos || !value || !wl_grad || !scratch ||
+      (n_pin > 0 && (!pin_obj || !pin_top || !pin_ox || !pin_oy || !pin_slot)) || !obj_slot_ptr ||
+      !(gamma > 0)) {
+    set_error("gp2d_wirelength: bad args");
+    return P3D_ERR_ARG;
+  }
+  Gp2dWlArgs a{};
+  a.n_net = n_net; a.n_obj = n_obj;
+  a.net_ptr = net_ptr; a.pin_obj = pin_obj; a.pin_top = pin_top;
+  a.pin_ox = pin_ox; a.pin_oy = pin_oy; a.pin_slot = pin_slot; a.obj_slot_ptr = obj_slot_ptr;
+  a.pos = pos; a.gamma = gamma;
+  a.rec = scratch;
+  a.counter = reinterpret_cast<unsigned int*>(scratch + 2 * (long long)n_pin);
+  a.partials = scratch + 2 * (long long)n_pin + 8;
+  a.value = value;
+  launch_gp2d_wl(a, wl_grad, STREAM(stream));
+  return check_launch("gp2d_wirelength");
+}
+
 int p3d_precondition(int32_t n, const double* gr, double lam, const double* q, const double* deg,
                      const uint8_t* macro, double* out, double* div, void* stream) {
   if (n < 0 || !gr || !q || !deg || !out) { set_error("precondition: bad args"); return P3D_ERR_ARG; }

@@ -108,6 +108,24 @@ struct FusedGatherArgs {
 };
 
 void launch_fused_net(const FusedNetArgs& a, bool f32, cudaStream_t s);
+
+// multi-die 2D GP wirelength (p3d_gp2d.cu)
+struct Gp2dWlArgs {
+  int n_net, n_obj;
+  const int32_t* net_ptr;      // [n_net+1] augmented CSR
+  const int32_t* pin_obj;      // [n_pin]
+  const uint8_t* pin_top;      // [n_pin] partial net (1: top)
+  const double *pin_ox, *pin_oy;  // [n_pin] offsets frozen at the partition
+  const int32_t* pin_slot;     // [n_pin] owner-sorted record slot
+  const int32_t* obj_slot_ptr; // [n_obj+1]
+  const double* pos;           // [2][n_obj]
+  double gamma;
+  double* rec;                 // [n_pin][2] per-pin gradients by slot
+  double* partials;            // [blocks]
+  unsigned int* counter;
+  double* value;               // 1 double: sum over segments of the WA spans
+};
+void launch_gp2d_wl(const Gp2dWlArgs& a, double* wl_grad, cudaStream_t s);
 void fused_net_setup();
 void launch_fused_gather(const FusedGatherArgs& a, cudaStream_t s);
 

@@ -181,7 +181,13 @@ def precondition(gradients, lam, charges, pin_degrees, macro_flags):
     _lib.require_cuda()
     g = _dev.f64(gradients)
     shape = g.shape
-    g = g.reshape(-1, 3) if g.dim() == 2 else g.reshape(-1, 1).expand(-1, 3).contiguous()
+    k = shape[1] if g.dim() == 2 else 0
+    if k == 3:
+        g = g.contiguous()
+    elif k:  # [n, k] (e.g. the 2D GP's [n, 2]): padded to the kernel's 3 columns
+        g = torch.cat([g, torch.zeros((g.shape[0], 3 - k), dtype=g.dtype, device=g.device)], 1)
+    else:
+        g = g.reshape(-1, 1).expand(-1, 3).contiguous()
     n = g.shape[0]
     q = _dev.f64(charges)
     deg = _dev.f64(pin_degrees)
@@ -192,6 +198,8 @@ def precondition(gradients, lam, charges, pin_degrees, macro_flags):
               _lib.ptr(m), _lib.ptr(out), _lib.ptr(div), _lib.stream_ptr())
     if len(shape) != 2:
         out = out[:, 0].reshape(shape)
+    elif k != 3:
+        out = out[:, :k].contiguous()
     return out, div
 
 

@@ -175,6 +175,26 @@ def optimal_region(top_box, bot_box):
     return tuple(out)
 
 
+def optimal_hbt_centers(arrays, x, y, z, rot, dz):
+    """Optimal-region centre per crossing net (wirelength.py:325-342):
+    {net index: (cx, cy)} for nets with pins on both dies; the boxes run on the
+    device (NetBoxes), the dict is assembled on the host."""
+    topo = NetTopology.from_arrays(arrays)
+    px, py, _, on_top = dynamic_pin_coords(arrays, x, y, z, rot, dz)
+    bx = NetBoxes(topo, px, on_top)
+    by = NetBoxes(topo, py, on_top)
+    cnt = bx.cnt.cpu().numpy()
+    crossing = np.flatnonzero((cnt[:, 0] > 0) & (cnt[:, 1] > 0))
+    mnx, mxx = bx.min1.cpu().numpy(), bx.max1.cpu().numpy()
+    mny, mxy = by.min1.cpu().numpy(), by.max1.cpu().numpy()
+    out = {}
+    for j in crossing:
+        r = optimal_region((mnx[j, 1], mxx[j, 1], mny[j, 1], mxy[j, 1]),
+                           (mnx[j, 0], mxx[j, 0], mny[j, 0], mxy[j, 0]))
+        out[int(j)] = ((r[0] + r[1]) / 2, (r[2] + r[3]) / 2)
+    return out
+
+
 def bistratal_spans(topo, coord, on_top, boxes=None):
     """Per-net exact bistratal extent on one axis (wirelength.py:167-170)."""
     if boxes is not None:
@@ -284,6 +304,7 @@ def dynamic_pin_coords(arrays: NetlistArrays, x, y, z, rot, dz):
 
 
 __all__ = [
+    "optimal_hbt_centers",
     "NetTopology", "DeviceTopology", "partial_hpwl", "wa_smooth", "NetBoxes", "bistratal_axis",
     "optimal_region", "bistratal_spans", "planar_objective", "z_cut_penalty",
     "fd_z_gradient_naive", "fd_z_gradient_incremental", "normalize_z_gradient",
