@@ -33,6 +33,7 @@ WORKLOADS = {
     1: "cfg1: synthetic 2-die F2F, 10,008 cells (8 macros), 12,010 nets, 128x128x2 bins",
     2: "cfg2: synthetic 100,032 cells (32 macros), 110k nets, 256x256x2 bins",
     3: "cfg3: synthetic ICCAD-2023-case4-scale, 800,064 cells (64 macros), 850k nets, 512x512x2 bins",
+    4: "cfg4: synthetic 4,000,128 cells (128 macros), 4.2M nets, 1024x1024x2 bins",
 }
 METRIC = "GP iterations/sec at 800k cells (WL+density+field+step); % HBM roofline"
 
@@ -83,10 +84,16 @@ class ClockSampler:
     def __enter__(self):
         self.t = threading.Thread(target=self._run, daemon=True)
         self.t.start()
-        time.sleep(0.01)
+        t0 = time.time()
+        while not self.rows and self.err is None and time.time() - t0 < 5.0:
+            time.sleep(0.001)  # NVML is up and sampling before the timed region starts
         return self
 
     def __exit__(self, *a):
+        n = len(self.rows)
+        t0 = time.time()
+        while len(self.rows) == n and self.err is None and time.time() - t0 < 0.05:
+            time.sleep(0.0005)  # at least one sample after the region's work was enqueued
         self.stop.set()
         self.t.join(timeout=2)
 
@@ -211,7 +218,7 @@ def make_problem_inputs(design, spec, grid_n, max_iters, G):
     return cfg, grid, st, pos0
 
 
-def roofline_of(design, n_fill, grid, stage_ms):
+def roofline_of(design, n_fill, grid, stage_ms, config):
     """Roofline of the dominant kernel family (SURVEY 8d algorithmic bytes)."""
     q = algorithmic_bytes(design, n_fill, grid.n_bins)
     fam_ms = {"K1": stage_ms[0] + stage_ms[1], "K2": stage_ms[2], "K3": stage_ms[3],
@@ -223,9 +230,11 @@ def roofline_of(design, n_fill, grid, stage_ms):
                       "GBs": round(q[k] / (v / 1000.0) / 1e9, 1) if v > 0 else None}
                   for k, v in fam_ms.items()}
     traffic = None
-    try:  # DRAM bytes per launch of the dominant family from the committed ncu capture
+    try:  # DRAM bytes per iteration of the dominant family from the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get(dom)
+            tr = json.load(fh)
+        if tr.get("config") == config:
+            traffic = tr.get(dom)
     except (OSError, ValueError):
         pass
     return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -387,7 +396,7 @@ def main():
         "final_row": list(prob.log_rows(W + K)[-1]),
     }
     if mode != "sharded":
-        line["roofline"] = roofline_of(design, prob.n_fill, grid, stage)
+        line["roofline"] = roofline_of(design, prob.n_fill, grid, stage, args.config)
     if not args.no_cpu_baseline and world == 1:
         rate, iters, el = cpu_baseline(design, grid_n, spec, seconds=args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "it/s", "cores": 1, "kind": "port",

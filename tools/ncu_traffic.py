@@ -1,6 +1,6 @@
 """Per-family DRAM traffic per launch (dram__bytes_read.sum + write.sum) from an
 ncu --set full capture of one GP iteration -> profiles/ncu_traffic.json, which
-bench.py reports as roofline.traffic.  usage: python tools/ncu_traffic.py REP.ncu-rep"""
+bench.py reports as roofline.traffic.  usage: python tools/ncu_traffic.py REP.ncu-rep [config]"""
 import csv
 import io
 import json
@@ -32,6 +32,7 @@ for r in rows[2:]:
 res = {k: int(v) for k, v in fam.items()}
 res["per_kernel"] = {k: int(v) for k, v in kern.items()}
 res["source"] = os.path.basename(sys.argv[1])
+res["config"] = int(sys.argv[2]) if len(sys.argv) > 2 else 3  # bench --config of the capture
 dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
                    "ncu_traffic.json")
 with open(dst, "w") as fh:
