@@ -273,6 +273,10 @@ typedef struct p3d_gp {
   double* shard_tot;           /* [32] per-rank totals the host all-reduces between
                                   stages: [0,6) net totals, [8,14) density totals,
                                   [16] max |g| (iteration 0) */
+  int32_t overlap;             /* 1: the wirelength branch (K1, K1b) runs on a side
+                                  stream concurrently with the density branch (K2,
+                                  K3), joined before K4 (fused loop) */
+  int32_t pad2;
 } p3d_gp;
 
 /* Stages of one sharded GP iteration.  The host runs them in this order with

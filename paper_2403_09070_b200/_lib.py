@@ -76,7 +76,8 @@ class Gp(C.Structure):
                 ("ts_order", P), ("ts_rec", P), ("rho", P), ("spec_scratch", P),
                 ("maps", P), ("partials", P), ("st", P), ("log", P), ("ovfl_hist", P),
                 ("shard_rank", I32), ("shard_size", I32), ("sh_i0", I32), ("sh_i1", I32),
-                ("sh_f0", I32), ("sh_f1", I32), ("shard_tot", P)]
+                ("sh_f0", I32), ("sh_f1", I32), ("shard_tot", P), ("overlap", I32),
+                ("pad2", I32)]
 
 SH_STAGES = ("NET", "GATHER", "NORMS", "SCATTER", "SPECTRAL", "DENS", "CONTROL", "STEP0",
              "STEP0_CONTROL", "ADVANCE")

@@ -22,6 +22,7 @@
 //                       block: mu schedule, lambda update, next gamma
 //                       (gp.py:220-227, 442-444)
 #include <math.h>
+#include <stdlib.h>
 
 #include "p3d_geom.cuh"
 #include "p3d_internal.cuh"
@@ -672,8 +673,48 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
   return check_launch("gp evaluation kernels");
 }
 
+// The WL branch (K1, K1b) and the density branch (K2, K3) are independent
+// until K4: with gp.overlap the density branch forks onto a high-priority
+// side stream (its latency-bound kernels get SM slots as soon as they free
+// up, next to the persistent K1 wave) and joins before K4; graph capture turns
+// this into two concurrent branches.
+struct ForkJoin {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static ForkJoin& fork_join() {
+  static ForkJoin f;
+  return f;
+}
+static void overlap_setup() {  // outside any capture (gp_init / gp_evaluate)
+  ForkJoin& f = fork_join();
+  if (f.side) return;
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  const char* e = getenv("P3D_OVERLAP_PRIO");
+  const int prio = (e && e[0] == '0') ? least : greatest;
+  cudaStreamCreateWithPriority(&f.side, cudaStreamNonBlocking, prio);
+  cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming);
+}
+
+static int eval_kernels_overlap(const p3d_gp& gp, cudaStream_t s) {
+  ForkJoin& f = fork_join();
+  if (!f.side) return eval_kernels(gp, s);
+  cudaEventRecord(f.fork, s);
+  cudaStreamWaitEvent(f.side, f.fork, 0);
+  scatter_k2(gp, &gp.st->done, f.side);
+  if (const int rc = launch_k3(gp, f.side)) return rc;
+  launch_k1(gp, s);
+  launch_k1b(gp, s);
+  cudaEventRecord(f.join, f.side);
+  cudaStreamWaitEvent(s, f.join, 0);
+  dens_kernel<<<gp.n_macro + gp.nblk_dens, 256, 0, s>>>(gp);
+  return check_launch("gp evaluation kernels (overlapped)");
+}
+
 int gp_iterate(const p3d_gp& gp, cudaStream_t s) {
-  if (const int rc = eval_kernels(gp, s)) return rc;
+  if (const int rc = gp.overlap ? eval_kernels_overlap(gp, s) : eval_kernels(gp, s)) return rc;
   gmax0_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
   advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
   return check_launch("gp_iterate");
@@ -725,6 +766,7 @@ int gp_kernels_per_iteration(const p3d_gp& gp) {
 }
 
 int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s) {
+  overlap_setup();
   spectral_setup();
   tiled_scatter_setup();
   fused_net_setup();
@@ -736,6 +778,7 @@ int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s) {
 }
 
 int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s) {
+  overlap_setup();
   spectral_setup();
   tiled_scatter_setup();
   fused_net_setup();

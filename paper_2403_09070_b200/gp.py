@@ -386,6 +386,8 @@ class Gp3dProblem:
         f_lo = r * q + min(r, rem)
         self.sh_f = (I + f_lo, I + f_lo + q + (1 if r < rem else 0))
         g.shard_rank, g.shard_size = r, (R if self.sharded else 0)
+        # WL and density branches concurrently inside the iteration graph
+        g.overlap = int(os.environ.get("P3D_OVERLAP", "1")) if not self.sharded else 0
         g.sh_i0, g.sh_i1 = self.sh_i
         g.sh_f0, g.sh_f1 = self.sh_f
         macro_ids = macro_ids[(macro_ids >= self.sh_i[0]) & (macro_ids < self.sh_i[1])]
