@@ -621,7 +621,8 @@ static void launch_k1b(const p3d_gp& gp, cudaStream_t s) {
   // K1b owner gather (per-instance sums; L1 norms + Eq. 17 scale on one GPU)
   FusedGatherArgs ga{};
   ga.n_obj = gp.n_inst;
-  ga.blocks = grid_blocks(gp.n_inst, 256, kMaxBlocks);
+  static const int gather_cap = getenv("P3D_NBLK_GATHER") ? atoi(getenv("P3D_NBLK_GATHER")) : kMaxBlocks;
+  ga.blocks = grid_blocks(gp.n_inst, 256, gather_cap);
   ga.obj_slot_ptr = gp.topo.obj_slot_ptr;
   ga.in_f = reinterpret_cast<const float4*>(gp.pin_out_f);
   ga.in_fd = gp.pin_out_fd;

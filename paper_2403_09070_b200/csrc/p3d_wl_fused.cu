@@ -71,6 +71,8 @@ struct Box2 {  // one axis, die 0 (bottom) and die 1 (top)
 
 // ---- weighted-average segment sums -------------------------------------------
 // exp(x) for x <= 0 (every WA argument is (v - max)/gamma or (min - v)/gamma).
+// Default: the table-free polynomial below (P3D_EXP_POLY, measured faster: the
+// table load was the kernel's top stall).  Alternative (-DP3D_EXP_POLY=0):
 // x = (64 m + k) ln2/64 + r with |r| <= ln2/128: exp(x) = 2^m T[k] (1 + q(r)),
 // T[k] = 2^(k/64) (64-entry table), q a degree-6 Taylor polynomial evaluated
 // with short dependency chains (Estrin) — this kernel is latency-bound at the
@@ -95,6 +97,33 @@ __device__ const double kExp2Tab[64] = {
     1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
     1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
 
+#ifndef P3D_EXP_POLY
+#define P3D_EXP_POLY 1
+#endif
+#if P3D_EXP_POLY
+// Table-free variant: n = rint(x / ln 2), Cody-Waite r (|r| <= ln2/2), degree-13
+// Taylor polynomial by Horner (<= 1.2 ulp over [-708, 0]); no memory access.
+__device__ __forceinline__ double exp_neg(double x) {
+  const double n = rint(x * 1.4426950408889634074);
+  const double r = fma(-n, 1.9082149292705877e-10, fma(-n, 0.693147180369123816490, x));
+  double p = 1.6059043836821613e-10;                 // 1/13!
+  p = fma(p, r, 2.08767569878680989792e-09);         // 1/12!
+  p = fma(p, r, 2.50521083854417187751e-08);         // 1/11!
+  p = fma(p, r, 2.75573192239858906526e-07);         // 1/10!
+  p = fma(p, r, 2.75573192239858906526e-06);         // 1/9!
+  p = fma(p, r, 2.48015873015873015873e-05);         // 1/8!
+  p = fma(p, r, 1.98412698412698412698e-04);         // 1/7!
+  p = fma(p, r, 1.38888888888888888889e-03);         // 1/6!
+  p = fma(p, r, 8.33333333333333333333e-03);         // 1/5!
+  p = fma(p, r, 4.16666666666666666667e-02);         // 1/4!
+  p = fma(p, r, 1.66666666666666666667e-01);         // 1/3!
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double sc = __longlong_as_double((long long)((int)n + 1023) << 52);
+  return x < -708.0 ? 0.0 : p * sc;
+}
+#else
 __device__ __forceinline__ double exp_neg(double x) {
   const double n = rint(x * 92.332482616893656877);  // 64 / ln 2
   const double r = fma(-n, 2.572804622327669e-14, fma(-n, 0.010830424696223417, x));
@@ -108,6 +137,7 @@ __device__ __forceinline__ double exp_neg(double x) {
   const double sc = __longlong_as_double((long long)((ni >> 6) + 1023) << 52);
   return x < -708.0 ? 0.0 : fma(t, q, t) * sc;
 }
+#endif
 
 // float64 WA sums with numpy's structure (wirelength.py:85-96): value
 // sxp/s1p - sxm/s1m, gradient ep/s1p (1 + (v - vp)/g) - em/s1m (1 - (v - vm)/g);
