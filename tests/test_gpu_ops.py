@@ -458,3 +458,68 @@ def test_energy_gradient_matches_finite_difference():
         for axis in (0, 1):
             fd = (energy_at(i, axis, h) - energy_at(i, axis, -h)) / (2 * h)
             assert grad[i, axis] == pytest.approx(fd, rel=0.02, abs=1e-9)  # test_density.py:442
+
+
+def _with_odd_nets(design):
+    """The small design plus nets the synthetic generator never makes: degree
+    1, degree 9 and 12, and nets where one instance owns several pins (the
+    O(|P|^2) exact FD path, wirelength.py:280-292) — the fused loop's generic
+    kernel."""
+    from paper_2403_09070_b200.model import ArrayDesign, NetlistArrays
+
+    a = design.arrays()
+    rng = np.random.default_rng(21)
+    I = a.n_inst
+    extra = [rng.choice(I, 12, replace=False), rng.choice(I, 9, replace=False), [5],
+             [7, 7, 11], [3, 9, 3, 14, 9], np.r_[rng.choice(I, 6, replace=False), 17, 17]]
+    ptr = list(a.net_ptr)
+    inst = list(a.pin_inst)
+    ox = [list(a.ox_top), list(a.oy_top), list(a.ox_bot), list(a.oy_bot)]
+    for net in extra:
+        for i in net:
+            inst.append(int(i))
+            for k in range(4):
+                ox[k].append(float(rng.integers(-6, 7)))
+        ptr.append(len(inst))
+    arr = NetlistArrays(is_macro=a.is_macro, w_top=a.w_top, h_top=a.h_top, w_bot=a.w_bot,
+                        h_bot=a.h_bot, net_ptr=np.array(ptr), pin_inst=np.array(inst),
+                        ox_top=np.array(ox[0]), oy_top=np.array(ox[1]), ox_bot=np.array(ox[2]),
+                        oy_bot=np.array(ox[3]))
+    return ArrayDesign(design.die, design.hbt, arr)
+
+
+def test_generic_and_duplicate_owner_nets_in_the_loop(small):
+    """evaluate + 25 loop iterations with degree-1/9/12 and duplicate-owner
+    nets (fused loop: generic kernel) against the oracle."""
+    from paper_2403_09070_b200 import gp as G
+
+    d0, g = small
+    d = _with_odd_nets(d0)
+    assert d.arrays().net_has_dup_inst.sum() >= 3
+    cfg = G.GpConfig(seed=1, nz=2, grid_nx=64, grid_ny=64, max_iters=25, stop_overflow=0.0)
+    ocfg = P.Cfg(seed=1, nz=2, grid_nx=64, grid_ny=64, max_iters=25, stop_overflow=0.0)
+    rng = np.random.default_rng(1)
+    grid = G.choose_grid(d, cfg)
+    st = G.init_state(d, grid, cfg, rng)
+    fill = G.make_fillers(d, grid, rng)
+    og = P.grid_for(d, ocfg)
+    ofill = P.Fill(fill.x, fill.y, fill.z, fill.die, fill.w, fill.h, fill.dep)
+    prob = G.Gp3dProblem(d, grid, fill, cfg, st.rot)
+    oprob = P.Problem(d, og, ofill, ocfg, st.rot)
+    n = d.n_insts
+    pos = np.zeros((prob.n_obj, 3))
+    pos[:n] = np.c_[st.x, st.y, st.z]
+    pos[n:] = np.c_[fill.x, fill.y, fill.z]
+    pos = oprob.project(pos)
+    b, ov, ex, nc = prob.evaluate(pos, 1e-3, 2 * grid.db)
+    e, ov2, ex2, nc2 = oprob.evaluate(pos, 1e-3, 2 * og.db)
+    assert nc == nc2 and ex == pytest.approx(ex2, rel=1e-12) and ov == pytest.approx(ov2, rel=1e-12)
+    assert rel(b.wl_grad, e.wl_grad) < 1e-12
+    rows, orows = [], []
+    st2 = G.PlacementState(x=st.x.copy(), y=st.y.copy(), z=st.z.copy(), rot=st.rot, dz=grid.dz,
+                           fillers=fill)
+    G.run_gp3d(d, st2, cfg, grid=grid, iteration_log=rows, rng=rng)
+    P.run_loop(d, pos[:n, 0], pos[:n, 1], pos[:n, 2], st.rot, ofill, ocfg, og, log=orows)
+    assert len(rows) == len(orows) == 25
+    for r, o in zip(rows, orows):
+        assert r[2] == o[2] and abs(r[1] - o[1]) <= 1e-9 * abs(o[1]) and abs(r[3] - o[3]) <= 1e-9
