@@ -292,6 +292,14 @@ def main():
         prob = runner.prob
         step = runner.iterate
         runner.init_loop(pos0)
+        if runner.comm.nccl:  # the iteration, collectives included, as one CUDA graph
+            try:
+                sgraph = runner.capture(1)
+                step = lambda n=1: [sgraph.replay() for _ in range(n)]  # noqa: E731
+            except Exception as exc:  # pragma: no cover - eager fallback, reported
+                print(f"# sharded graph capture failed ({exc!r}); running eagerly",
+                      file=sys.stderr)
+                runner.init_loop(pos0)
     else:
         prob = G.Gp3dProblem(design, grid, st.fillers, cfg, st.rot, precision=args.precision)
         prob.init_loop(pos0)

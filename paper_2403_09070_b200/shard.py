@@ -44,8 +44,10 @@ STAGE = {name: k for k, name in enumerate(_lib.SH_STAGES)}
 class ShardComm:
     """The four collectives the sharded loop needs, on CUDA tensors."""
 
-    def __init__(self):
-        self.on = dist.is_initialized() and dist.get_world_size() > 1
+    def __init__(self, force=False):
+        """force: issue the collectives even for a world of one (tests the
+        NCCL calls and their graph capture on a single GPU)."""
+        self.on = dist.is_initialized() and (dist.get_world_size() > 1 or force)
         self.rank = dist.get_rank() if self.on else 0
         self.world = dist.get_world_size() if self.on else 1
         self.nccl = self.on and dist.get_backend() == "nccl"
@@ -115,13 +117,31 @@ class ShardedGp3d:
             c.all_reduce(self._dv2)
             c.all_gather_chunks(p.t_pos4, 4 * p.inst_slab)
 
-    def run(self, pos0, poll_every=8):
+    def capture(self, iters_per_graph=1):
+        """CUDA graph of `iters_per_graph` sharded iterations, collectives
+        included (nccl only: gloo stages through host memory).  Replaying it
+        removes the per-stage host launch cost."""
+        if self.comm.on and not self.comm.nccl:
+            raise RuntimeError("graph capture needs the nccl backend")
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+            self.iterate(iters_per_graph)
+        torch.cuda.current_stream().wait_stream(s)
+        return g
+
+    def run(self, pos0, poll_every=8, use_graph=False):
         """Initialise and run to completion (max_iters or an exit)."""
         self.init_loop(pos0)
+        step = self.iterate
+        if use_graph:
+            graph = self.capture(1)
+            step = lambda n: [graph.replay() for _ in range(n)]  # noqa: E731
         done = 0
         while done < self.prob.max_iters:
             k = min(poll_every, self.prob.max_iters - done)
-            self.iterate(k)
+            step(k)
             done += k
             if self.prob.state().done:
                 break

@@ -104,3 +104,41 @@ def test_sharded_world2_gloo_one_gpu():
         assert abs(a[2] - b[2]) <= 1e-9 * max(b[2], 1)
     assert np.array_equal(res[0][1], res[1][1])
     assert np.abs(res[0][1] - u).max() <= 1e-6 * np.abs(u).max()
+
+
+def _nccl_world1(port, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_2403_09070_b200.shard import ShardComm, ShardedGp3d
+
+        design, cfg, grid, st, fill, pos0 = _setup()
+        res = []
+        for use_graph in (False, True):
+            sh = ShardedGp3d(design, grid, fill, cfg, st.rot, comm=ShardComm(force=True))
+            assert sh.comm.on and sh.comm.nccl
+            s = sh.run(pos0, use_graph=use_graph)
+            res.append(sh.log_rows(s.iterations))
+        out[0] = res
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_nccl_collectives_and_graph_capture():
+    """The nccl path of every collective (world of one, forced on) run eagerly
+    and replayed from a CUDA graph with the collectives captured: both equal
+    the fused single-GPU loop."""
+    rows, _ = _single()
+    with mp.get_context("spawn").Manager() as m:
+        out = m.dict()
+        p = mp.get_context("spawn").Process(target=_nccl_world1, args=(_free_port(), out))
+        p.start()
+        p.join(600)
+        assert p.exitcode == 0
+        eager, graphed = dict(out)[0]
+    assert eager == graphed
+    for a, b in zip(eager, rows):
+        assert a[2] == b[2] and abs(a[1] - b[1]) <= 1e-12 * abs(b[1]) and abs(a[3] - b[3]) <= 1e-12
