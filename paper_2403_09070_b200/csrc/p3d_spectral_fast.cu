@@ -31,7 +31,10 @@ namespace {
 
 constexpr int kMaxNz = 16;
 constexpr int kThreads = 256;
-constexpr int kColsB = 2;     // columns per CTA in B
+#ifndef P3D_SPEC_COLS
+#define P3D_SPEC_COLS 4
+#endif
+constexpr int kColsB = P3D_SPEC_COLS;  // columns per CTA in B
 constexpr int kFftRoundC = 4; // complex lines per round in C
 
 enum { T_DCT2 = 0, T_COS = 1, T_SIN = 2 };
