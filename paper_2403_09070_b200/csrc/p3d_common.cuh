@@ -95,6 +95,13 @@ __device__ __forceinline__ bool last_block(unsigned int* counter) {
   return is_last;
 }
 
+// last_block for kernels whose every thread published global data (e.g.
+// atomics) the last block must see: all threads fence before the ticket.
+__device__ __forceinline__ bool last_block_all(unsigned int* counter) {
+  __threadfence();
+  return last_block(counter);
+}
+
 // Ordered sum of n partials by one block (fixed order => deterministic).
 __device__ __forceinline__ double ordered_sum(const volatile double* p, int n, double* smem) {
   double acc[1] = {0.0};

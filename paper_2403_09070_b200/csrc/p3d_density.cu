@@ -58,43 +58,16 @@ constexpr int kTile = 16;
 constexpr int kChunk = 1024;
 constexpr int kBoxBins = 6144;  // 48 KB of int64 bins per CTA
 
-template <class Cloud>
-__global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_grid g, TileSort ts,
-                                                       const int* halt) {
-  if (halt && *halt) return;
-  extern __shared__ int sh_hist[];
-  for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x) sh_hist[t] = 0;
-  __syncthreads();
-  const double tw = g.wb * kTile, th = g.hb * kTile;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int i = k < ts.ni ? ts.i0 + k : ts.f0 + (k - ts.ni);  // this rank's objects
-    if (cl.is_macro(i)) {
-      ts.tile_of[k] = -1;
-      continue;
-    }
-    const Charge q = cl.get(i);
-    int tx = (int)floor(q.x / tw), ty = (int)floor(q.y / th);
-    tx = tx < 0 ? 0 : (tx >= ts.tiles_x ? ts.tiles_x - 1 : tx);
-    ty = ty < 0 ? 0 : (ty >= ts.tiles_y ? ts.tiles_y - 1 : ty);
-    const int t = tx * ts.tiles_y + ty;
-    ts.tile_of[k] = t;
-    atomicAdd(&sh_hist[t], 1);
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x)
-    if (sh_hist[t]) atomicAdd(&ts.hist[t], sh_hist[t]);
-}
-
-// exclusive scan of the tile histogram (one CTA); re-zeroes the histogram
-__global__ void __launch_bounds__(1024) tile_scan_kernel(TileSort ts, const int* halt) {
-  if (halt && *halt) return;
+// exclusive scan of the tile histogram by one block; re-zeroes the histogram
+__device__ __forceinline__ void scan_tiles(const TileSort& ts) {
   __shared__ int carry;
   __shared__ int wsum[32];
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
+  const int nw = blockDim.x >> 5;
   for (int base = 0; base < ts.n_tiles; base += blockDim.x) {
     const int t = base + threadIdx.x;
-    const int v = t < ts.n_tiles ? ts.hist[t] : 0;
+    const int v = t < ts.n_tiles ? ((volatile int*)ts.hist)[t] : 0;
     int x = v;  // inclusive warp scan
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -105,7 +78,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(TileSort ts, const int*
     if (lane == 31) wsum[wid] = x;
     __syncthreads();
     if (wid == 0) {
-      int w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+      int w = lane < nw ? wsum[lane] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, w, o);
@@ -125,6 +98,43 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(TileSort ts, const int*
     __syncthreads();
   }
   if (threadIdx.x == 0) ts.start[ts.n_tiles] = carry;
+}
+
+// K2 step 1: per-object tile of the centre + tile histogram; the last block
+// scans the histogram.  The first n_macro blocks scatter one macro each
+// (per-macro footprint tile, int64 global atomics), independent of the sort.
+template <class Cloud>
+__global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_grid g, TileSort ts,
+                                                       const int32_t* macro_ids, int n_macro,
+                                                       unsigned long long* rho, const int* halt) {
+  if (halt && *halt) return;
+  extern __shared__ int sh_hist[];
+  if ((int)blockIdx.x < n_macro) {
+    scatter_object_block(cl.get(macro_ids[blockIdx.x]), g, rho);
+  } else {
+    for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x) sh_hist[t] = 0;
+    __syncthreads();
+    const double tw = g.wb * kTile, th = g.hb * kTile;
+    const int b = blockIdx.x - n_macro, nb = gridDim.x - n_macro;
+    for (int k = b * blockDim.x + threadIdx.x; k < n; k += nb * blockDim.x) {
+      const int i = k < ts.ni ? ts.i0 + k : ts.f0 + (k - ts.ni);  // this rank's objects
+      if (cl.is_macro(i)) {
+        ts.tile_of[k] = -1;
+        continue;
+      }
+      const Charge q = cl.get(i);
+      int tx = (int)floor(q.x / tw), ty = (int)floor(q.y / th);
+      tx = tx < 0 ? 0 : (tx >= ts.tiles_x ? ts.tiles_x - 1 : tx);
+      ty = ty < 0 ? 0 : (ty >= ts.tiles_y ? ts.tiles_y - 1 : ty);
+      const int t = tx * ts.tiles_y + ty;
+      ts.tile_of[k] = t;
+      atomicAdd(&sh_hist[t], 1);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x)
+      if (sh_hist[t]) atomicAdd(&ts.hist[t], sh_hist[t]);
+  }
+  if (last_block_all(ts.counter)) scan_tiles(ts);
 }
 
 // Stable-per-block placement: each CTA ranks its objects per tile in shared
@@ -328,13 +338,12 @@ void launch_scatter_tiled(const CloudGP& cl, int n, int n_macro, const int32_t* 
                           cudaStream_t s) {
   unsigned long long* r = reinterpret_cast<unsigned long long*>(rho);
   const int nb = grid_blocks(n, 256, 148 * 8);
-  tile_hist_kernel<CloudGP><<<nb, 256, ts.n_tiles * sizeof(int), s>>>(cl, n, g, ts, halt);
-  tile_scan_kernel<<<1, 1024, 0, s>>>(ts, halt);
+  tile_hist_kernel<CloudGP><<<n_macro + nb, 256, ts.n_tiles * sizeof(int), s>>>(
+      cl, n, g, ts, macro_ids, n_macro, r, halt);
   const int np = (n + 256 * kPlacePerThread - 1) / (256 * kPlacePerThread);
   tile_place_kernel<CloudGP><<<np, 256, 2 * ts.n_tiles * sizeof(int), s>>>(cl, n, ts, halt);
   const int chunks = (n + kChunk - 1) / kChunk;
   scatter_tiled_kernel<<<chunks, 256, kBoxBins * 8, s>>>(g, ts, r, halt);
-  if (n_macro > 0) scatter_macros_kernel<<<n_macro, 256, 0, s>>>(cl, macro_ids, g, r, halt);
 }
 
 template void launch_scatter<CloudGP>(const CloudGP&, int, int, const int32_t*, const p3d_grid&,

@@ -31,7 +31,7 @@ enum FinalIdx {
   kFinGeneric = 24, // 6 values: generic-net totals
 };
 // counters inside p3d_loop_state::counters
-enum CounterIdx { kCntNet = 0, kCntGather, kCntOvfl, kCntDens, kCntStep, kCntAdvance, kCntOp, kCntGeneric };
+enum CounterIdx { kCntNet = 0, kCntGather, kCntOvfl, kCntDens, kCntStep, kCntAdvance, kCntOp, kCntGeneric, kCntTile };
 
 struct NetArgs {
   int n_net, blocks;
@@ -141,6 +141,7 @@ struct TileSort {
   int32_t* cursor;   // [n_tiles]
   int32_t* order;    // [n_obj] tile of each record, in tile order
   double* rec;       // [n_obj][6] charge records in tile order
+  unsigned int* counter;  // last-block ticket of the histogram kernel
 };
 struct CloudGP;
 void tiled_scatter_setup();

@@ -564,6 +564,7 @@ static void scatter_k2(const p3d_gp& gp, const int* halt, cudaStream_t s) {
     ts.cursor = gp.ts_cursor;
     ts.order = gp.ts_order;
     ts.rec = gp.ts_rec;
+    ts.counter = &gp.st->counters[kCntTile];
     ts.i0 = gp.sh_i0;
     ts.ni = gp.sh_i1 - gp.sh_i0;
     ts.f0 = gp.sh_f0;
@@ -762,7 +763,10 @@ int gp_stage_times(float* ms) {
 
 // kernels enqueued by one gp_iterate (for the benchmark's launch count)
 int gp_kernels_per_iteration(const p3d_gp& gp) {
-  return (gp.topo.n_net > 0) + (gp.f_n_generic > 0) /*net*/ + (gp.n_inst > 0) /*gather*/ + 1 + (gp.ts_order ? 3 : 0) /*tile sort*/ + (gp.n_macro > 0) /*scatter*/ + (spectral_fast_ok(&gp.grid) ? 3 : 6) /*spectral*/ +
+  const int k2 = gp.ts_order ? 3 /*histogram+scan+macros, place, scatter*/
+                             : 1 + (gp.n_macro > 0) /*cells, macros*/;
+  return (gp.topo.n_net > 0) + (gp.f_n_generic > 0) /*net*/ + (gp.n_inst > 0) /*gather*/ + k2 +
+         (spectral_fast_ok(&gp.grid) ? 3 : 6) /*spectral*/ +
          1 /*dens*/ + 2 /*step, advance*/;
 }
 
