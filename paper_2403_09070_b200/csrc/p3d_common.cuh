@@ -20,6 +20,38 @@ void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 
 // ---------------------------------------------------------------------------
+// programmatic dependent launch (PDL): the loop's kernels are launched with
+// programmatic stream serialisation so a kernel's launch overlaps its
+// predecessor's tail; every such kernel waits for the predecessor's memory
+// (griddepcontrol.wait) before its first global access, so the semantics are
+// those of plain stream order.  A no-op when launched without the attribute.
+// ---------------------------------------------------------------------------
+#ifndef P3D_PDL
+#define P3D_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if P3D_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = P3D_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+// ---------------------------------------------------------------------------
 // warp / block reductions (deterministic: fixed shuffle tree, fixed order)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {

@@ -107,6 +107,7 @@ template <class Cloud>
 __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_grid g, TileSort ts,
                                                        const int32_t* macro_ids, int n_macro,
                                                        unsigned long long* rho, const int* halt) {
+  pdl_wait();
   if (halt && *halt) return;
   extern __shared__ int sh_hist[];
   if ((int)blockIdx.x < n_macro) {
@@ -146,6 +147,7 @@ constexpr int kPlacePerThread = 8;
 template <class Cloud>
 __global__ void __launch_bounds__(256) tile_place_kernel(Cloud cl, int n, TileSort ts,
                                                         const int* halt) {
+  pdl_wait();
   if (halt && *halt) return;
   extern __shared__ int sh[];
   int* cnt = sh;                  // [n_tiles]
@@ -257,6 +259,7 @@ __device__ __forceinline__ void scatter_terms(const Charge& q, const p3d_grid& g
 __global__ void __launch_bounds__(256) scatter_tiled_kernel(p3d_grid g, TileSort ts,
                                                            unsigned long long* rho,
                                                            const int* halt) {
+  pdl_wait();
   if (halt && *halt) return;
   extern __shared__ unsigned int sbin32[];
   __shared__ int box[4];
@@ -338,12 +341,12 @@ void launch_scatter_tiled(const CloudGP& cl, int n, int n_macro, const int32_t* 
                           cudaStream_t s) {
   unsigned long long* r = reinterpret_cast<unsigned long long*>(rho);
   const int nb = grid_blocks(n, 256, 148 * 8);
-  tile_hist_kernel<CloudGP><<<n_macro + nb, 256, ts.n_tiles * sizeof(int), s>>>(
-      cl, n, g, ts, macro_ids, n_macro, r, halt);
+  pdl_launch(tile_hist_kernel<CloudGP>, n_macro + nb, 256, ts.n_tiles * sizeof(int), s, cl, n, g,
+             ts, macro_ids, n_macro, r, halt);
   const int np = (n + 256 * kPlacePerThread - 1) / (256 * kPlacePerThread);
-  tile_place_kernel<CloudGP><<<np, 256, 2 * ts.n_tiles * sizeof(int), s>>>(cl, n, ts, halt);
+  pdl_launch(tile_place_kernel<CloudGP>, np, 256, 2 * ts.n_tiles * sizeof(int), s, cl, n, ts, halt);
   const int chunks = (n + kChunk - 1) / kChunk;
-  scatter_tiled_kernel<<<chunks, 256, kBoxBins * 8, s>>>(g, ts, r, halt);
+  pdl_launch(scatter_tiled_kernel, chunks, 256, kBoxBins * 8, s, g, ts, r, halt);
 }
 
 template void launch_scatter<CloudGP>(const CloudGP&, int, int, const int32_t*, const p3d_grid&,

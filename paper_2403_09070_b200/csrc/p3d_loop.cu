@@ -356,6 +356,7 @@ __device__ __forceinline__ void control_after_eval(const p3d_gp& gp, double ener
 #define P3D_K4_MINB 4
 #endif
 __global__ void __launch_bounds__(256, P3D_K4_MINB) dens_kernel(p3d_gp gp) {
+  pdl_wait();
   const p3d_loop_state* st = gp.st;
   if (st->done) return;
   __shared__ double red[32 * 6];
@@ -420,6 +421,7 @@ __global__ void __launch_bounds__(256, P3D_K4_MINB) dens_kernel(p3d_gp gp) {
 // just-initialised lambda, then the initial step wb / max|g| (gp.py:198-202)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) gmax0_kernel(p3d_gp gp) {
+  pdl_wait();
   p3d_loop_state* st = gp.st;
   if (st->done || st->step_set || st->stop_now) return;
   __shared__ double red[32];
@@ -459,6 +461,7 @@ __global__ void __launch_bounds__(256) gmax0_kernel(p3d_gp gp) {
 // K5b: projected Nesterov update (gp.py:220-227); last block: schedules
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
+  pdl_wait();
   p3d_loop_state* st = gp.st;
   if (st->done) return;
   __shared__ double red[32];
@@ -670,7 +673,7 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
   mark(3);
   if (const int rc = launch_k3(gp, s)) return rc;  // K3 (+ overflow, re-zero)
   mark(4);
-  dens_kernel<<<gp.n_macro + gp.nblk_dens, 256, 0, s>>>(gp);  // K4
+  pdl_launch(dens_kernel, gp.n_macro + gp.nblk_dens, 256, 0, s, gp);  // K4
   mark(5);
   return check_launch("gp evaluation kernels");
 }
@@ -711,14 +714,14 @@ static int eval_kernels_overlap(const p3d_gp& gp, cudaStream_t s) {
   launch_k1b(gp, s);
   cudaEventRecord(f.join, f.side);
   cudaStreamWaitEvent(s, f.join, 0);
-  dens_kernel<<<gp.n_macro + gp.nblk_dens, 256, 0, s>>>(gp);
+  pdl_launch(dens_kernel, gp.n_macro + gp.nblk_dens, 256, 0, s, gp);
   return check_launch("gp evaluation kernels (overlapped)");
 }
 
 int gp_iterate(const p3d_gp& gp, cudaStream_t s) {
   if (const int rc = gp.overlap ? eval_kernels_overlap(gp, s) : eval_kernels(gp, s)) return rc;
-  gmax0_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
-  advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  pdl_launch(gmax0_kernel, gp.nblk_obj, 256, 0, s, gp);
+  pdl_launch(advance_kernel, gp.nblk_obj, 256, 0, s, gp);
   return check_launch("gp_iterate");
 }
 
@@ -729,9 +732,9 @@ int gp_iterate_profiled(const p3d_gp& gp, cudaStream_t s, float* ms) {
   if (!ev[0])
     for (int k = 0; k < 8; ++k) cudaEventCreate(&ev[k]);
   if (const int rc = eval_kernels(gp, s, ev)) return rc;
-  gmax0_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  pdl_launch(gmax0_kernel, gp.nblk_obj, 256, 0, s, gp);
   cudaEventRecord(ev[6], s);
-  advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  pdl_launch(advance_kernel, gp.nblk_obj, 256, 0, s, gp);
   cudaEventRecord(ev[7], s);
   cudaEventSynchronize(ev[7]);
   for (int k = 0; k < 7; ++k) cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]);
@@ -747,9 +750,9 @@ int gp_iterate_marked(const p3d_gp& gp, cudaStream_t s) {
   if (!g_marks[0])
     for (int k = 0; k < 8; ++k) cudaEventCreate(&g_marks[k]);
   if (const int rc = eval_kernels(gp, s, g_marks, true)) return rc;
-  gmax0_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  pdl_launch(gmax0_kernel, gp.nblk_obj, 256, 0, s, gp);
   cudaEventRecordWithFlags(g_marks[6], s, cudaEventRecordExternal);
-  advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp);
+  pdl_launch(advance_kernel, gp.nblk_obj, 256, 0, s, gp);
   cudaEventRecordWithFlags(g_marks[7], s, cudaEventRecordExternal);
   return check_launch("gp_iterate_marked");
 }
@@ -862,11 +865,11 @@ int gp_shard_stage(const p3d_gp& gp, int stage, cudaStream_t s) {
       break;
     case P3D_SH_SCATTER: scatter_k2(gp, &gp.st->done, s); break;
     case P3D_SH_SPECTRAL: if (const int rc = launch_k3(gp, s)) return rc; break;
-    case P3D_SH_DENS: dens_kernel<<<gp.n_macro + gp.nblk_dens, 256, 0, s>>>(gp); break;
+    case P3D_SH_DENS: pdl_launch(dens_kernel, gp.n_macro + gp.nblk_dens, 256, 0, s, gp); break;
     case P3D_SH_CONTROL: shard_control_kernel<<<1, 1, 0, s>>>(gp); break;
-    case P3D_SH_STEP0: gmax0_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp); break;
+    case P3D_SH_STEP0: pdl_launch(gmax0_kernel, gp.nblk_obj, 256, 0, s, gp); break;
     case P3D_SH_STEP0_CONTROL: step0_control_kernel<<<1, 1, 0, s>>>(gp); break;
-    case P3D_SH_ADVANCE: advance_kernel<<<gp.nblk_obj, 256, 0, s>>>(gp); break;
+    case P3D_SH_ADVANCE: pdl_launch(advance_kernel, gp.nblk_obj, 256, 0, s, gp); break;
     default: return P3D_ERR_ARG;
   }
   return check_launch("gp_shard_stage");

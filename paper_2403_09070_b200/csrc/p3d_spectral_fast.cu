@@ -319,6 +319,7 @@ __device__ __forceinline__ void ovfl_epilogue(const FastArgs& a, long long exces
 // staged; other nz stage the slab and run the direct z transform.
 template <int LY, bool NZ2>
 __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
+  pdl_wait();
   using F = Fft<LY>;
   if (a.halt && *a.halt) return;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -411,6 +412,7 @@ __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
 // in 2 kColsB complex FFTs)
 template <int LX>
 __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
+  pdl_wait();
   using F = Fft<LX>;
   if (a.halt && *a.halt) return;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -494,6 +496,7 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
 // the output write.  Other nz stage the slab and loop over rounds of lines.
 template <int LY, bool NZ2>
 __global__ void __launch_bounds__(kThreads) spec_inv_yz(FastArgs a) {
+  pdl_wait();
   using F = Fft<LY>;
   if (a.halt && *a.halt) return;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -692,13 +695,13 @@ int launch_spectral_fast(const p3d_grid* g, const double* rho, const int64_t* rh
   const int ga = (g->nx + a.sa - 1) / a.sa, ta = threads_a(g, a.sa), tc = threads_c(g);
   const bool nz2 = g->nz == 2;
   if (!coef_in) {
-    if (nz2) P3D_SPEC_SWITCH(a.logy, (spec_fwd_yz<LL, true><<<ga, ta, smem_a(g, a.sa), s>>>(a)))
-    else P3D_SPEC_SWITCH(a.logy, (spec_fwd_yz<LL, false><<<ga, ta, smem_a(g, a.sa), s>>>(a)))
+    if (nz2) P3D_SPEC_SWITCH(a.logy, (pdl_launch(spec_fwd_yz<LL, true>, ga, ta, smem_a(g, a.sa), s, a)))
+    else P3D_SPEC_SWITCH(a.logy, (pdl_launch(spec_fwd_yz<LL, false>, ga, ta, smem_a(g, a.sa), s, a)))
   }
-  P3D_SPEC_SWITCH(a.logx, (spec_x<LL><<<(int)(S / kColsB), kThreads, smem_b(g), s>>>(a)));
+  P3D_SPEC_SWITCH(a.logx, (pdl_launch(spec_x<LL>, (int)(S / kColsB), kThreads, smem_b(g), s, a)));
   if (maps) {
-    if (nz2) P3D_SPEC_SWITCH(a.logy, (spec_inv_yz<LL, true><<<g->nx, tc, smem_c(g), s>>>(a)))
-    else P3D_SPEC_SWITCH(a.logy, (spec_inv_yz<LL, false><<<g->nx, tc, smem_c(g), s>>>(a)))
+    if (nz2) P3D_SPEC_SWITCH(a.logy, (pdl_launch(spec_inv_yz<LL, true>, g->nx, tc, smem_c(g), s, a)))
+    else P3D_SPEC_SWITCH(a.logy, (pdl_launch(spec_inv_yz<LL, false>, g->nx, tc, smem_c(g), s, a)))
   }
   return check_launch("spectral (fast path)");
 }

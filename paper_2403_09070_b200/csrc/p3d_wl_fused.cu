@@ -626,6 +626,7 @@ __device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk
 
 template <bool F32>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_kernel(FusedNetArgs a) {
+  pdl_wait();
   if (a.halt && *a.halt) return;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ double red[32 * 6];
@@ -699,6 +700,7 @@ __global__ void __launch_bounds__(256) generic_net_kernel(FusedNetArgs a) {
 // owner gather: per object, ordered fp64 sums over its contiguous slot records
 // (pin order within the owner, like bincount)
 __global__ void __launch_bounds__(256) fused_gather_kernel(FusedGatherArgs a) {
+  pdl_wait();
   if (a.halt && *a.halt) return;
   __shared__ double red[32 * 3];
   double acc[3] = {0, 0, 0};
@@ -762,13 +764,13 @@ void launch_fused_net(const FusedNetArgs& a, bool f32, cudaStream_t s) {
     else generic_net_kernel<false><<<gb, 256, 0, s>>>(a);
   }
   if (f32)
-    fused_net_kernel<true><<<a.blocks, 32 * kWarpsPerBlock, kWarpsPerBlock * sizeof(WarpCols<true>), s>>>(a);
+    pdl_launch(fused_net_kernel<true>, a.blocks, 32 * kWarpsPerBlock, kWarpsPerBlock * sizeof(WarpCols<true>), s, a);
   else
-    fused_net_kernel<false><<<a.blocks, 32 * kWarpsPerBlock, kWarpsPerBlock * sizeof(WarpCols<false>), s>>>(a);
+    pdl_launch(fused_net_kernel<false>, a.blocks, 32 * kWarpsPerBlock, kWarpsPerBlock * sizeof(WarpCols<false>), s, a);
 }
 
 void launch_fused_gather(const FusedGatherArgs& a, cudaStream_t s) {
-  fused_gather_kernel<<<a.blocks, 256, 0, s>>>(a);
+  pdl_launch(fused_gather_kernel, a.blocks, 256, 0, s, a);
 }
 
 }  // namespace p3d
