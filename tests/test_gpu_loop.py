@@ -121,3 +121,37 @@ def test_run_to_run_bit_identical():
     assert a[0] == b[0]
     assert np.array_equal(a[2].x, b[2].x) and np.array_equal(a[2].y, b[2].y)
     assert np.array_equal(a[2].z, b[2].z)
+
+
+@pytest.mark.parametrize("grid_n,nz", [(48, 3), (64, 4), (32, 1)])
+def test_loop_other_grids_vs_oracle(grid_n, nz):
+    """The fused loop on grids the BASELINE configs never use — a
+    non-power-of-two xy (generic spectral passes), nz = 3 / 4 (direct z
+    transforms, staged slabs) and nz = 1 — against the oracle loop."""
+    from oracle import port as P
+    from paper_2403_09070_b200 import gp as G
+    from paper_2403_09070_b200.synth import SynthSpec, synth_arrays
+
+    d = synth_arrays(SynthSpec(n_insts=1500, n_macros=4, r_ma=0.3, seed=4, nets_per_inst=1.2))
+    cfg = G.GpConfig(seed=1, nz=nz, grid_nx=grid_n, grid_ny=grid_n, max_iters=20,
+                     stop_overflow=0.0)
+    ocfg = P.Cfg(seed=1, nz=nz, grid_nx=grid_n, grid_ny=grid_n, max_iters=20, stop_overflow=0.0)
+    rng = np.random.default_rng(1)
+    grid = G.choose_grid(d, cfg)
+    st = G.init_state(d, grid, cfg, rng)
+    fill = G.make_fillers(d, grid, rng)
+    st.fillers = fill
+    og = P.grid_for(d, ocfg)
+    ofill = P.Fill(fill.x, fill.y, fill.z, fill.die, fill.w, fill.h, fill.dep)
+    n = d.n_insts
+    oprob = P.Problem(d, og, ofill, ocfg, st.rot)
+    pos = np.zeros((n + fill.count, 3))
+    pos[:n] = np.c_[st.x, st.y, st.z]
+    pos[n:] = np.c_[fill.x, fill.y, fill.z]
+    pos = oprob.project(pos)
+    rows, orows = [], []
+    G.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+    P.run_loop(d, pos[:n, 0], pos[:n, 1], pos[:n, 2], st.rot, ofill, ocfg, og, log=orows)
+    assert len(rows) == len(orows) == 20
+    for r, o in zip(rows, orows):
+        assert r[2] == o[2] and abs(r[1] - o[1]) <= 1e-9 * abs(o[1]) and abs(r[3] - o[3]) <= 1e-9
