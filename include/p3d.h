@@ -177,6 +177,21 @@ int p3d_gp2d_wirelength(int32_t n_net, int32_t n_pin, int32_t n_obj, const int32
                         const int32_t* obj_slot_ptr, const double* pos, double gamma,
                         double* value, double* wl_grad, double* scratch, void* stream);
 
+/* Solution score (evaluate_score, model.py:364-400): out[3] = (D2D HPWL, #HBT,
+ * HPWL + hbt_cost * #HBT); n_bad[1] = nets whose crossing state disagrees with
+ * their HBT (the reference's SolutionError cases).  Pins per net from
+ * net_ptr/pin_inst; pin offsets from the instance centre per die; unrotated
+ * instance sizes per die; die [n_inst] (1 top), rot [n_inst] quarter turns,
+ * x/y lower-left corners; hbt_ok/hbt_x/hbt_y per net (lower-left corner).
+ * scratch: zeroed, >= 8 + 2*1024 doubles. */
+int p3d_score(int32_t n_net, const int32_t* net_ptr, const int32_t* pin_inst,
+              const double* ox_top, const double* oy_top, const double* ox_bot,
+              const double* oy_bot, const double* w_top, const double* h_top,
+              const double* w_bot, const double* h_bot, const uint8_t* die, const int32_t* rot,
+              const double* x, const double* y, const uint8_t* hbt_ok, const double* hbt_x,
+              const double* hbt_y, double hbt_pitch, double hbt_cost, double* out, int32_t* n_bad,
+              double* scratch, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* optimiser pieces (gp.py:142-147, 178-227, 280-294)                        */
 /* ------------------------------------------------------------------------ */

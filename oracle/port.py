@@ -1218,3 +1218,45 @@ def gp2d_run(design, x, y, z, rot, dz, cfg, rng, log=None):
     centers = {int(j): (float(final[prob.n_inst + t, 0]), float(final[prob.n_inst + t, 1]))
                for t, j in enumerate(prob.crossing)}
     return final[: prob.n_inst, 0].copy(), final[: prob.n_inst, 1].copy(), info, centers
+
+
+# ==========================================================================
+# solution score (model.py:364-400)
+# ==========================================================================
+
+
+def score(arr, hbt_pitch, hbt_cost, die, x, y, rot, hbt_xy):
+    """evaluate_score(design, sol, allow_illegal=True) on flat arrays: die-to-die
+    HPWL (per die, pins at lower-left + rotated half size + rotated offset,
+    the HBT centre joining both partial nets of its net) + cost * #HBTs.
+    Returns (hpwl, hbt_count, raw_score)."""
+    half = hbt_pitch / 2
+    q = np.asarray(rot)[arr.pin_inst]
+    d = np.asarray(die)[arr.pin_inst]
+    rxt, ryt = turn_offsets(arr.ox_top, arr.oy_top, q)
+    rxb, ryb = turn_offsets(arr.ox_bot, arr.oy_bot, q)
+    wt, ht = turn_offsets_dims(arr.w_top, arr.h_top, rot)
+    wb, hb = turn_offsets_dims(arr.w_bot, arr.h_bot, rot)
+    top = np.asarray(die) == 1
+    w = np.where(top, wt, wb)[arr.pin_inst]
+    h = np.where(top, ht, hb)[arr.pin_inst]
+    px = np.asarray(x)[arr.pin_inst] + w / 2 + np.where(d == 1, rxt, rxb)  # model.py:352-361
+    py = np.asarray(y)[arr.pin_inst] + h / 2 + np.where(d == 1, ryt, ryb)
+    hpwl, count = 0.0, 0
+    for j in range(arr.n_net):
+        b, e = arr.net_ptr[j], arr.net_ptr[j + 1]
+        xs = {0: list(px[b:e][d[b:e] == 0]), 1: list(px[b:e][d[b:e] == 1])}
+        ys = {0: list(py[b:e][d[b:e] == 0]), 1: list(py[b:e][d[b:e] == 1])}
+        crossing = bool(xs[0]) and bool(xs[1])
+        t = hbt_xy.get(j)
+        if t is not None:
+            count += 1
+            cx, cy = t[0] + half, t[1] + half
+            for k in (0, 1):
+                if crossing or xs[k]:
+                    xs[k].append(cx)
+                    ys[k].append(cy)
+        for k in (0, 1):
+            if xs[k]:
+                hpwl += max(xs[k]) - min(xs[k]) + max(ys[k]) - min(ys[k])
+    return hpwl, count, hpwl + hbt_cost * count

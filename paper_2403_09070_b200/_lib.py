@@ -110,6 +110,7 @@ _SIGS = {
     "p3d_gp_evaluate": (I32, [P, D, D, P]),
     "p3d_gp_project": (I32, [P, P, P, P]),
     "p3d_gp_density_fx": (I32, [P, P, P]),
+    "p3d_score": (I32, [I32] + [P] * 17 + [D, D, P, P, P, P]),
     "p3d_gp2d_wirelength": (I32, [I32, I32, I32] + [P] * 8 + [D] + [P] * 4),
     "p3d_density_energy_gradient": (I32, [P, P, P, P, P, P, P, P]),
     "p3d_gp_shard_stage": (I32, [P, C.c_int, P]),

@@ -319,6 +319,36 @@ int p3d_gp2d_wirelength(int32_t n_net, int32_t n_pin, int32_t n_obj, const int32
   return check_launch("gp2d_wirelength");
 }
 
+int p3d_score(int32_t n_net, const int32_t* net_ptr, const int32_t* pin_inst,
+              const double* ox_top, const double* oy_top, const double* ox_bot,
+              const double* oy_bot, const double* w_top, const double* h_top,
+              const double* w_bot, const double* h_bot, const uint8_t* die, const int32_t* rot,
+              const double* x, const double* y, const uint8_t* hbt_ok, const double* hbt_x,
+              const double* hbt_y, double hbt_pitch, double hbt_cost, double* out, int32_t* n_bad,
+              double* scratch, void* stream) {
+  if (n_net < 0 || !net_ptr || !out || !n_bad || !scratch ||
+      (n_net > 0 && (!pin_inst || !ox_top || !oy_top || !ox_bot || !oy_bot || !w_top || !h_top ||
+                     !w_bot || !h_bot || !die || !rot || !x || !y || !hbt_ok || !hbt_x || !hbt_y))) {
+    set_error("score: bad args");
+    return P3D_ERR_ARG;
+  }
+  ScoreArgs a{};
+  a.n_net = n_net; a.net_ptr = net_ptr; a.pin_inst = pin_inst;
+  a.ox_top = ox_top; a.oy_top = oy_top; a.ox_bot = ox_bot; a.oy_bot = oy_bot;
+  a.w_top = w_top; a.h_top = h_top; a.w_bot = w_bot; a.h_bot = h_bot;
+  a.die = die; a.rot = rot; a.x = x; a.y = y;
+  a.hbt_ok = hbt_ok; a.hbt_x = hbt_x; a.hbt_y = hbt_y;
+  a.half = hbt_pitch / 2;
+  a.cost = hbt_cost;
+  a.counter = reinterpret_cast<unsigned int*>(scratch);
+  a.partials = scratch + 8;
+  a.n_bad = n_bad;
+  a.out = out;
+  if (n_net == 0) { cudaMemsetAsync(out, 0, 3 * sizeof(double), STREAM(stream)); return check_launch("score"); }
+  launch_score(a, STREAM(stream));
+  return check_launch("score");
+}
+
 int p3d_precondition(int32_t n, const double* gr, double lam, const double* q, const double* deg,
                      const uint8_t* macro, double* out, double* div, void* stream) {
   if (n < 0 || !gr || !q || !deg || !out) { set_error("precondition: bad args"); return P3D_ERR_ARG; }

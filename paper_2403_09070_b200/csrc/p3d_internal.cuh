@@ -126,6 +126,25 @@ struct Gp2dWlArgs {
   double* value;               // 1 double: sum over segments of the WA spans
 };
 void launch_gp2d_wl(const Gp2dWlArgs& a, double* wl_grad, cudaStream_t s);
+
+// solution score (p3d_score.cu)
+struct ScoreArgs {
+  int n_net;
+  const int32_t *net_ptr, *pin_inst;
+  const double *ox_top, *oy_top, *ox_bot, *oy_bot;  // [n_pin]
+  const double *w_top, *h_top, *w_bot, *h_bot;      // [n_inst] unrotated
+  const uint8_t* die;
+  const int32_t* rot;
+  const double *x, *y;                               // lower-left corners
+  const uint8_t* hbt_ok;                             // [n_net] net carries an HBT
+  const double *hbt_x, *hbt_y;                       // [n_net] its lower-left corner
+  double half, cost;
+  double* partials;
+  unsigned int* counter;
+  int* n_bad;                                        // crossing / HBT mismatches
+  double* out;                                       // hpwl, hbt count, raw score
+};
+void launch_score(const ScoreArgs& a, cudaStream_t s);
 void fused_net_setup();
 void launch_fused_gather(const FusedGatherArgs& a, cudaStream_t s);
 
