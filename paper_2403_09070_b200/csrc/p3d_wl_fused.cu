@@ -270,6 +270,40 @@ __device__ __forceinline__ void store_pin(const FusedNetArgs& a, int idx, double
   else a.out_f[s] = make_float4((float)gx, (float)gy, (float)gc, (float)gb);
 }
 
+
+// ---- L2 residency hints: the per-pin records are written here and read back
+// by the owner gather right after, so they are stored with an evict-last
+// policy; the bucketed pin streams (owner, offsets, slot) are read once per
+// iteration and loaded evict-first.  (-DP3D_L2_HINTS=0 disables.)
+#ifndef P3D_L2_HINTS
+#define P3D_L2_HINTS 1
+#endif
+__device__ __forceinline__ void store_rec(double* base, int slot, double a, double b, double c,
+                                          double d) {
+  double* p = base + 4 * (long long)slot;
+#if P3D_L2_HINTS
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b),
+               "l"(pol)
+               : "memory");
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p + 2), "d"(c), "d"(d),
+               "l"(pol)
+               : "memory");
+#else
+  reinterpret_cast<double4*>(p)[0] = make_double4(a, b, c, d);
+#endif
+}
+
+template <class T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+#if P3D_L2_HINTS
+  return __ldcs(p);  // streaming: evict-first in L1 and L2
+#else
+  return *p;
+#endif
+}
+
 // Dup-owner exact path (wirelength.py:280-292): value for the first pin of
 // each owner, 0 for its other pins.
 __device__ __noinline__ double dup_fd(const FusedNetArgs& a, int base, int deg, int stride,
@@ -474,8 +508,8 @@ __device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk,
 #pragma unroll
   for (int k = 0; k < KM; ++k) {
     if (k >= DD) break;
-    inst[k] = a.pin_inst[pin0 + k * nb];
-    off[k] = a.off[pin0 + k * nb];
+    inst[k] = ld_stream(a.pin_inst + pin0 + k * nb);
+    off[k] = ld_stream(a.off + pin0 + k * nb);
   }
   topm = 0;
   zhi = -P3D_INF;
@@ -536,7 +570,7 @@ P3D_K1_LOOP_UNROLL
 #pragma unroll
   for (int k = 0; k < KM; ++k) {
     if (k >= DD) break;
-    slot[k] = a.slot[pin0 + k * nb];
+    slot[k] = ld_stream(a.slot + pin0 + k * nb);
   }
 #pragma unroll
   for (int k = 0; k < KM; ++k) {
@@ -547,8 +581,7 @@ P3D_K1_LOOP_UNROLL
       a.out_f[slot[k]] = make_float4((float)sm.px[k][lane], (float)sm.py[k][lane],
                                      (float)sm.gc[k][lane], (float)gb);
     else
-      reinterpret_cast<double4*>(a.out_d)[slot[k]] =
-          make_double4(sm.px[k][lane], sm.py[k][lane], sm.gc[k][lane], gb);
+      store_rec(a.out_d, slot[k], sm.px[k][lane], sm.py[k][lane], sm.gc[k][lane], gb);
   }
 }
 
@@ -587,9 +620,9 @@ __device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, 
   const int nb = tk.y, j = tk.z + lane;
   if (j >= nb || a.net_dup[t0 + j]) return;  // duplicate-owner nets: generic kernel
   const int p0 = tk.x + j, p1 = p0 + nb;
-  const int i0 = a.pin_inst[p0], i1 = a.pin_inst[p1];
-  const int s0 = a.slot[p0], s1 = a.slot[p1];
-  const float4 o0 = a.off[p0], o1 = a.off[p1];
+  const int i0 = ld_stream(a.pin_inst + p0), i1 = ld_stream(a.pin_inst + p1);
+  const int s0 = ld_stream(a.slot + p0), s1 = ld_stream(a.slot + p1);
+  const float4 o0 = ld_stream(a.off + p0), o1 = ld_stream(a.off + p1);
   const double4 q0 = a.pos4[i0], q1 = a.pos4[i1];
   const int t0p = (q0.z - a.dz2) > 0.0, t1p = (q1.z - a.dz2) > 0.0;
   const double x0 = q0.x + (double)(t0p ? o0.x : o0.z), y0 = q0.y + (double)(t0p ? o0.y : o0.w);
@@ -609,8 +642,8 @@ __device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, 
     a.out_f[s0] = make_float4((float)gx0, (float)gy0, (float)gz0, 0.f);
     a.out_f[s1] = make_float4((float)gx1, (float)gy1, (float)gz1, 0.f);
   } else {
-    reinterpret_cast<double4*>(a.out_d)[s0] = make_double4(gx0, gy0, gz0, 0.0);
-    reinterpret_cast<double4*>(a.out_d)[s1] = make_double4(gx1, gy1, gz1, 0.0);
+    store_rec(a.out_d, s0, gx0, gy0, gz0, 0.0);
+    store_rec(a.out_d, s1, gx1, gy1, gz1, 0.0);
   }
 }
 
