@@ -51,6 +51,33 @@ inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// Store a double with an L2 evict-last policy (data the next kernel gathers
+// from: field maps, the step's pos4 copy).  -DP3D_L2_KEEP=0 disables.
+#ifndef P3D_L2_KEEP
+#define P3D_L2_KEEP 1
+#endif
+__device__ __forceinline__ void st_keep(double* p, double v) {
+#if P3D_L2_KEEP
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#else
+  *p = v;
+#endif
+}
+__device__ __forceinline__ void st_keep2(double* p, double a, double b) {  // 16-byte aligned
+#if P3D_L2_KEEP
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b),
+               "l"(pol)
+               : "memory");
+#else
+  p[0] = a;
+  p[1] = b;
+#endif
+}
+
 // ---------------------------------------------------------------------------
 // warp / block reductions (deterministic: fixed shuffle tree, fixed order)
 // ---------------------------------------------------------------------------

@@ -503,7 +503,10 @@ __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
       gp.u[j] = un[c];
       gp.v[j] = vn[c];
     }
-    if (i < I) reinterpret_cast<double4*>(gp.pos4)[i] = make_double4(vn[0], vn[1], vn[2], 0.0);
+    if (i < I) {  // K1 gathers these next iteration: keep them in L2
+      st_keep2(gp.pos4 + 4 * (long long)i, vn[0], vn[1]);
+      st_keep2(gp.pos4 + 4 * (long long)i + 2, vn[2], 0.0);
+    }
   }
   double* part = gp.partials + (long long)kSlotAdv * kPartialStride;
   block_sum<1>(dv2, red);

@@ -524,8 +524,8 @@ __global__ void __launch_bounds__(kThreads) spec_inv_yz(FastArgs a) {
       double y0, y1;
       if (map == 3) { y0 = z.y * r2; y1 = y0; }  // sine series along z (Ez)
       else { y0 = z.x + z.y * r2; y1 = z.x - z.y * r2; }
-      out[m * 8 + map] = y0;
-      out[m * 8 + 4 + map] = y1;
+      st_keep(out + m * 8 + map, y0);  // K4 gathers the maps next: keep them in L2
+      st_keep(out + m * 8 + 4 + map, y1);
     }
     return;
   }

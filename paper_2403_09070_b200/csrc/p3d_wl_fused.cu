@@ -745,8 +745,9 @@ __global__ void __launch_bounds__(256) fused_gather_kernel(FusedGatherArgs a) {
       const double4* in = reinterpret_cast<const double4*>(a.in_d);
 #pragma unroll 4
       for (int s = b; s < e; ++s) {
-        const double4 r = in[s];
-        s0 += r.x; s1 += r.y; s2 += r.z; s3 += r.w;
+        const double2* r2 = reinterpret_cast<const double2*>(in + s);
+        const double2 ra = __ldcs(r2), rb = __ldcs(r2 + 1);  // dead after this read
+        s0 += ra.x; s1 += ra.y; s2 += rb.x; s3 += rb.y;
       }
     } else {
 #pragma unroll 4
