@@ -262,7 +262,8 @@ typedef struct p3d_gp {
   float* pin_out_f;            /* [n_pin][4] slot order (gx, gy, g_cut, 0) */
   double* pin_out_fd;          /* [n_pin] slot order FD depth term */
   double* pos4;                /* [n_inst][4] AoS copy of v (x, y, z, 0) */
-  double* inst_g;              /* [4][n_inst] gx, gy, gz_hbt, gz_bist */
+  double* inst_g;              /* [n_inst][4] gx, gy, gz_hbt, gz_bist (sharded: rows
+                                  padded to shard_size equal slabs) */
   int64_t* rho_fx;             /* [B] */
   /* spatial tile sort of the objects for the privatised scatter (K2) */
   int32_t ts_n_tiles, ts_tiles_x, ts_tiles_y;
@@ -287,7 +288,7 @@ typedef struct p3d_gp {
   int32_t sh_i0, sh_i1, sh_f0, sh_f1;
   double* shard_tot;           /* [32] per-rank totals the host all-reduces between
                                   stages: [0,6) net totals, [8,14) density totals,
-                                  [16] max |g| (iteration 0) */
+                                  [16] max |g| (iteration 0), [20,23) L1 norms */
   int32_t overlap;             /* 1: the wirelength branch (K1, K1b) runs on a side
                                   stream concurrently with the density branch (K2,
                                   K3), joined before K4 (fused loop) */
@@ -296,7 +297,8 @@ typedef struct p3d_gp {
 
 /* Stages of one sharded GP iteration.  The host runs them in this order with
  * the collectives in brackets (sum unless noted):
- *   NET, GATHER, [inst_g], NORMS, SCATTER, [rho_fx (int64, exact)], SPECTRAL,
+ *   NET, GATHER, [reduce-scatter inst_g slabs], NORMS, [shard_tot[20:23]],
+ *   NORMS_FINAL, SCATTER, [rho_fx (int64, exact)], SPECTRAL,
  *   DENS, [shard_tot[0:16]], CONTROL, STEP0, [shard_tot[16], max],
  *   STEP0_CONTROL, ADVANCE, [st->dv2_next], [all-gather of pos4 slabs]. */
 enum {
@@ -310,7 +312,8 @@ enum {
   P3D_SH_STEP0 = 7,
   P3D_SH_STEP0_CONTROL = 8,
   P3D_SH_ADVANCE = 9,
-  P3D_SH_N_STAGES = 10
+  P3D_SH_NORMS_FINAL = 10,
+  P3D_SH_N_STAGES = 11
 };
 
 /* Reset the loop state (lambda unset, a = 1, iteration 0) and project u = v =

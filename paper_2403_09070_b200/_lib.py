@@ -80,7 +80,7 @@ class Gp(C.Structure):
                 ("pad2", I32)]
 
 SH_STAGES = ("NET", "GATHER", "NORMS", "SCATTER", "SPECTRAL", "DENS", "CONTROL", "STEP0",
-             "STEP0_CONTROL", "ADVANCE")
+             "STEP0_CONTROL", "ADVANCE", "NORMS_FINAL")
 
 
 _SIGS = {

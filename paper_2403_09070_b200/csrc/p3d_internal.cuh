@@ -100,7 +100,7 @@ struct FusedGatherArgs {
   const float4* in_f;         // fp32-mode records by slot
   const double* in_fd;
   const double* in_d;         // nullable: fp64-mode double4 records by slot
-  double* out;                // [4][n_obj]
+  double* out;                // [n_obj][4] (gx, gy, g_cut, FD)
   double* partials;
   unsigned int* counter;
   double* final_norms;

@@ -234,7 +234,10 @@ __device__ __forceinline__ void load_object_inputs(const p3d_gp& gp, int i, cons
   wl4[0] = wl4[1] = wl4[2] = wl4[3] = 0.0;
   if (i < I) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) wl4[k] = gp.inst_g[(long long)k * I + i];
+    {
+      const double4 g = reinterpret_cast<const double4*>(gp.inst_g)[i];
+      wl4[0] = g.x; wl4[1] = g.y; wl4[2] = g.z; wl4[3] = g.w;
+    }
   }
   pq = mdeg = 0.0;
   pw[0] = pw[1] = pw[2] = pd[0] = pd[1] = pd[2] = 0.0;
@@ -806,17 +809,19 @@ int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 // sharded loop (config 4): the stages that follow a collective
 // ---------------------------------------------------------------------------
-// L1 norms of the all-reduced owner sums + the Eq. 17 scale (every rank, all
-// instances: identical on every rank)
+// L1 norms of this rank's instance slab of the reduced owner sums (partials
+// into shard_tot[20, 23), all-reduced by the host, then norms_final_kernel)
 __global__ void __launch_bounds__(256) inst_norms_kernel(p3d_gp gp) {
   if (gp.st->done) return;
   __shared__ double red[32 * 3];
-  const int I = gp.n_inst;
   double acc[3] = {0, 0, 0};
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < I; i += gridDim.x * blockDim.x) {
-    acc[0] += fabs(gp.inst_g[i]);
-    acc[1] += fabs(gp.inst_g[I + i]);
-    acc[2] += fabs(gp.inst_g[3 * (long long)I + i]);
+  const double4* g4 = reinterpret_cast<const double4*>(gp.inst_g);
+  for (int i = gp.sh_i0 + blockIdx.x * blockDim.x + threadIdx.x; i < gp.sh_i1;
+       i += gridDim.x * blockDim.x) {
+    const double4 g = g4[i];
+    acc[0] += fabs(g.x);
+    acc[1] += fabs(g.y);
+    acc[2] += fabs(g.w);
   }
   double* part = gp.partials + (long long)kSlotGather * kPartialStride;
   block_sum<3>(acc, red);
@@ -825,14 +830,20 @@ __global__ void __launch_bounds__(256) inst_norms_kernel(p3d_gp gp) {
   if (last_block(&gp.st->counters[kCntGather])) {
     double n[3];
     for (int q = 0; q < 3; ++q) n[q] = ordered_sum(part + q * gridDim.x, gridDim.x, red);
-    if (threadIdx.x == 0) {
-      double* f = fin(gp) + kFinNorm;
-      f[0] = n[0];
-      f[1] = n[1];
-      f[2] = n[2];
-      f[3] = n[2] == 0.0 ? 0.0 : (n[0] + n[1]) / (2.0 * n[2]);  // Eq. 17
-    }
+    if (threadIdx.x == 0)
+      for (int q = 0; q < 3; ++q) gp.shard_tot[20 + q] = n[q];
   }
+}
+
+// the norms over all ranks + the Eq. 17 scale (identical on every rank)
+__global__ void norms_final_kernel(p3d_gp gp) {
+  if (gp.st->done) return;
+  double* f = fin(gp) + kFinNorm;
+  const double* t = gp.shard_tot + 20;
+  f[0] = t[0];
+  f[1] = t[1];
+  f[2] = t[2];
+  f[3] = t[2] == 0.0 ? 0.0 : (t[0] + t[1]) / (2.0 * t[2]);  // Eq. 17
 }
 
 // loop control with the all-reduced totals (net: shard_tot[0,6), density:
@@ -866,6 +877,7 @@ int gp_shard_stage(const p3d_gp& gp, int stage, cudaStream_t s) {
     case P3D_SH_NORMS:
       inst_norms_kernel<<<grid_blocks(gp.n_inst, 256, kMaxBlocks), 256, 0, s>>>(gp);
       break;
+    case P3D_SH_NORMS_FINAL: norms_final_kernel<<<1, 1, 0, s>>>(gp); break;
     case P3D_SH_SCATTER: scatter_k2(gp, &gp.st->done, s); break;
     case P3D_SH_SPECTRAL: if (const int rc = launch_k3(gp, s)) return rc; break;
     case P3D_SH_DENS: pdl_launch(dens_kernel, gp.n_macro + gp.nblk_dens, 256, 0, s, gp); break;

@@ -756,10 +756,7 @@ __global__ void __launch_bounds__(256) fused_gather_kernel(FusedGatherArgs a) {
         s0 += (double)r.x; s1 += (double)r.y; s2 += (double)r.z; s3 += (double)r.w;
       }
     }
-    a.out[i] = s0;
-    a.out[a.n_obj + i] = s1;
-    a.out[2 * a.n_obj + i] = s2;
-    a.out[3 * a.n_obj + i] = s3;
+    reinterpret_cast<double4*>(a.out)[i] = make_double4(s0, s1, s2, s3);  // [n_obj][4]
     acc[0] += fabs(s0);
     acc[1] += fabs(s1);
     acc[2] += fabs(s3);

@@ -466,7 +466,7 @@ class Gp3dProblem:
         self.t_pos4 = z(4 * max(I, R * self.inst_slab))
         self.t_shard_tot = z(32)
         g.shard_tot = keep(self.t_shard_tot)
-        self.t_inst_g = z(4 * I)
+        self.t_inst_g = z(4 * max(I, R * self.inst_slab))
         self.t_rho_fx = torch.zeros(B, dtype=torch.int64, device="cuda")
         self.t_rho = z(B)
         tx, ty = -(-grid.nx // 16), -(-grid.ny // 16)  # kTile in p3d_density.cu

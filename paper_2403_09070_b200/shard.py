@@ -5,8 +5,9 @@ Each rank owns a slab of instances (equal padded size), a slab of fillers and
 the K1 warp tasks w with w % world == rank.  Per iteration (gp.py:386-444):
 
     NET, GATHER       K1 on own nets -> records of own pins; owner partial sums
-    [all-reduce]      per-instance WL sums inst_g [4][I] (fp64)
-    NORMS             L1 norms + Eq. 17 scale (identical on every rank)
+    [reduce-scatter]  per-instance WL sums inst_g [I][4] (fp64): own slab only
+    NORMS             L1 norms over the own slab
+    [all-reduce]      the three norms;  NORMS_FINAL: Eq. 17 scale
     SCATTER           K2 on own objects -> partial int64 fixed-point rho
     [all-reduce]      rho (int64: exact, the single-GPU map bit for bit)
     SPECTRAL          K3, replicated (maps are small and L2-resident)
@@ -63,6 +64,20 @@ class ShardComm:
             dist.all_reduce(h, op=op)
             t.copy_(h)
 
+    def reduce_scatter_chunks(self, buf, n):
+        """buf[r*n:(r+1)*n] <- sum over ranks of that chunk (every rank's own
+        chunk; the other chunks are left undefined)."""
+        if not self.on or n == 0:
+            return
+        full = buf[: self.world * n]
+        mine = full[self.rank * n:(self.rank + 1) * n]
+        if self.nccl:
+            dist.reduce_scatter_tensor(mine, full)
+        else:
+            h = full.cpu()
+            dist.all_reduce(h)
+            mine.copy_(h[self.rank * n:(self.rank + 1) * n])
+
     def all_gather_chunks(self, buf, n):
         """buf[:world*n] <- concatenation of every rank's chunk buf[r*n:(r+1)*n]."""
         if not self.on or n == 0:
@@ -90,6 +105,7 @@ class ShardedGp3d:
         self._dv2 = p.t_st[off: off + 8].view(torch.float64)
         self._tot16 = p.t_shard_tot[:16]
         self._tot_max = p.t_shard_tot[16:17]
+        self._norms = p.t_shard_tot[20:23]
 
     def _stage(self, name):
         _lib.call("p3d_gp_shard_stage", _lib.byref(self.prob.gp), STAGE[name], _lib.stream_ptr())
@@ -102,8 +118,10 @@ class ShardedGp3d:
         for _ in range(n):
             self._stage("NET")
             self._stage("GATHER")
-            c.all_reduce(p.t_inst_g)
+            c.reduce_scatter_chunks(p.t_inst_g, 4 * p.inst_slab)  # own instance slab
             self._stage("NORMS")
+            c.all_reduce(self._norms)
+            self._stage("NORMS_FINAL")
             self._stage("SCATTER")
             c.all_reduce(p.t_rho_fx)
             self._stage("SPECTRAL")
