@@ -255,7 +255,10 @@ typedef struct p3d_gp {
   double mu_min, mu_max, gamma0, gamma1, min_step, step_scale;
   int64_t rho_t_fx;
   /* state, [3][n_obj] SoA unless noted */
-  double *u, *v, *v_prev, *best;
+  double *u, *v;
+  double *v_prev;              /* unused since the step reduces |v_new - v|^2 itself
+                                  (kept for ABI stability; may be null) */
+  double *best;
   double *wl_grad, *dens_grad, *pre, *prev_wl, *prev_dens;
   double* prev_q;              /* [n_obj] */
   double* pin_out;             /* [n_pin][4] slot order (exact mode) */

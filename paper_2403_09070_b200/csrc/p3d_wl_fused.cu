@@ -674,6 +674,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_ke
     if (w >= a.n_tasks) break;
     const int4 tk = a.tasks[w];
     const int t0 = a.task_t0[w];
+    // timing probes only (they drop work; results are wrong): -DP3D_SKIP_D2 / _DGE3
 #ifdef P3D_SKIP_D2
     if (tk.w == 2) continue;
 #endif

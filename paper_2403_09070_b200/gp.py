@@ -457,7 +457,8 @@ class Gp3dProblem:
         g.step_scale = grid.wb
         g.rho_t_fx = int(np.rint(cfg.target_density * np.ldexp(1.0, dn.FX_BITS)))
         z = lambda n: torch.zeros(max(int(n), 1), dtype=torch.float64, device="cuda")  # noqa: E731
-        self.t_u, self.t_v, self.t_vprev, self.t_best = z(3 * O), z(3 * O), z(3 * O), z(3 * O)
+        self.t_u, self.t_v, self.t_best = z(3 * O), z(3 * O), z(3 * O)
+        self.t_vprev = z(1)  # p3d_gp.v_prev is unused (the step reduces |dv|^2 itself)
         self.t_wl, self.t_dens, self.t_pre = z(3 * O), z(3 * O), z(3 * O)
         self.t_prev_wl, self.t_prev_dens, self.t_prev_q = z(3 * O), z(3 * O), z(O)
         self.t_pin_out = z(4 * P)
