@@ -218,9 +218,11 @@ def make_problem_inputs(design, spec, grid_n, max_iters, G):
     return cfg, grid, st, pos0
 
 
-def roofline_of(design, n_fill, grid, stage_ms, config):
-    """Roofline of the dominant kernel family (SURVEY 8d algorithmic bytes)."""
+def roofline_of(design, n_fill, grid, stage_ms, config, shards=1):
+    """Roofline of the dominant kernel family (SURVEY 8d algorithmic bytes;
+    with `shards`, one rank's share: every family but the replicated K3)."""
     q = algorithmic_bytes(design, n_fill, grid.n_bins)
+    q = {k: (v if k == "K3" else v / shards) for k, v in q.items()}
     fam_ms = {"K1": stage_ms[0] + stage_ms[1], "K2": stage_ms[2], "K3": stage_ms[3],
               "K4": stage_ms[4], "K5": stage_ms[5] + stage_ms[6]}
     dom = max(fam_ms, key=fam_ms.get)
@@ -341,6 +343,12 @@ def main():
         kpi = _lib.load().p3d_gp_kernels_per_iteration(_lib.byref(prob.gp))
     else:
         kpi = _lib.load().p3d_gp_kernels_per_iteration(_lib.byref(prob.gp)) + 3
+        marks = []
+        runner.iterate(K, marks=marks)  # eager, with events between stages
+        att = runner.attribute(marks)
+        stage = np.array([att.get("K1", 0.0), 0.0, att.get("K2", 0.0), att.get("K3", 0.0),
+                          att.get("K4", 0.0), att.get("K5", 0.0), 0.0]) / K
+        comm_ms = att.get("comm", 0.0) / K
 
     # ---- end to end through the public API: pinned host state in, K steps with
     # the per-iteration log row read back every step, final positions out
@@ -403,8 +411,13 @@ def main():
         "clocks": clocks.summary(),
         "final_row": list(prob.log_rows(W + K)[-1]),
     }
-    if mode != "sharded":
-        line["roofline"] = roofline_of(design, prob.n_fill, grid, stage, args.config)
+    line["roofline"] = roofline_of(design, prob.n_fill, grid, stage, args.config,
+                                   shards=world if mode == "sharded" else 1)
+    if mode == "sharded":  # rank 0's stage attribution of one shard (eager replay)
+        line["roofline"]["traffic"] = None
+        line["roofline"]["note"] = ("rank-0 shard, eager stages; algorithmic bytes of the whole "
+                                    "placement / world per family")
+        line["config"]["collective_ms_per_step"] = round(comm_ms, 4)
     if not args.no_cpu_baseline and world == 1:
         rate, iters, el = cpu_baseline(design, grid_n, spec, seconds=args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "it/s", "cores": 1, "kind": "port",

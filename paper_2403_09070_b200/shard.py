@@ -113,27 +113,58 @@ class ShardedGp3d:
     def init_loop(self, pos0):
         self.prob.init_loop(pos0)
 
-    def iterate(self, n=1):
+    def iterate(self, n=1, marks=None):
+        """n sharded iterations; `marks` (a list) collects (label, cuda Event)
+        after every stage / collective for attribution (eager runs only)."""
         p, c = self.prob, self.comm
+
+        def mark(label):
+            if marks is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                marks.append((label, e))
+
         for _ in range(n):
+            mark("start")
             self._stage("NET")
             self._stage("GATHER")
+            mark("K1")
             c.reduce_scatter_chunks(p.t_inst_g, 4 * p.inst_slab)  # own instance slab
+            mark("comm")
             self._stage("NORMS")
             c.all_reduce(self._norms)
             self._stage("NORMS_FINAL")
+            mark("comm")
             self._stage("SCATTER")
+            mark("K2")
             c.all_reduce(p.t_rho_fx)
+            mark("comm")
             self._stage("SPECTRAL")
+            mark("K3")
             self._stage("DENS")
+            mark("K4")
             c.all_reduce(self._tot16)
             self._stage("CONTROL")
             self._stage("STEP0")
             c.all_reduce(self._tot_max, dist.ReduceOp.MAX if c.on else None)
             self._stage("STEP0_CONTROL")
+            mark("comm")
             self._stage("ADVANCE")
+            mark("K5")
             c.all_reduce(self._dv2)
             c.all_gather_chunks(p.t_pos4, 4 * p.inst_slab)
+            mark("comm")
+
+    @staticmethod
+    def attribute(marks):
+        """{label: total ms} from the marks of iterate(marks=...)."""
+        torch.cuda.synchronize()
+        out = {}
+        for (_, a), (lab, b) in zip(marks, marks[1:]):
+            if lab == "start":
+                continue
+            out[lab] = out.get(lab, 0.0) + a.elapsed_time(b)
+        return out
 
     def capture(self, iters_per_graph=1):
         """CUDA graph of `iters_per_graph` sharded iterations, collectives
