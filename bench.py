@@ -193,7 +193,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "it/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / rate,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": WORKLOADS[args.config], "grid": [grid_n] * 2 + [2],
                                         "max_iters_schedule": 200},
         "cpu_baseline": {"value": rate, "unit": "it/s", "cores": 1, "kind": "port",
