@@ -120,6 +120,53 @@ def gp2d_wirelength(prob: Gp2dProblem, dp, pos_soa, n_obj, gamma):
     return value, grad
 
 
+class _Layer:
+    """One planar field of the 2D GP (nz = 1 grid): a persistent device charge
+    cloud whose x/y buffers are refreshed from the positions each iteration,
+    then the K2 scatter, the K3 spectral solve (one pass: phi and E), the K4
+    force gather and the fixed-point overflow, all through the C-ABI."""
+
+    def __init__(self, grid, idx, sw, sh, weight, is_macro, movable_volume, rho_t):
+        self.grid, self.idx, self.n = grid, idx, int(idx.numel())
+        self.mv, self.rho_t = movable_volume, rho_t
+        if not self.n:
+            return
+        k = self.n
+        full = lambda v: torch.full((k,), v, dtype=torch.float64, device="cuda")  # noqa: E731
+        self.x = torch.empty(k, dtype=torch.float64, device="cuda")
+        self.y = torch.empty(k, dtype=torch.float64, device="cuda")
+        self.cloud = dn.ChargeCloud(x=self.x, y=self.y, z=full(grid.dz / 2), w=sw[idx].contiguous(),
+                                    h=sh[idx].contiguous(), dep=full(grid.dz),
+                                    weight=_dev.f64(weight), is_macro=np.asarray(is_macro))
+        self.dc = dn._DevCloud(self.cloud)
+        self.g, _ = grid.device()
+        B = grid.n_bins
+        self.rho_fx = torch.zeros(B, dtype=torch.int64, device="cuda")
+        self.rho = torch.empty(B, dtype=torch.float64, device="cuda")
+        self.maps = torch.empty((B, 4), dtype=torch.float64, device="cuda")
+        self.spec = torch.empty(6 * B, dtype=torch.float64, device="cuda")
+        self.force = torch.empty((k, 3), dtype=torch.float64, device="cuda")
+        self.energy = torch.zeros(1, dtype=torch.float64, device="cuda")
+        self.gscr = _dev.scratch(8 + self.dc.struct.n_macro + 1024 + 8)
+        self.oscr = _dev.scratch(8 + 1024 + 8)
+
+    def run(self, p, dens_grad, ovfl_out):
+        torch.index_select(p[:, 0], 0, self.idx, out=self.x)
+        torch.index_select(p[:, 1], 0, self.idx, out=self.y)
+        g, s = _lib.byref(self.g), _lib.stream_ptr()
+        self.rho_fx.zero_()
+        _lib.call("p3d_accumulate_density", g, _lib.byref(self.dc.struct), _lib.ptr(self.rho_fx), s)
+        _lib.call("p3d_fx_to_density", int(self.rho.numel()), _lib.ptr(self.rho_fx),
+                  _lib.ptr(self.rho), s)
+        _lib.call("p3d_spectral", g, _lib.ptr(self.rho), None, _lib.ptr(self.maps),
+                  _lib.ptr(self.spec), s)
+        _lib.call("p3d_density_gather", g, _lib.byref(self.dc.struct), _lib.ptr(self.maps), None,
+                  _lib.ptr(self.energy), _lib.ptr(self.force), _lib.ptr(self.gscr), s)
+        dens_grad[self.idx] = self.force[:, :2]
+        _lib.call("p3d_overflow_fx", g, _lib.ptr(self.rho_fx), float(self.rho_t), float(self.mv),
+                  _lib.ptr(ovfl_out), _lib.ptr(self.oscr), s)
+
+
 def run_gp2d_multi(design, state, cfg: GpConfig, iteration_log=None, rng=None):
     """Planar refinement with a fixed partition (gp.py:531-690); returns
     (state, GpInfo, {crossing net: HBT centre})."""
@@ -183,36 +230,24 @@ def run_gp2d_multi(design, state, cfg: GpConfig, iteration_log=None, rng=None):
         return out
 
     layer_idx = [torch.from_numpy(np.flatnonzero(obj_layer == l)).cuda() for l in range(3)]
-    layer_w = [sw[i] for i in layer_idx]
-    layer_h = [sh[i] for i in layer_idx]
-    layer_weight = [_dev.f64(np.where(is_macro_obj[obj_layer == l], cfg.target_density, 1.0))
-                    for l in range(3)]
-    layer_macro = [is_macro_obj[obj_layer == l] for l in range(3)]
+    layers = [_Layer(grids[l], layer_idx[l], sw, sh,
+                     np.where(is_macro_obj[obj_layer == l], cfg.target_density, 1.0),
+                     is_macro_obj[obj_layer == l], movable_vol[l], cfg.target_density)
+              for l in range(3)]
 
     def evaluate(p, gamma):
-        """gp.py:586-626: WL value/grads + per-layer raw density grads/overflow."""
+        """gp.py:586-626: WL value/grads + per-layer raw density grads/overflow
+        (one host read per iteration: the WL value and the three overflows)."""
         pos_soa = p.t().contiguous()
         val, wl_grad = gp2d_wirelength(prob, dp, pos_soa, n_obj, gamma)
         dens_grad = torch.zeros((n_obj, 2), dtype=torch.float64, device="cuda")
-        ovfls = []
-        for layer in range(3):
-            idx = layer_idx[layer]
-            g = grids[layer]
-            k = int(idx.numel())
-            if k == 0:
-                ovfls.append(0.0)
-                continue
-            full = lambda v: torch.full((k,), v, dtype=torch.float64, device="cuda")  # noqa: E731
-            cloud = dn.ChargeCloud(x=p[idx, 0], y=p[idx, 1], z=full(g.dz / 2), w=layer_w[layer],
-                                   h=layer_h[layer], dep=full(g.dz), weight=layer_weight[layer],
-                                   is_macro=layer_macro[layer])
-            rho_fx = dn.accumulate_density_fx(g, cloud)
-            phi, coef = dn.solve_potential(dn.fx_to_density(rho_fx), g)
-            ex, ey, _ = dn.electric_field(coef, g)
-            dgr = dn.density_force(g, cloud, ex, ey, torch.zeros_like(phi))
-            dens_grad[idx] = dgr[:, :2]
-            ovfls.append(dn.overflow_fx(rho_fx, g, cfg.target_density, movable_vol[layer]))
-        return float(val.item()), wl_grad, dens_grad, ovfls
+        ov = torch.zeros(4, dtype=torch.float64, device="cuda")
+        ov[3:4].copy_(val)
+        for layer, ctx in enumerate(layers):
+            if ctx.n:
+                ctx.run(p, dens_grad, ov[layer:layer + 1])
+        host = ov.cpu().tolist()
+        return host[3], wl_grad, dens_grad, host[:3]
 
     opt = NesterovOptimizer(_dev.f64(pos), project=project)
     info = GpInfo()
