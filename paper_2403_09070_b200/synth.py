@@ -222,7 +222,7 @@ def cached_synth(spec: SynthSpec, cache_dir=None) -> ArrayDesign:
     a = des.arrays()
     try:
         os.makedirs(cache_dir, exist_ok=True)
-        tmp = path + ".tmp.npz"
+        tmp = f"{path}.{os.getpid()}.tmp.npz"  # per process: ranks may race here
         np.savez(tmp, is_macro=a.is_macro, w_top=a.w_top, h_top=a.h_top, w_bot=a.w_bot,
                  h_bot=a.h_bot, net_ptr=a.net_ptr, pin_inst=a.pin_inst, ox_top=a.ox_top,
                  oy_top=a.oy_top, ox_bot=a.ox_bot, oy_bot=a.oy_bot,
