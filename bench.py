@@ -270,9 +270,16 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    # test hooks (not for measurements): P3D_BENCH_DEVICE pins every rank to one
+    # GPU, P3D_BENCH_BACKEND=gloo replaces NCCL (several ranks on one device)
+    dev = int(os.environ.get("P3D_BENCH_DEVICE", local))
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("P3D_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     from paper_2403_09070_b200 import _lib
     from paper_2403_09070_b200 import gp as G
 
@@ -312,7 +319,7 @@ def main():
     step(W)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev) as clocks:
         torch.cuda.synchronize()
         e0.record(stream)
         step(K)

@@ -1,4 +1,8 @@
-python -c 'import __graft_entry__ as g; g.build()' > /dev/null 2>&1
-timeout 900 python bench.py --steps 30 --warmup 5 --cpu-seconds 20 > gpurun_out/bench_final1.log 2>&1; echo bench $?
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_final1.csv python bench.py --steps 10 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu_l $?
-bash tools/gpu_ncu.sh final1 "advance|dens_kernel|fused|scatter|spec_|tile_|gmax0" 11 60
+python -c 'import __graft_entry__ as g; g.build()' >/dev/null 2>&1
+export P3D_BENCH_DEVICE=0 P3D_BENCH_BACKEND=gloo
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 5 --warmup 3 --no-cpu-baseline --config 2 > gpurun_out/b2_sharded.log 2>&1; echo sharded $?
+tail -1 gpurun_out/b2_sharded.log | cut -c1-700
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --steps 5 --warmup 3 --no-cpu-baseline --config 2 --mode replicas > gpurun_out/b2_rep.log 2>&1; echo replicas $?
+tail -1 gpurun_out/b2_rep.log | cut -c1-400
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 2 --steps 2 --warmup 1 --impl reference --config 1 > gpurun_out/b2_ref.log 2>&1; echo ref $?
+tail -1 gpurun_out/b2_ref.log | cut -c1-300
