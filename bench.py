@@ -244,6 +244,114 @@ def roofline_of(design, n_fill, grid, stage_ms, config, shards=1):
             "per_family": per_family}
 
 
+def run_batch(args, rank, world, local):
+    """Config-5 style throughput: args.batch independent placements per GPU
+    (seeds differ per placement and rank), each a CUDA graph of one iteration,
+    replayed round-robin on its own stream so the GPU overlaps them."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_09070_b200 import gp as G
+
+    dev = int(os.environ.get("P3D_BENCH_DEVICE", local))
+    torch.cuda.set_device(dev)
+    if world > 1:
+        backend = os.environ.get("P3D_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    W, K, Bn = max(args.warmup, 3), args.steps, args.batch
+    max_iters = max(200, W + 2 * K + 2)
+    probs, graphs, starts = [], [], []
+    for b in range(Bn):
+        design, grid_n, spec = setup_design(args.config, rank * Bn + b)
+        cfg, grid, st, pos0 = make_problem_inputs(design, spec, grid_n, max_iters, G)
+        prob = G.Gp3dProblem(design, grid, st.fillers, cfg, st.rot, precision=args.precision)
+        prob.init_loop(pos0)
+        probs.append(prob)
+        graphs.append(prob.capture(1))
+        starts.append(pos0)
+    streams = [torch.cuda.Stream() for _ in range(Bn)]
+    cur = torch.cuda.current_stream()
+
+    def step(n):
+        for s_ in streams:
+            s_.wait_stream(cur)
+        for _ in range(n):
+            for g_, s_ in zip(graphs, streams):
+                with torch.cuda.stream(s_):
+                    g_.replay()
+        for s_ in streams:
+            cur.wait_stream(s_)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    step(W)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        torch.cuda.synchronize()
+        e0.record(cur)
+        step(K)
+        e1.record(cur)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    for p_ in probs:
+        s_ = p_.state()
+        assert not s_.done and s_.it == W + K, f"loop ended early (it={s_.it})"
+    # end to end: every placement's host positions in, K steps, positions out
+    host_pos = [torch.from_numpy(p0).pin_memory() for p0 in starts]
+    host_out = [torch.empty((p_.n_obj, 3), dtype=torch.float64).pin_memory() for p_ in probs]
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    f0.record(cur)
+    for p_, h in zip(probs, host_pos):
+        p_.init_loop(h.to("cuda", non_blocking=True))
+    step(K)
+    for p_, h in zip(probs, host_out):
+        h.copy_(p_._aos(p_.t_u), non_blocking=True)
+    f1.record(cur)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, e2e_ms = float(t[0]), float(t[1])
+    if rank != 0:
+        dist.destroy_process_group() if world > 1 else None
+        return
+    units = world * Bn * K
+    line = {
+        "metric": METRIC, "value": units / (ms / 1000.0), "unit": "it/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (paper_2403_09070_b200.synth, one seed per placement)",
+        "config": {"workload": f"cfg5-style: {Bn} independent placements per GPU of "
+                               + WORKLOADS[args.config], "placements": world * Bn,
+                   "parallelism": f"{Bn} concurrent graphs per GPU x {world} GPUs",
+                   "mode": "batch", "l2": "no flush: working sets exceed L2"},
+        "e2e": {"value": units / (e2e_ms / 1000.0), "unit": "it/s",
+                "h2d_bytes_per_step": int(sum(h.numel() * 8 for h in host_pos) / K),
+                "d2h_bytes_per_step": int(sum(h.numel() * 8 for h in host_out) / K)},
+        "gpu_launches": int(_lib_kernels(probs[0]) * Bn * K),
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _lib_kernels(prob):
+    from paper_2403_09070_b200 import _lib
+
+    return _lib.load().p3d_gp_kernels_per_iteration(_lib.byref(prob.gp))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -251,10 +359,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default=None, choices=["fused", "sharded", "replicas"],
+    ap.add_argument("--mode", default=None, choices=["fused", "sharded", "replicas", "batch"],
                     help="fused: one GPU, the whole iteration in one CUDA graph (N=1 default); "
                          "sharded: ONE placement partitioned over the N ranks (N>1 default, "
-                         "strong scaling); replicas: N independent placements (weak scaling)")
+                         "strong scaling); replicas: N independent placements (weak scaling); "
+                         "batch: --batch independent placements per GPU, their iteration "
+                         "graphs replayed on concurrent streams (config 5 throughput)")
+    ap.add_argument("--batch", type=int, default=8, help="placements per GPU in --mode batch")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
@@ -266,6 +377,8 @@ def main():
     mode = args.mode or ("sharded" if world > 1 else "fused")
     if mode == "fused" and world > 1:
         mode = "replicas"
+    if mode == "batch":
+        return run_batch(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
