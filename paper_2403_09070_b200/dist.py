@@ -29,6 +29,17 @@ def shard_range(n, rank, world):
     return lo, lo + q + (1 if rank < r else 0)
 
 
+def object_slabs(n_inst, n_fill, rank, world):
+    """This rank's objects in the sharded loop: (instance slab size padded to
+    equal slabs, (i0, i1) instance range, (f0, f1) filler range in object
+    indices).  Equal padded instance slabs make the owner-sum reduce-scatter
+    and the position all-gather equal-count collectives."""
+    slab = -(-n_inst // world) if n_inst else 0
+    inst = (min(rank * slab, n_inst), min((rank + 1) * slab, n_inst))
+    lo, hi = shard_range(n_fill, rank, world)
+    return slab, inst, (n_inst + lo, n_inst + hi)
+
+
 def replica_seed(base_seed, rank):
     """Seed of the independent placement a rank runs in replica mode."""
     return int(base_seed) + int(rank)

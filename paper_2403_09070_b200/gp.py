@@ -25,6 +25,7 @@ import torch
 from . import _dev, _lib
 from . import density as dn
 from . import wirelength as wl
+from .dist import object_slabs
 from .model import PlacementState, partition_from_z, rotated_dims
 
 log = logging.getLogger("place3d")
@@ -380,11 +381,7 @@ class Gp3dProblem:
         # this rank's objects: an instance slab of equal padded size
         # (so the pos4 slabs all-gather with equal counts) and a filler slab
         R, r = self.shard_size, self.shard_rank
-        self.inst_slab = -(-I // R) if I else 0
-        self.sh_i = (min(r * self.inst_slab, I), min((r + 1) * self.inst_slab, I))
-        q, rem = divmod(F, R)
-        f_lo = r * q + min(r, rem)
-        self.sh_f = (I + f_lo, I + f_lo + q + (1 if r < rem else 0))
+        self.inst_slab, self.sh_i, self.sh_f = object_slabs(I, F, r, R)
         g.shard_rank, g.shard_size = r, (R if self.sharded else 0)
         # WL and density branches concurrently inside the iteration graph
         g.overlap = int(os.environ.get("P3D_OVERLAP", "1")) if not self.sharded else 0

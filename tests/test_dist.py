@@ -71,3 +71,57 @@ def test_gloo_world2_fixed_point_allreduce_exact():
         res = dict(out)
     assert all(res[r][0] for r in range(world))
     assert all(res[r][1] == [2.0, 5.0] for r in range(world))
+
+
+def test_object_slabs_cover_every_object_once():
+    from paper_2403_09070_b200.dist import object_slabs
+
+    for I, F in ((0, 0), (1, 0), (10, 3), (1001, 77), (800064, 40000)):
+        for world in (1, 2, 3, 8):
+            seen = np.zeros(I + F, dtype=int)
+            slab = None
+            for r in range(world):
+                s, (i0, i1), (f0, f1) = object_slabs(I, F, r, world)
+                slab = s if slab is None else slab
+                assert s == slab and i1 - i0 <= s and i0 == min(r * s, I)
+                seen[i0:i1] += 1
+                seen[f0:f1] += 1
+                assert I <= f0 <= f1 <= I + F
+            assert np.all(seen == 1)
+
+
+def _comm_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2403_09070_b200.shard import ShardComm
+
+        c = ShardComm()
+        n = 5
+        buf = torch.arange(world * n, dtype=torch.float64) + 100 * rank
+        c.reduce_scatter_chunks(buf, n)  # own chunk = sum over ranks of that chunk
+        mine = buf[rank * n:(rank + 1) * n].clone()
+        g = torch.zeros(world * n, dtype=torch.float64)
+        g[rank * n:(rank + 1) * n] = rank + 1
+        c.all_gather_chunks(g, n)
+        t = torch.tensor([float(rank)])
+        c.all_reduce(t, dist.ReduceOp.MAX)
+        out[rank] = (mine.tolist(), g.tolist(), float(t))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_shard_collectives():
+    """The sharded loop's collectives (shard.ShardComm) on CPU tensors with gloo:
+    reduce-scatter of equal slabs, all-gather of slabs, max all-reduce."""
+    world, n = 2, 5
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_comm_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+        res = dict(out)
+    for r in range(world):
+        mine, g, t = res[r]
+        base = np.arange(world * n, dtype=float)[r * n:(r + 1) * n]
+        assert mine == list(world * base + 100 * sum(range(world)))
+        assert g == [float(k // n + 1) for k in range(world * n)]
+        assert t == world - 1
