@@ -409,6 +409,9 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
 #else
 #define P3D_K1_LOOP_UNROLL _Pragma("unroll 1")
 #endif
+#ifndef P3D_K1_TRIPLE
+#define P3D_K1_TRIPLE 1
+#endif
 #ifndef P3D_K1_RTD
 #define P3D_K1_RTD 0
 #endif
@@ -585,6 +588,77 @@ P3D_K1_LOOP_UNROLL
   }
 }
 
+// Degree-3 nets (a fifth of all nets) are never split either — one die holds
+// at most one pin or all three, so top + bot <= full — and their FD flip
+// delta is exactly 0: flipping a pin leaves spans that are differences of the
+// same coordinates and never exceed the full span (rounding is monotonic), so
+// max(full, sp + op) - full = 0 (wirelength.py:227-248).  Register-resident
+// like the pair path; the WA sums run in pin order as in the staged path (the
+// per-net totals may associate differently: same values to the last ulp).
+template <bool F32>
+__device__ __forceinline__ void triple_axis(const double (&v)[3], typename WaSel<F32>::R ig,
+                                            double& val, double (&g)[3]) {
+  using W = typename WaSel<F32>::W;
+  using R = typename WaSel<F32>::R;
+  const double hi = fmax(fmax(v[0], v[1]), v[2]), lo = fmin(fmin(v[0], v[1]), v[2]);
+  R ep[3], em[3];
+  W w;
+  w.init();
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    W::term(v[k], hi, lo, ig, ep[k], em[k]);
+    w.acc(v[k], hi, lo, ep[k], em[k], 1);
+  }
+  w.finalize();
+  val = w.value(hi, lo);
+  const GradK<R> gk = w.gk(hi, lo);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g[k] = (double)gk.grad(v[k], ig, ep[k], em[k]);
+}
+
+template <bool F32>
+__device__ __forceinline__ void triple_task(const FusedNetArgs& a, const int4 tk, int t0, int lane,
+                                            double (&acc)[6]) {
+  const int nb = tk.y, j = tk.z + lane;
+  if (j >= nb || a.net_dup[t0 + j]) return;  // duplicate-owner nets: generic kernel
+  const int p0 = tk.x + j;
+  int inst[3], slot[3];
+  float4 off[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    inst[k] = ld_stream(a.pin_inst + p0 + k * nb);
+    slot[k] = ld_stream(a.slot + p0 + k * nb);
+    off[k] = ld_stream(a.off + p0 + k * nb);
+  }
+  double x[3], y[3], z[3];
+  int tp[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double4 q = a.pos4[inst[k]];
+    tp[k] = (q.z - a.dz2) > 0.0;
+    x[k] = q.x + (double)(tp[k] ? off[k].x : off[k].z);
+    y[k] = q.y + (double)(tp[k] ? off[k].y : off[k].w);
+    z[k] = q.z;
+  }
+  const typename WaSel<F32>::R ig = (typename WaSel<F32>::R)a.inv_gamma;
+  double vx, vy, vz, gx[3], gy[3], gz[3];
+  triple_axis<F32>(x, ig, vx, gx);
+  triple_axis<F32>(y, ig, vy, gy);
+  triple_axis<F32>(z, ig, vz, gz);
+  acc[0] += vx;
+  acc[1] += vy;
+  acc[2] += vz;
+  acc[3] += fmax(fmax(x[0], x[1]), x[2]) - fmin(fmin(x[0], x[1]), x[2]);  // never split: full
+  acc[4] += fmax(fmax(y[0], y[1]), y[2]) - fmin(fmin(y[0], y[1]), y[2]);
+  const int ntop = tp[0] + tp[1] + tp[2];
+  acc[5] += (ntop > 0 && ntop < 3) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (F32) a.out_f[slot[k]] = make_float4((float)gx[k], (float)gy[k], (float)gz[k], 0.f);
+    else store_rec(a.out_d, slot[k], gx[k], gy[k], gz[k], 0.0);
+  }
+}
+
 // Two-pin WA on one axis (wirelength.py:76-98): the anchor pin's terms are
 // exp(0) = 1 and both non-trivial terms share the argument (lo - hi) / gamma,
 // so one exponential serves the segment.  Accumulated exactly like the staged
@@ -683,10 +757,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_ke
 #endif
     switch (tk.w) {
       case 2: pair_task<F32>(a, tk, t0, lane, acc); break;
-#if P3D_K1_RTD
-      case 3: case 4: case 5: case 6: staged_task<0, F32>(a, tk, t0, sm, lane, acc); break;
+#if P3D_K1_TRIPLE
+      case 3: triple_task<F32>(a, tk, t0, lane, acc); break;
 #else
       case 3: staged_task<3, F32>(a, tk, t0, sm, lane, acc); break;
+#endif
+#if P3D_K1_RTD
+      case 4: case 5: case 6: staged_task<0, F32>(a, tk, t0, sm, lane, acc); break;
+#else
       case 4: staged_task<4, F32>(a, tk, t0, sm, lane, acc); break;
       case 5: staged_task<5, F32>(a, tk, t0, sm, lane, acc); break;
       case 6: staged_task<6, F32>(a, tk, t0, sm, lane, acc); break;
