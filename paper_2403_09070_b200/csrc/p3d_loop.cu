@@ -463,7 +463,30 @@ __global__ void __launch_bounds__(256) gmax0_kernel(p3d_gp gp) {
 // ---------------------------------------------------------------------------
 // K5b: projected Nesterov update (gp.py:220-227); last block: schedules
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
+#ifndef P3D_K5_MINB
+#define P3D_K5_MINB 3
+#endif
+// project_obj (gp.py:280-294) on sizes loaded up front (same arithmetic)
+__device__ __forceinline__ void project_loaded(const p3d_gp& gp, bool inst, bool mac, double s0,
+                                               double s1, double s2, double s3, double fz,
+                                               double& x, double& y, double& z) {
+  const double dz = gp.grid.dz;
+  if (inst) {
+    z = clipd(z, dz / 4, 3 * dz / 4);
+    double w, h;
+    dynamic_wh(z, dz, mac, s0, s1, s2, s3, w, h);
+    x = clamp_span(x, w, gp.grid.dx);
+    y = clamp_span(y, h, gp.grid.dy);
+  } else {
+    x = clamp_span(x, s0, gp.grid.dx);
+    y = clamp_span(y, s1, gp.grid.dy);
+    z = fz;
+  }
+}
+
+// Every input of an object is loaded before the first store (read-only data
+// through the non-coherent path), so one object costs one memory round trip.
+__global__ void __launch_bounds__(256, P3D_K5_MINB) advance_kernel(p3d_gp gp) {
   pdl_wait();
   p3d_loop_state* st = gp.st;
   if (st->done) return;
@@ -475,29 +498,46 @@ __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
   const int n_own = own_count(gp);
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_own; k += gridDim.x * blockDim.x) {
     const int i = own_obj(gp, k);
-    double u[3];
+    const bool inst = i < I;
+    double u[3], v[3], pw[3], pd[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) u[c] = gp.u[(long long)c * O + i];
+    for (int c = 0; c < 3; ++c) {
+      const long long j = (long long)c * O + i;
+      u[c] = gp.u[j];
+      v[c] = gp.v[j];
+      pw[c] = __ldg(gp.prev_wl + j);
+      pd[c] = __ldg(gp.prev_dens + j);
+    }
+    const double pq = __ldg(gp.prev_q + i);
+    bool mac = false;
+    double s0, s1, s2 = 0.0, s3 = 0.0, fz = 0.0, mdeg = 0.0;
+    if (inst) {
+      mac = __ldg(gp.is_macro + i) != 0;
+      s0 = __ldg(gp.w_top + i);
+      s1 = __ldg(gp.h_top + i);
+      s2 = __ldg(gp.w_bot + i);
+      s3 = __ldg(gp.h_bot + i);
+      if (mac) mdeg = __ldg(gp.degree + i);
+    } else {
+      const int f = i - I;
+      s0 = __ldg(gp.fill_w + f);
+      s1 = __ldg(gp.fill_h + f);
+      fz = __ldg(gp.fill_z + f);
+    }
     if (best) {  // gp.py:406-409 (taken before the stop / advance, as in the reference)
 #pragma unroll
       for (int c = 0; c < 3; ++c) gp.best[(long long)c * O + i] = u[c];
     }
     if (stop) continue;
     // the step's gradient, re-derived from the stored raw gradients (gp.py:424-426)
-    const double mdeg = (i < I && gp.is_macro[i]) ? gp.degree[i] : 0.0;
-    const double div = precond_div(lam, gp.prev_q[i], mdeg);
-    double v[3], un[3], vn[3];
+    const double div = precond_div(lam, pq, mdeg);
+    double un[3], vn[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const long long j = (long long)c * O + i;
-      v[c] = gp.v[j];
-      const double pre = (gp.prev_wl[j] + lam * gp.prev_dens[j]) / div;
-      un[c] = v[c] - step * pre;
-    }
-    project_obj(gp, i, un[0], un[1], un[2]);
+    for (int c = 0; c < 3; ++c) un[c] = v[c] - step * ((pw[c] + lam * pd[c]) / div);
+    project_loaded(gp, inst, mac, s0, s1, s2, s3, fz, un[0], un[1], un[2]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) vn[c] = un[c] + mom * (un[c] - u[c]);
-    project_obj(gp, i, vn[0], vn[1], vn[2]);
+    project_loaded(gp, inst, mac, s0, s1, s2, s3, fz, vn[0], vn[1], vn[2]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const long long j = (long long)c * O + i;
@@ -506,7 +546,7 @@ __global__ void __launch_bounds__(256) advance_kernel(p3d_gp gp) {
       gp.u[j] = un[c];
       gp.v[j] = vn[c];
     }
-    if (i < I) {  // K1 gathers these next iteration: keep them in L2
+    if (inst) {  // K1 gathers these next iteration: keep them in L2
       st_keep2(gp.pos4 + 4 * (long long)i, vn[0], vn[1]);
       st_keep2(gp.pos4 + 4 * (long long)i + 2, vn[2], 0.0);
     }

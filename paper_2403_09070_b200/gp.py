@@ -394,11 +394,11 @@ class Gp3dProblem:
         mi = max(self.max_iters, 1)
         g.max_iters = self.max_iters
         g.divergence_window = int(cfg.divergence_window)
-        # object kernels run persistent waves of 256-thread CTAs: K5 with 8 per
-        # SM, K4 (64 registers) with the 4 per SM it can hold
+        # object kernels run one persistent wave of 256-thread CTAs: K5 (85
+        # registers, every load hoisted) 3 per SM, K4 (64 registers) 4 per SM
         n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
         g.nblk_obj = max(1, min(-(-O // 256), K_MAX_BLOCKS,
-                                int(os.environ.get("P3D_NBLK_OBJ", 8 * n_sm))))
+                                int(os.environ.get("P3D_NBLK_OBJ", 3 * n_sm))))
         g.nblk_dens = max(1, min(-(-O // 256), K_MAX_BLOCKS - g.n_macro,
                                  int(os.environ.get("P3D_NBLK_DENS", 4 * n_sm))))
         g.nblk_net = max(1, min(-(-max(arr.n_net, 1) // 256), K_MAX_BLOCKS))
