@@ -809,6 +809,11 @@ __global__ void __launch_bounds__(256) generic_net_kernel(FusedNetArgs a) {
   }
 }
 
+#ifndef P3D_GATHER_BATCH
+#define P3D_GATHER_BATCH 4
+#endif
+constexpr int kGatherBatch = P3D_GATHER_BATCH;
+
 // owner gather: per object, ordered fp64 sums over its contiguous slot records
 // (pin order within the owner, like bincount)
 __global__ void __launch_bounds__(256) fused_gather_kernel(FusedGatherArgs a) {
@@ -821,12 +826,25 @@ __global__ void __launch_bounds__(256) fused_gather_kernel(FusedGatherArgs a) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     const int b = a.obj_slot_ptr[i], e = a.obj_slot_ptr[i + 1];
     if (a.in_d) {
-      const double4* in = reinterpret_cast<const double4*>(a.in_d);
-#pragma unroll 4
-      for (int s = b; s < e; ++s) {
-        const double2* r2 = reinterpret_cast<const double2*>(in + s);
-        const double2 ra = __ldcs(r2), rb = __ldcs(r2 + 1);  // dead after this read
-        s0 += ra.x; s1 += ra.y; s2 += rb.x; s3 += rb.y;
+      // the first kGatherBatch records are loaded together (predicated, no
+      // branch between them), then summed in slot order: one memory round
+      // trip for almost every object instead of one per record
+      const double2* r2 = reinterpret_cast<const double2*>(a.in_d);
+      double2 ra[kGatherBatch], rb[kGatherBatch];
+#pragma unroll
+      for (int k = 0; k < kGatherBatch; ++k) {
+        if (b + k < e) {
+          ra[k] = __ldcs(r2 + 2 * (long long)(b + k));  // dead after this read
+          rb[k] = __ldcs(r2 + 2 * (long long)(b + k) + 1);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kGatherBatch; ++k) {
+        if (b + k < e) { s0 += ra[k].x; s1 += ra[k].y; s2 += rb[k].x; s3 += rb[k].y; }
+      }
+      for (int s = b + kGatherBatch; s < e; ++s) {
+        const double2 xa = __ldcs(r2 + 2 * (long long)s), xb = __ldcs(r2 + 2 * (long long)s + 1);
+        s0 += xa.x; s1 += xa.y; s2 += xb.x; s3 += xb.y;
       }
     } else {
 #pragma unroll 4
