@@ -223,12 +223,9 @@ __device__ __forceinline__ void scatter_terms(const Charge& q, const p3d_grid& g
   const int nxr = f.ax.i1 - f.ax.i0 + 1, nyr = f.ay.i1 - f.ay.i0 + 1, nzr = f.az.i1 - f.az.i0 + 1;
   if (nxr <= 3 && nyr <= 3 && nzr <= 2) {
     double wx[3], wy[3], wz[2];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) wx[k] = k < nxr ? overlap_len(f.ax, f.ax.i0 + k, g.wb) : 0.0;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) wy[k] = k < nyr ? overlap_len(f.ay, f.ay.i0 + k, g.hb) : 0.0;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) wz[k] = k < nzr ? overlap_len(f.az, f.az.i0 + k, g.db) : 0.0;
+    axis_weights<3>(f.ax, g.wb, wx);
+    axis_weights<3>(f.ay, g.hb, wy);
+    axis_weights<2>(f.az, g.db, wz);
 #pragma unroll
     for (int x = 0; x < 3; ++x)
 #pragma unroll

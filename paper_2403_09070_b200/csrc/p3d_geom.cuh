@@ -53,6 +53,41 @@ __device__ __forceinline__ double overlap_len(const AxisSpan& s, int i, double s
   return fmax(fmin(s.hi, (double)(i + 1) * step) - fmax(s.lo, (double)i * step), 0.0);
 }
 
+// overlap_len of the first M bins of a span at once, entries k >= nr zero.
+// The reference's min/max are kept only where they can bind: with
+// i0 = floor(lo / step) and i1 = ceil(hi / step) - 1 (rounded quotients,
+// monotone rounding) every interior boundary e_k = (i0 + k) * step satisfies
+// lo <= e_k for k >= 1 and e_k <= hi for i0 + k <= i1, so
+// max(lo, e_k) = e_k, min(hi, e_k+1) = e_k+1 and the clip at 0 is the
+// identity there: the values are identical to overlap_len's.
+#ifndef P3D_AXIS_WEIGHTS
+#define P3D_AXIS_WEIGHTS 1
+#endif
+template <int M>
+__device__ __forceinline__ void axis_weights(const AxisSpan& s, double step, double (&w)[M]) {
+  const int nr = s.i1 - s.i0 + 1;
+#if P3D_AXIS_WEIGHTS
+  const double d0 = (double)s.i0;
+  double e[M + 1];
+#pragma unroll
+  for (int k = 0; k <= M; ++k) e[k] = (d0 + (double)k) * step;  // == (double)(i0 + k) * step
+  double right_edge = e[M];
+#pragma unroll
+  for (int k = 1; k < M; ++k)
+    if (nr == k) right_edge = e[k];
+  right_edge = fmin(s.hi, right_edge);
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    const double right = (k == nr - 1) ? right_edge : e[k + 1];
+    const double v = k == 0 ? fmax(right - fmax(s.lo, e[0]), 0.0) : right - e[k];
+    w[k] = k < nr ? v : 0.0;
+  }
+#else
+#pragma unroll
+  for (int k = 0; k < M; ++k) w[k] = k < nr ? overlap_len(s, s.i0 + k, step) : 0.0;
+#endif
+}
+
 struct Footprint {
   AxisSpan ax, ay, az;
 };
@@ -176,12 +211,9 @@ __device__ __forceinline__ void gather_small(const Footprint& f, const p3d_grid&
                                              const double4* m4, double& tot, double (&a)[4]) {
   const int nxr = f.ax.i1 - f.ax.i0 + 1, nyr = f.ay.i1 - f.ay.i0 + 1, nzr = f.az.i1 - f.az.i0 + 1;
   double wx[MX], wy[MY], wz[MZ];
-#pragma unroll
-  for (int k = 0; k < MX; ++k) wx[k] = k < nxr ? overlap_len(f.ax, f.ax.i0 + k, g.wb) : 0.0;
-#pragma unroll
-  for (int k = 0; k < MY; ++k) wy[k] = k < nyr ? overlap_len(f.ay, f.ay.i0 + k, g.hb) : 0.0;
-#pragma unroll
-  for (int k = 0; k < MZ; ++k) wz[k] = k < nzr ? overlap_len(f.az, f.az.i0 + k, g.db) : 0.0;
+  axis_weights<MX>(f.ax, g.wb, wx);
+  axis_weights<MY>(f.ay, g.hb, wy);
+  axis_weights<MZ>(f.az, g.db, wz);
   const long long b0 = (long long)(f.ax.i0 * g.ny + f.ay.i0) * g.nz + f.az.i0;
 #pragma unroll
   for (int x = 0; x < MX; ++x) {
