@@ -162,6 +162,12 @@ __device__ __forceinline__ double precond_div(double lam, double q, double mdeg)
   return fmax(d, 1.0);
 }
 
+#ifndef P3D_K4_KEEP
+#define P3D_K4_KEEP 1
+#endif
+#ifndef P3D_K4_LDCS
+#define P3D_K4_LDCS 0
+#endif
 // per-launch scalars of K4 (the loop state changes only in the last block,
 // after every object has been processed)
 struct DensScal {
@@ -218,12 +224,21 @@ __device__ __forceinline__ void finish_object(const p3d_gp& gp, int i, const Cha
       acc[5] += d * d;
     }
   }
+#if P3D_K4_KEEP  // K5 reads these right after: keep them in L2
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    st_keep(gp.prev_wl + (long long)k * O + i, wl[k]);
+    st_keep(gp.prev_dens + (long long)k * O + i, dg[k]);
+  }
+  st_keep(gp.prev_q + i, qq);
+#else
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     gp.prev_wl[(long long)k * O + i] = wl[k];
     gp.prev_dens[(long long)k * O + i] = dg[k];
   }
   gp.prev_q[i] = qq;
+#endif
 }
 
 // the caller-side loads of finish_object's inputs
@@ -235,8 +250,14 @@ __device__ __forceinline__ void load_object_inputs(const p3d_gp& gp, int i, cons
   if (i < I) {
 #pragma unroll
     {
+#if P3D_K4_LDCS  // read once: evict first
+      const double2* g2 = reinterpret_cast<const double2*>(gp.inst_g) + 2 * (long long)i;
+      const double2 ga = __ldcs(g2), gb = __ldcs(g2 + 1);
+      wl4[0] = ga.x; wl4[1] = ga.y; wl4[2] = gb.x; wl4[3] = gb.y;
+#else
       const double4 g = reinterpret_cast<const double4*>(gp.inst_g)[i];
       wl4[0] = g.x; wl4[1] = g.y; wl4[2] = g.z; wl4[3] = g.w;
+#endif
     }
   }
   pq = mdeg = 0.0;
