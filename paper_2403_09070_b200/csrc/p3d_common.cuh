@@ -200,9 +200,17 @@ __device__ __forceinline__ double block_max_partials(const volatile double* p, i
 // ---------------------------------------------------------------------------
 // numpy-faithful small math (compiled with -fmad=false where used)
 // ---------------------------------------------------------------------------
+// max / min of two doubles as one compare and a select (fmax / fmin spend ~7
+// SASS instructions on NaN handling).  Identical to fmax / fmin whenever
+// neither argument is NaN; every caller passes finite coordinates / spans
+// (or +-inf sentinels).
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
+
 __device__ __forceinline__ double clipd(double v, double lo, double hi) {
-  // np.clip(v, lo, hi) == minimum(maximum(v, lo), hi)
-  return fmin(fmax(v, lo), hi);
+  // np.clip(v, lo, hi) == minimum(maximum(v, lo), hi) for lo <= hi (every
+  // caller); a NaN v stays NaN as in numpy
+  return v < lo ? lo : (v > hi ? hi : v);
 }
 
 }  // namespace p3d

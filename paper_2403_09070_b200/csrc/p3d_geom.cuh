@@ -75,11 +75,11 @@ __device__ __forceinline__ void axis_weights(const AxisSpan& s, double step, dou
 #pragma unroll
   for (int k = 1; k < M; ++k)
     if (nr == k) right_edge = e[k];
-  right_edge = fmin(s.hi, right_edge);
+  right_edge = dmin(s.hi, right_edge);
 #pragma unroll
   for (int k = 0; k < M; ++k) {
     const double right = (k == nr - 1) ? right_edge : e[k + 1];
-    const double v = k == 0 ? fmax(right - fmax(s.lo, e[0]), 0.0) : right - e[k];
+    const double v = k == 0 ? dmax(right - dmax(s.lo, e[0]), 0.0) : right - e[k];
     w[k] = k < nr ? v : 0.0;
   }
 #else

@@ -46,16 +46,16 @@ __device__ __forceinline__ double flip_delta(const Side& same, const Side& other
                                              double full, double cur) {
   double sp = 0.0;
   if (same.cnt > 1) sp = ((c == same.hi1) ? same.hi2 : same.hi1) - ((c == same.lo1) ? same.lo2 : same.lo1);
-  const double op = fmax(other.hi1, c) - fmin(other.lo1, c);
-  return fmax(full, sp + op) - cur;
+  const double op = dmax(other.hi1, c) - dmin(other.lo1, c);
+  return dmax(full, sp + op) - cur;
 }
 
 struct Box2 {  // one axis, die 0 (bottom) and die 1 (top)
   Side b, t;
   __device__ __forceinline__ void init() { b.init(); t.init(); }
   __device__ __forceinline__ void add(double c, int d) { if (d) t.add(c); else b.add(c); }
-  __device__ __forceinline__ double fmx() const { return fmax(b.hi1, t.hi1); }
-  __device__ __forceinline__ double fmn() const { return fmin(b.lo1, t.lo1); }
+  __device__ __forceinline__ double fmx() const { return dmax(b.hi1, t.hi1); }
+  __device__ __forceinline__ double fmn() const { return dmin(b.lo1, t.lo1); }
   __device__ __forceinline__ double full() const { return (b.cnt + t.cnt) > 0 ? fmx() - fmn() : 0.0; }
   // wirelength.py:227-248 with the pin's own segment / the other segment picked by selects
   __device__ __forceinline__ double flip(double c, int d, double full_, double cur) const {
@@ -64,8 +64,8 @@ struct Box2 {  // one axis, die 0 (bottom) and die 1 (top)
     const double slo1 = d ? t.lo1 : b.lo1, slo2 = d ? t.lo2 : b.lo2;
     const double ohi1 = d ? b.hi1 : t.hi1, olo1 = d ? b.lo1 : t.lo1;
     const double sp = scnt > 1 ? ((c == shi1) ? shi2 : shi1) - ((c == slo1) ? slo2 : slo1) : 0.0;
-    const double op = fmax(ohi1, c) - fmin(olo1, c);
-    return fmax(full_, sp + op) - cur;
+    const double op = dmax(ohi1, c) - dmin(olo1, c);
+    return dmax(full_, sp + op) - cur;
   }
 };
 
@@ -253,12 +253,12 @@ __device__ __noinline__ double forced_ext(const FusedNetArgs& a, int base, int d
     load_pin(a, base + k * stride, x, y, z, t);
     const double c = axis == 0 ? x : y;
     if (a.pin_inst[base + k * stride] == w) t = forced;
-    fhi = fmax(fhi, c);
-    flo = fmin(flo, c);
-    if (t) { nt++; thi = fmax(thi, c); tlo = fmin(tlo, c); } else { nb++; bhi = fmax(bhi, c); blo = fmin(blo, c); }
+    fhi = dmax(fhi, c);
+    flo = dmin(flo, c);
+    if (t) { nt++; thi = dmax(thi, c); tlo = dmin(tlo, c); } else { nb++; bhi = dmax(bhi, c); blo = dmin(blo, c); }
   }
   const double full = deg > 0 ? fhi - flo : 0.0;
-  return fmax(full, (nt ? thi - tlo : 0.0) + (nb ? bhi - blo : 0.0));
+  return dmax(full, (nt ? thi - tlo : 0.0) + (nb ? bhi - blo : 0.0));
 }
 
 // one output record per pin, written at its owner-sorted slot (the owner
@@ -345,12 +345,12 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
     load_pin(a, base + k * stride, x, y, z, tp);
     bx.add(x, tp);
     by.add(y, tp);
-    zhi = fmax(zhi, z);
-    zlo = fmin(zlo, z);
+    zhi = dmax(zhi, z);
+    zlo = dmin(zlo, z);
   }
   const double fx = bx.full(), fy = by.full();
-  const double ex = fmax(fx, bx.t.span() + bx.b.span());
-  const double ey = fmax(fy, by.t.span() + by.b.span());
+  const double ex = dmax(fx, bx.t.span() + bx.b.span());
+  const double ey = dmax(fy, by.t.span() + by.b.span());
   const bool sx = (bx.t.span() + bx.b.span()) > fx;
   const bool sy = (by.t.span() + by.b.span()) > fy;
   acc[3] += ex;
@@ -452,7 +452,7 @@ __device__ __forceinline__ void staged_axis(double (&c)[kMaxStagedDeg][32], Warp
   for (int k = 0; k < (D ? D : kMaxStagedDeg); ++k)
     if (k < DD) bx.add(c[k][lane], (topm >> k) & 1);
   const double full = bx.full(), part = bx.t.span() + bx.b.span();
-  const double ex = fmax(full, part);
+  const double ex = dmax(full, part);
   const bool split = part > full;  // ties resolve to the full box (wirelength.py:186)
   exact = ex;
   crossing = bx.b.cnt > 0 && bx.t.cnt > 0;
@@ -526,8 +526,8 @@ __device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk,
     sm.px[k][lane] = p.x + (double)(tp ? off[k].x : off[k].z);
     sm.py[k][lane] = p.y + (double)(tp ? off[k].y : off[k].w);
     sm.pz[k][lane] = p.z;
-    zhi = fmax(zhi, p.z);
-    zlo = fmin(zlo, p.z);
+    zhi = dmax(zhi, p.z);
+    zlo = dmin(zlo, p.z);
   }
   return true;
 }
@@ -600,7 +600,7 @@ __device__ __forceinline__ void triple_axis(const double (&v)[3], typename WaSel
                                             double& val, double (&g)[3]) {
   using W = typename WaSel<F32>::W;
   using R = typename WaSel<F32>::R;
-  const double hi = fmax(fmax(v[0], v[1]), v[2]), lo = fmin(fmin(v[0], v[1]), v[2]);
+  const double hi = dmax(dmax(v[0], v[1]), v[2]), lo = dmin(dmin(v[0], v[1]), v[2]);
   R ep[3], em[3];
   W w;
   w.init();
@@ -648,8 +648,8 @@ __device__ __forceinline__ void triple_task(const FusedNetArgs& a, const int4 tk
   acc[0] += vx;
   acc[1] += vy;
   acc[2] += vz;
-  acc[3] += fmax(fmax(x[0], x[1]), x[2]) - fmin(fmin(x[0], x[1]), x[2]);  // never split: full
-  acc[4] += fmax(fmax(y[0], y[1]), y[2]) - fmin(fmin(y[0], y[1]), y[2]);
+  acc[3] += dmax(dmax(x[0], x[1]), x[2]) - dmin(dmin(x[0], x[1]), x[2]);  // never split: full
+  acc[4] += dmax(dmax(y[0], y[1]), y[2]) - dmin(dmin(y[0], y[1]), y[2]);
   const int ntop = tp[0] + tp[1] + tp[2];
   acc[5] += (ntop > 0 && ntop < 3) ? 1.0 : 0.0;
 #pragma unroll
@@ -668,7 +668,7 @@ __device__ __forceinline__ void pair_axis(double v0, double v1, typename WaSel<F
                                           double& val, double& g0, double& g1) {
   using W = typename WaSel<F32>::W;
   using R = typename WaSel<F32>::R;
-  const double hi = fmax(v0, v1), lo = fmin(v0, v1);
+  const double hi = dmax(v0, v1), lo = dmin(v0, v1);
   R e, one_p, one_m;
   W::term(lo, hi, lo, ig, e, one_m);  // e = exp((lo - hi)/g); one_m = exp(0)
   one_p = one_m;
@@ -709,8 +709,8 @@ __device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, 
   acc[0] += vx;
   acc[1] += vy;
   acc[2] += vz;
-  acc[3] += fmax(x0, x1) - fmin(x0, x1);
-  acc[4] += fmax(y0, y1) - fmin(y0, y1);
+  acc[3] += dmax(x0, x1) - dmin(x0, x1);
+  acc[4] += dmax(y0, y1) - dmin(y0, y1);
   acc[5] += (t0p != t1p) ? 1.0 : 0.0;
   if (F32) {
     a.out_f[s0] = make_float4((float)gx0, (float)gy0, (float)gz0, 0.f);
