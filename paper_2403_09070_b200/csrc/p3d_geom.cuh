@@ -50,7 +50,7 @@ __device__ __forceinline__ AxisSpan axis_span(double c, double size, double exte
 
 // density.py:172-173
 __device__ __forceinline__ double overlap_len(const AxisSpan& s, int i, double step) {
-  return fmax(fmin(s.hi, (double)(i + 1) * step) - fmax(s.lo, (double)i * step), 0.0);
+  return dmax(dmin(s.hi, (double)(i + 1) * step) - dmax(s.lo, (double)i * step), 0.0);
 }
 
 // overlap_len of the first M bins of a span at once, entries k >= nr zero.
@@ -245,7 +245,7 @@ __device__ __forceinline__ void gather_object(const Charge& q, const p3d_grid& g
     gather_small<3, 3, 2>(f, g, m4, tot, a);
   else
     gather_generic(f, g, m4, tot, a);
-  tot = fmax(tot, 1e-300);
+  tot = dmax(tot, 1e-300);
   mean[0] = a[0] / tot;
   mean[1] = a[1] / tot;
   mean[2] = a[2] / tot;

@@ -63,8 +63,8 @@ __device__ __forceinline__ CloudGP cloud_of(const p3d_gp& gp, const double* pos)
 __device__ __forceinline__ double clamp_span(double v, double size, double extent) {
   const double lo = size / 2;
   const double hi = extent - size / 2;
-  if (lo <= hi) return clipd(v, fmin(lo, hi), fmax(lo, hi));
-  return fmin(lo, hi) + fabs(hi - lo) / 2;
+  if (lo <= hi) return clipd(v, lo, hi);
+  return dmin(lo, hi) + fabs(hi - lo) / 2;
 }
 
 // Gp3dProblem.project for one object (gp.py:280-294)
@@ -159,7 +159,7 @@ __global__ void pos4_kernel(int I, int O, const double* v, double* pos4) {
 __device__ __forceinline__ double precond_div(double lam, double q, double mdeg) {
   double d = lam * q;  // gp.py:142-147 operation order
   d = d + mdeg;
-  return fmax(d, 1.0);
+  return dmax(d, 1.0);
 }
 
 #ifndef P3D_K4_KEEP
