@@ -100,26 +100,49 @@ __device__ const double kExp2Tab[64] = {
 #ifndef P3D_EXP_POLY
 #define P3D_EXP_POLY 1
 #endif
+#ifndef P3D_EXP_CONST
+#define P3D_EXP_CONST 1
+#endif
 #if P3D_EXP_POLY
 // Table-free variant: n = rint(x / ln 2), Cody-Waite r (|r| <= ln2/2), degree-13
 // Taylor polynomial by Horner (<= 1.2 ulp over [-708, 0]); no memory access.
+// The coefficients live in constant memory so every DFMA takes its constant
+// as a c[][] operand: as immediates the compiler rematerialised each fp64
+// constant with two UMOVs per use (9% of K1's instructions).
+__constant__ double kExpPoly[17] = {
+    1.4426950408889634074,     // 1 / ln 2
+    0.693147180369123816490,   // ln 2 (high part)
+    1.9082149292705877e-10,    // ln 2 (low part)
+    1.6059043836821613e-10,    // 1/13!
+    2.08767569878680989792e-09,  // 1/12!
+    2.50521083854417187751e-08,  // 1/11!
+    2.75573192239858906526e-07,  // 1/10!
+    2.75573192239858906526e-06,  // 1/9!
+    2.48015873015873015873e-05,  // 1/8!
+    1.98412698412698412698e-04,  // 1/7!
+    1.38888888888888888889e-03,  // 1/6!
+    8.33333333333333333333e-03,  // 1/5!
+    4.16666666666666666667e-02,  // 1/4!
+    1.66666666666666666667e-01,  // 1/3!
+    0.5, 1.0, 1.0};
 __device__ __forceinline__ double exp_neg(double x) {
-  const double n = rint(x * 1.4426950408889634074);
-  const double r = fma(-n, 1.9082149292705877e-10, fma(-n, 0.693147180369123816490, x));
-  double p = 1.6059043836821613e-10;                 // 1/13!
-  p = fma(p, r, 2.08767569878680989792e-09);         // 1/12!
-  p = fma(p, r, 2.50521083854417187751e-08);         // 1/11!
-  p = fma(p, r, 2.75573192239858906526e-07);         // 1/10!
-  p = fma(p, r, 2.75573192239858906526e-06);         // 1/9!
-  p = fma(p, r, 2.48015873015873015873e-05);         // 1/8!
-  p = fma(p, r, 1.98412698412698412698e-04);         // 1/7!
-  p = fma(p, r, 1.38888888888888888889e-03);         // 1/6!
-  p = fma(p, r, 8.33333333333333333333e-03);         // 1/5!
-  p = fma(p, r, 4.16666666666666666667e-02);         // 1/4!
-  p = fma(p, r, 1.66666666666666666667e-01);         // 1/3!
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+#if P3D_EXP_CONST
+  const double* c = kExpPoly;
+#else
+  constexpr double c[17] = {1.4426950408889634074, 0.693147180369123816490,
+                            1.9082149292705877e-10, 1.6059043836821613e-10,
+                            2.08767569878680989792e-09, 2.50521083854417187751e-08,
+                            2.75573192239858906526e-07, 2.75573192239858906526e-06,
+                            2.48015873015873015873e-05, 1.98412698412698412698e-04,
+                            1.38888888888888888889e-03, 8.33333333333333333333e-03,
+                            4.16666666666666666667e-02, 1.66666666666666666667e-01,
+                            0.5, 1.0, 1.0};
+#endif
+  const double n = rint(x * c[0]);
+  const double r = fma(-n, c[2], fma(-n, c[1], x));
+  double p = c[3];
+#pragma unroll
+  for (int k = 4; k < 17; ++k) p = fma(p, r, c[k]);
   const double sc = __longlong_as_double((long long)((int)n + 1023) << 52);
   return x < -708.0 ? 0.0 : p * sc;
 }
