@@ -24,6 +24,10 @@ namespace p3d {
 
 namespace {
 
+#ifndef P3D_BOX_SELECT
+#define P3D_BOX_SELECT 1
+#endif
+
 struct Side {  // extrema of one (net, die) segment on one axis (float64, exact)
   int cnt;
   double hi1, hi2, lo1, lo2;
@@ -35,8 +39,21 @@ struct Side {  // extrema of one (net, die) segment on one axis (float64, exact)
   // top-2 with multiplicity (NetBoxes order statistics, wirelength.py:113-131)
   __device__ __forceinline__ void add(double c) {
     cnt += 1;
-    if (c > hi1) { hi2 = hi1; hi1 = c; } else if (c > hi2) { hi2 = c; }
-    if (c < lo1) { lo2 = lo1; lo1 = c; } else if (c < lo2) { lo2 = c; }
+    push(c, c);
+  }
+  // the same update without branches: hi2' = max(hi2, min(hi1, h)) and
+  // hi1' = max(hi1, h) pick exactly the values of the if/else chain; h = -inf
+  // (l = +inf) leaves the side unchanged
+  __device__ __forceinline__ void push(double h, double l) {
+#if P3D_BOX_SELECT
+    hi2 = dmax(hi2, dmin(hi1, h));
+    hi1 = dmax(hi1, h);
+    lo2 = dmin(lo2, dmax(lo1, l));
+    lo1 = dmin(lo1, l);
+#else
+    if (h > hi1) { hi2 = hi1; hi1 = h; } else if (h > hi2) { hi2 = h; }
+    if (l < lo1) { lo2 = lo1; lo1 = l; } else if (l < lo2) { lo2 = l; }
+#endif
   }
   __device__ __forceinline__ double span() const { return cnt > 0 ? hi1 - lo1 : 0.0; }
 };
@@ -53,7 +70,16 @@ __device__ __forceinline__ double flip_delta(const Side& same, const Side& other
 struct Box2 {  // one axis, die 0 (bottom) and die 1 (top)
   Side b, t;
   __device__ __forceinline__ void init() { b.init(); t.init(); }
-  __device__ __forceinline__ void add(double c, int d) { if (d) t.add(c); else b.add(c); }
+  __device__ __forceinline__ void add(double c, int d) {
+#if P3D_BOX_SELECT
+    t.push(d ? c : -P3D_INF, d ? c : P3D_INF);
+    b.push(d ? -P3D_INF : c, d ? P3D_INF : c);
+    t.cnt += d;
+    b.cnt += 1 - d;
+#else
+    if (d) t.add(c); else b.add(c);
+#endif
+  }
   __device__ __forceinline__ double fmx() const { return dmax(b.hi1, t.hi1); }
   __device__ __forceinline__ double fmn() const { return dmin(b.lo1, t.lo1); }
   __device__ __forceinline__ double full() const { return (b.cnt + t.cnt) > 0 ? fmx() - fmn() : 0.0; }
