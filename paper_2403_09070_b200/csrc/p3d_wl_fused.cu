@@ -465,7 +465,7 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
 #define P3D_K1_RTD 0
 #endif
 #ifndef P3D_K1_MINB
-#define P3D_K1_MINB 5
+#define P3D_K1_MINB 4
 #endif
 
 constexpr int kMaxStagedDeg = 6;
