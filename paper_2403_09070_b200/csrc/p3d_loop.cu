@@ -409,12 +409,12 @@ __global__ void __launch_bounds__(256, P3D_K4_MINB) dens_kernel(p3d_gp gp) {
     const int b = blockIdx.x - nm, nb = gridDim.x - nm, n_own = own_count(gp);
     for (int k = b * blockDim.x + threadIdx.x; k < n_own; k += nb * blockDim.x) {
       const int i = own_obj(gp, k);
+      const Charge q = cl.get(i);  // reads the macro flag too: one round trip
       if (cl.is_macro(i)) continue;
       double wl4[4], pw[3], pd[3], pq, mdeg;
 #if P3D_K4_PREFETCH
       load_object_inputs(gp, i, sc, wl4, pw, pd, pq, mdeg);
 #endif
-      const Charge q = cl.get(i);
       double mean[4];
       gather_object(q, gp.grid, gp.maps, mean);
 #if !P3D_K4_PREFETCH
