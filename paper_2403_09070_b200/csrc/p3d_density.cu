@@ -119,11 +119,11 @@ __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_gri
     const int b = blockIdx.x - n_macro, nb = gridDim.x - n_macro;
     for (int k = b * blockDim.x + threadIdx.x; k < n; k += nb * blockDim.x) {
       const int i = k < ts.ni ? ts.i0 + k : ts.f0 + (k - ts.ni);  // this rank's objects
+      const Charge q = cl.get(i);  // reads the macro flag too: one round trip
       if (cl.is_macro(i)) {
         ts.tile_of[k] = -1;
         continue;
       }
-      const Charge q = cl.get(i);
       int tx = (int)floor(q.x / tw), ty = (int)floor(q.y / th);
       tx = tx < 0 ? 0 : (tx >= ts.tiles_x ? ts.tiles_x - 1 : tx);
       ty = ty < 0 ? 0 : (ty >= ts.tiles_y ? ts.tiles_y - 1 : ty);
