@@ -451,14 +451,18 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
       }
   }
   if (!a.maps) return;
-  // A = X (w_j/nx)(w_k/ny)(w_l/nz) / lambda  (DC mode: 0)
+  // A = X (w_j/nx)(w_k/ny)(w_l/nz) / lambda  (DC mode: 0).  nx and ny are
+  // powers of two here, so w/nx == w * (1/nx) exactly; the two w_l/nz values
+  // are hoisted (same divisions)
+  const double inx = 1.0 / a.nx, iny = 1.0 / a.ny;
+  const double wz0 = 1.0 / a.nz, wz1 = 2.0 / a.nz;
   for (int t = threadIdx.x; t < CB * nx; t += blockDim.x) {
     const int c = t >> LX, j = t & (nx - 1);
     const int col = c0 + c, ky = col / a.nz, kz = col - ky * a.nz;
     const double ox = om[j], oy = a.omy[ky], oz = a.omz[kz];
     const double lam = ox * ox + oy * oy + oz * oz;
     const double inv = lam > 0.0 ? 1.0 / lam : 0.0;
-    const double sc = (j ? 2.0 : 1.0) / a.nx * ((ky ? 2.0 : 1.0) / a.ny) * ((kz ? 2.0 : 1.0) / a.nz) * inv;
+    const double sc = (j ? 2.0 : 1.0) * inx * ((ky ? 2.0 : 1.0) * iny) * (kz ? wz1 : wz0) * inv;
     Xs[t] *= sc * a.in_scale;
   }
   __syncthreads();

@@ -1,7 +1,2 @@
-python -c 'import __graft_entry__ as g; g.build(); g.smoke()' 2>&1 | tail -2
-timeout 1200 python -m pytest tests -q -m gpu -x > gpurun_out/tests_f3.log 2>&1; tail -2 gpurun_out/tests_f3.log
-timeout 600 python bench.py --steps 30 --warmup 5 --cpu-seconds 20 > gpurun_out/bench_f3.log 2>&1; echo bench $?; tail -1 gpurun_out/bench_f3.log
-timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_f3_ref.log 2>&1; echo ref $?
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_f3.csv python bench.py --steps 30 --warmup 5 --no-cpu-baseline > /dev/null 2>&1; echo ncu_l $?
-bash tools/gpu_ncu.sh f3 "advance|dens_kernel|fused|scatter|spec_|tile_|gmax0" 11 60
-for c in 1 2 4; do timeout 600 python bench.py --config $c --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/bench_f3_c$c.log 2>&1; echo cfg$c $?; done
+P3D_LIB_VARIANT=k4m3 bash tools/gpu_env_ab.sh k4m3b P3D_NBLK_DENS=444
+bash tools/gpu_env_ab.sh gth P3D_NBLK_GATHER=1184 P3D_NBLK_GATHER=592
