@@ -1,2 +1,3 @@
-P3D_LIB_VARIANT=k4m3 bash tools/gpu_env_ab.sh k4m3b P3D_NBLK_DENS=444
-bash tools/gpu_env_ab.sh gth P3D_NBLK_GATHER=1184 P3D_NBLK_GATHER=592
+timeout 600 python bench.py --mode batch --batch 4 --config 2 --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/bench_b4.log 2>&1; echo b4 $?; tail -1 gpurun_out/bench_b4.log | cut -c1-300
+timeout 600 python bench.py --precision fp32 --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/bench_fp32.log 2>&1; echo fp32 $?; tail -1 gpurun_out/bench_fp32.log | cut -c1-300
+timeout 600 python bench.py --mode sharded --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_sh1.log 2>&1; echo sh1 $?; tail -1 gpurun_out/bench_sh1.log | cut -c1-300
