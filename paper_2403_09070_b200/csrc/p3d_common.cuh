@@ -207,6 +207,24 @@ __device__ __forceinline__ double block_max_partials(const volatile double* p, i
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 __device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
 
+// x / b from y = 1/b (one IEEE division shared by several quotients with the
+// same divisor): q = x y, then one exact FMA residual correction.  With
+// y = RN(1/b) this is Markstein's correctly rounded quotient, i.e. the same
+// value as the IEEE division, for results in the normal range (every caller:
+// preconditioner divisors >= 1, overlap volumes >= 1e-300 with numerators
+// bounded by them); -DP3D_SHARED_RCP=0 restores plain divisions.
+#ifndef P3D_SHARED_RCP
+#define P3D_SHARED_RCP 1
+#endif
+__device__ __forceinline__ double div_rcp(double x, double b, double y) {
+#if P3D_SHARED_RCP
+  const double q = x * y;
+  return fma(fma(-q, b, x), y, q);
+#else
+  return x / b;
+#endif
+}
+
 __device__ __forceinline__ double clipd(double v, double lo, double hi) {
   // np.clip(v, lo, hi) == minimum(maximum(v, lo), hi) for lo <= hi (every
   // caller); a NaN v stays NaN as in numpy

@@ -246,10 +246,11 @@ __device__ __forceinline__ void gather_object(const Charge& q, const p3d_grid& g
   else
     gather_generic(f, g, m4, tot, a);
   tot = dmax(tot, 1e-300);
-  mean[0] = a[0] / tot;
-  mean[1] = a[1] / tot;
-  mean[2] = a[2] / tot;
-  mean[3] = a[3] / tot;
+  const double ytot = 1.0 / tot;
+  mean[0] = div_rcp(a[0], tot, ytot);
+  mean[1] = div_rcp(a[1], tot, ytot);
+  mean[2] = div_rcp(a[2], tot, ytot);
+  mean[3] = div_rcp(a[3], tot, ytot);
 }
 
 // block-cooperative macro means: sum m*vol over the footprint / unclipped

@@ -216,10 +216,11 @@ __device__ __forceinline__ void finish_object(const p3d_gp& gp, int i, const Cha
   if (sc.bb) {
     const double div = precond_div(lam, qq, mdeg);
     const double divp = precond_div(lam, pq, mdeg);
+    const double ydiv = 1.0 / div, ydivp = 1.0 / divp;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const double pre = (wl[k] + lam * dg[k]) / div;
-      const double pp = (pw[k] + lam * pd[k]) / divp;
+      const double pre = div_rcp(wl[k] + lam * dg[k], div, ydiv);
+      const double pp = div_rcp(pw[k] + lam * pd[k], divp, ydivp);
       const double d = pre - pp;
       acc[5] += d * d;
     }
@@ -553,8 +554,9 @@ __global__ void __launch_bounds__(256, P3D_K5_MINB) advance_kernel(p3d_gp gp) {
     // the step's gradient, re-derived from the stored raw gradients (gp.py:424-426)
     const double div = precond_div(lam, pq, mdeg);
     double un[3], vn[3];
+    const double ydiv = 1.0 / div;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) un[c] = v[c] - step * ((pw[c] + lam * pd[c]) / div);
+    for (int c = 0; c < 3; ++c) un[c] = v[c] - step * div_rcp(pw[c] + lam * pd[c], div, ydiv);
     project_loaded(gp, inst, mac, s0, s1, s2, s3, fz, un[0], un[1], un[2]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) vn[c] = un[c] + mom * (un[c] - u[c]);
