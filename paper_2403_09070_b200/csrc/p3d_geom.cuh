@@ -33,13 +33,15 @@ struct AxisSpan {
 };
 
 // density.py:155-169: clipped extent and inclusive bin range on one axis
+// (ystep = 1 / step: both quotients from one reciprocal, same values as lo /
+// step and hi / step, see div_rcp)
 __device__ __forceinline__ AxisSpan axis_span(double c, double size, double extent, double step,
-                                              int n) {
+                                              double ystep, int n) {
   AxisSpan s;
   s.lo = clipd(c - size / 2, 0.0, extent);
   s.hi = clipd(c + size / 2, 0.0, extent);
-  long long a = (long long)floor(s.lo / step);
-  long long b = (long long)ceil(s.hi / step) - 1;
+  long long a = (long long)floor(div_rcp(s.lo, step, ystep));
+  long long b = (long long)ceil(div_rcp(s.hi, step, ystep)) - 1;
   a = a < 0 ? 0 : (a > n - 1 ? n - 1 : a);
   b = b < 0 ? 0 : (b > n - 1 ? n - 1 : b);
   if (b < a) b = a;
@@ -94,9 +96,9 @@ struct Footprint {
 
 __device__ __forceinline__ Footprint footprint(const Charge& c, const p3d_grid& g) {
   Footprint f;
-  f.ax = axis_span(c.x, c.w, g.dx, g.wb, g.nx);
-  f.ay = axis_span(c.y, c.h, g.dy, g.hb, g.ny);
-  f.az = axis_span(c.z, c.dep, g.dz, g.db, g.nz);
+  f.ax = axis_span(c.x, c.w, g.dx, g.wb, 1.0 / g.wb, g.nx);
+  f.ay = axis_span(c.y, c.h, g.dy, g.hb, 1.0 / g.hb, g.ny);
+  f.az = axis_span(c.z, c.dep, g.dz, g.db, 1.0 / g.db, g.nz);
   return f;
 }
 
