@@ -115,16 +115,20 @@ __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_gri
   } else {
     for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x) sh_hist[t] = 0;
     __syncthreads();
-    const double tw = g.wb * kTile, th = g.hb * kTile;
+    // the tile of an object's centre only groups the records (any assignment
+    // is exact: a footprint outside its CTA's window goes to global atomics),
+    // so the centre is scaled by reciprocals, and only x, y and the macro
+    // flag are read
+    const double rtw = 1.0 / (g.wb * kTile), rth = 1.0 / (g.hb * kTile);
     const int b = blockIdx.x - n_macro, nb = gridDim.x - n_macro;
     for (int k = b * blockDim.x + threadIdx.x; k < n; k += nb * blockDim.x) {
       const int i = k < ts.ni ? ts.i0 + k : ts.f0 + (k - ts.ni);  // this rank's objects
-      const Charge q = cl.get(i);  // reads the macro flag too: one round trip
+      const double cx = cl.cx(i), cy = cl.cy(i);
       if (cl.is_macro(i)) {
         ts.tile_of[k] = -1;
         continue;
       }
-      int tx = (int)floor(q.x / tw), ty = (int)floor(q.y / th);
+      int tx = (int)floor(cx * rtw), ty = (int)floor(cy * rth);
       tx = tx < 0 ? 0 : (tx >= ts.tiles_x ? ts.tiles_x - 1 : tx);
       ty = ty < 0 ? 0 : (ty >= ts.tiles_y ? ts.tiles_y - 1 : ty);
       const int t = tx * ts.tiles_y + ty;

@@ -108,6 +108,8 @@ __device__ __forceinline__ Footprint footprint(const Charge& c, const p3d_grid& 
 struct CloudArrays {  // explicit ChargeCloud (per-op API)
   p3d_cloud c;
   __device__ __forceinline__ bool is_macro(int i) const { return c.is_macro && c.is_macro[i]; }
+  __device__ __forceinline__ double cx(int i) const { return c.x[i]; }
+  __device__ __forceinline__ double cy(int i) const { return c.y[i]; }
   __device__ __forceinline__ Charge get(int i) const {
     Charge q;
     q.x = c.x[i]; q.y = c.y[i]; q.z = c.z[i];
@@ -123,6 +125,8 @@ struct CloudGP {  // Gp3dProblem.cloud(pos) computed on the fly (gp.py:267-278)
   const uint8_t* macro;
   double dz, target_density;
   __device__ __forceinline__ bool is_macro(int i) const { return i < n_inst && macro[i]; }
+  __device__ __forceinline__ double cx(int i) const { return pos[i]; }
+  __device__ __forceinline__ double cy(int i) const { return pos[n_obj + i]; }
   __device__ __forceinline__ Charge get(int i) const {
     Charge q;
     q.x = pos[i];
