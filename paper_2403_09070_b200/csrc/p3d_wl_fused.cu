@@ -210,6 +210,11 @@ struct Wa64 {
     ep = exp_neg((v - hi) * ig);
     em = exp_neg((lo - v) * ig);
   }
+  // the ep of the lower of two pins, (lo - hi)/g (the other exponentials of a
+  // 2-pin segment are exp(0) = 1 exactly, as term() would return them)
+  __device__ static __forceinline__ double gap(double hi, double lo, double ig) {
+    return exp_neg((lo - hi) * ig);
+  }
   __device__ __forceinline__ void acc(double v, double, double, double ep, double em, double on) {
     s1p = fma(on, ep, s1p);
     sxp = fma(on, v * ep, sxp);
@@ -239,6 +244,9 @@ struct Wa32 {
                                               float& em) {
     ep = __expf((float)(v - hi) * ig);
     em = __expf(-(float)(v - lo) * ig);
+  }
+  __device__ static __forceinline__ float gap(double hi, double lo, float ig) {
+    return __expf((float)(lo - hi) * ig);
   }
   __device__ __forceinline__ void acc(double v, double hi, double lo, float ep, float em, float on) {
     const float dp = (float)(v - hi), dm = (float)(v - lo);
@@ -718,9 +726,7 @@ __device__ __forceinline__ void pair_axis(double v0, double v1, typename WaSel<F
   using W = typename WaSel<F32>::W;
   using R = typename WaSel<F32>::R;
   const double hi = dmax(v0, v1), lo = dmin(v0, v1);
-  R e, one_p, one_m;
-  W::term(lo, hi, lo, ig, e, one_m);  // e = exp((lo - hi)/g); one_m = exp(0)
-  one_p = one_m;
+  const R e = W::gap(hi, lo, ig), one_p = (R)1, one_m = (R)1;  // exp((lo - hi)/g), exp(0)
   const bool first_hi = v0 >= v1;
   const R e0p = first_hi ? one_p : e, e1p = first_hi ? e : one_p;
   const R e0m = first_hi ? e : one_m, e1m = first_hi ? one_m : e;
