@@ -228,6 +228,9 @@ def roofline_of(design, n_fill, grid, stage_ms, config, shards=1):
     dom = max(fam_ms, key=fam_ms.get)
     peak, peak_kind = load_peaks()
     achieved = q[dom] / (fam_ms[dom] / 1000.0) / 1e9
+    names = ("K1_net", "K1b_gather", "K2_scatter", "K3_spectral", "K4_dens", "K5a_step0",
+             "K5b_advance")
+    stages_us = {n: round(float(v) * 1000.0, 1) for n, v in zip(names, stage_ms)}
     per_family = {k: {"ms": round(float(v), 4), "alg_MB": round(q[k] / 1e6, 2),
                       "GBs": round(q[k] / (v / 1000.0) / 1e9, 1) if v > 0 else None}
                   for k, v in fam_ms.items()}
@@ -241,7 +244,8 @@ def roofline_of(design, n_fill, grid, stage_ms, config, shards=1):
         pass
     return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-            "per_family": per_family}
+            "per_family": per_family,
+            "stages_us": stages_us}
 
 
 def run_batch(args, rank, world, local):

@@ -17,6 +17,8 @@
 //     float64 with numpy's operation order (default) or, opt-in, float32 on
 //     anchor-relative differences (SURVEY App. B plan).
 // Nets with degree outside [2, kMaxStagedDeg] take a per-thread generic path.
+#include <algorithm>
+
 #include "p3d_common.cuh"
 #include "p3d_internal.cuh"
 
@@ -928,6 +930,68 @@ __global__ void __launch_bounds__(256) fused_gather_kernel(FusedGatherArgs a) {
   }
 }
 
+// Warp-cooperative variant (fp64 records): a warp owns 32 consecutive
+// objects, whose records are one contiguous slot range; the warp copies the
+// range into shared memory with coalesced 16-byte loads (all in flight
+// together), then each lane sums its own object's records in slot order —
+// the same order, hence the same values, as the thread-per-object kernel.
+constexpr int kGatherWarps = 8;
+constexpr int kGatherStage = 128;  // records staged per warp and chunk (4 KB)
+__global__ void __launch_bounds__(32 * kGatherWarps) gather_warp_kernel(FusedGatherArgs a) {
+  pdl_wait();
+  if (a.halt && *a.halt) return;
+  __shared__ double2 stage[kGatherWarps][2 * kGatherStage];
+  __shared__ double red[32 * 3];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const double2* in2 = reinterpret_cast<const double2*>(a.in_d);
+  double2* st = stage[wib];
+  double acc[3] = {0, 0, 0};
+  const int wstride = gridDim.x * kGatherWarps * 32;
+  for (int o0 = (blockIdx.x * kGatherWarps + wib) * 32; o0 < a.n_obj; o0 += wstride) {
+    const int i = o0 + lane;
+    const int last = min(a.n_obj, o0 + 32) - 1;
+    const int b = i <= last ? a.obj_slot_ptr[i] : 0;
+    const int e = i <= last ? a.obj_slot_ptr[i + 1] : 0;
+    const int rb = __shfl_sync(0xffffffffu, b, 0);
+    const int re = __shfl_sync(0xffffffffu, e, last - o0);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int c0 = rb; c0 < re; c0 += kGatherStage) {
+      const int c1 = min(re, c0 + kGatherStage), nv = 2 * (c1 - c0);
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 2 * kGatherStage / 32; ++k) {
+        const int t = lane + 32 * k;
+        if (t < nv) st[t] = __ldcs(in2 + 2 * (long long)c0 + t);  // dead after this read
+      }
+      __syncwarp();
+      const int lo = max(b, c0), hi = min(e, c1);
+      for (int r = lo; r < hi; ++r) {
+        const double2 ra = st[2 * (r - c0)], rb2 = st[2 * (r - c0) + 1];
+        s0 += ra.x; s1 += ra.y; s2 += rb2.x; s3 += rb2.y;
+      }
+    }
+    if (i <= last) {
+      reinterpret_cast<double4*>(a.out)[i] = make_double4(s0, s1, s2, s3);  // [n_obj][4]
+      acc[0] += fabs(s0);
+      acc[1] += fabs(s1);
+      acc[2] += fabs(s3);
+    }
+  }
+  block_sum<3>(acc, red);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 3; ++q) a.partials[q * gridDim.x + blockIdx.x] = acc[q];
+  if (a.final_norms && last_block(a.counter)) {
+    double n[3];
+    for (int q = 0; q < 3; ++q) n[q] = ordered_sum(a.partials + q * gridDim.x, gridDim.x, red);
+    if (threadIdx.x == 0) {
+      a.final_norms[0] = n[0];
+      a.final_norms[1] = n[1];
+      a.final_norms[2] = n[2];
+      a.final_norms[3] = n[2] == 0.0 ? 0.0 : (n[0] + n[1]) / (2.0 * n[2]);  // Eq. 17
+    }
+  }
+}
+
 }  // namespace
 
 void fused_net_setup() {
@@ -952,7 +1016,16 @@ void launch_fused_net(const FusedNetArgs& a, bool f32, cudaStream_t s) {
     pdl_launch(fused_net_kernel<false>, a.blocks, 32 * kWarpsPerBlock, kWarpsPerBlock * sizeof(WarpCols<false>), s, a);
 }
 
+#ifndef P3D_GATHER_WARP
+#define P3D_GATHER_WARP 1
+#endif
 void launch_fused_gather(const FusedGatherArgs& a, cudaStream_t s) {
+  if (P3D_GATHER_WARP && a.in_d) {
+    FusedGatherArgs w = a;  // one warp per 32 objects, same partial slots
+    w.blocks = std::min(a.blocks, std::max(1, (a.n_obj + 32 * kGatherWarps - 1) / (32 * kGatherWarps)));
+    pdl_launch(gather_warp_kernel, w.blocks, 32 * kGatherWarps, 0, s, w);
+    return;
+  }
   pdl_launch(fused_gather_kernel, a.blocks, 256, 0, s, a);
 }
 
