@@ -197,6 +197,9 @@ __device__ __forceinline__ Charge rec_charge(const TileSort& ts, int pos, double
 // two u32 halves: 32-bit shared atomics, native ATOMS.ADD, with the carry
 // propagated by the thread that produced it — exact), or straight to the
 // global map when it falls outside the window.
+#ifndef P3D_PUT_NOBRANCH
+#define P3D_PUT_NOBRANCH 1
+#endif
 struct SmemWindow {
   unsigned int *lo32, *hi32;
   int X0, Y0, W, H, nz;
@@ -206,14 +209,20 @@ struct SmemWindow {
 __device__ __forceinline__ void put_term(const SmemWindow& w, const p3d_grid& g,
                                          unsigned long long* rho, long long t, int ix, int iy,
                                          int iz) {
+#if !P3D_PUT_NOBRANCH
   if (!t) return;
+#endif
   const int lx = ix - w.X0, ly = iy - w.Y0;
   if (w.local && (unsigned)lx < (unsigned)w.W && (unsigned)ly < (unsigned)w.H) {
     const int b = (lx * w.H + ly) * w.nz + iz;
     const unsigned int tl = (unsigned int)t, th = (unsigned int)((unsigned long long)t >> 32);
     const unsigned int old = atomicAdd(&w.lo32[b], tl);
     const unsigned int hadd = th + (old + tl < old ? 1u : 0u);
+#if P3D_PUT_NOBRANCH  // the high half is almost never 0: no branch (adding 0 is exact)
+    atomicAdd(&w.hi32[b], hadd);
+#else
     if (hadd) atomicAdd(&w.hi32[b], hadd);
+#endif
   } else {
     atomicAdd(rho + ((long long)(ix * g.ny + iy) * g.nz + iz), (unsigned long long)t);
   }
@@ -311,12 +320,25 @@ __global__ void __launch_bounds__(256) scatter_tiled_kernel(p3d_grid g, TileSort
     scatter_terms(rec_charge(ts, k, dep), g, w, rho);
   if (!w.local) return;
   __syncthreads();
+#if P3D_PUT_NOBRANCH
+  // one (x, y) column of nz bins per thread and step: one division per column
+  for (int r = threadIdx.x; r < w.W * w.H; r += blockDim.x) {
+    const int ix = r / w.H, iy = r - ix * w.H;
+    unsigned long long* dst = rho + ((long long)((ix + w.X0) * g.ny + (iy + w.Y0)) * g.nz);
+    for (int iz = 0; iz < w.nz; ++iz) {
+      const int b = r * w.nz + iz;
+      const unsigned long long v = ((unsigned long long)w.hi32[b] << 32) | w.lo32[b];
+      if (v) atomicAdd(dst + iz, v);
+    }
+  }
+#else
   for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
     const unsigned long long v = ((unsigned long long)w.hi32[b] << 32) | w.lo32[b];
     if (!v) continue;
     const int iz = b % w.nz, r = b / w.nz, iy = r % w.H, ix = r / w.H;
     atomicAdd(rho + ((long long)((ix + w.X0) * g.ny + (iy + w.Y0)) * g.nz + iz), v);
   }
+#endif
 }
 
 void tiled_scatter_setup() {
