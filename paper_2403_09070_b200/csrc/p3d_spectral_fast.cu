@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
   const double wz0 = 1.0 / a.nz, wz1 = 2.0 / a.nz;
   for (int t = threadIdx.x; t < CB * nx; t += blockDim.x) {
     const int c = t >> LX, j = t & (nx - 1);
-    const int col = c0 + c, ky = col / a.nz, kz = col - ky * a.nz;
+    const int col = c0 + c, ky = a.nz == 2 ? col >> 1 : col / a.nz, kz = col - ky * a.nz;
     const double ox = om[j], oy = a.omy[ky], oz = a.omz[kz];
     const double lam = ox * ox + oy * oy + oz * oz;
     const double inv = lam > 0.0 ? 1.0 / lam : 0.0;
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
       va = inv_pre(T_COS, n, nx, an, am, a.phx);
       vb = inv_pre(T_SIN, n, nx, an * om[n], am * om[nn], a.phx);
     } else {
-      const int col = c0 + c, ky = col / a.nz, kz = col - ky * a.nz;
+      const int col = c0 + c, ky = a.nz == 2 ? col >> 1 : col / a.nz, kz = col - ky * a.nz;
       const double my = a.omy[ky], mz = a.omz[kz];
       va = inv_pre(T_COS, n, nx, an * my, am * my, a.phx);
       vb = inv_pre(T_COS, n, nx, an * mz, am * mz, a.phx);
