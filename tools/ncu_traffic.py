@@ -8,7 +8,7 @@ import os
 import subprocess
 import sys
 
-FAMILY = [("fused_net", "K1"), ("generic_net", "K1"), ("fused_gather", "K1"),
+FAMILY = [("fused_net", "K1"), ("generic_net", "K1"), ("fused_gather", "K1"), ("gather_warp", "K1"),
           ("tile_", "K2"), ("scatter", "K2"), ("spec_", "K3"), ("dens_kernel", "K4"),
           ("gmax0", "K5"), ("advance", "K5")]
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv", "--metrics",
