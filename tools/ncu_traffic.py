@@ -17,7 +17,9 @@ out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv", "--met
 rows = list(csv.reader(io.StringIO(out)))
 hdr, units = rows[0], rows[1]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-fam, kern = {}, {}
+# a kernel captured more than once (the window straddles two iterations)
+# counts once, at its mean
+fam, kern, seen, famof = {}, {}, {}, {}
 for r in rows[2:]:
     d = dict(zip(hdr, r))
     u = dict(zip(hdr, units))
@@ -28,7 +30,11 @@ for r in rows[2:]:
         continue
     short = name.split("(")[0].split("::")[-1]
     kern[short] = kern.get(short, 0) + b
-    fam[f] = fam.get(f, 0) + b
+    seen[short] = seen.get(short, 0) + 1
+    famof[short] = f
+kern = {k: v / seen[k] for k, v in kern.items()}
+for k, v in kern.items():
+    fam[famof[k]] = fam.get(famof[k], 0) + v
 res = {k: int(v) for k, v in fam.items()}
 res["per_kernel"] = {k: int(v) for k, v in kern.items()}
 res["source"] = os.path.basename(sys.argv[1])
