@@ -468,6 +468,9 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
 #else
 #define P3D_K1_LOOP_UNROLL _Pragma("unroll 1")
 #endif
+#ifndef P3D_FLIP_SELECT
+#define P3D_FLIP_SELECT 1
+#endif
 #ifndef P3D_K1_TRIPLE
 #define P3D_K1_TRIPLE 1
 #endif
@@ -548,8 +551,12 @@ P3D_K1_LOOP_UNROLL
     const bool up = (umask >> k) & 1;
     const GradK<R> gk = {up ? k1.rp : k0.rp, up ? k1.rm : k0.rm, up ? k1.vp : k0.vp,
                          up ? k1.vm : k0.vm};
+#if P3D_FLIP_SELECT  // select the pin's sides first, one flip evaluation
+    sm.pz[k][lane] += bx.flip(v, (topm >> k) & 1, full, ex);
+#else
     const double fb = flip_delta(bx.b, bx.t, v, full, ex), ft = flip_delta(bx.t, bx.b, v, full, ex);
     sm.pz[k][lane] += ((topm >> k) & 1) ? ft : fb;
+#endif
     c[k][lane] = (double)gk.grad(v, ig, sm.ep[k][lane], sm.em[k][lane]);
   }
 }
