@@ -271,8 +271,10 @@ typedef struct p3d_gp {
   /* spatial tile sort of the objects for the privatised scatter (K2) */
   int32_t ts_n_tiles, ts_tiles_x, ts_tiles_y;
   int32_t ts_margin;           /* bins an object footprint can reach past its centre tile */
-  int32_t *ts_tile_of, *ts_hist, *ts_start, *ts_cursor, *ts_order;  /* [O], [T], [T+1], [T], [O]:
-                                  ts_order = tile of each record, in tile order */
+  int32_t *ts_tile_of, *ts_hist, *ts_start, *ts_cursor, *ts_order;  /* [O], [T], [T+1], [T], [2O+1]:
+                                  ts_order = tile of each record in tile order, then the
+                                  sort permutation [O] and a permutation-valid flag (the
+                                  sort reruns every P3D_RESORT_EVERY iterations) */
   double* ts_rec;              /* [O][6] charge records (x, y, z, w, h, weight) in tile order */
   double* rho;                 /* [B] */
   double* spec_scratch;        /* [6*B] */

@@ -100,6 +100,14 @@ __device__ __forceinline__ void scan_tiles(const TileSort& ts) {
   if (threadIdx.x == 0) ts.start[ts.n_tiles] = carry;
 }
 
+#ifndef P3D_RESORT_EVERY
+#define P3D_RESORT_EVERY 4
+#endif
+__device__ __forceinline__ bool resort_now(const TileSort& ts) {
+  if (!ts.perm || !ts.it || ts.every <= 1) return true;
+  return !*(volatile const int32_t*)ts.valid || (*ts.it % ts.every) == 0;
+}
+
 // K2 step 1: per-object tile of the centre + tile histogram; the last block
 // scans the histogram.  The first n_macro blocks scatter one macro each
 // (per-macro footprint tile, int64 global atomics), independent of the sort.
@@ -112,7 +120,7 @@ __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_gri
   extern __shared__ int sh_hist[];
   if ((int)blockIdx.x < n_macro) {
     scatter_object_block(cl.get(macro_ids[blockIdx.x]), g, rho);
-  } else {
+  } else if (resort_now(ts)) {
     for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x) sh_hist[t] = 0;
     __syncthreads();
     // the tile of an object's centre only groups the records (any assignment
@@ -139,7 +147,7 @@ __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_gri
     for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x)
       if (sh_hist[t]) atomicAdd(&ts.hist[t], sh_hist[t]);
   }
-  if (last_block_all(ts.counter)) scan_tiles(ts);
+  if (last_block_all(ts.counter) && resort_now(ts)) scan_tiles(ts);
 }
 
 // Stable-per-block placement: each CTA ranks its objects per tile in shared
@@ -153,6 +161,22 @@ __global__ void __launch_bounds__(256) tile_place_kernel(Cloud cl, int n, TileSo
                                                         const int* halt) {
   pdl_wait();
   if (halt && *halt) return;
+  const bool sorting = resort_now(ts);
+  if (!sorting) {
+    // refresh the records in the last sort's order (coalesced record writes)
+    const int total = ts.start[ts.n_tiles];
+    for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < total;
+         pos += gridDim.x * blockDim.x) {
+      const int kl = ts.perm[pos];
+      const int i = kl < ts.ni ? ts.i0 + kl : ts.f0 + (kl - ts.ni);
+      const Charge q = cl.get(i);
+      double2* r = reinterpret_cast<double2*>(ts.rec) + 3 * (long long)pos;
+      r[0] = make_double2(q.x, q.y);
+      r[1] = make_double2(q.z, q.w);
+      r[2] = make_double2(q.h, q.weight);
+    }
+    return;
+  }
   extern __shared__ int sh[];
   int* cnt = sh;                  // [n_tiles]
   int* base = sh + ts.n_tiles;    // [n_tiles]
@@ -178,11 +202,13 @@ __global__ void __launch_bounds__(256) tile_place_kernel(Cloud cl, int n, TileSo
     const int pos = base[tile[k]] + rank[k];
     const Charge q = cl.get(i);
     ts.order[pos] = tile[k];
+    if (ts.perm) ts.perm[pos] = kl;
     double2* r = reinterpret_cast<double2*>(ts.rec) + 3 * (long long)pos;
     r[0] = make_double2(q.x, q.y);
     r[1] = make_double2(q.z, q.w);
     r[2] = make_double2(q.h, q.weight);
   }
+  if (ts.valid && blockIdx.x == 0 && threadIdx.x == 0) *ts.valid = 1;
 }
 
 __device__ __forceinline__ Charge rec_charge(const TileSort& ts, int pos, double dep) {

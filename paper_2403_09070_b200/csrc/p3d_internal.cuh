@@ -161,6 +161,14 @@ struct TileSort {
   int32_t* order;    // [n_obj] tile of each record, in tile order
   double* rec;       // [n_obj][6] charge records in tile order
   unsigned int* counter;  // last-block ticket of the histogram kernel
+  // periodic re-sort: the counting sort runs when *it % every == 0 (or before
+  // the first sort, *valid == 0); in between, the records are refreshed in the
+  // last sort's order (perm[pos] = local object index).  rho is int64 fixed
+  // point, so any record order gives the same map bit for bit.
+  int32_t* perm;          // [n_obj] (null: sort every call)
+  int32_t* valid;         // [1] set once perm holds a sort
+  const int32_t* it;      // the loop's iteration counter (null: sort every call)
+  int every;
 };
 struct CloudGP;
 void tiled_scatter_setup();

@@ -614,6 +614,9 @@ __global__ void __launch_bounds__(256, P3D_K5_MINB) advance_kernel(p3d_gp gp) {
 // ---------------------------------------------------------------------------
 // K2 of the loop: spatially sorted, shared-memory privatised scatter of the
 // cells / fillers + per-macro tiles, into gp.rho_fx (int64 fixed point)
+#ifndef P3D_RESORT_EVERY
+#define P3D_RESORT_EVERY 4
+#endif
 static void scatter_k2(const p3d_gp& gp, const int* halt, cudaStream_t s) {
   CloudGP cl;
   cl.pos = gp.v;
@@ -640,6 +643,11 @@ static void scatter_k2(const p3d_gp& gp, const int* halt, cudaStream_t s) {
     ts.i0 = gp.sh_i0;
     ts.ni = gp.sh_i1 - gp.sh_i0;
     ts.f0 = gp.sh_f0;
+    // ts_order holds [n_obj] tiles, then [n_obj] perm, then the valid flag
+    ts.perm = gp.ts_order + gp.n_obj;
+    ts.valid = gp.ts_order + 2 * (long long)gp.n_obj;
+    ts.it = &gp.st->it;
+    ts.every = P3D_RESORT_EVERY;
     launch_scatter_tiled(cl, own_count(gp), gp.n_macro, gp.macro_ids, gp.grid, ts, gp.rho_fx,
                          halt, s);
   } else {

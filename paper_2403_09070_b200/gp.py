@@ -473,7 +473,8 @@ class Gp3dProblem:
         tx, ty = -(-grid.nx // 16), -(-grid.ny // 16)  # kTile in p3d_density.cu
         nt = tx * ty
         i32z = lambda n: torch.zeros(max(int(n), 1), dtype=torch.int32, device="cuda")  # noqa: E731
-        self.t_ts = [i32z(O), i32z(nt), i32z(nt + 1), i32z(nt), i32z(O)]
+        # ts_order: [O] tiles, [O] sort permutation, [1] permutation-valid flag
+        self.t_ts = [i32z(O), i32z(nt), i32z(nt + 1), i32z(nt), i32z(2 * O + 1)]
         g.ts_n_tiles, g.ts_tiles_x, g.ts_tiles_y = nt, tx, ty
         # footprint reach past the centre tile, in bins (+2: centre-bin rounding)
         cell = ~arr.is_macro
