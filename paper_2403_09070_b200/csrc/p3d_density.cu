@@ -55,7 +55,10 @@ void launch_scatter(const Cloud& cl, int n, int n_macro, const int32_t* macro_id
 // map independent of the (atomic, unstable) order within a tile.
 // ---------------------------------------------------------------------------
 constexpr int kTile = 16;
-constexpr int kChunk = 1024;
+#ifndef P3D_CHUNK
+#define P3D_CHUNK 1024
+#endif
+constexpr int kChunk = P3D_CHUNK;  // records per scatter CTA
 constexpr int kBoxBins = 6144;  // 48 KB of int64 bins per CTA
 
 // exclusive scan of the tile histogram by one block; re-zeroes the histogram
