@@ -106,6 +106,9 @@ __device__ __forceinline__ void scan_tiles(const TileSort& ts) {
 #ifndef P3D_RESORT_EVERY
 #define P3D_RESORT_EVERY 4
 #endif
+#ifndef P3D_SCATTER_DIRECT
+#define P3D_SCATTER_DIRECT 1
+#endif
 __device__ __forceinline__ bool resort_now(const TileSort& ts) {
   if (!ts.perm || !ts.it || ts.every <= 1) return true;
   return !*(volatile const int32_t*)ts.valid || (*ts.it % ts.every) == 0;
@@ -165,6 +168,9 @@ __global__ void __launch_bounds__(256) tile_place_kernel(Cloud cl, int n, TileSo
   pdl_wait();
   if (halt && *halt) return;
   const bool sorting = resort_now(ts);
+#if P3D_SCATTER_DIRECT
+  if (!sorting) return;  // the scatter reads the objects through perm itself
+#endif
   if (!sorting) {
     // refresh the records in the last sort's order (coalesced record writes)
     const int total = ts.start[ts.n_tiles];
@@ -295,11 +301,25 @@ __device__ __forceinline__ void scatter_terms(const Charge& q, const p3d_grid& g
   }
 }
 
-__global__ void __launch_bounds__(256) scatter_tiled_kernel(p3d_grid g, TileSort ts,
+// the k-th charge of the sorted order: its record, or (between re-sorts, with
+// P3D_SCATTER_DIRECT) the object itself through the last sort's permutation
+__device__ __forceinline__ Charge chunk_charge(const TileSort& ts, const CloudGP& cl, bool direct,
+                                               int k, double dep) {
+#if P3D_SCATTER_DIRECT
+  if (direct) {
+    const int kl = ts.perm[k];
+    return cl.get(kl < ts.ni ? ts.i0 + kl : ts.f0 + (kl - ts.ni));
+  }
+#endif
+  return rec_charge(ts, k, dep);
+}
+
+__global__ void __launch_bounds__(256) scatter_tiled_kernel(p3d_grid g, TileSort ts, CloudGP cl,
                                                            unsigned long long* rho,
                                                            const int* halt) {
   pdl_wait();
   if (halt && *halt) return;
+  const bool direct = !resort_now(ts);
   extern __shared__ unsigned int sbin32[];
   __shared__ int box[4];
   const int total = ts.start[ts.n_tiles];
@@ -323,7 +343,7 @@ __global__ void __launch_bounds__(256) scatter_tiled_kernel(p3d_grid g, TileSort
   } else {
     int bx0 = INT_MAX, bx1 = -1, by0 = INT_MAX, by1 = -1;
     for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
-      const Footprint f = footprint(rec_charge(ts, k, dep), g);
+      const Footprint f = footprint(chunk_charge(ts, cl, direct, k, dep), g);
       bx0 = min(bx0, f.ax.i0); bx1 = max(bx1, f.ax.i1);
       by0 = min(by0, f.ay.i0); by1 = max(by1, f.ay.i1);
     }
@@ -346,7 +366,7 @@ __global__ void __launch_bounds__(256) scatter_tiled_kernel(p3d_grid g, TileSort
     __syncthreads();
   }
   for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x)
-    scatter_terms(rec_charge(ts, k, dep), g, w, rho);
+    scatter_terms(chunk_charge(ts, cl, direct, k, dep), g, w, rho);
   if (!w.local) return;
   __syncthreads();
 #if P3D_PUT_NOBRANCH
@@ -398,7 +418,7 @@ void launch_scatter_tiled(const CloudGP& cl, int n, int n_macro, const int32_t* 
   const int np = (n + 256 * kPlacePerThread - 1) / (256 * kPlacePerThread);
   pdl_launch(tile_place_kernel<CloudGP>, np, 256, 2 * ts.n_tiles * sizeof(int), s, cl, n, ts, halt);
   const int chunks = (n + kChunk - 1) / kChunk;
-  pdl_launch(scatter_tiled_kernel, chunks, 256, kBoxBins * 8, s, g, ts, r, halt);
+  pdl_launch(scatter_tiled_kernel, chunks, 256, kBoxBins * 8, s, g, ts, cl, r, halt);
 }
 
 template void launch_scatter<CloudGP>(const CloudGP&, int, int, const int32_t*, const p3d_grid&,
