@@ -46,8 +46,9 @@ void launch_scatter(const Cloud& cl, int n, int n_macro, const int32_t* macro_id
 
 // ---------------------------------------------------------------------------
 // Spatially ordered, shared-memory-privatised scatter (the fused loop's K2).
-// Every iteration the non-macro objects are counting-sorted by the planar
-// tile (kTile x kTile bins) of their current centre; a CTA then takes 1024
+// Every P3D_RESORT_EVERY-th iteration the non-macro objects are counting-sorted
+// by the planar tile (kTile x kTile bins) of their current centre (in between,
+// the last sort's order is reused); a CTA then takes 1024
 // consecutive objects of that order, whose footprints cover a small bounding
 // box of bins: it accumulates their int64 terms in shared memory (contention
 // moves from L2 atomics to shared-memory atomics) and flushes the box once.
@@ -59,6 +60,10 @@ constexpr int kTile = 16;
 #define P3D_CHUNK 1024
 #endif
 constexpr int kChunk = P3D_CHUNK;  // records per scatter CTA
+#ifndef P3D_MACRO_SPLIT
+#define P3D_MACRO_SPLIT 1
+#endif
+constexpr int kMacroSplit = P3D_MACRO_SPLIT;  // CTAs per macro footprint in the scatter
 constexpr int kBoxBins = 6144;  // 48 KB of int64 bins per CTA
 
 // exclusive scan of the tile histogram by one block; re-zeroes the histogram
@@ -104,7 +109,7 @@ __device__ __forceinline__ void scan_tiles(const TileSort& ts) {
 }
 
 #ifndef P3D_RESORT_EVERY
-#define P3D_RESORT_EVERY 4
+#define P3D_RESORT_EVERY 8
 #endif
 #ifndef P3D_SCATTER_DIRECT
 #define P3D_SCATTER_DIRECT 1
@@ -115,7 +120,7 @@ __device__ __forceinline__ bool resort_now(const TileSort& ts) {
 }
 
 // K2 step 1: per-object tile of the centre + tile histogram; the last block
-// scans the histogram.  The first n_macro blocks scatter one macro each
+// scans the histogram.  The first n_macro * kMacroSplit blocks scatter the macros
 // (per-macro footprint tile, int64 global atomics), independent of the sort.
 template <class Cloud>
 __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_grid g, TileSort ts,
@@ -124,8 +129,9 @@ __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_gri
   pdl_wait();
   if (halt && *halt) return;
   extern __shared__ int sh_hist[];
-  if ((int)blockIdx.x < n_macro) {
-    scatter_object_block(cl.get(macro_ids[blockIdx.x]), g, rho);
+  if ((int)blockIdx.x < n_macro * kMacroSplit) {  // kMacroSplit CTAs per macro footprint
+    scatter_object_block(cl.get(macro_ids[blockIdx.x / kMacroSplit]), g, rho,
+                         blockIdx.x % kMacroSplit, kMacroSplit);
   } else if (resort_now(ts)) {
     for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x) sh_hist[t] = 0;
     __syncthreads();
@@ -134,7 +140,7 @@ __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_gri
     // so the centre is scaled by reciprocals, and only x, y and the macro
     // flag are read
     const double rtw = 1.0 / (g.wb * kTile), rth = 1.0 / (g.hb * kTile);
-    const int b = blockIdx.x - n_macro, nb = gridDim.x - n_macro;
+    const int b = blockIdx.x - n_macro * kMacroSplit, nb = gridDim.x - n_macro * kMacroSplit;
     for (int k = b * blockDim.x + threadIdx.x; k < n; k += nb * blockDim.x) {
       const int i = k < ts.ni ? ts.i0 + k : ts.f0 + (k - ts.ni);  // this rank's objects
       const double cx = cl.cx(i), cy = cl.cy(i);
@@ -413,7 +419,7 @@ void launch_scatter_tiled(const CloudGP& cl, int n, int n_macro, const int32_t* 
                           cudaStream_t s) {
   unsigned long long* r = reinterpret_cast<unsigned long long*>(rho);
   const int nb = grid_blocks(n, 256, 148 * 8);
-  pdl_launch(tile_hist_kernel<CloudGP>, n_macro + nb, 256, ts.n_tiles * sizeof(int), s, cl, n, g,
+  pdl_launch(tile_hist_kernel<CloudGP>, n_macro * kMacroSplit + nb, 256, ts.n_tiles * sizeof(int), s, cl, n, g,
              ts, macro_ids, n_macro, r, halt);
   const int np = (n + 256 * kPlacePerThread - 1) / (256 * kPlacePerThread);
   pdl_launch(tile_place_kernel<CloudGP>, np, 256, 2 * ts.n_tiles * sizeof(int), s, cl, n, ts, halt);

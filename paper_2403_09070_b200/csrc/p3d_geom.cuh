@@ -171,11 +171,12 @@ __device__ __forceinline__ void scatter_object(const Charge& q, const p3d_grid& 
 
 // block-cooperative scatter of one large object (per-macro tile path)
 __device__ __forceinline__ void scatter_object_block(const Charge& q, const p3d_grid& g,
-                                                     unsigned long long* rho) {
+                                                     unsigned long long* rho, int part = 0,
+                                                     int nparts = 1) {
   const Footprint f = footprint(q, g);
   const int nxr = f.ax.i1 - f.ax.i0 + 1, nyr = f.ay.i1 - f.ay.i0 + 1, nzr = f.az.i1 - f.az.i0 + 1;
   const int tot = nxr * nyr * nzr;
-  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+  for (int t = part * blockDim.x + threadIdx.x; t < tot; t += nparts * blockDim.x) {
     const int iz = f.az.i0 + t % nzr;
     const int iy = f.ay.i0 + (t / nzr) % nyr;
     const int ix = f.ax.i0 + t / (nzr * nyr);

@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(256, P3D_K5_MINB) advance_kernel(p3d_gp gp) {
 // K2 of the loop: spatially sorted, shared-memory privatised scatter of the
 // cells / fillers + per-macro tiles, into gp.rho_fx (int64 fixed point)
 #ifndef P3D_RESORT_EVERY
-#define P3D_RESORT_EVERY 4
+#define P3D_RESORT_EVERY 8
 #endif
 static void scatter_k2(const p3d_gp& gp, const int* halt, cudaStream_t s) {
   CloudGP cl;
