@@ -114,6 +114,9 @@ __device__ __forceinline__ void scan_tiles(const TileSort& ts) {
 #ifndef P3D_SCATTER_DIRECT
 #define P3D_SCATTER_DIRECT 1
 #endif
+#ifndef P3D_SCATTER_CELL
+#define P3D_SCATTER_CELL 1
+#endif
 __device__ __forceinline__ bool resort_now(const TileSort& ts) {
   if (!ts.perm || !ts.it || ts.every <= 1) return true;
   return !*(volatile const int32_t*)ts.valid || (*ts.it % ts.every) == 0;
@@ -215,7 +218,11 @@ __global__ void __launch_bounds__(256) tile_place_kernel(Cloud cl, int n, TileSo
     const int kl = i0 + k * blockDim.x;
     const int i = kl < ts.ni ? ts.i0 + kl : ts.f0 + (kl - ts.ni);  // this rank's objects
     const int pos = base[tile[k]] + rank[k];
+#if P3D_SCATTER_CELL
+    const Charge q = cl.get_nonmacro(i);  // tile >= 0: not a macro
+#else
     const Charge q = cl.get(i);
+#endif
     ts.order[pos] = tile[k];
     if (ts.perm) ts.perm[pos] = kl;
     double2* r = reinterpret_cast<double2*>(ts.rec) + 3 * (long long)pos;
@@ -314,7 +321,12 @@ __device__ __forceinline__ Charge chunk_charge(const TileSort& ts, const CloudGP
 #if P3D_SCATTER_DIRECT
   if (direct) {
     const int kl = ts.perm[k];
-    return cl.get(kl < ts.ni ? ts.i0 + kl : ts.f0 + (kl - ts.ni));
+    const int i = kl < ts.ni ? ts.i0 + kl : ts.f0 + (kl - ts.ni);
+#if P3D_SCATTER_CELL
+    return cl.get_nonmacro(i);  // perm holds no macro (their tile is -1)
+#else
+    return cl.get(i);
+#endif
   }
 #endif
   return rec_charge(ts, k, dep);

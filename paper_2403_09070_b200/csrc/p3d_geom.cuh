@@ -144,6 +144,28 @@ struct CloudGP {  // Gp3dProblem.cloud(pos) computed on the fly (gp.py:267-278)
     q.dep = dz / 2;
     return q;
   }
+  // get(i) for an object known not to be a macro (the scatter's sorted cells
+  // and fillers): the same values, loading only the die's width / height pair
+  __device__ __forceinline__ Charge get_nonmacro(int i) const {
+    Charge q;
+    q.x = pos[i];
+    q.y = pos[n_obj + i];
+    q.z = pos[2 * n_obj + i];
+    if (i < n_inst) {
+      const double zc = clipd(q.z, dz / 4, 3 * dz / 4);  // dynamic_wh's cell branch
+      const bool top = (zc - dz / 2) > 0.0;
+      const double* pw = top ? wt : wb;
+      const double* ph = top ? ht : hb;
+      q.w = pw[i];
+      q.h = ph[i];
+    } else {
+      q.w = fw[i - n_inst];
+      q.h = fh[i - n_inst];
+    }
+    q.weight = 1.0;
+    q.dep = dz / 2;
+    return q;
+  }
 };
 
 __device__ __forceinline__ double charge_of(const Charge& q) {
