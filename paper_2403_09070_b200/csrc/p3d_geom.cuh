@@ -124,6 +124,7 @@ struct CloudGP {  // Gp3dProblem.cloud(pos) computed on the fly (gp.py:267-278)
   const double *wt, *ht, *wb, *hb, *fw, *fh;
   const uint8_t* macro;
   double dz, target_density;
+  const double4* pos4 = nullptr;  // optional [n_inst] AoS copy of pos (x, y, z, 0)
   __device__ __forceinline__ bool is_macro(int i) const { return i < n_inst && macro[i]; }
   __device__ __forceinline__ double cx(int i) const { return pos[i]; }
   __device__ __forceinline__ double cy(int i) const { return pos[n_obj + i]; }
@@ -148,9 +149,14 @@ struct CloudGP {  // Gp3dProblem.cloud(pos) computed on the fly (gp.py:267-278)
   // and fillers): the same values, loading only the die's width / height pair
   __device__ __forceinline__ Charge get_nonmacro(int i) const {
     Charge q;
-    q.x = pos[i];
-    q.y = pos[n_obj + i];
-    q.z = pos[2 * n_obj + i];
+    if (pos4 && i < n_inst) {  // one 32-byte load instead of three scattered ones
+      const double4 p = pos4[i];
+      q.x = p.x; q.y = p.y; q.z = p.z;
+    } else {
+      q.x = pos[i];
+      q.y = pos[n_obj + i];
+      q.z = pos[2 * n_obj + i];
+    }
     if (i < n_inst) {
       const double zc = clipd(q.z, dz / 4, 3 * dz / 4);  // dynamic_wh's cell branch
       const bool top = (zc - dz / 2) > 0.0;

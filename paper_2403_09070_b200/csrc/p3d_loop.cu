@@ -627,6 +627,16 @@ static void scatter_k2(const p3d_gp& gp, const int* halt, cudaStream_t s) {
   cl.macro = gp.is_macro;
   cl.dz = gp.grid.dz;
   cl.target_density = gp.target_density;
+#ifndef P3D_SCATTER_POS4
+#define P3D_SCATTER_POS4 1
+#endif
+#if P3D_SCATTER_POS4
+  // inside the loop (halt set) K5 / gp_init / gp_evaluate keep pos4 (evict-last)
+  // in step with v for the instances, as K1 relies on too; the sorted scatter
+  // then reads a cell's centre from it in one sector.  The per-op density
+  // call (halt null) reads v only.
+  if (halt && gp.pos4) cl.pos4 = reinterpret_cast<const double4*>(gp.pos4);
+#endif
   if (gp.ts_order) {
     TileSort ts;
     ts.n_tiles = gp.ts_n_tiles;
