@@ -423,11 +423,12 @@ class Gp3dProblem:
         g.f_pin_off = keep(_dev.dev(one(L["pin_off"].reshape(-1), np.float32), torch.float32))
         g.f_pin_slot = keep(_dev.i32(one(L["pin_slot"], np.int64)))
         # K1 runs one persistent wave of 128-thread CTAs: 4 per SM (all its
-        # 124-register budget allows) alone, 3 per SM when it shares the GPU
-        # with the density branch (measured at config 3: +1.4% over 4 per SM)
+        # 124-register budget allows) alone, 3.5 per SM when it shares the GPU
+        # with the density branch (measured at config 3: +0.9% over 3 per SM,
+        # +1.5% over 4 per SM; 3.25 / 3.75 per SM in between)
         g.nblk_net = max(1, min(-(-g.f_n_tasks // 4), K_MAX_BLOCKS,
                                 int(os.environ.get("P3D_NBLK_NET",
-                                                   (3 if g.overlap else 4) * n_sm))))
+                                                   (7 * n_sm) // 2 if g.overlap else 4 * n_sm))))
         gs, gkeep = grid.device()
         g.grid = gs
         self._gkeep = gkeep
