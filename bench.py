@@ -180,28 +180,130 @@ def _cpu_baseline(P, design, grid_n, spec, seconds, max_iters):
     return it / el, it, el
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _import_reference():
+    """The unmodified reference package installed in baseline/_ref (pip
+    --target; it travels to the GPU box with the snapshot), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "place3d")):
+        return None
+    sys.path.insert(0, REF_DIR)
+    try:
+        import place3d.gp  # noqa: F401
+        import place3d.model  # noqa: F401
+        import place3d.synth  # noqa: F401
+    finally:
+        sys.path.remove(REF_DIR)
+    return sys.modules["place3d"]
+
+
+class _IterClock(list):
+    """iteration_log for the reference's run_gp3d: stamps every appended row
+    (one row per GP iteration, gp.py:400-401) and ends the run after `stop`."""
+
+    class Done(Exception):
+        pass
+
+    def __init__(self, warmup, steps, budget_s=240.0):
+        super().__init__()
+        self.warmup, self.stop, self.budget_s = warmup, warmup + steps, budget_s
+        self.t = [time.perf_counter()]
+
+    def append(self, row):
+        super().append(row)
+        self.t.append(time.perf_counter())
+        if len(self) == self.warmup + 1:  # trim the timed sample to the budget
+            dt = self.t[-1] - self.t[-2]
+            self.stop = min(self.stop, self.warmup + max(3, int(self.budget_s / max(dt, 1e-9))))
+        if len(self) >= self.stop:
+            raise _IterClock.Done()
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the CPU implementation of the path (oracle port of the
-    reference numpy code; the Python reference itself cannot travel to the GPU
-    box) on rank 0's host cores."""
+    """--impl reference: the reference's own run_gp3d (baseline/_ref, its stock
+    numpy code path, gp.py:359-455) on rank 0's host cores, timed iteration
+    by iteration through its iteration_log (setup excluded); without
+    baseline/_ref, the oracle port.  Other ranks exit without work."""
     if rank != 0:
         return
-    design, grid_n, spec = setup_design(args.config, 0)
-    budget = min(60.0, 6.0 * (args.steps + args.warmup))
-    rate, iters, el = cpu_baseline(design, grid_n, spec, seconds=budget)
+    from paper_2403_09070_b200.synth import CONFIGS
+
+    ref = _import_reference()
+    c = CONFIGS[args.config]
+    grid_n, spec = c["grid"], c["spec"]
     ncpu = os.cpu_count()
+    W, K = max(args.warmup, 0), args.steps
+    if ref is None:
+        design, grid_n, spec = setup_design(args.config, 0)
+        budget = min(60.0, 6.0 * (K + W))
+        rate, iters, el = cpu_baseline(design, grid_n, spec, seconds=budget)
+        kind, sample, W, K = "port", (f"{iters} GP iterations from the initial state "
+                                      f"({el:.1f} s), oracle.port numpy, 1 thread"), 0, iters
+    else:
+        from threadpoolctl import threadpool_limits
+
+        t0 = time.perf_counter()
+        d = ref.model.parse_design(ref.synth.gen_synthetic(ref.synth.SynthSpec(**spec.__dict__)))
+        setup_s = time.perf_counter() - t0
+        cfg = ref.gp.GpConfig(seed=spec.seed, nz=2, grid_nx=grid_n, grid_ny=grid_n,
+                              max_iters=200, stop_overflow=0.0)
+        rng = np.random.default_rng(spec.seed)
+        grid = ref.gp.choose_grid(d, cfg)
+        st = ref.gp.init_state(d, grid, cfg, rng)
+        # bounded sample: W + K iterations of the 200-iteration schedule, K
+        # trimmed so the timed part stays within ~4 minutes (per-iteration cost
+        # measured on the first timed iteration)
+        W = max(W, 1)  # the first iteration also builds the reference's Gp3dProblem
+        clock = _IterClock(W, K)
+        with threadpool_limits(limits=ncpu):
+            try:
+                ref.gp.run_gp3d(d, st, cfg, grid=grid, iteration_log=clock, rng=rng)
+            except _IterClock.Done:
+                pass
+        ts = np.array(clock.t)
+        iters = len(ts) - 1 - W
+        el = float(ts[-1] - ts[W])
+        rate = iters / el
+        kind = "reference"
+        sample = (f"place3d.gp.run_gp3d (baseline/_ref, unmodified) on config {args.config}: "
+                  f"{W} warm-up + {iters} timed iterations of the 200-iteration schedule "
+                  f"({el:.1f} s timed; setup {setup_s:.0f} s excluded); numpy/scipy, "
+                  f"threadpool limit {ncpu} (the reference loop is single-threaded); "
+                  f"final row {list(clock[-1])}")
+        K = iters
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "it/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / rate,
+        "steps": K, "warmup": W, "ms_per_step": 1000.0 / rate,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": WORKLOADS[args.config], "grid": [grid_n] * 2 + [2],
                                         "max_iters_schedule": 200},
-        "cpu_baseline": {"value": rate, "unit": "it/s", "cores": 1, "kind": "port",
-                         "sample": f"{iters} GP iterations from the initial state ({el:.1f} s), "
-                                   f"numpy single-threaded, host has {ncpu} cpus"},
+        "cpu_baseline": {"value": rate, "unit": "it/s", "cores": 1, "kind": kind,
+                         "sample": sample + f"; host has {ncpu} cpus"},
         "e2e": {"value": rate, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def parity_vs_reference(config, max_iters, row):
+    """The bench's last log row against the reference's row at the same
+    iteration (tests/golden/cfg3_rows.json, made by the reference itself)."""
+    if config != 3 or max_iters != 200:
+        return None
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "cfg3_rows.json")) as fh:
+            gold = json.load(fh)["sched200_first25"]
+    except (OSError, ValueError, KeyError):
+        return None
+    it = int(row[0])
+    if it >= len(gold):
+        return {"iteration": it, "note": "beyond the committed reference rows"}
+    r = gold[it]
+    wl_rel = abs(row[1] - r[1]) / r[1]
+    ov_rel = abs(row[3] - r[3]) / r[3]
+    return {"iteration": it, "reference_row": r, "wl_rel": wl_rel, "overflow_rel": ov_rel,
+            "crossings_equal": int(row[2]) == int(r[2]),
+            "ok": bool(wl_rel <= 5e-3 and ov_rel <= 5e-3)}
 
 
 def make_problem_inputs(design, spec, grid_n, max_iters, G):
@@ -376,6 +478,15 @@ def main():
                     help="WA arithmetic: fp64 numpy-order (default) or fp32 anchored")
     args = ap.parse_args()
     rank, world, local = rank_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not under torchrun: spawn one rank per GPU ourselves
+        import subprocess
+
+        port = os.environ.get("MASTER_PORT", "29511")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", port, os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         return run_reference(args, rank, world)
     mode = args.mode or ("sharded" if world > 1 else "fused")
@@ -535,6 +646,7 @@ def main():
         "clocks": clocks.summary(),
         "final_row": list(prob.log_rows(W + K)[-1]),
     }
+    line["parity"] = parity_vs_reference(args.config, max_iters, line["final_row"])
     line["roofline"] = roofline_of(design, prob.n_fill, grid, stage, args.config,
                                    shards=world if mode == "sharded" else 1)
     if mode == "sharded":  # rank 0's stage attribution of one shard (eager replay)

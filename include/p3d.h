@@ -40,6 +40,8 @@ size_t p3d_sizeof_grid(void);
 size_t p3d_sizeof_cloud(void);
 size_t p3d_sizeof_gp(void);
 size_t p3d_sizeof_loop_state(void);
+/* Doubles the p3d_gp.partials buffer must hold (16 slots x 8 x 2048 blocks). */
+size_t p3d_gp_partials_doubles(void);
 
 /* ------------------------------------------------------------------------ */
 /* netlist topology: CSR pins by net (wirelength.py:30-47 NetTopology)       */
@@ -271,15 +273,18 @@ typedef struct p3d_gp {
   /* spatial tile sort of the objects for the privatised scatter (K2) */
   int32_t ts_n_tiles, ts_tiles_x, ts_tiles_y;
   int32_t ts_margin;           /* bins an object footprint can reach past its centre tile */
-  int32_t *ts_tile_of, *ts_hist, *ts_start, *ts_cursor, *ts_order;  /* [O], [T], [T+1], [T], [2O+1]:
+  int32_t *ts_tile_of, *ts_hist, *ts_start, *ts_cursor, *ts_order;  /* [O], [T], [T+1], [T], [2O+2]:
                                   ts_order = tile of each record in tile order, then the
-                                  sort permutation [O] and a permutation-valid flag (the
-                                  sort reruns every P3D_RESORT_EVERY iterations) */
+                                  sort permutation [O], a permutation-valid flag and the
+                                  iteration's sort decision (the sort reruns every
+                                  P3D_RESORT_EVERY iterations) */
   double* ts_rec;              /* [O][6] charge records (x, y, z, w, h, weight) in tile order */
   double* rho;                 /* [B] */
   double* spec_scratch;        /* [6*B] */
   double* maps;                /* [B][4] */
-  double* partials;            /* [16][4096] */
+  double* partials;            /* [16][8 * 2048] = p3d_gp_partials_doubles() doubles:
+                                  16 slots of per-block partial sums (8 per block, up
+                                  to 2048 blocks per launch) */
   p3d_loop_state* st;
   double* log;                 /* [max_iters][4]: it, exact WL, crossings, overflow */
   double* ovfl_hist;           /* [max_iters] */

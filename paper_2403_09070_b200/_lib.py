@@ -91,6 +91,7 @@ _SIGS = {
     "p3d_sizeof_cloud": (C.c_size_t, []),
     "p3d_sizeof_gp": (C.c_size_t, []),
     "p3d_sizeof_loop_state": (C.c_size_t, []),
+    "p3d_gp_partials_doubles": (C.c_size_t, []),
     "p3d_netboxes": (I32, [P, P, P, P, P, P, P, P, P, P, P, P]),
     "p3d_planar_objective_ex": (I32, [P, P, P, P, D, P, P, P, P, P]),
     "p3d_z_cut_penalty_ex": (I32, [P, P, D, P, P, P, P]),

@@ -2,13 +2,17 @@
 
 Translation units whose arithmetic must round exactly like numpy (density
 overlaps, the optimiser) are compiled with ``-fmad=false``; the others keep FMA
-contraction.  Object files are rebuilt only when a source or header changed.
+contraction.  Object files are rebuilt only when a source or header changed,
+or when the nvcc flags differ from the ones the object dir was built with
+(a flags stamp in the object dir).
 """
 
 from __future__ import annotations
 
 import concurrent.futures as cf
+import hashlib
 import os
+import shutil
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -56,7 +60,15 @@ def build(verbose=False, extra=(), variant=""):
     with the `extra` nvcc flags (e.g. -D switches) in its own object dir."""
     objdir = OBJDIR + (f"_{variant}" if variant else "")
     lib_path = LIB if not variant else os.path.join(HERE, f"libp3d_{variant}.so")
+    stamp = hashlib.sha256(" ".join([_nvcc(), *ARCH, *COMMON, *extra, "|", *sorted(NO_FMA)])
+                           .encode()).hexdigest()
+    stamp_path = os.path.join(objdir, "FLAGS")
+    if os.path.isdir(objdir) and (not os.path.exists(stamp_path) or
+                                  open(stamp_path).read().strip() != stamp):
+        shutil.rmtree(objdir)  # built with other flags (e.g. -D switches): rebuild all
     os.makedirs(objdir, exist_ok=True)
+    with open(stamp_path, "w") as fh:
+        fh.write(stamp + "\n")
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         results = list(ex.map(lambda s: _compile(s, list(extra), objdir), SOURCES))
     objs = [o for o, _ in results]

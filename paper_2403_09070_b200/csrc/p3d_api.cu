@@ -117,6 +117,7 @@ size_t p3d_sizeof_grid(void) { return sizeof(p3d_grid); }
 size_t p3d_sizeof_cloud(void) { return sizeof(p3d_cloud); }
 size_t p3d_sizeof_gp(void) { return sizeof(p3d_gp); }
 size_t p3d_sizeof_loop_state(void) { return sizeof(p3d_loop_state); }
+size_t p3d_gp_partials_doubles(void) { return (size_t)16 * kPartialStride; }
 
 int p3d_netboxes(const p3d_topology* t, const double* coord, const uint8_t* on_top, int64_t* cnt,
                  double* min1, double* min2, double* max1, double* max2, double* full_min,
@@ -358,9 +359,12 @@ int p3d_precondition(int32_t n, const double* gr, double lam, const double* q, c
 }
 
 static bool bad_gp(const p3d_gp* gp) {
-  if (!gp || !gp->st || !gp->u || !gp->v || gp->n_obj <= 0 || gp->n_inst < 0 ||
-      gp->nblk_obj <= 0 || gp->nblk_obj > kMaxBlocks || gp->nblk_net <= 0 ||
-      gp->nblk_net > kMaxBlocks || gp->n_macro > kMaxBlocks) {
+  // every per-launch grid writes one partial per block into a kMaxBlocks-wide
+  // slot: the density kernel runs n_macro + nblk_dens blocks
+  if (!gp || !gp->st || !gp->u || !gp->v || !gp->partials || gp->n_obj <= 0 ||
+      gp->n_inst < 0 || gp->nblk_obj <= 0 || gp->nblk_obj > kMaxBlocks || gp->nblk_net <= 0 ||
+      gp->nblk_net > kMaxBlocks || gp->nblk_dens < 1 || gp->n_macro < 0 ||
+      gp->n_macro + gp->nblk_dens > kMaxBlocks) {
     set_error("invalid p3d_gp descriptor");
     return true;
   }
@@ -403,7 +407,8 @@ int p3d_gp_evaluate(const p3d_gp* gp, double lam, double gamma, void* stream) {
 }
 
 int p3d_gp_density_fx(const p3d_gp* gp, int64_t* out, void* stream) {
-  if (!gp || !out) { set_error("gp_density_fx: null argument"); return P3D_ERR_ARG; }
+  if (bad_gp(gp)) return P3D_ERR_ARG;
+  if (!out) { set_error("gp_density_fx: null argument"); return P3D_ERR_ARG; }
   return gp_density_fx(*gp, out, STREAM(stream));
 }
 

@@ -11,6 +11,15 @@
 
 namespace p3d {
 
+// one-time per-device setup (function attributes, side streams) is keyed by
+// the current device: cudaFuncSetAttribute and streams are per context
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 ? 0 : (d >= kMaxDevices ? kMaxDevices - 1 : d);
+}
+
 constexpr int kFxBits = 40;  // fixed-point density: 2^-40 per unit density
 
 // ---------------------------------------------------------------------------

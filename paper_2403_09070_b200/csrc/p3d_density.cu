@@ -121,6 +121,11 @@ __device__ __forceinline__ bool resort_now(const TileSort& ts) {
   if (!ts.perm || !ts.it || ts.every <= 1) return true;
   return !*(volatile const int32_t*)ts.valid || (*ts.it % ts.every) == 0;
 }
+// the decision as the histogram pass took it (place / scatter: valid may have
+// been set by then, so they must not re-evaluate resort_now)
+__device__ __forceinline__ bool resort_decided(const TileSort& ts) {
+  return ts.decision ? *(volatile const int32_t*)ts.decision != 0 : resort_now(ts);
+}
 
 // K2 step 1: per-object tile of the centre + tile histogram; the last block
 // scans the histogram.  The first n_macro * kMacroSplit blocks scatter the macros
@@ -162,7 +167,11 @@ __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_gri
     for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x)
       if (sh_hist[t]) atomicAdd(&ts.hist[t], sh_hist[t]);
   }
-  if (last_block_all(ts.counter) && resort_now(ts)) scan_tiles(ts);
+  if (last_block_all(ts.counter)) {
+    const bool sort = resort_now(ts);
+    if (ts.decision && threadIdx.x == 0) *ts.decision = sort;
+    if (sort) scan_tiles(ts);
+  }
 }
 
 // Stable-per-block placement: each CTA ranks its objects per tile in shared
@@ -176,7 +185,7 @@ __global__ void __launch_bounds__(256) tile_place_kernel(Cloud cl, int n, TileSo
                                                         const int* halt) {
   pdl_wait();
   if (halt && *halt) return;
-  const bool sorting = resort_now(ts);
+  const bool sorting = resort_decided(ts);
 #if P3D_SCATTER_DIRECT
   if (!sorting) return;  // the scatter reads the objects through perm itself
 #endif
@@ -337,7 +346,7 @@ __global__ void __launch_bounds__(256) scatter_tiled_kernel(p3d_grid g, TileSort
                                                            const int* halt) {
   pdl_wait();
   if (halt && *halt) return;
-  const bool direct = !resort_now(ts);
+  const bool direct = !resort_decided(ts);
   extern __shared__ unsigned int sbin32[];
   __shared__ int box[4];
   const int total = ts.start[ts.n_tiles];
@@ -409,7 +418,8 @@ __global__ void __launch_bounds__(256) scatter_tiled_kernel(p3d_grid g, TileSort
 }
 
 void tiled_scatter_setup() {
-  static bool done = false;
+  static bool done_dev[kMaxDevices] = {};  // function attributes are per device
+  bool& done = done_dev[current_device()];
   if (done) return;
   cudaFuncSetAttribute(scatter_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kBoxBins * 8);

@@ -167,6 +167,8 @@ struct TileSort {
   // point, so any record order gives the same map bit for bit.
   int32_t* perm;          // [n_obj] (null: sort every call)
   int32_t* valid;         // [1] set once perm holds a sort
+  int32_t* decision;      // [1] this iteration's sort decision, written once by the
+                          // histogram kernel's last block (place / scatter read it)
   const int32_t* it;      // the loop's iteration counter (null: sort every call)
   int every;
 };

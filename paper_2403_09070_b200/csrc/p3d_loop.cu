@@ -653,9 +653,11 @@ static void scatter_k2(const p3d_gp& gp, const int* halt, cudaStream_t s) {
     ts.i0 = gp.sh_i0;
     ts.ni = gp.sh_i1 - gp.sh_i0;
     ts.f0 = gp.sh_f0;
-    // ts_order holds [n_obj] tiles, then [n_obj] perm, then the valid flag
+    // ts_order holds [n_obj] tiles, then [n_obj] perm, then the valid flag and
+    // the iteration's sort decision
     ts.perm = gp.ts_order + gp.n_obj;
     ts.valid = gp.ts_order + 2 * (long long)gp.n_obj;
+    ts.decision = ts.valid + 1;
     ts.it = &gp.st->it;
     ts.every = P3D_RESORT_EVERY;
     launch_scatter_tiled(cl, own_count(gp), gp.n_macro, gp.macro_ids, gp.grid, ts, gp.rho_fx,
@@ -712,7 +714,7 @@ static void launch_k1b(const p3d_gp& gp, cudaStream_t s) {
   // K1b owner gather (per-instance sums; L1 norms + Eq. 17 scale on one GPU)
   FusedGatherArgs ga{};
   ga.n_obj = gp.n_inst;
-  static const int gather_cap = getenv("P3D_NBLK_GATHER") ? atoi(getenv("P3D_NBLK_GATHER")) : kMaxBlocks;
+  static const int gather_cap = std::max(1, std::min(kMaxBlocks, getenv("P3D_NBLK_GATHER") ? atoi(getenv("P3D_NBLK_GATHER")) : kMaxBlocks));
   ga.blocks = grid_blocks(gp.n_inst, 256, gather_cap);
   ga.obj_slot_ptr = gp.topo.obj_slot_ptr;
   ga.in_f = reinterpret_cast<const float4*>(gp.pin_out_f);
@@ -774,9 +776,9 @@ struct ForkJoin {
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
-static ForkJoin& fork_join() {
-  static ForkJoin f;
-  return f;
+static ForkJoin& fork_join() {  // one side stream + events per device
+  static ForkJoin f[kMaxDevices];
+  return f[current_device()];
 }
 static void overlap_setup() {  // outside any capture (gp_init / gp_evaluate)
   ForkJoin& f = fork_join();

@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(256) line_pass(PassArgs a) {
 // non-captured entry points (init / per-op) so graph capture never sees it.
 void spectral_setup() {
   spectral_fast_setup();
-  static bool done = false;
+  static bool done_dev[kMaxDevices] = {};  // function attributes are per device
+  bool& done = done_dev[current_device()];
   if (!done) {
     cudaFuncSetAttribute(line_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     done = true;

@@ -655,7 +655,8 @@ bool spectral_fast_ok(const p3d_grid* g) {
 }
 
 void spectral_fast_setup() {
-  static bool done = false;
+  static bool done_dev[kMaxDevices] = {};  // function attributes are per device
+  bool& done = done_dev[current_device()];
   if (done) return;
   set_smem_attrs<3>(); set_smem_attrs<4>(); set_smem_attrs<5>(); set_smem_attrs<6>();
   set_smem_attrs<7>(); set_smem_attrs<8>(); set_smem_attrs<9>(); set_smem_attrs<10>();

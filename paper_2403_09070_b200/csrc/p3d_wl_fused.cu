@@ -1002,7 +1002,8 @@ __global__ void __launch_bounds__(32 * kGatherWarps) gather_warp_kernel(FusedGat
 }  // namespace
 
 void fused_net_setup() {
-  static bool done = false;
+  static bool done_dev[kMaxDevices] = {};  // function attributes are per device
+  bool& done = done_dev[current_device()];
   if (done) return;
   cudaFuncSetAttribute(fused_net_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(kWarpsPerBlock * sizeof(WarpCols<true>)));

@@ -87,6 +87,14 @@ class DensityGrid:
     def n_bins(self):
         return self.nx * self.ny * self.nz
 
+    @classmethod
+    def of(cls, grid):
+        """This class for any grid with the reference's (dx, dy, nx, ny, nz)
+        (e.g. place3d.density.DensityGrid, as flow.run_flow passes it)."""
+        if grid is None or isinstance(grid, cls):
+            return grid
+        return cls(grid.dx, grid.dy, grid.nx, grid.ny, grid.nz)
+
     def device(self):
         """ctypes ``p3d_grid`` + the device tables it points at (cached)."""
         if self._dev is not None:

@@ -324,10 +324,12 @@ class Gp3dProblem:
     ``cloud`` keep the reference semantics; ``run`` drives the fused loop."""
 
     def __init__(self, design, grid: dn.DensityGrid, fillers: dn.FillerSet, cfg: GpConfig, rot,
-                 max_iters=None, precision=None, shard=None):
+                 max_iters=None, precision=None, shard=None, min_step=1e-18):
         """precision: "fp64" (default; WA sums in float64 with numpy's
         operation order) or "fp32" (WA sums in float32 on anchor-relative
-        differences, the SURVEY App. B plan; faster, ~1e-7 relative)."""
+        differences, the SURVEY App. B plan; faster, ~1e-7 relative).
+        min_step: the step-underflow bound of the reference's
+        NesterovOptimizer (gp.py:188, default 1e-18)."""
         _lib.require_cuda()
         import os
 
@@ -361,6 +363,7 @@ class Gp3dProblem:
                       np.where(up, self.h_top, self.h_bot))
         self.movable_volume = float((wv * hv).sum() * grid.dz / 2)
         self.max_iters = int(cfg.max_iters if max_iters is None else max_iters)
+        self.min_step = float(min_step)
         # shard: None (fused single-GPU loop) or (rank, world) for shard.ShardedGp3d
         self.sharded = shard is not None
         self.shard_rank, self.shard_size = (int(shard[0]), int(shard[1])) if shard else (0, 1)
@@ -389,7 +392,7 @@ class Gp3dProblem:
         g.sh_f0, g.sh_f1 = self.sh_f
         macro_ids = macro_ids[(macro_ids >= self.sh_i[0]) & (macro_ids < self.sh_i[1])]
         g.n_macro = len(macro_ids)
-        if g.n_macro >= K_MAX_BLOCKS:
+        if g.n_macro + 1 > K_MAX_BLOCKS:  # K4 runs n_macro + nblk_dens (>= 1) CTAs
             raise ValueError(f"{g.n_macro} macros exceed the per-launch CTA budget {K_MAX_BLOCKS}")
         mi = max(self.max_iters, 1)
         g.max_iters = self.max_iters
@@ -454,7 +457,7 @@ class Gp3dProblem:
         g.mu_min, g.mu_max = cfg.mu_min, cfg.mu_max
         g.gamma0 = cfg.gamma_start_factor * grid.db
         g.gamma1 = cfg.gamma_end_factor * grid.db
-        g.min_step = 1e-18
+        g.min_step = self.min_step
         g.step_scale = grid.wb
         g.rho_t_fx = int(np.rint(cfg.target_density * np.ldexp(1.0, dn.FX_BITS)))
         z = lambda n: torch.zeros(max(int(n), 1), dtype=torch.float64, device="cuda")  # noqa: E731
@@ -474,8 +477,9 @@ class Gp3dProblem:
         tx, ty = -(-grid.nx // 16), -(-grid.ny // 16)  # kTile in p3d_density.cu
         nt = tx * ty
         i32z = lambda n: torch.zeros(max(int(n), 1), dtype=torch.int32, device="cuda")  # noqa: E731
-        # ts_order: [O] tiles, [O] sort permutation, [1] permutation-valid flag
-        self.t_ts = [i32z(O), i32z(nt), i32z(nt + 1), i32z(nt), i32z(2 * O + 1)]
+        # ts_order: [O] tiles, [O] sort permutation, [1] permutation-valid flag, [1] the
+        # iteration's sort decision
+        self.t_ts = [i32z(O), i32z(nt), i32z(nt + 1), i32z(nt), i32z(2 * O + 2)]
         g.ts_n_tiles, g.ts_tiles_x, g.ts_tiles_y = nt, tx, ty
         # footprint reach past the centre tile, in bins (+2: centre-bin rounding)
         cell = ~arr.is_macro
@@ -489,7 +493,7 @@ class Gp3dProblem:
         g.ts_rec = keep(self.t_ts_rec)
         self.t_spec = z(6 * B)
         self.t_maps = z(4 * B)
-        self.t_partials = z(16 * K_PARTIAL_STRIDE)
+        self.t_partials = z(_lib.load().p3d_gp_partials_doubles())
         self.t_st = torch.zeros(C.sizeof(_lib.LoopState), dtype=torch.uint8, device="cuda")
         self.t_log = z(4 * mi)
         self.t_hist = z(mi)
@@ -615,15 +619,18 @@ class Gp3dProblem:
 
 
 def run_gp3d(design, state: PlacementState, cfg: GpConfig, grid=None, iteration_log=None,
-             rng=None, use_graph=True, precision=None):
+             rng=None, use_graph=True, precision=None, min_step=1e-18):
     """3D global placement (gp.py:359-455) with the whole loop on the device.
-    On exit z is rounded to the die planes; returns (state, GpInfo)."""
+    On exit z is rounded to the die planes; returns (state, GpInfo).
+    Extra keywords (not in the reference signature): use_graph, precision
+    (see Gp3dProblem) and min_step (NesterovOptimizer's bound, gp.py:188)."""
     rng = rng or np.random.default_rng(cfg.seed)
-    grid = grid or choose_grid(design, cfg)
+    grid = dn.DensityGrid.of(grid) or choose_grid(design, cfg)
     if state.fillers is None:
         state.fillers = make_fillers(design, grid, rng)
     state.dz = grid.dz
-    prob = Gp3dProblem(design, grid, state.fillers, cfg, state.rot, precision=precision)
+    prob = Gp3dProblem(design, grid, state.fillers, cfg, state.rot, precision=precision,
+                       min_step=min_step)
     n = prob.n_inst
     pos0 = np.zeros((prob.n_obj, 3))
     pos0[:n] = np.c_[state.x, state.y, state.z]

@@ -14,6 +14,13 @@ Writes, next to this script:
   small_log.json         60-iteration run_gp3d log rows of that design
   cfg1_log.json          config-1 (10k cells, 128x128x2) 200-iteration log rows
   cfg2_log.json          (--big) config-2 (100k cells, 256x256x2) 200-iteration rows
+  cfg3_rows.json         (--cfg3) config-3 (800k cells, 512x512x2): the first 25 rows
+                         of the 200-iteration schedule (the bench's workload) and
+                         every row of the 20-iteration schedule
+  exits.json             (--exits) the three early exits of run_gp3d (gp.py:390-393
+                         non-finite, :414-422 divergence, :438-441 step underflow)
+                         and a second pass with rotated macros (flow.py:121-122)
+  flow_small.json        (--flow) place3d.flow.run_flow end to end (3D and 2D paths)
 The reference is never imported at test time or on the GPU box.
 """
 
@@ -44,7 +51,167 @@ SPECS = {
     "small": dict(n_insts=2000, n_macros=6, r_ma=0.30, seed=3, nets_per_inst=1.2),
     "cfg1": dict(n_insts=10_008, n_macros=8, r_ma=0.30, seed=1, nets_per_inst=1.2),
     "cfg2": dict(n_insts=100_032, n_macros=32, r_ma=0.30, seed=1, nets_per_inst=1.1),
+    "cfg3": dict(n_insts=800_064, n_macros=64, r_ma=0.30, seed=1, nets_per_inst=1.0625),
+    # the reference's own end-to-end designs (test_acceptance.py:329-360)
+    "flow3d": dict(n_insts=200, n_macros=3, r_ma=0.45, seed=1, fill_fraction=0.72),
+    "flow2d": dict(n_insts=120, n_macros=5, r_ma=0.88, seed=7, fill_fraction=0.75),
 }
+
+
+class _StopAfter(list):
+    """iteration_log that ends run_gp3d after n rows (the rows of a long
+    schedule's prefix, without running the whole schedule)."""
+
+    class Done(Exception):
+        pass
+
+    def __init__(self, n):
+        super().__init__()
+        self.n = n
+
+    def append(self, row):
+        super().append(row)
+        if len(self) >= self.n:
+            raise _StopAfter.Done()
+
+
+def _rows(rows):
+    return [[int(r[0]), float(r[1]), int(r[2]), float(r[3])] for r in rows]
+
+
+def cfg3_rows():
+    d = design_of("cfg3")
+    out = {"spec": SPECS["cfg3"], "grid": 512, "nz": 2}
+    cfg, rng, grid, st = setup(d, 512, 2, 200)
+    rows = _StopAfter(25)
+    t = time.perf_counter()
+    try:
+        rgp.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+    except _StopAfter.Done:
+        pass
+    out["sched200_first25"] = _rows(rows)
+    out["sched200_seconds_1core"] = time.perf_counter() - t
+    cfg, rng, grid, st = setup(d, 512, 2, 20)
+    rows = []
+    _, info = rgp.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+    out["sched20"] = _rows(rows)
+    out["sched20_info"] = [info.iterations, info.final_overflow, bool(info.diverged),
+                           info.wirelength, info.hbt_count]
+    with open(os.path.join(HERE, "cfg3_rows.json"), "w") as fh:
+        json.dump(out, fh, indent=0)
+
+
+def _state_digest(st):
+    return {"x": [float(st.x.sum()), float(st.x.min()), float(st.x.max())],
+            "y": [float(st.y.sum()), float(st.y.min()), float(st.y.max())],
+            "z": [float(st.z.sum())],
+            "fx": [float(st.fillers.x.sum())], "fy": [float(st.fillers.y.sum())]}
+
+
+# the early exits, each provoked through a GpConfig knob the reference reads
+EXIT_CASES = {
+    # NesterovOptimizer(min_step=1.5) (gp.py:188; run_gp3d uses the default
+    # 1e-18, which no GpConfig knob reaches): the BB step of this design falls
+    # from ~3 to ~0.5 over 60 iterations and first drops to <= 1.5 at the 29th
+    "step_underflow": dict(min_step=1.5),
+    # mu >= 1e200 per iteration: lambda overflows to inf by iteration 2
+    "nonfinite": dict(mu_min=1e200, mu_max=1e200),
+    # a window of 1: the first rise of the objective beyond the mu ramp
+    "divergence": dict(divergence_window=1),
+}
+
+
+def exits():
+    out = {"spec": SPECS["small"], "grid": 64, "nz": 2, "max_iters": 60, "cases": {}}
+    for name, kw in EXIT_CASES.items():
+        kw = dict(kw)
+        min_step = kw.pop("min_step", None)
+        d = design_of("small")
+        cfg = rgp.GpConfig(seed=1, nz=2, grid_nx=64, grid_ny=64, max_iters=60,
+                           stop_overflow=0.0, **kw)
+        rng = np.random.default_rng(1)
+        grid = rgp.choose_grid(d, cfg)
+        st = rgp.init_state(d, grid, cfg, rng)
+        rows = []
+        orig = rgp.NesterovOptimizer
+        if min_step is not None:
+            rgp.NesterovOptimizer = lambda x0, project=None: orig(x0, project, min_step)
+            kw["min_step"] = min_step
+        try:
+            st, info = rgp.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+        finally:
+            rgp.NesterovOptimizer = orig
+        out["cases"][name] = {
+            "cfg": {k: v for k, v in kw.items()}, "rows": _rows(rows),
+            "info": [info.iterations, info.final_overflow, bool(info.diverged),
+                     info.wirelength, info.hbt_count],
+            "state": _state_digest(st)}
+    # second pass with rotated macros (flow.py:121-122 runs run_gp3d again
+    # after rt.apply_rotation): every quarter turn, from the first pass's state
+    d = design_of("small")
+    cfg, rng, grid, st = setup(d, 64, 2, 30)
+    rows1 = []
+    st, _ = rgp.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows1, rng=rng)
+    mids = np.flatnonzero(d.arrays().is_macro)
+    st.rot = np.zeros(d.n_insts, dtype=int)
+    st.rot[mids] = (np.arange(len(mids)) % 3) + 1
+    rows = []
+    st, info = rgp.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+    out["rotated_second_pass"] = {
+        "max_iters": 30, "rot": st.rot[mids].tolist(), "rows_first": _rows(rows1),
+        "rows": _rows(rows),
+        "info": [info.iterations, info.final_overflow, bool(info.diverged), info.wirelength,
+                 info.hbt_count],
+        "state": _state_digest(st)}
+    with open(os.path.join(HERE, "exits.json"), "w") as fh:
+        json.dump(out, fh, indent=0)
+
+
+def _perturbed_flow(args):
+    """run_flow with the density force perturbed by 1e-15 relative noise
+    (the trajectory's own last-bit sensitivity, as in _perturbed_run)."""
+    name, iters, seed = args
+    from place3d.flow import run_flow
+
+    rs = np.random.default_rng(seed)
+    orig = rdn.density_force
+
+    def noisy(*a, **k):
+        g = orig(*a, **k)
+        return g * (1 + 1e-15 * rs.standard_normal(g.shape))
+
+    rdn.density_force = noisy
+    try:
+        _, rep, rows, _ = run_flow(design_of(name), rgp.GpConfig(seed=1, max_iters=iters))
+    finally:
+        rdn.density_force = orig
+    return {"seed": seed, "n_rows": len(rows), "hpwl": rep.hpwl, "hbt_count": rep.hbt_count,
+            "final_overflow": rep.final_overflow}
+
+
+def flow_small():
+    from concurrent.futures import ProcessPoolExecutor
+
+    from place3d.flow import run_flow
+
+    out = {}
+    for name, iters in (("flow3d", 500), ("flow2d", 500)):
+        d = design_of(name)
+        t = time.perf_counter()
+        sol, rep, rows, _ = run_flow(d, rgp.GpConfig(seed=1, max_iters=iters))
+        out[name] = {"spec": SPECS[name], "max_iters": iters, "flow_path": rep.flow_path,
+                     "hpwl": rep.hpwl, "hbt_count": rep.hbt_count, "raw_score": rep.raw_score,
+                     "final_overflow": rep.final_overflow, "diverged": bool(rep.diverged),
+                     "rotation": rep.rotation, "rows": _rows(rows),
+                     "seconds": time.perf_counter() - t}
+        # the 2D flow's second pass (run_gp2d_multi) is chaotic on this
+        # design: its end state under last-bit perturbations is the gate
+        if name == "flow2d":
+            with ProcessPoolExecutor(max_workers=8) as ex:
+                out[name]["band"] = list(ex.map(_perturbed_flow,
+                                                [(name, iters, s) for s in range(1, 9)]))
+    with open(os.path.join(HERE, "flow_small.json"), "w") as fh:
+        json.dump(out, fh, indent=0)
 
 
 def digest(a):
@@ -176,6 +343,10 @@ if __name__ == "__main__":
     if "--band" in sys.argv:
         band("cfg2", 256, "cfg2_band.json")
         sys.exit(0)
+    for flag, fn in (("--cfg3", cfg3_rows), ("--exits", exits), ("--flow", flow_small)):
+        if flag in sys.argv:
+            fn()
+            sys.exit(0)
     checksums()
     small_ops()
     loop_rows("cfg1", 128, "cfg1_log.json")

@@ -155,3 +155,34 @@ def test_loop_other_grids_vs_oracle(grid_n, nz):
     assert len(rows) == len(orows) == 20
     for r, o in zip(rows, orows):
         assert r[2] == o[2] and abs(r[1] - o[1]) <= 1e-9 * abs(o[1]) and abs(r[3] - o[3]) <= 1e-9
+
+
+def test_cfg3_headline_config_vs_reference():
+    """Config 3 (800,064 cells, 512x512x2: the bench's workload) against rows
+    the reference itself logged (tests/golden/cfg3_rows.json, make_golden.py
+    --cfg3): the first 25 iterations of the 200-iteration schedule (what
+    bench.py times) and every iteration of a 20-iteration schedule, each row
+    within 1e-9 with identical crossing counts; the 20-iteration end state
+    within the north_star's 0.5%."""
+    from paper_2403_09070_b200 import gp as G
+    from paper_2403_09070_b200.synth import CONFIGS, cached_synth
+
+    gold = json.load(open(os.path.join(GOLD, "cfg3_rows.json")))
+    d = cached_synth(CONFIGS[3]["spec"])
+    for max_iters, ref in ((200, gold["sched200_first25"]), (20, gold["sched20"])):
+        cfg = G.GpConfig(seed=1, nz=2, grid_nx=512, grid_ny=512, max_iters=max_iters,
+                         stop_overflow=0.0)
+        rng = np.random.default_rng(1)
+        grid = G.choose_grid(d, cfg)
+        st = G.init_state(d, grid, cfg, rng)
+        rows = []
+        st, info = G.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+        got = np.array(rows[: len(ref)], dtype=float)
+        r = np.array(ref, dtype=float)
+        assert np.array_equal(got[:, 2], r[:, 2])
+        assert np.all(np.abs(got[:, 1] - r[:, 1]) <= 1e-9 * r[:, 1])
+        assert np.all(np.abs(got[:, 3] - r[:, 3]) <= 1e-9 * r[:, 3])
+    it, ovfl, div, wl, hbt = gold["sched20_info"]
+    assert info.iterations == it and not info.diverged and info.hbt_count == hbt
+    assert abs(info.wirelength - wl) <= 5e-3 * wl
+    assert abs(info.final_overflow - ovfl) <= 5e-3 * ovfl
