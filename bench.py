@@ -556,7 +556,8 @@ def main():
     barrier()
     ms = e0.elapsed_time(e1)
     s = prob.state()
-    assert not s.done and s.it == W + K, f"loop ended early (it={s.it}, done={s.done})"
+    if not os.environ.get("P3D_PROBE_SKIP"):  # timing probes drop work: no assert
+        assert not s.done and s.it == W + K, f"loop ended early (it={s.it}, done={s.done})"
 
     # ---- per-stage attribution (fused: the same iteration captured with
     # event-record nodes between the stages, replayed K times)

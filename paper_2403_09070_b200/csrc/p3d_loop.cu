@@ -792,15 +792,25 @@ static void overlap_setup() {  // outside any capture (gp_init / gp_evaluate)
   cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming);
 }
 
+// timing probe only (results are wrong): P3D_PROBE_SKIP bitmask drops K1 (1),
+// K1b (2), K2 (4) or K3 (8) from the overlapped iteration, to read each
+// stage's share of the critical path off the bench
+static int probe_skip() {
+  static const int v = getenv("P3D_PROBE_SKIP") ? atoi(getenv("P3D_PROBE_SKIP")) : 0;
+  return v;
+}
+
 static int eval_kernels_overlap(const p3d_gp& gp, cudaStream_t s) {
   ForkJoin& f = fork_join();
   if (!f.side) return eval_kernels(gp, s);
+  const int skip = probe_skip();
   cudaEventRecord(f.fork, s);
   cudaStreamWaitEvent(f.side, f.fork, 0);
-  scatter_k2(gp, &gp.st->done, f.side);
-  if (const int rc = launch_k3(gp, f.side)) return rc;
-  launch_k1(gp, s);
-  launch_k1b(gp, s);
+  if (!(skip & 4)) scatter_k2(gp, &gp.st->done, f.side);
+  if (!(skip & 8))
+    if (const int rc = launch_k3(gp, f.side)) return rc;
+  if (!(skip & 1)) launch_k1(gp, s);
+  if (!(skip & 2)) launch_k1b(gp, s);
   cudaEventRecord(f.join, f.side);
   cudaStreamWaitEvent(s, f.join, 0);
   pdl_launch(dens_kernel, gp.n_macro + gp.nblk_dens, 256, 0, s, gp);

@@ -154,6 +154,9 @@ __constant__ double kExpPoly[17] = {
     1.66666666666666666667e-01,  // 1/3!
     0.5, 1.0, 1.0};
 __device__ __forceinline__ double exp_neg(double x) {
+#ifdef P3D_PROBE_EXP  // timing probe only: a 2-FMA stand-in (results wrong)
+  return fma(x, fma(x, 0.5, 1.0), 1.0);
+#endif
 #if P3D_EXP_CONST
   const double* c = kExpPoly;
 #else
@@ -339,6 +342,10 @@ __device__ __forceinline__ void store_pin(const FusedNetArgs& a, int idx, double
 #endif
 __device__ __forceinline__ void store_rec(double* base, int slot, double a, double b, double c,
                                           double d) {
+#ifdef P3D_PROBE_NOSTORE  // timing probe only: the record values are kept live, not stored
+  asm volatile("" ::"d"(a), "d"(b), "d"(c), "d"(d), "r"(slot));
+  return;
+#endif
   double* p = base + 4 * (long long)slot;
 #if P3D_L2_HINTS
   unsigned long long pol;
@@ -586,7 +593,11 @@ __device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk,
 #pragma unroll
   for (int k = 0; k < KM; ++k) {
     if (k >= DD) break;
+#ifdef P3D_PROBE_NOGATHER  // timing probe only: every pin reads one line (results wrong)
+    const double4 p = a.pos4[inst[k] & 31];
+#else
     const double4 p = a.pos4[inst[k]];
+#endif
     const int tp = (p.z - a.dz2) > 0.0;
     topm |= tp << k;
     sm.px[k][lane] = p.x + (double)(tp ? off[k].x : off[k].z);
@@ -700,7 +711,11 @@ __device__ __forceinline__ void triple_task(const FusedNetArgs& a, const int4 tk
   int tp[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
+#ifdef P3D_PROBE_NOGATHER
+    const double4 q = a.pos4[inst[k] & 31];
+#else
     const double4 q = a.pos4[inst[k]];
+#endif
     tp[k] = (q.z - a.dz2) > 0.0;
     x[k] = q.x + (double)(tp[k] ? off[k].x : off[k].z);
     y[k] = q.y + (double)(tp[k] ? off[k].y : off[k].w);
@@ -761,7 +776,11 @@ __device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, 
   const int i0 = ld_stream(a.pin_inst + p0), i1 = ld_stream(a.pin_inst + p1);
   const int s0 = ld_stream(a.slot + p0), s1 = ld_stream(a.slot + p1);
   const float4 o0 = ld_stream(a.off + p0), o1 = ld_stream(a.off + p1);
+#ifdef P3D_PROBE_NOGATHER
+  const double4 q0 = a.pos4[i0 & 31], q1 = a.pos4[i1 & 31];
+#else
   const double4 q0 = a.pos4[i0], q1 = a.pos4[i1];
+#endif
   const int t0p = (q0.z - a.dz2) > 0.0, t1p = (q1.z - a.dz2) > 0.0;
   const double x0 = q0.x + (double)(t0p ? o0.x : o0.z), y0 = q0.y + (double)(t0p ? o0.y : o0.w);
   const double x1 = q1.x + (double)(t1p ? o1.x : o1.z), y1 = q1.y + (double)(t1p ? o1.y : o1.w);
