@@ -179,6 +179,69 @@ int p3d_gp2d_wirelength(int32_t n_net, int32_t n_pin, int32_t n_obj, const int32
                         const int32_t* obj_slot_ptr, const double* pos, double gamma,
                         double* value, double* wl_grad, double* scratch, void* stream);
 
+/* p3d_gp2d_wirelength with the smoothing gamma read from device memory
+ * (gamma_dev, the loop's schedule) and a halt flag (nullable: the loop's done
+ * flag; the kernels return at once when set), for a graph-captured loop. */
+int p3d_gp2d_wirelength_ex(int32_t n_net, int32_t n_pin, int32_t n_obj, const int32_t* net_ptr,
+                           const int32_t* pin_obj, const uint8_t* pin_top, const double* pin_ox,
+                           const double* pin_oy, const int32_t* pin_slot,
+                           const int32_t* obj_slot_ptr, const double* pos,
+                           const double* gamma_dev, const int32_t* halt, double* value,
+                           double* wl_grad, double* scratch, void* stream);
+
+/* Device-resident run_gp2d_multi loop (gp.py:640-681): the per-layer planar
+ * fields and the wirelength are computed by the entry points above; the
+ * per-layer lambda init (gp.py:643-649), the log row and stop test
+ * (gp.py:650-656), the Eq. 19 preconditioning of the current and the
+ * re-weighted previous gradient (gp.py:657-667), the Nesterov / BB step with
+ * the 2D span clamp (gp.py:668-673, 178-227, 344-348) and the per-layer mu
+ * update (gp.py:678-681) run in three kernels (p3d_gp2d_step) with all loop
+ * control in p3d_gp2d_state: one iteration is graph-capturable, and nothing
+ * is read back until the loop ends. */
+typedef struct p3d_gp2d_state {
+  int32_t it, done, diverged, converged;
+  int32_t lam_set, step_set, iterations, pad0;
+  double lam[3], prev_ovfl[3];
+  double step, a, a_new, mom, dv2_next, gamma, final_overflow, gmax;
+  uint32_t counters[8];
+} p3d_gp2d_state;
+
+typedef struct p3d_gp2d_ctl {
+  int32_t n_obj, max_iters, n_hbt, nblk;
+  const int32_t* layer;        /* [n_obj] 0 bottom, 1 top, 2 terminal layer */
+  const double *size_w, *size_h;  /* [n_obj] planar sizes (gp.py:563-566) */
+  const double* charge;        /* [n_obj] size_w * size_h * db (gp.py:640) */
+  const uint8_t* is_macro;     /* [n_obj] */
+  const double* degree;        /* [n_obj] (Eq. 19) */
+  const double* gamma_tab;     /* [max_iters] */
+  double die_w, die_h, stop_overflow, mu_min, mu_max, step_scale, min_step, pad1;
+  double *u, *v;               /* [2][n_obj] */
+  const double* wl_grad;       /* [n_obj][2] (p3d_gp2d_wirelength_ex) */
+  const double* dens_grad;     /* [n_obj][2] (p3d_gp2d_layer_force) */
+  const double* wl_value;      /* [1] */
+  const double* ovfl;          /* [3] per-layer overflow (p3d_overflow_fx) */
+  double *prev_wl, *prev_dens; /* [n_obj][2] raw gradients of the previous point */
+  double* pre;                 /* [n_obj][2] the step's preconditioned gradient */
+  double* partials;            /* >= 8 * nblk doubles */
+  double* log;                 /* [max_iters][4]: it, WL value, #HBT, worst overflow */
+  p3d_gp2d_state* st;
+} p3d_gp2d_ctl;
+
+size_t p3d_sizeof_gp2d_ctl(void);
+size_t p3d_sizeof_gp2d_state(void);
+/* state <- initial; u = v = project(pos0) (pos0 [2][n_obj]). */
+int p3d_gp2d_init(const p3d_gp2d_ctl* c, const double* pos0, void* stream);
+/* lambda init / log / stop, preconditioned BB step, projected advance. */
+int p3d_gp2d_step(const p3d_gp2d_ctl* c, void* stream);
+/* out = project(in) ([2][n_obj]; gp.py:571-575). */
+int p3d_gp2d_project(const p3d_gp2d_ctl* c, const double* in, double* out, void* stream);
+/* x[k] = pos[idx[k]], y[k] = pos[n_obj + idx[k]] (a layer's charge cloud). */
+int p3d_gp2d_layer_xy(int32_t n, const int32_t* idx, const double* pos, int32_t n_obj, double* x,
+                      double* y, const int32_t* halt, void* stream);
+/* dens_grad[idx[k]] = force[k][0:2] (density_force of a layer, gp.py:624). */
+int p3d_gp2d_layer_force(int32_t n, const int32_t* idx, const double* force, double* dens_grad,
+                         const int32_t* halt, void* stream);
+
 /* Solution score (evaluate_score, model.py:364-400): out[3] = (D2D HPWL, #HBT,
  * HPWL + hbt_cost * #HBT); n_bad[1] = nets whose crossing state disagrees with
  * their HBT (the reference's SolutionError cases).  Pins per net from

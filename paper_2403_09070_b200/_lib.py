@@ -79,6 +79,24 @@ class Gp(C.Structure):
                 ("sh_f0", I32), ("sh_f1", I32), ("shard_tot", P), ("overlap", I32),
                 ("pad2", I32)]
 
+class Gp2dState(C.Structure):
+    _fields_ = [("it", I32), ("done", I32), ("diverged", I32), ("converged", I32),
+                ("lam_set", I32), ("step_set", I32), ("iterations", I32), ("pad0", I32),
+                ("lam", D * 3), ("prev_ovfl", D * 3), ("step", D), ("a", D), ("a_new", D),
+                ("mom", D), ("dv2_next", D), ("gamma", D), ("final_overflow", D), ("gmax", D),
+                ("counters", C.c_uint32 * 8)]
+
+
+class Gp2dCtl(C.Structure):
+    _fields_ = [("n_obj", I32), ("max_iters", I32), ("n_hbt", I32), ("nblk", I32),
+                ("layer", P), ("size_w", P), ("size_h", P), ("charge", P), ("is_macro", P),
+                ("degree", P), ("gamma_tab", P), ("die_w", D), ("die_h", D),
+                ("stop_overflow", D), ("mu_min", D), ("mu_max", D), ("step_scale", D),
+                ("min_step", D), ("pad1", D), ("u", P), ("v", P), ("wl_grad", P),
+                ("dens_grad", P), ("wl_value", P), ("ovfl", P), ("prev_wl", P),
+                ("prev_dens", P), ("pre", P), ("partials", P), ("log", P), ("st", P)]
+
+
 SH_STAGES = ("NET", "GATHER", "NORMS", "SCATTER", "SPECTRAL", "DENS", "CONTROL", "STEP0",
              "STEP0_CONTROL", "ADVANCE", "NORMS_FINAL")
 
@@ -113,6 +131,14 @@ _SIGS = {
     "p3d_gp_density_fx": (I32, [P, P, P]),
     "p3d_score": (I32, [I32] + [P] * 17 + [D, D, P, P, P, P]),
     "p3d_gp2d_wirelength": (I32, [I32, I32, I32] + [P] * 8 + [D] + [P] * 4),
+    "p3d_gp2d_wirelength_ex": (I32, [I32, I32, I32] + [P] * 14),
+    "p3d_sizeof_gp2d_ctl": (C.c_size_t, []),
+    "p3d_sizeof_gp2d_state": (C.c_size_t, []),
+    "p3d_gp2d_init": (I32, [P, P, P]),
+    "p3d_gp2d_step": (I32, [P, P]),
+    "p3d_gp2d_project": (I32, [P, P, P, P]),
+    "p3d_gp2d_layer_xy": (I32, [I32, P, P, I32, P, P, P, P]),
+    "p3d_gp2d_layer_force": (I32, [I32, P, P, P, P, P]),
     "p3d_density_energy_gradient": (I32, [P, P, P, P, P, P, P, P]),
     "p3d_gp_shard_stage": (I32, [P, C.c_int, P]),
     "p3d_gp_iterate_profiled": (I32, [P, P, P]),
@@ -141,7 +167,8 @@ def load():
         fn.restype = res
         fn.argtypes = args
     for nm, st in (("topology", Topology), ("grid", Grid), ("cloud", Cloud),
-                   ("gp", Gp), ("loop_state", LoopState)):
+                   ("gp", Gp), ("loop_state", LoopState), ("gp2d_ctl", Gp2dCtl),
+                   ("gp2d_state", Gp2dState)):
         got = getattr(lib, f"p3d_sizeof_{nm}")()
         if got != C.sizeof(st):
             raise ImportError(f"ABI mismatch: sizeof(p3d_{nm}) C={got} ctypes={C.sizeof(st)}")

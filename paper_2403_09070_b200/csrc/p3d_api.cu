@@ -312,6 +312,7 @@ int p3d_gp2d_wirelength(int32_t n_net, int32_t n_pin, int32_t n_obj, const int32
   a.net_ptr = net_ptr; a.pin_obj = pin_obj; a.pin_top = pin_top;
   a.pin_ox = pin_ox; a.pin_oy = pin_oy; a.pin_slot = pin_slot; a.obj_slot_ptr = obj_slot_ptr;
   a.pos = pos; a.gamma = gamma;
+  a.gamma_ptr = nullptr; a.halt = nullptr;
   a.rec = scratch;
   a.counter = reinterpret_cast<unsigned int*>(scratch + 2 * (long long)n_pin);
   a.partials = scratch + 2 * (long long)n_pin + 8;
@@ -348,6 +349,78 @@ int p3d_score(int32_t n_net, const int32_t* net_ptr, const int32_t* pin_inst,
   if (n_net == 0) { cudaMemsetAsync(out, 0, 3 * sizeof(double), STREAM(stream)); return check_launch("score"); }
   launch_score(a, STREAM(stream));
   return check_launch("score");
+}
+
+int p3d_gp2d_wirelength_ex(int32_t n_net, int32_t n_pin, int32_t n_obj, const int32_t* net_ptr,
+                           const int32_t* pin_obj, const uint8_t* pin_top, const double* pin_ox,
+                           const double* pin_oy, const int32_t* pin_slot,
+                           const int32_t* obj_slot_ptr, const double* pos,
+                           const double* gamma_dev, const int32_t* halt, double* value,
+                           double* wl_grad, double* scratch, void* stream) {
+  if (n_net < 0 || n_pin < 0 || n_obj < 0 || !net_ptr || !pos || !value || !wl_grad || !scratch ||
+      (n_pin > 0 && (!pin_obj || !pin_top || !pin_ox || !pin_oy || !pin_slot)) || !obj_slot_ptr ||
+      !gamma_dev) {
+    set_error("gp2d_wirelength_ex: bad args");
+    return P3D_ERR_ARG;
+  }
+  Gp2dWlArgs a{};
+  a.n_net = n_net; a.n_obj = n_obj;
+  a.net_ptr = net_ptr; a.pin_obj = pin_obj; a.pin_top = pin_top;
+  a.pin_ox = pin_ox; a.pin_oy = pin_oy; a.pin_slot = pin_slot; a.obj_slot_ptr = obj_slot_ptr;
+  a.pos = pos; a.gamma = 0.0;
+  a.gamma_ptr = gamma_dev; a.halt = halt;
+  a.rec = scratch;
+  a.counter = reinterpret_cast<unsigned int*>(scratch + 2 * (long long)n_pin);
+  a.partials = scratch + 2 * (long long)n_pin + 8;
+  a.value = value;
+  launch_gp2d_wl(a, wl_grad, STREAM(stream));
+  return check_launch("gp2d_wirelength_ex");
+}
+
+size_t p3d_sizeof_gp2d_ctl(void) { return sizeof(p3d_gp2d_ctl); }
+size_t p3d_sizeof_gp2d_state(void) { return sizeof(p3d_gp2d_state); }
+
+static bool bad_gp2d(const p3d_gp2d_ctl* c) {
+  if (!c || c->n_obj < 0 || !c->st || !c->u || !c->v || !c->partials || c->nblk < 1 ||
+      c->nblk > kMaxBlocks || (c->n_obj > 0 && (!c->layer || !c->size_w || !c->size_h ||
+                                                 !c->charge || !c->is_macro || !c->degree)) ||
+      (c->max_iters > 0 && (!c->gamma_tab || !c->log)) || !c->wl_grad || !c->dens_grad ||
+      !c->wl_value || !c->ovfl || !c->prev_wl || !c->prev_dens || !c->pre) {
+    set_error("invalid p3d_gp2d_ctl descriptor");
+    return true;
+  }
+  return false;
+}
+
+int p3d_gp2d_init(const p3d_gp2d_ctl* c, const double* pos0, void* stream) {
+  if (bad_gp2d(c) || !pos0) return P3D_ERR_ARG;
+  return gp2d_init(*c, pos0, STREAM(stream));
+}
+
+int p3d_gp2d_step(const p3d_gp2d_ctl* c, void* stream) {
+  if (bad_gp2d(c)) return P3D_ERR_ARG;
+  return gp2d_step(*c, STREAM(stream));
+}
+
+int p3d_gp2d_project(const p3d_gp2d_ctl* c, const double* in, double* out, void* stream) {
+  if (bad_gp2d(c) || !in || !out) return P3D_ERR_ARG;
+  return gp2d_project(*c, in, out, STREAM(stream));
+}
+
+int p3d_gp2d_layer_xy(int32_t n, const int32_t* idx, const double* pos, int32_t n_obj, double* x,
+                      double* y, const int32_t* halt, void* stream) {
+  if (n < 0 || n_obj < 0 || (n > 0 && (!idx || !pos || !x || !y))) { set_error("gp2d_layer_xy: bad args"); return P3D_ERR_ARG; }
+  if (n == 0) return P3D_OK;
+  launch_gp2d_layer_xy(n, idx, pos, n_obj, x, y, halt, STREAM(stream));
+  return check_launch("gp2d_layer_xy");
+}
+
+int p3d_gp2d_layer_force(int32_t n, const int32_t* idx, const double* force, double* dens_grad,
+                         const int32_t* halt, void* stream) {
+  if (n < 0 || (n > 0 && (!idx || !force || !dens_grad))) { set_error("gp2d_layer_force: bad args"); return P3D_ERR_ARG; }
+  if (n == 0) return P3D_OK;
+  launch_gp2d_layer_force(n, idx, force, dens_grad, halt, STREAM(stream));
+  return check_launch("gp2d_layer_force");
 }
 
 int p3d_precondition(int32_t n, const double* gr, double lam, const double* q, const double* deg,

@@ -120,12 +120,21 @@ struct Gp2dWlArgs {
   const int32_t* obj_slot_ptr; // [n_obj+1]
   const double* pos;           // [2][n_obj]
   double gamma;
+  const double* gamma_ptr;     // nullable: gamma from device memory (graph-captured loop)
+  const int32_t* halt;         // nullable: return at once when set
   double* rec;                 // [n_pin][2] per-pin gradients by slot
   double* partials;            // [blocks]
   unsigned int* counter;
   double* value;               // 1 double: sum over segments of the WA spans
 };
 void launch_gp2d_wl(const Gp2dWlArgs& a, double* wl_grad, cudaStream_t s);
+int gp2d_init(const p3d_gp2d_ctl& c, const double* pos0, cudaStream_t s);
+int gp2d_step(const p3d_gp2d_ctl& c, cudaStream_t s);
+int gp2d_project(const p3d_gp2d_ctl& c, const double* in, double* out, cudaStream_t s);
+void launch_gp2d_layer_xy(int n, const int32_t* idx, const double* pos, int n_obj, double* x,
+                          double* y, const int32_t* halt, cudaStream_t s);
+void launch_gp2d_layer_force(int n, const int32_t* idx, const double* force, double* dens_grad,
+                             const int32_t* halt, cudaStream_t s);
 
 // solution score (p3d_score.cu)
 struct ScoreArgs {

@@ -11,16 +11,21 @@ the reference; the per-iteration work runs on the device:
   of every (net, die) segment of the augmented pin list and its owner sums;
 * density per layer: the K2 fixed-point scatter, the K3 spectral solve and
   the K4 force gather of the 3D path, on an nz = 1 grid (density.py API);
-* preconditioner (Eq. 19) and the Nesterov / BB step of the drop-in
-  ``NesterovOptimizer`` with the 2D span clamp as projection.
+* loop control (``p3d_gp2d_step``): per-layer lambda init, the log row and
+  the stop test, the Eq. 19 preconditioning of the current and the
+  re-weighted previous gradient, the Nesterov / BB step with the 2D span
+  clamp as projection, the step-underflow exit and the per-layer mu update,
+  with every scalar in a device-resident ``p3d_gp2d_state``.
 
-Host work is setup only (partition, augmented pin list, fillers with the
-reference's numpy RNG stream) plus one overflow scalar read per iteration for
-the stop test, as in the reference loop.
+One iteration is captured as a CUDA graph and replayed; the host polls the
+done flag every few replays and reads the log rows once at the end.  Host
+work is setup only (partition, augmented pin list, fillers with the
+reference's numpy RNG stream).
 """
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 
 import numpy as np
@@ -29,8 +34,7 @@ import torch
 from . import _dev, _lib
 from . import density as dn
 from . import wirelength as wl
-from .gp import (GpConfig, GpInfo, NesterovOptimizer, StepUnderflow, gamma_schedule,
-                 lambda_init, mu_from_overflow, precondition)
+from .gp import GpConfig, GpInfo, gamma_schedule
 from .model import partition_from_z, rotate_offsets, rotated_dims
 
 
@@ -139,6 +143,9 @@ class _Layer:
                                     h=sh[idx].contiguous(), dep=full(grid.dz),
                                     weight=_dev.f64(weight), is_macro=np.asarray(is_macro))
         self.dc = dn._DevCloud(self.cloud)
+        # the cloud's x / y are the buffers refreshed below
+        self.dc.struct.x = _lib.ptr(self.x).value
+        self.dc.struct.y = _lib.ptr(self.y).value
         self.g, _ = grid.device()
         B = grid.n_bins
         self.rho_fx = torch.zeros(B, dtype=torch.int64, device="cuda")
@@ -149,11 +156,13 @@ class _Layer:
         self.energy = torch.zeros(1, dtype=torch.float64, device="cuda")
         self.gscr = _dev.scratch(8 + self.dc.struct.n_macro + 1024 + 8)
         self.oscr = _dev.scratch(8 + 1024 + 8)
+        self.idx32 = idx.to(torch.int32).contiguous()
 
-    def run(self, p, dens_grad, ovfl_out):
-        torch.index_select(p[:, 0], 0, self.idx, out=self.x)
-        torch.index_select(p[:, 1], 0, self.idx, out=self.y)
+    def enqueue(self, pos_soa, n_obj, dens_grad, ovfl_out, halt):
+        """gp.py:610-626 for this layer at pos_soa [2][n_obj] (stream-ordered)."""
         g, s = _lib.byref(self.g), _lib.stream_ptr()
+        _lib.call("p3d_gp2d_layer_xy", self.n, _lib.ptr(self.idx32), _lib.ptr(pos_soa), int(n_obj),
+                  _lib.ptr(self.x), _lib.ptr(self.y), _lib.ptr(halt), s)
         self.rho_fx.zero_()
         _lib.call("p3d_accumulate_density", g, _lib.byref(self.dc.struct), _lib.ptr(self.rho_fx), s)
         _lib.call("p3d_fx_to_density", int(self.rho.numel()), _lib.ptr(self.rho_fx),
@@ -162,16 +171,140 @@ class _Layer:
                   _lib.ptr(self.spec), s)
         _lib.call("p3d_density_gather", g, _lib.byref(self.dc.struct), _lib.ptr(self.maps), None,
                   _lib.ptr(self.energy), _lib.ptr(self.force), _lib.ptr(self.gscr), s)
-        dens_grad[self.idx] = self.force[:, :2]
+        _lib.call("p3d_gp2d_layer_force", self.n, _lib.ptr(self.idx32), _lib.ptr(self.force),
+                  _lib.ptr(dens_grad), _lib.ptr(halt), s)
         _lib.call("p3d_overflow_fx", g, _lib.ptr(self.rho_fx), float(self.rho_t), float(self.mv),
                   _lib.ptr(ovfl_out), _lib.ptr(self.oscr), s)
 
 
-def run_gp2d_multi(design, state, cfg: GpConfig, iteration_log=None, rng=None):
+class Gp2dLoop:
+    """The device-resident iteration of run_gp2d_multi (gp.py:640-681): the
+    wirelength, the three layers and ``p3d_gp2d_step`` enqueued on one stream
+    (graph-capturable); every loop scalar lives in ``p3d_gp2d_state``."""
+
+    def __init__(self, prob, dp, layers, n_obj, size_w, size_h, obj_layer, is_macro_obj,
+                 degree_obj, charges, grid0, cfg, die):
+        self.prob, self.dp, self.layers, self.n_obj = prob, dp, layers, n_obj
+        keep = self._keep = _dev.Keep()
+        mi = max(int(cfg.max_iters), 1)
+        z = lambda n: torch.zeros(max(int(n), 1), dtype=torch.float64, device="cuda")  # noqa: E731
+        self.u, self.v = z(2 * n_obj), z(2 * n_obj)
+        self.wl_grad, self.dens_grad = z(2 * n_obj), z(2 * n_obj)
+        self.prev_wl, self.prev_dens, self.pre = z(2 * n_obj), z(2 * n_obj), z(2 * n_obj)
+        self.value, self.ovfl = z(1), z(3)
+        self.log = z(4 * mi)
+        self.wl_scr = _dev.scratch(2 * dp["n_pin"] + 8 + 1024)
+        self.st = torch.zeros(C.sizeof(_lib.Gp2dState), dtype=torch.uint8, device="cuda")
+        self._st_host = torch.empty(C.sizeof(_lib.Gp2dState), dtype=torch.uint8, pin_memory=True)
+        n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        c = self.ctl = _lib.Gp2dCtl()
+        c.n_obj, c.max_iters, c.n_hbt = int(n_obj), int(cfg.max_iters), int(prob.n_hbt)
+        c.nblk = max(1, min(-(-max(n_obj, 1) // 256), 2 * n_sm, 2048))
+        c.layer = keep(_dev.i32(obj_layer))
+        c.size_w, c.size_h = keep(_dev.f64(size_w)), keep(_dev.f64(size_h))
+        c.charge = keep(_dev.f64(charges))
+        c.is_macro = keep(_dev.u8(is_macro_obj))
+        c.degree = keep(_dev.f64(degree_obj))
+        gam = [gamma_schedule(grid0, it, cfg.max_iters, cfg) for it in range(mi)]
+        c.gamma_tab = keep(_dev.f64(np.asarray(gam, dtype=np.float64)))
+        c.die_w, c.die_h = float(die.width), float(die.height)
+        c.stop_overflow, c.mu_min, c.mu_max = cfg.stop_overflow, cfg.mu_min, cfg.mu_max
+        c.step_scale, c.min_step = grid0.wb, 1e-18
+        for name in ("u", "v", "wl_grad", "dens_grad", "prev_wl", "prev_dens", "pre", "log"):
+            setattr(c, name, keep(getattr(self, name)))
+        c.wl_value, c.ovfl = keep(self.value), keep(self.ovfl)
+        c.partials = keep(_dev.scratch(8 * c.nblk + 8))
+        c.st = keep(self.st)
+        # p3d_gp2d_state field offsets of gamma / done (the WL kernel and the
+        # layer kernels read them straight from device memory)
+        self.gamma_ptr = self.st[_lib.Gp2dState.gamma.offset:].view(torch.float64)[:1] \
+            if _lib.Gp2dState.gamma.offset % 8 == 0 else None
+        self.halt = self.st[_lib.Gp2dState.done.offset:].view(torch.int32)[:1]
+
+    def state(self):
+        self._st_host.copy_(self.st)
+        return _lib.Gp2dState.from_buffer_copy(bytes(self._st_host.numpy()))
+
+    def init(self, pos0_soa):
+        _lib.call("p3d_gp2d_init", _lib.byref(self.ctl), _lib.ptr(pos0_soa), _lib.stream_ptr())
+
+    def iterate(self):
+        """One iteration (gp.py:641-681), stream-ordered, no host sync."""
+        dp, n_obj = self.dp, self.n_obj
+        _lib.call("p3d_gp2d_wirelength_ex", int(len(self.prob.net_ptr) - 1), int(dp["n_pin"]),
+                  int(n_obj), _lib.ptr(dp["net_ptr"]), _lib.ptr(dp["pin_obj"]),
+                  _lib.ptr(dp["pin_top"]), _lib.ptr(dp["pin_ox"]), _lib.ptr(dp["pin_oy"]),
+                  _lib.ptr(dp["pin_slot"]), _lib.ptr(dp["obj_slot_ptr"]), _lib.ptr(self.v),
+                  _lib.ptr(self.gamma_ptr), _lib.ptr(self.halt), _lib.ptr(self.value),
+                  _lib.ptr(self.wl_grad), _lib.ptr(self.wl_scr), _lib.stream_ptr())
+        for layer, ctx in enumerate(self.layers):
+            if ctx.n:
+                ctx.enqueue(self.v, n_obj, self.dens_grad, self.ovfl[layer:layer + 1], self.halt)
+        _lib.call("p3d_gp2d_step", _lib.byref(self.ctl), _lib.stream_ptr())
+
+    def capture(self):
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+            self.iterate()
+        torch.cuda.current_stream().wait_stream(s)
+        return g
+
+    def run(self, pos0_soa, use_graph=True, poll_every=8):
+        self.init(pos0_soa)
+        total = int(self.ctl.max_iters)
+        if use_graph and total > 0:
+            self.iterate()  # warm-up outside capture (first-use allocations)
+            self.init(pos0_soa)
+            g = self.capture()
+            for r in range(total):
+                g.replay()
+                if (r + 1) % poll_every == 0 and self.state().done:
+                    break
+        else:
+            for r in range(total):
+                self.iterate()
+                if (r + 1) % poll_every == 0 and self.state().done:
+                    break
+        return self.state()
+
+    def log_rows(self, n):
+        rows = self.log[: 4 * n].reshape(n, 4).cpu().numpy()
+        return [(int(r[0]), float(r[1]), int(r[2]), float(r[3])) for r in rows]
+
+    def project(self, soa):
+        out = torch.empty_like(soa)
+        _lib.call("p3d_gp2d_project", _lib.byref(self.ctl), _lib.ptr(soa), _lib.ptr(out),
+                  _lib.stream_ptr())
+        return out
+
+
+def run_gp2d_multi(design, state, cfg: GpConfig, iteration_log=None, rng=None, use_graph=True):
     """Planar refinement with a fixed partition (gp.py:531-690); returns
-    (state, GpInfo, {crossing net: HBT centre})."""
-    _lib.require_cuda()
+    (state, GpInfo, {crossing net: HBT centre}).  use_graph (not in the
+    reference signature): replay one captured iteration (default) or enqueue
+    each iteration eagerly."""
     rng = rng or np.random.default_rng(cfg.seed)
+    loop, pos0 = setup_gp2d(design, state, cfg, rng)
+    prob, n_obj = loop.prob, loop.n_obj
+    st = loop.run(pos0, use_graph=use_graph)
+    info = GpInfo(iterations=int(st.iterations), final_overflow=float(st.final_overflow),
+                  diverged=bool(st.diverged))
+    if iteration_log is not None:
+        iteration_log.extend(loop.log_rows(int(st.iterations)))
+    final = loop.project(loop.u).reshape(2, n_obj).t().cpu().numpy()
+    state.x = final[: prob.n_inst, 0].copy()
+    state.y = final[: prob.n_inst, 1].copy()
+    hbt_centers = {int(j): (float(final[prob.n_inst + t, 0]), float(final[prob.n_inst + t, 1]))
+                   for t, j in enumerate(prob.crossing)}
+    return state, info, hbt_centers
+
+
+def setup_gp2d(design, state, cfg: GpConfig, rng):
+    """Host setup of run_gp2d_multi (gp.py:531-639, the reference's RNG draws):
+    returns (Gp2dLoop, initial positions [2][n_obj] on the device)."""
+    _lib.require_cuda()
     delta = partition_from_z(state.z, state.dz)
     prob = Gp2dProblem(design, cfg, delta, state.rot, gp2d_grid_n(design.n_insts))
     die = design.die
@@ -211,88 +344,19 @@ def run_gp2d_multi(design, state, cfg: GpConfig, iteration_log=None, rng=None):
     is_filler = np.r_[np.zeros(n_core, bool), np.ones(len(fx), bool)]
     movable_vol = [float((size_w[m] * size_h[m]).sum() * grids[l].db)
                    for l, m in enumerate([(obj_layer == l) & ~is_filler for l in range(3)])]
+    charges = size_w * size_h * grids[0].db
 
-    # ---- device constants
     dp = prob.device_pins(n_obj)
     sw, sh = _dev.f64(size_w), _dev.f64(size_h)
-
-    def bounds(size, extent):  # gp.py:344-348 per object
-        lo, hi = size / 2, extent - size / 2
-        return torch.minimum(lo, hi), torch.maximum(lo, hi), lo <= hi, \
-            torch.minimum(lo, hi) + (hi - lo).abs() / 2
-
-    bx, by = bounds(sw, die.width), bounds(sh, die.height)
-
-    def project(p):
-        out = p.clone()
-        for c, (lo, hi, ok, mid) in ((0, bx), (1, by)):
-            out[:, c] = torch.where(ok, torch.minimum(torch.maximum(p[:, c], lo), hi), mid)
-        return out
-
     layer_idx = [torch.from_numpy(np.flatnonzero(obj_layer == l)).cuda() for l in range(3)]
     layers = [_Layer(grids[l], layer_idx[l], sw, sh,
                      np.where(is_macro_obj[obj_layer == l], cfg.target_density, 1.0),
                      is_macro_obj[obj_layer == l], movable_vol[l], cfg.target_density)
               for l in range(3)]
-
-    def evaluate(p, gamma):
-        """gp.py:586-626: WL value/grads + per-layer raw density grads/overflow
-        (one host read per iteration: the WL value and the three overflows)."""
-        pos_soa = p.t().contiguous()
-        val, wl_grad = gp2d_wirelength(prob, dp, pos_soa, n_obj, gamma)
-        dens_grad = torch.zeros((n_obj, 2), dtype=torch.float64, device="cuda")
-        ov = torch.zeros(4, dtype=torch.float64, device="cuda")
-        ov[3:4].copy_(val)
-        for layer, ctx in enumerate(layers):
-            if ctx.n:
-                ctx.run(p, dens_grad, ov[layer:layer + 1])
-        host = ov.cpu().tolist()
-        return host[3], wl_grad, dens_grad, host[:3]
-
-    opt = NesterovOptimizer(_dev.f64(pos), project=project)
-    info = GpInfo()
-    lams = None
-    charges = sw * sh * grids[0].db
-    lay = torch.from_numpy(obj_layer).cuda()
-    prev = [math.inf] * 3
-    prev_raw = None
-    for it in range(cfg.max_iters):
-        gamma = gamma_schedule(grids[0], it, cfg.max_iters, cfg)
-        val, wl_grad, dens_grad, ovfls = evaluate(opt.v, gamma)
-        if lams is None:
-            lams = [lambda_init(float(wl_grad[layer_idx[l]].abs().sum().item()),
-                                float(dens_grad[layer_idx[l]].abs().sum().item()))
-                    for l in range(3)]
-        worst = max(ovfls)
-        info.iterations = it + 1
-        info.final_overflow = worst
-        if iteration_log is not None:
-            iteration_log.append((it, val, prob.n_hbt, worst))
-        if worst <= cfg.stop_overflow:
-            break
-        lam_obj = torch.tensor(lams, dtype=torch.float64, device="cuda")[lay]
-        total = wl_grad + lam_obj[:, None] * dens_grad
-        pre, _ = precondition(total, 1.0, lam_obj * charges, degree_obj, is_macro_obj)
-        pre_prev = None
-        if prev_raw is not None:
-            pre_prev, _ = precondition(prev_raw[0] + lam_obj[:, None] * prev_raw[1], 1.0,
-                                       lam_obj * charges, degree_obj, is_macro_obj)
-        prev_raw = (wl_grad, dens_grad)
-        try:
-            opt.advance(pre, step_scale=grids[0].wb, g_prev_reval=pre_prev)
-        except StepUnderflow:
-            info.diverged = True
-            break
-        for layer in range(3):
-            lams[layer] *= mu_from_overflow(prev[layer], ovfls[layer], cfg)
-            prev[layer] = ovfls[layer]
-
-    final = project(opt.u).cpu().numpy()
-    state.x = final[: prob.n_inst, 0].copy()
-    state.y = final[: prob.n_inst, 1].copy()
-    hbt_centers = {int(j): (float(final[prob.n_inst + t, 0]), float(final[prob.n_inst + t, 1]))
-                   for t, j in enumerate(prob.crossing)}
-    return state, info, hbt_centers
+    loop = Gp2dLoop(prob, dp, layers, n_obj, size_w, size_h, obj_layer, is_macro_obj,
+                    degree_obj, charges, grids[0], cfg, die)
+    return loop, _dev.f64(pos).t().contiguous()
 
 
-__all__ = ["Gp2dProblem", "gp2d_grid_n", "gp2d_wirelength", "run_gp2d_multi"]
+__all__ = ["Gp2dProblem", "Gp2dLoop", "gp2d_grid_n", "gp2d_wirelength", "run_gp2d_multi",
+           "setup_gp2d"]

