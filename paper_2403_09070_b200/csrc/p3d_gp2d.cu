@@ -2,9 +2,9 @@
 // partial-net weighted-average wirelength over the augmented pin list (each
 // HBT joins both partial nets of its crossing net, gp.py:482-498) and its
 // per-object owner sums.  Compiled with -fmad=false and written in numpy's
-// operation order (wirelength.py:76-98) so values and gradients round like
-// the reference's _segment_wa (exp itself is CUDA's correctly-rounded-to-1-ulp
-// exp, numpy's is SVML/glibc: <= 1 ulp apart).
+// operation order (wirelength.py:76-98) up to hoisted reciprocals (1/gamma and
+// the per-segment 1/s1p, 1/s1m: <= 1 ulp per quotient) and a <= 1.2 ulp
+// polynomial exp (numpy's exp is itself <= 1 ulp).
 #include <math.h>
 
 #include "p3d_common.cuh"
@@ -14,34 +14,85 @@ namespace p3d {
 
 namespace {
 
+// exp(x) for x <= 0 (every WA argument): Cody-Waite reduction by ln 2 and a
+// degree-13 Taylor polynomial (<= 1.2 ulp over [-708, 0], the same
+// evaluation as K1's exp_neg; numpy's exp is itself <= 1 ulp)
+__device__ __forceinline__ double exp_nonpos(double x) {
+  const double n = rint(x * 1.4426950408889634074);
+  const double r = fma(-n, 1.9082149292705877e-10, fma(-n, 0.693147180369123816490, x));
+  double p = 1.6059043836821613e-10;
+  p = fma(p, r, 2.08767569878680989792e-09);
+  p = fma(p, r, 2.50521083854417187751e-08);
+  p = fma(p, r, 2.75573192239858906526e-07);
+  p = fma(p, r, 2.75573192239858906526e-06);
+  p = fma(p, r, 2.48015873015873015873e-05);
+  p = fma(p, r, 1.98412698412698412698e-04);
+  p = fma(p, r, 1.38888888888888888889e-03);
+  p = fma(p, r, 8.33333333333333333333e-03);
+  p = fma(p, r, 4.16666666666666666667e-02);
+  p = fma(p, r, 1.66666666666666666667e-01);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double sc = __longlong_as_double((long long)((int)n + 1023) << 52);
+  return x < -708.0 ? 0.0 : p * sc;
+}
+
 struct Seg {
-  double hi, lo, s1p, sxp, s1m, sxm, vp, vm;
+  double hi, lo, s1p, sxp, s1m, sxm, rp, rm, vp, vm;
 };
 
-// one (net, die) segment on one axis: extrema, sums in pin order
-__device__ __forceinline__ void seg_stats(const Gp2dWlArgs& a, int b, int e, int die, int axis,
-                                          double gamma, Seg& s) {
-  s.hi = -P3D_INF;
-  s.lo = P3D_INF;
+__device__ __forceinline__ double pin_coord(const Gp2dWlArgs& a, int k, int axis) {
+  return a.pos[(long long)axis * a.n_obj + a.pin_obj[k]] + (axis ? a.pin_oy[k] : a.pin_ox[k]);
+}
+
+// One net, one axis: both (net, die) segments of _segment_wa
+// (wirelength.py:76-98) in three passes over the net's pins (extrema, sums in
+// pin order, per-pin gradients), 1/gamma and the per-segment reciprocals
+// hoisted (<= 1 ulp from numpy's divisions).  Returns the two segments' value.
+__device__ __forceinline__ double net_axis(const Gp2dWlArgs& a, int b, int e, int axis,
+                                           double ig) {
+  Seg sg[2];
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    sg[d].hi = -P3D_INF;
+    sg[d].lo = P3D_INF;
+    sg[d].s1p = sg[d].sxp = sg[d].s1m = sg[d].sxm = 0.0;
+  }
   for (int k = b; k < e; ++k) {
-    if (a.pin_top[k] != die) continue;
-    const double v = a.pos[(long long)axis * a.n_obj + a.pin_obj[k]] + (axis ? a.pin_oy[k] : a.pin_ox[k]);
+    const double v = pin_coord(a, k, axis);
+    Seg& s = sg[a.pin_top[k]];
     s.hi = fmax(s.hi, v);
     s.lo = fmin(s.lo, v);
   }
-  s.s1p = s.sxp = s.s1m = s.sxm = 0.0;
   for (int k = b; k < e; ++k) {
-    if (a.pin_top[k] != die) continue;
-    const double v = a.pos[(long long)axis * a.n_obj + a.pin_obj[k]] + (axis ? a.pin_oy[k] : a.pin_ox[k]);
-    const double ep = exp((v - s.hi) / gamma), em = exp((s.lo - v) / gamma);
+    const double v = pin_coord(a, k, axis);
+    Seg& s = sg[a.pin_top[k]];
+    const double ep = exp_nonpos((v - s.hi) * ig), em = exp_nonpos((s.lo - v) * ig);
     s.s1p += ep;
     s.sxp += v * ep;
     s.s1m += em;
     s.sxm += v * em;
   }
-  const bool live = s.s1p > 0;
-  s.vp = live ? s.sxp / s.s1p : 0.0;
-  s.vm = live ? s.sxm / s.s1m : 0.0;
+  double val = 0.0;
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    Seg& s = sg[d];
+    const bool live = s.s1p > 0;
+    s.rp = live ? 1.0 / s.s1p : 0.0;
+    s.rm = live ? 1.0 / s.s1m : 0.0;
+    s.vp = live ? s.sxp * s.rp : 0.0;
+    s.vm = live ? s.sxm * s.rm : 0.0;
+    val += live ? s.vp - s.vm : 0.0;
+  }
+  for (int k = b; k < e; ++k) {  // wirelength.py:94-96
+    const Seg& s = sg[a.pin_top[k]];
+    const double v = pin_coord(a, k, axis);
+    const double ep = exp_nonpos((v - s.hi) * ig), em = exp_nonpos((s.lo - v) * ig);
+    const double g = ep * s.rp * (1 + (v - s.vp) * ig) - em * s.rm * (1 - (v - s.vm) * ig);
+    a.rec[2 * (long long)a.pin_slot[k] + axis] = g;
+  }
+  return val;
 }
 
 __global__ void __launch_bounds__(256) gp2d_wl_kernel(Gp2dWlArgs a) {
@@ -49,22 +100,11 @@ __global__ void __launch_bounds__(256) gp2d_wl_kernel(Gp2dWlArgs a) {
   __shared__ double red[32];
   double acc[1] = {0.0};
   const double gamma = a.gamma_ptr ? *a.gamma_ptr : a.gamma;
+  const double ig = 1.0 / gamma;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < a.n_net; j += gridDim.x * blockDim.x) {
     const int b = a.net_ptr[j], e = a.net_ptr[j + 1];
-    for (int axis = 0; axis < 2; ++axis) {
-      Seg sg[2];
-      for (int die = 0; die < 2; ++die) {
-        seg_stats(a, b, e, die, axis, gamma, sg[die]);
-        acc[0] += sg[die].s1p > 0 ? sg[die].vp - sg[die].vm : 0.0;
-      }
-      for (int k = b; k < e; ++k) {  // wirelength.py:94-96
-        const Seg& s = sg[a.pin_top[k]];
-        const double v = a.pos[(long long)axis * a.n_obj + a.pin_obj[k]] + (axis ? a.pin_oy[k] : a.pin_ox[k]);
-        const double ep = exp((v - s.hi) / gamma), em = exp((s.lo - v) / gamma);
-        const double g = ep / s.s1p * (1 + (v - s.vp) / gamma) - em / s.s1m * (1 - (v - s.vm) / gamma);
-        a.rec[2 * (long long)a.pin_slot[k] + axis] = g;
-      }
-    }
+    acc[0] += net_axis(a, b, e, 0, ig);
+    acc[0] += net_axis(a, b, e, 1, ig);
   }
   block_sum<1>(acc, red);
   if (threadIdx.x == 0) a.partials[blockIdx.x] = acc[0];

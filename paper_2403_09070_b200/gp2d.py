@@ -229,17 +229,29 @@ class Gp2dLoop:
         _lib.call("p3d_gp2d_init", _lib.byref(self.ctl), _lib.ptr(pos0_soa), _lib.stream_ptr())
 
     def iterate(self):
-        """One iteration (gp.py:641-681), stream-ordered, no host sync."""
+        """One iteration (gp.py:641-681), stream-ordered, no host sync.  The
+        three layers' fields are independent of each other and of the
+        wirelength: each runs on its own side stream (concurrent branches
+        of the captured graph), joined before the step."""
         dp, n_obj = self.dp, self.n_obj
+        main = torch.cuda.current_stream()
+        if not hasattr(self, "_side"):
+            self._side = [torch.cuda.Stream() for _ in self.layers]
+        for layer, (ctx, side) in enumerate(zip(self.layers, self._side)):
+            if ctx.n:
+                side.wait_stream(main)
+                with torch.cuda.stream(side):
+                    ctx.enqueue(self.v, n_obj, self.dens_grad, self.ovfl[layer:layer + 1],
+                                self.halt)
         _lib.call("p3d_gp2d_wirelength_ex", int(len(self.prob.net_ptr) - 1), int(dp["n_pin"]),
                   int(n_obj), _lib.ptr(dp["net_ptr"]), _lib.ptr(dp["pin_obj"]),
                   _lib.ptr(dp["pin_top"]), _lib.ptr(dp["pin_ox"]), _lib.ptr(dp["pin_oy"]),
                   _lib.ptr(dp["pin_slot"]), _lib.ptr(dp["obj_slot_ptr"]), _lib.ptr(self.v),
                   _lib.ptr(self.gamma_ptr), _lib.ptr(self.halt), _lib.ptr(self.value),
                   _lib.ptr(self.wl_grad), _lib.ptr(self.wl_scr), _lib.stream_ptr())
-        for layer, ctx in enumerate(self.layers):
+        for ctx, side in zip(self.layers, self._side):
             if ctx.n:
-                ctx.enqueue(self.v, n_obj, self.dens_grad, self.ovfl[layer:layer + 1], self.halt)
+                main.wait_stream(side)
         _lib.call("p3d_gp2d_step", _lib.byref(self.ctl), _lib.stream_ptr())
 
     def capture(self):

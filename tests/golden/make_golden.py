@@ -209,7 +209,7 @@ def flow_small():
         if name == "flow2d":
             with ProcessPoolExecutor(max_workers=8) as ex:
                 out[name]["band"] = list(ex.map(_perturbed_flow,
-                                                [(name, iters, s) for s in range(1, 9)]))
+                                                [(name, iters, s) for s in range(1, 25)]))
     with open(os.path.join(HERE, "flow_small.json"), "w") as fh:
         json.dump(out, fh, indent=0)
 
