@@ -258,6 +258,47 @@ int p3d_score(int32_t n_net, const int32_t* net_ptr, const int32_t* pin_inst,
               double* scratch, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* post-GP steps                                       */
+/* ------------------------------------------------------------------------ */
+/* rebalance_partition (legalize.py:464-499): moves instances off the die
+ * that overshoots its utilisation cap more, cheapest first, until both caps
+ * hold.  area_*: [n] rotated w*h per die; order_*: [n] all instances sorted
+ * by (is_macro, area on that die, index); delta [n] (bit 0: 1 top) is
+ * updated in place, bit 1 set on every instance that moved at least once.  out[4] = (status: 0 done, 1 caps unsatisfiable (LegalizationError),
+ * 2 no convergence; moves; top overshoot; bottom overshoot).  One CTA. */
+int p3d_rebalance(int32_t n, const double* area_top, const double* area_bot,
+                  const int32_t* order_top, const int32_t* order_bot, uint8_t* delta,
+                  double cap_top, double cap_bot, double* out, void* stream);
+
+/* check_solution (check.py:74-152), per-object part: inst_flags [n_inst]
+ * (bit 0 rotated cell, 1 out of the die, 2 off the row grid, 3 off the site
+ * grid), box [n_inst][4] (x0, x1, y0, y1 of the rotated outline), area[2]
+ * (per die), net_flags [n_net] (bit 0 crossing net without terminal, 1
+ * single-die net with one, 2 terminal out of the die).  x, y: lower-left
+ * corners; w/h_*: unrotated outline per die; hbt_*: per net.
+ * scratch: >= 2*2048 + 8 doubles (counter zeroed once). */
+int p3d_check_objects(int32_t n_inst, int32_t n_net, const uint8_t* die, const int32_t* rot,
+                      const double* x, const double* y, const uint8_t* is_macro,
+                      const double* w_top, const double* h_top, const double* w_bot,
+                      const double* h_bot, const int32_t* net_ptr, const int32_t* pin_inst,
+                      const uint8_t* hbt_ok, const double* hbt_x, const double* hbt_y,
+                      double die_w, double die_h, double row_top, double row_bot, double site_w,
+                      double pitch, double tol, uint8_t* inst_flags, uint8_t* net_flags,
+                      double* box, double* area, double* scratch, void* stream);
+/* Pair search over boxes [n][4] (members only) on an nbx x nby grid of
+ * `bucket`-sized buckets (check.py:47-71): phase 0 counts entries per bucket
+ * into count [nbx*nby] (zeroed); phase 1 fills list [sum count] from start
+ * [nbx*nby + 1] (exclusive scan of count; cursor = a copy of start); phase 2
+ * tests every pair of every bucket (mode 0: outlines overlap by more than
+ * 1e-9; mode 1: terminal boxes overlap and max(|dx|, |dy|) < min_cc - tol)
+ * and writes each hit once as (p, q), p < q, into out [cap][2]; n_out[1]
+ * counts all hits (may exceed cap). */
+int p3d_pair_search(int32_t phase, int32_t n, const double* box, const uint8_t* member,
+                    double bucket, int32_t nbx, int32_t nby, int32_t mode, double min_cc,
+                    double tol, int32_t* count, int32_t* start, int32_t* cursor, int32_t* list,
+                    int32_t* out, int32_t cap, int32_t* n_out, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* optimiser pieces (gp.py:142-147, 178-227, 280-294)                        */
 /* ------------------------------------------------------------------------ */
 /* precondition: out[n][3] = g / max(1, lam*q + macro*deg); div[n]. */

@@ -423,6 +423,67 @@ int p3d_gp2d_layer_force(int32_t n, const int32_t* idx, const double* force, dou
   return check_launch("gp2d_layer_force");
 }
 
+int p3d_rebalance(int32_t n, const double* area_top, const double* area_bot,
+                  const int32_t* order_top, const int32_t* order_bot, uint8_t* delta,
+                  double cap_top, double cap_bot, double* out, void* stream) {
+  if (n < 0 || !out || (n > 0 && (!area_top || !area_bot || !order_top || !order_bot || !delta))) {
+    set_error("rebalance: bad args");
+    return P3D_ERR_ARG;
+  }
+  RebalanceArgs a{n, area_top, area_bot, order_top, order_bot, delta, cap_top, cap_bot, out};
+  launch_rebalance(a, STREAM(stream));
+  return check_launch("rebalance");
+}
+
+int p3d_check_objects(int32_t n_inst, int32_t n_net, const uint8_t* die, const int32_t* rot,
+                      const double* x, const double* y, const uint8_t* is_macro,
+                      const double* w_top, const double* h_top, const double* w_bot,
+                      const double* h_bot, const int32_t* net_ptr, const int32_t* pin_inst,
+                      const uint8_t* hbt_ok, const double* hbt_x, const double* hbt_y,
+                      double die_w, double die_h, double row_top, double row_bot, double site_w,
+                      double pitch, double tol, uint8_t* inst_flags, uint8_t* net_flags,
+                      double* box, double* area, double* scratch, void* stream) {
+  if (n_inst < 1 || n_net < 0 || !die || !rot || !x || !y || !is_macro || !w_top || !h_top ||
+      !w_bot || !h_bot || !inst_flags || !box || !area || !scratch ||
+      (n_net > 0 && (!net_ptr || !pin_inst || !hbt_ok || !hbt_x || !hbt_y || !net_flags)) ||
+      !(row_top > 0) || !(row_bot > 0) || !(site_w > 0)) {
+    set_error("check_objects: bad args");
+    return P3D_ERR_ARG;
+  }
+  CheckArgs a{};
+  a.n_inst = n_inst; a.n_net = n_net; a.die = die; a.rot = rot; a.x = x; a.y = y;
+  a.is_macro = is_macro; a.w_top = w_top; a.h_top = h_top; a.w_bot = w_bot; a.h_bot = h_bot;
+  a.net_ptr = net_ptr; a.pin_inst = pin_inst; a.hbt_ok = hbt_ok; a.hbt_x = hbt_x; a.hbt_y = hbt_y;
+  a.die_w = die_w; a.die_h = die_h; a.row_top = row_top; a.row_bot = row_bot; a.site_w = site_w;
+  a.pitch = pitch; a.tol = tol; a.inst_flags = inst_flags; a.net_flags = net_flags; a.box = box;
+  a.area = area;
+  a.counter = reinterpret_cast<unsigned int*>(scratch);
+  a.partials = scratch + 8;
+  launch_check(a, STREAM(stream));
+  return check_launch("check_objects");
+}
+
+int p3d_pair_search(int32_t phase, int32_t n, const double* box, const uint8_t* member,
+                    double bucket, int32_t nbx, int32_t nby, int32_t mode, double min_cc,
+                    double tol, int32_t* count, int32_t* start, int32_t* cursor, int32_t* list,
+                    int32_t* out, int32_t cap, int32_t* n_out, void* stream) {
+  if (phase < 0 || phase > 2 || n < 0 || nbx < 1 || nby < 1 || !(bucket > 0) || mode < 0 ||
+      mode > 1 || (n > 0 && (!box || !member)) || (phase == 0 && !count) ||
+      (phase == 1 && (!cursor || !list)) || (phase == 2 && (!start || !list || !out || !n_out || cap < 0))) {
+    set_error("pair_search: bad args");
+    return P3D_ERR_ARG;
+  }
+  PairArgs a{};
+  a.n = n; a.box = box; a.member = member; a.bucket = bucket; a.nbx = nbx; a.nby = nby;
+  a.mode = mode; a.min_cc = min_cc; a.tol = tol; a.count = count; a.start = start;
+  a.cursor = cursor; a.list = list; a.out = out; a.cap_out = cap; a.n_out = n_out;
+  if (n == 0) return P3D_OK;
+  if (phase == 0) launch_pair_count(a, STREAM(stream));
+  else if (phase == 1) launch_pair_fill(a, STREAM(stream));
+  else launch_pair_test(a, STREAM(stream));
+  return check_launch("pair_search");
+}
+
 int p3d_precondition(int32_t n, const double* gr, double lam, const double* q, const double* deg,
                      const uint8_t* macro, double* out, double* div, void* stream) {
   if (n < 0 || !gr || !q || !deg || !out) { set_error("precondition: bad args"); return P3D_ERR_ARG; }

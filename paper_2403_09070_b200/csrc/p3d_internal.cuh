@@ -136,6 +136,50 @@ void launch_gp2d_layer_xy(int n, const int32_t* idx, const double* pos, int n_ob
 void launch_gp2d_layer_force(int n, const int32_t* idx, const double* force, double* dens_grad,
                              const int32_t* halt, cudaStream_t s);
 
+// post-GP steps (p3d_post.cu)
+struct RebalanceArgs {
+  int n;
+  const double *area_top, *area_bot;     // [n] rotated w*h on each die
+  const int32_t *order_top, *order_bot;  // [n] sorted by (is_macro, area on the die, index)
+  uint8_t* delta;                        // [n] in/out: 1 top
+  double cap_top, cap_bot;
+  double* out;                           // [4]: status (0 ok, 1 unsatisfiable, 2 no convergence), moves, over_top, over_bot
+};
+void launch_rebalance(const RebalanceArgs& a, cudaStream_t s);
+struct CheckArgs {
+  int n_inst, n_net;
+  const uint8_t* die;
+  const int32_t* rot;
+  const double *x, *y;
+  const uint8_t* is_macro;
+  const double *w_top, *h_top, *w_bot, *h_bot;
+  const int32_t *net_ptr, *pin_inst;
+  const uint8_t* hbt_ok;
+  const double *hbt_x, *hbt_y;
+  double die_w, die_h, row_top, row_bot, site_w, pitch, tol;
+  uint8_t *inst_flags, *net_flags;
+  double* box;    // [n_inst][4] x0, x1, y0, y1
+  double* area;   // [2] per-die cell + macro area
+  double* partials;  // [2 * kMaxBlocks]
+  unsigned int* counter;
+};
+void launch_check(const CheckArgs& a, cudaStream_t s);
+struct PairArgs {
+  int n;
+  const double* box;       // [n][4]
+  const uint8_t* member;   // [n] 1: take part
+  double bucket;
+  int nbx, nby, mode;      // mode 0: overlap, 1: terminal spacing
+  double min_cc, tol;
+  int32_t *count, *start, *cursor, *list;
+  int32_t* out;            // [cap_out][2] pairs (p < q)
+  int32_t cap_out;
+  int32_t* n_out;
+};
+void launch_pair_count(const PairArgs& a, cudaStream_t s);
+void launch_pair_fill(const PairArgs& a, cudaStream_t s);
+void launch_pair_test(const PairArgs& a, cudaStream_t s);
+
 // solution score (p3d_score.cu)
 struct ScoreArgs {
   int n_net;

@@ -371,9 +371,10 @@ def density_energy_and_gradient(grid, cloud, phi, ex=None, ey=None, ez=None, fre
     energy = torch.zeros(1, dtype=torch.float64, device="cuda")
     fr = None if freeze_z is None else _dev.u8(freeze_z)
     scr = _dev.scratch(grid.n_bins + 8 + 1024)
+    phi_d = _dev.f64(phi).reshape(-1).contiguous()  # alive until the kernel ran
     if dc.n:
         _lib.call("p3d_density_energy_gradient", _lib.byref(g), _lib.byref(dc.struct),
-                  _lib.ptr(_dev.f64(phi).reshape(-1).contiguous()), _lib.ptr(fr),
+                  _lib.ptr(phi_d), _lib.ptr(fr),
                   _lib.ptr(energy), _lib.ptr(grad), _lib.ptr(scr), _lib.stream_ptr())
     return float(energy.item()), grad
 

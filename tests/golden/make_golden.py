@@ -189,6 +189,116 @@ def _perturbed_flow(args):
             "final_overflow": rep.final_overflow}
 
 
+def rebalance():
+    """legalize.rebalance_partition (legalize.py:464-499) on partitions that
+    need it: everything on one die (with and without rotated macros), a GP
+    result, and caps no partition satisfies (the LegalizationError path)."""
+    import dataclasses
+
+    from place3d import legalize as rlg
+    from place3d.model import PlacementState
+
+    out = {}
+    for name in ("small", "cfg1"):
+        d = design_of(name)
+        n = d.n_insts
+        cfg, rng, grid, st = setup(d, 64 if name == "small" else 128, 2, 30)
+        st, _ = rgp.run_gp3d(d, st, cfg, grid=grid, rng=rng)
+        dz = grid.dz
+        mids = np.flatnonzero(d.arrays().is_macro)
+        rot = np.zeros(n, dtype=int)
+        rot[mids] = (np.arange(len(mids)) % 3) + 1
+        top, bot = np.full(n, 3 * dz / 4), np.full(n, dz / 4)
+        alt = np.where(np.arange(n) % 3 == 0, dz / 4, 3 * dz / 4)
+        zero = np.zeros(n, dtype=int)
+        # (z, rot, max_util_top, max_util_bottom); None keeps the design's caps
+        cases = {
+            "all_top": (top, zero, 0.45, None),
+            "all_bottom": (bot, zero, None, None),
+            "all_top_rotated": (top, rot, 0.45, None),
+            "gp": (st.z.copy(), zero, None, None),
+            "gp_tight_top": (st.z.copy(), rot, 0.3, None),
+            "alternating": (alt, rot, 0.5, 0.5),
+            "both_ways": (top, zero, 0.62, 0.62),
+            "tight_caps": (top, zero, 0.2, 0.2),
+        }
+        res = {}
+        for cname, (z, r, ut, ub) in cases.items():
+            dd = design_of(name)
+            if ut is not None or ub is not None:
+                dd.die = dataclasses.replace(
+                    dd.die, max_util_top=ut if ut is not None else dd.die.max_util_top,
+                    max_util_bottom=ub if ub is not None else dd.die.max_util_bottom)
+            s0 = PlacementState(x=st.x.copy(), y=st.y.copy(), z=z.copy(), rot=r.copy(), dz=dz)
+            try:
+                rlg.rebalance_partition(dd, s0)
+                moved = np.flatnonzero(s0.z != z)
+                res[cname] = {"ok": True, "moved": moved.tolist(),
+                              "z_moved": s0.z[moved].tolist(), "caps": [ut, ub]}
+            except rlg.LegalizationError as e:
+                res[cname] = {"ok": False, "error": str(e), "caps": [ut, ub]}
+        out[name] = {"spec": SPECS[name], "dz": dz, "rot": rot.tolist(), "z_gp": st.z.tolist(),
+                     "cases": res}
+    with open(os.path.join(HERE, "rebalance.json"), "w") as fh:
+        json.dump(out, fh)
+
+
+def check():
+    """check.check_solution (check.py:74-152) on legal and broken solutions."""
+    from place3d import check as rck
+    from place3d.flow import run_flow
+
+    out = {}
+    for name, iters in (("flow3d", 500), ("flow2d", 500)):
+        d = design_of(name)
+        sol, rep, rows, _ = run_flow(d, rgp.GpConfig(seed=1, max_iters=iters))
+        base = {"die": sol.die.tolist(), "x": sol.x.tolist(), "y": sol.y.tolist(),
+                "rot": sol.rot.tolist(),
+                "hbt_xy": {str(k): list(v) for k, v in sol.hbt_xy.items()}}
+        cases = {"legal": base}
+        rs = np.random.default_rng(3)
+        n = d.n_insts
+        b = json.loads(json.dumps(base))  # overlaps, off-grid, bounds, rotation
+        for i in rs.choice(n, 5, replace=False):
+            b["x"][int(i)] += 0.37
+        j = int(rs.integers(n))
+        b["x"][j] = -5.0
+        cell = int(np.flatnonzero(~d.arrays().is_macro)[0])
+        b["rot"][cell] = 1
+        k = int(np.flatnonzero(~d.arrays().is_macro)[1])
+        b["x"][k], b["y"][k] = b["x"][cell], b["y"][cell]
+        b["die"][k] = b["die"][cell]
+        cases["broken_cells"] = b
+        t = json.loads(json.dumps(base))  # terminals: missing, extra, spacing, bounds
+        keys = sorted(t["hbt_xy"], key=int)
+        if keys:
+            t["hbt_xy"].pop(keys[0])
+        if len(keys) > 2:
+            t["hbt_xy"][keys[2]] = list(t["hbt_xy"][keys[1]])
+        if len(keys) > 3:
+            t["hbt_xy"][keys[3]] = [d.die.width + 3.0, 1.0]
+        crossing = set(int(k) for k in base["hbt_xy"])
+        single = next(jj for jj in range(d.n_nets) if jj not in crossing)
+        t["hbt_xy"][str(single)] = [10.0, 10.0]
+        cases["broken_hbts"] = t
+        u = json.loads(json.dumps(base))  # utilization: everything on the top die
+        u["die"] = [1] * n
+        cases["all_top"] = u
+        res = {}
+        from place3d.model import Solution
+        for cname, c in cases.items():
+            s = Solution(die=np.array(c["die"]), x=np.array(c["x"], float),
+                         y=np.array(c["y"], float), rot=np.array(c["rot"]),
+                         hbt_xy={int(k): tuple(v) for k, v in c["hbt_xy"].items()})
+            r = rck.check_solution(d, s)
+            res[cname] = {"solution": c, "passed": r.passed,
+                          "violations": [str(v) for v in r.violations], "hpwl": r.hpwl,
+                          "hbt_count": r.hbt_count, "raw_score": r.raw_score}
+        out[name] = {"spec": SPECS[name], "cases": res}
+    with open(os.path.join(HERE, "check.json"), "w") as fh:
+        json.dump(out, fh)
+
+
 def flow_small():
     from concurrent.futures import ProcessPoolExecutor
 
@@ -343,7 +453,8 @@ if __name__ == "__main__":
     if "--band" in sys.argv:
         band("cfg2", 256, "cfg2_band.json")
         sys.exit(0)
-    for flag, fn in (("--cfg3", cfg3_rows), ("--exits", exits), ("--flow", flow_small)):
+    for flag, fn in (("--cfg3", cfg3_rows), ("--exits", exits), ("--flow", flow_small),
+                     ("--rebalance", rebalance), ("--check", check)):
         if flag in sys.argv:
             fn()
             sys.exit(0)

@@ -17,6 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--post", type=int, default=None, help="(separate mode) post-GP rows")
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
@@ -118,5 +119,72 @@ def main():
           flush=True)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--post" not in sys.argv:
     main()
+
+
+def post_rows(config=2):
+    """rebalance_partition and check_solution on the device at `config`
+    (GPU wall time around the call, synchronised)."""
+    import dataclasses
+
+    import torch
+
+    from paper_2403_09070_b200.check import check_solution
+    from paper_2403_09070_b200.legalize import rebalance_partition
+    from paper_2403_09070_b200.model import PlacementState
+    from paper_2403_09070_b200.synth import CONFIGS, cached_synth
+
+    d = cached_synth(CONFIGS[config]["spec"])
+    n = d.n_insts
+    d.die = dataclasses.replace(d.die, max_util_top=0.45)
+    dz = 100.0
+    for rep in range(2):
+        st = PlacementState(x=np.zeros(n), y=np.zeros(n), z=np.full(n, 75.0),
+                            rot=np.zeros(n, dtype=np.int64), dz=dz)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rebalance_partition(d, st)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+    moved = int((st.z != 75.0).sum())
+    print(json.dumps({"row": "rebalance_partition (legalize.py:464-499)", "config": config,
+                      "n_inst": n, "moves": moved, "gpu_ms": dt * 1e3,
+                      "note": "all instances start on the top die, top cap 0.45"}), flush=True)
+    # a legal-shaped row-aligned solution: cells on rows / sites, terminals for crossing nets
+    rs = np.random.default_rng(2)
+    a = d.arrays()
+    die = rs.integers(0, 2, n)
+    rh = np.where(die == 1, d.die.row_height_top, d.die.row_height_bottom)
+    x = np.floor(rs.uniform(0, d.die.width - 2000, n))
+    y = np.floor(rs.uniform(0, d.die.height - 2000, n) / rh) * rh
+    pdie = die[a.pin_inst]
+    mx = np.zeros(a.n_net, int)
+    mn = np.ones(a.n_net, int)
+    np.maximum.at(mx, a.pin_net, pdie)
+    np.minimum.at(mn, a.pin_net, pdie)
+    hbt = {int(j): (float(rs.uniform(0, d.die.width - 50)), float(rs.uniform(0, d.die.height - 50)))
+           for j in np.flatnonzero(mx > mn)}
+
+    class Sol:
+        pass
+
+    sol = Sol()
+    sol.die, sol.x, sol.y, sol.rot, sol.hbt_xy = die, x, y, np.zeros(n, dtype=np.int64), hbt
+    for rep in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = check_solution(d, sol)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+    kinds = {}
+    for v in r.violations:
+        kinds[v.kind] = kinds.get(v.kind, 0) + 1
+    print(json.dumps({"row": "check_solution (check.py:74-152)", "config": config, "n_inst": n,
+                      "n_net": a.n_net, "gpu_ms": dt * 1e3, "violations": kinds,
+                      "note": "random row-aligned solution (overlapping): every check runs"}),
+          flush=True)
+
+
+if __name__ == "__main__" and "--post" in sys.argv:
+    post_rows(int(sys.argv[sys.argv.index("--post") + 1]) if len(sys.argv) > sys.argv.index("--post") + 1 else 2)
