@@ -258,6 +258,31 @@ int p3d_score(int32_t n_net, const int32_t* net_ptr, const int32_t* pin_inst,
               double* scratch, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* small per-op pieces of the operator API                                   */
+/* ------------------------------------------------------------------------ */
+/* dynamic_size (density.py:134-147): w, h [n] at depth z [n]. */
+int p3d_dynamic_size(int32_t n, const double* w_top, const double* h_top, const double* w_bot,
+                     const double* h_bot, const uint8_t* is_macro, const double* z, double dz,
+                     double* w, double* h, void* stream);
+/* prefix_sum_3d (reverse 0) / suffix_sum_3d (reverse 1) in place on a
+ * C-ordered [nx][ny][nz] map (density.py:207-217): x, then y, then z. */
+int p3d_prefix_sum_3d(int32_t nx, int32_t ny, int32_t nz, int32_t reverse, double* a,
+                      void* stream);
+/* overflow (density.py:612-617) of a float64 map [n]: out[1]; scratch: >= 8 +
+ * 1024 doubles (counter zeroed once). */
+int p3d_overflow(int64_t n, const double* rho, double rho_t, double bin_vol,
+                 double movable_volume, double* out, double* scratch, void* stream);
+/* NetBoxes.spans (wirelength.py:136-142): top, bottom, full [n_net]. */
+int p3d_net_spans(int32_t n_net, const int64_t* cnt, const double* min1, const double* max1,
+                  const double* full_min, const double* full_max, double* top, double* bot,
+                  double* full, void* stream);
+/* NesterovOptimizer.advance pieces (gp.py:198-226) over n doubles:
+ * op 0: out[0] = |v - vp|^2, out[1] = |g - ref|^2;  op 1: out[0] = max |g|;
+ * op 2: out = v + s * g (c null) or v + s * (g - c).  scratch: >= 8 + 2*2048. */
+int p3d_nesterov_op(int32_t op, int64_t n, const double* v, const double* vp, const double* g,
+                    const double* ref, double s, double* out, double* scratch, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* post-GP steps                                       */
 /* ------------------------------------------------------------------------ */
 /* rebalance_partition (legalize.py:464-499): moves instances off the die

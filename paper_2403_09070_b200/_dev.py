@@ -2,6 +2,8 @@
 
 from __future__ import annotations
 
+import functools
+
 import numpy as np
 import torch
 
@@ -66,3 +68,43 @@ class Keep:
     def __call__(self, t):
         self.items.append(t)
         return _lib.ptr(t)
+
+
+def _numpy_arg(a):
+    if isinstance(a, np.ndarray):
+        return True
+    x = getattr(a, "x", None)  # a charge cloud of numpy arrays
+    return isinstance(x, np.ndarray) and hasattr(a, "weight")
+
+
+def _to_host(out):
+    if isinstance(out, torch.Tensor):
+        return out.detach().cpu().numpy()
+    if isinstance(out, tuple):
+        return tuple(_to_host(o) for o in out)
+    if isinstance(out, list):
+        return [_to_host(o) for o in out]
+    return out
+
+
+def numpy_io(*names):
+    """Per-op drop-in convention: when the caller passes its data arrays (the
+    arguments `names`) as numpy arrays, as the reference's callers do, the
+    results come back as numpy arrays; CUDA tensors in, CUDA tensors out.  The
+    computation is on the device either way."""
+    import inspect
+
+    def deco(fn):
+        sig = inspect.signature(fn)
+
+        @functools.wraps(fn)
+        def wrapper(*args, **kw):
+            out = fn(*args, **kw)
+            b = sig.bind_partial(*args, **kw).arguments
+            if any(_numpy_arg(b.get(n)) for n in names):
+                return _to_host(out)
+            return out
+
+        return wrapper
+
+    return deco

@@ -139,6 +139,11 @@ _SIGS = {
     "p3d_gp2d_project": (I32, [P, P, P, P]),
     "p3d_gp2d_layer_xy": (I32, [I32, P, P, I32, P, P, P, P]),
     "p3d_gp2d_layer_force": (I32, [I32, P, P, P, P, P]),
+    "p3d_dynamic_size": (I32, [I32, P, P, P, P, P, P, D, P, P, P]),
+    "p3d_prefix_sum_3d": (I32, [I32, I32, I32, I32, P, P]),
+    "p3d_overflow": (I32, [I64, P, D, D, D, P, P, P]),
+    "p3d_net_spans": (I32, [I32, P, P, P, P, P, P, P, P, P]),
+    "p3d_nesterov_op": (I32, [I32, I64, P, P, P, P, D, P, P, P]),
     "p3d_rebalance": (I32, [I32, P, P, P, P, P, D, D, P, P]),
     "p3d_check_objects": (I32, [I32, I32] + [P] * 14 + [D] * 7 + [P] * 5),
     "p3d_pair_search": (I32, [I32, I32, P, P, D, I32, I32, I32, D, D, P, P, P, P, P, I32, P, P]),

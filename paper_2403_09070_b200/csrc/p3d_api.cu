@@ -423,6 +423,57 @@ int p3d_gp2d_layer_force(int32_t n, const int32_t* idx, const double* force, dou
   return check_launch("gp2d_layer_force");
 }
 
+int p3d_dynamic_size(int32_t n, const double* w_top, const double* h_top, const double* w_bot,
+                     const double* h_bot, const uint8_t* is_macro, const double* z, double dz,
+                     double* w, double* h, void* stream) {
+  if (n < 0 || (n > 0 && (!w_top || !h_top || !w_bot || !h_bot || !is_macro || !z || !w || !h))) {
+    set_error("dynamic_size: bad args");
+    return P3D_ERR_ARG;
+  }
+  if (n == 0) return P3D_OK;
+  launch_dynamic_size(n, w_top, h_top, w_bot, h_bot, is_macro, z, dz, w, h, STREAM(stream));
+  return check_launch("dynamic_size");
+}
+
+int p3d_prefix_sum_3d(int32_t nx, int32_t ny, int32_t nz, int32_t reverse, double* a,
+                      void* stream) {
+  if (nx < 1 || ny < 1 || nz < 1 || !a) { set_error("prefix_sum_3d: bad args"); return P3D_ERR_ARG; }
+  for (int ax = 0; ax < 3; ++ax) launch_axis_scan(nx, ny, nz, ax, reverse != 0, a, STREAM(stream));
+  return check_launch("prefix_sum_3d");
+}
+
+int p3d_overflow(int64_t n, const double* rho, double rho_t, double bin_vol,
+                 double movable_volume, double* out, double* scratch, void* stream) {
+  if (n < 1 || !rho || !out || !scratch) { set_error("overflow: bad args"); return P3D_ERR_ARG; }
+  launch_overflow_d(n, rho, rho_t, bin_vol / movable_volume, scratch, out, STREAM(stream));
+  return check_launch("overflow");
+}
+
+int p3d_net_spans(int32_t n_net, const int64_t* cnt, const double* min1, const double* max1,
+                  const double* full_min, const double* full_max, double* top, double* bot,
+                  double* full, void* stream) {
+  if (n_net < 0 || (n_net > 0 && (!cnt || !min1 || !max1 || !full_min || !full_max || !top || !bot || !full))) {
+    set_error("net_spans: bad args");
+    return P3D_ERR_ARG;
+  }
+  if (n_net == 0) return P3D_OK;
+  launch_spans(n_net, cnt, min1, max1, full_min, full_max, top, bot, full, STREAM(stream));
+  return check_launch("net_spans");
+}
+
+int p3d_nesterov_op(int32_t op, int64_t n, const double* v, const double* vp, const double* g,
+                    const double* ref, double s, double* out, double* scratch, void* stream) {
+  if (n < 1 || !out || !g || (op == 0 && (!v || !vp || !ref || !scratch)) ||
+      (op == 1 && !scratch) || (op == 2 && !v) || op < 0 || op > 2) {
+    set_error("nesterov_op: bad args");
+    return P3D_ERR_ARG;
+  }
+  if (op == 0) launch_bb_norms(n, v, vp, g, ref, scratch, out, STREAM(stream));
+  else if (op == 1) launch_absmax(n, g, scratch, out, STREAM(stream));
+  else launch_axpy(n, v, s, g, ref, out, STREAM(stream));
+  return check_launch("nesterov_op");
+}
+
 int p3d_rebalance(int32_t n, const double* area_top, const double* area_bot,
                   const int32_t* order_top, const int32_t* order_bot, uint8_t* delta,
                   double cap_top, double cap_bot, double* out, void* stream) {

@@ -180,6 +180,22 @@ void launch_pair_count(const PairArgs& a, cudaStream_t s);
 void launch_pair_fill(const PairArgs& a, cudaStream_t s);
 void launch_pair_test(const PairArgs& a, cudaStream_t s);
 
+// small per-op kernels (p3d_ops.cu)
+void launch_dynamic_size(int n, const double* wt, const double* ht, const double* wb,
+                         const double* hb, const uint8_t* mac, const double* z, double dz,
+                         double* w, double* h, cudaStream_t s);
+void launch_axis_scan(int nx, int ny, int nz, int axis, bool reverse, double* a, cudaStream_t s);
+void launch_overflow_d(long long n, const double* rho, double rho_t, double scale, double* scratch,
+                       double* out, cudaStream_t s);
+void launch_spans(int n, const int64_t* cnt, const double* min1, const double* max1,
+                  const double* fmin, const double* fmax, double* top, double* bot, double* full,
+                  cudaStream_t s);
+void launch_bb_norms(long long n, const double* v, const double* vp, const double* g,
+                     const double* ref, double* scratch, double* out, cudaStream_t s);
+void launch_absmax(long long n, const double* g, double* scratch, double* out, cudaStream_t s);
+void launch_axpy(long long n, const double* a, double sc, const double* b, const double* c,
+                 double* out, cudaStream_t s);
+
 // solution score (p3d_score.cu)
 struct ScoreArgs {
   int n_net;

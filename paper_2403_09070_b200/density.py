@@ -206,17 +206,21 @@ def build_fillers(die_area_wh, dz, u_top, u_bot, cell_area_hint, rng):
     return FillerSet(*cols, dz / 2)
 
 
+@_dev.numpy_io("z")
 def dynamic_size(w_top, h_top, w_bot, h_bot, is_macro, z, dz):
     """Footprint vs depth (density.py:134-147, Eqs. 6-7): cells switch at the
-    midplane, macros blend linearly over z in [dz/4, 3dz/4]."""
-    z = torch.clamp(_dev.f64(z), dz / 4, 3 * dz / 4)
-    wt, ht, wb, hb = (_dev.f64(a) for a in (w_top, h_top, w_bot, h_bot))
-    m = _dev.u8(is_macro).to(torch.bool)
-    top = (z - dz / 2) > 0
-    t = 2 * z / dz - 0.5
-    wm = t * wt + (1 - t) * wb
-    hm = t * ht + (1 - t) * hb
-    return torch.where(m, wm, torch.where(top, wt, wb)), torch.where(m, hm, torch.where(top, ht, hb))
+    midplane, macros blend linearly over z in [dz/4, 3dz/4] (p3d_dynamic_size)."""
+    _lib.require_cuda()
+    zt = _dev.f64(z).reshape(-1)
+    n = zt.numel()
+    wt, ht, wb, hb = (_dev.f64(np.broadcast_to(a, (n,)) if not isinstance(a, torch.Tensor)
+                               else a).reshape(-1) for a in (w_top, h_top, w_bot, h_bot))
+    m = _dev.u8(np.broadcast_to(np.asarray(is_macro, dtype=bool), (n,))
+                if not isinstance(is_macro, torch.Tensor) else is_macro)
+    w, h = torch.empty_like(zt), torch.empty_like(zt)
+    _lib.call("p3d_dynamic_size", int(n), _lib.ptr(wt), _lib.ptr(ht), _lib.ptr(wb), _lib.ptr(hb),
+              _lib.ptr(m), _lib.ptr(zt), float(dz), _lib.ptr(w), _lib.ptr(h), _lib.stream_ptr())
+    return w, h
 
 
 # ---------------------------------------------------------------------------
@@ -243,17 +247,20 @@ def fx_to_density(rho_fx):
     return out
 
 
+@_dev.numpy_io("cloud")
 def accumulate_density(grid, cloud):
     """Density map (density.py:301-311): cells/fillers thread-per-object,
     macros one CTA each over their footprint tile."""
     return fx_to_density(accumulate_density_fx(grid, cloud))
 
 
+@_dev.numpy_io("cloud")
 def direct_density(grid, cloud):
     """Per-object traversal of every given charge (density.py:199-204)."""
     return fx_to_density(accumulate_density_fx(grid, cloud, macro_override=False))
 
 
+@_dev.numpy_io("cloud")
 def macro_prefix_density(grid, cloud):
     """Macro map (density.py:291-298); on the device every charge takes the
     per-macro tile path, which equals the corner-stamp prefix sum exactly in
@@ -261,17 +268,24 @@ def macro_prefix_density(grid, cloud):
     return fx_to_density(accumulate_density_fx(grid, cloud, macro_override=True))
 
 
+@_dev.numpy_io("a")
 def prefix_sum_3d(a):
-    """Inclusive prefix sum along x, y, z (density.py:207-209)."""
-    t = _dev.f64(a)
-    return torch.cumsum(torch.cumsum(torch.cumsum(t, 0), 1), 2)
+    """Inclusive prefix sum along x, y, z (density.py:207-209; p3d_prefix_sum_3d)."""
+    return _scan3(a, 0)
 
 
+@_dev.numpy_io("a")
 def suffix_sum_3d(a):
     """Adjoint of prefix_sum_3d (density.py:212-217)."""
-    t = _dev.f64(a)
-    for ax in range(3):
-        t = torch.flip(torch.cumsum(torch.flip(t, (ax,)), ax), (ax,))
+    return _scan3(a, 1)
+
+
+def _scan3(a, reverse):
+    _lib.require_cuda()
+    t = _dev.f64(a).clone()
+    nx, ny, nz = t.shape
+    _lib.call("p3d_prefix_sum_3d", int(nx), int(ny), int(nz), int(reverse), _lib.ptr(t),
+              _lib.stream_ptr())
     return t
 
 
@@ -299,6 +313,7 @@ def _spectral(grid, rho=None, coef=None, want_coef=False):
     return maps, out_coef
 
 
+@_dev.numpy_io("rho")
 def solve_potential(rho, grid):
     """Neumann Poisson solve by cosine transforms, DC dropped
     (density.py:319-328).  Returns (phi, scipy-normalised DCT-II coef)."""
@@ -306,12 +321,14 @@ def solve_potential(rho, grid):
     return maps[:, 0].reshape(grid.shape).contiguous(), coef
 
 
+@_dev.numpy_io("coef")
 def electric_field(coef, grid):
     """E = -grad(phi) evaluated spectrally (density.py:357-368)."""
     maps, _ = _spectral(grid, coef=coef)
     return tuple(maps[:, k].reshape(grid.shape).contiguous() for k in (1, 2, 3))
 
 
+@_dev.numpy_io("rho")
 def potential_and_field(rho, grid):
     """Both at once as the interleaved [B][4] (phi, Ex, Ey, Ez) map the
     density gather reads (what the fused loop uses)."""
@@ -353,11 +370,13 @@ def density_energy(grid, cloud, phi):
     return _gather(grid, cloud, _interleave(grid, phi=phi))[0]
 
 
+@_dev.numpy_io("ex")
 def density_force(grid, cloud, ex, ey, ez, freeze_z=None):
     """-2 q * overlap-weighted mean E (density.py:582-609)."""
     return _gather(grid, cloud, _interleave(grid, ex=ex, ey=ey, ez=ez), freeze_z)[1]
 
 
+@_dev.numpy_io("phi")
 def density_energy_and_gradient(grid, cloud, phi, ex=None, ey=None, ez=None, freeze_z=None):
     """Energy U = sum q * phibar and its EXACT gradient (density.py:533-565):
     cells through the two face columns of each axis, macros through their
@@ -385,11 +404,75 @@ def density_energy_and_force(grid, cloud, maps, freeze_z=None):
 
 
 def overflow(rho, grid, rho_t, movable_volume):
-    """Fraction of movable volume above the target density (density.py:612-617)."""
+    """Fraction of movable volume above the target density (density.py:612-617;
+    p3d_overflow)."""
     if movable_volume <= 0:
         return 0.0
-    r = _dev.f64(rho)
-    return float((torch.clamp(r - rho_t, min=0).sum() * grid.bin_vol / movable_volume).item())
+    _lib.require_cuda()
+    r = _dev.f64(rho).reshape(-1)
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    scr = _dev.scratch(8 + 1024 + 8)
+    _lib.call("p3d_overflow", int(r.numel()), _lib.ptr(r), float(rho_t), float(grid.bin_vol),
+              float(movable_volume), _lib.ptr(out), _lib.ptr(scr), _lib.stream_ptr())
+    return float(out.item())
+
+
+def macro_overflow(grid, cloud, rho_t):
+    """Overflow of the macro-only density map (density.py:620-627): the macros'
+    per-macro tile map (K2) and the overflow kernel."""
+    m = np.asarray(cloud.is_macro.cpu() if isinstance(cloud.is_macro, torch.Tensor)
+                   else cloud.is_macro, dtype=bool)
+    if not m.any():
+        return 0.0
+    idx = np.flatnonzero(m)
+    sel = (lambda v: v[torch.from_numpy(idx).to(v.device)]) if isinstance(cloud.x, torch.Tensor) \
+        else (lambda v: np.asarray(v)[idx])
+    big = ChargeCloud(*(sel(getattr(cloud, k)) for k in ("x", "y", "z", "w", "h", "dep",
+                                                          "weight")), is_macro=np.ones(len(idx), bool))
+    vol = float(_dev.f64(big.w * big.h * big.dep).sum().item()) if isinstance(big.w, torch.Tensor) \
+        else float(np.sum(big.w * big.h * big.dep))
+    rho = macro_prefix_density(grid, big)
+    return overflow(rho, grid, rho_t, vol)
+
+
+def corner_map(corner, grid):
+    """Sparse stamp of one cuboid corner (density.py:220-240): host helper of
+    the corner-stamp formulation (the device path stamps whole macro tiles)."""
+    xh, yh, zh = corner[0] / grid.wb, corner[1] / grid.hb, corner[2] / grid.db
+    idx = []
+    for base, n in ((xh, grid.nx), (yh, grid.ny), (zh, grid.nz)):
+        i0 = int(np.floor(base))
+        ax = [(i0, 1.0 - (base - i0)), (i0 + 1, base - i0)]
+        idx.append([(i, v) for i, v in ax if 0 <= i < n and v != 0.0])
+    out_idx, out_val = [], []
+    for i, vi in idx[0]:
+        for j, vj in idx[1]:
+            for k, vk in idx[2]:
+                out_idx.append((i, j, k))
+                out_val.append(vi * vj * vk)
+    return out_idx, out_val
+
+
+def dump_fields(path_prefix, grid, named_maps):
+    """Debug dump, one flat float64 file per map with a text header line
+    (density.py:630-640; the reference's format)."""
+    paths = []
+    for name, m in named_maps.items():
+        path = f"{path_prefix}{name}.bin"
+        arr = np.ascontiguousarray(_dev.host(m), dtype=np.float64)
+        with open(path, "wb") as fh:
+            fh.write(f"{name} float64 {grid.nx} {grid.ny} {grid.nz}\n".encode())
+            fh.write(arr.tobytes())
+        paths.append(path)
+    return paths
+
+
+def load_field(path):
+    """density.py:643-647."""
+    with open(path, "rb") as fh:
+        header = fh.readline().decode().split()
+        data = np.frombuffer(fh.read(), dtype=header[1])
+    return header[0], data.reshape([int(t) for t in header[2:]])
 
 
 def overflow_fx(rho_fx, grid, rho_t, movable_volume):
@@ -409,4 +492,5 @@ __all__ = [
     "electric_field", "potential_and_field", "density_energy", "density_force",
     "density_energy_and_gradient",
     "density_energy_and_force", "overflow", "overflow_fx", "partition_from_z",
+    "macro_overflow", "corner_map", "dump_fields", "load_field",
 ]

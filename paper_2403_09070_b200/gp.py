@@ -177,6 +177,7 @@ def gamma_schedule(grid, it, max_iters, cfg: GpConfig):
     return g0 * (g1 / g0) ** t
 
 
+@_dev.numpy_io("gradients")
 def precondition(gradients, lam, charges, pin_degrees, macro_flags):
     """Eq. 19 (gp.py:142-147) on the device: g / max(1, lam q [+ #pins])."""
     _lib.require_cuda()
@@ -207,7 +208,9 @@ def precondition(gradients, lam, charges, pin_degrees, macro_flags):
 class NesterovOptimizer:
     """Accelerated descent with a clipped Barzilai-Borwein step (gp.py:178-227),
     on CUDA tensors, for callers that drive their own loop (the fused device
-    loop in ``run_gp3d`` does not use this class)."""
+    loop in ``run_gp3d`` does not use this class).  The norms, max |g| and the
+    two updates are device kernels (``p3d_nesterov_op``); ``project`` is the
+    caller's (e.g. ``Gp3dProblem.project``)."""
 
     def __init__(self, x0, project=None, min_step=1e-18):
         self.project = project or (lambda p: p)
@@ -218,26 +221,43 @@ class NesterovOptimizer:
         self.min_step = min_step
         self._prev_v = None
         self._prev_g = None
+        self._scr = _dev.scratch(8 + 2 * 2048 + 8)
+        self._out = torch.zeros(4, dtype=torch.float64, device="cuda")
+
+    def _op(self, op, v, vp, g, ref, s=0.0, out=None):
+        _lib.call("p3d_nesterov_op", int(op), int(g.numel()), _lib.ptr(v), _lib.ptr(vp),
+                  _lib.ptr(g), _lib.ptr(ref), float(s), _lib.ptr(self._out if out is None else out),
+                  _lib.ptr(self._scr), _lib.stream_ptr())
 
     def advance(self, g, step_scale=1.0, g_prev_reval=None):
-        g = _dev.f64(g)
-        ref = _dev.f64(g_prev_reval) if g_prev_reval is not None else self._prev_g
+        g = _dev.f64(g).contiguous()
+        ref = _dev.f64(g_prev_reval).contiguous() if g_prev_reval is not None else self._prev_g
         if self.step is None or self._prev_v is None or ref is None:
             if self.step is None:
-                gmax = float(g.abs().max().item()) if g.numel() else 0.0
+                if g.numel():
+                    self._op(1, None, None, g, None)
+                    gmax = float(self._out[0].item())
+                else:
+                    gmax = 0.0
                 self.step = 1.0 if gmax == 0 else step_scale / gmax
         else:
-            den = float(torch.linalg.norm((g - ref).reshape(-1)).item())
+            self._op(0, self.v, self._prev_v, g, ref)
+            dv2, dg2 = self._out[:2].tolist()
+            den = math.sqrt(dg2)
             if den > 0:
-                new = float(torch.linalg.norm((self.v - self._prev_v).reshape(-1)).item()) / den
+                new = math.sqrt(dv2) / den
                 self.step = float(min(max(new, self.step / 4), self.step * 4))
         if not math.isfinite(self.step) or self.step <= self.min_step:
             raise StepUnderflow(f"step size underflow ({self.step!r})")
         self._prev_v = self.v.clone()
         self._prev_g = g.clone()
-        u_new = self.project(self.v - self.step * g)
+        u_new = torch.empty_like(self.v)
+        self._op(2, self.v, None, g, None, -self.step, out=u_new)  # v - step * g
+        u_new = self.project(u_new)
         a_new = (1 + math.sqrt(4 * self.a ** 2 + 1)) / 2
-        self.v = self.project(u_new + (self.a - 1) / a_new * (u_new - self.u))
+        v_new = torch.empty_like(u_new)
+        self._op(2, u_new, None, u_new, self.u, (self.a - 1) / a_new, out=v_new)
+        self.v = self.project(v_new)
         self.u = u_new
         self.a = a_new
         return self.u

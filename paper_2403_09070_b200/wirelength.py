@@ -125,7 +125,8 @@ def wa_smooth(values, gamma):
 
 class NetBoxes:
     """First/second extrema per (net, die) with multiplicity (wirelength.py:101-142).
-    Attributes are CUDA tensors: cnt/min1/min2/max1/max2 [N,2], full_min/max [N]."""
+    Attributes cnt/min1/min2/max1/max2 [N,2], full_min/max [N]: CUDA tensors, or
+    numpy arrays when the coordinates were given as numpy."""
 
     def __init__(self, topo, coord, on_top):
         _lib.require_cuda()
@@ -145,13 +146,24 @@ class NetBoxes:
                   _lib.ptr(self.cnt), _lib.ptr(self.min1), _lib.ptr(self.min2),
                   _lib.ptr(self.max1), _lib.ptr(self.max2), _lib.ptr(self.full_min),
                   _lib.ptr(self.full_max), _lib.ptr(self.bistratal), _lib.stream_ptr())
+        self._dev = {k: getattr(self, k) for k in ("cnt", "min1", "min2", "max1", "max2",
+                                                    "full_min", "full_max", "bistratal")}
+        # numpy coordinates in (the reference's callers): numpy attributes out
+        self._host = isinstance(coord, np.ndarray)
+        if self._host:
+            for k, v in self._dev.items():
+                setattr(self, k, v.cpu().numpy())
 
     def spans(self):
-        """(top span, bottom span, full span); empty partial nets span 0."""
-        z = torch.zeros((), dtype=torch.float64, device="cuda")
-        top = torch.where(self.cnt[:, 1] > 0, self.max1[:, 1] - self.min1[:, 1], z)
-        bot = torch.where(self.cnt[:, 0] > 0, self.max1[:, 0] - self.min1[:, 0], z)
-        full = torch.where(self.cnt.sum(dim=1) > 0, self.full_max - self.full_min, z)
+        """(top span, bottom span, full span); empty partial nets span 0
+        (wirelength.py:136-142; p3d_net_spans)."""
+        d = [self._dev[k] for k in ("cnt", "min1", "max1", "full_min", "full_max")]
+        n = d[0].shape[0]
+        top, bot, full = (torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(3))
+        _lib.call("p3d_net_spans", int(n), *[_lib.ptr(t) for t in d], _lib.ptr(top),
+                  _lib.ptr(bot), _lib.ptr(full), _lib.stream_ptr())
+        if self._host:
+            return top.cpu().numpy(), bot.cpu().numpy(), full.cpu().numpy()
         return top, bot, full
 
 
@@ -183,10 +195,10 @@ def optimal_hbt_centers(arrays, x, y, z, rot, dz):
     px, py, _, on_top = dynamic_pin_coords(arrays, x, y, z, rot, dz)
     bx = NetBoxes(topo, px, on_top)
     by = NetBoxes(topo, py, on_top)
-    cnt = bx.cnt.cpu().numpy()
+    cnt = _dev.host(bx.cnt)
     crossing = np.flatnonzero((cnt[:, 0] > 0) & (cnt[:, 1] > 0))
-    mnx, mxx = bx.min1.cpu().numpy(), bx.max1.cpu().numpy()
-    mny, mxy = by.min1.cpu().numpy(), by.max1.cpu().numpy()
+    mnx, mxx = _dev.host(bx.min1), _dev.host(bx.max1)
+    mny, mxy = _dev.host(by.min1), _dev.host(by.max1)
     out = {}
     for j in crossing:
         r = optimal_region((mnx[j, 1], mxx[j, 1], mny[j, 1], mxy[j, 1]),
@@ -195,6 +207,7 @@ def optimal_hbt_centers(arrays, x, y, z, rot, dz):
     return out
 
 
+@_dev.numpy_io("coord")
 def bistratal_spans(topo, coord, on_top, boxes=None):
     """Per-net exact bistratal extent on one axis (wirelength.py:167-170)."""
     if boxes is not None:
@@ -202,6 +215,7 @@ def bistratal_spans(topo, coord, on_top, boxes=None):
     return NetBoxes(topo, coord, on_top).bistratal
 
 
+@_dev.numpy_io("pin_x")
 def planar_objective(topo, pin_x, pin_y, on_top, gamma, boxes_x=None, boxes_y=None):
     """Smoothed bistratal WL + per-pin planar gradients (wirelength.py:173-192).
     The branch per net/axis is re-derived on the device from the same exact
@@ -220,6 +234,7 @@ def planar_objective(topo, pin_x, pin_y, on_top, gamma, boxes_x=None, boxes_y=No
     return float(val.item()), gx, gy
 
 
+@_dev.numpy_io("pin_z")
 def z_cut_penalty(topo, pin_z, gamma):
     """Smoothed z-span per net and per-pin gradients (wirelength.py:195-198)."""
     _lib.require_cuda()
@@ -249,6 +264,7 @@ def _fd(topo, pin_x, pin_y, on_top, dz, net_has_dup):
     return g[: dt.n_obj]
 
 
+@_dev.numpy_io("pin_x")
 def fd_z_gradient_incremental(topo, pin_x, pin_y, on_top, dz, net_has_dup=None,
                               boxes_x=None, boxes_y=None):
     """Depth gradient by single-pin die flips (wirelength.py:251-293): O(1) per
@@ -259,12 +275,14 @@ def fd_z_gradient_incremental(topo, pin_x, pin_y, on_top, dz, net_has_dup=None,
     return _fd(topo, pin_x, pin_y, on_top, dz, np.asarray(net_has_dup, bool))
 
 
+@_dev.numpy_io("pin_x")
 def fd_z_gradient_naive(topo, pin_x, pin_y, on_top, dz):
     """Per-owner forced re-evaluation of every net (wirelength.py:205-224):
     the exact O(|P_e|^2) device path applied to all nets."""
     return _fd(topo, pin_x, pin_y, on_top, dz, np.ones(topo.n_net, dtype=bool))
 
 
+@_dev.numpy_io("grad_x")
 def normalize_z_gradient(grad_x, grad_y, grad_z_bistratal, grad_z_hbt, alpha):
     """Eq. 17 (wirelength.py:296-305)."""
     _lib.require_cuda()
@@ -286,6 +304,7 @@ def rotated_pin_offsets(arrays, rot):
     return np.ascontiguousarray(np.stack([rx_t, ry_t, rx_b, ry_b], axis=1))
 
 
+@_dev.numpy_io("x")
 def dynamic_pin_coords(arrays: NetlistArrays, x, y, z, rot, dz):
     """Absolute pin coordinates with offsets picked by the owner's die
     (wirelength.py:308-322).  Returns CUDA tensors (px, py, pz, on_top bool)."""
