@@ -625,8 +625,8 @@ def main():
     ws_mb = (sum(t.numel() * t.element_size() for t in prob._keep.items) +
              sum(t.numel() * t.element_size() for t in prob._dtopo.keep.items)) / 1e6
     parallelism = {"fused": "single", "replicas": f"replicas x{world}",
-                   "sharded": f"sharded over {world} (objects + nets per rank, int64 rho "
-                              f"all-reduce)"}[mode]
+                   "sharded": f"sharded over {world} (instance slabs + the nets touching them "
+                              f"per rank, halo positions, int64 rho all-reduce)"}[mode]
     line = {
         "metric": METRIC, "value": it_s, "unit": "it/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
@@ -655,6 +655,10 @@ def main():
         line["roofline"]["note"] = ("rank-0 shard, eager stages; algorithmic bytes of the whole "
                                     "placement / world per family")
         line["config"]["collective_ms_per_step"] = round(comm_ms, 4)
+        line["config"]["exchange_bytes_per_rank_per_step"] = runner.exchange_bytes()
+        line["config"]["partition"] = ("halo: locality-ordered instance slabs, nets run on every "
+                                       "rank they touch, halo positions all-to-all"
+                                       if runner.halo else "round-robin K1 tasks")
     if not args.no_cpu_baseline and world == 1:
         rate, iters, el = cpu_baseline(design, grid_n, spec, seconds=args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "it/s", "cores": 1, "kind": "port",

@@ -431,7 +431,11 @@ typedef struct p3d_gp {
   int32_t overlap;             /* 1: the wirelength branch (K1, K1b) runs on a side
                                   stream concurrently with the density branch (K2,
                                   K3), joined before K4 (fused loop) */
-  int32_t pad2;
+  int32_t shard_halo;          /* sharded loop only: 1 = halo mode (each rank runs its own
+                                  task list: every net touching its instance slab, and
+                                  counts the value of the nets whose f_net_dup bit 1 is
+                                  clear; owner sums over its own slab only, no owner-sum
+                                  exchange); 0 = tasks dealt round-robin + reduce-scatter */
 } p3d_gp;
 
 /* Stages of one sharded GP iteration.  The host runs them in this order with

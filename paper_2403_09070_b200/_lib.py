@@ -77,7 +77,7 @@ class Gp(C.Structure):
                 ("maps", P), ("partials", P), ("st", P), ("log", P), ("ovfl_hist", P),
                 ("shard_rank", I32), ("shard_size", I32), ("sh_i0", I32), ("sh_i1", I32),
                 ("sh_f0", I32), ("sh_f1", I32), ("shard_tot", P), ("overlap", I32),
-                ("pad2", I32)]
+                ("shard_halo", I32)]
 
 class Gp2dState(C.Structure):
     _fields_ = [("it", I32), ("done", I32), ("diverged", I32), ("converged", I32),

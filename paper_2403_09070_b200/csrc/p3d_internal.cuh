@@ -78,7 +78,8 @@ struct FusedNetArgs {
   const int32_t* net_base;    // [n_net] first pin index of the net (permuted order)
   const int32_t* net_deg;     // [n_net]
   const int32_t* net_stride;  // [n_net] distance between consecutive pins of a net
-  const uint8_t* net_dup;     // [n_net] permuted dup flags
+  const uint8_t* net_dup;     // [n_net] permuted: bit 0 duplicate-owner net, bit 1 value
+                              // counted by another rank (sharded halo mode)
   const int32_t* pin_inst;    // [n_pin] permuted
   const float4* off;          // [n_pin] permuted (rx_top, ry_top, rx_bot, ry_bot)
   const int32_t* slot;        // [n_pin] owner-sorted record slot of each permuted pin
@@ -96,6 +97,7 @@ struct FusedNetArgs {
 
 struct FusedGatherArgs {
   int n_obj, blocks;
+  int obj0;                   // first object (the sharded halo mode sums its own slab only)
   const int32_t* obj_slot_ptr;
   const float4* in_f;         // fp32-mode records by slot
   const double* in_fd;

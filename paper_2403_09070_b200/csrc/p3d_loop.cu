@@ -676,8 +676,10 @@ static void launch_k1(const p3d_gp& gp, cudaStream_t s) {
   FusedNetArgs na{};
   na.n_net = gp.topo.n_net;
   na.n_tasks = gp.f_n_tasks;
-  na.task_rank = gp.shard_size > 0 ? gp.shard_rank : 0;  // shard_size 0: the fused loop
-  na.task_size = gp.shard_size > 0 ? gp.shard_size : 1;
+  // shard_size 0: the fused loop; halo mode: this rank's own task list
+  const bool rr = gp.shard_size > 0 && !gp.shard_halo;
+  na.task_rank = rr ? gp.shard_rank : 0;
+  na.task_size = rr ? gp.shard_size : 1;
   na.tasks = reinterpret_cast<const int4*>(gp.f_tasks);
   na.task_t0 = gp.f_task_t0;
   na.n_generic = gp.f_n_generic;
@@ -714,8 +716,13 @@ static void launch_k1b(const p3d_gp& gp, cudaStream_t s) {
   // K1b owner gather (per-instance sums; L1 norms + Eq. 17 scale on one GPU)
   FusedGatherArgs ga{};
   ga.n_obj = gp.n_inst;
+  ga.obj0 = 0;
+  if (gp.shard_size > 0 && gp.shard_halo) {  // own slab only (complete: every net touching it ran here)
+    ga.obj0 = gp.sh_i0;
+    ga.n_obj = gp.sh_i1 - gp.sh_i0;
+  }
   static const int gather_cap = std::max(1, std::min(kMaxBlocks, getenv("P3D_NBLK_GATHER") ? atoi(getenv("P3D_NBLK_GATHER")) : kMaxBlocks));
-  ga.blocks = grid_blocks(gp.n_inst, 256, gather_cap);
+  ga.blocks = grid_blocks(ga.n_obj, 256, gather_cap);
   ga.obj_slot_ptr = gp.topo.obj_slot_ptr;
   ga.in_f = reinterpret_cast<const float4*>(gp.pin_out_f);
   ga.in_fd = gp.pin_out_fd;
@@ -725,7 +732,7 @@ static void launch_k1b(const p3d_gp& gp, cudaStream_t s) {
   ga.counter = &st->counters[kCntGather];
   ga.final_norms = gp.shard_size > 0 ? nullptr : finals + kFinNorm;  // sharded: NORMS stage
   ga.halt = halt;
-  if (gp.n_inst > 0) launch_fused_gather(ga, s);
+  if (ga.n_obj > 0) launch_fused_gather(ga, s);
 }
 
 static int launch_k3(const p3d_gp& gp, cudaStream_t s) {

@@ -401,6 +401,8 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
   using W = typename WaSel<F32>::W;
   using R = typename WaSel<F32>::R;
   const int base = a.net_base[t], deg = a.net_deg[t], stride = a.net_stride[t];
+  const uint8_t nd = a.net_dup[t];
+  const double pm = (nd & 2) ? 0.0 : 1.0;  // value counted by another rank (halo mode)
   Box2 bx, by;
   bx.init();
   by.init();
@@ -419,9 +421,9 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
   const double ey = dmax(fy, by.t.span() + by.b.span());
   const bool sx = (bx.t.span() + bx.b.span()) > fx;
   const bool sy = (by.t.span() + by.b.span()) > fy;
-  acc[3] += ex;
-  acc[4] += ey;
-  acc[5] += (bx.b.cnt > 0 && bx.t.cnt > 0) ? 1.0 : 0.0;
+  acc[3] += pm * ex;
+  acc[4] += pm * ey;
+  acc[5] += pm * ((bx.b.cnt > 0 && bx.t.cnt > 0) ? 1.0 : 0.0);
   const R ig = (R)a.inv_gamma;
   W wx0, wx1, wy0, wy1, wz;
   wx0.init(); wx1.init(); wy0.init(); wy1.init(); wz.init();
@@ -441,10 +443,10 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
     wz.acc(z, zhi, zlo, ep, em, 1);
   }
   wx0.finalize(); wx1.finalize(); wy0.finalize(); wy1.finalize(); wz.finalize();
-  acc[0] += sx ? (wx0.value(bx.b.hi1, bx.b.lo1) + wx1.value(bx.t.hi1, bx.t.lo1)) : wx0.value(bx.fmx(), bx.fmn());
-  acc[1] += sy ? (wy0.value(by.b.hi1, by.b.lo1) + wy1.value(by.t.hi1, by.t.lo1)) : wy0.value(by.fmx(), by.fmn());
-  acc[2] += wz.value(zhi, zlo);
-  const bool dup = a.net_dup[t] != 0;
+  acc[0] += pm * (sx ? (wx0.value(bx.b.hi1, bx.b.lo1) + wx1.value(bx.t.hi1, bx.t.lo1)) : wx0.value(bx.fmx(), bx.fmn()));
+  acc[1] += pm * (sy ? (wy0.value(by.b.hi1, by.b.lo1) + wy1.value(by.t.hi1, by.t.lo1)) : wy0.value(by.fmx(), by.fmn()));
+  acc[2] += pm * wz.value(zhi, zlo);
+  const bool dup = (nd & 1) != 0;
   for (int k = 0; k < deg; ++k) {
     double x, y, z;
     int tp;
@@ -573,9 +575,12 @@ P3D_K1_LOOP_UNROLL
 template <int D, bool F32>
 __device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk, int t0,
                                            WarpCols<F32>& sm, int lane, int& topm, double& zhi,
-                                           double& zlo) {
+                                           double& zlo, double& pm) {
   const int nb = tk.y, j = tk.z + lane;
-  if (j >= nb || a.net_dup[t0 + j]) return false;  // duplicate-owner nets: generic kernel
+  if (j >= nb) return false;
+  const uint8_t nd = a.net_dup[t0 + j];
+  if (nd & 1) return false;  // duplicate-owner nets: generic kernel
+  pm = (nd & 2) ? 0.0 : 1.0;  // value counted by another rank (halo mode)
   const int pin0 = tk.x + j;
   constexpr int KM = D ? D : kMaxStagedDeg;
   const int DD = D ? D : tk.w;
@@ -612,7 +617,7 @@ __device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk,
 template <int D, bool F32>
 __device__ __forceinline__ void staged_eval(const FusedNetArgs& a, int pin0, int nb,
                                             WarpCols<F32>& sm, int lane, int topm, double zhi,
-                                            double zlo, double (&acc)[6], int nd) {
+                                            double zlo, double (&acc)[6], int nd, double pm) {
   using W = typename WaSel<F32>::W;
   using R = typename WaSel<F32>::R;
   const R ig = (R)a.inv_gamma;
@@ -630,7 +635,7 @@ P3D_K1_LOOP_UNROLL
     wz.acc(sm.pz[k][lane], zhi, zlo, ep, em, 1);
   }
   wz.finalize();
-  acc[2] += wz.value(zhi, zlo);
+  acc[2] += pm * wz.value(zhi, zlo);
   const GradK<R> kz = wz.gk(zhi, zlo);
 P3D_K1_LOOP_UNROLL
   for (int k = 0; k < DD; ++k) {
@@ -640,12 +645,12 @@ P3D_K1_LOOP_UNROLL
   double v, ex;
   bool cross;
   staged_axis<D, F32>(sm.px, sm, lane, topm, ig, v, ex, cross, nd);
-  acc[0] += v;
-  acc[3] += ex;
-  acc[5] += cross ? 1.0 : 0.0;
+  acc[0] += pm * v;
+  acc[3] += pm * ex;
+  acc[5] += pm * (cross ? 1.0 : 0.0);
   staged_axis<D, F32>(sm.py, sm, lane, topm, ig, v, ex, cross, nd);
-  acc[1] += v;
-  acc[4] += ex;
+  acc[1] += pm * v;
+  acc[4] += pm * ex;
   int slot[KM];
 #pragma unroll
   for (int k = 0; k < KM; ++k) {
@@ -697,7 +702,10 @@ template <bool F32>
 __device__ __forceinline__ void triple_task(const FusedNetArgs& a, const int4 tk, int t0, int lane,
                                             double (&acc)[6]) {
   const int nb = tk.y, j = tk.z + lane;
-  if (j >= nb || a.net_dup[t0 + j]) return;  // duplicate-owner nets: generic kernel
+  if (j >= nb) return;
+  const uint8_t nd = a.net_dup[t0 + j];
+  if (nd & 1) return;  // duplicate-owner nets: generic kernel
+  const double pm = (nd & 2) ? 0.0 : 1.0;  // value counted by another rank (halo mode)
   const int p0 = tk.x + j;
   int inst[3], slot[3];
   float4 off[3];
@@ -726,13 +734,13 @@ __device__ __forceinline__ void triple_task(const FusedNetArgs& a, const int4 tk
   triple_axis<F32>(x, ig, vx, gx);
   triple_axis<F32>(y, ig, vy, gy);
   triple_axis<F32>(z, ig, vz, gz);
-  acc[0] += vx;
-  acc[1] += vy;
-  acc[2] += vz;
-  acc[3] += dmax(dmax(x[0], x[1]), x[2]) - dmin(dmin(x[0], x[1]), x[2]);  // never split: full
-  acc[4] += dmax(dmax(y[0], y[1]), y[2]) - dmin(dmin(y[0], y[1]), y[2]);
+  acc[0] += pm * vx;
+  acc[1] += pm * vy;
+  acc[2] += pm * vz;
+  acc[3] += pm * (dmax(dmax(x[0], x[1]), x[2]) - dmin(dmin(x[0], x[1]), x[2]));  // never split: full
+  acc[4] += pm * (dmax(dmax(y[0], y[1]), y[2]) - dmin(dmin(y[0], y[1]), y[2]));
   const int ntop = tp[0] + tp[1] + tp[2];
-  acc[5] += (ntop > 0 && ntop < 3) ? 1.0 : 0.0;
+  acc[5] += pm * ((ntop > 0 && ntop < 3) ? 1.0 : 0.0);
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     if (F32) a.out_f[slot[k]] = make_float4((float)gx[k], (float)gy[k], (float)gz[k], 0.f);
@@ -771,7 +779,10 @@ template <bool F32>
 __device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, int t0, int lane,
                                           double (&acc)[6]) {
   const int nb = tk.y, j = tk.z + lane;
-  if (j >= nb || a.net_dup[t0 + j]) return;  // duplicate-owner nets: generic kernel
+  if (j >= nb) return;
+  const uint8_t nd = a.net_dup[t0 + j];
+  if (nd & 1) return;  // duplicate-owner nets: generic kernel
+  const double pm = (nd & 2) ? 0.0 : 1.0;  // value counted by another rank (halo mode)
   const int p0 = tk.x + j, p1 = p0 + nb;
   const int i0 = ld_stream(a.pin_inst + p0), i1 = ld_stream(a.pin_inst + p1);
   const int s0 = ld_stream(a.slot + p0), s1 = ld_stream(a.slot + p1);
@@ -789,12 +800,12 @@ __device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, 
   pair_axis<F32>(x0, x1, ig, vx, gx0, gx1);
   pair_axis<F32>(y0, y1, ig, vy, gy0, gy1);
   pair_axis<F32>(q0.z, q1.z, ig, vz, gz0, gz1);
-  acc[0] += vx;
-  acc[1] += vy;
-  acc[2] += vz;
-  acc[3] += dmax(x0, x1) - dmin(x0, x1);
-  acc[4] += dmax(y0, y1) - dmin(y0, y1);
-  acc[5] += (t0p != t1p) ? 1.0 : 0.0;
+  acc[0] += pm * vx;
+  acc[1] += pm * vy;
+  acc[2] += pm * vz;
+  acc[3] += pm * (dmax(x0, x1) - dmin(x0, x1));
+  acc[4] += pm * (dmax(y0, y1) - dmin(y0, y1));
+  acc[5] += pm * ((t0p != t1p) ? 1.0 : 0.0);
   if (F32) {
     a.out_f[s0] = make_float4((float)gx0, (float)gy0, (float)gz0, 0.f);
     a.out_f[s1] = make_float4((float)gx1, (float)gy1, (float)gz1, 0.f);
@@ -809,9 +820,9 @@ __device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk
                                             WarpCols<F32>& sm, int lane, double (&acc)[6]) {
   const int nd = tk.w;
   int topm;
-  double zhi, zlo;
-  if (stage_pins<D, F32>(a, tk, t0, sm, lane, topm, zhi, zlo))
-    staged_eval<D, F32>(a, tk.x + tk.z + lane, tk.y, sm, lane, topm, zhi, zlo, acc, nd);
+  double zhi, zlo, pm;
+  if (stage_pins<D, F32>(a, tk, t0, sm, lane, topm, zhi, zlo, pm))
+    staged_eval<D, F32>(a, tk.x + tk.z + lane, tk.y, sm, lane, topm, zhi, zlo, acc, nd, pm);
 }
 
 template <bool F32>
@@ -905,7 +916,8 @@ __global__ void __launch_bounds__(256) fused_gather_kernel(FusedGatherArgs a) {
   __shared__ double red[32 * 3];
   double acc[3] = {0, 0, 0};
   const int stride = gridDim.x * blockDim.x;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_obj; i += stride) {
+  for (int il = blockIdx.x * blockDim.x + threadIdx.x; il < a.n_obj; il += stride) {
+    const int i = a.obj0 + il;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     const int b = a.obj_slot_ptr[i], e = a.obj_slot_ptr[i + 1];
     if (a.in_d) {
@@ -974,10 +986,10 @@ __global__ void __launch_bounds__(32 * kGatherWarps) gather_warp_kernel(FusedGat
   double acc[3] = {0, 0, 0};
   const int wstride = gridDim.x * kGatherWarps * 32;
   for (int o0 = (blockIdx.x * kGatherWarps + wib) * 32; o0 < a.n_obj; o0 += wstride) {
-    const int i = o0 + lane;
+    const int il = o0 + lane, i = a.obj0 + il;
     const int last = min(a.n_obj, o0 + 32) - 1;
-    const int b = i <= last ? a.obj_slot_ptr[i] : 0;
-    const int e = i <= last ? a.obj_slot_ptr[i + 1] : 0;
+    const int b = il <= last ? a.obj_slot_ptr[i] : 0;
+    const int e = il <= last ? a.obj_slot_ptr[i + 1] : 0;
     const int rb = __shfl_sync(0xffffffffu, b, 0);
     const int re = __shfl_sync(0xffffffffu, e, last - o0);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -996,7 +1008,7 @@ __global__ void __launch_bounds__(32 * kGatherWarps) gather_warp_kernel(FusedGat
         s0 += ra.x; s1 += ra.y; s2 += rb2.x; s3 += rb2.y;
       }
     }
-    if (i <= last) {
+    if (il <= last) {
       reinterpret_cast<double4*>(a.out)[i] = make_double4(s0, s1, s2, s3);  // [n_obj][4]
       acc[0] += fabs(s0);
       acc[1] += fabs(s1);

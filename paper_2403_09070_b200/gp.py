@@ -271,7 +271,7 @@ class NesterovOptimizer:
 MAX_STAGED_DEG = 6  # kMaxStagedDeg in p3d_wl_fused.cu
 
 
-def fused_pin_layout(net_ptr, pin_inst, off4, dup):
+def fused_pin_layout(net_ptr, pin_inst, off4, dup, net_key=None):
     """Host build of the fused-K1 layout.  Nets are grouped by degree and each
     degree bucket is stored transposed ([pin k][net j]) so a warp owning 32
     nets of a bucket loads pin k of all of them in one transaction.  Returns a
@@ -279,11 +279,13 @@ def fused_pin_layout(net_ptr, pin_inst, off4, dup):
     stride, dup), permuted per-pin (owner, float32 offsets, owner-sorted record
     slot) and, per original pin, its permuted index.  Records are written at
     their owner-sorted slot (stable: original pin order within an owner, like
-    bincount), so the owner gather streams them."""
+    bincount), so the owner gather streams them.  net_key (sharded halo mode):
+    a secondary sort key inside each degree bucket, so nets evaluated by the
+    same set of ranks share warp tasks."""
     net_ptr = np.asarray(net_ptr, dtype=np.int64)
     deg = np.diff(net_ptr)
     n_net = len(deg)
-    order = np.argsort(deg, kind="stable")
+    order = np.argsort(deg, kind="stable") if net_key is None else np.lexsort((net_key, deg))
     dsorted = deg[order]
     base = np.zeros(n_net, dtype=np.int64)
     stride = np.ones(n_net, dtype=np.int64)
@@ -325,7 +327,7 @@ def fused_pin_layout(net_ptr, pin_inst, off4, dup):
                 task_t0=np.asarray(t0s, dtype=np.int64), net_base=base, net_deg=dsorted,
                 net_stride=stride, net_dup=np.asarray(dup, bool)[order], pin_inst=f_inst,
                 pin_off=f_off, pin_slot=pin_slot, dest=dest,
-                generic=np.asarray(generic, dtype=np.int64))
+                generic=np.asarray(generic, dtype=np.int64), order=order)
 
 
 def _with_dup_nets(layout):
@@ -385,9 +387,31 @@ class Gp3dProblem:
         self.max_iters = int(cfg.max_iters if max_iters is None else max_iters)
         self.min_step = float(min_step)
         # shard: None (fused single-GPU loop) or (rank, world) for shard.ShardedGp3d
+        # shard: (rank, world) deals K1 tasks round-robin; (rank, world, HaloPlan)
+        # runs this rank's own nets (partition.py) in halo mode
         self.sharded = shard is not None
         self.shard_rank, self.shard_size = (int(shard[0]), int(shard[1])) if shard else (0, 1)
+        self.plan = shard[2] if shard is not None and len(shard) > 2 else None
         self._build()
+
+    def _halo_filter(self, L):
+        """Halo mode: keep the warp tasks / generic nets holding a net that
+        touches this rank's slab; mark (bit 1 of the dup byte) the nets whose
+        value another rank counts."""
+        mask, prim = self.plan.nets_of(self.shard_rank)
+        order = L["order"]
+        m_perm = mask[order]
+        keep = []
+        for k, (pos, nb, j0, D) in enumerate(L["tasks"]):
+            t0 = int(L["task_t0"][k])
+            if m_perm[t0 + j0: t0 + min(nb, j0 + 32)].any():
+                keep.append(k)
+        keep = np.asarray(keep, dtype=np.int64)
+        L["tasks"] = L["tasks"][keep].reshape(-1, 4)
+        L["task_t0"] = L["task_t0"][keep]
+        L["generic"] = L["generic"][m_perm[L["generic"]]] if len(L["generic"]) else L["generic"]
+        L["net_dup"] = (np.asarray(L["net_dup"], dtype=np.uint8) |
+                        ((~prim[order]).astype(np.uint8) << 1))
 
     # -- device descriptor -------------------------------------------------
     def _build(self):
@@ -408,6 +432,7 @@ class Gp3dProblem:
         g.shard_rank, g.shard_size = r, (R if self.sharded else 0)
         # WL and density branches concurrently inside the iteration graph
         g.overlap = int(os.environ.get("P3D_OVERLAP", "1")) if not self.sharded else 0
+        g.shard_halo = 1 if self.plan is not None else 0
         g.sh_i0, g.sh_i1 = self.sh_i
         g.sh_f0, g.sh_f1 = self.sh_f
         macro_ids = macro_ids[(macro_ids >= self.sh_i[0]) & (macro_ids < self.sh_i[1])]
@@ -430,8 +455,15 @@ class Gp3dProblem:
                                tp.net_order, tp.pin_slot, tp.obj_slot_ptr)
         g.wl_f32 = 1 if self.precision == "fp32" else 0
         off4 = wl.rotated_pin_offsets(arr, self.rot) if P else np.zeros((0, 4))
+        key = None
+        if self.plan is not None:  # group nets by (primary rank, set of ranks touching them)
+            key = self.plan.primary * (1 << R)
+            for q in range(R):
+                key = key + (self.plan.touches[q].astype(np.int64) << q)
         L = self.layout = _with_dup_nets(
-            fused_pin_layout(arr.net_ptr, arr.pin_inst, off4, arr.net_has_dup_inst))
+            fused_pin_layout(arr.net_ptr, arr.pin_inst, off4, arr.net_has_dup_inst, net_key=key))
+        if self.plan is not None:
+            self._halo_filter(L)
         one = lambda a, dt_: a if len(a) else np.zeros(1, dt_)  # noqa: E731
         g.f_n_tasks = len(L["tasks"])
         g.f_n_generic = len(L["generic"])
@@ -441,7 +473,7 @@ class Gp3dProblem:
         g.f_net_base = keep(_dev.i32(one(L["net_base"], np.int64)))
         g.f_net_deg = keep(_dev.i32(one(L["net_deg"], np.int64)))
         g.f_net_stride = keep(_dev.i32(one(L["net_stride"], np.int64)))
-        g.f_net_dup = keep(_dev.u8(one(L["net_dup"], bool)))
+        g.f_net_dup = keep(_dev.u8(one(L["net_dup"].astype(np.uint8), np.uint8)))
         g.f_pin_inst = keep(_dev.i32(one(L["pin_inst"], np.int64)))
         g.f_pin_off = keep(_dev.dev(one(L["pin_off"].reshape(-1), np.float32), torch.float32))
         g.f_pin_slot = keep(_dev.i32(one(L["pin_slot"], np.int64)))

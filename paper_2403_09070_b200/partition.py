@@ -1,0 +1,136 @@
+"""Partition of one placement over the ranks of the sharded loop.
+
+Two host-side steps, both on the netlist alone (they run once per run):
+
+* ``locality_order``: an instance numbering in which connected instances sit
+  next to each other, by label propagation over the netlist's clique
+  expansion (each pin pair of a net weighted 1 / (degree - 1), the usual
+  net model): every instance repeatedly adopts the label with the largest
+  total weight among its net neighbours, so the netlist's clusters (the
+  ~40-instance clusters of the synthetic generator, synth.py:145-157; the
+  modules of a real design) collapse onto single labels, and sorting by label
+  makes them contiguous.  Contiguous instance slabs then hold whole clusters,
+  and only the nets that genuinely span clusters cross ranks.
+* ``HaloPlan``: with instance slabs fixed, each rank evaluates every net
+  that touches its slab (a net spanning k ranks is evaluated on each of them,
+  each keeping the gradients of its own pins), so the per-instance WL sums
+  need no exchange at all; the net's value, exact WL and crossing flag are
+  counted by its primary rank only (the owner of its first pin).  What each
+  rank then needs from the others is the positions of the remote instances
+  of its nets (its halo): static lists, exchanged once per iteration after
+  the step (``ShardedGp3d``), instead of every position on every rank.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def locality_order(net_ptr, pin_inst, n_inst, sweeps=30, seed=0):
+    """Permutation `perm` (new index -> old index) grouping connected
+    instances (label propagation, see module docstring)."""
+    net_ptr = np.asarray(net_ptr, dtype=np.int64)
+    pin_inst = np.asarray(pin_inst, dtype=np.int64)
+    deg = np.diff(net_ptr)
+    if n_inst == 0 or len(pin_inst) == 0:
+        return np.arange(n_inst, dtype=np.int64)
+    # clique expansion: (a, b, w) for every ordered pin pair of a net
+    pin_net = np.repeat(np.arange(len(deg)), deg)
+    a_list, b_list, w_list = [], [], []
+    for d in np.unique(deg):
+        if d < 2:
+            continue
+        nets = np.flatnonzero(deg == d)
+        base = net_ptr[nets]
+        pins = pin_inst[base[:, None] + np.arange(d)[None, :]]  # [n_d, d]
+        ii, jj = np.nonzero(~np.eye(d, dtype=bool))
+        a_list.append(pins[:, ii].reshape(-1))
+        b_list.append(pins[:, jj].reshape(-1))
+        w_list.append(np.full(len(nets) * len(ii), 1.0 / (d - 1)))
+    del pin_net
+    if not a_list:
+        return np.arange(n_inst, dtype=np.int64)
+    a = np.concatenate(a_list)
+    b = np.concatenate(b_list)
+    w = np.concatenate(w_list)
+    keep = a != b
+    a, b, w = a[keep], b[keep], w[keep]
+    rs = np.random.default_rng(seed)
+    label = np.arange(n_inst, dtype=np.int64)
+    for _ in range(sweeps):
+        lb = label[b]
+        # total weight per (instance, neighbour label); ties broken by a random
+        # rank per label (fixed seed: deterministic)
+        key = a * (n_inst + 1) + lb
+        order = np.argsort(key, kind="stable")
+        ks = key[order]
+        first = np.flatnonzero(np.r_[True, ks[1:] != ks[:-1]])
+        tot = np.add.reduceat(w[order], first)
+        inst = ks[first] // (n_inst + 1)
+        lab = ks[first] % (n_inst + 1)
+        jitter = rs.random(n_inst + 1)[lab] * 1e-9
+        # best label per instance: sort by (instance, -weight)
+        o2 = np.lexsort((-(tot + jitter), inst))
+        best_first = np.flatnonzero(np.r_[True, inst[o2][1:] != inst[o2][:-1]])
+        # semi-synchronous: a random half of the instances adopts its best
+        # label per sweep (fully synchronous updates oscillate between
+        # neighbouring labels)
+        upd = inst[o2][best_first]
+        take = rs.random(len(upd)) < 0.5
+        new = label.copy()
+        new[upd[take]] = lab[o2][best_first][take]
+        changed = int(np.count_nonzero(new != label))
+        label = new
+        if changed <= n_inst // 1000:
+            break
+    return np.lexsort((np.arange(n_inst), label)).astype(np.int64)
+
+
+class HaloPlan:
+    """Per-rank net sets and position halos of the sharded loop (module
+    docstring).  Instance slabs: rank r owns [r * slab, (r + 1) * slab)."""
+
+    def __init__(self, net_ptr, pin_inst, n_inst, world, slab):
+        net_ptr = np.asarray(net_ptr, dtype=np.int64)
+        pin_inst = np.asarray(pin_inst, dtype=np.int64)
+        self.world, self.slab, self.n_inst = int(world), int(slab), int(n_inst)
+        deg = np.diff(net_ptr)
+        n_net = len(deg)
+        pin_net = np.repeat(np.arange(n_net), deg)
+        owner = pin_inst // max(slab, 1)
+        self.primary = np.full(n_net, -1, dtype=np.int64)
+        has = deg > 0
+        self.primary[has] = owner[net_ptr[:-1][has]]  # the owner of the net's first pin
+        # touches[r]: nets with a pin in slab r
+        self.touches = []
+        self.halo = []
+        for r in range(world):
+            t = np.zeros(n_net, dtype=bool)
+            t[pin_net[owner == r]] = True
+            self.touches.append(t)
+            pins = np.flatnonzero(t[pin_net])
+            inst = np.unique(pin_inst[pins])
+            self.halo.append(inst[(inst // max(slab, 1)) != r])
+        # send[r][s]: instances of slab r that rank s needs (sorted)
+        self.send = [[self.halo[s][(self.halo[s] // max(slab, 1)) == r] if s != r
+                      else np.zeros(0, dtype=np.int64) for s in range(world)]
+                     for r in range(world)]
+
+    def nets_of(self, rank):
+        """(net mask evaluated by `rank`, mask of those it counts the value of)."""
+        t = self.touches[rank]
+        return t, t & (self.primary == rank)
+
+    def exchange_bytes(self, rank, bytes_per_inst=32):
+        """Position bytes received per iteration by `rank` (pos4 rows)."""
+        return int(len(self.halo[rank]) * bytes_per_inst)
+
+    def split_sizes(self, rank):
+        """(input splits: rows sent to each rank, output splits: rows received
+        from each rank) of the all-to-all halo exchange."""
+        ins = [len(self.send[rank][s]) for s in range(self.world)]
+        outs = [len(self.send[s][rank]) for s in range(self.world)]
+        return ins, outs
+
+
+__all__ = ["HaloPlan", "locality_order"]

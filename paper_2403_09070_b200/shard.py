@@ -1,6 +1,23 @@
 """Sharded GP loop (north_star's config-4 path): one placement
 partitioned over the ranks of a torch.distributed group, one GPU per rank.
 
+Default (halo mode, partition.py): instances are renumbered so connected
+instances are contiguous (label propagation over the netlist), each rank owns
+an instance slab and evaluates every net touching it (a net spanning several
+ranks runs on each, each keeping its own pins' gradients; its value is counted
+once, by its first pin's owner), so the per-instance WL sums are complete on
+their owner and only three exchanges remain per iteration:
+
+    [all-reduce]   the three L1 norms (Eq. 17)
+    [all-reduce]   rho, int64 fixed point (exact: the single-GPU map bit for bit)
+    [all-reduce]   the density totals, |v_new - v|^2, (iteration 0) max |g|
+    [all-to-all]   positions of the halo: each rank receives the pos4 rows of the
+                   remote instances of its nets (static lists) -- instead of every
+                   position on every rank
+
+The round-robin mode (halo=False) below deals the K1 warp tasks round-robin
+and exchanges full per-instance arrays:
+
 Each rank owns a slab of instances (equal padded size), a slab of fillers and
 the K1 warp tasks w with w % world == rank.  Per iteration (gp.py:386-444):
 
@@ -37,7 +54,10 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
+from .dist import object_slabs
 from .gp import Gp3dProblem
+from .model import ArrayDesign, NetlistArrays
+from .partition import HaloPlan, locality_order
 
 STAGE = {name: k for k, name in enumerate(_lib.SH_STAGES)}
 
@@ -78,6 +98,19 @@ class ShardComm:
             dist.all_reduce(h)
             mine.copy_(h[self.rank * n:(self.rank + 1) * n])
 
+    def all_to_all_rows(self, out, inp, out_splits, in_splits):
+        """out (rows grouped by source rank) <- rows of inp grouped by
+        destination rank (uneven splits)."""
+        if not self.on:
+            out.copy_(inp)
+            return
+        if self.nccl:
+            dist.all_to_all_single(out, inp, out_splits, in_splits)
+        else:
+            h = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_to_all_single(h, inp.cpu(), out_splits, in_splits)
+            out.copy_(h)
+
     def all_gather_chunks(self, buf, n):
         """buf[:world*n] <- concatenation of every rank's chunk buf[r*n:(r+1)*n]."""
         if not self.on or n == 0:
@@ -96,22 +129,87 @@ class ShardedGp3d:
     """run_gp3d's device loop partitioned over the process group."""
 
     def __init__(self, design, grid, fillers, cfg, rot, max_iters=None, precision=None,
-                 comm=None):
+                 comm=None, halo=True):
         self.comm = comm or ShardComm()
+        self.halo = bool(halo)
+        R, r = self.comm.world, self.comm.rank
+        arr = design.arrays()
+        I = design.n_insts
+        self.perm = self.inv = None
+        if self.halo:
+            # locality numbering (every rank computes the same, deterministic one)
+            perm = locality_order(arr.net_ptr, arr.pin_inst, I)
+            inv = np.empty_like(perm)
+            inv[perm] = np.arange(I)
+            self.perm, self.inv = perm, inv
+            pa = NetlistArrays(is_macro=arr.is_macro[perm], w_top=arr.w_top[perm],
+                               h_top=arr.h_top[perm], w_bot=arr.w_bot[perm],
+                               h_bot=arr.h_bot[perm], net_ptr=arr.net_ptr,
+                               pin_inst=inv[arr.pin_inst], ox_top=arr.ox_top,
+                               oy_top=arr.oy_top, ox_bot=arr.ox_bot, oy_bot=arr.oy_bot)
+            design = ArrayDesign(design.die, design.hbt, pa)
+            rot = np.asarray(rot)[perm]
+            slab, _, _ = object_slabs(I, fillers.count, r, R)
+            self.plan = HaloPlan(pa.net_ptr, pa.pin_inst, I, R, slab)
+            shard = (r, R, self.plan)
+        else:
+            self.plan = None
+            shard = (r, R)
         self.prob = Gp3dProblem(design, grid, fillers, cfg, rot, max_iters=max_iters,
-                                precision=precision, shard=(self.comm.rank, self.comm.world))
+                                precision=precision, shard=shard)
         p = self.prob
         off = _lib.LoopState.dv2_next.offset
         self._dv2 = p.t_st[off: off + 8].view(torch.float64)
         self._tot16 = p.t_shard_tot[:16]
         self._tot_max = p.t_shard_tot[16:17]
         self._norms = p.t_shard_tot[20:23]
+        if self.halo:
+            pl = self.plan
+            self._in_splits, self._out_splits = pl.split_sizes(r)
+            cat = lambda xs: np.concatenate(xs) if len(xs) else np.zeros(0, np.int64)  # noqa: E731
+            self._send_idx = torch.from_numpy(cat(pl.send[r]).astype(np.int64)).cuda()
+            self._recv_idx = torch.from_numpy(cat([pl.send[q][r] for q in range(R)])
+                                              .astype(np.int64)).cuda()
+            self._pos4 = p.t_pos4.view(-1, 4)
+            self._send = torch.empty((len(self._send_idx), 4), dtype=torch.float64, device="cuda")
+            self._recv = torch.empty((len(self._recv_idx), 4), dtype=torch.float64, device="cuda")
+
+    def exchange_bytes(self):
+        """Bytes this rank receives per iteration through its collectives
+        (data-path exchanges: owner sums, rho, positions; scalars excluded)."""
+        p = self.prob
+        rho = 8 * p.grid.n_bins
+        if self.halo:
+            return {"positions_halo": int(len(self._recv_idx) * 32), "rho_allreduce": rho}
+        slab = 32 * p.inst_slab
+        return {"owner_sums_reduce_scatter": slab * self.comm.world,
+                "positions_allgather": slab * self.comm.world, "rho_allreduce": rho}
+
+    def _halo_exchange(self):
+        """pos4 rows of this rank's halo from their owners (all-to-all)."""
+        if not self.comm.on:
+            return
+        torch.index_select(self._pos4, 0, self._send_idx, out=self._send)
+        self.comm.all_to_all_rows(self._recv, self._send, self._out_splits, self._in_splits)
+        self._pos4.index_copy_(0, self._recv_idx, self._recv)
 
     def _stage(self, name):
         _lib.call("p3d_gp_shard_stage", _lib.byref(self.prob.gp), STAGE[name], _lib.stream_ptr())
 
     def init_loop(self, pos0):
-        self.prob.init_loop(pos0)
+        # every rank starts from the same positions, so pos4 starts complete
+        self.prob.init_loop(self._to_local(pos0))
+
+    def _to_local(self, pos):
+        """[O,3] positions in the caller's instance order -> the loop's order."""
+        if self.perm is None:
+            return pos
+        I = self.prob.n_inst
+        if isinstance(pos, torch.Tensor):
+            idx = torch.from_numpy(self.perm).to(pos.device)
+            return torch.cat([pos[:I][idx], pos[I:]])
+        pos = np.asarray(pos)
+        return np.concatenate([pos[:I][self.perm], pos[I:]])
 
     def iterate(self, n=1, marks=None):
         """n sharded iterations; `marks` (a list) collects (label, cuda Event)
@@ -124,23 +222,40 @@ class ShardedGp3d:
                 e.record()
                 marks.append((label, e))
 
+        # nccl: the density branch (K2, the rho all-reduce, K3) runs on a side
+        # stream next to K1 (they are independent until K4), as in the fused
+        # loop; every rank issues the collectives in the same program order
+        overlap = c.nccl and marks is None
+        if overlap and not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream()
         for _ in range(n):
             mark("start")
+            if overlap:
+                main = torch.cuda.current_stream()
+                self._side.wait_stream(main)
+                with torch.cuda.stream(self._side):
+                    self._stage("SCATTER")
+                    c.all_reduce(p.t_rho_fx)
+                    self._stage("SPECTRAL")
             self._stage("NET")
             self._stage("GATHER")
             mark("K1")
-            c.reduce_scatter_chunks(p.t_inst_g, 4 * p.inst_slab)  # own instance slab
+            if not self.halo:
+                c.reduce_scatter_chunks(p.t_inst_g, 4 * p.inst_slab)  # own instance slab
             mark("comm")
             self._stage("NORMS")
             c.all_reduce(self._norms)
             self._stage("NORMS_FINAL")
             mark("comm")
-            self._stage("SCATTER")
-            mark("K2")
-            c.all_reduce(p.t_rho_fx)
-            mark("comm")
-            self._stage("SPECTRAL")
-            mark("K3")
+            if overlap:
+                main.wait_stream(self._side)
+            else:
+                self._stage("SCATTER")
+                mark("K2")
+                c.all_reduce(p.t_rho_fx)
+                mark("comm")
+                self._stage("SPECTRAL")
+                mark("K3")
             self._stage("DENS")
             mark("K4")
             c.all_reduce(self._tot16)
@@ -152,7 +267,10 @@ class ShardedGp3d:
             self._stage("ADVANCE")
             mark("K5")
             c.all_reduce(self._dv2)
-            c.all_gather_chunks(p.t_pos4, 4 * p.inst_slab)
+            if self.halo:
+                self._halo_exchange()
+            else:
+                c.all_gather_chunks(p.t_pos4, 4 * p.inst_slab)
             mark("comm")
 
     @staticmethod
@@ -206,7 +324,14 @@ class ShardedGp3d:
             for c in range(3):
                 full[c * O + lo: c * O + hi] = src[c * O + lo: c * O + hi]
         self.comm.all_reduce(full)  # disjoint slabs: the sum is exact
-        return full.reshape(3, O).t().contiguous()
+        out = full.reshape(3, O).t().contiguous()
+        if self.perm is not None:  # back to the caller's instance order
+            I = p.n_inst
+            res = out.clone()
+            res[torch.from_numpy(self.perm).to(out.device)] = out[:I]
+            res[I:] = out[I:]
+            out = res
+        return out
 
     def log_rows(self, n):
         return self.prob.log_rows(n)
