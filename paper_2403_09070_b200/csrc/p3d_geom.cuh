@@ -276,6 +276,17 @@ __device__ __forceinline__ void gather_object(const Charge& q, const p3d_grid& g
   const Footprint f = footprint(q, g);
   double tot = 0.0, a[4] = {0.0, 0.0, 0.0, 0.0};
   const double4* m4 = reinterpret_cast<const double4*>(maps);
+#ifndef P3D_SMALL2
+#define P3D_SMALL2 1
+#endif
+#if P3D_SMALL2
+  // 2 x 2 x 2 first (every cell and filler of the BASELINE configs): the
+  // unrolled 3 x 3 x 2 set issues its guarded-off slots too.  Same terms in
+  // the same order, so the same sums.
+  if (f.ax.i1 - f.ax.i0 < 2 && f.ay.i1 - f.ay.i0 < 2 && f.az.i1 - f.az.i0 < 2)
+    gather_small<2, 2, 2>(f, g, m4, tot, a);
+  else
+#endif
   if (f.ax.i1 - f.ax.i0 < 3 && f.ay.i1 - f.ay.i0 < 3 && f.az.i1 - f.az.i0 < 2)
     gather_small<3, 3, 2>(f, g, m4, tot, a);
   else
