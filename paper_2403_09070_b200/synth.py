@@ -203,7 +203,8 @@ CONFIGS = {
 def cached_synth(spec: SynthSpec, cache_dir=None) -> ArrayDesign:
     """``synth_arrays`` with an on-disk npz cache (setup of config 3 is ~25 s)."""
     if cache_dir is None:
-        cache_dir = os.environ.get("P3D_CACHE", os.path.join(os.path.dirname(__file__), "..", ".cache"))
+        # outside the repo: the snapshot shipped to the GPU box must stay small
+        cache_dir = os.environ.get("P3D_CACHE", "/tmp/p3d_cache")
     key = "|".join(f"{k}={v}" for k, v in sorted(asdict(spec).items()))
     import hashlib
     h = hashlib.sha1(key.encode()).hexdigest()[:12]
