@@ -577,6 +577,26 @@ def main():
             stage += np.frombuffer(buf, dtype=np.float32)
         stage /= K
         kpi = _lib.load().p3d_gp_kernels_per_iteration(_lib.byref(prob.gp))
+        # the production (overlapped) iteration's critical path, from event
+        # nodes at its branch points inside a replayed graph
+        crit = None
+        if prob.gp.overlap:
+            tb = (C.c_float * 7)()
+            og = torch.cuda.CUDAGraph()
+            side.wait_stream(stream)
+            with torch.cuda.stream(side), torch.cuda.graph(og, stream=side):
+                _lib.call("p3d_gp_iterate_marked_overlap", _lib.byref(prob.gp), _lib.stream_ptr())
+            stream.wait_stream(side)
+            acc = np.zeros(7)
+            for _ in range(K):
+                og.replay()
+                torch.cuda.synchronize()
+                _lib.call("p3d_gp_overlap_times", tb)
+                acc += np.frombuffer(tb, dtype=np.float32)
+            acc = acc / K * 1000.0
+            crit = {"wl_branch_K1_K1b": round(acc[1], 1), "of_which_K1": round(acc[0], 1),
+                    "density_branch_K2_K3": round(acc[3], 1), "of_which_K2": round(acc[2], 1),
+                    "K4_end": round(acc[4], 1), "K5_end": round(acc[6], 1)}
     else:
         kpi = _lib.load().p3d_gp_kernels_per_iteration(_lib.byref(prob.gp)) + 3
         marks = []
@@ -648,6 +668,8 @@ def main():
         "final_row": list(prob.log_rows(W + K)[-1]),
     }
     line["parity"] = parity_vs_reference(args.config, max_iters, line["final_row"])
+    if mode != "sharded" and crit is not None:
+        line["critical_path_us"] = crit
     line["roofline"] = roofline_of(design, prob.n_fill, grid, stage, args.config,
                                    shards=world if mode == "sharded" else 1)
     if mode == "sharded":  # rank 0's stage attribution of one shard (eager replay)

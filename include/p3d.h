@@ -479,6 +479,12 @@ int p3d_gp_iterate_profiled(const p3d_gp* gp, void* stream, float* stage_ms);
  * and returns the 7 stage durations (ms, HOST float[7]) of the most recent
  * marked iteration (e.g. a replayed graph). */
 int p3d_gp_iterate_marked(const p3d_gp* gp, void* stream);
+/* The overlapped (production) iteration with event-record nodes at its branch
+ * points (graph-capturable, descriptors with overlap set); then
+ * p3d_gp_overlap_times(t[7]): ms from the fork to the end of K1, K1b (WL
+ * branch), K2, K3 (density branch), K4, K5a, K5b. */
+int p3d_gp_iterate_marked_overlap(const p3d_gp* gp, void* stream);
+int p3d_gp_overlap_times(float* t);
 int p3d_gp_stage_times(float* stage_ms);
 /* Number of kernels one p3d_gp_iterate enqueues (>0), or -1 on bad input. */
 int p3d_gp_kernels_per_iteration(const p3d_gp* gp);

@@ -152,6 +152,8 @@ _SIGS = {
     "p3d_gp_iterate_profiled": (I32, [P, P, P]),
     "p3d_gp_kernels_per_iteration": (I32, [P]),
     "p3d_gp_iterate_marked": (I32, [P, P]),
+    "p3d_gp_iterate_marked_overlap": (I32, [P, P]),
+    "p3d_gp_overlap_times": (I32, [P]),
     "p3d_gp_stage_times": (I32, [P]),
 }
 

@@ -49,6 +49,8 @@ void launch_normalize(int n, const double* gx, const double* gy, const double* g
                       const double* gzh, double alpha, double* out, double* scratch,
                       cudaStream_t s);
 int gp_iterate(const p3d_gp& gp, cudaStream_t s);
+int gp_iterate_marked_overlap(const p3d_gp& gp, cudaStream_t s);
+int gp_overlap_times(float* t);
 int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s);
 int gp_init(const p3d_gp& gp, const double* pos0, cudaStream_t s);
 int gp_project(const p3d_gp& gp, const double* in, double* out, cudaStream_t s);
@@ -569,6 +571,17 @@ int p3d_gp_iterate(const p3d_gp* gp, void* stream) {
 int p3d_gp_iterate_profiled(const p3d_gp* gp, void* stream, float* stage_ms) {
   if (bad_gp(gp) || !stage_ms) return P3D_ERR_ARG;
   return gp_iterate_profiled(*gp, STREAM(stream), stage_ms);
+}
+
+int p3d_gp_iterate_marked_overlap(const p3d_gp* gp, void* stream) {
+  if (bad_gp(gp)) return P3D_ERR_ARG;
+  if (!gp->overlap) { set_error("gp_iterate_marked_overlap: descriptor without overlap"); return P3D_ERR_ARG; }
+  return gp_iterate_marked_overlap(*gp, STREAM(stream));
+}
+
+int p3d_gp_overlap_times(float* t) {
+  if (!t) return P3D_ERR_ARG;
+  return gp_overlap_times(t);
 }
 
 int p3d_gp_iterate_marked(const p3d_gp* gp, void* stream) {

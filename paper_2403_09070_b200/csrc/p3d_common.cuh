@@ -2,6 +2,8 @@
 // See DESIGN.md for the HBM layout and include/p3d.h for the C-ABI.
 #pragma once
 
+#include <stdlib.h>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -42,6 +44,28 @@ __device__ __forceinline__ void pdl_wait() {
 #if P3D_PDL
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
+}
+
+// P3D_NOPDL (environment, A/B only): bitmask of launch groups started without
+// the PDL attribute (1 K1 net, 2 K1b gather, 4 K2, 8 K3, 16 K4, 32 K5a, 64 K5b)
+inline int nopdl_mask() {
+  static const int m = getenv("P3D_NOPDL") ? atoi(getenv("P3D_NOPDL")) : 0;
+  return m;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch_tag(int tag, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                                  size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = P3D_PDL && !(nopdl_mask() & tag);
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 template <typename... KArgs, typename... Args>

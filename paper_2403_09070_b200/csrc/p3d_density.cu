@@ -458,12 +458,12 @@ void launch_scatter_tiled(const CloudGP& cl, int n, int n_macro, const int32_t* 
                           cudaStream_t s) {
   unsigned long long* r = reinterpret_cast<unsigned long long*>(rho);
   const int nb = grid_blocks(n, 256, 148 * 8);
-  pdl_launch(tile_hist_kernel<CloudGP>, n_macro * kMacroSplit + nb, 256, ts.n_tiles * sizeof(int), s, cl, n, g,
+  pdl_launch_tag(4, tile_hist_kernel<CloudGP>, n_macro * kMacroSplit + nb, 256, ts.n_tiles * sizeof(int), s, cl, n, g,
              ts, macro_ids, n_macro, r, halt);
   const int np = (n + 256 * kPlacePerThread - 1) / (256 * kPlacePerThread);
-  pdl_launch(tile_place_kernel<CloudGP>, np, 256, 2 * ts.n_tiles * sizeof(int), s, cl, n, ts, halt);
+  pdl_launch_tag(4, tile_place_kernel<CloudGP>, np, 256, 2 * ts.n_tiles * sizeof(int), s, cl, n, ts, halt);
   const int chunks = (n + kChunk - 1) / kChunk;
-  pdl_launch(scatter_tiled_kernel, chunks, 256, kBoxBins * 8, s, g, ts, cl, r, halt);
+  pdl_launch_tag(4, scatter_tiled_kernel, chunks, 256, kBoxBins * 8, s, g, ts, cl, r, halt);
 }
 
 template void launch_scatter<CloudGP>(const CloudGP&, int, int, const int32_t*, const p3d_grid&,

@@ -769,7 +769,7 @@ static int eval_kernels(const p3d_gp& gp, cudaStream_t s, cudaEvent_t* ev = null
   mark(3);
   if (const int rc = launch_k3(gp, s)) return rc;  // K3 (+ overflow, re-zero)
   mark(4);
-  pdl_launch(dens_kernel, gp.n_macro + gp.nblk_dens, 256, 0, s, gp);  // K4
+  pdl_launch_tag(16, dens_kernel, gp.n_macro + gp.nblk_dens, 256, 0, s, gp);  // K4
   mark(5);
   return check_launch("gp evaluation kernels");
 }
@@ -820,14 +820,14 @@ static int eval_kernels_overlap(const p3d_gp& gp, cudaStream_t s) {
   if (!(skip & 2)) launch_k1b(gp, s);
   cudaEventRecord(f.join, f.side);
   cudaStreamWaitEvent(s, f.join, 0);
-  pdl_launch(dens_kernel, gp.n_macro + gp.nblk_dens, 256, 0, s, gp);
+  pdl_launch_tag(16, dens_kernel, gp.n_macro + gp.nblk_dens, 256, 0, s, gp);
   return check_launch("gp evaluation kernels (overlapped)");
 }
 
 int gp_iterate(const p3d_gp& gp, cudaStream_t s) {
   if (const int rc = gp.overlap ? eval_kernels_overlap(gp, s) : eval_kernels(gp, s)) return rc;
-  pdl_launch(gmax0_kernel, gp.nblk_obj, 256, 0, s, gp);
-  pdl_launch(advance_kernel, gp.nblk_obj, 256, 0, s, gp);
+  pdl_launch_tag(32, gmax0_kernel, gp.nblk_obj, 256, 0, s, gp);
+  pdl_launch_tag(64, advance_kernel, gp.nblk_obj, 256, 0, s, gp);
   return check_launch("gp_iterate");
 }
 
@@ -838,9 +838,9 @@ int gp_iterate_profiled(const p3d_gp& gp, cudaStream_t s, float* ms) {
   if (!ev[0])
     for (int k = 0; k < 8; ++k) cudaEventCreate(&ev[k]);
   if (const int rc = eval_kernels(gp, s, ev)) return rc;
-  pdl_launch(gmax0_kernel, gp.nblk_obj, 256, 0, s, gp);
+  pdl_launch_tag(32, gmax0_kernel, gp.nblk_obj, 256, 0, s, gp);
   cudaEventRecord(ev[6], s);
-  pdl_launch(advance_kernel, gp.nblk_obj, 256, 0, s, gp);
+  pdl_launch_tag(64, advance_kernel, gp.nblk_obj, 256, 0, s, gp);
   cudaEventRecord(ev[7], s);
   cudaEventSynchronize(ev[7]);
   for (int k = 0; k < 7; ++k) cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]);
@@ -856,11 +856,53 @@ int gp_iterate_marked(const p3d_gp& gp, cudaStream_t s) {
   if (!g_marks[0])
     for (int k = 0; k < 8; ++k) cudaEventCreate(&g_marks[k]);
   if (const int rc = eval_kernels(gp, s, g_marks, true)) return rc;
-  pdl_launch(gmax0_kernel, gp.nblk_obj, 256, 0, s, gp);
+  pdl_launch_tag(32, gmax0_kernel, gp.nblk_obj, 256, 0, s, gp);
   cudaEventRecordWithFlags(g_marks[6], s, cudaEventRecordExternal);
-  pdl_launch(advance_kernel, gp.nblk_obj, 256, 0, s, gp);
+  pdl_launch_tag(64, advance_kernel, gp.nblk_obj, 256, 0, s, gp);
   cudaEventRecordWithFlags(g_marks[7], s, cudaEventRecordExternal);
   return check_launch("gp_iterate_marked");
+}
+
+// The overlapped iteration with event-record nodes at the branch points
+// (graph-capturable): t[k] = ms from the fork to mark k, k = 1 K1 net done,
+// 2 K1b done (WL branch), 3 K2 done, 4 K3 done (density branch), 5 K4 done,
+// 6 K5a done, 7 K5b done -- the iteration's critical path as it runs
+// (the per-stage times above are taken on the serialised variant).
+static cudaEvent_t g_omarks[8] = {nullptr};
+
+int gp_iterate_marked_overlap(const p3d_gp& gp, cudaStream_t s) {
+  if (!g_omarks[0])
+    for (int k = 0; k < 8; ++k) cudaEventCreate(&g_omarks[k]);
+  ForkJoin& f = fork_join();
+  if (!f.side) return P3D_ERR_ARG;
+  auto mark = [&](int k, cudaStream_t st) { cudaEventRecordWithFlags(g_omarks[k], st, cudaEventRecordExternal); };
+  mark(0, s);
+  cudaEventRecord(f.fork, s);
+  cudaStreamWaitEvent(f.side, f.fork, 0);
+  scatter_k2(gp, &gp.st->done, f.side);
+  mark(3, f.side);
+  if (const int rc = launch_k3(gp, f.side)) return rc;
+  mark(4, f.side);
+  launch_k1(gp, s);
+  mark(1, s);
+  launch_k1b(gp, s);
+  mark(2, s);
+  cudaEventRecord(f.join, f.side);
+  cudaStreamWaitEvent(s, f.join, 0);
+  pdl_launch_tag(16, dens_kernel, gp.n_macro + gp.nblk_dens, 256, 0, s, gp);
+  mark(5, s);
+  pdl_launch_tag(32, gmax0_kernel, gp.nblk_obj, 256, 0, s, gp);
+  mark(6, s);
+  pdl_launch_tag(64, advance_kernel, gp.nblk_obj, 256, 0, s, gp);
+  mark(7, s);
+  return check_launch("gp_iterate_marked_overlap");
+}
+
+int gp_overlap_times(float* t) {
+  if (!g_omarks[0]) return P3D_ERR_ARG;
+  if (cudaEventSynchronize(g_omarks[7]) != cudaSuccess) return check_launch("overlap times");
+  for (int k = 1; k < 8; ++k) cudaEventElapsedTime(&t[k - 1], g_omarks[0], g_omarks[k]);
+  return check_launch("overlap times");
 }
 
 int gp_stage_times(float* ms) {
@@ -980,11 +1022,11 @@ int gp_shard_stage(const p3d_gp& gp, int stage, cudaStream_t s) {
     case P3D_SH_NORMS_FINAL: norms_final_kernel<<<1, 1, 0, s>>>(gp); break;
     case P3D_SH_SCATTER: scatter_k2(gp, &gp.st->done, s); break;
     case P3D_SH_SPECTRAL: if (const int rc = launch_k3(gp, s)) return rc; break;
-    case P3D_SH_DENS: pdl_launch(dens_kernel, gp.n_macro + gp.nblk_dens, 256, 0, s, gp); break;
+    case P3D_SH_DENS: pdl_launch_tag(16, dens_kernel, gp.n_macro + gp.nblk_dens, 256, 0, s, gp); break;
     case P3D_SH_CONTROL: shard_control_kernel<<<1, 1, 0, s>>>(gp); break;
-    case P3D_SH_STEP0: pdl_launch(gmax0_kernel, gp.nblk_obj, 256, 0, s, gp); break;
+    case P3D_SH_STEP0: pdl_launch_tag(32, gmax0_kernel, gp.nblk_obj, 256, 0, s, gp); break;
     case P3D_SH_STEP0_CONTROL: step0_control_kernel<<<1, 1, 0, s>>>(gp); break;
-    case P3D_SH_ADVANCE: pdl_launch(advance_kernel, gp.nblk_obj, 256, 0, s, gp); break;
+    case P3D_SH_ADVANCE: pdl_launch_tag(64, advance_kernel, gp.nblk_obj, 256, 0, s, gp); break;
     default: return P3D_ERR_ARG;
   }
   return check_launch("gp_shard_stage");

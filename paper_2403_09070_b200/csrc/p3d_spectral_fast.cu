@@ -700,13 +700,17 @@ int launch_spectral_fast(const p3d_grid* g, const double* rho, const int64_t* rh
   const int ga = (g->nx + a.sa - 1) / a.sa, ta = threads_a(g, a.sa), tc = threads_c(g);
   const bool nz2 = g->nz == 2;
   if (!coef_in) {
-    if (nz2) P3D_SPEC_SWITCH(a.logy, (pdl_launch(spec_fwd_yz<LL, true>, ga, ta, smem_a(g, a.sa), s, a)))
-    else P3D_SPEC_SWITCH(a.logy, (pdl_launch(spec_fwd_yz<LL, false>, ga, ta, smem_a(g, a.sa), s, a)))
+    if (nz2) P3D_SPEC_SWITCH(a.logy, (pdl_launch_tag(8, spec_fwd_yz<LL, true>, ga, ta, smem_a(g, a.sa), s, a)))
+    else P3D_SPEC_SWITCH(a.logy, (pdl_launch_tag(8, spec_fwd_yz<LL, false>, ga, ta, smem_a(g, a.sa), s, a)))
   }
-  P3D_SPEC_SWITCH(a.logx, (pdl_launch(spec_x<LL>, (int)(S / kColsB), kThreads, smem_b(g), s, a)));
+  // timing probe only (results wrong): P3D_PROBE_K3=1 keeps the A pass (overflow,
+  // re-zero) and drops the B and C passes
+  static const bool probe = getenv("P3D_PROBE_K3") && getenv("P3D_PROBE_K3")[0] == '1';
+  if (probe && halt) return check_launch("spectral (probe)");
+  P3D_SPEC_SWITCH(a.logx, (pdl_launch_tag(8, spec_x<LL>, (int)(S / kColsB), kThreads, smem_b(g), s, a)));
   if (maps) {
-    if (nz2) P3D_SPEC_SWITCH(a.logy, (pdl_launch(spec_inv_yz<LL, true>, g->nx, tc, smem_c(g), s, a)))
-    else P3D_SPEC_SWITCH(a.logy, (pdl_launch(spec_inv_yz<LL, false>, g->nx, tc, smem_c(g), s, a)))
+    if (nz2) P3D_SPEC_SWITCH(a.logy, (pdl_launch_tag(8, spec_inv_yz<LL, true>, g->nx, tc, smem_c(g), s, a)))
+    else P3D_SPEC_SWITCH(a.logy, (pdl_launch_tag(8, spec_inv_yz<LL, false>, g->nx, tc, smem_c(g), s, a)))
   }
   return check_launch("spectral (fast path)");
 }

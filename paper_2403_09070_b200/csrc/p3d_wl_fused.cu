@@ -1050,9 +1050,9 @@ void launch_fused_net(const FusedNetArgs& a, bool f32, cudaStream_t s) {
     else generic_net_kernel<false><<<gb, 256, 0, s>>>(a);
   }
   if (f32)
-    pdl_launch(fused_net_kernel<true>, a.blocks, 32 * kWarpsPerBlock, kWarpsPerBlock * sizeof(WarpCols<true>), s, a);
+    pdl_launch_tag(1, fused_net_kernel<true>, a.blocks, 32 * kWarpsPerBlock, kWarpsPerBlock * sizeof(WarpCols<true>), s, a);
   else
-    pdl_launch(fused_net_kernel<false>, a.blocks, 32 * kWarpsPerBlock, kWarpsPerBlock * sizeof(WarpCols<false>), s, a);
+    pdl_launch_tag(1, fused_net_kernel<false>, a.blocks, 32 * kWarpsPerBlock, kWarpsPerBlock * sizeof(WarpCols<false>), s, a);
 }
 
 #ifndef P3D_GATHER_WARP
@@ -1062,10 +1062,10 @@ void launch_fused_gather(const FusedGatherArgs& a, cudaStream_t s) {
   if (P3D_GATHER_WARP && a.in_d) {
     FusedGatherArgs w = a;  // one warp per 32 objects, same partial slots
     w.blocks = std::min(a.blocks, std::max(1, (a.n_obj + 32 * kGatherWarps - 1) / (32 * kGatherWarps)));
-    pdl_launch(gather_warp_kernel, w.blocks, 32 * kGatherWarps, 0, s, w);
+    pdl_launch_tag(2, gather_warp_kernel, w.blocks, 32 * kGatherWarps, 0, s, w);
     return;
   }
-  pdl_launch(fused_gather_kernel, a.blocks, 256, 0, s, a);
+  pdl_launch_tag(2, fused_gather_kernel, a.blocks, 256, 0, s, a);
 }
 
 }  // namespace p3d
