@@ -178,6 +178,102 @@ __device__ __forceinline__ void fft_lines(double2* buf, int nl, const double2* t
   }
 }
 
+// The per-pass twiddles a thread needs, held in registers: when blockDim.x
+// is a multiple of the butterflies per line (every BASELINE shape), a thread
+// always works on the same butterfly index u of every line, so its 7 twiddles
+// per pass are fixed.  They are loaded at kernel entry, BEFORE the wait on the
+// predecessor grid (the tables are constant), so their latency hides under the
+// previous kernel's tail instead of stalling each pass (the A pass's second
+// largest stall).
+#ifndef P3D_TW_REGS
+#define P3D_TW_REGS 1
+#endif
+template <int L>
+struct TwRegs {
+  using F = Fft<L>;
+  static constexpr int NP = F::P8 > 0 ? F::P8 : 1;
+  double2 w[NP][7];
+  bool ok;
+  __device__ __forceinline__ void load(const double* twg) {
+    const int nb = F::N >> 3;
+    ok = P3D_TW_REGS && (blockDim.x % nb) == 0;
+    if (!ok) return;
+    const double2* tw = pass_twiddles(twg, F::N);
+    const int u = threadIdx.x & (nb - 1);
+#pragma unroll
+    for (int s = 0; s < F::P8; ++s) {
+      const int ls = F::lspan(s);
+      if (ls > 0) {
+        const int j = u & ((1 << ls) - 1);
+#pragma unroll
+        for (int q = 1; q < 8; ++q) w[s][q - 1] = __ldg(tw + F::tw_off(s) + j + ((q - 1) << ls));
+      }
+    }
+  }
+};
+
+// In-place DIF FFT with the twiddles from registers (TwRegs::ok)
+template <int L, bool INV>
+__device__ __forceinline__ void fft_lines_reg(double2* buf, int nl, const TwRegs<L>& tr) {
+  using F = Fft<L>;
+#pragma unroll
+  for (int s = 0; s < F::P8; ++s) {
+    const int ls = F::lspan(s);
+    const int nb = F::N >> 3;
+    for (int t = threadIdx.x; t < nl * nb; t += blockDim.x) {
+      const int l = t >> (L - 3), u = t & (nb - 1);
+      const int j = u & ((1 << ls) - 1), b = u >> ls;
+      double2* x = buf + l * F::LS;
+      const int base = (b << (ls + 3)) + j;
+      double2 a[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) a[m] = x[F::pad(base + (m << ls))];
+      dft8<INV>(a);
+      if (ls > 0) {
+#pragma unroll
+        for (int q = 1; q < 8; ++q) {
+          double2 wq = tr.w[s][q - 1];
+          if (INV) wq.y = -wq.y;
+          a[q] = cmul(a[q], wq);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 8; ++m) x[F::pad(base + (m << ls))] = a[m];
+    }
+    __syncthreads();
+  }
+  if (F::REM == 2) {
+    for (int t = threadIdx.x; t < nl * (F::N >> 2); t += blockDim.x) {
+      const int l = t >> (L - 2), u = t & ((F::N >> 2) - 1);
+      double2* x = buf + l * F::LS + F::pad(u << 2);
+      const double2 a0 = x[0], a1 = x[1], a2 = x[2], a3 = x[3];
+      const double2 b0 = cadd(a0, a2), b2 = csub(a0, a2), b1 = cadd(a1, a3);
+      const double2 b3 = rot_i<INV>(csub(a1, a3));
+      x[0] = cadd(b0, b1);
+      x[1] = cadd(b2, b3);
+      x[2] = csub(b0, b1);
+      x[3] = csub(b2, b3);
+    }
+    __syncthreads();
+  } else if (F::REM == 1) {
+    for (int t = threadIdx.x; t < nl * (F::N >> 1); t += blockDim.x) {
+      const int l = t >> (L - 1), u = t & ((F::N >> 1) - 1);
+      double2* x = buf + l * F::LS + F::pad(u << 1);
+      const double2 a0 = x[0], a1 = x[1];
+      x[0] = cadd(a0, a1);
+      x[1] = csub(a0, a1);
+    }
+    __syncthreads();
+  }
+}
+
+template <int L, bool INV>
+__device__ __forceinline__ void fft_any(double2* buf, int nl, const double2* tw,
+                                        const TwRegs<L>& tr) {
+  if (tr.ok) fft_lines_reg<L, INV>(buf, nl, tr);
+  else fft_lines<L, INV>(buf, nl, tw);
+}
+
 // Makhoul DCT-II input slot of element n
 template <int L>
 __device__ __forceinline__ int dct_slot(int n) {
@@ -319,6 +415,8 @@ __device__ __forceinline__ void ovfl_epilogue(const FastArgs& a, long long exces
 // staged; other nz stage the slab and run the direct z transform.
 template <int LY, bool NZ2>
 __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
+  TwRegs<LY> tr;
+  tr.load(a.twy);  // constant tables: before the wait on the predecessor
   pdl_wait();
   using F = Fft<LY>;
   if (a.halt && *a.halt) return;
@@ -361,7 +459,7 @@ __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
       }
     }
     __syncthreads();
-    fft_lines<LY, false>(buf, nf, tw);
+    fft_any<LY, false>(buf, nf, tw, tr);
     for (int t = threadIdx.x; t < nf << LY; t += blockDim.x) {
       const int sl = t >> LY, k = t & (ny - 1);
       reinterpret_cast<double2*>(a.X + base)[t] = dct2_post<LY>(buf + sl * F::LS, k, a.phy);
@@ -392,7 +490,7 @@ __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
       buf[f * F::LS + F::pad(dct_slot<LY>(n))] = make_double2(xa, xb);
     }
     __syncthreads();
-    fft_lines<LY, false>(buf, nf, tw);
+    fft_any<LY, false>(buf, nf, tw, tr);
     for (int t = threadIdx.x; t < nf << LY; t += blockDim.x) {
       const int f = t >> LY, k = t & (ny - 1);
       const int sl = f / nfs, p = f - sl * nfs;
@@ -412,6 +510,8 @@ __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
 // in 2 kColsB complex FFTs)
 template <int LX>
 __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
+  TwRegs<LX> tr;
+  tr.load(a.twx);  // constant tables: before the wait on the predecessor
   pdl_wait();
   using F = Fft<LX>;
   if (a.halt && *a.halt) return;
@@ -436,7 +536,7 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
           make_double2(Xs[(2 * f) * nx + n], Xs[(2 * f + 1) * nx + n]);
     }
     __syncthreads();
-    fft_lines<LX, false>(buf, CB / 2, tw);
+    fft_any<LX, false>(buf, CB / 2, tw, tr);
     for (int t = threadIdx.x; t < (CB / 2) * nx; t += blockDim.x) {
       const int f = t >> LX, k = t & (nx - 1);
       const double2 r = dct2_post<LX>(buf + f * F::LS, k, a.phx);
@@ -484,7 +584,7 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
     buf[f * F::LS + F::pad(n)] = make_double2(va.x - vb.y, va.y + vb.x);
   }
   __syncthreads();
-  fft_lines<LX, true>(buf, 2 * CB, tw);
+  fft_any<LX, true>(buf, 2 * CB, tw, tr);
   for (int t = threadIdx.x; t < 4 * CB * nx; t += blockDim.x) {  // contiguous row segments
     const int map = t & 3, c = (t >> 2) % CB, ix = t / (4 * CB);
     const double2 z = inv_post<LX>(buf + (2 * c + (map >> 1)) * F::LS, ix);
@@ -500,6 +600,8 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
 // the output write.  Other nz stage the slab and loop over rounds of lines.
 template <int LY, bool NZ2>
 __global__ void __launch_bounds__(kThreads) spec_inv_yz(FastArgs a) {
+  TwRegs<LY> tr;
+  tr.load(a.twy);  // constant tables: before the wait on the predecessor
   pdl_wait();
   using F = Fft<LY>;
   if (a.halt && *a.halt) return;
@@ -518,7 +620,7 @@ __global__ void __launch_bounds__(kThreads) spec_inv_yz(FastArgs a) {
       buf[f * F::LS + F::pad(n)] = make_double2(va.x - vb.y, va.y + vb.x);
     }
     __syncthreads();
-    fft_lines<LY, true>(buf, 4, tw);
+    fft_any<LY, true>(buf, 4, tw, tr);
     const double r2 = 0.70710678118654752440;
     double* out = a.maps + base * 4;
     for (int t = threadIdx.x; t < 4 << LY; t += blockDim.x) {
@@ -553,7 +655,7 @@ __global__ void __launch_bounds__(kThreads) spec_inv_yz(FastArgs a) {
       buf[fl * F::LS + F::pad(n)] = make_double2(v[0].x - v[1].y, v[0].y + v[1].x);
     }
     __syncthreads();
-    fft_lines<LY, true>(buf, nf, tw);
+    fft_any<LY, true>(buf, nf, tw, tr);
     for (int t = threadIdx.x; t < nf << LY; t += blockDim.x) {
       const int fl = t >> LY, m = t & (ny - 1);
       const double2 z = inv_post<LY>(buf + fl * F::LS, m);
