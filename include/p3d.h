@@ -258,6 +258,27 @@ int p3d_score(int32_t n_net, const int32_t* net_ptr, const int32_t* pin_inst,
               double* scratch, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* design input (host code)                                */
+/* ------------------------------------------------------------------------ */
+/* parse_design (model.py:423-571) + the Design checks (model.py:121-190) +
+ * NetlistArrays (model.py:231-275) in one native pass over the text.  On a
+ * malformed design returns P3D_ERR_ARG with the reference's message
+ * (p3d_last_error: "line N: ..." for its ParseError cases, the DesignError
+ * text otherwise).  handle: freed with p3d_parsed_free. */
+int p3d_parse_design(const char* text, int64_t len, void** handle);
+/* counts[5] = (n_inst, n_net, n_pin, inst-name bytes, net-name bytes);
+ * scalars[9] = (die w, h, row height top, bottom, max util top, bottom,
+ * HBT pitch, spacing, cost). */
+int p3d_parsed_counts(const void* handle, int64_t* counts, double* scalars);
+/* Fills the NetlistArrays fields (net_ptr [n_net+1], pin_* [n_pin], per-
+ * instance sizes [n_inst]) and the names, each '\n'-terminated. */
+int p3d_parsed_fill(const void* handle, uint8_t* is_macro, double* w_top, double* h_top,
+                    double* w_bot, double* h_bot, int64_t* net_ptr, int64_t* pin_inst,
+                    double* ox_top, double* oy_top, double* ox_bot, double* oy_bot,
+                    char* inst_names, char* net_names);
+void p3d_parsed_free(void* handle);
+
+/* ------------------------------------------------------------------------ */
 /* small per-op pieces of the operator API                                   */
 /* ------------------------------------------------------------------------ */
 /* dynamic_size (density.py:134-147): w, h [n] at depth z [n]. */

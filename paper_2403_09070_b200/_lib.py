@@ -144,6 +144,10 @@ _SIGS = {
     "p3d_overflow": (I32, [I64, P, D, D, D, P, P, P]),
     "p3d_net_spans": (I32, [I32, P, P, P, P, P, P, P, P, P]),
     "p3d_nesterov_op": (I32, [I32, I64, P, P, P, P, D, P, P, P]),
+    "p3d_parse_design": (I32, [C.c_char_p, I64, C.POINTER(C.c_void_p)]),
+    "p3d_parsed_counts": (I32, [P, P, P]),
+    "p3d_parsed_fill": (I32, [P] * 14),
+    "p3d_parsed_free": (None, [P]),
     "p3d_rebalance": (I32, [I32, P, P, P, P, P, D, D, P, P]),
     "p3d_check_objects": (I32, [I32, I32] + [P] * 14 + [D] * 7 + [P] * 5),
     "p3d_pair_search": (I32, [I32, I32, P, P, D, I32, I32, I32, D, D, P, P, P, P, P, I32, P, P]),

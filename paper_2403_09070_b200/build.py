@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
           "--expt-relaxed-constexpr", "-I", CSRC, "-I", INCLUDE]
 NO_FMA = {"p3d_density.cu", "p3d_loop.cu", "p3d_gp2d.cu", "p3d_score.cu", "p3d_post.cu", "p3d_ops.cu"}
-SOURCES = ["p3d_api.cu", "p3d_wl.cu", "p3d_wl_fused.cu", "p3d_density.cu", "p3d_spectral.cu", "p3d_spectral_fast.cu", "p3d_loop.cu", "p3d_gp2d.cu", "p3d_score.cu", "p3d_post.cu", "p3d_ops.cu"]
+SOURCES = ["p3d_api.cu", "p3d_wl.cu", "p3d_wl_fused.cu", "p3d_density.cu", "p3d_spectral.cu", "p3d_spectral_fast.cu", "p3d_loop.cu", "p3d_gp2d.cu", "p3d_score.cu", "p3d_post.cu", "p3d_ops.cu", "p3d_parse.cu"]
 
 
 def _nvcc():

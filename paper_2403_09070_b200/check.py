@@ -54,6 +54,8 @@ def _names(design):
     generator's convention (cells c<i>, macros m<k>, nets n<j>; synth.py:135-167)."""
     if hasattr(design, "insts") and hasattr(design, "nets"):
         return [x.name for x in design.insts], [e.name for e in design.nets]
+    if getattr(design, "inst_names", None) is not None:  # model.parse_design_arrays
+        return design.inst_names, design.net_names
     a = design.arrays()
     k = np.cumsum(a.is_macro) - 1
     inst = [f"m{k[i]}" if a.is_macro[i] else f"c{i}" for i in range(design.n_insts)]

@@ -150,3 +150,61 @@ def rotated_dims(w, h, quarters):
     """Swap footprint sides on odd quarter turns (``model.py:292-295``)."""
     odd = (np.asarray(quarters) % 4) % 2 == 1
     return np.where(odd, h, w), np.where(odd, w, h)
+
+
+class ParseError(ValueError):
+    """Malformed design text (model.py:28-35); the message carries the line."""
+
+
+def parse_design_arrays(stream) -> ArrayDesign:
+    """The reference's ``parse_design`` (model.py:423-571) with its Design
+    checks (model.py:121-190), straight to the flat arrays the GP loop reads
+    (``NetlistArrays``, model.py:231-275): one native pass over the text
+    (``p3d_parse_design``, host C++) instead of Python objects per instance
+    and pin.  ``stream``: the text, or an iterable of lines / a file object.
+    Raises ``ParseError`` with the reference's message on malformed input.
+    Instance / net names are kept (``inst_names``, ``net_names``) for the
+    solution check's messages."""
+    import ctypes as C
+
+    from . import _lib
+
+    if isinstance(stream, bytes):
+        text = stream
+    elif isinstance(stream, str):
+        text = stream.encode()
+    else:
+        text = "".join(stream).encode()
+    lib = _lib.load()
+    h = C.c_void_p()
+    rc = lib.p3d_parse_design(text, len(text), C.byref(h))
+    if rc != 0:
+        buf = C.create_string_buffer(1024)
+        lib.p3d_last_error(buf, 1024)
+        raise ParseError(buf.value.decode(errors="replace"))
+    try:
+        counts = np.zeros(5, dtype=np.int64)
+        sc = np.zeros(9)
+        lib.p3d_parsed_counts(h, counts.ctypes.data, sc.ctypes.data)
+        n, m, p, ib, nb = (int(v) for v in counts)
+        is_macro = np.zeros(n, dtype=np.uint8)
+        wt, ht, wb, hb = (np.zeros(n) for _ in range(4))
+        net_ptr = np.zeros(m + 1, dtype=np.int64)
+        pin_inst = np.zeros(p, dtype=np.int64)
+        oxt, oyt, oxb, oyb = (np.zeros(p) for _ in range(4))
+        inames, nnames = C.create_string_buffer(max(ib, 1)), C.create_string_buffer(max(nb, 1))
+        lib.p3d_parsed_fill(h, *(a.ctypes.data for a in (is_macro, wt, ht, wb, hb, net_ptr,
+                                                         pin_inst, oxt, oyt, oxb, oyb)),
+                            inames, nnames)
+    finally:
+        lib.p3d_parsed_free(h)
+    arr = NetlistArrays(is_macro=is_macro.astype(bool), w_top=wt, h_top=ht, w_bot=wb, h_bot=hb,
+                        net_ptr=net_ptr, pin_inst=pin_inst, ox_top=oxt, oy_top=oyt, ox_bot=oxb,
+                        oy_bot=oyb)
+    sc = [float(v) for v in sc]
+    die = DieSpec(width=sc[0], height=sc[1], row_height_top=sc[2], row_height_bottom=sc[3],
+                  max_util_top=sc[4], max_util_bottom=sc[5])
+    d = ArrayDesign(die, HbtSpec(sc[6], sc[7], sc[8]), arr)
+    d.inst_names = inames.raw[:ib].decode().split("\n")[:n]
+    d.net_names = nnames.raw[:nb].decode().split("\n")[:m]
+    return d

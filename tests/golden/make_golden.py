@@ -299,6 +299,77 @@ def check():
         json.dump(out, fh)
 
 
+def parse_cases():
+    """parse_design (model.py:423-571) on a small synthetic design and on
+    malformed variants of it: the arrays (sha256 per NetlistArrays field) or
+    the exact error message."""
+    text = gen_synthetic(SynthSpec(**SPECS["tiny"]))
+    lines = text.splitlines()
+
+    def edit(fn):
+        return "\n".join(fn(list(lines))) + "\n"
+
+    def first(ls, prefix):
+        return next(i for i, l in enumerate(ls) if l.startswith(prefix))
+
+    def swap(ls, prefix, new):
+        ls[first(ls, prefix)] = new
+        return ls
+
+    def drop(ls, prefix):
+        del ls[first(ls, prefix)]
+        return ls
+
+    cell_line = first(lines, "Cell ")
+    ck = lines[cell_line].split()[1]
+    inst_line = first(lines, "Inst ")
+    iname = lines[inst_line].split()[1]
+    net_line = first(lines, "Net ")
+    nname = lines[net_line].split()[1]
+    variants = {
+        "ok": text,
+        "ok_comments": "# header comment\n" + text.replace("\n", "  # trailing\n", 3),
+        "no_diesize": edit(lambda ls: drop(ls, "DieSize")),
+        "no_hbt": edit(lambda ls: drop(ls, "HBT")),
+        "no_util": edit(lambda ls: drop(ls, "TopDieMaxUtil")),
+        "bad_flag": edit(lambda ls: swap(ls, "Inst ", " ".join(ls[inst_line].split()[:3] + ["2"]))),
+        "dup_inst": edit(lambda ls: ls[:inst_line + 1] + [ls[inst_line]] + ls[inst_line + 1:]),
+        "unknown_inst": edit(lambda ls: swap(ls, "Pin " + iname + "/", "Pin nosuch/p0")),
+        "cell_pin_count": edit(lambda ls: swap(ls, "Cell ", " ".join(ls[cell_line].split()[:4] + ["99"]))),
+        "net_pin_count": edit(lambda ls: swap(ls, "Net ", f"Net {nname} 7")),
+        "pin_outside": edit(lambda ls: ["Pin x/y"] + ls),
+        "unknown_directive": edit(lambda ls: ls + ["Bogus 1 2"]),
+        "bad_number": edit(lambda ls: swap(ls, "DieSize", "DieSize 10x 20")),
+        "util_range": edit(lambda ls: swap(ls, "TopDieMaxUtil", "TopDieMaxUtil 1.5")),
+        "rows_no_tile": edit(lambda ls: swap(ls, "TopDieRowHeight", "TopDieRowHeight 7.3")),
+        "bad_hbt": edit(lambda ls: swap(ls, "HBT", "HBT 0 4 10")),
+        "cell_dims": edit(lambda ls: swap(ls, "Cell ", " ".join([ls[cell_line].split()[0], ck, "0",
+                                                               ls[cell_line].split()[3],
+                                                               ls[cell_line].split()[4]]))),
+        "net_unknown_pin": edit(lambda ls: swap(ls, "Pin " + iname + "/", f"Pin {iname}/zz")),
+        "dup_net": edit(lambda ls: ls[:net_line] + [f"Net {nname} 0"] + ls[net_line:]),
+        "pin_offset": edit(lambda ls: ls[:cell_line + 1] + ["Pin p0 9999 0"] + ls[cell_line + 2:]),
+        "cell_outside_tech": "Cell a 1 1 0\n" + text,
+    }
+    out = {}
+    for name, t in variants.items():
+        try:
+            d = parse_design(t)
+            a = d.arrays()
+            out[name] = {"text": t, "error": None,
+                         "fields": {f: digest(getattr(a, f)) for f in FIELDS},
+                         "die": [d.die.width, d.die.height, d.die.row_height_top,
+                                 d.die.row_height_bottom, d.die.max_util_top,
+                                 d.die.max_util_bottom],
+                         "hbt": [d.hbt.pitch, d.hbt.spacing, d.hbt.cost],
+                         "inst_names": [x.name for x in d.insts],
+                         "net_names": [e.name for e in d.nets]}
+        except Exception as e:  # ParseError (a ValueError)
+            out[name] = {"text": t, "error": str(e), "type": type(e).__name__}
+    with open(os.path.join(HERE, "parse_cases.json"), "w") as fh:
+        json.dump(out, fh)
+
+
 def flow_small():
     from concurrent.futures import ProcessPoolExecutor
 
@@ -454,7 +525,7 @@ if __name__ == "__main__":
         band("cfg2", 256, "cfg2_band.json")
         sys.exit(0)
     for flag, fn in (("--cfg3", cfg3_rows), ("--exits", exits), ("--flow", flow_small),
-                     ("--rebalance", rebalance), ("--check", check)):
+                     ("--rebalance", rebalance), ("--check", check), ("--parse", parse_cases)):
         if flag in sys.argv:
             fn()
             sys.exit(0)
