@@ -57,7 +57,7 @@ from . import _lib
 from .dist import object_slabs
 from .gp import Gp3dProblem
 from .model import ArrayDesign, NetlistArrays
-from .partition import HaloPlan, locality_order
+from .partition import HaloPlan, cached_locality_order
 
 STAGE = {name: k for k, name in enumerate(_lib.SH_STAGES)}
 
@@ -138,7 +138,7 @@ class ShardedGp3d:
         self.perm = self.inv = None
         if self.halo:
             # locality numbering (every rank computes the same, deterministic one)
-            perm = locality_order(arr.net_ptr, arr.pin_inst, I)
+            perm = cached_locality_order(arr.net_ptr, arr.pin_inst, I)
             inv = np.empty_like(perm)
             inv[perm] = np.arange(I)
             self.perm, self.inv = perm, inv
