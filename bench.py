@@ -39,17 +39,20 @@ METRIC = "GP iterations/sec at 800k cells (WL+density+field+step); % HBM rooflin
 
 
 def rank_env():
-    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
-            int(os.environ.get("LOCAL_RANK", 0)))
+    from paper_2403_09070_b200.dist import rank_world
+
+    return rank_world()
 
 
 def setup_design(config, rank):
     from paper_2403_09070_b200.synth import CONFIGS, cached_synth, SynthSpec
 
+    from paper_2403_09070_b200.dist import replica_seed
+
     c = CONFIGS[config]
     spec = c["spec"]
     if rank:
-        spec = SynthSpec(**{**spec.__dict__, "seed": spec.seed + rank})
+        spec = SynthSpec(**{**spec.__dict__, "seed": replica_seed(spec.seed, rank)})
     return cached_synth(spec), c["grid"], spec
 
 
@@ -632,10 +635,9 @@ def main():
     barrier()
 
     # max over ranks
-    t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, e2e_ms = float(t[0]), float(t[1])
+    from paper_2403_09070_b200.dist import max_over_ranks
+
+    ms, e2e_ms = max_over_ranks([ms, e2e_ms])
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
         return

@@ -1,11 +1,11 @@
-"""Multi-GPU plumbing for the GP loop (one process per GPU, torch.distributed).
-
-Round 1 runs independent replicas per rank (config-5 style); the sharded
-config-4 path partitions objects and nets into contiguous slabs and combines
-the density map with an all-reduce.  Because rho is int64 fixed point
-(2^-40 per unit density) the all-reduced map is bit-identical to the
-single-GPU map for any number of ranks and any reduction order — the property
-``tests/test_dist.py`` checks with the gloo backend on CPU.
+"""Multi-GPU plumbing for the GP loop (one process per GPU, torch.distributed):
+the launcher environment, the object slabs of the sharded loop (shard.py,
+partition.py), the replica seeds of ``bench.py --mode replicas`` and the
+max-over-ranks timing reduction of ``bench.py``.  Because rho is int64 fixed
+point (2^-40 per unit density), the all-reduced density map of the sharded
+loop is bit-identical to the single-GPU map for any number of ranks and any
+reduction order — the property ``tests/test_dist.py`` checks with the gloo
+backend on CPU.
 """
 
 from __future__ import annotations
@@ -43,15 +43,6 @@ def object_slabs(n_inst, n_fill, rank, world):
 def replica_seed(base_seed, rank):
     """Seed of the independent placement a rank runs in replica mode."""
     return int(base_seed) + int(rank)
-
-
-def allreduce_rho_fx(rho_fx: torch.Tensor) -> torch.Tensor:
-    """Sum the per-rank int64 fixed-point density maps in place (exact)."""
-    if rho_fx.dtype != torch.int64:
-        raise TypeError("the density map must be int64 fixed point")
-    if dist.is_initialized() and dist.get_world_size() > 1:
-        dist.all_reduce(rho_fx, op=dist.ReduceOp.SUM)
-    return rho_fx
 
 
 def max_over_ranks(values):

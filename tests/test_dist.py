@@ -16,8 +16,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2403_09070_b200.dist import (allreduce_rho_fx, max_over_ranks, replica_seed,
-                                        shard_range)
+from paper_2403_09070_b200.dist import max_over_ranks, replica_seed, shard_range
 
 
 def _free_port():
@@ -43,7 +42,7 @@ def _worker(rank, world, port, out):
                      np.full(n, grid.dz / 2), np.ones(n), rng.random(n) < 0.05)
         lo, hi = shard_range(n, rank, world)
         part = torch.from_numpy(FX.fixed_rho(grid, cl.take(np.arange(lo, hi))).reshape(-1).copy())
-        allreduce_rho_fx(part)
+        dist.all_reduce(part)  # int64: the sum is exact in any order
         full = FX.fixed_rho(grid, cl).reshape(-1)
         ok = bool(np.array_equal(part.numpy(), full))
         mx = max_over_ranks([1.0 + rank, 5.0 - rank])
