@@ -186,3 +186,27 @@ def test_cfg3_headline_config_vs_reference():
     assert info.iterations == it and not info.diverged and info.hbt_count == hbt
     assert abs(info.wirelength - wl) <= 5e-3 * wl
     assert abs(info.final_overflow - ovfl) <= 5e-3 * ovfl
+
+
+def test_cfg3_fp32_wa_mode_within_gate():
+    """The opt-in fp32 weighted-average mode (SURVEY App. B plan) at the
+    headline config: every row of the 20-iteration schedule (WL, crossings,
+    overflow) within the north_star's 0.5% of the reference's (measured: WL
+    within 1.4e-4, crossings 0.08%, final overflow 2e-5)."""
+    from paper_2403_09070_b200 import gp as G
+    from paper_2403_09070_b200.synth import CONFIGS, cached_synth
+
+    gold = json.load(open(os.path.join(GOLD, "cfg3_rows.json")))
+    d = cached_synth(CONFIGS[3]["spec"])
+    cfg = G.GpConfig(seed=1, nz=2, grid_nx=512, grid_ny=512, max_iters=20, stop_overflow=0.0)
+    rng = np.random.default_rng(1)
+    grid = G.choose_grid(d, cfg)
+    st = G.init_state(d, grid, cfg, rng)
+    rows = []
+    st, info = G.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng, precision="fp32")
+    got, r = np.array(rows, dtype=float), np.array(gold["sched20"], dtype=float)
+    rel = np.abs(got[:, 1] - r[:, 1]) / r[:, 1]
+    print("fp32 mode: max row WL rel", rel.max(), "final", got[-1], r[-1])
+    assert np.all(rel <= 5e-3)
+    assert np.all(np.abs(got[:, 2] - r[:, 2]) <= 5e-3 * r[:, 2])
+    assert np.all(np.abs(got[:, 3] - r[:, 3]) <= 5e-3 * r[:, 3])
