@@ -645,22 +645,29 @@ class Gp3dProblem:
         return g
 
     def run(self, pos0, use_graph=True, iters_per_graph=8, poll_every=4):
-        """Initialise and run the loop to completion (max_iters or an exit)."""
-        self.init_loop(pos0)
+        """Initialise and run the loop to completion (max_iters or an exit).
+        NVTX ranges mark the host phases (init, capture, each replay batch)
+        for an external profiler's timeline."""
+        nvtx = torch.cuda.nvtx
+        with nvtx.range("p3d.gp3d.init"):
+            self.init_loop(pos0)
         total = self.max_iters
         if not use_graph:
             done_calls = 0
             while done_calls < total:
                 k = min(iters_per_graph, total - done_calls)
-                self.iterate(k)
+                with nvtx.range(f"p3d.gp3d.iterate[{done_calls}:{done_calls + k}]"):
+                    self.iterate(k)
                 done_calls += k
                 if (done_calls // k) % poll_every == 0 and self.state().done:
                     break
             return self.state()
-        g = self.capture(iters_per_graph)
+        with nvtx.range("p3d.gp3d.capture"):
+            g = self.capture(iters_per_graph)
         replays = -(-total // iters_per_graph)
         for r in range(replays):
-            g.replay()
+            with nvtx.range(f"p3d.gp3d.replay[{r * iters_per_graph}]"):
+                g.replay()
             if (r + 1) % poll_every == 0 and self.state().done:
                 break
         return self.state()

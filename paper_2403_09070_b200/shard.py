@@ -194,7 +194,9 @@ class ShardedGp3d:
         self._pos4.index_copy_(0, self._recv_idx, self._recv)
 
     def _stage(self, name):
-        _lib.call("p3d_gp_shard_stage", _lib.byref(self.prob.gp), STAGE[name], _lib.stream_ptr())
+        with torch.cuda.nvtx.range(f"p3d.shard.{name}"):  # free when no profiler listens
+            _lib.call("p3d_gp_shard_stage", _lib.byref(self.prob.gp), STAGE[name],
+                      _lib.stream_ptr())
 
     def init_loop(self, pos0):
         # every rank starts from the same positions, so pos4 starts complete

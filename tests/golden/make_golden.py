@@ -52,6 +52,7 @@ SPECS = {
     "cfg1": dict(n_insts=10_008, n_macros=8, r_ma=0.30, seed=1, nets_per_inst=1.2),
     "cfg2": dict(n_insts=100_032, n_macros=32, r_ma=0.30, seed=1, nets_per_inst=1.1),
     "cfg3": dict(n_insts=800_064, n_macros=64, r_ma=0.30, seed=1, nets_per_inst=1.0625),
+    "cfg4": dict(n_insts=4_000_128, n_macros=128, r_ma=0.30, seed=1, nets_per_inst=1.05),
     # the reference's own end-to-end designs (test_acceptance.py:329-360)
     "flow3d": dict(n_insts=200, n_macros=3, r_ma=0.45, seed=1, fill_fraction=0.72),
     "flow2d": dict(n_insts=120, n_macros=5, r_ma=0.88, seed=7, fill_fraction=0.75),
@@ -99,6 +100,22 @@ def cfg3_rows():
                            info.wirelength, info.hbt_count]
     with open(os.path.join(HERE, "cfg3_rows.json"), "w") as fh:
         json.dump(out, fh, indent=0)
+
+
+def cfg4_rows():
+    """Config 4 (4,000,128 cells, 1024x1024x2): the first 3 rows of the
+    200-iteration schedule (the reference needs ~50 s per iteration here)."""
+    d = design_of("cfg4")
+    cfg, rng, grid, st = setup(d, 1024, 2, 200)
+    rows = _StopAfter(3)
+    t = time.perf_counter()
+    try:
+        rgp.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+    except _StopAfter.Done:
+        pass
+    with open(os.path.join(HERE, "cfg4_rows.json"), "w") as fh:
+        json.dump({"spec": SPECS["cfg4"], "grid": 1024, "nz": 2, "sched200_first3": _rows(rows),
+                   "seconds_1core": time.perf_counter() - t}, fh, indent=0)
 
 
 def _state_digest(st):
@@ -524,7 +541,7 @@ if __name__ == "__main__":
     if "--band" in sys.argv:
         band("cfg2", 256, "cfg2_band.json")
         sys.exit(0)
-    for flag, fn in (("--cfg3", cfg3_rows), ("--exits", exits), ("--flow", flow_small),
+    for flag, fn in (("--cfg3", cfg3_rows), ("--cfg4", cfg4_rows), ("--exits", exits), ("--flow", flow_small),
                      ("--rebalance", rebalance), ("--check", check), ("--parse", parse_cases)):
         if flag in sys.argv:
             fn()
