@@ -22,6 +22,8 @@ def dev(x, dtype):
             t = t.to(DEV)
         return t.contiguous()
     a = np.ascontiguousarray(np.asarray(x))
+    if not a.flags.writeable:  # e.g. np.broadcast_to views
+        a = a.copy()
     return torch.from_numpy(a).to(device=DEV, dtype=dtype).contiguous()
 
 
@@ -71,7 +73,7 @@ class Keep:
 
 
 def _numpy_arg(a):
-    if isinstance(a, np.ndarray):
+    if isinstance(a, (np.ndarray, list, tuple)):
         return True
     x = getattr(a, "x", None)  # a charge cloud of numpy arrays
     return isinstance(x, np.ndarray) and hasattr(a, "weight")

@@ -74,7 +74,8 @@ class GpInfo:
 
 @dataclass
 class GradientBundle:
-    """Per-object gradients ([n_obj, 3] CUDA tensors) and objective parts (gp.py:62-72)."""
+    """Per-object gradients ([n_obj, 3]; numpy when evaluate() got numpy
+    positions, else CUDA tensors) and objective parts (gp.py:62-72)."""
 
     wl_grad: torch.Tensor
     dens_grad: torch.Tensor
@@ -213,9 +214,13 @@ class NesterovOptimizer:
     caller's (e.g. ``Gp3dProblem.project``)."""
 
     def __init__(self, x0, project=None, min_step=1e-18):
-        self.project = project or (lambda p: p)
-        self.u = self.project(_dev.f64(x0).clone())
-        self.v = self.u.clone()
+        # numpy in, numpy out (the per-op convention): a host caller's
+        # `project` sees numpy arrays and `u` / `v` / `advance` return them
+        self._host = not isinstance(x0, torch.Tensor)
+        user = project or (lambda p: p)
+        self.project = (lambda t: _dev.f64(user(_dev.host(t)))) if self._host else user
+        self._u = self.project(_dev.f64(np.array(x0, dtype=float) if self._host else x0).clone())
+        self._v = self._u.clone()
         self.a = 1.0
         self.step = None
         self.min_step = min_step
@@ -223,6 +228,14 @@ class NesterovOptimizer:
         self._prev_g = None
         self._scr = _dev.scratch(8 + 2 * 2048 + 8)
         self._out = torch.zeros(4, dtype=torch.float64, device="cuda")
+
+    @property
+    def u(self):
+        return _dev.host(self._u) if self._host else self._u
+
+    @property
+    def v(self):
+        return _dev.host(self._v) if self._host else self._v
 
     def _op(self, op, v, vp, g, ref, s=0.0, out=None):
         _lib.call("p3d_nesterov_op", int(op), int(g.numel()), _lib.ptr(v), _lib.ptr(vp),
@@ -241,7 +254,7 @@ class NesterovOptimizer:
                     gmax = 0.0
                 self.step = 1.0 if gmax == 0 else step_scale / gmax
         else:
-            self._op(0, self.v, self._prev_v, g, ref)
+            self._op(0, self._v, self._prev_v, g, ref)
             dv2, dg2 = self._out[:2].tolist()
             den = math.sqrt(dg2)
             if den > 0:
@@ -249,16 +262,16 @@ class NesterovOptimizer:
                 self.step = float(min(max(new, self.step / 4), self.step * 4))
         if not math.isfinite(self.step) or self.step <= self.min_step:
             raise StepUnderflow(f"step size underflow ({self.step!r})")
-        self._prev_v = self.v.clone()
+        self._prev_v = self._v.clone()
         self._prev_g = g.clone()
-        u_new = torch.empty_like(self.v)
-        self._op(2, self.v, None, g, None, -self.step, out=u_new)  # v - step * g
+        u_new = torch.empty_like(self._v)
+        self._op(2, self._v, None, g, None, -self.step, out=u_new)  # v - step * g
         u_new = self.project(u_new)
         a_new = (1 + math.sqrt(4 * self.a ** 2 + 1)) / 2
         v_new = torch.empty_like(u_new)
-        self._op(2, u_new, None, u_new, self.u, (self.a - 1) / a_new, out=v_new)
-        self.v = self.project(v_new)
-        self.u = u_new
+        self._op(2, u_new, None, u_new, self._u, (self.a - 1) / a_new, out=v_new)
+        self._v = self.project(v_new)
+        self._u = u_new
         self.a = a_new
         return self.u
 
@@ -579,7 +592,15 @@ class Gp3dProblem:
 
     # -- reference API ---------------------------------------------------------
     def cloud(self, pos):
-        """ChargeCloud at pos [O,3] (gp.py:267-278), CUDA tensors."""
+        """ChargeCloud at pos [O,3] (gp.py:267-278): numpy arrays for numpy
+        positions, CUDA tensors for tensors."""
+        c = self._cloud(pos)
+        if not isinstance(pos, torch.Tensor):
+            c = dn.ChargeCloud(*(_dev.host(getattr(c, k)) for k in (
+                "x", "y", "z", "w", "h", "dep", "weight", "is_macro")))
+        return c
+
+    def _cloud(self, pos):
         p = _dev.f64(pos).reshape(self.n_obj, 3)
         w, h = dn.dynamic_size(self.w_top, self.h_top, self.w_bot, self.h_bot, self.arr.is_macro,
                                p[: self.n_inst, 2], self.grid.dz)
@@ -595,7 +616,8 @@ class Gp3dProblem:
         out = torch.empty_like(src)
         _lib.call("p3d_gp_project", _lib.byref(self.gp), _lib.ptr(src), _lib.ptr(out),
                   _lib.stream_ptr())
-        return self._aos(out)
+        out = self._aos(out)
+        return out if isinstance(pos, torch.Tensor) else _dev.host(out)
 
     def evaluate(self, pos, lam, gamma):
         """gp.py:296-341: (GradientBundle, overflow, exact WL, crossings)."""
@@ -609,8 +631,10 @@ class Gp3dProblem:
         wl_g = self._aos(self.t_wl)
         dg = self._aos(self.t_dens)
         total = wl_g + lam * dg
-        q = self.cloud(pos).charge
+        q = self._cloud(pos).charge
         _, div = precondition(total, lam, q, self.degree_obj, self.is_macro_obj)
+        if not isinstance(pos, torch.Tensor):  # numpy in, numpy out
+            wl_g, dg, total, div = (_dev.host(t) for t in (wl_g, dg, total, div))
         bundle = GradientBundle(wl_grad=wl_g, dens_grad=dg, total=total, divisors=div,
                                 value=st.value, wl_value=st.wl_value, energy=st.energy)
         return bundle, st.ovfl, st.exact, int(st.ncross)

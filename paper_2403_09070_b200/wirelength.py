@@ -115,12 +115,14 @@ def partial_hpwl(values):
 def wa_smooth(values, gamma):
     """WA smoothed span and gradient of one coordinate set (wirelength.py:58-73),
     evaluated by the K1 kernel as a single-net z-span."""
-    v = _dev.f64(np.asarray(values, dtype=float) if not isinstance(values, torch.Tensor) else values)
+    host = not isinstance(values, torch.Tensor)
+    v = _dev.f64(np.asarray(values, dtype=float) if host else values)
     n = v.numel()
     if n == 0:
-        return 0.0, torch.zeros(0, dtype=torch.float64, device="cuda")
+        return 0.0, (np.zeros(0) if host else torch.zeros(0, dtype=torch.float64, device="cuda"))
     topo = NetTopology(np.array([0, n]), np.zeros(n, np.int64), np.arange(n), n)
-    return z_cut_penalty(topo, v, gamma)
+    val, grad = z_cut_penalty(topo, v, gamma)
+    return float(val), (_dev.host(grad) if host else grad)
 
 
 class NetBoxes:

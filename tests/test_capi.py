@@ -15,7 +15,7 @@ LIB = os.path.join(ROOT, "paper_2403_09070_b200", "libp3d.so")
 def declared():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:int|size_t)\s+(p3d_\w+)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|void|double)\s+(p3d_\w+)\s*\(", src, flags=re.M)))
 
 
 @pytest.fixture(scope="module")

@@ -113,7 +113,7 @@ def test_nesterov_optimizer_matches_oracle():
     proj_np = lambda p: np.clip(p, lo, hi)  # noqa: E731
     proj_t = lambda p: torch.clamp(p, lo, hi)  # noqa: E731
     ref = P.Nesterov(x0, project=proj_np)
-    opt = NesterovOptimizer(x0, project=proj_t)
+    opt = NesterovOptimizer(torch.from_numpy(x0).cuda(), project=proj_t)  # tensors in, tensors out
     prev_r = prev_t = None
     for k in range(12):
         gr = A * ref.v - b  # gradient of sum(A x^2 / 2 - b x) at the lookahead point
