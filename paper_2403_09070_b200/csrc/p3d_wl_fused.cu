@@ -131,6 +131,15 @@ __device__ const double kExp2Tab[64] = {
 #ifndef P3D_EXP_CONST
 #define P3D_EXP_CONST 1
 #endif
+#ifndef P3D_K1_EARLY
+#define P3D_K1_EARLY 1
+#endif
+#ifndef P3D_K1_PREFETCH
+#define P3D_K1_PREFETCH 0  // 1: next task's pin streams prefetched to L1, 2: to L2
+#endif
+#ifndef P3D_EXP_ESTRIN
+#define P3D_EXP_ESTRIN 0
+#endif
 #if P3D_EXP_POLY
 // Table-free variant: n = rint(x / ln 2), Cody-Waite r (|r| <= ln2/2), degree-13
 // Taylor polynomial by Horner (<= 1.2 ulp over [-708, 0]); no memory access.
@@ -171,9 +180,23 @@ __device__ __forceinline__ double exp_neg(double x) {
 #endif
   const double n = rint(x * c[0]);
   const double r = fma(-n, c[2], fma(-n, c[1], x));
+#if P3D_EXP_ESTRIN
+  // Estrin's scheme: the same polynomial at dependency depth 4 instead of
+  // 13 (three more operations; K1's exp stalls were fixed-latency waits on
+  // the Horner chain).  c[16 - k] = 1/k!.
+  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+  const double q0 = fma(c[15], r, c[16]), q1 = fma(c[13], r, c[14]);
+  const double q2 = fma(c[11], r, c[12]), q3 = fma(c[9], r, c[10]);
+  const double q4 = fma(c[7], r, c[8]), q5 = fma(c[5], r, c[6]);
+  const double q6 = fma(c[3], r, c[4]);
+  const double s0 = fma(q1, r2, q0), s1 = fma(q3, r2, q2), s2 = fma(q5, r2, q4);
+  const double t0 = fma(s1, r4, s0), t1 = fma(q6, r4, s2);
+  const double p = fma(t1, r8, t0);
+#else
   double p = c[3];
 #pragma unroll
   for (int k = 4; k < 17; ++k) p = fma(p, r, c[k]);
+#endif
   const double sc = __longlong_as_double((long long)((int)n + 1023) << 52);
   return x < -708.0 ? 0.0 : p * sc;
 }
@@ -579,7 +602,9 @@ __device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk,
   const int nb = tk.y, j = tk.z + lane;
   if (j >= nb) return false;
   const uint8_t nd = a.net_dup[t0 + j];
+#if !P3D_K1_EARLY
   if (nd & 1) return false;  // duplicate-owner nets: generic kernel
+#endif
   pm = (nd & 2) ? 0.0 : 1.0;  // value counted by another rank (halo mode)
   const int pin0 = tk.x + j;
   constexpr int KM = D ? D : kMaxStagedDeg;
@@ -592,6 +617,9 @@ __device__ __forceinline__ bool stage_pins(const FusedNetArgs& a, const int4 tk,
     inst[k] = ld_stream(a.pin_inst + pin0 + k * nb);
     off[k] = ld_stream(a.off + pin0 + k * nb);
   }
+#if P3D_K1_EARLY
+  if (nd & 1) return false;  // duplicate-owner nets: generic kernel
+#endif
   topm = 0;
   zhi = -P3D_INF;
   zlo = P3D_INF;
@@ -704,7 +732,9 @@ __device__ __forceinline__ void triple_task(const FusedNetArgs& a, const int4 tk
   const int nb = tk.y, j = tk.z + lane;
   if (j >= nb) return;
   const uint8_t nd = a.net_dup[t0 + j];
+#if !P3D_K1_EARLY
   if (nd & 1) return;  // duplicate-owner nets: generic kernel
+#endif
   const double pm = (nd & 2) ? 0.0 : 1.0;  // value counted by another rank (halo mode)
   const int p0 = tk.x + j;
   int inst[3], slot[3];
@@ -715,6 +745,9 @@ __device__ __forceinline__ void triple_task(const FusedNetArgs& a, const int4 tk
     slot[k] = ld_stream(a.slot + p0 + k * nb);
     off[k] = ld_stream(a.off + p0 + k * nb);
   }
+#if P3D_K1_EARLY
+  if (nd & 1) return;  // duplicate-owner nets: generic kernel
+#endif
   double x[3], y[3], z[3];
   int tp[3];
 #pragma unroll
@@ -781,12 +814,17 @@ __device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, 
   const int nb = tk.y, j = tk.z + lane;
   if (j >= nb) return;
   const uint8_t nd = a.net_dup[t0 + j];
+#if !P3D_K1_EARLY
   if (nd & 1) return;  // duplicate-owner nets: generic kernel
+#endif
   const double pm = (nd & 2) ? 0.0 : 1.0;  // value counted by another rank (halo mode)
   const int p0 = tk.x + j, p1 = p0 + nb;
   const int i0 = ld_stream(a.pin_inst + p0), i1 = ld_stream(a.pin_inst + p1);
   const int s0 = ld_stream(a.slot + p0), s1 = ld_stream(a.slot + p1);
   const float4 o0 = ld_stream(a.off + p0), o1 = ld_stream(a.off + p1);
+#if P3D_K1_EARLY  // the flag load overlaps the pin loads instead of preceding them
+  if (nd & 1) return;  // duplicate-owner nets: generic kernel
+#endif
 #ifdef P3D_PROBE_NOGATHER
   const double4 q0 = a.pos4[i0 & 31], q1 = a.pos4[i1 & 31];
 #else
@@ -825,6 +863,27 @@ __device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk
     staged_eval<D, F32>(a, tk.x + tk.z + lane, tk.y, sm, lane, topm, zhi, zlo, acc, nd, pm);
 }
 
+#if P3D_K1_PREFETCH
+// Prefetch the pin streams of a lane's net in the next task (its descriptor
+// arrived during this task), so that task's first loads hit the cache.
+__device__ __forceinline__ void prefetch_task(const FusedNetArgs& a, const int4 tk, int t0, int lane) {
+  const int nb = tk.y, j = tk.z + lane;
+  if (j >= nb || tk.w > kMaxStagedDeg) return;
+  const int p0 = tk.x + j;
+  for (int k = 0; k < tk.w; ++k) {
+#if P3D_K1_PREFETCH == 1
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.pin_inst + p0 + k * nb));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.off + p0 + k * nb));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.slot + p0 + k * nb));
+#else
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.pin_inst + p0 + k * nb));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.off + p0 + k * nb));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.slot + p0 + k * nb));
+#endif
+  }
+}
+#endif
+
 template <bool F32>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_kernel(FusedNetArgs a) {
   pdl_wait();
@@ -837,11 +896,24 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_ke
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   WarpCols<F32>& sm = reinterpret_cast<WarpCols<F32>*>(dyn_smem)[wib];
   const int wstride = gridDim.x * kWarpsPerBlock;
+#if P3D_K1_EARLY  // the next task's descriptor is loaded while this one runs
+  int wn = a.task_rank + (blockIdx.x * kWarpsPerBlock + wib) * a.task_size;
+  int4 tkn = make_int4(0, 0, 0, 0);
+  int t0n = 0;
+  if (wn < a.n_tasks) { tkn = a.tasks[wn]; t0n = a.task_t0[wn]; }
+  for (;;) {
+    if (wn >= a.n_tasks) break;
+    const int4 tk = tkn;
+    const int t0 = t0n;
+    wn += wstride * a.task_size;
+    if (wn < a.n_tasks) { tkn = a.tasks[wn]; t0n = a.task_t0[wn]; }
+#else
   for (int j = blockIdx.x * kWarpsPerBlock + wib;; j += wstride) {
     const int w = a.task_rank + j * a.task_size;  // this rank's warp tasks (sharded loop)
     if (w >= a.n_tasks) break;
     const int4 tk = a.tasks[w];
     const int t0 = a.task_t0[w];
+#endif
     // timing probes only (they drop work; results are wrong): -DP3D_SKIP_D2 / _DGE3
 #ifdef P3D_SKIP_D2
     if (tk.w == 2) continue;
@@ -865,6 +937,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_ke
 #endif
       default: break;  // generic nets run in generic_net_kernel
     }
+#if P3D_K1_PREFETCH && P3D_K1_EARLY
+    if (wn < a.n_tasks) prefetch_task(a, tkn, t0n, lane);
+#endif
   }
   block_sum<6>(acc, red);
   if (threadIdx.x == 0)
