@@ -134,6 +134,9 @@ __device__ const double kExp2Tab[64] = {
 #ifndef P3D_K1_EARLY
 #define P3D_K1_EARLY 1
 #endif
+#ifndef P3D_K1_SLOT_EARLY
+#define P3D_K1_SLOT_EARLY 1  // 1: before the y axis, 2: before the x axis
+#endif
 #ifndef P3D_K1_PREFETCH
 #define P3D_K1_PREFETCH 0  // 1: next task's pin streams prefetched to L1, 2: to L2
 #endif
@@ -672,19 +675,35 @@ P3D_K1_LOOP_UNROLL
   }
   double v, ex;
   bool cross;
-  staged_axis<D, F32>(sm.px, sm, lane, topm, ig, v, ex, cross, nd);
-  acc[0] += pm * v;
-  acc[3] += pm * ex;
-  acc[5] += pm * (cross ? 1.0 : 0.0);
-  staged_axis<D, F32>(sm.py, sm, lane, topm, ig, v, ex, cross, nd);
-  acc[1] += pm * v;
-  acc[4] += pm * ex;
   int slot[KM];
+#if P3D_K1_SLOT_EARLY == 2
 #pragma unroll
   for (int k = 0; k < KM; ++k) {
     if (k >= DD) break;
     slot[k] = ld_stream(a.slot + pin0 + k * nb);
   }
+#endif
+  staged_axis<D, F32>(sm.px, sm, lane, topm, ig, v, ex, cross, nd);
+  acc[0] += pm * v;
+  acc[3] += pm * ex;
+  acc[5] += pm * (cross ? 1.0 : 0.0);
+#if P3D_K1_SLOT_EARLY == 1  // the record slots load while the y axis is evaluated
+#pragma unroll
+  for (int k = 0; k < KM; ++k) {
+    if (k >= DD) break;
+    slot[k] = ld_stream(a.slot + pin0 + k * nb);
+  }
+#endif
+  staged_axis<D, F32>(sm.py, sm, lane, topm, ig, v, ex, cross, nd);
+  acc[1] += pm * v;
+  acc[4] += pm * ex;
+#if !P3D_K1_SLOT_EARLY
+#pragma unroll
+  for (int k = 0; k < KM; ++k) {
+    if (k >= DD) break;
+    slot[k] = ld_stream(a.slot + pin0 + k * nb);
+  }
+#endif
 #pragma unroll
   for (int k = 0; k < KM; ++k) {
     if (k >= DD) break;
