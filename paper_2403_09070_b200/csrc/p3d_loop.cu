@@ -165,13 +165,35 @@ __device__ __forceinline__ double precond_div(double lam, double q, double mdeg)
 #ifndef P3D_K4_KEEP
 #define P3D_K4_KEEP 1
 #endif
+// P3D_PRE_STORE: K4 stores the preconditioned gradient the step uses (K5 reads
+// 24 B per object instead of re-deriving it from 56 B of raw gradients) and
+// this point's gradient re-weighted under the NEXT lambda, which is known here
+// already: lambda_{t+1} = lambda_t mu(ovfl_{t-1}, ovfl_t), and ovfl_t comes
+// from K3.  So K4 reads 24 B of re-weighted previous gradient instead of 56 B
+// of raw ones.  Same operations on the same operands: bit-identical iterates.
+// Iteration 0 (lambda set by K4's own reduction) keeps the raw gradients and
+// gmax0_kernel converts them in place.
+#ifndef P3D_PRE_STORE
+#define P3D_PRE_STORE 1
+#endif
+
+// mu_from_overflow (gp.py:156-168)
+__device__ __forceinline__ double mu_of(const p3d_gp& gp, double prev_ovfl, double ovfl) {
+  const double drop = prev_ovfl - ovfl;
+  double mu;
+  if (drop < 0) mu = gp.mu_min;
+  else if (drop >= 2e-3) mu = gp.mu_min + 0.01;
+  else if (drop >= 5e-4) mu = (gp.mu_min + gp.mu_max) / 2;
+  else mu = gp.mu_max;
+  return fmin(fmax(mu, gp.mu_min), gp.mu_max);
+}
 #ifndef P3D_K4_LDCS
 #define P3D_K4_LDCS 0
 #endif
 // per-launch scalars of K4 (the loop state changes only in the last block,
 // after every object has been processed)
 struct DensScal {
-  double lam, zscale;
+  double lam, zscale, lam_next;
   bool eval_only, bb;
 };
 
@@ -213,6 +235,30 @@ __device__ __forceinline__ void finish_object(const p3d_gp& gp, int i, const Cha
   // BB denominator: the previous iteration's raw gradients re-weighted by the
   // current lambda (gp.py:427-435); at iteration 0 there is no previous point.
   // (The numerator |v - v_prev|^2 comes from the last advance.)
+#if P3D_PRE_STORE
+  if (sc.bb) {  // pw = this point's predecessor, re-weighted under lam (last K4)
+    const double div = precond_div(lam, qq, mdeg);
+    const double ydiv = 1.0 / div;
+    const double lamn = sc.lam_next;
+    const double divn = precond_div(lamn, qq, mdeg);
+    const double ydivn = 1.0 / divn;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double pre = div_rcp(wl[k] + lam * dg[k], div, ydiv);
+      const double d = pre - pw[k];
+      acc[5] += d * d;
+      const double ppn = div_rcp(wl[k] + lamn * dg[k], divn, ydivn);
+#if P3D_K4_KEEP
+      st_keep(gp.prev_wl + (long long)k * O + i, pre);
+      st_keep(gp.prev_dens + (long long)k * O + i, ppn);
+#else
+      gp.prev_wl[(long long)k * O + i] = pre;
+      gp.prev_dens[(long long)k * O + i] = ppn;
+#endif
+    }
+    return;
+  }
+#else
   if (sc.bb) {
     const double div = precond_div(lam, qq, mdeg);
     const double divp = precond_div(lam, pq, mdeg);
@@ -225,6 +271,7 @@ __device__ __forceinline__ void finish_object(const p3d_gp& gp, int i, const Cha
       acc[5] += d * d;
     }
   }
+#endif
 #if P3D_K4_KEEP  // K5 reads these right after: keep them in L2
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -264,12 +311,17 @@ __device__ __forceinline__ void load_object_inputs(const p3d_gp& gp, int i, cons
   pq = mdeg = 0.0;
   pw[0] = pw[1] = pw[2] = pd[0] = pd[1] = pd[2] = 0.0;
   if (sc.bb && !sc.eval_only) {
+#if P3D_PRE_STORE
+#pragma unroll
+    for (int k = 0; k < 3; ++k) pw[k] = gp.prev_dens[(long long)k * O + i];
+#else
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       pw[k] = gp.prev_wl[(long long)k * O + i];
       pd[k] = gp.prev_dens[(long long)k * O + i];
     }
     pq = gp.prev_q[i];
+#endif
     mdeg = (i < I && gp.is_macro[i]) ? gp.degree[i] : 0.0;
   }
 }
@@ -392,6 +444,9 @@ __global__ void __launch_bounds__(256, P3D_K4_MINB) dens_kernel(p3d_gp gp) {
   {
     const double* f = fin(gp);
     sc.zscale = f[kFinNorm + 2] == 0.0 ? 0.0 : f[kFinNorm + 3];  // Eq. 17 (0 if |gz| = 0)
+    // lambda of the next iteration, exactly as advance_kernel will form it
+    const double ovfl = gp.movable_volume <= 0 ? 0.0 : f[kFinOvfl];
+    sc.lam_next = sc.lam * mu_of(gp, st->prev_ovfl, ovfl);
   }
   const CloudGP cl = cloud_of(gp, gp.v);
   double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -452,16 +507,28 @@ __global__ void __launch_bounds__(256) gmax0_kernel(p3d_gp gp) {
   __shared__ double red[32];
   const int O = gp.n_obj, I = gp.n_inst;
   const double lam = st->lam;
+#if P3D_PRE_STORE
+  const double lam1 = lam * mu_of(gp, st->prev_ovfl, st->ovfl);  // as advance_kernel forms it
+#endif
   double m = 0.0;
   const int n_own = own_count(gp);
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_own; k += gridDim.x * blockDim.x) {
     const int i = own_obj(gp, k);
     const double mdeg = (i < I && gp.is_macro[i]) ? gp.degree[i] : 0.0;
     const double div = precond_div(lam, gp.prev_q[i], mdeg);
+#if P3D_PRE_STORE  // the raw gradients of iteration 0 -> (pre, re-weighted under lambda_1)
+    const double ydiv = 1.0 / div;
+    const double divn = precond_div(lam1, gp.prev_q[i], mdeg), ydivn = 1.0 / divn;
+#endif
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       const long long j = (long long)k * O + i;
       m = fmax(m, fabs((gp.prev_wl[j] + lam * gp.prev_dens[j]) / div));
+#if P3D_PRE_STORE
+      const double w = gp.prev_wl[j], d = gp.prev_dens[j];
+      gp.prev_wl[j] = div_rcp(w + lam * d, div, ydiv);
+      gp.prev_dens[j] = div_rcp(w + lam1 * d, divn, ydivn);
+#endif
     }
   }
   double* part = gp.partials + (long long)kSlotStep * kPartialStride;
@@ -521,16 +588,23 @@ __global__ void __launch_bounds__(256, P3D_K5_MINB) advance_kernel(p3d_gp gp) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_own; k += gridDim.x * blockDim.x) {
     const int i = own_obj(gp, k);
     const bool inst = i < I;
-    double u[3], v[3], pw[3], pd[3];
+    double u[3], v[3], pw[3];
+#if !P3D_PRE_STORE
+    double pd[3];
+#endif
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const long long j = (long long)c * O + i;
       u[c] = gp.u[j];
       v[c] = gp.v[j];
-      pw[c] = __ldg(gp.prev_wl + j);
+      pw[c] = __ldg(gp.prev_wl + j);  // P3D_PRE_STORE: the preconditioned gradient
+#if !P3D_PRE_STORE
       pd[c] = __ldg(gp.prev_dens + j);
+#endif
     }
+#if !P3D_PRE_STORE
     const double pq = __ldg(gp.prev_q + i);
+#endif
     bool mac = false;
     double s0, s1, s2 = 0.0, s3 = 0.0, fz = 0.0, mdeg = 0.0;
     if (inst) {
@@ -539,7 +613,9 @@ __global__ void __launch_bounds__(256, P3D_K5_MINB) advance_kernel(p3d_gp gp) {
       s1 = __ldg(gp.h_top + i);
       s2 = __ldg(gp.w_bot + i);
       s3 = __ldg(gp.h_bot + i);
+#if !P3D_PRE_STORE
       if (mac) mdeg = __ldg(gp.degree + i);
+#endif
     } else {
       const int f = i - I;
       s0 = __ldg(gp.fill_w + f);
@@ -551,12 +627,19 @@ __global__ void __launch_bounds__(256, P3D_K5_MINB) advance_kernel(p3d_gp gp) {
       for (int c = 0; c < 3; ++c) gp.best[(long long)c * O + i] = u[c];
     }
     if (stop) continue;
+    double un[3], vn[3];
+#if P3D_PRE_STORE
+    (void)mdeg;
+    (void)lam;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) un[c] = v[c] - step * pw[c];
+#else
     // the step's gradient, re-derived from the stored raw gradients (gp.py:424-426)
     const double div = precond_div(lam, pq, mdeg);
-    double un[3], vn[3];
     const double ydiv = 1.0 / div;
 #pragma unroll
     for (int c = 0; c < 3; ++c) un[c] = v[c] - step * div_rcp(pw[c] + lam * pd[c], div, ydiv);
+#endif
     project_loaded(gp, inst, mac, s0, s1, s2, s3, fz, un[0], un[1], un[2]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) vn[c] = un[c] + mom * (un[c] - u[c]);
@@ -587,13 +670,7 @@ __global__ void __launch_bounds__(256, P3D_K5_MINB) advance_kernel(p3d_gp gp) {
       st->dv2_next = tot;
       st->a = st->a_new;
       // mu_from_overflow (gp.py:156-168), lambda update (gp.py:442-444)
-      const double drop = st->prev_ovfl - st->ovfl;
-      double mu;
-      if (drop < 0) mu = gp.mu_min;
-      else if (drop >= 2e-3) mu = gp.mu_min + 0.01;
-      else if (drop >= 5e-4) mu = (gp.mu_min + gp.mu_max) / 2;
-      else mu = gp.mu_max;
-      mu = fmin(fmax(mu, gp.mu_min), gp.mu_max);
+      const double mu = mu_of(gp, st->prev_ovfl, st->ovfl);
       st->last_mu = mu;
       st->lam *= mu;
       st->prev_ovfl = st->ovfl;

@@ -137,6 +137,9 @@ __device__ const double kExp2Tab[64] = {
 #ifndef P3D_K1_SLOT_EARLY
 #define P3D_K1_SLOT_EARLY 1  // 1: before the y axis, 2: before the x axis
 #endif
+#ifndef P3D_K1_PAIR2
+#define P3D_K1_PAIR2 0
+#endif
 #ifndef P3D_K1_PREFETCH
 #define P3D_K1_PREFETCH 0  // 1: next task's pin streams prefetched to L1, 2: to L2
 #endif
@@ -827,36 +830,64 @@ __device__ __forceinline__ void pair_axis(double v0, double v1, typename WaSel<F
 // Degree-2 nets (about half of all nets): never split (both partial spans are
 // 0 or the full span) and the FD flip delta is exactly 0 for both pins
 // (wirelength.py:227-248), so a lane evaluates its net from registers.
-template <bool F32>
-__device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, int t0, int lane,
-                                          double (&acc)[6]) {
+// One lane's degree-2 net, split into its loads and its evaluation so that two
+// tasks' loads can be in flight together (pair2_task).
+struct PairLd {
+  int ok, s0, s1;
+  double pm;
+  double2 q0, q1;  // (x, y) of the two owners
+  double z0, z1;
+  float4 o0, o1;
+};
+
+__device__ __forceinline__ PairLd pair_load(const FusedNetArgs& a, const int4 tk, int t0, int lane) {
+  PairLd L;
   const int nb = tk.y, j = tk.z + lane;
-  if (j >= nb) return;
+  L.ok = 0;
+  if (j >= nb) return L;
   const uint8_t nd = a.net_dup[t0 + j];
 #if !P3D_K1_EARLY
-  if (nd & 1) return;  // duplicate-owner nets: generic kernel
+  if (nd & 1) return L;  // duplicate-owner nets: generic kernel
 #endif
-  const double pm = (nd & 2) ? 0.0 : 1.0;  // value counted by another rank (halo mode)
+  L.pm = (nd & 2) ? 0.0 : 1.0;  // value counted by another rank (halo mode)
   const int p0 = tk.x + j, p1 = p0 + nb;
   const int i0 = ld_stream(a.pin_inst + p0), i1 = ld_stream(a.pin_inst + p1);
-  const int s0 = ld_stream(a.slot + p0), s1 = ld_stream(a.slot + p1);
-  const float4 o0 = ld_stream(a.off + p0), o1 = ld_stream(a.off + p1);
+  L.s0 = ld_stream(a.slot + p0);
+  L.s1 = ld_stream(a.slot + p1);
+  L.o0 = ld_stream(a.off + p0);
+  L.o1 = ld_stream(a.off + p1);
 #if P3D_K1_EARLY  // the flag load overlaps the pin loads instead of preceding them
-  if (nd & 1) return;  // duplicate-owner nets: generic kernel
+  if (nd & 1) return L;  // duplicate-owner nets: generic kernel
 #endif
 #ifdef P3D_PROBE_NOGATHER
-  const double4 q0 = a.pos4[i0 & 31], q1 = a.pos4[i1 & 31];
+  const double* pb0 = reinterpret_cast<const double*>(a.pos4 + (i0 & 31));
+  const double* pb1 = reinterpret_cast<const double*>(a.pos4 + (i1 & 31));
 #else
-  const double4 q0 = a.pos4[i0], q1 = a.pos4[i1];
+  const double* pb0 = reinterpret_cast<const double*>(a.pos4 + i0);
+  const double* pb1 = reinterpret_cast<const double*>(a.pos4 + i1);
 #endif
-  const int t0p = (q0.z - a.dz2) > 0.0, t1p = (q1.z - a.dz2) > 0.0;
+  L.q0 = *reinterpret_cast<const double2*>(pb0);
+  L.q1 = *reinterpret_cast<const double2*>(pb1);
+  L.z0 = pb0[2];
+  L.z1 = pb1[2];
+  L.ok = 1;
+  return L;
+}
+
+template <bool F32>
+__device__ __forceinline__ void pair_eval(const FusedNetArgs& a, const PairLd& L, double (&acc)[6]) {
+  if (!L.ok) return;
+  const double2 q0 = L.q0, q1 = L.q1;
+  const float4 o0 = L.o0, o1 = L.o1;
+  const double pm = L.pm;
+  const int t0p = (L.z0 - a.dz2) > 0.0, t1p = (L.z1 - a.dz2) > 0.0;
   const double x0 = q0.x + (double)(t0p ? o0.x : o0.z), y0 = q0.y + (double)(t0p ? o0.y : o0.w);
   const double x1 = q1.x + (double)(t1p ? o1.x : o1.z), y1 = q1.y + (double)(t1p ? o1.y : o1.w);
   const typename WaSel<F32>::R ig = (typename WaSel<F32>::R)a.inv_gamma;
   double vx, vy, vz, gx0, gx1, gy0, gy1, gz0, gz1;
   pair_axis<F32>(x0, x1, ig, vx, gx0, gx1);
   pair_axis<F32>(y0, y1, ig, vy, gy0, gy1);
-  pair_axis<F32>(q0.z, q1.z, ig, vz, gz0, gz1);
+  pair_axis<F32>(L.z0, L.z1, ig, vz, gz0, gz1);
   acc[0] += pm * vx;
   acc[1] += pm * vy;
   acc[2] += pm * vz;
@@ -864,12 +895,33 @@ __device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, 
   acc[4] += pm * (dmax(y0, y1) - dmin(y0, y1));
   acc[5] += pm * ((t0p != t1p) ? 1.0 : 0.0);
   if (F32) {
-    a.out_f[s0] = make_float4((float)gx0, (float)gy0, (float)gz0, 0.f);
-    a.out_f[s1] = make_float4((float)gx1, (float)gy1, (float)gz1, 0.f);
+    a.out_f[L.s0] = make_float4((float)gx0, (float)gy0, (float)gz0, 0.f);
+    a.out_f[L.s1] = make_float4((float)gx1, (float)gy1, (float)gz1, 0.f);
   } else {
-    store_rec(a.out_d, s0, gx0, gy0, gz0, 0.0);
-    store_rec(a.out_d, s1, gx1, gy1, gz1, 0.0);
+    store_rec(a.out_d, L.s0, gx0, gy0, gz0, 0.0);
+    store_rec(a.out_d, L.s1, gx1, gy1, gz1, 0.0);
   }
+}
+
+// Degree-2 nets (about half of all nets): never split (both partial spans are
+// 0 or the full span) and the FD flip delta is exactly 0 for both pins
+// (wirelength.py:227-248), so a lane evaluates its net from registers.
+template <bool F32>
+__device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, int t0, int lane,
+                                          double (&acc)[6]) {
+  pair_eval<F32>(a, pair_load(a, tk, t0, lane), acc);
+}
+
+// Two consecutive degree-2 tasks of one warp: both tasks' loads are issued
+// before either net is evaluated (twice the loads in flight); the nets are
+// accumulated in task order, so the sums are those of two pair_task calls.
+template <bool F32>
+__device__ __forceinline__ void pair2_task(const FusedNetArgs& a, const int4 tk, int t0,
+                                           const int4 tk2, int t02, int lane, double (&acc)[6]) {
+  const PairLd L1 = pair_load(a, tk, t0, lane);
+  const PairLd L2 = pair_load(a, tk2, t02, lane);
+  pair_eval<F32>(a, L1, acc);
+  pair_eval<F32>(a, L2, acc);
 }
 
 template <int D, bool F32>
@@ -939,6 +991,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_ke
 #endif
 #ifdef P3D_SKIP_DGE3
     if (tk.w >= 3) continue;
+#endif
+#if P3D_K1_PAIR2 && P3D_K1_EARLY
+    if (tk.w == 2 && tkn.w == 2 && wn < a.n_tasks) {
+      pair2_task<F32>(a, tk, t0, tkn, t0n, lane, acc);
+      wn += wstride * a.task_size;
+      if (wn < a.n_tasks) { tkn = a.tasks[wn]; t0n = a.task_t0[wn]; }
+      continue;
+    }
 #endif
     switch (tk.w) {
       case 2: pair_task<F32>(a, tk, t0, lane, acc); break;
