@@ -1061,6 +1061,9 @@ __global__ void __launch_bounds__(256) generic_net_kernel(FusedNetArgs a) {
 #define P3D_GATHER_BATCH 4
 #endif
 constexpr int kGatherBatch = P3D_GATHER_BATCH;
+#ifndef P3D_GATHER_EARLY
+#define P3D_GATHER_EARLY 0
+#endif
 
 // owner gather: per object, ordered fp64 sums over its contiguous slot records
 // (pin order within the owner, like bincount)
@@ -1139,11 +1142,29 @@ __global__ void __launch_bounds__(32 * kGatherWarps) gather_warp_kernel(FusedGat
   double2* st = stage[wib];
   double acc[3] = {0, 0, 0};
   const int wstride = gridDim.x * kGatherWarps * 32;
+#if P3D_GATHER_EARLY  // the next group's slot range loads while this group is summed
+  int o0 = (blockIdx.x * kGatherWarps + wib) * 32;
+  int bn = 0, en = 0;
+  if (o0 + lane < a.n_obj) {
+    bn = a.obj_slot_ptr[a.obj0 + o0 + lane];
+    en = a.obj_slot_ptr[a.obj0 + o0 + lane + 1];
+  }
+  for (; o0 < a.n_obj; o0 += wstride) {
+    const int il = o0 + lane, i = a.obj0 + il;
+    const int last = min(a.n_obj, o0 + 32) - 1;
+    const int b = bn, e = en;
+    bn = en = 0;
+    if (o0 + wstride + lane < a.n_obj) {
+      bn = a.obj_slot_ptr[i + wstride];
+      en = a.obj_slot_ptr[i + wstride + 1];
+    }
+#else
   for (int o0 = (blockIdx.x * kGatherWarps + wib) * 32; o0 < a.n_obj; o0 += wstride) {
     const int il = o0 + lane, i = a.obj0 + il;
     const int last = min(a.n_obj, o0 + 32) - 1;
     const int b = il <= last ? a.obj_slot_ptr[i] : 0;
     const int e = il <= last ? a.obj_slot_ptr[i + 1] : 0;
+#endif
     const int rb = __shfl_sync(0xffffffffu, b, 0);
     const int re = __shfl_sync(0xffffffffu, e, last - o0);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;

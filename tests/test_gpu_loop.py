@@ -188,6 +188,30 @@ def test_cfg3_headline_config_vs_reference():
     assert abs(info.final_overflow - ovfl) <= 5e-3 * ovfl
 
 
+def test_cfg4_rows_vs_reference():
+    """Config 4 (4,000,128 cells, 1024x1024x2, the sharded bench's design)
+    against the reference's own first three rows of the 200-iteration
+    schedule (tests/golden/cfg4_rows.json, make_golden.py --cfg4; ~80 s per
+    iteration on one host core): each row within 1e-9, crossings equal."""
+    from paper_2403_09070_b200 import gp as G
+    from paper_2403_09070_b200.synth import CONFIGS, cached_synth
+
+    gold = json.load(open(os.path.join(GOLD, "cfg4_rows.json")))
+    d = cached_synth(CONFIGS[4]["spec"])
+    assert d.n_insts == gold["spec"]["n_insts"]
+    cfg = G.GpConfig(seed=1, nz=2, grid_nx=1024, grid_ny=1024, max_iters=200, stop_overflow=0.0)
+    rng = np.random.default_rng(1)
+    grid = G.choose_grid(d, cfg)
+    st = G.init_state(d, grid, cfg, rng)
+    rows = []
+    G.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+    ref = np.array(gold["sched200_first3"], dtype=float)
+    got = np.array(rows[: len(ref)], dtype=float)
+    assert np.array_equal(got[:, 2], ref[:, 2])
+    assert np.all(np.abs(got[:, 1] - ref[:, 1]) <= 1e-9 * ref[:, 1])
+    assert np.all(np.abs(got[:, 3] - ref[:, 3]) <= 1e-9 * ref[:, 3])
+
+
 def test_cfg3_fp32_wa_mode_within_gate():
     """The opt-in fp32 weighted-average mode (SURVEY App. B plan) at the
     headline config: every row of the 20-iteration schedule (WL, crossings,
