@@ -41,6 +41,17 @@ def u8(x):
     return dev(np.asarray(x).astype(np.uint8), torch.uint8)
 
 
+def stable_argsort(a):
+    """np.argsort(a, kind="stable") of a 1-D integer array, computed on the
+    device (host setup of the loop layouts: the stable order is unique, so
+    the result is the same permutation)."""
+    a = np.ascontiguousarray(np.asarray(a))
+    if a.size < (1 << 16) or not torch.cuda.is_available():
+        return np.argsort(a, kind="stable")
+    t = torch.from_numpy(a).to(DEV)
+    return torch.argsort(t, stable=True).cpu().numpy().astype(np.int64, copy=False)
+
+
 def host(x):
     """Tensor -> numpy (for the reference-shaped return values of the loop driver)."""
     if isinstance(x, torch.Tensor):

@@ -298,7 +298,7 @@ def fused_pin_layout(net_ptr, pin_inst, off4, dup, net_key=None):
     net_ptr = np.asarray(net_ptr, dtype=np.int64)
     deg = np.diff(net_ptr)
     n_net = len(deg)
-    order = np.argsort(deg, kind="stable") if net_key is None else np.lexsort((net_key, deg))
+    order = _dev.stable_argsort(deg) if net_key is None else np.lexsort((net_key, deg))
     dsorted = deg[order]
     base = np.zeros(n_net, dtype=np.int64)
     stride = np.ones(n_net, dtype=np.int64)
@@ -333,7 +333,7 @@ def fused_pin_layout(net_ptr, pin_inst, off4, dup, net_key=None):
     f_off = np.empty((len(pin_inst), 4), dtype=np.float32)
     f_off[dest] = off32
     # owner-sorted slots (stable: original pin order within an owner, like bincount)
-    slot_order = np.argsort(pin_inst, kind="stable")
+    slot_order = _dev.stable_argsort(pin_inst)
     pin_slot = np.empty(len(pin_inst), dtype=np.int64)
     pin_slot[dest[slot_order]] = np.arange(len(pin_inst))
     return dict(tasks=np.asarray(tasks, dtype=np.int64).reshape(-1, 4),
@@ -467,7 +467,7 @@ class Gp3dProblem:
         g.topo = _lib.Topology(tp.n_net, tp.n_pin, I, 0, tp.net_ptr, tp.pin_inst, tp.net_dup,
                                tp.net_order, tp.pin_slot, tp.obj_slot_ptr)
         g.wl_f32 = 1 if self.precision == "fp32" else 0
-        off4 = wl.rotated_pin_offsets(arr, self.rot) if P else np.zeros((0, 4))
+        off4 = self._off4 = wl.rotated_pin_offsets(arr, self.rot) if P else np.zeros((0, 4))
         key = None
         if self.plan is not None:  # group nets by (primary rank, set of ranks touching them)
             key = self.plan.primary * (1 << R)
@@ -500,7 +500,7 @@ class Gp3dProblem:
         gs, gkeep = grid.device()
         g.grid = gs
         self._gkeep = gkeep
-        self.t_pin_off = _dev.f64(wl.rotated_pin_offsets(arr, self.rot) if P else np.zeros((1, 4)))
+        self.t_pin_off = _dev.f64(self._off4 if P else np.zeros((1, 4)))
         g.pin_off = keep(self.t_pin_off)
         g.w_top = keep(_dev.f64(self.w_top if I else np.zeros(1)))
         g.h_top = keep(_dev.f64(self.h_top if I else np.zeros(1)))

@@ -67,8 +67,8 @@ class DeviceTopology:
         if net_has_dup is None:
             net_has_dup = net_dup_flags(net_ptr, pin_inst)
         deg = np.diff(net_ptr)
-        order = np.argsort(deg, kind="stable")
-        slot_order = np.argsort(pin_inst, kind="stable")
+        order = _dev.stable_argsort(deg)
+        slot_order = _dev.stable_argsort(pin_inst)
         slot = np.empty(n_pin, dtype=np.int64)
         slot[slot_order] = np.arange(n_pin)
         optr = np.zeros(n_obj + 1, dtype=np.int64)
@@ -300,7 +300,11 @@ def normalize_z_gradient(grad_x, grad_y, grad_z_bistratal, grad_z_hbt, alpha):
 
 def rotated_pin_offsets(arrays, rot):
     """[n_pin][4] (rx_top, ry_top, rx_bot, ry_bot), fixed while GP runs."""
-    q = np.asarray(rot)[arrays.pin_inst]
+    rot = np.asarray(rot)
+    if not np.any(rot % 4):  # no quarter turn anywhere (every first GP pass): the offsets
+        return np.ascontiguousarray(np.stack([arrays.ox_top, arrays.oy_top, arrays.ox_bot,
+                                              arrays.oy_bot], axis=1), dtype=np.float64)
+    q = rot[arrays.pin_inst]
     rx_t, ry_t = rotate_offsets(arrays.ox_top, arrays.oy_top, q)
     rx_b, ry_b = rotate_offsets(arrays.ox_bot, arrays.oy_bot, q)
     return np.ascontiguousarray(np.stack([rx_t, ry_t, rx_b, ry_b], axis=1))
