@@ -191,22 +191,26 @@ def optimal_region(top_box, bot_box):
 
 def optimal_hbt_centers(arrays, x, y, z, rot, dz):
     """Optimal-region centre per crossing net (wirelength.py:325-342):
-    {net index: (cx, cy)} for nets with pins on both dies; the boxes run on the
-    device (NetBoxes), the dict is assembled on the host."""
+    {net index: (cx, cy)} for nets with pins on both dies.  The per-die boxes
+    run on the device (NetBoxes); the region centres are formed vectorised
+    with optimal_region's arithmetic ((min(lo, hi) + max(lo, hi)) / 2 ==
+    (lo + hi) / 2 exactly) and the dict is assembled once."""
     topo = NetTopology.from_arrays(arrays)
     px, py, _, on_top = dynamic_pin_coords(arrays, x, y, z, rot, dz)
     bx = NetBoxes(topo, px, on_top)
     by = NetBoxes(topo, py, on_top)
     cnt = _dev.host(bx.cnt)
     crossing = np.flatnonzero((cnt[:, 0] > 0) & (cnt[:, 1] > 0))
-    mnx, mxx = _dev.host(bx.min1), _dev.host(bx.max1)
-    mny, mxy = _dev.host(by.min1), _dev.host(by.max1)
-    out = {}
-    for j in crossing:
-        r = optimal_region((mnx[j, 1], mxx[j, 1], mny[j, 1], mxy[j, 1]),
-                           (mnx[j, 0], mxx[j, 0], mny[j, 0], mxy[j, 0]))
-        out[int(j)] = ((r[0] + r[1]) / 2, (r[2] + r[3]) / 2)
-    return out
+    mnx, mxx = _dev.host(bx.min1)[crossing], _dev.host(bx.max1)[crossing]
+    mny, mxy = _dev.host(by.min1)[crossing], _dev.host(by.max1)[crossing]
+
+    def centre(mn, mx):  # optimal_region on one axis: top box index 1, bottom index 0
+        lo = np.maximum(mn[:, 1], mn[:, 0])
+        hi = np.minimum(mx[:, 1], mx[:, 0])
+        return (np.minimum(lo, hi) + np.maximum(lo, hi)) / 2
+
+    cx, cy = centre(mnx, mxx), centre(mny, mxy)
+    return dict(zip(crossing.tolist(), zip(cx.tolist(), cy.tolist())))
 
 
 @_dev.numpy_io("coord")

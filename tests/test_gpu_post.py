@@ -92,3 +92,28 @@ def test_check_solution_vs_reference(name):
         assert rep.hpwl == pytest.approx(ref["hpwl"], rel=1e-12)
         assert rep.hbt_count == ref["hbt_count"]
         assert rep.raw_score == pytest.approx(ref["raw_score"], rel=1e-12)
+
+
+@pytest.mark.parametrize("rotated", [False, True])
+def test_optimal_hbt_centers_vs_oracle(rotated):
+    """wirelength.optimal_hbt_centers (wirelength.py:325-342)
+    against the oracle's restatement (oracle.port.hbt_centers, pinned to the
+    reference by test_oracle.py) on a config-1 design with random positions
+    across both dies (and quarter-turned instances): the same crossing nets,
+    the same centres bit for bit."""
+    from oracle import port as P
+    from paper_2403_09070_b200 import wirelength as wl
+    from paper_2403_09070_b200.synth import CONFIGS, synth_arrays
+
+    d = synth_arrays(CONFIGS[1]["spec"])
+    a = d.arrays()
+    rng = np.random.default_rng(5)
+    dz = 47.52
+    x = rng.uniform(0, d.die.width, a.n_inst)
+    y = rng.uniform(0, d.die.height, a.n_inst)
+    z = np.where(rng.random(a.n_inst) < 0.5, dz / 4, 3 * dz / 4)
+    rot = rng.integers(0, 4, a.n_inst) if rotated else np.zeros(a.n_inst, dtype=np.int64)
+    got = wl.optimal_hbt_centers(a, x, y, z, rot, dz)
+    want = P.hbt_centers(a, x, y, z, rot, dz)
+    assert len(want) > 1000 and got.keys() == want.keys()
+    assert all(got[j] == want[j] for j in want)
