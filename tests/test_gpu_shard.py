@@ -153,3 +153,18 @@ def test_sharded_nccl_collectives_and_graph_capture():
     assert eager == graphed
     for a, b in zip(eager, rows):
         assert a[2] == b[2] and abs(a[1] - b[1]) <= 1e-12 * abs(b[1]) and abs(a[3] - b[3]) <= 1e-12
+
+
+def test_locality_order_device_matches_host():
+    """The sharded loop's instance numbering (partition.locality_order) runs
+    on the GPU; it must be reproducible (every rank computes it on its own)
+    and equal to the CPU result: stable sorts and integer scans only."""
+    from paper_2403_09070_b200.partition import locality_order
+    from paper_2403_09070_b200.synth import CONFIGS, synth_arrays
+
+    a = synth_arrays(CONFIGS[1]["spec"]).arrays()
+    g1 = locality_order(a.net_ptr, a.pin_inst, a.n_inst, device="cuda")
+    g2 = locality_order(a.net_ptr, a.pin_inst, a.n_inst, device="cuda")
+    c = locality_order(a.net_ptr, a.pin_inst, a.n_inst, device="cpu")
+    assert np.array_equal(g1, g2) and np.array_equal(g1, c)
+    assert np.array_equal(np.sort(g1), np.arange(a.n_inst))
