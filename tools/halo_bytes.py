@@ -1,7 +1,7 @@
 """Per-rank, per-iteration exchange bytes of the sharded loop at a config:
 halo mode (partition.HaloPlan on the locality order) vs the round-robin
 mode's owner-sum reduce-scatter + pos4 all-gather; plus the rho all-reduce
-both modes share.  CPU only.  usage: python tools/halo_bytes.py CONFIG"""
+both modes share (the numbering runs on the GPU when there is one).  usage: python tools/halo_bytes.py CONFIG"""
 import json
 import os
 import sys
