@@ -114,6 +114,9 @@ __device__ __forceinline__ void scan_tiles(const TileSort& ts) {
 #ifndef P3D_SCATTER_DIRECT
 #define P3D_SCATTER_DIRECT 1
 #endif
+#ifndef P3D_SCATTER_SZREC
+#define P3D_SCATTER_SZREC 1  // sort records hold both dies' sizes (see chunk_charge)
+#endif
 #ifndef P3D_SCATTER_CELL
 #define P3D_SCATTER_CELL 1
 #endif
@@ -235,6 +238,19 @@ __global__ void __launch_bounds__(256) tile_place_kernel(Cloud cl, int n, TileSo
     ts.order[pos] = tile[k];
     if (ts.perm) ts.perm[pos] = kl;
     double2* r = reinterpret_cast<double2*>(ts.rec) + 3 * (long long)pos;
+#if P3D_SCATTER_SZREC
+    if (ts.perm) {  // the record holds the sizes of both dies: the scatter reads the
+      (void)q;      // centre through perm and picks the die's pair itself
+      if (i < cl.n_inst) {
+        r[0] = make_double2(cl.wt[i], cl.ht[i]);
+        r[1] = make_double2(cl.wb[i], cl.hb[i]);
+      } else {
+        const int f = i - cl.n_inst;
+        r[0] = r[1] = make_double2(cl.fw[f], cl.fh[f]);
+      }
+      continue;
+    }
+#endif
     r[0] = make_double2(q.x, q.y);
     r[1] = make_double2(q.z, q.w);
     r[2] = make_double2(q.h, q.weight);
@@ -344,6 +360,15 @@ __device__ __forceinline__ void scatter_terms(const Charge& q, const p3d_grid& g
 // P3D_SCATTER_DIRECT) the object itself through the last sort's permutation
 __device__ __forceinline__ Charge chunk_charge(const TileSort& ts, const CloudGP& cl, bool direct,
                                                int k, double dep) {
+#if P3D_SCATTER_SZREC
+  if (ts.perm) {  // every iteration: perm + the sorted sizes, then the centre
+    const int kl = ts.perm[k];
+    const double2* r = reinterpret_cast<const double2*>(ts.rec) + 3 * (long long)k;
+    const double2 s0 = r[0], s1 = r[1];
+    const int i = kl < ts.ni ? ts.i0 + kl : ts.f0 + (kl - ts.ni);
+    return cl.get_sized(i, s0, s1);
+  }
+#endif
 #if P3D_SCATTER_DIRECT
   if (direct) {
     const int kl = ts.perm[k];

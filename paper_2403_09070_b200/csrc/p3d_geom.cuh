@@ -147,6 +147,26 @@ struct CloudGP {  // Gp3dProblem.cloud(pos) computed on the fly (gp.py:267-278)
   }
   // get(i) for an object known not to be a macro (the scatter's sorted cells
   // and fillers): the same values, loading only the die's width / height pair
+  // get_nonmacro with the sizes given: (wt, ht), (wb, hb) of an instance,
+  // (fw, fh) twice for a filler
+  __device__ __forceinline__ Charge get_sized(int i, double2 s_top, double2 s_bot) const {
+    Charge q;
+    if (pos4 && i < n_inst) {
+      const double4 p = pos4[i];
+      q.x = p.x; q.y = p.y; q.z = p.z;
+    } else {
+      q.x = pos[i];
+      q.y = pos[n_obj + i];
+      q.z = pos[2 * n_obj + i];
+    }
+    const double zc = clipd(q.z, dz / 4, 3 * dz / 4);  // dynamic_wh's cell branch
+    const bool top = (i >= n_inst) || (zc - dz / 2) > 0.0;
+    q.w = top ? s_top.x : s_bot.x;
+    q.h = top ? s_top.y : s_bot.y;
+    q.weight = 1.0;
+    q.dep = dz / 2;
+    return q;
+  }
   __device__ __forceinline__ Charge get_nonmacro(int i) const {
     Charge q;
     if (pos4 && i < n_inst) {  // one 32-byte load instead of three scattered ones
