@@ -534,7 +534,7 @@ def main():
         prob = runner.prob
         step = runner.iterate
         runner.init_loop(pos0)
-        if runner.comm.nccl:  # the iteration, collectives included, as one CUDA graph
+        if runner.comm.nccl or not runner.comm.on:  # the iteration (+ collectives) as one graph
             try:
                 sgraph = runner.capture(1)
                 step = lambda n=1: [sgraph.replay() for _ in range(n)]  # noqa: E731

@@ -72,13 +72,17 @@ class ShardComm:
         self.rank = dist.get_rank() if self.on else 0
         self.world = dist.get_world_size() if self.on else 1
         self.nccl = self.on and dist.get_backend() == "nccl"
+        # a second NCCL communicator for the density branch's rho all-reduce:
+        # collectives on one communicator run in issue order, so with a single
+        # one the WL branch's norm all-reduce would wait for the scatter
+        self.side_group = dist.new_group(list(range(self.world))) if self.nccl else None
 
-    def all_reduce(self, t, op=None):
+    def all_reduce(self, t, op=None, side=False):
         if not self.on:
             return
         op = dist.ReduceOp.SUM if op is None else op
         if self.nccl:
-            dist.all_reduce(t, op=op)
+            dist.all_reduce(t, op=op, group=self.side_group if side else None)
         else:
             h = t.cpu()
             dist.all_reduce(h, op=op)
@@ -227,7 +231,7 @@ class ShardedGp3d:
         # nccl: the density branch (K2, the rho all-reduce, K3) runs on a side
         # stream next to K1 (they are independent until K4), as in the fused
         # loop; every rank issues the collectives in the same program order
-        overlap = c.nccl and marks is None
+        overlap = (c.nccl or not c.on) and marks is None
         if overlap and not hasattr(self, "_side"):
             self._side = torch.cuda.Stream()
         for _ in range(n):
@@ -237,7 +241,7 @@ class ShardedGp3d:
                 self._side.wait_stream(main)
                 with torch.cuda.stream(self._side):
                     self._stage("SCATTER")
-                    c.all_reduce(p.t_rho_fx)
+                    c.all_reduce(p.t_rho_fx, side=True)
                     self._stage("SPECTRAL")
             self._stage("NET")
             self._stage("GATHER")
