@@ -668,6 +668,9 @@ __global__ void __launch_bounds__(256, P3D_K5_MINB) advance_kernel(p3d_gp gp) {
         return;
       }
       st->dv2_next = tot;
+      // sharded: this rank's share; it rides along the next iteration's
+      // density-totals all-reduce (shard_control_kernel reads the sum)
+      if (gp.shard_size > 0) gp.shard_tot[14] = tot;
       st->a = st->a_new;
       // mu_from_overflow (gp.py:156-168), lambda update (gp.py:442-444)
       const double mu = mu_of(gp, st->prev_ovfl, st->ovfl);
@@ -1066,12 +1069,14 @@ __global__ void norms_final_kernel(p3d_gp gp) {
 }
 
 // loop control with the all-reduced totals (net: shard_tot[0,6), density:
-// shard_tot[8,14)); identical on every rank
+// shard_tot[8,14), the last step's |v - v_prev|^2: shard_tot[14]); identical
+// on every rank
 __global__ void shard_control_kernel(p3d_gp gp) {
   if (gp.st->done) return;
   double* f = fin(gp);
   const double* t = gp.shard_tot;
   for (int q = 0; q < 6; ++q) f[kFinNet + q] = t[q];
+  gp.st->dv2_next = t[14];  // |v - v_prev|^2 summed over the ranks' objects
   control_after_eval(gp, t[8], t[9], t[10], t[11], t[12], t[13]);
 }
 

@@ -8,12 +8,15 @@ ranks runs on each, each keeping its own pins' gradients; its value is counted
 once, by its first pin's owner), so the per-instance WL sums are complete on
 their owner and only three exchanges remain per iteration:
 
-    [all-reduce]   the three L1 norms (Eq. 17)
-    [all-reduce]   rho, int64 fixed point (exact: the single-GPU map bit for bit)
-    [all-reduce]   the density totals, |v_new - v|^2, (iteration 0) max |g|
     [all-to-all]   positions of the halo: each rank receives the pos4 rows of the
                    remote instances of its nets (static lists) -- instead of every
-                   position on every rank
+                   position on every rank; at the start of the iteration, next
+                   to the density branch (which needs only the rank's own rows)
+    [all-reduce]   the three L1 norms (Eq. 17)
+    [all-reduce]   rho, int64 fixed point (exact: the single-GPU map bit for bit),
+                   on its own communicator (the density branch's side stream)
+    [all-reduce]   the density totals with the last step's |v_new - v|^2,
+                   (iteration 0) max |g|
 
 The round-robin mode (halo=False) below deals the K1 warp tasks round-robin
 and exchanges full per-instance arrays:
@@ -32,8 +35,9 @@ the K1 warp tasks w with w % world == rank.  Per iteration (gp.py:386-444):
     [all-reduce]      totals (energy, L1 norms, |dg|^2, net totals)
     CONTROL           objective, lambda init, log row, best/stop/divergence, BB step
     STEP0 [max] STEP0_CONTROL   iteration 0 only: initial step from max |g|
-    ADVANCE           Nesterov step on own objects
-    [all-reduce]      |v_new - v|^2;   [all-gather] own pos4 slabs for K1
+    ADVANCE           Nesterov step on own objects (|v_new - v|^2 rides along the
+                      next all-reduce of totals)
+    [all-gather]      own pos4 slabs for K1
 
 All control state is replicated and updated identically on every rank, so the
 ranks agree on every branch (stop, divergence, underflow) without host syncs.
@@ -162,8 +166,6 @@ class ShardedGp3d:
         self.prob = Gp3dProblem(design, grid, fillers, cfg, rot, max_iters=max_iters,
                                 precision=precision, shard=shard)
         p = self.prob
-        off = _lib.LoopState.dv2_next.offset
-        self._dv2 = p.t_st[off: off + 8].view(torch.float64)
         self._tot16 = p.t_shard_tot[:16]
         self._tot_max = p.t_shard_tot[16:17]
         self._norms = p.t_shard_tot[20:23]
@@ -243,6 +245,9 @@ class ShardedGp3d:
                     self._stage("SCATTER")
                     c.all_reduce(p.t_rho_fx, side=True)
                     self._stage("SPECTRAL")
+            if self.halo:  # the previous step's halo rows, overlapping the density branch
+                self._halo_exchange()
+                mark("comm")
             self._stage("NET")
             self._stage("GATHER")
             mark("K1")
@@ -272,12 +277,10 @@ class ShardedGp3d:
             mark("comm")
             self._stage("ADVANCE")
             mark("K5")
-            c.all_reduce(self._dv2)
-            if self.halo:
-                self._halo_exchange()
-            else:
+            # |v - v_prev|^2 rides along the next iteration's density totals
+            if not self.halo:
                 c.all_gather_chunks(p.t_pos4, 4 * p.inst_slab)
-            mark("comm")
+                mark("comm")
 
     @staticmethod
     def attribute(marks):
