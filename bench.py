@@ -533,17 +533,18 @@ def main():
         runner = ShardedGp3d(design, grid, st.fillers, cfg, st.rot, precision=args.precision)
         prob = runner.prob
         step = runner.iterate
+        init_loop = runner.init_loop  # caller's instance order -> the shard's numbering
         runner.init_loop(pos0)
         if runner.comm.nccl or not runner.comm.on:  # the iteration (+ collectives) as one graph
-            try:
-                sgraph = runner.capture(1)
-                step = lambda n=1: [sgraph.replay() for _ in range(n)]  # noqa: E731
+            try:  # iteration 0's graph with the initial step, then the steady-state one
+                step = runner.stepper()
             except Exception as exc:  # pragma: no cover - eager fallback, reported
                 print(f"# sharded graph capture failed ({exc!r}); running eagerly",
                       file=sys.stderr)
                 runner.init_loop(pos0)
     else:
         prob = G.Gp3dProblem(design, grid, st.fillers, cfg, st.rot, precision=args.precision)
+        init_loop = prob.init_loop
         prob.init_loop(pos0)
         graph = prob.capture(1)
         step = lambda n=1: [graph.replay() for _ in range(n)]  # noqa: E731
@@ -603,7 +604,11 @@ def main():
                     "density_branch_K2_K3": round(acc[3], 1), "of_which_K2": round(acc[2], 1),
                     "K4_end": round(acc[4], 1), "K5_end": round(acc[6], 1)}
     else:
-        kpi = _lib.load().p3d_gp_kernels_per_iteration(_lib.byref(prob.gp)) + 3
+        # the staged protocol adds the norm pass, its finaliser and the control
+        # kernel; the steady-state graph drops the initial-step pair (+2), the
+        # eager path keeps it (+4)
+        kpi = _lib.load().p3d_gp_kernels_per_iteration(_lib.byref(prob.gp)) + (
+            2 if hasattr(step, "reset") else 4)
         marks = []
         runner.iterate(K, marks=marks)  # eager, with events between stages
         att = runner.attribute(marks)
@@ -621,7 +626,9 @@ def main():
 
     def e2e_pass(n):
         dev_pos.copy_(host_pos, non_blocking=True)
-        prob.init_loop(dev_pos)
+        init_loop(dev_pos)
+        if hasattr(step, "reset"):
+            step.reset()
         for k in range(n):
             step(1)
             host_row.copy_(prob.t_log[4 * k: 4 * k + 4], non_blocking=True)

@@ -219,9 +219,11 @@ class ShardedGp3d:
         pos = np.asarray(pos)
         return np.concatenate([pos[:I][self.perm], pos[I:]])
 
-    def iterate(self, n=1, marks=None):
+    def iterate(self, n=1, marks=None, steady=False):
         """n sharded iterations; `marks` (a list) collects (label, cuda Event)
-        after every stage / collective for attribution (eager runs only)."""
+        after every stage / collective for attribution (eager runs only).
+        steady=True leaves out the iteration-0 initial step (STEP0, its max
+        all-reduce, STEP0_CONTROL): for every iteration after the first."""
         p, c = self.prob, self.comm
 
         def mark(label):
@@ -271,9 +273,10 @@ class ShardedGp3d:
             mark("K4")
             c.all_reduce(self._tot16)
             self._stage("CONTROL")
-            self._stage("STEP0")
-            c.all_reduce(self._tot_max, dist.ReduceOp.MAX if c.on else None)
-            self._stage("STEP0_CONTROL")
+            if not steady:
+                self._stage("STEP0")
+                c.all_reduce(self._tot_max, dist.ReduceOp.MAX if c.on else None)
+                self._stage("STEP0_CONTROL")
             mark("comm")
             self._stage("ADVANCE")
             mark("K5")
@@ -293,7 +296,7 @@ class ShardedGp3d:
             out[lab] = out.get(lab, 0.0) + a.elapsed_time(b)
         return out
 
-    def capture(self, iters_per_graph=1):
+    def capture(self, iters_per_graph=1, steady=False):
         """CUDA graph of `iters_per_graph` sharded iterations, collectives
         included (nccl only: gloo stages through host memory).  Replaying it
         removes the per-stage host launch cost."""
@@ -303,18 +306,32 @@ class ShardedGp3d:
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
-            self.iterate(iters_per_graph)
+            self.iterate(iters_per_graph, steady=steady)
         torch.cuda.current_stream().wait_stream(s)
         return g
+
+    def stepper(self):
+        """step(n): n iterations replaying two captured graphs -- iteration 0
+        with its initial-step stages, every later one without them.
+        reset() rewinds to iteration 0 (after init_loop)."""
+        g0, gs = self.capture(1), self.capture(1, steady=True)
+        first = [True]
+
+        def step(n=1):
+            for _ in range(n):
+                (g0 if first[0] else gs).replay()
+                first[0] = False
+
+        step.reset = lambda: first.__setitem__(0, True)
+        return step
 
     def run(self, pos0, poll_every=8, use_graph=False):
         """Initialise and run to completion (max_iters or an exit)."""
         self.init_loop(pos0)
+        done = 0
         step = self.iterate
         if use_graph:
-            graph = self.capture(1)
-            step = lambda n: [graph.replay() for _ in range(n)]  # noqa: E731
-        done = 0
+            step = self.stepper()
         while done < self.prob.max_iters:
             k = min(poll_every, self.prob.max_iters - done)
             step(k)
