@@ -741,6 +741,16 @@ def run_gp3d(design, state: PlacementState, cfg: GpConfig, grid=None, iteration_
     return state, info
 
 
+def __getattr__(name):
+    """gp.Gp2dProblem / gp.run_gp2d_multi (gp.py:463-690) live in gp2d.py
+    (imported lazily: gp2d builds on this module)."""
+    if name in ("Gp2dProblem", "run_gp2d_multi"):
+        from . import gp2d
+
+        return getattr(gp2d, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
+
+
 __all__ = [
     "GpConfig", "GpInfo", "GradientBundle", "StepUnderflow", "choose_grid", "alpha_value",
     "select_flow", "init_state", "make_fillers", "precondition", "lambda_init",

@@ -332,10 +332,36 @@ def dynamic_pin_coords(arrays: NetlistArrays, x, y, z, rot, dz):
     return px, py, pz, top.to(torch.bool)
 
 
+@_dev.numpy_io("x")
+def gp_wirelength_objective(arrays, x, y, z, rot, dz, gamma, alpha):
+    """Instance-level GP wirelength objective (wirelength.py:345-358): the
+    smoothed bistratal total plus alpha times the smoothed z-span total, and
+    dW/dx, dW/dy summed per instance.  Pins, both objectives and the
+    pin -> instance sums (p3d_gather_pins: per owner in pin order, the
+    np.bincount order) all run on the device."""
+    _lib.require_cuda()
+    topo = NetTopology.from_arrays(arrays)
+    dt = topo.device()
+    px, py, pz, on_top = dynamic_pin_coords(arrays, _dev.f64(x), _dev.f64(y), _dev.f64(z), rot, dz)
+    w_bi, gx_pin, gy_pin = planar_objective(dt, px, py, on_top, gamma)
+    w_cut, _ = z_cut_penalty(dt, pz, gamma)
+    n_obj = max(int(topo.n_obj), 1)
+    pin4 = torch.zeros((max(dt.n_pin, 1), 4), dtype=torch.float64, device="cuda")
+    obj4 = torch.zeros(4 * n_obj, dtype=torch.float64, device="cuda")
+    if dt.n_pin:
+        slot = dt.pin_slot.long()
+        pin4[slot, 0] = gx_pin
+        pin4[slot, 1] = gy_pin
+        _lib.call("p3d_gather_pins", _lib.byref(dt.struct), _lib.ptr(pin4), _lib.ptr(obj4),
+                  _lib.stream_ptr())
+    n = int(topo.n_obj)
+    return w_bi + alpha * w_cut, obj4[:n].clone(), obj4[n_obj: n_obj + n].clone()
+
+
 __all__ = [
     "optimal_hbt_centers",
     "NetTopology", "DeviceTopology", "partial_hpwl", "wa_smooth", "NetBoxes", "bistratal_axis",
     "optimal_region", "bistratal_spans", "planar_objective", "z_cut_penalty",
     "fd_z_gradient_naive", "fd_z_gradient_incremental", "normalize_z_gradient",
-    "dynamic_pin_coords", "rotated_pin_offsets", "partition_from_z",
+    "dynamic_pin_coords", "rotated_pin_offsets", "partition_from_z", "gp_wirelength_objective",
 ]

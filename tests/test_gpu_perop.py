@@ -123,3 +123,42 @@ def test_nesterov_optimizer_matches_oracle():
         prev_r, prev_t = gr, gt
         assert opt.step == pytest.approx(ref.step, rel=1e-12), k
         assert np.abs(opt.u.cpu().numpy() - ref.u).max() <= 1e-12 * np.abs(ref.u).max(), k
+
+
+@pytest.mark.parametrize("rotated", [False, True])
+def test_gp_wirelength_objective_vs_oracle(rotated):
+    """wirelength.gp_wirelength_objective (wirelength.py:345-358) on the
+    device against the oracle's pieces (pins_at, planar_wl, zcut and
+    np.bincount, each pinned to the reference): value to 1e-12, the
+    per-instance sums to 1e-12 of their scale."""
+    from paper_2403_09070_b200 import wirelength as wl
+    from paper_2403_09070_b200.synth import CONFIGS, synth_arrays
+
+    d = synth_arrays(CONFIGS[1]["spec"])
+    a = d.arrays()
+    rs = np.random.default_rng(9)
+    dz, gamma, alpha = 47.52, 17.3, 0.37
+    x = rs.uniform(0, d.die.width, a.n_inst)
+    y = rs.uniform(0, d.die.height, a.n_inst)
+    z = rs.uniform(dz / 4, 3 * dz / 4, a.n_inst)
+    rot = rs.integers(0, 4, a.n_inst) if rotated else np.zeros(a.n_inst, dtype=np.int64)
+    val, gx, gy = wl.gp_wirelength_objective(a, x, y, z, rot, dz, gamma, alpha)
+    assert isinstance(gx, np.ndarray) and gx.shape == (a.n_inst,)
+    px, py, pz, top = P.pins_at(a, x, y, z, rot, dz)
+    w_bi, gxp, gyp = P.planar_wl(a.pin_net, a.n_net, px, py, top, gamma)
+    w_cut, _ = P.zcut(a.pin_net, a.n_net, pz, gamma)
+    want_gx = np.bincount(a.pin_inst, weights=gxp, minlength=a.n_inst)
+    want_gy = np.bincount(a.pin_inst, weights=gyp, minlength=a.n_inst)
+    assert val == pytest.approx(w_bi + alpha * w_cut, rel=1e-12)
+    assert np.abs(gx - want_gx).max() <= 1e-12 * np.abs(want_gx).max()
+    assert np.abs(gy - want_gy).max() <= 1e-12 * np.abs(want_gy).max()
+
+
+def test_gp2d_names_in_gp_module():
+    """The reference keeps Gp2dProblem and run_gp2d_multi in gp.py
+    (gp.py:463-690); so does the drop-in's gp module (gp2d.py behind it)."""
+    from paper_2403_09070_b200 import gp, gp2d
+
+    assert gp.run_gp2d_multi is gp2d.run_gp2d_multi
+    assert gp.Gp2dProblem is gp2d.Gp2dProblem
+    from paper_2403_09070_b200.gp import run_gp2d_multi  # noqa: F401
