@@ -134,18 +134,6 @@ __device__ const double kExp2Tab[64] = {
 #ifndef P3D_K1_EARLY
 #define P3D_K1_EARLY 1
 #endif
-#ifndef P3D_K1_SLOT_EARLY
-#define P3D_K1_SLOT_EARLY 1  // 1: before the y axis, 2: before the x axis
-#endif
-#ifndef P3D_K1_PAIR2
-#define P3D_K1_PAIR2 0
-#endif
-#ifndef P3D_K1_PREFETCH
-#define P3D_K1_PREFETCH 0  // 1: next task's pin streams prefetched to L1, 2: to L2
-#endif
-#ifndef P3D_EXP_ESTRIN
-#define P3D_EXP_ESTRIN 0
-#endif
 #if P3D_EXP_POLY
 // Table-free variant: n = rint(x / ln 2), Cody-Waite r (|r| <= ln2/2), degree-13
 // Taylor polynomial by Horner (<= 1.2 ulp over [-708, 0]); no memory access.
@@ -186,23 +174,9 @@ __device__ __forceinline__ double exp_neg(double x) {
 #endif
   const double n = rint(x * c[0]);
   const double r = fma(-n, c[2], fma(-n, c[1], x));
-#if P3D_EXP_ESTRIN
-  // Estrin's scheme: the same polynomial at dependency depth 4 instead of
-  // 13 (three more operations; K1's exp stalls were fixed-latency waits on
-  // the Horner chain).  c[16 - k] = 1/k!.
-  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
-  const double q0 = fma(c[15], r, c[16]), q1 = fma(c[13], r, c[14]);
-  const double q2 = fma(c[11], r, c[12]), q3 = fma(c[9], r, c[10]);
-  const double q4 = fma(c[7], r, c[8]), q5 = fma(c[5], r, c[6]);
-  const double q6 = fma(c[3], r, c[4]);
-  const double s0 = fma(q1, r2, q0), s1 = fma(q3, r2, q2), s2 = fma(q5, r2, q4);
-  const double t0 = fma(s1, r4, s0), t1 = fma(q6, r4, s2);
-  const double p = fma(t1, r8, t0);
-#else
   double p = c[3];
 #pragma unroll
   for (int k = 4; k < 17; ++k) p = fma(p, r, c[k]);
-#endif
   const double sc = __longlong_as_double((long long)((int)n + 1023) << 52);
   return x < -708.0 ? 0.0 : p * sc;
 }
@@ -679,34 +653,19 @@ P3D_K1_LOOP_UNROLL
   double v, ex;
   bool cross;
   int slot[KM];
-#if P3D_K1_SLOT_EARLY == 2
-#pragma unroll
-  for (int k = 0; k < KM; ++k) {
-    if (k >= DD) break;
-    slot[k] = ld_stream(a.slot + pin0 + k * nb);
-  }
-#endif
   staged_axis<D, F32>(sm.px, sm, lane, topm, ig, v, ex, cross, nd);
   acc[0] += pm * v;
   acc[3] += pm * ex;
   acc[5] += pm * (cross ? 1.0 : 0.0);
-#if P3D_K1_SLOT_EARLY == 1  // the record slots load while the y axis is evaluated
+  // the record slots load while the y axis is evaluated
 #pragma unroll
   for (int k = 0; k < KM; ++k) {
     if (k >= DD) break;
     slot[k] = ld_stream(a.slot + pin0 + k * nb);
   }
-#endif
   staged_axis<D, F32>(sm.py, sm, lane, topm, ig, v, ex, cross, nd);
   acc[1] += pm * v;
   acc[4] += pm * ex;
-#if !P3D_K1_SLOT_EARLY
-#pragma unroll
-  for (int k = 0; k < KM; ++k) {
-    if (k >= DD) break;
-    slot[k] = ld_stream(a.slot + pin0 + k * nb);
-  }
-#endif
 #pragma unroll
   for (int k = 0; k < KM; ++k) {
     if (k >= DD) break;
@@ -830,8 +789,7 @@ __device__ __forceinline__ void pair_axis(double v0, double v1, typename WaSel<F
 // Degree-2 nets (about half of all nets): never split (both partial spans are
 // 0 or the full span) and the FD flip delta is exactly 0 for both pins
 // (wirelength.py:227-248), so a lane evaluates its net from registers.
-// One lane's degree-2 net, split into its loads and its evaluation so that two
-// tasks' loads can be in flight together (pair2_task).
+// One lane's degree-2 net: its loads, then its evaluation from registers.
 struct PairLd {
   int ok, s0, s1;
   double pm;
@@ -912,17 +870,6 @@ __device__ __forceinline__ void pair_task(const FusedNetArgs& a, const int4 tk, 
   pair_eval<F32>(a, pair_load(a, tk, t0, lane), acc);
 }
 
-// Two consecutive degree-2 tasks of one warp: both tasks' loads are issued
-// before either net is evaluated (twice the loads in flight); the nets are
-// accumulated in task order, so the sums are those of two pair_task calls.
-template <bool F32>
-__device__ __forceinline__ void pair2_task(const FusedNetArgs& a, const int4 tk, int t0,
-                                           const int4 tk2, int t02, int lane, double (&acc)[6]) {
-  const PairLd L1 = pair_load(a, tk, t0, lane);
-  const PairLd L2 = pair_load(a, tk2, t02, lane);
-  pair_eval<F32>(a, L1, acc);
-  pair_eval<F32>(a, L2, acc);
-}
 
 template <int D, bool F32>
 __device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk, int t0,
@@ -934,26 +881,6 @@ __device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk
     staged_eval<D, F32>(a, tk.x + tk.z + lane, tk.y, sm, lane, topm, zhi, zlo, acc, nd, pm);
 }
 
-#if P3D_K1_PREFETCH
-// Prefetch the pin streams of a lane's net in the next task (its descriptor
-// arrived during this task), so that task's first loads hit the cache.
-__device__ __forceinline__ void prefetch_task(const FusedNetArgs& a, const int4 tk, int t0, int lane) {
-  const int nb = tk.y, j = tk.z + lane;
-  if (j >= nb || tk.w > kMaxStagedDeg) return;
-  const int p0 = tk.x + j;
-  for (int k = 0; k < tk.w; ++k) {
-#if P3D_K1_PREFETCH == 1
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.pin_inst + p0 + k * nb));
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.off + p0 + k * nb));
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.slot + p0 + k * nb));
-#else
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.pin_inst + p0 + k * nb));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.off + p0 + k * nb));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.slot + p0 + k * nb));
-#endif
-  }
-}
-#endif
 
 template <bool F32>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_kernel(FusedNetArgs a) {
@@ -992,14 +919,6 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_ke
 #ifdef P3D_SKIP_DGE3
     if (tk.w >= 3) continue;
 #endif
-#if P3D_K1_PAIR2 && P3D_K1_EARLY
-    if (tk.w == 2 && tkn.w == 2 && wn < a.n_tasks) {
-      pair2_task<F32>(a, tk, t0, tkn, t0n, lane, acc);
-      wn += wstride * a.task_size;
-      if (wn < a.n_tasks) { tkn = a.tasks[wn]; t0n = a.task_t0[wn]; }
-      continue;
-    }
-#endif
     switch (tk.w) {
       case 2: pair_task<F32>(a, tk, t0, lane, acc); break;
 #if P3D_K1_TRIPLE
@@ -1016,9 +935,6 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_ke
 #endif
       default: break;  // generic nets run in generic_net_kernel
     }
-#if P3D_K1_PREFETCH && P3D_K1_EARLY
-    if (wn < a.n_tasks) prefetch_task(a, tkn, t0n, lane);
-#endif
   }
   block_sum<6>(acc, red);
   if (threadIdx.x == 0)
@@ -1061,9 +977,6 @@ __global__ void __launch_bounds__(256) generic_net_kernel(FusedNetArgs a) {
 #define P3D_GATHER_BATCH 4
 #endif
 constexpr int kGatherBatch = P3D_GATHER_BATCH;
-#ifndef P3D_GATHER_EARLY
-#define P3D_GATHER_EARLY 0
-#endif
 
 // owner gather: per object, ordered fp64 sums over its contiguous slot records
 // (pin order within the owner, like bincount)
@@ -1142,29 +1055,11 @@ __global__ void __launch_bounds__(32 * kGatherWarps) gather_warp_kernel(FusedGat
   double2* st = stage[wib];
   double acc[3] = {0, 0, 0};
   const int wstride = gridDim.x * kGatherWarps * 32;
-#if P3D_GATHER_EARLY  // the next group's slot range loads while this group is summed
-  int o0 = (blockIdx.x * kGatherWarps + wib) * 32;
-  int bn = 0, en = 0;
-  if (o0 + lane < a.n_obj) {
-    bn = a.obj_slot_ptr[a.obj0 + o0 + lane];
-    en = a.obj_slot_ptr[a.obj0 + o0 + lane + 1];
-  }
-  for (; o0 < a.n_obj; o0 += wstride) {
-    const int il = o0 + lane, i = a.obj0 + il;
-    const int last = min(a.n_obj, o0 + 32) - 1;
-    const int b = bn, e = en;
-    bn = en = 0;
-    if (o0 + wstride + lane < a.n_obj) {
-      bn = a.obj_slot_ptr[i + wstride];
-      en = a.obj_slot_ptr[i + wstride + 1];
-    }
-#else
   for (int o0 = (blockIdx.x * kGatherWarps + wib) * 32; o0 < a.n_obj; o0 += wstride) {
     const int il = o0 + lane, i = a.obj0 + il;
     const int last = min(a.n_obj, o0 + 32) - 1;
     const int b = il <= last ? a.obj_slot_ptr[i] : 0;
     const int e = il <= last ? a.obj_slot_ptr[i + 1] : 0;
-#endif
     const int rb = __shfl_sync(0xffffffffu, b, 0);
     const int re = __shfl_sync(0xffffffffu, e, last - o0);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
