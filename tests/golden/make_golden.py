@@ -20,6 +20,9 @@ Writes, next to this script:
   exits.json             (--exits) the three early exits of run_gp3d (gp.py:390-393
                          non-finite, :414-422 divergence, :438-441 step underflow)
                          and a second pass with rotated macros (flow.py:121-122)
+  edges.json             (--edges) run_gp3d at its boundaries: converged before the first
+                         step, 1 and 2 iterations, every instance on one die,
+                         single-pin nets only
   flow_small.json        (--flow) place3d.flow.run_flow end to end (3D and 2D paths)
 The reference is never imported at test time or on the GPU box.
 """
@@ -181,6 +184,80 @@ def exits():
                  info.hbt_count],
         "state": _state_digest(st)}
     with open(os.path.join(HERE, "exits.json"), "w") as fh:
+        json.dump(out, fh, indent=0)
+
+
+# run_gp3d edge cases (the loop's boundaries): converged before the first
+# step, one and two iterations, all instances starting on one die, and a
+# netlist the generator never makes (every net a single pin)
+EDGE_CASES = {
+    "converged_at_0": dict(cfg=dict(stop_overflow=0.99)),
+    "max_iters_1": dict(cfg=dict(max_iters=1)),
+    "max_iters_2": dict(cfg=dict(max_iters=2)),
+    "all_bottom": dict(z="bottom"),
+    "single_pin_nets": dict(nets="first_pin"),
+}  # (a design without nets: the reference's NetBoxes raises IndexError)
+
+
+def _edge_design(kind):
+    from place3d.model import Design, Net
+
+    d = design_of("small")
+    if kind is None:
+        return d
+    nets = [Net(n.name, [n.pins[0]]) for n in d.nets]  # kind "first_pin"
+    return Design([type(i)(i.name, i.kind, i.is_macro) for i in d.insts], nets, d.tech_top,
+                  d.tech_bottom, d.die, d.hbt)
+
+
+def edges():
+    out = {"spec": SPECS["small"], "grid": 64, "nz": 2, "max_iters": 40, "cases": {}}
+    for name, case in EDGE_CASES.items():
+        d = _edge_design(case.get("nets"))
+        kw = dict(max_iters=40, stop_overflow=0.0)
+        kw.update(case.get("cfg", {}))
+        cfg = rgp.GpConfig(seed=1, nz=2, grid_nx=64, grid_ny=64, **kw)
+        rng = np.random.default_rng(1)
+        grid = rgp.choose_grid(d, cfg)
+        st = rgp.init_state(d, grid, cfg, rng)
+        if case.get("z") == "bottom":
+            st.z[:] = grid.dz / 4
+        rows = []
+        st, info = rgp.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+        out["cases"][name] = {
+            "case": case, "cfg": kw, "rows": _rows(rows),
+            "info": [info.iterations, info.final_overflow, bool(info.diverged),
+                     info.wirelength, info.hbt_count],
+            "state": _state_digest(st)}
+        print(name, info.iterations, info.final_overflow, info.diverged, flush=True)
+        if case.get("nets") == "first_pin":
+            # without wirelength the density-only descent amplifies small
+            # differences: the reference's own spread under 1e-12 relative
+            # noise on the density force (the int64 density map quantises
+            # every term at 2^-40 ~ 1e-12 of a unit density), per row, is
+            # this case's band
+            spread = np.zeros((len(rows), 2))
+            for seed in (11, 12, 13, 14):
+                rs = np.random.default_rng(seed)
+                orig = rdn.density_force
+
+                def noisy(*a, **k):
+                    g = orig(*a, **k)
+                    return g * (1 + 1e-12 * rs.standard_normal(g.shape))
+
+                rdn.density_force = noisy
+                try:
+                    rng2 = np.random.default_rng(1)
+                    st2 = rgp.init_state(d, grid, cfg, rng2)
+                    rows2 = []
+                    rgp.run_gp3d(d, st2, cfg, grid=grid, iteration_log=rows2, rng=rng2)
+                finally:
+                    rdn.density_force = orig
+                a, b = np.array(_rows(rows), float), np.array(_rows(rows2), float)
+                spread = np.maximum(spread, np.abs(a[:, [1, 3]] - b[:, [1, 3]]))
+            out["cases"][name]["band_wl_ovfl"] = spread.tolist()
+            print(name, "band", spread[-1], flush=True)
+    with open(os.path.join(HERE, "edges.json"), "w") as fh:
         json.dump(out, fh, indent=0)
 
 
@@ -541,7 +618,8 @@ if __name__ == "__main__":
     if "--band" in sys.argv:
         band("cfg2", 256, "cfg2_band.json")
         sys.exit(0)
-    for flag, fn in (("--cfg3", cfg3_rows), ("--cfg4", cfg4_rows), ("--exits", exits), ("--flow", flow_small),
+    for flag, fn in (("--cfg3", cfg3_rows), ("--cfg4", cfg4_rows), ("--exits", exits),
+                     ("--edges", edges), ("--flow", flow_small),
                      ("--rebalance", rebalance), ("--check", check), ("--parse", parse_cases)):
         if flag in sys.argv:
             fn()
