@@ -719,3 +719,43 @@ def test_run_gp2d_hbt_converges_to_optimal_region():
     lo, hi = sorted([state.x[0], state.x[1]])
     assert lo - 2 <= hx <= hi + 2
     assert abs(hy - 32.0) <= 4.0
+
+
+# ==== edge cases beyond the reference's own tests ========================================
+
+
+def test_density_boxes_clipped_at_the_region_boundary():
+    """Charges straddling or outside the region's faces (the reference clips
+    each box to [0, dx] x [0, dy] x [0, dz], density.py:155-169): the device
+    maps (direct and per-macro tile paths) equal the brute-force overlap
+    integration, which clips the same way."""
+    rng = np.random.default_rng(31)
+    grid = dn.DensityGrid(10, 8, 5, 4, 2)
+    boxes = []
+    for _ in range(40):
+        w, h = rng.uniform(0.5, 6), rng.uniform(0.5, 6)
+        dep = rng.uniform(0.5, grid.dz)
+        boxes.append((rng.uniform(-2, 12), rng.uniform(-2, 10), rng.uniform(-1, grid.dz + 1),
+                      w, h, dep))
+    weights = rng.uniform(0.5, 2, 40)
+    want = brute_density(grid, make_cloud(boxes, weights=weights))
+    got_cells = dn.direct_density(grid, make_cloud(boxes, weights=weights))
+    got_macros = dn.macro_prefix_density(grid, make_cloud(boxes, weights=weights, macro=[True] * 40))
+    assert np.abs(got_cells - want).max() < 1e-9
+    assert np.abs(got_macros - want).max() < 1e-9
+
+
+def test_wa_extreme_spread_is_finite():
+    """A net spanning ~1e6 gammas: the shifted exponentials underflow to 0
+    for the far pins (wirelength.py:64-66 shifts by the max / min), the value
+    tends to the span and the gradient to +-1 at the extremes; nothing is
+    non-finite."""
+    v = np.array([0.0, 1.0, 5e5, 1e6])
+    val, grad = wl.wa_smooth(v, 1.0)
+    assert np.isfinite(val) and np.all(np.isfinite(grad))
+    # wirelength.py:58-73 in numpy
+    ep, em = np.exp(v - v.max()), np.exp(v.min() - v)
+    vp, vm = (v * ep).sum() / ep.sum(), (v * em).sum() / em.sum()
+    want = ep / ep.sum() * (1 + (v - vp)) - em / em.sum() * (1 - (v - vm))
+    assert val == pytest.approx(vp - vm, rel=1e-12)
+    assert np.allclose(grad, want, rtol=1e-9, atol=1e-12)
