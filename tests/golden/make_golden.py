@@ -23,6 +23,8 @@ Writes, next to this script:
   edges.json             (--edges) run_gp3d at its boundaries: converged before the first
                          step, 1 and 2 iterations, every instance on one die,
                          single-pin nets only
+  cfg1_variants.json     (--variants) 200-iteration rows of three more config-1-sized
+                         designs (other seeds, r_ma 0.45, 16 macros / denser nets)
   flow_small.json        (--flow) place3d.flow.run_flow end to end (3D and 2D paths)
 The reference is never imported at test time or on the GPU box.
 """
@@ -582,6 +584,28 @@ def loop_rows(name, nx, out):
                    "seconds_1core": dt, "rows": [list(map(float, r)) for r in rows]}, fh)
 
 
+# config-1-sized designs the headline spec does not cover: other generator
+# seeds, a higher macro-area ratio, more macros and denser nets
+VARIANTS = [
+    dict(n_insts=10_008, n_macros=8, r_ma=0.30, seed=2, nets_per_inst=1.2),
+    dict(n_insts=10_008, n_macros=8, r_ma=0.45, seed=3, nets_per_inst=1.2),
+    dict(n_insts=10_008, n_macros=16, r_ma=0.30, seed=4, nets_per_inst=1.4),
+]
+
+
+def variants():
+    out = {"grid": 128, "nz": 2, "max_iters": 200, "cases": []}
+    for spec in VARIANTS:
+        d = parse_design(gen_synthetic(SynthSpec(**spec)))
+        cfg, rng, grid, st = setup(d, 128, 2, 200)
+        rows = []
+        rgp.run_gp3d(d, st, cfg, grid=grid, iteration_log=rows, rng=rng)
+        out["cases"].append({"spec": spec, "rows": [list(map(float, r)) for r in rows]})
+        print(spec, rows[-1], flush=True)
+    with open(os.path.join(HERE, "cfg1_variants.json"), "w") as fh:
+        json.dump(out, fh)
+
+
 def _perturbed_run(args):
     """Reference run_gp3d with the density force perturbed by 1e-15 relative
     noise (seeded): samples the trajectory's own sensitivity to last-bit
@@ -619,7 +643,7 @@ if __name__ == "__main__":
         band("cfg2", 256, "cfg2_band.json")
         sys.exit(0)
     for flag, fn in (("--cfg3", cfg3_rows), ("--cfg4", cfg4_rows), ("--exits", exits),
-                     ("--edges", edges), ("--flow", flow_small),
+                     ("--edges", edges), ("--variants", variants), ("--flow", flow_small),
                      ("--rebalance", rebalance), ("--check", check), ("--parse", parse_cases)):
         if flag in sys.argv:
             fn()

@@ -65,6 +65,17 @@ def test_cfg1_200_iterations_fp64():
     assert info.wirelength == pytest.approx(417269.76175678306, rel=5e-3)
 
 
+@pytest.mark.parametrize("case", [0, 1, 2])
+def test_cfg1_sized_variants_vs_reference(case):
+    """Three more config-1-sized designs (generator seeds 2-4, r_ma 0.45, 16
+    macros with denser nets; tests/golden/cfg1_variants.json, made by the
+    reference): all 200 rows within 1e-9, crossings equal."""
+    gold = json.load(open(os.path.join(GOLD, "cfg1_variants.json")))
+    c = gold["cases"][case]
+    rows, info, st, grid = _run(c["spec"], gold["grid"], gold["max_iters"])
+    _check(rows, {"rows": c["rows"]}, tight=1e-9)
+
+
 def test_cfg1_200_iterations_fp32():
     """The default fast path (fp32 WA on anchored differences) meets the 0.5% gate."""
     gold = json.load(open(os.path.join(GOLD, "cfg1_log.json")))
