@@ -64,11 +64,25 @@ def test_gp2d_wirelength_vs_oracle(case):
 
 
 def test_run_gp2d_vs_reference(case):
+    _run_gp2d_case(*case)
+
+
+@pytest.mark.parametrize("k", [0, 1])
+def test_run_gp2d_variants_vs_reference(k):
+    """Two more designs (r_ma 0.55, the 2D flow's territory; 3,000 instances
+    with 12 macros), tests/golden/gp2d_variants.json from the reference
+    (make_gp2d.py --variants), under the same gates."""
+    from paper_2403_09070_b200.synth import SynthSpec, synth_arrays
+
+    g = json.load(open(os.path.join(GOLD, "gp2d_variants.json")))[k]
+    _run_gp2d_case(synth_arrays(SynthSpec(**g["spec"])), g)
+
+
+def _run_gp2d_case(d, g):
     from paper_2403_09070_b200 import gp2d as G2
     from paper_2403_09070_b200.gp import GpConfig
     from paper_2403_09070_b200.model import PlacementState
 
-    d, g = case
     st = PlacementState(x=np.array(g["x0"]), y=np.array(g["y0"]), z=np.array(g["z0"]),
                         rot=np.array(g["rot"]), dz=g["dz"])
     cfg = GpConfig(seed=1, max_iters=g["max_iters"], stop_overflow=g["stop_overflow"])
@@ -79,8 +93,15 @@ def test_run_gp2d_vs_reference(case):
     got = np.array(rows, float)
     assert got.shape == ref.shape and info.iterations == g["iterations"]
     assert np.array_equal(got[:, 2], ref[:, 2])
-    assert np.all(np.abs(got[:5, 1] - ref[:5, 1]) <= 1e-9 * np.abs(ref[:5, 1]))
-    assert np.all(np.abs(got[:5, 3] - ref[:5, 3]) <= 1e-9)
+    # tight rows up to the first knife edge: mu_from_overflow (gp.py:156-168)
+    # picks mu by the sign / size of the overflow drop, so a drop within 1e-12
+    # of a threshold (0, 5e-4, 2e-3) is decided by last-bit differences
+    drops = ref[:-1, 3] - ref[1:, 3]
+    edge = [i + 1 for i, dr in enumerate(drops)
+            if min(abs(dr), abs(dr - 5e-4), abs(dr - 2e-3)) < 1e-12]
+    n_tight = min(5, edge[0] + 2 if edge else 5)
+    assert np.all(np.abs(got[:n_tight, 1] - ref[:n_tight, 1]) <= 1e-9 * np.abs(ref[:n_tight, 1]))
+    assert np.all(np.abs(got[:n_tight, 3] - ref[:n_tight, 3]) <= 1e-9)
     assert np.all(np.abs(got[:, 1] - ref[:, 1]) <= 1e-5 * np.abs(ref[:, 1]))
     assert np.all(np.abs(got[:, 3] - ref[:, 3]) <= 1e-6)
     assert abs(got[-1, 1] - ref[-1, 1]) <= 5e-3 * ref[-1, 1]
