@@ -80,6 +80,11 @@ class ShardComm:
         # collectives on one communicator run in issue order, so with a single
         # one the WL branch's norm all-reduce would wait for the scatter
         self.side_group = dist.new_group(list(range(self.world))) if self.nccl else None
+        if self.nccl:  # initialise both communicators now, not inside a graph capture
+            t = torch.zeros(1, device="cuda")
+            dist.all_reduce(t)
+            dist.all_reduce(t, group=self.side_group)
+            torch.cuda.synchronize()
 
     def all_reduce(self, t, op=None, side=False):
         if not self.on:
