@@ -148,6 +148,15 @@ int p3d_spectral(const p3d_grid* g, const double* rho, double* coef, double* map
 /* The same from a given scipy-normalised coefficient array (electric_field). */
 int p3d_spectral_from_coef(const p3d_grid* g, const double* coef, double* maps,
                            double* scratch, void* stream);
+/* The loop's field solve straight from the int64 fixed-point map (rho_fx, 2^-40
+ * per unit density): maps [B][4] (phi, Ex, Ey, Ez), the overflow of the map
+ * against rho_t (density.py:612-617, movable volume mv) into ovfl_out[1], fused
+ * into the first pass, and, with rezero, the map zeroed for the next
+ * accumulation.  scratch: >= 6*B doubles; ovfl_scratch: >= 8 + 1024 doubles,
+ * zeroed once (its ticket counter re-arms itself). */
+int p3d_spectral_fx(const p3d_grid* g, int64_t* rho_fx, double* maps, double* scratch,
+                    double rho_t, double mv, double* ovfl_out, double* ovfl_scratch, int rezero,
+                    void* stream);
 
 /* Overlap-weighted map means per charge (density.py:376-386, 489-609):
  * energy = sum q*phibar (one double), force[n][3] = -2 q Ebar (freeze: nullable

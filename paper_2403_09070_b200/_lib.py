@@ -122,6 +122,7 @@ _SIGS = {
     "p3d_overflow_fx": (I32, [P, P, D, D, P, P, P]),
     "p3d_spectral": (I32, [P, P, P, P, P, P]),
     "p3d_spectral_from_coef": (I32, [P, P, P, P, P]),
+    "p3d_spectral_fx": (I32, [P, P, P, P, D, D, P, P, I32, P]),
     "p3d_density_gather": (I32, [P, P, P, P, P, P, P, P]),
     "p3d_precondition": (I32, [I32, P, D, P, P, P, P, P, P]),
     "p3d_gp_init": (I32, [P, P, P]),

@@ -273,6 +273,24 @@ int p3d_spectral(const p3d_grid* g, const double* rho, double* coef, double* map
                             STREAM(stream));
 }
 
+int p3d_spectral_fx(const p3d_grid* g, int64_t* rho_fx, double* maps, double* scratch,
+                    double rho_t, double mv, double* ovfl_out, double* ovfl_scratch, int rezero,
+                    void* stream) {
+  if (bad_grid(g) || !rho_fx || !maps || !scratch || !ovfl_out || !ovfl_scratch) {
+    if (!g_err[0]) set_error("spectral_fx: bad args");
+    return P3D_ERR_ARG;
+  }
+  SpecOvfl ov;
+  ov.zero = rezero ? 1 : 0;
+  ov.rho_t_fx = __builtin_llrint(rho_t * 1099511627776.0);
+  ov.partials = ovfl_scratch + 8;
+  ov.counter = reinterpret_cast<unsigned int*>(ovfl_scratch);
+  ov.out = ovfl_out;
+  ov.scale = mv > 0 ? 9.094947017729282379150390625e-13 * g->bin_vol / mv : 0.0;
+  return launch_spectral_ex(g, nullptr, rho_fx, nullptr, nullptr, maps, scratch, nullptr, &ov,
+                            STREAM(stream));
+}
+
 int p3d_spectral_from_coef(const p3d_grid* g, const double* coef, double* maps, double* scratch,
                            void* stream) {
   if (bad_grid(g) || !coef || !maps || !scratch) { if (!g_err[0]) set_error("spectral: bad args"); return P3D_ERR_ARG; }

@@ -149,7 +149,6 @@ class _Layer:
         self.g, _ = grid.device()
         B = grid.n_bins
         self.rho_fx = torch.zeros(B, dtype=torch.int64, device="cuda")
-        self.rho = torch.empty(B, dtype=torch.float64, device="cuda")
         self.maps = torch.empty((B, 4), dtype=torch.float64, device="cuda")
         self.spec = torch.empty(6 * B, dtype=torch.float64, device="cuda")
         self.force = torch.empty((k, 3), dtype=torch.float64, device="cuda")
@@ -163,18 +162,16 @@ class _Layer:
         g, s = _lib.byref(self.g), _lib.stream_ptr()
         _lib.call("p3d_gp2d_layer_xy", self.n, _lib.ptr(self.idx32), _lib.ptr(pos_soa), int(n_obj),
                   _lib.ptr(self.x), _lib.ptr(self.y), _lib.ptr(halt), s)
-        self.rho_fx.zero_()
+        # rho_fx is zero here: allocated zeroed, re-zeroed by the solve that reads it
         _lib.call("p3d_accumulate_density", g, _lib.byref(self.dc.struct), _lib.ptr(self.rho_fx), s)
-        _lib.call("p3d_fx_to_density", int(self.rho.numel()), _lib.ptr(self.rho_fx),
-                  _lib.ptr(self.rho), s)
-        _lib.call("p3d_spectral", g, _lib.ptr(self.rho), None, _lib.ptr(self.maps),
-                  _lib.ptr(self.spec), s)
+        # field maps straight from the fixed-point map, the overflow fused in
+        _lib.call("p3d_spectral_fx", g, _lib.ptr(self.rho_fx), _lib.ptr(self.maps),
+                  _lib.ptr(self.spec), float(self.rho_t), float(self.mv), _lib.ptr(ovfl_out),
+                  _lib.ptr(self.oscr), 1, s)
         _lib.call("p3d_density_gather", g, _lib.byref(self.dc.struct), _lib.ptr(self.maps), None,
                   _lib.ptr(self.energy), _lib.ptr(self.force), _lib.ptr(self.gscr), s)
         _lib.call("p3d_gp2d_layer_force", self.n, _lib.ptr(self.idx32), _lib.ptr(self.force),
                   _lib.ptr(dens_grad), _lib.ptr(halt), s)
-        _lib.call("p3d_overflow_fx", g, _lib.ptr(self.rho_fx), float(self.rho_t), float(self.mv),
-                  _lib.ptr(ovfl_out), _lib.ptr(self.oscr), s)
 
 
 class Gp2dLoop:
