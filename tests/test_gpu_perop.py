@@ -162,3 +162,37 @@ def test_gp2d_names_in_gp_module():
     assert gp.run_gp2d_multi is gp2d.run_gp2d_multi
     assert gp.Gp2dProblem is gp2d.Gp2dProblem
     from paper_2403_09070_b200.gp import run_gp2d_multi  # noqa: F401
+
+
+def test_precondition_two_column_gradients():
+    """gp.precondition on [n, 2] gradients (the GP2D step's shape): the
+    reference's gradients / div[..., None] (gp.py:142-147) to the last ulp."""
+    from paper_2403_09070_b200 import gp as G
+
+    rs = np.random.default_rng(12)
+    n = 5000
+    g = rs.standard_normal((n, 2)) * 10.0
+    q = rs.uniform(0, 4, n)
+    deg = rs.integers(0, 30, n).astype(float)
+    mac = rs.random(n) < 0.1
+    lam = 0.37
+    out, div = G.precondition(g, lam, q, deg, mac)
+    want_div = np.maximum(lam * q + np.where(mac, deg, 0.0), 1.0)
+    assert isinstance(out, np.ndarray) and out.shape == (n, 2)
+    assert np.array_equal(div, want_div)
+    assert np.abs(out - g / want_div[:, None]).max() <= 1e-15 * np.abs(g / want_div[:, None]).max()
+
+
+def test_overflow_degenerate_volumes():
+    """density.overflow with no movable volume and macro_overflow without
+    macros both return 0.0, as the reference does (density.py:612-627)."""
+    from paper_2403_09070_b200 import density as dn
+
+    grid = dn.DensityGrid(8, 8, 4, 4, 2)
+    rho = np.full(grid.shape, 3.0)
+    assert dn.overflow(rho, grid, 1.0, 0.0) == 0.0
+    assert dn.overflow(rho, grid, 1.0, -1.0) == 0.0
+    cloud = dn.ChargeCloud(x=np.array([2.0]), y=np.array([2.0]), z=np.array([1.0]),
+                           w=np.array([1.0]), h=np.array([1.0]), dep=np.array([1.0]),
+                           weight=np.array([1.0]), is_macro=np.array([False]))
+    assert dn.macro_overflow(grid, cloud, 1.0) == 0.0
