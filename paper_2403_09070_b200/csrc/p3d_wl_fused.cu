@@ -487,7 +487,7 @@ __device__ __noinline__ void process_net_generic(const FusedNetArgs& a, int t, d
 #define P3D_K1_TRIPLE 1
 #endif
 #ifndef P3D_K1_RTD
-#define P3D_K1_RTD 0
+#define P3D_K1_RTD 1
 #endif
 #ifndef P3D_K1_MINB
 #define P3D_K1_MINB 4
