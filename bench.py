@@ -547,6 +547,7 @@ def main():
         if runner.comm.nccl or not runner.comm.on:  # the iteration (+ collectives) as one graph
             try:  # iteration 0's graph with the initial step, then the steady-state one
                 step = runner.stepper()
+                ipg = 8  # ShardedGp3d.stepper: steady iterations per replay
             except Exception as exc:  # pragma: no cover - eager fallback, reported
                 print(f"# sharded graph capture failed ({exc!r}); running eagerly",
                       file=sys.stderr)

@@ -315,17 +315,26 @@ class ShardedGp3d:
         torch.cuda.current_stream().wait_stream(s)
         return g
 
-    def stepper(self):
-        """step(n): n iterations replaying two captured graphs -- iteration 0
-        with its initial-step stages, every later one without them.
-        reset() rewinds to iteration 0 (after init_loop)."""
+    def stepper(self, iters_per_graph=8):
+        """step(n): n iterations replaying captured graphs -- iteration 0 with
+        its initial-step stages, every later one without them, in runs of
+        `iters_per_graph` steady iterations per replay (the remainder one by
+        one).  reset() rewinds to iteration 0 (after init_loop)."""
         g0, gs = self.capture(1), self.capture(1, steady=True)
+        gk = self.capture(iters_per_graph, steady=True) if iters_per_graph > 1 else None
         first = [True]
 
         def step(n=1):
-            for _ in range(n):
-                (g0 if first[0] else gs).replay()
+            if n and first[0]:
+                g0.replay()
                 first[0] = False
+                n -= 1
+            if gk is not None:
+                for _ in range(n // iters_per_graph):
+                    gk.replay()
+                n %= iters_per_graph
+            for _ in range(n):
+                gs.replay()
 
         step.reset = lambda: first.__setitem__(0, True)
         return step
