@@ -140,10 +140,12 @@ __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_gri
   pdl_wait();
   if (halt && *halt) return;
   extern __shared__ int sh_hist[];
+  // the same value in every CTA: valid and it change only in later kernels
+  const bool sort = resort_now(ts);
   if ((int)blockIdx.x < n_macro * kMacroSplit) {  // kMacroSplit CTAs per macro footprint
     scatter_object_block(cl.get(macro_ids[blockIdx.x / kMacroSplit]), g, rho,
                          blockIdx.x % kMacroSplit, kMacroSplit);
-  } else if (resort_now(ts)) {
+  } else if (sort) {
     for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x) sh_hist[t] = 0;
     __syncthreads();
     // the tile of an object's centre only groups the records (any assignment
@@ -170,10 +172,13 @@ __global__ void __launch_bounds__(256) tile_hist_kernel(Cloud cl, int n, p3d_gri
     for (int t = threadIdx.x; t < ts.n_tiles; t += blockDim.x)
       if (sh_hist[t]) atomicAdd(&ts.hist[t], sh_hist[t]);
   }
+  if (!sort) {  // nothing to scan: no ticket (most CTAs exit at once); CTA 0 records it
+    if (blockIdx.x == 0 && threadIdx.x == 0 && ts.decision) *ts.decision = 0;
+    return;
+  }
   if (last_block_all(ts.counter)) {
-    const bool sort = resort_now(ts);
-    if (ts.decision && threadIdx.x == 0) *ts.decision = sort;
-    if (sort) scan_tiles(ts);
+    if (ts.decision && threadIdx.x == 0) *ts.decision = 1;
+    scan_tiles(ts);
   }
 }
 

@@ -268,6 +268,10 @@ struct SpecOvfl {  // overflow + re-zero fused into the first (fixed-point) pass
   unsigned int* counter;
   double* out;
   double scale;    // 2^-40 * bin_vol / movable_volume
+  // nullable (fast path only): the first pass adds its per-CTA excess to this
+  // zeroed int64 total with one atomic each (no last-block reduction on the
+  // pass's tail); the second pass converts it into *out and re-zeroes it
+  unsigned long long* acc = nullptr;
 };
 int launch_spectral_ex(const p3d_grid* g, const double* rho, const int64_t* rho_fx,
                        const double* coef_in, double* coef_out, double* maps, double* scratch,

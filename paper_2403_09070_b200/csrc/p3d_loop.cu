@@ -826,6 +826,8 @@ static int launch_k3(const p3d_gp& gp, cudaStream_t s) {
   ov.partials = gp.partials + (long long)kSlotOvfl * kPartialStride;
   ov.counter = &st->counters[kCntOvfl];
   ov.out = finals + kFinOvfl;
+  // the int64 excess total: the (otherwise unused) last double of the slot
+  ov.acc = reinterpret_cast<unsigned long long*>(ov.partials + kPartialStride - 1);
   ov.scale = gp.movable_volume > 0 ? 9.094947017729282379150390625e-13 * gp.grid.bin_vol / gp.movable_volume : 0.0;
   const int rc = launch_spectral_ex(&gp.grid, nullptr, gp.rho_fx, nullptr, nullptr, gp.maps,
                                     gp.spec_scratch, halt, &ov, s);

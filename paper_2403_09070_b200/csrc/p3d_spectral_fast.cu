@@ -282,28 +282,58 @@ __device__ __forceinline__ int dct_slot(int n) {
 
 // packed DCT-II post-processing of frequency k: (X_a[k], X_b[k])
 template <int L>
-__device__ __forceinline__ double2 dct2_post(const double2* line, int k, const double* ph) {
+__device__ __forceinline__ double2 dct2_post_p(const double2* line, int k, double2 p) {
   using F = Fft<L>;
   const double2 zk = line[F::pad(F::pos_of(k))];
   const double2 zn = line[F::pad(F::pos_of((F::N - k) & (F::N - 1)))];
-  const double cs = __ldg(ph + 2 * k), sn = __ldg(ph + 2 * k + 1);
+  const double cs = p.x, sn = p.y;
   // V_a = (Z_k + conj Z_{N-k}) / 2, V_b = -i (Z_k - conj Z_{N-k}) / 2; X = Re(e^{-i pi k/2N} V)
   const double ar = 0.5 * (zk.x + zn.x), ai = 0.5 * (zk.y - zn.y);
   const double br = 0.5 * (zk.y + zn.y), bi = 0.5 * (zn.x - zk.x);
   return make_double2(cs * ar + sn * ai, cs * br + sn * bi);
 }
+__device__ __forceinline__ double2 ld_phase(const double* ph, int k) {
+  return make_double2(__ldg(ph + 2 * k), __ldg(ph + 2 * k + 1));
+}
+template <int L>
+__device__ __forceinline__ double2 dct2_post(const double2* line, int k, const double* ph) {
+  return dct2_post_p<L>(line, k, ld_phase(ph, k));
+}
 
 // inverse (cosine / sine series) pre-processing of element n of one real
 // line with coefficients c_k = get(k): V_n = e^{i pi n/2N} (t_n c'_n - i t_{N-n} c'_{N-n})
-__device__ __forceinline__ double2 inv_pre(int op, int n, int N, double cn_self, double cn_mirror,
-                                           const double* ph) {
+__device__ __forceinline__ double2 inv_pre_p(int op, int n, double cn_self, double cn_mirror,
+                                             double2 p) {
   // COS: c'_n = c_n; SIN: c'_n = c_{N-n} (c'_0 = 0), output sign (-1)^m in post
   double ck, cm;
   if (op == T_COS) { ck = cn_self; cm = n ? cn_mirror : 0.0; }
   else { ck = n ? cn_mirror : 0.0; cm = n ? cn_self : 0.0; }
   const double A = (n ? 0.5 : 1.0) * ck, B = 0.5 * cm;
-  const double cs = __ldg(ph + 2 * n), sn = __ldg(ph + 2 * n + 1);
+  const double cs = p.x, sn = p.y;
   return make_double2(cs * A + sn * B, sn * A - cs * B);
+}
+__device__ __forceinline__ double2 inv_pre(int op, int n, int N, double cn_self, double cn_mirror,
+                                           const double* ph) {
+  return inv_pre_p(op, n, cn_self, cn_mirror, ld_phase(ph, n));
+}
+// a constant table (phases, omega) staged into shared memory; called BEFORE
+// the wait on the predecessor grid, so its load latency hides under that
+// grid's tail
+__device__ __forceinline__ void stage_table(double* dst, const double* src, int n) {
+  constexpr int U = 4;  // loads in flight per thread
+  for (int t0 = threadIdx.x; t0 < n; t0 += U * blockDim.x) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u * blockDim.x;
+      v[u] = t < n ? __ldg(src + t) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u * blockDim.x;
+      if (t < n) dst[t] = v[u];
+    }
+  }
 }
 
 template <int L>
@@ -387,6 +417,7 @@ struct FastArgs {
   unsigned int* counter;
   double* ovfl_out;
   double ovfl_scale;
+  unsigned long long* ovfl_acc;  // nullable: SpecOvfl::acc
   const int* halt;
 };
 
@@ -400,8 +431,13 @@ __device__ __forceinline__ void ovfl_epilogue(const FastArgs& a, long long exces
   if (threadIdx.x == 0) {
     long long b = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += ws[w];
+    if (a.ovfl_acc) {  // exact integer total, any order; B converts it
+      atomicAdd(a.ovfl_acc, (unsigned long long)b);
+      return;
+    }
     reinterpret_cast<long long*>(a.partials)[blockIdx.x] = b;
   }
+  if (a.ovfl_acc) return;
   if (last_block(a.counter)) {
     const long long sum = block_sum_ll_partials(
         reinterpret_cast<const volatile long long*>(a.partials), gridDim.x);
@@ -417,16 +453,29 @@ template <int LY, bool NZ2>
 __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
   TwRegs<LY> tr;
   tr.load(a.twy);  // constant tables: before the wait on the predecessor
-  pdl_wait();
   using F = Fft<LY>;
-  if (a.halt && *a.halt) return;
-  extern __shared__ __align__(16) unsigned char smraw[];
   const int ny = F::N, nz = a.nz, S = ny * nz, nfs = (nz + 1) >> 1;
   const int x0 = blockIdx.x * a.sa, nsl = min(a.sa, a.nx - x0);
+  const int nf = nsl * nfs;
+  // the post-processing phases of this thread's first KP outputs (constant
+  // table): loaded before the wait as well
+  constexpr int KP = 8;
+  double2 php[KP];
+  if (NZ2) {
+#pragma unroll
+    for (int i = 0; i < KP; ++i) {
+      const int t = threadIdx.x + i * blockDim.x;
+      php[i] = t < (nf << LY) ? ld_phase(a.phy, t & (ny - 1)) : make_double2(0.0, 0.0);
+    }
+  }
+  pdl_wait();
+  // nz == 2: the halt flag loads together with the first batch of rho
+  const int halted = a.halt ? *a.halt : 0;
+  if (!NZ2 && halted) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
   const double2* tw = pass_twiddles(a.twy, ny);
   double2* buf = reinterpret_cast<double2*>(smraw);  // [sa * nfs][LS]
   const long long base = (long long)x0 * S;
-  const int nf = nsl * nfs;
   long long excess = 0;
   if (NZ2) {
     constexpr int U = 8;  // all loads of a batch issued before its re-zero stores
@@ -448,6 +497,7 @@ __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
           v[u] = reinterpret_cast<const double2*>(a.rho_d + base)[t];
         }
       }
+      if (halted) return;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int t = t0 + u * blockDim.x;
@@ -458,9 +508,17 @@ __global__ void __launch_bounds__(kThreads) spec_fwd_yz(FastArgs a) {
             make_double2(v[u].x + v[u].y, (v[u].x - v[u].y) * r2);  // DCT-II along z (nz = 2)
       }
     }
+    if (halted) return;  // (threads without a batch)
     __syncthreads();
     fft_any<LY, false>(buf, nf, tw, tr);
-    for (int t = threadIdx.x; t < nf << LY; t += blockDim.x) {
+#pragma unroll
+    for (int i = 0; i < KP; ++i) {
+      const int t = threadIdx.x + i * blockDim.x;
+      if (t < (nf << LY))
+        reinterpret_cast<double2*>(a.X + base)[t] =
+            dct2_post_p<LY>(buf + (t >> LY) * F::LS, t & (ny - 1), php[i]);
+    }
+    for (int t = threadIdx.x + KP * blockDim.x; t < nf << LY; t += blockDim.x) {
       const int sl = t >> LY, k = t & (ny - 1);
       reinterpret_cast<double2*>(a.X + base)[t] = dct2_post<LY>(buf + sl * F::LS, k, a.phy);
     }
@@ -512,9 +570,7 @@ template <int LX>
 __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
   TwRegs<LX> tr;
   tr.load(a.twx);  // constant tables: before the wait on the predecessor
-  pdl_wait();
   using F = Fft<LX>;
-  if (a.halt && *a.halt) return;
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int CB = kColsB;
   const int nx = F::N, S = a.ny * a.nz, c0 = blockIdx.x * CB;
@@ -522,11 +578,39 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
   double2* buf = reinterpret_cast<double2*>(smraw);            // [2 CB][LS]
   double* Xs = reinterpret_cast<double*>(buf + 2 * CB * F::LS);  // [CB][nx]
   double* om = Xs + CB * nx;                                    // [nx]
-  for (int t = threadIdx.x; t < nx; t += blockDim.x) om[t] = a.omx[t];
+  double2* phs = reinterpret_cast<double2*>(om + nx);           // [nx] x phases
+  double* ocol = reinterpret_cast<double*>(phs + nx);           // [2][CB] omega_y, omega_z
+  // the constant tables go to shared memory before the wait as well
+  stage_table(om, a.omx, nx);
+  stage_table(reinterpret_cast<double*>(phs), a.phx, 2 * nx);
+  if (threadIdx.x < CB) {
+    const int col = c0 + threadIdx.x, ky = a.nz == 2 ? col >> 1 : col / a.nz;
+    ocol[threadIdx.x] = __ldg(a.omy + ky);
+    ocol[CB + threadIdx.x] = __ldg(a.omz + (col - ky * a.nz));
+  }
+  pdl_wait();
+  const int halted = a.halt ? *a.halt : 0;  // loads together with the columns
   const double* src = a.coef_in ? a.coef_in : a.X;
-  for (int t = threadIdx.x; t < CB * nx; t += blockDim.x) {
-    const int ix = t / CB, c = t % CB;
-    Xs[c * nx + ix] = src[(long long)ix * S + c0 + c];
+  constexpr int UB = 8;  // a batch of column loads in flight before its smem stores
+  for (int t0 = threadIdx.x; t0 < CB * nx; t0 += UB * blockDim.x) {
+    double v[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int t = t0 + u * blockDim.x;
+      v[u] = t < CB * nx ? src[(long long)(t / CB) * S + c0 + t % CB] : 0.0;
+    }
+    if (halted) break;
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int t = t0 + u * blockDim.x;
+      if (t < CB * nx) Xs[(t % CB) * nx + t / CB] = v[u];
+    }
+  }
+  if (halted) return;
+  if (a.ovfl_acc && blockIdx.x == 0 && threadIdx.x == 0) {  // A's excess total (A is complete)
+    const unsigned long long tot = *a.ovfl_acc;
+    *a.ovfl_out = (double)(long long)tot * a.ovfl_scale;
+    *a.ovfl_acc = 0ull;
   }
   __syncthreads();
   if (!a.coef_in) {
@@ -539,7 +623,7 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
     fft_any<LX, false>(buf, CB / 2, tw, tr);
     for (int t = threadIdx.x; t < (CB / 2) * nx; t += blockDim.x) {
       const int f = t >> LX, k = t & (nx - 1);
-      const double2 r = dct2_post<LX>(buf + f * F::LS, k, a.phx);
+      const double2 r = dct2_post_p<LX>(buf + f * F::LS, k, phs[k]);
       Xs[(2 * f) * nx + k] = r.x;
       Xs[(2 * f + 1) * nx + k] = r.y;
     }
@@ -559,7 +643,7 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
   for (int t = threadIdx.x; t < CB * nx; t += blockDim.x) {
     const int c = t >> LX, j = t & (nx - 1);
     const int col = c0 + c, ky = a.nz == 2 ? col >> 1 : col / a.nz, kz = col - ky * a.nz;
-    const double ox = om[j], oy = a.omy[ky], oz = a.omz[kz];
+    const double ox = om[j], oy = ocol[c], oz = ocol[CB + c];
     const double lam = ox * ox + oy * oy + oz * oz;
     const double inv = lam > 0.0 ? 1.0 / lam : 0.0;
     const double sc = (j ? 2.0 : 1.0) * inx * ((ky ? 2.0 : 1.0) * iny) * (kz ? wz1 : wz0) * inv;
@@ -572,14 +656,14 @@ __global__ void __launch_bounds__(kThreads) spec_x(FastArgs a) {
     const int nn = (nx - n) & (nx - 1);
     const double an = Xs[c * nx + n], am = Xs[c * nx + nn];
     double2 va, vb;
+    const double2 p = phs[n];
     if (!h) {
-      va = inv_pre(T_COS, n, nx, an, am, a.phx);
-      vb = inv_pre(T_SIN, n, nx, an * om[n], am * om[nn], a.phx);
+      va = inv_pre_p(T_COS, n, an, am, p);
+      vb = inv_pre_p(T_SIN, n, an * om[n], am * om[nn], p);
     } else {
-      const int col = c0 + c, ky = a.nz == 2 ? col >> 1 : col / a.nz, kz = col - ky * a.nz;
-      const double my = a.omy[ky], mz = a.omz[kz];
-      va = inv_pre(T_COS, n, nx, an * my, am * my, a.phx);
-      vb = inv_pre(T_COS, n, nx, an * mz, am * mz, a.phx);
+      const double my = ocol[c], mz = ocol[CB + c];
+      va = inv_pre_p(T_COS, n, an * my, am * my, p);
+      vb = inv_pre_p(T_COS, n, an * mz, am * mz, p);
     }
     buf[f * F::LS + F::pad(n)] = make_double2(va.x - vb.y, va.y + vb.x);
   }
@@ -602,23 +686,43 @@ template <int LY, bool NZ2>
 __global__ void __launch_bounds__(kThreads) spec_inv_yz(FastArgs a) {
   TwRegs<LY> tr;
   tr.load(a.twy);  // constant tables: before the wait on the predecessor
-  pdl_wait();
   using F = Fft<LY>;
-  if (a.halt && *a.halt) return;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int ny = F::N, nz = a.nz, S = ny * nz, SP = S + 1;
   const double2* tw = pass_twiddles(a.twy, ny);
   double2* buf = reinterpret_cast<double2*>(smraw);  // [kFftRoundC][LS] (>= S doubles)
   const long long base = (long long)blockIdx.x * S;
   if (NZ2) {
+    pdl_wait();
+    const int halted = a.halt ? *a.halt : 0;  // loads together with the first batch
     const double* Mb = a.M + base * 4;  // [iy][iz][map]
-    for (int t = threadIdx.x; t < 4 << LY; t += blockDim.x) {
-      const int f = t & 3, n = t >> 2, nn = (ny - n) & (ny - 1);
-      const int op = f == 2 ? T_SIN : T_COS;  // Ey: sine series along y
-      const double2 va = inv_pre(op, n, ny, Mb[n * 8 + f], Mb[nn * 8 + f], a.phy);
-      const double2 vb = inv_pre(op, n, ny, Mb[n * 8 + 4 + f], Mb[nn * 8 + 4 + f], a.phy);
-      buf[f * F::LS + F::pad(n)] = make_double2(va.x - vb.y, va.y + vb.x);
+    constexpr int UC = 4;  // a batch of 4 UC intermediate loads in flight
+    for (int t0 = threadIdx.x; t0 < 4 << LY; t0 += UC * blockDim.x) {
+      double m4[UC][4];
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int t = t0 + u * blockDim.x;
+        const int f = t & 3, n = (t >> 2) & (ny - 1), nn = (ny - n) & (ny - 1);
+        const bool in = t < (4 << LY);
+        m4[u][0] = in ? Mb[n * 8 + f] : 0.0;
+        m4[u][1] = in ? Mb[nn * 8 + f] : 0.0;
+        m4[u][2] = in ? Mb[n * 8 + 4 + f] : 0.0;
+        m4[u][3] = in ? Mb[nn * 8 + 4 + f] : 0.0;
+      }
+      if (halted) break;
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int t = t0 + u * blockDim.x;
+        if (t >= (4 << LY)) continue;
+        const int f = t & 3, n = t >> 2;
+        const int op = f == 2 ? T_SIN : T_COS;  // Ey: sine series along y
+        const double2 p = ld_phase(a.phy, n);
+        const double2 va = inv_pre_p(op, n, m4[u][0], m4[u][1], p);
+        const double2 vb = inv_pre_p(op, n, m4[u][2], m4[u][3], p);
+        buf[f * F::LS + F::pad(n)] = make_double2(va.x - vb.y, va.y + vb.x);
+      }
     }
+    if (halted) return;
     __syncthreads();
     fft_any<LY, true>(buf, 4, tw, tr);
     const double r2 = 0.70710678118654752440;
@@ -635,6 +739,8 @@ __global__ void __launch_bounds__(kThreads) spec_inv_yz(FastArgs a) {
     }
     return;
   }
+  pdl_wait();
+  if (a.halt && *a.halt) return;
   double* slab = reinterpret_cast<double*>(buf + max(kFftRoundC * F::LS, (S + 1) / 2));  // [4][S+1]
   for (int t = threadIdx.x; t < 4 * S; t += blockDim.x)  // contiguous interleaved slab
     slab[(t & 3) * SP + (t >> 2)] = a.M[base * 4 + t];
@@ -698,7 +804,8 @@ size_t smem_a(const p3d_grid* g, int sa) {
 }
 size_t smem_b(const p3d_grid* g) {
   const int L = ilog2_pow2(g->nx);
-  return 2 * kColsB * line_stride(L) * 16 + (size_t)(kColsB + 1) * g->nx * 8;
+  return 2 * kColsB * line_stride(L) * 16 + (size_t)(kColsB + 1) * g->nx * 8 +
+         (size_t)g->nx * 16 + 2 * kColsB * 8;  // + x phases, per-column omegas
 }
 size_t smem_c(const p3d_grid* g) {
   const int L = ilog2_pow2(g->ny);
@@ -798,6 +905,7 @@ int launch_spectral_fast(const p3d_grid* g, const double* rho, const int64_t* rh
     a.counter = ov->counter;
     a.ovfl_out = ov->out;
     a.ovfl_scale = ov->scale;
+    a.ovfl_acc = ov->acc;
   }
   const int ga = (g->nx + a.sa - 1) / a.sa, ta = threads_a(g, a.sa), tc = threads_c(g);
   const bool nz2 = g->nz == 2;
