@@ -31,6 +31,11 @@ from .model import PlacementState, partition_from_z, rotated_dims
 log = logging.getLogger("place3d")
 
 K_MAX_BLOCKS = 2048
+# The persistent grids (K1, K4, K5) are sized for B200's 148 SMs as a constant,
+# not queried: their block counts partition the ordered reductions (WL value,
+# energy, norms), so a fixed count keeps the logged rows bit-identical on any
+# GPU model (another SM count only over- or under-fills the one wave).
+GRID_SMS = 148
 K_PARTIAL_STRIDE = 8 * K_MAX_BLOCKS
 
 
@@ -457,7 +462,7 @@ class Gp3dProblem:
         g.divergence_window = int(cfg.divergence_window)
         # object kernels run one persistent wave of 256-thread CTAs: K5 (85
         # registers, every load hoisted) 3 per SM, K4 (64 registers) 4 per SM
-        n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        n_sm = GRID_SMS
         g.nblk_obj = max(1, min(-(-O // 256), K_MAX_BLOCKS,
                                 int(os.environ.get("P3D_NBLK_OBJ", 3 * n_sm))))
         g.nblk_dens = max(1, min(-(-O // 256), K_MAX_BLOCKS - g.n_macro,

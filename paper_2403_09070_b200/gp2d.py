@@ -34,7 +34,7 @@ import torch
 from . import _dev, _lib
 from . import density as dn
 from . import wirelength as wl
-from .gp import GpConfig, GpInfo, gamma_schedule
+from .gp import GRID_SMS, GpConfig, GpInfo, gamma_schedule
 from .model import partition_from_z, rotate_offsets, rotated_dims
 
 
@@ -193,7 +193,7 @@ class Gp2dLoop:
         self.wl_scr = _dev.scratch(2 * dp["n_pin"] + 8 + 1024)
         self.st = torch.zeros(C.sizeof(_lib.Gp2dState), dtype=torch.uint8, device="cuda")
         self._st_host = torch.empty(C.sizeof(_lib.Gp2dState), dtype=torch.uint8, pin_memory=True)
-        n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        n_sm = GRID_SMS  # fixed: the block count partitions its reductions (gp.GRID_SMS)
         c = self.ctl = _lib.Gp2dCtl()
         c.n_obj, c.max_iters, c.n_hbt = int(n_obj), int(cfg.max_iters), int(prob.n_hbt)
         c.nblk = max(1, min(-(-max(n_obj, 1) // 256), 2 * n_sm, 2048))
