@@ -374,7 +374,8 @@ def run_batch(args, rank, world, local):
             dist.init_process_group(backend)
     W, K, Bn = max(args.warmup, 3), args.steps, args.batch
     max_iters = max(200, W + 2 * K + 2)
-    probs, graphs, starts = [], [], []
+    ipg = int(os.environ.get("P3D_BENCH_IPG", "8"))  # iterations per replay, as run_gp3d
+    probs, graphs, bigs, starts = [], [], [], []
     for b in range(Bn):
         design, grid_n, spec = setup_design(args.config, rank * Bn + b)
         cfg, grid, st, pos0 = make_problem_inputs(design, spec, grid_n, max_iters, G)
@@ -382,6 +383,11 @@ def run_batch(args, rank, world, local):
         prob.init_loop(pos0)
         probs.append(prob)
         graphs.append(prob.capture(1))
+        bigs.append(prob.capture(ipg) if ipg > 1 else None)
+        for g_ in (graphs[-1], bigs[-1]):  # the first launch uploads a graph: not timed
+            if g_ is not None:
+                g_.replay()
+        prob.init_loop(pos0)
         starts.append(pos0)
     streams = [torch.cuda.Stream() for _ in range(Bn)]
     cur = torch.cuda.current_stream()
@@ -389,10 +395,12 @@ def run_batch(args, rank, world, local):
     def step(n):
         for s_ in streams:
             s_.wait_stream(cur)
-        for _ in range(n):
-            for g_, s_ in zip(graphs, streams):
-                with torch.cuda.stream(s_):
-                    g_.replay()
+        reps = [(bigs, n // ipg), (graphs, n % ipg)] if ipg > 1 else [(graphs, n)]
+        for gl, cnt in reps:
+            for _ in range(cnt):
+                for g_, s_ in zip(gl, streams):
+                    with torch.cuda.stream(s_):
+                        g_.replay()
         for s_ in streams:
             cur.wait_stream(s_)
 
@@ -425,12 +433,16 @@ def run_batch(args, rank, world, local):
     f0.record(cur)
     for p_, h in zip(probs, host_pos):
         p_.init_loop(h.to("cuda", non_blocking=True))
-    for k in range(K):
-        step(1)
+    k = 0
+    while k < K:  # the timed replays; each replay's rows read back beside the next one
+        c = min(ipg, K - k)
+        step(c)
         row_stream.wait_stream(cur)
         with torch.cuda.stream(row_stream):
             for b, p_ in enumerate(probs):
-                host_rows[b, k].copy_(p_.t_log[4 * k: 4 * k + 4], non_blocking=True)
+                host_rows[b, k:k + c].copy_(p_.t_log[4 * k: 4 * (k + c)].view(c, 4),
+                                            non_blocking=True)
+        k += c
     for p_, h in zip(probs, host_out):
         h.copy_(p_.t_u[: 3 * p_.n_obj].view(3, p_.n_obj), non_blocking=True)
     cur.wait_stream(row_stream)
@@ -453,7 +465,8 @@ def run_batch(args, rank, world, local):
         "config": {"workload": f"cfg5-style: {Bn} independent placements per GPU of "
                                + WORKLOADS[args.config], "placements": world * Bn,
                    "parallelism": f"{Bn} concurrent graphs per GPU x {world} GPUs",
-                   "mode": "batch", "l2": "no flush: working sets exceed L2"},
+                   "mode": "batch", "iterations_per_graph": ipg,
+                   "l2": "no flush: working sets exceed L2"},
         "e2e": {"value": units / (e2e_ms / 1000.0), "unit": "it/s",
                 "h2d_bytes_per_step": int(sum(h.numel() * 8 for h in host_pos) / K),
                 "d2h_bytes_per_step": int(32 * Bn + sum(h.numel() * 8 for h in host_out) / K)},
