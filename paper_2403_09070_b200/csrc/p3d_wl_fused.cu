@@ -100,7 +100,8 @@ struct Box2 {  // one axis, die 0 (bottom) and die 1 (top)
 // ---- weighted-average segment sums -------------------------------------------
 // exp(x) for x <= 0 (every WA argument is (v - max)/gamma or (min - v)/gamma).
 // Default: the table-free polynomial below (P3D_EXP_POLY, measured faster: the
-// table load was the kernel's top stall).  Alternative (-DP3D_EXP_POLY=0):
+// table load was the kernel's top stall; re-measured late in round 2 with the
+// table in L1 or in shared memory: K1 +7 / +5.5 us, -2.3% / -1.7% it/s).  Alternative (-DP3D_EXP_POLY=0):
 // x = (64 m + k) ln2/64 + r with |r| <= ln2/128: exp(x) = 2^m T[k] (1 + q(r)),
 // T[k] = 2^(k/64) (64-entry table), q a degree-6 Taylor polynomial evaluated
 // with short dependency chains (Estrin) — this kernel is latency-bound at the
@@ -884,21 +885,24 @@ __device__ __forceinline__ void staged_task(const FusedNetArgs& a, const int4 tk
 
 template <bool F32>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_kernel(FusedNetArgs a) {
-  pdl_wait();
-  if (a.halt && *a.halt) return;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ double red[32 * 6];
-  if (a.gamma_ptr) a.gamma = *a.gamma_ptr;
-  a.inv_gamma = 1.0 / a.gamma;
-  double acc[6] = {0, 0, 0, 0, 0, 0};
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  WarpCols<F32>& sm = reinterpret_cast<WarpCols<F32>*>(dyn_smem)[wib];
   const int wstride = gridDim.x * kWarpsPerBlock;
 #if P3D_K1_EARLY  // the next task's descriptor is loaded while this one runs
+  // (the first one before the grid wait: the task list is constant)
   int wn = a.task_rank + (blockIdx.x * kWarpsPerBlock + wib) * a.task_size;
   int4 tkn = make_int4(0, 0, 0, 0);
   int t0n = 0;
-  if (wn < a.n_tasks) { tkn = a.tasks[wn]; t0n = a.task_t0[wn]; }
+  if (wn < a.n_tasks) { tkn = __ldg(a.tasks + wn); t0n = __ldg(a.task_t0 + wn); }
+#endif
+  pdl_wait();
+  if (a.halt && *a.halt) return;
+  if (a.gamma_ptr) a.gamma = *a.gamma_ptr;
+  a.inv_gamma = 1.0 / a.gamma;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  WarpCols<F32>& sm = reinterpret_cast<WarpCols<F32>*>(dyn_smem)[wib];
+#if P3D_K1_EARLY
   for (;;) {
     if (wn >= a.n_tasks) break;
     const int4 tk = tkn;
