@@ -127,6 +127,7 @@ _SIGS = {
     "p3d_precondition": (I32, [I32, P, D, P, P, P, P, P, P]),
     "p3d_gp_init": (I32, [P, P, P]),
     "p3d_gp_iterate": (I32, [P, P]),
+    "p3d_gp_iterate_steady": (I32, [P, P]),
     "p3d_gp_evaluate": (I32, [P, D, D, P]),
     "p3d_gp_project": (I32, [P, P, P, P]),
     "p3d_gp_density_fx": (I32, [P, P, P]),

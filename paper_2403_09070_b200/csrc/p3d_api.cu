@@ -48,7 +48,7 @@ void launch_pin_coords(int n_pin, const int32_t* pin_inst, const double* x, cons
 void launch_normalize(int n, const double* gx, const double* gy, const double* gzb,
                       const double* gzh, double alpha, double* out, double* scratch,
                       cudaStream_t s);
-int gp_iterate(const p3d_gp& gp, cudaStream_t s);
+int gp_iterate(const p3d_gp& gp, cudaStream_t s, bool steady = false);
 int gp_iterate_marked_overlap(const p3d_gp& gp, cudaStream_t s);
 int gp_overlap_times(float* t);
 int gp_evaluate(const p3d_gp& gp, double lam, double gamma, cudaStream_t s);
@@ -584,6 +584,11 @@ int p3d_gp_init(const p3d_gp* gp, const double* pos0, void* stream) {
 int p3d_gp_iterate(const p3d_gp* gp, void* stream) {
   if (bad_gp(gp)) return P3D_ERR_ARG;
   return gp_iterate(*gp, STREAM(stream));
+}
+
+int p3d_gp_iterate_steady(const p3d_gp* gp, void* stream) {
+  if (bad_gp(gp)) return P3D_ERR_ARG;
+  return gp_iterate(*gp, STREAM(stream), /*steady=*/true);
 }
 
 int p3d_gp_iterate_profiled(const p3d_gp* gp, void* stream, float* stage_ms) {

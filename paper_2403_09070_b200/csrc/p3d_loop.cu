@@ -906,9 +906,9 @@ static int eval_kernels_overlap(const p3d_gp& gp, cudaStream_t s) {
   return check_launch("gp evaluation kernels (overlapped)");
 }
 
-int gp_iterate(const p3d_gp& gp, cudaStream_t s) {
+int gp_iterate(const p3d_gp& gp, cudaStream_t s, bool steady) {
   if (const int rc = gp.overlap ? eval_kernels_overlap(gp, s) : eval_kernels(gp, s)) return rc;
-  pdl_launch_tag(32, gmax0_kernel, gp.nblk_obj, 256, 0, s, gp);
+  if (!steady) pdl_launch_tag(32, gmax0_kernel, gp.nblk_obj, 256, 0, s, gp);
   pdl_launch_tag(64, advance_kernel, gp.nblk_obj, 256, 0, s, gp);
   return check_launch("gp_iterate");
 }

@@ -657,21 +657,53 @@ class Gp3dProblem:
         src = self._soa(pos0)
         _lib.call("p3d_gp_init", _lib.byref(self.gp), _lib.ptr(src), _lib.stream_ptr())
 
-    def iterate(self, n=1):
+    def iterate(self, n=1, steady=False):
+        """n iterations; steady: without the iteration-0 initial-step kernel
+        (only after the first iteration since init_loop)."""
+        fn = "p3d_gp_iterate_steady" if steady else "p3d_gp_iterate"
         for _ in range(n):
-            _lib.call("p3d_gp_iterate", _lib.byref(self.gp), _lib.stream_ptr())
+            _lib.call(fn, _lib.byref(self.gp), _lib.stream_ptr())
 
-    def capture(self, iters_per_graph=8):
+    def capture(self, iters_per_graph=8, steady=False):
         """CUDA graph of `iters_per_graph` iterations (replayable; each
-        iteration is a no-op once the device loop is done)."""
+        iteration is a no-op once the device loop is done).  steady: the
+        graph is for iterations after the first one (see iterate)."""
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             with torch.cuda.graph(g, stream=s):
-                self.iterate(iters_per_graph)
+                self.iterate(iters_per_graph, steady=steady)
         torch.cuda.current_stream().wait_stream(s)
         return g
+
+    def stepper(self, iters_per_graph=8, steady=True):
+        """step(n): n iterations replaying captured graphs -- the first one
+        after init_loop as p3d_gp_iterate, every later one steady, in runs of
+        `iters_per_graph` per replay (the remainder one by one).  Each graph
+        is launched once here (its upload) and the loop re-initialised, so
+        call init_loop / step.reset() before stepping."""
+        g0, g1 = self.capture(1), self.capture(1, steady=steady)
+        gk = self.capture(iters_per_graph, steady=steady) if iters_per_graph > 1 else None
+        for g_ in (g0, g1, gk):
+            if g_ is not None:
+                g_.replay()
+        first = [True]
+
+        def step(n=1):
+            if n and first[0]:
+                g0.replay()
+                first[0] = False
+                n -= 1
+            if gk is not None:
+                for _ in range(n // iters_per_graph):
+                    gk.replay()
+                n %= iters_per_graph
+            for _ in range(n):
+                g1.replay()
+
+        step.reset = lambda: first.__setitem__(0, True)
+        return step
 
     def run(self, pos0, use_graph=True, iters_per_graph=8, poll_every=4):
         """Initialise and run the loop to completion (max_iters or an exit).
@@ -692,10 +724,13 @@ class Gp3dProblem:
                     break
             return self.state()
         with nvtx.range("p3d.gp3d.capture"):
-            g = self.capture(iters_per_graph)
-        replays = -(-total // iters_per_graph)
+            g0 = self.capture(1)  # iteration 0, with its initial-step kernel
+            g = self.capture(iters_per_graph, steady=True)
+        if total > 0:
+            g0.replay()
+        replays = -(-(total - 1) // iters_per_graph) if total > 1 else 0
         for r in range(replays):
-            with nvtx.range(f"p3d.gp3d.replay[{r * iters_per_graph}]"):
+            with nvtx.range(f"p3d.gp3d.replay[{1 + r * iters_per_graph}]"):
                 g.replay()
             if (r + 1) % poll_every == 0 and self.state().done:
                 break
