@@ -375,19 +375,16 @@ def run_batch(args, rank, world, local):
     W, K, Bn = max(args.warmup, 3), args.steps, args.batch
     max_iters = max(200, W + 2 * K + 2)
     ipg = int(os.environ.get("P3D_BENCH_IPG", "8"))  # iterations per replay, as run_gp3d
-    probs, graphs, bigs, starts = [], [], [], []
+    probs, steppers, starts = [], [], []
     for b in range(Bn):
         design, grid_n, spec = setup_design(args.config, rank * Bn + b)
         cfg, grid, st, pos0 = make_problem_inputs(design, spec, grid_n, max_iters, G)
         prob = G.Gp3dProblem(design, grid, st.fillers, cfg, st.rot, precision=args.precision)
         prob.init_loop(pos0)
         probs.append(prob)
-        graphs.append(prob.capture(1))
-        bigs.append(prob.capture(ipg) if ipg > 1 else None)
-        for g_ in (graphs[-1], bigs[-1]):  # the first launch uploads a graph: not timed
-            if g_ is not None:
-                g_.replay()
+        steppers.append(prob.stepper(ipg))  # iteration 0, then steady graphs (uploaded)
         prob.init_loop(pos0)
+        steppers[-1].reset()
         starts.append(pos0)
     streams = [torch.cuda.Stream() for _ in range(Bn)]
     cur = torch.cuda.current_stream()
@@ -395,12 +392,13 @@ def run_batch(args, rank, world, local):
     def step(n):
         for s_ in streams:
             s_.wait_stream(cur)
-        reps = [(bigs, n // ipg), (graphs, n % ipg)] if ipg > 1 else [(graphs, n)]
-        for gl, cnt in reps:
-            for _ in range(cnt):
-                for g_, s_ in zip(gl, streams):
-                    with torch.cuda.stream(s_):
-                        g_.replay()
+        k = 0
+        while k < n:  # one replay per placement in turn, each on its own stream
+            c = min(ipg, n - k)
+            for st_, s_ in zip(steppers, streams):
+                with torch.cuda.stream(s_):
+                    st_(c)
+            k += c
         for s_ in streams:
             cur.wait_stream(s_)
 
@@ -431,8 +429,9 @@ def run_batch(args, rank, world, local):
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     f0.record(cur)
-    for p_, h in zip(probs, host_pos):
+    for p_, st_, h in zip(probs, steppers, host_pos):
         p_.init_loop(h.to("cuda", non_blocking=True))
+        st_.reset()
     k = 0
     while k < K:  # the timed replays; each replay's rows read back beside the next one
         c = min(ipg, K - k)
@@ -470,7 +469,7 @@ def run_batch(args, rank, world, local):
         "e2e": {"value": units / (e2e_ms / 1000.0), "unit": "it/s",
                 "h2d_bytes_per_step": int(sum(h.numel() * 8 for h in host_pos) / K),
                 "d2h_bytes_per_step": int(32 * Bn + sum(h.numel() * 8 for h in host_out) / K)},
-        "gpu_launches": int(_lib_kernels(probs[0]) * Bn * K),
+        "gpu_launches": int((_lib_kernels(probs[0]) - 1) * Bn * K),  # steady iterations
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)

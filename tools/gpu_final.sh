@@ -19,4 +19,4 @@ timeout 900 python bench.py --mode batch --batch 4 --config 2 --steps 20 --warmu
 timeout 900 python bench.py --mode sharded --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_${TAG}_sh1.log 2>&1; echo sh1 $?
 timeout 900 python tools/bench_next.py --config 2 --iters 50 > gpurun_out/next_$TAG.jsonl 2>&1; echo next $?
 timeout 900 python tools/bench_next.py --post 3 >> gpurun_out/next_$TAG.jsonl 2>&1; echo post $?
-bash tools/sanitize.sh $TAG > gpurun_out/sanitize_$TAG.txt 2>&1; cat gpurun_out/sanitize_$TAG.txt
+# (compute-sanitizer: closed on this pool late in round 2; profiles/round2_sanitize.txt holds the last run)
