@@ -245,3 +245,46 @@ def test_cfg3_fp32_wa_mode_within_gate():
     assert np.all(rel <= 5e-3)
     assert np.all(np.abs(got[:, 2] - r[:, 2]) <= 5e-3 * r[:, 2])
     assert np.all(np.abs(got[:, 3] - r[:, 3]) <= 5e-3 * r[:, 3])
+
+
+def test_steady_graphs_equal_eager_bit_for_bit():
+    """run_gp3d's graph path (iteration 0 as p3d_gp_iterate, then 8 steady
+    iterations per replay through p3d_gp_iterate_steady, which leaves out the
+    iteration-0 initial-step kernel) and the eager p3d_gp_iterate loop give
+    the same rows and the same final positions bit for bit; a stepper driven
+    in uneven chunks (1 + 8 + 3 + 8 + ...) lands on the same state too."""
+    from paper_2403_09070_b200 import gp as G
+    from paper_2403_09070_b200.synth import SynthSpec, synth_arrays
+
+    gold = json.load(open(os.path.join(GOLD, "small_log.json")))
+    r_e, _, st_e, _ = _run(gold["spec"], gold["grid"], gold["max_iters"], use_graph=False)
+    r_g, _, st_g, _ = _run(gold["spec"], gold["grid"], gold["max_iters"], use_graph=True)
+    assert r_e == r_g
+    for a in ("x", "y", "z"):
+        assert np.array_equal(getattr(st_e, a), getattr(st_g, a))
+
+    design = synth_arrays(SynthSpec(n_insts=3000, n_macros=5, r_ma=0.3, seed=11, nets_per_inst=1.2))
+    n_it = 37
+    cfg = G.GpConfig(seed=2, nz=2, grid_nx=64, grid_ny=64, max_iters=60, stop_overflow=0.0)
+    rng = np.random.default_rng(2)
+    grid = G.choose_grid(design, cfg)
+    st = G.init_state(design, grid, cfg, rng)
+    fill = G.make_fillers(design, grid, rng)
+    n = design.n_insts
+    pos0 = np.zeros((n + fill.count, 3))
+    pos0[:n] = np.c_[st.x, st.y, st.z]
+    pos0[n:] = np.c_[fill.x, fill.y, fill.z]
+    prob = G.Gp3dProblem(design, grid, fill, cfg, st.rot)
+    prob.init_loop(pos0)
+    prob.iterate(n_it)
+    eager_rows, eager_u = prob.log_rows(n_it), prob.t_u.clone()
+    step = prob.stepper(8)
+    prob.init_loop(pos0)
+    step.reset()
+    done = 0
+    for c in (1, 8, 3, 8, 8, 9):
+        step(c)
+        done += c
+    assert done == n_it and prob.state().it == n_it
+    assert prob.log_rows(n_it) == eager_rows
+    assert bool((prob.t_u == eager_u).all())
