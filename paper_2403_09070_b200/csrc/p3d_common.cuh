@@ -207,6 +207,24 @@ __device__ __forceinline__ double ordered_sum(const volatile double* p, int n, d
   return acc[0];  // valid in thread 0
 }
 
+// K ordered sums at once (partials of sum k at p + k * stride): the same
+// per-thread chunks and the same tree as K calls of ordered_sum, so the
+// results are identical, but every partial load is in flight together and
+// the block reduces once (the last-block tails of the loop kernels).
+template <int K>
+__device__ __forceinline__ void ordered_sums(const volatile double* p, int stride, int n,
+                                             double* smem /* >= 32*K */, double (&out)[K]) {
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int b = threadIdx.x * per, e = min(n, b + per);
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = 0.0;
+  for (int i = b; i < e; ++i) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] += p[k * stride + i];
+  }
+  block_sum<K>(out, smem);  // valid in thread 0
+}
+
 // Sum of n int64 partials by the whole block (integer: order-independent);
 // result valid in thread 0.
 __device__ __forceinline__ long long block_sum_ll_partials(const volatile long long* p, int n) {

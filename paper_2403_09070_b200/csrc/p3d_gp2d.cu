@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(256) gp2d_eval_kernel(p3d_gp2d_ctl c) {
   if (!last_block(&st->counters[kC2Eval])) return;
   double tot[6];
   if (need)
-    for (int k = 0; k < 6; ++k) tot[k] = ordered_sum(part + k * gridDim.x, gridDim.x, red);
+    ordered_sums<6>(part, gridDim.x, gridDim.x, red, tot);
   if (threadIdx.x != 0) return;
   if (need) {
     for (int l = 0; l < 3; ++l)  // lambda_init (gp.py:150-153)

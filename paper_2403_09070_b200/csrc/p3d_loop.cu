@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(256, P3D_K4_MINB) dens_kernel(p3d_gp gp) {
     for (int k = 0; k < 6; ++k) part[k * gridDim.x + blockIdx.x] = acc[k];
   if (last_block(&gp.st->counters[kCntDens])) {
     double tot[6];
-    for (int k = 0; k < 6; ++k) tot[k] = ordered_sum(part + k * gridDim.x, gridDim.x, red);
+    ordered_sums<6>(part, gridDim.x, gridDim.x, red, tot);
     if (threadIdx.x == 0) {
       if (gp.shard_size > 0) {  // sharded: the host all-reduces, then shard_control_kernel
         for (int k = 0; k < 6; ++k) gp.shard_tot[8 + k] = tot[k];
@@ -1053,7 +1053,7 @@ __global__ void __launch_bounds__(256) inst_norms_kernel(p3d_gp gp) {
     for (int q = 0; q < 3; ++q) part[q * gridDim.x + blockIdx.x] = acc[q];
   if (last_block(&gp.st->counters[kCntGather])) {
     double n[3];
-    for (int q = 0; q < 3; ++q) n[q] = ordered_sum(part + q * gridDim.x, gridDim.x, red);
+    ordered_sums<3>(part, gridDim.x, gridDim.x, red, n);
     if (threadIdx.x == 0)
       for (int q = 0; q < 3; ++q) gp.shard_tot[20 + q] = n[q];
   }

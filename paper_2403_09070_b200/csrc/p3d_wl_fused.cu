@@ -944,10 +944,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, P3D_K1_MINB) fused_net_ke
   if (threadIdx.x == 0)
     for (int q = 0; q < 6; ++q) a.partials[q * gridDim.x + blockIdx.x] = acc[q];
   if (last_block(a.counter)) {
-    for (int q = 0; q < 6; ++q) {
-      const double v = ordered_sum(a.partials + q * gridDim.x, gridDim.x, red);
-      if (threadIdx.x == 0) a.final6[q] = a.n_generic ? v + a.generic6[q] : v;
-    }
+    double v[6];
+    ordered_sums<6>(a.partials, gridDim.x, gridDim.x, red, v);
+    if (threadIdx.x == 0)
+      for (int q = 0; q < 6; ++q) a.final6[q] = a.n_generic ? v[q] + a.generic6[q] : v[q];
   }
 }
 
@@ -1094,7 +1094,7 @@ __global__ void __launch_bounds__(32 * kGatherWarps) gather_warp_kernel(FusedGat
     for (int q = 0; q < 3; ++q) a.partials[q * gridDim.x + blockIdx.x] = acc[q];
   if (a.final_norms && last_block(a.counter)) {
     double n[3];
-    for (int q = 0; q < 3; ++q) n[q] = ordered_sum(a.partials + q * gridDim.x, gridDim.x, red);
+    ordered_sums<3>(a.partials, gridDim.x, gridDim.x, red, n);
     if (threadIdx.x == 0) {
       a.final_norms[0] = n[0];
       a.final_norms[1] = n[1];
