@@ -342,24 +342,40 @@ __device__ __forceinline__ void step_tail(const p3d_gp& gp) {
 __device__ __forceinline__ void control_after_eval(const p3d_gp& gp, double energy, double l1_dens,
                                    double l1_wl, double nonfinite, double dv2, double dg2) {
   p3d_loop_state* st = gp.st;
+  // one thread on the critical path of every iteration: every state scalar it
+  // reads is loaded up front, so the control below costs one round trip
+  // rather than a chain of dependent ones
   const double* f = fin(gp);
-  const double wl_bi = f[kFinNet + 0] + f[kFinNet + 1];
-  const double cut = f[kFinNet + 2];
-  const double exact = f[kFinNet + 3] + f[kFinNet + 4];
-  const double ncross = f[kFinNet + 5];
-  const double ovfl = gp.movable_volume <= 0 ? 0.0 : f[kFinOvfl];
+  const double f0 = f[kFinNet + 0], f1 = f[kFinNet + 1], f2 = f[kFinNet + 2];
+  const double f3 = f[kFinNet + 3], f4 = f[kFinNet + 4], f5 = f[kFinNet + 5];
+  const double fov = f[kFinOvfl];
+  const double n0 = f[kFinNorm + 0], n1 = f[kFinNorm + 1], n2 = f[kFinNorm + 2];
+  const double n3 = f[kFinNorm + 3];
   const double lam_eval = st->lam_eval;
+  const bool eval_only = st->eval_only != 0, lam_set = st->lam_set != 0;
+  const bool step_set = st->step_set != 0;
+  const int it = st->it, rise0 = st->rise;
+  const double best0 = st->best0, best1 = st->best1, prev_value = st->prev_value;
+  const double last_mu = st->last_mu, dv2_next = st->dv2_next, step0 = st->step, a0 = st->a;
+  const int W = gp.divergence_window;
+  const int first = W > 0 ? it - W + 1 : 0;
+  const double hist_first = (first >= 0 && first < it) ? gp.ovfl_hist[first] : 0.0;
+  const double wl_bi = f0 + f1;
+  const double cut = f2;
+  const double exact = f3 + f4;
+  const double ncross = f5;
+  const double ovfl = gp.movable_volume <= 0 ? 0.0 : fov;
   const double wl_value = wl_bi + gp.alpha * cut;
   double value = wl_bi + gp.alpha * cut + lam_eval * energy;  // gp.py:326
-  st->wl_x = f[kFinNet + 0];
-  st->wl_y = f[kFinNet + 1];
+  st->wl_x = f0;
+  st->wl_y = f1;
   st->cut = cut;
   st->exact = exact;
   st->ncross = ncross;
-  st->norm_x = f[kFinNorm + 0];
-  st->norm_y = f[kFinNorm + 1];
-  st->norm_zb = f[kFinNorm + 2];
-  st->gz_scale = f[kFinNorm + 3];
+  st->norm_x = n0;
+  st->norm_y = n1;
+  st->norm_zb = n2;
+  st->gz_scale = n3;
   st->energy = energy;
   st->ovfl = ovfl;
   st->wl_value = wl_value;
@@ -367,7 +383,7 @@ __device__ __forceinline__ void control_after_eval(const p3d_gp& gp, double ener
   st->l1_dens = l1_dens;
   st->nonfinite = nonfinite != 0.0;
   st->value = value;
-  if (st->eval_only) {
+  if (eval_only) {
     st->done = 1;
     return;
   }
@@ -376,13 +392,13 @@ __device__ __forceinline__ void control_after_eval(const p3d_gp& gp, double ener
     st->done = 1;
     return;
   }
-  if (!st->lam_set) {  // gp.py:394-399, lambda_init gp.py:150-153
-    st->lam = (l1_wl <= 0 || l1_dens <= 0) ? 1e-3 : 1e-3 * l1_wl / l1_dens;
+  if (!lam_set) {  // gp.py:394-399, lambda_init gp.py:150-153
+    const double lam = (l1_wl <= 0 || l1_dens <= 0) ? 1e-3 : 1e-3 * l1_wl / l1_dens;
+    st->lam = lam;
     st->lam_set = 1;
-    value = wl_value + st->lam * energy;
+    value = wl_value + lam * energy;
     st->value = value;
   }
-  const int it = st->it;
   gp.log[4 * it + 0] = it;
   gp.log[4 * it + 1] = exact;
   gp.log[4 * it + 2] = ncross;
@@ -392,7 +408,7 @@ __device__ __forceinline__ void control_after_eval(const p3d_gp& gp, double ener
   st->wirelength = exact;
   st->hbt_count = (int)ncross;
   const double k0 = fmax(ovfl - gp.stop_overflow, 0.0);  // gp.py:406-409
-  if (k0 < st->best0 || (k0 == st->best0 && value < st->best1)) {
+  if (k0 < best0 || (k0 == best0 && value < best1)) {
     st->best0 = k0;
     st->best1 = value;
     st->best_flag = 1;
@@ -402,28 +418,38 @@ __device__ __forceinline__ void control_after_eval(const p3d_gp& gp, double ener
     st->stop_now = 1;
     return;
   }
-  st->rise = value > st->prev_value * st->last_mu ? st->rise + 1 : 0;  // gp.py:414-422
+  const int rise = value > prev_value * last_mu ? rise0 + 1 : 0;  // gp.py:414-422
+  st->rise = rise;
   st->prev_value = value;
   gp.ovfl_hist[it] = ovfl;
-  const int W = gp.divergence_window;
-  if (st->rise >= W) {
-    const int first = W > 0 ? it - W + 1 : 0;
-    if (gp.ovfl_hist[first] - gp.ovfl_hist[it] < 1e-3) {
+  if (rise >= W) {
+    const double hf = first == it ? ovfl : hist_first;
+    if (hf - ovfl < 1e-3) {
       st->diverged = 1;
       st->stop_now = 1;
       return;
     }
   }
-  st->dv2 = st->dv2_next;  // |v - v_prev|^2, accumulated by the last advance
+  st->dv2 = dv2_next;  // |v - v_prev|^2, accumulated by the last advance
   st->dg2 = dg2;
-  dv2 = st->dv2;
-  if (!st->step_set) return;  // iteration 0: gmax0_kernel sets the initial step
+  dv2 = dv2_next;
+  if (!step_set) return;  // iteration 0: gmax0_kernel sets the initial step
+  double step = step0;
   const double den = sqrt(dg2);  // gp.py:210-217
   if (den > 0) {
     const double bb = sqrt(dv2) / den;
-    st->step = fmin(fmax(bb, st->step / 4), st->step * 4);
+    step = fmin(fmax(bb, step0 / 4), step0 * 4);
+    st->step = step;
   }
-  step_tail(gp);
+  // step_tail (gp.py:218-226, 438-441) on the values in registers
+  if (!isfinite(step) || step <= gp.min_step) {
+    st->diverged = 1;
+    st->stop_now = 1;  // the best snapshot of this iteration is still taken
+    return;
+  }
+  const double a_new = (1 + sqrt(4 * (a0 * a0) + 1)) / 2;
+  st->a_new = a_new;
+  st->mom = (a0 - 1) / a_new;
 }
 
 #ifndef P3D_K4_PREFETCH
