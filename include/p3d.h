@@ -498,8 +498,9 @@ int p3d_gp_iterate(const p3d_gp* gp, void* stream);
 /* p3d_gp_iterate without the iteration-0 initial-step kernel (gp.py:198-202),
  * for every iteration after the first: that kernel is a no-op once the first
  * step is set, and leaving it out removes a dependency hop from the step's
- * tail.  Call it only after one p3d_gp_iterate since the last p3d_gp_init
- * (the device state is not checked on the host). */
+ * tail.  Call it only after one p3d_gp_iterate since the last p3d_gp_init:
+ * called at iteration 0 (no initial step yet) the step kernel ends the loop
+ * with st->diverged and st->done set instead of advancing. */
 int p3d_gp_iterate_steady(const p3d_gp* gp, void* stream);
 /* Gp3dProblem.evaluate (gp.py:296-341) at gp->v with the given lambda and
  * gamma, filling wl_grad, dens_grad, rho_fx -> maps and the st result fields

@@ -609,6 +609,13 @@ __global__ void __launch_bounds__(256, P3D_K5_MINB) advance_kernel(p3d_gp gp) {
   const int O = gp.n_obj, I = gp.n_inst;
   const bool best = st->best_flag != 0, stop = st->stop_now != 0;
   const double step = st->step, mom = st->mom, lam = st->lam;
+  if (!stop && !st->step_set) {  // no initial step: p3d_gp_iterate_steady at iteration 0
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->diverged = 1;
+      st->done = 1;
+    }
+    return;
+  }
   double dv2[1] = {0.0};
   const int n_own = own_count(gp);
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_own; k += gridDim.x * blockDim.x) {

@@ -288,3 +288,31 @@ def test_steady_graphs_equal_eager_bit_for_bit():
     assert done == n_it and prob.state().it == n_it
     assert prob.log_rows(n_it) == eager_rows
     assert bool((prob.t_u == eager_u).all())
+
+
+def test_steady_iteration_before_the_first_step_fails_loudly():
+    """p3d_gp_iterate_steady right after init (no initial step yet) ends the
+    loop with diverged + done instead of advancing silently with a zero step."""
+    from paper_2403_09070_b200 import gp as G
+    from paper_2403_09070_b200.synth import SynthSpec, synth_arrays
+
+    design = synth_arrays(SynthSpec(n_insts=600, n_macros=3, r_ma=0.25, seed=5, nets_per_inst=1.2))
+    cfg = G.GpConfig(seed=1, nz=2, grid_nx=32, grid_ny=32, max_iters=12, stop_overflow=0.0)
+    rng = np.random.default_rng(1)
+    grid = G.choose_grid(design, cfg)
+    st = G.init_state(design, grid, cfg, rng)
+    fill = G.make_fillers(design, grid, rng)
+    n = design.n_insts
+    pos0 = np.zeros((n + fill.count, 3))
+    pos0[:n] = np.c_[st.x, st.y, st.z]
+    pos0[n:] = np.c_[fill.x, fill.y, fill.z]
+    prob = G.Gp3dProblem(design, grid, fill, cfg, st.rot)
+    prob.init_loop(pos0)
+    prob.iterate(1, steady=True)
+    s = prob.state()
+    assert s.done and s.diverged
+    prob.init_loop(pos0)  # the proper order runs
+    prob.iterate(1)
+    prob.iterate(3, steady=True)
+    s = prob.state()
+    assert not s.done and not s.diverged and s.it == 4
