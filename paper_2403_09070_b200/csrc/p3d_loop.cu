@@ -834,7 +834,10 @@ static void launch_k1b(const p3d_gp& gp, cudaStream_t s) {
     ga.obj0 = gp.sh_i0;
     ga.n_obj = gp.sh_i1 - gp.sh_i0;
   }
-  static const int gather_cap = std::max(1, std::min(kMaxBlocks, getenv("P3D_NBLK_GATHER") ? atoi(getenv("P3D_NBLK_GATHER")) : kMaxBlocks));
+  // 8 CTAs per SM of a B200 as a constant (the block count partitions the
+  // norms' ordered sums, like gp.GRID_SMS): measured +0.5% over 2,048 CTAs
+  // and +0.2% over 592 (late round 2, three A/B rounds)
+  static const int gather_cap = std::max(1, std::min(kMaxBlocks, getenv("P3D_NBLK_GATHER") ? atoi(getenv("P3D_NBLK_GATHER")) : 8 * 148));
   ga.blocks = grid_blocks(ga.n_obj, 256, gather_cap);
   ga.obj_slot_ptr = gp.topo.obj_slot_ptr;
   ga.in_f = reinterpret_cast<const float4*>(gp.pin_out_f);
